@@ -1,0 +1,444 @@
+"""fp64 CPU oracle for UPipe's headwise-chunked Ulysses attention layer.
+
+TEST INFRASTRUCTURE ONLY. Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py`` (its ``cpu_baseline`` leg and ``--impl reference`` arm) may import
+this package. The product path (``paper_2602_21196_b200``) never imports it and
+shares no code with it; the only shared module is ``synth`` (input generation,
+no arithmetic of the method).
+
+Citations: ``P:n`` = /root/reference/PAPER.md line n, ``S:n`` = SPEC.md line n.
+Readings of silent/ambiguous points are DESIGN.md §"Readings" (A1..A25, same
+numbering as SURVEY.md §8c).
+
+Everything is float64 numpy. Library primitives used as single steps: matmul
+(``@``), ``exp``, ``log``, ``max``, ``sum``. Rows of the attention are
+independent by definition, so they are processed in blocks of rows only to bound
+memory; each row is computed with the plain (non-online) softmax definition.
+
+Functions and their pins (tests/test_oracle_*.py):
+
+* ``attn_fwd``      -- pinned: SPEC worked examples, torch fp64 SDPA,
+                       closed forms (constant V, zero K), rows sum to 1, GQA==MHA
+                       with repeated K/V, causal perturbation.
+* ``attn_bwd``      -- pinned: central finite differences, torch fp64 autograd,
+                       dO=0, S=1 closed form.
+* ``layer_fwd/bwd`` -- pinned: finite differences on all of dX, dW*, torch fp64
+                       autograd of the composed layer, stage decomposition.
+* ``gqa_schedule``, ``comm_volume`` -- pinned: Fig. 4 / §4.1 example,
+                       §4.1 volume formulas with the paper's numbers,
+                       SPEC S:279-281.
+* ``a2a_seq_to_head``/``a2a_head_to_seq`` -- pinned: §3.1 example,
+                       round trip identity, C=1 identity.
+* ``upipe_forward/backward`` (sharded simulation) -- pinned: equal to the
+                       un-sharded oracle for every (C, U) (method exactness).
+* ``memory_*``      -- pinned: §3.4 numbers (96 -> 12 S d_head, 87.5 %).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# ----------------------------------------------------------------------------
+# Attention core  (Table 1 stage 2; DESIGN A1-A3, A17)
+# ----------------------------------------------------------------------------
+
+_ROW_BLOCK = 512
+
+
+def _kv_map(Hq: int, Hkv: int, kv_of_head=None):
+    """GQA map: query head h reads kv head floor(h / R), R = Hq/Hkv (DESIGN A3)."""
+    if kv_of_head is not None:
+        return list(kv_of_head)
+    if Hq % Hkv:
+        raise ValueError("Hq % Hkv != 0 (S:37)")
+    R = Hq // Hkv
+    return [h // R for h in range(Hq)]
+
+
+def attn_fwd(Q, K, V, causal=True, kv_of_head=None, rows=None):
+    """Causal GQA softmax attention, scale 1/sqrt(d) (DESIGN A1, A2).
+
+    Q: [S, Hq, d], K/V: [Skv, Hkv, d] (float64). Key j is visible to query i iff
+    j <= i (global token index). Returns O [S, Hq, d] and the natural-log
+    log-sum-exp lse [Hq, S] with lse_i = m_i + ln(sum_j exp(s_ij - m_i)).
+
+    ``rows``: optional array of query rows to compute (row-sampled mode); the
+    returned O/lse then have len(rows) rows, in that order, and Q must be the full
+    [S, Hq, d] tensor or only those rows (``Q.shape[0] == len(rows)``).
+    """
+    Sq, Hq, d = Q.shape
+    Skv, Hkv, _ = K.shape
+    kvh = _kv_map(Hq, Hkv, kv_of_head)
+    scale = 1.0 / math.sqrt(d)
+    if rows is None:
+        qrows = np.arange(Sq)
+        Qr = Q
+    else:
+        qrows = np.asarray(rows, dtype=np.int64)
+        Qr = Q if Q.shape[0] == len(qrows) else Q[qrows]
+    n = len(qrows)
+    O = np.zeros((n, Hq, d))
+    lse = np.zeros((Hq, n))
+    keys = np.arange(Skv)
+    for h in range(Hq):
+        g = kvh[h]
+        for b0 in range(0, n, _ROW_BLOCK):
+            b1 = min(n, b0 + _ROW_BLOCK)
+            qi = qrows[b0:b1]
+            s = (Qr[b0:b1, h, :] @ K[:, g, :].T) * scale          # s_ij = <q_i,k_j>/sqrt(d)
+            if causal:
+                s = np.where(keys[None, :] <= qi[:, None], s, -np.inf)
+            m = np.max(s, axis=1, keepdims=True)                    # m_i
+            l = np.sum(np.exp(s - m), axis=1, keepdims=True)        # l_i
+            lse_b = m + np.log(l)                                   # lse_i
+            P = np.exp(s - lse_b)                                   # P_ij
+            O[b0:b1, h, :] = P @ V[:, g, :]                         # O_i = sum_j P_ij V_j
+            lse[h, b0:b1] = lse_b[:, 0]
+    return O, lse
+
+
+def attn_bwd(Q, K, V, dO, causal=True, kv_of_head=None):
+    """Gradients of O = attn_fwd(Q,K,V) for cotangent dO.
+
+    D_i = <dO_i, O_i>; dV_j += sum_i P_ij dO_i; dP_ij = <dO_i, V_j>;
+    dS_ij = P_ij (dP_ij - D_i); dQ_i = (1/sqrt d) sum_j dS_ij K_j;
+    dK_j += (1/sqrt d) sum_i dS_ij Q_i, kv gradients summed over the group's heads.
+    P is recomputed from its definition (no saved state is trusted).
+    """
+    S, Hq, d = Q.shape
+    Skv, Hkv, _ = K.shape
+    kvh = _kv_map(Hq, Hkv, kv_of_head)
+    scale = 1.0 / math.sqrt(d)
+    dQ = np.zeros_like(Q)
+    dK = np.zeros_like(K)
+    dV = np.zeros_like(V)
+    keys = np.arange(Skv)
+    for h in range(Hq):
+        g = kvh[h]
+        for b0 in range(0, S, _ROW_BLOCK):
+            b1 = min(S, b0 + _ROW_BLOCK)
+            qi = np.arange(b0, b1)
+            s = (Q[b0:b1, h, :] @ K[:, g, :].T) * scale
+            if causal:
+                s = np.where(keys[None, :] <= qi[:, None], s, -np.inf)
+            m = np.max(s, axis=1, keepdims=True)
+            P = np.exp(s - m)
+            P /= np.sum(P, axis=1, keepdims=True)
+            Ob = P @ V[:, g, :]
+            dOb = dO[b0:b1, h, :]
+            Dv = np.sum(dOb * Ob, axis=1, keepdims=True)            # D_i
+            dV[:, g, :] += P.T @ dOb
+            dP = dOb @ V[:, g, :].T
+            dS = P * (dP - Dv)
+            dQ[b0:b1, h, :] = (dS @ K[:, g, :]) * scale
+            dK[:, g, :] += (dS.T @ Q[b0:b1, h, :]) * scale
+    return dQ, dK, dV
+
+
+# ----------------------------------------------------------------------------
+# Layer = projections + attention + output projection (§3.1)
+# Weights are nn.Linear [out, in]; head h <-> rows [h d, (h+1) d) (DESIGN A4).
+# ----------------------------------------------------------------------------
+
+
+def layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, causal=True):
+    """Y = O Wo^T with O = attn(X Wq^T, X Wk^T, X Wv^T).  Returns (Y, O [S,Hq*d], lse [Hq,S])."""
+    S = X.shape[0]
+    Q = (X @ Wq.T).reshape(S, Hq, d)
+    K = (X @ Wk.T).reshape(S, Hkv, d)
+    V = (X @ Wv.T).reshape(S, Hkv, d)
+    O, lse = attn_fwd(Q, K, V, causal)
+    O2 = O.reshape(S, Hq * d)
+    return O2 @ Wo.T, O2, lse
+
+
+def layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, causal=True):
+    """(dX, dWq, dWk, dWv, dWo) of the layer for cotangent dY."""
+    S = X.shape[0]
+    Q = (X @ Wq.T).reshape(S, Hq, d)
+    K = (X @ Wk.T).reshape(S, Hkv, d)
+    V = (X @ Wv.T).reshape(S, Hkv, d)
+    O, _ = attn_fwd(Q, K, V, causal)
+    O2 = O.reshape(S, Hq * d)
+    dWo = dY.T @ O2
+    dO = (dY @ Wo).reshape(S, Hq, d)
+    dQ, dK, dV = attn_bwd(Q, K, V, dO, causal)
+    dQ2, dK2, dV2 = dQ.reshape(S, -1), dK.reshape(S, -1), dV.reshape(S, -1)
+    dWq = dQ2.T @ X
+    dWk = dK2.T @ X
+    dWv = dV2.T @ X
+    dX = dQ2 @ Wq + dK2 @ Wk + dV2 @ Wv
+    return dX, dWq, dWk, dWv, dWo
+
+
+# ----------------------------------------------------------------------------
+# GQA schedule  (§4.1, Fig. 4 caption P:306; DESIGN A8)
+# ----------------------------------------------------------------------------
+
+
+@dataclass
+class Stage:
+    q_heads: list                       # per device p: list of global q heads (qpd of them)
+    kv_heads: list                      # per device p: kv heads resident for this stage
+    kv_sent: list                       # per device p: kv heads newly sent in this stage
+    heads: list = field(default_factory=list)   # all U q heads of the stage, device-major
+
+
+def gqa_schedule(Hq, Hkv, C, U):
+    """Head -> (stage, device) assignment and KV transfers (§4.1, Fig. 4).
+
+    Written as the paper describes it: stages are grouped into super-stages. The
+    first stage of a super-stage "communicate[s] as many unique key/value heads as
+    possible along with the corresponding queries"; the following stages "only
+    communicate the next queries of the corresponding groups, reusing the key/value
+    tensors". With R = Hq/Hkv (the paper's G, DESIGN A3):
+
+    * super-stage b gives device p the KV heads (b C + p) kv_res + i, i < kv_res
+      (round robin over devices), kv_res = max(1, qpd/R);
+    * stage r of the super-stage gives device p the next qpd = U/C queries of
+      those groups: g R + r qpd + j (qpd <= R), or all R queries of its kv_res
+      groups (qpd >= R, one stage per super-stage).
+
+    Reproduces Fig. 3b (MHA: stage 0 = H0, H1), Fig. 4 (16/4/4: stage 0
+    Q0,Q4,Q8,Q12 with K0..K3) and Ulysses at U = Hq.
+    Reading for U > C and Hkv > C: DESIGN A8. Hkv % C != 0 or qpd, R not dividing
+    one another: unsupported (DESIGN A9).
+    """
+    if U % C:
+        raise ValueError("U must be divisible by C (P:317)")
+    if Hq % U:
+        raise ValueError("Hq % U != 0")
+    if Hq % Hkv:
+        raise ValueError("Hq % Hkv != 0")
+    if Hkv % C:
+        raise ValueError("Hkv % C != 0: unsupported GQA shape (DESIGN A9)")
+    R = Hq // Hkv
+    qpd = U // C
+    if R % qpd and qpd % R:
+        raise ValueError("qpd and R must divide one another (DESIGN A9)")
+    kv_res = max(1, qpd // R)
+    sigma = max(1, R // qpd)
+    stages = []
+    for b in range(Hkv // (C * kv_res)):
+        kv_of_dev = [[(b * C + p) * kv_res + i for i in range(kv_res)] for p in range(C)]
+        for r in range(sigma):
+            q_of_dev = []
+            for p in range(C):
+                if qpd <= R:
+                    q_of_dev.append([g * R + r * qpd + j for g in kv_of_dev[p] for j in range(qpd)])
+                else:
+                    q_of_dev.append([g * R + j for g in kv_of_dev[p] for j in range(R)])
+            stages.append(Stage(q_heads=q_of_dev, kv_heads=[list(k) for k in kv_of_dev],
+                                kv_sent=[list(k) for k in kv_of_dev] if r == 0 else [[] for _ in range(C)],
+                                heads=[h for q in q_of_dev for h in q]))
+    return stages
+
+
+def naive_schedule(Hq, Hkv, C, U):
+    """Naive processing: stage s takes heads [sU, (s+1)U), device p the
+    p-th block of U/C, and K/V for every q head are re-sent each stage."""
+    R = Hq // Hkv
+    qpd = U // C
+    stages = []
+    for s in range(Hq // U):
+        qh = [list(range(s * U + p * qpd, s * U + (p + 1) * qpd)) for p in range(C)]
+        kv = [[h // R for h in q] for q in qh]       # one K/V per q head, duplicates sent
+        stages.append(Stage(q_heads=qh, kv_heads=kv, kv_sent=kv,
+                            heads=[h for q in qh for h in q]))
+    return stages
+
+
+def comm_volume(stages, C):
+    """Head-slices (one head x S/C tokens) each device sends in the forward inp_all_to_all:
+    for every stage and every other device q: its q heads, plus K and V for kv_sent."""
+    vol = 0
+    for st in stages:
+        for q in range(1, C):
+            vol += len(st.q_heads[q]) + 2 * len(st.kv_sent[q])
+    return vol
+
+
+def comm_volume_formula(Hq, Hkv, C, scheduled):
+    """P:373 naive 3 (H/C)(C-1); P:380 scheduled (3+G-1) H/(C G) (C-1), G = R = Hq/Hkv."""
+    G = Hq // Hkv
+    if not scheduled:
+        return 3 * (Hq // C) * (C - 1)
+    return (3 + G - 1) * Hq * (C - 1) // (C * G)
+
+
+# ----------------------------------------------------------------------------
+# All-to-all resharding (§3.1) on explicit per-device arrays
+# ----------------------------------------------------------------------------
+
+
+def a2a_seq_to_head(shards, heads_of_device):
+    """inp_all_to_all: device r holds [S/C, Hx, d] for the stage's heads (device-major:
+    the heads of device p are columns heads_of_device offsets). Returns per device p
+    [S, n_p, d] covering all tokens (rank r's block at rows r S/C ...) for its heads.
+
+    ``shards[r]``: dict head -> [S/C, d] array.  ``heads_of_device[p]``: list of heads.
+    """
+    C = len(shards)
+    out = []
+    for p in range(C):
+        cols = [np.concatenate([shards[r][h] for r in range(C)], axis=0) for h in heads_of_device[p]]
+        out.append(np.stack(cols, axis=1))
+    return out
+
+
+def a2a_head_to_seq(full, heads_of_device, C):
+    """out_all_to_all: device p holds [S, n_p, d] for its heads; returns per device r a
+    dict head -> [S/C, d] (rank r's token block)."""
+    S = full[0].shape[0]
+    Sl = S // C
+    res = [dict() for _ in range(C)]
+    for p in range(C):
+        for j, h in enumerate(heads_of_device[p]):
+            for r in range(C):
+                res[r][h] = full[p][r * Sl:(r + 1) * Sl, j, :]
+    return res
+
+
+# ----------------------------------------------------------------------------
+# Sharded UPipe simulation (§3.3, §4.1) in fp64
+# ----------------------------------------------------------------------------
+
+
+def upipe_forward(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, C, U, causal=True, schedule=None):
+    """Stage loop of §3.3 on C simulated devices. Returns (Y [S,D], O [S,Hq d], lse [Hq,S]).
+
+    Per stage: every device projects its sequence shard for the stage's U heads
+    (P:316), inp_all_to_all Q then K then V, attention on its U/C
+    heads over the full sequence, out_all_to_all, the output is
+    written into a pre-allocated buffer and the output projection is
+    accumulated (BASELINE north_star).
+    """
+    S, D = X.shape
+    if S % C:
+        raise ValueError("S % C != 0")
+    Sl = S // C
+    stages = schedule or gqa_schedule(Hq, Hkv, C, U)
+    Xs = [X[r * Sl:(r + 1) * Sl] for r in range(C)]
+    O_buf = [np.zeros((Sl, Hq * d)) for _ in range(C)]     # pre-allocated output
+    Y_acc = [np.zeros((Sl, D)) for _ in range(C)]
+    lse_all = np.zeros((Hq, S))
+    kv_res = [None] * C                                      # resident K/V per device
+    for st in stages:
+        qsh = [{h: Xs[r] @ Wq[h * d:(h + 1) * d].T for h in st.heads} for r in range(C)]
+        Qh = a2a_seq_to_head(qsh, st.q_heads)
+        if any(st.kv_sent[p] for p in range(C)):
+            kv_heads = [st.kv_heads[p] for p in range(C)]
+            all_kv = sorted({g for p in range(C) for g in kv_heads[p]})
+            ksh = [{g: Xs[r] @ Wk[g * d:(g + 1) * d].T for g in all_kv} for r in range(C)]
+            vsh = [{g: Xs[r] @ Wv[g * d:(g + 1) * d].T for g in all_kv} for r in range(C)]
+            Kh = a2a_seq_to_head(ksh, kv_heads)
+            Vh = a2a_seq_to_head(vsh, kv_heads)
+            kv_res = [(kv_heads[p], Kh[p], Vh[p]) for p in range(C)]
+        Oh = []
+        for p in range(C):
+            kvlist, Kp, Vp = kv_res[p]
+            kmap = [kvlist.index(h // (Hq // Hkv)) for h in st.q_heads[p]]
+            Op, lp = attn_fwd(Qh[p], Kp, Vp, causal, kv_of_head=kmap)
+            Oh.append(Op)
+            for j, h in enumerate(st.q_heads[p]):
+                lse_all[h] = lp[j]
+        Os = a2a_head_to_seq(Oh, st.q_heads, C)
+        for r in range(C):
+            for h in st.heads:
+                O_buf[r][:, h * d:(h + 1) * d] = Os[r][h]
+                Y_acc[r] += Os[r][h] @ Wo[:, h * d:(h + 1) * d].T
+    return np.concatenate(Y_acc, 0), np.concatenate(O_buf, 0), lse_all
+
+
+def upipe_backward(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, C, U, causal=True, schedule=None):
+    """Backward stage loop (Table 4 order: out_all_to_all of dO, attention
+    backward, inp_all_to_all of dQ/dK/dV), recomputing the stage's projections
+    (full AC). KV gradients are accumulated over the stages that share the
+    resident K/V and sent back when the K/V buffer is retired. dW is summed over
+    devices at the end (the FSDP reduction). Returns (dX, dWq, dWk, dWv, dWo).
+    """
+    S, D = X.shape
+    Sl = S // C
+    R = Hq // Hkv
+    stages = schedule or gqa_schedule(Hq, Hkv, C, U)
+    _, O_full, _ = upipe_forward(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, C, U, causal, stages)
+    Xs = [X[r * Sl:(r + 1) * Sl] for r in range(C)]
+    dYs = [dY[r * Sl:(r + 1) * Sl] for r in range(C)]
+    Os = [O_full[r * Sl:(r + 1) * Sl] for r in range(C)]
+    dX = [np.zeros((Sl, D)) for _ in range(C)]
+    dW = [dict(q=np.zeros_like(Wq), k=np.zeros_like(Wk), v=np.zeros_like(Wv),
+               o=np.zeros_like(Wo)) for _ in range(C)]
+    kv_state = [None] * C
+
+    def retire(p_state_list):
+        # send accumulated dK/dV of every device back to sequence layout
+        heads_of = [st_[0] for st_ in p_state_list]
+        dKs = a2a_head_to_seq([st_[3] for st_ in p_state_list], heads_of, C)
+        dVs = a2a_head_to_seq([st_[4] for st_ in p_state_list], heads_of, C)
+        for r in range(C):
+            for g in sorted({g for h in heads_of for g in h}):
+                dX[r] += dKs[r][g] @ Wk[g * d:(g + 1) * d] + dVs[r][g] @ Wv[g * d:(g + 1) * d]
+                dW[r]["k"][g * d:(g + 1) * d] += dKs[r][g].T @ Xs[r]
+                dW[r]["v"][g * d:(g + 1) * d] += dVs[r][g].T @ Xs[r]
+
+    for st in stages:
+        if any(st.kv_sent[p] for p in range(C)):
+            if kv_state[0] is not None:
+                retire(kv_state)
+            kv_heads = [st.kv_heads[p] for p in range(C)]
+            all_kv = sorted({g for p in range(C) for g in kv_heads[p]})
+            ksh = [{g: Xs[r] @ Wk[g * d:(g + 1) * d].T for g in all_kv} for r in range(C)]
+            vsh = [{g: Xs[r] @ Wv[g * d:(g + 1) * d].T for g in all_kv} for r in range(C)]
+            Kh = a2a_seq_to_head(ksh, kv_heads)
+            Vh = a2a_seq_to_head(vsh, kv_heads)
+            kv_state = [(kv_heads[p], Kh[p], Vh[p], np.zeros_like(Kh[p]), np.zeros_like(Vh[p]))
+                        for p in range(C)]
+        qsh = [{h: Xs[r] @ Wq[h * d:(h + 1) * d].T for h in st.heads} for r in range(C)]
+        dosh = [{h: dYs[r] @ Wo[:, h * d:(h + 1) * d] for h in st.heads} for r in range(C)]
+        Qh = a2a_seq_to_head(qsh, st.q_heads)
+        dOh = a2a_seq_to_head(dosh, st.q_heads)
+        dQh = []
+        for p in range(C):
+            kvlist, Kp, Vp, dKp, dVp = kv_state[p]
+            kmap = [kvlist.index(h // R) for h in st.q_heads[p]]
+            dq, dk, dv = attn_bwd(Qh[p], Kp, Vp, dOh[p], causal, kv_of_head=kmap)
+            dKp += dk
+            dVp += dv
+            dQh.append(dq)
+        dQs = a2a_head_to_seq(dQh, st.q_heads, C)
+        for r in range(C):
+            for h in st.heads:
+                dX[r] += dQs[r][h] @ Wq[h * d:(h + 1) * d]
+                dW[r]["q"][h * d:(h + 1) * d] += dQs[r][h].T @ Xs[r]
+                dW[r]["o"][:, h * d:(h + 1) * d] += dYs[r].T @ Os[r][:, h * d:(h + 1) * d]
+    retire(kv_state)
+    tot = {k: sum(dW[r][k] for r in range(C)) for k in ("q", "k", "v", "o")}
+    return np.concatenate(dX, 0), tot["q"], tot["k"], tot["v"], tot["o"]
+
+
+# ----------------------------------------------------------------------------
+# Memory accounting (§3.4; DESIGN A21-A22)
+# ----------------------------------------------------------------------------
+
+
+def memory_ulysses_mha(S, C, H, d_head):
+    """6 (S/C) H d_head bytes of QKV + the same for a2a buffers = 12 (S/C) H d_head."""
+    return 12 * (S // C) * H * d_head
+
+
+def memory_upipe_mha(S, C, U, d_head):
+    """H replaced by U: 12 (S/C) U d_head bytes."""
+    return 12 * (S // C) * U * d_head
+
+
+def intermediate_elems_gqa(S, C, Hq, Hkv, d, U):
+    """Per-device forward intermediates (elements, all held): Q/K/V after projection plus
+    their a2a receive buffers (DESIGN A22). UPipe holds U q heads and C*kv_res kv heads
+    per stage (send side) and the same on the receive side."""
+    qpd = U // C
+    R = Hq // Hkv
+    kv_res = 1 if qpd <= R else qpd // R
+    Sl = S // C
+    return 2 * Sl * d * (U + 2 * C * kv_res)

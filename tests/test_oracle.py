@@ -1,0 +1,367 @@
+"""Pins for the fp64 oracle (-m "not gpu"). Each test pins the oracle to something
+other than itself: a worked example from the paper/SPEC (tests/golden), a closed
+form, an invariant, an independent library routine (torch fp64 SDPA/autograd),
+or finite differences."""
+import math
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+import oracle as O
+import synth
+
+RNG = np.random.default_rng(1234)
+
+
+def rand(*shape, scale=1.0):
+    return RNG.standard_normal(shape) * scale
+
+
+# ---------------------------------------------------------------- attention fwd
+
+def test_spec_s2_example(golden):
+    g = golden("spec_attention_examples.json")["s2_example"]
+    Q = np.array(g["Q"])[:, None, :]
+    K = np.array(g["K"])[:, None, :]
+    V = np.array(g["V"])[:, None, :]
+    out, _ = O.attn_fwd(Q, K, V, causal=True)
+    np.testing.assert_allclose(out[:, 0, :], np.array(g["out"]), rtol=0, atol=1e-15)
+
+
+def test_zero_keys_gives_prefix_mean():
+    # K all zeros, causal -> out[i] = mean(V[0..i])
+    S, H, d = 9, 2, 3
+    Q = rand(S, H, d)
+    K = np.zeros((S, H, d))
+    V = rand(S, H, d)
+    out, lse = O.attn_fwd(Q, K, V, causal=True)
+    pref = np.cumsum(V, axis=0) / np.arange(1, S + 1)[:, None, None]
+    np.testing.assert_allclose(out, pref, atol=1e-14)
+    # lse of i+1 equal zero scores = ln(i+1)
+    np.testing.assert_allclose(lse, np.log(np.arange(1, S + 1))[None, :].repeat(H, 0), atol=1e-14)
+
+
+def test_constant_v_yields_v():
+    S, Hq, Hkv, d = 17, 4, 2, 5
+    Q, K = rand(S, Hq, d, scale=2), rand(S, Hkv, d, scale=2)
+    row = rand(1, Hkv, d)
+    V = np.repeat(row, S, axis=0)
+    out, _ = O.attn_fwd(Q, K, V, causal=True)
+    np.testing.assert_allclose(out, np.repeat(V[:, [0, 0, 1, 1], :], 1, 0), atol=1e-13)
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,d,causal", [(8, 4, 2, 4, True), (37, 8, 2, 16, True),
+                                               (64, 4, 4, 8, False), (130, 6, 3, 32, True)])
+def test_fwd_matches_torch_sdpa(S, Hq, Hkv, d, causal):
+    Q, K, V = rand(S, Hq, d), rand(S, Hkv, d), rand(S, Hkv, d)
+    out, lse = O.attn_fwd(Q, K, V, causal=causal)
+    tq = torch.from_numpy(Q).permute(1, 0, 2)[None]
+    tk = torch.from_numpy(K).permute(1, 0, 2)[None]
+    tv = torch.from_numpy(V).permute(1, 0, 2)[None]
+    ref = F.scaled_dot_product_attention(tq, tk, tv, is_causal=causal, enable_gqa=True)
+    np.testing.assert_allclose(out, ref[0].permute(1, 0, 2).numpy(), atol=1e-12)
+    # lse against torch.logsumexp of the masked scores (library routine)
+    R = Hq // Hkv
+    kk = torch.from_numpy(K).repeat_interleave(R, dim=1)
+    s = torch.einsum("ihd,jhd->hij", torch.from_numpy(Q), kk) / math.sqrt(d)
+    if causal:
+        s = s.masked_fill(torch.triu(torch.ones(S, S, dtype=torch.bool), 1), float("-inf"))
+    np.testing.assert_allclose(lse, torch.logsumexp(s, -1).numpy(), atol=1e-12)
+
+
+def test_softmax_rows_sum_to_one_via_lse():
+    S, H, d = 40, 3, 6
+    Q, K, V = rand(S, H, d), rand(S, H, d), rand(S, H, d)
+    _, lse = O.attn_fwd(Q, K, V, causal=True)
+    for h in range(H):
+        s = Q[:, h] @ K[:, h].T / math.sqrt(d)
+        P = np.exp(s - lse[h][:, None]) * np.tril(np.ones((S, S)))
+        np.testing.assert_allclose(P.sum(1), 1.0, atol=1e-12)
+
+
+def test_gqa_equals_mha_with_repeated_kv():
+    S, Hq, Hkv, d = 33, 8, 2, 4
+    Q, K, V = rand(S, Hq, d), rand(S, Hkv, d), rand(S, Hkv, d)
+    a, la = O.attn_fwd(Q, K, V)
+    b, lb = O.attn_fwd(Q, np.repeat(K, 4, axis=1), np.repeat(V, 4, axis=1))
+    np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(la, lb)
+
+
+def test_causal_perturbation_leaves_earlier_rows_bitwise():
+    S, Hq, Hkv, d, t = 50, 4, 2, 8, 31
+    Q, K, V = rand(S, Hq, d), rand(S, Hkv, d), rand(S, Hkv, d)
+    a, la = O.attn_fwd(Q, K, V)
+    K2, V2, Q2 = K.copy(), V.copy(), Q.copy()
+    K2[t:] += 5.0
+    V2[t:] -= 3.0
+    Q2[t:] *= 2.0
+    b, lb = O.attn_fwd(Q2, K2, V2)
+    np.testing.assert_array_equal(a[:t], b[:t])
+    np.testing.assert_array_equal(la[:, :t], lb[:, :t])
+    assert np.abs(a[t:] - b[t:]).max() > 1e-3
+
+
+def test_row_sampled_mode_matches_full():
+    S, Hq, Hkv, d = 300, 4, 2, 8
+    Q, K, V = rand(S, Hq, d), rand(S, Hkv, d), rand(S, Hkv, d)
+    a, la = O.attn_fwd(Q, K, V)
+    rows = np.array([0, 5, 127, 128, 299])
+    b, lb = O.attn_fwd(Q[rows], K, V, rows=rows)
+    np.testing.assert_allclose(b, a[rows], atol=1e-14)
+    np.testing.assert_allclose(lb, la[:, rows], atol=1e-14)
+
+
+def test_head_permutation_equivariance():
+    # permuting query heads (with the gqa map) permutes the outputs identically
+    S, Hq, Hkv, d = 20, 4, 2, 4
+    Q, K, V = rand(S, Hq, d), rand(S, Hkv, d), rand(S, Hkv, d)
+    a, _ = O.attn_fwd(Q, K, V)
+    perm = [2, 0, 3, 1]
+    b, _ = O.attn_fwd(Q[:, perm], K, V, kv_of_head=[p // 2 for p in perm])
+    np.testing.assert_allclose(b, a[:, perm], atol=1e-15)
+
+
+# ---------------------------------------------------------------- attention bwd
+
+def test_spec_s1_backward(golden):
+    g = golden("spec_attention_examples.json")["s1_backward"]
+    arr = {k: np.array(g[k])[:, None, :] for k in ("Q", "K", "V", "dO")}
+    dq, dk, dv = O.attn_bwd(arr["Q"], arr["K"], arr["V"], arr["dO"])
+    np.testing.assert_array_equal(dq[:, 0], np.array(g["dQ"]))
+    np.testing.assert_array_equal(dk[:, 0], np.array(g["dK"]))
+    np.testing.assert_array_equal(dv[:, 0], np.array(g["dV"]))
+
+
+def test_zero_cotangent_zero_grads():
+    S, Hq, Hkv, d = 12, 4, 2, 3
+    dq, dk, dv = O.attn_bwd(rand(S, Hq, d), rand(S, Hkv, d), rand(S, Hkv, d), np.zeros((S, Hq, d)))
+    assert not dq.any() and not dk.any() and not dv.any()
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,d,causal", [(6, 2, 1, 3, True), (8, 4, 2, 4, True), (5, 2, 2, 2, False)])
+def test_bwd_finite_differences(S, Hq, Hkv, d, causal):
+    # central differences, step 1e-5, relative error <= 1e-6
+    Q, K, V, G = rand(S, Hq, d), rand(S, Hkv, d), rand(S, Hkv, d), rand(S, Hq, d)
+    dq, dk, dv = O.attn_bwd(Q, K, V, G, causal)
+
+    def loss(Q_, K_, V_):
+        return float(np.sum(O.attn_fwd(Q_, K_, V_, causal)[0] * G))
+    h = 1e-5
+    for T, dT, idx in ((Q, dq, 0), (K, dk, 1), (V, dv, 2)):
+        num = np.zeros_like(T)
+        for i in np.ndindex(T.shape):
+            args_p = [Q.copy(), K.copy(), V.copy()]
+            args_m = [Q.copy(), K.copy(), V.copy()]
+            args_p[idx][i] += h
+            args_m[idx][i] -= h
+            num[i] = (loss(*args_p) - loss(*args_m)) / (2 * h)
+        assert np.linalg.norm(num - dT) <= 1e-6 * max(1e-30, np.linalg.norm(dT))
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,d", [(50, 4, 2, 8), (129, 8, 2, 16)])
+def test_bwd_matches_torch_autograd(S, Hq, Hkv, d):
+    Q, K, V, G = rand(S, Hq, d), rand(S, Hkv, d), rand(S, Hkv, d), rand(S, Hq, d)
+    dq, dk, dv = O.attn_bwd(Q, K, V, G)
+    tq, tk, tv = (torch.from_numpy(a.transpose(1, 0, 2).copy())[None].requires_grad_() for a in (Q, K, V))
+    out = F.scaled_dot_product_attention(tq, tk, tv, is_causal=True, enable_gqa=True)
+    out.backward(torch.from_numpy(G.transpose(1, 0, 2).copy())[None])
+    for mine, t in ((dq, tq), (dk, tk), (dv, tv)):
+        np.testing.assert_allclose(mine, t.grad[0].permute(1, 0, 2).numpy(), atol=1e-10)
+
+
+# ---------------------------------------------------------------- layer
+
+def _torch_layer(X, Wq, Wk, Wv, Wo, Hq, Hkv, d):
+    S = X.shape[0]
+    q = (X @ Wq.T).view(S, Hq, d).transpose(0, 1)[None]
+    k = (X @ Wk.T).view(S, Hkv, d).transpose(0, 1)[None]
+    v = (X @ Wv.T).view(S, Hkv, d).transpose(0, 1)[None]
+    o = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+    return o[0].transpose(0, 1).reshape(S, Hq * d) @ Wo.T
+
+
+def test_layer_matches_torch_autograd():
+    S, D, Hq, Hkv, d = 70, 24, 4, 2, 6
+    X, Wq, Wk, Wv = rand(S, D), rand(Hq * d, D, scale=.3), rand(Hkv * d, D, scale=.3), rand(Hkv * d, D, scale=.3)
+    Wo, dY = rand(D, Hq * d, scale=.3), rand(S, D)
+    Y, _, _ = O.layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d)
+    grads = O.layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d)
+    ts = [torch.from_numpy(a).requires_grad_() for a in (X, Wq, Wk, Wv, Wo)]
+    ty = _torch_layer(*ts, Hq, Hkv, d)
+    np.testing.assert_allclose(Y, ty.detach().numpy(), atol=1e-11)
+    ty.backward(torch.from_numpy(dY))
+    for mine, t in zip(grads, ts):
+        np.testing.assert_allclose(mine, t.grad.numpy(), atol=1e-10)
+
+
+def test_layer_finite_differences():
+    # closed-form check of every gradient: S=6, Hq=2, Hkv=1, d=3, D=5
+    S, D, Hq, Hkv, d = 6, 5, 2, 1, 3
+    X, Wq, Wk, Wv, Wo, dY = (rand(S, D), rand(Hq * d, D), rand(Hkv * d, D), rand(Hkv * d, D),
+                             rand(D, Hq * d), rand(S, D))
+    grads = O.layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d)
+    args = [X, Wq, Wk, Wv, Wo]
+    h = 1e-5
+
+    def loss(a):
+        return float(np.sum(O.layer_fwd(*a, Hq, Hkv, d)[0] * dY))
+    for idx, g in enumerate(grads):
+        num = np.zeros_like(args[idx])
+        for i in np.ndindex(num.shape):
+            ap = [a.copy() for a in args]
+            am = [a.copy() for a in args]
+            ap[idx][i] += h
+            am[idx][i] -= h
+            num[i] = (loss(ap) - loss(am)) / (2 * h)
+        assert np.linalg.norm(num - g) <= 1e-6 * np.linalg.norm(g)
+
+
+def test_output_projection_stage_decomposition():
+    # sum over stages of O_s Wo_s^T equals O Wo^T (the accumulated output projection)
+    S, D, Hq, d, U = 30, 16, 8, 4, 2
+    Oo, Wo = rand(S, Hq * d), rand(D, Hq * d)
+    acc = np.zeros((S, D))
+    for s in range(Hq // U):
+        cols = slice(s * U * d, (s + 1) * U * d)
+        acc += Oo[:, cols] @ Wo[:, cols].T
+    np.testing.assert_allclose(acc, Oo @ Wo.T, atol=1e-12)
+
+
+# ---------------------------------------------------------------- schedule / volume
+
+def test_fig4_schedule(golden):
+    g = golden("gqa_schedule.json")["fig4_16_4_4"]
+    st = O.gqa_schedule(g["Hq"], g["Hkv"], g["C"], g["U"])
+    assert st[0].heads == g["stage0_q"]
+    assert sorted(k for ks in st[0].kv_sent for k in ks) == g["stage0_kv_sent"]
+    assert st[1].heads == g["stage1_q"]
+    assert [k for ks in st[1].kv_sent for k in ks] == g["stage1_kv_sent"]
+
+
+@pytest.mark.parametrize("name", ["llama3_8b", "qwen3_32b"])
+def test_model_stage_counts(golden, name):
+    g = golden("gqa_schedule.json")[name]
+    st = O.gqa_schedule(g["Hq"], g["Hkv"], g["C"], g["U"])
+    assert len(st) == g["n_stages"]
+    if "kv_sent_stages" in g:
+        assert [i for i, s in enumerate(st) if any(s.kv_sent)] == g["kv_sent_stages"]
+
+
+def test_fig3_layouts(golden):
+    g = golden("fig3_ulysses_layout.json")
+    u = g["ulysses"]
+    st = O.gqa_schedule(u["H"], u["H"], u["C"], u["U"])
+    assert len(st) == 1 and st[0].q_heads == u["heads_of_device"]
+    p = g["upipe"]
+    st = O.gqa_schedule(p["H"], p["H"], p["C"], p["U"])
+    assert len(st) == p["n_stages"]
+    assert [s.heads for s in st] == p["stage_heads"]
+    assert st[0].q_heads[0] == p["device0_stage0"]
+
+
+def test_comm_volume_formulas(golden):
+    for c in golden("gqa_schedule.json")["comm_volume"]["cases"]:
+        Hq, Hkv, C = c["Hq"], c["Hkv"], c["C"]
+        assert O.comm_volume_formula(Hq, Hkv, C, False) == c["naive"]
+        assert O.comm_volume_formula(Hq, Hkv, C, True) == c["scheduled"]
+        assert O.comm_volume(O.gqa_schedule(Hq, Hkv, C, C), C) == c["scheduled"]
+        assert O.comm_volume(O.naive_schedule(Hq, Hkv, C, C), C) == c["naive"]
+
+
+GRID = [(Hq, Hkv, C, U) for Hq, Hkv in ((8, 2), (16, 4), (8, 8), (32, 8), (12, 4))
+        for C in (1, 2, 4) for U in range(C, Hq + 1, C)
+        if Hkv % C == 0 and Hq % U == 0 and ((U // C) % (Hq // Hkv) == 0 or (Hq // Hkv) % (U // C) == 0)]
+
+
+@pytest.mark.parametrize("Hq,Hkv,C,U", GRID)
+def test_schedule_invariants(Hq, Hkv, C, U):
+    st = O.gqa_schedule(Hq, Hkv, C, U)
+    R = Hq // Hkv
+    seen = [h for s in st for h in s.heads]
+    assert sorted(seen) == list(range(Hq))                  # each q head exactly once
+    assert all(len(s.heads) == U for s in st)
+    for s in st:
+        for p in range(C):
+            assert len(s.q_heads[p]) == U // C
+            assert {h // R for h in s.q_heads[p]} <= set(s.kv_heads[p])   # KV resident
+    # every kv head transferred exactly once per device set (no re-sends)
+    sent = [g for s in st for ks in s.kv_sent for g in ks]
+    assert sorted(sent) == list(range(Hkv))
+    if R > 1 and C > 1:
+        assert O.comm_volume(st, C) < O.comm_volume(O.naive_schedule(Hq, Hkv, C, U), C)
+
+
+# ---------------------------------------------------------------- a2a maps
+
+def test_a2a_round_trip_and_identity():
+    C, Sl, d = 4, 3, 2
+    heads = [[0, 1], [2, 3], [4, 5], [6, 7]]
+    shards = [{h: rand(Sl, d) for h in range(8)} for _ in range(C)]
+    full = O.a2a_seq_to_head(shards, heads)
+    assert full[1].shape == (C * Sl, 2, d)
+    np.testing.assert_array_equal(full[1][Sl:2 * Sl, 0], shards[1][2])   # rank 1's block, head 2
+    back = O.a2a_head_to_seq(full, heads, C)
+    for r in range(C):
+        for h in range(8):
+            np.testing.assert_array_equal(back[r][h], shards[r][h])
+    one = O.a2a_seq_to_head([shards[0]], [list(range(8))])
+    for h in range(8):
+        np.testing.assert_array_equal(one[0][:, h], shards[0][h])
+
+
+# ---------------------------------------------------------------- sharded sim
+
+SIM = [(Hq, Hkv, C, U) for (Hq, Hkv, C, U) in GRID if Hq <= 16]
+
+
+@pytest.mark.parametrize("Hq,Hkv,C,U", SIM)
+def test_upipe_sim_equals_unsharded(Hq, Hkv, C, U):
+    S, D, d = 16, 12, 4
+    X, Wq, Wk, Wv = rand(S, D), rand(Hq * d, D, scale=.4), rand(Hkv * d, D, scale=.4), rand(Hkv * d, D, scale=.4)
+    Wo, dY = rand(D, Hq * d, scale=.4), rand(S, D)
+    Y, Ob, lse = O.layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d)
+    Y2, Ob2, lse2 = O.upipe_forward(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, C, U)
+    np.testing.assert_allclose(Y2, Y, atol=1e-12)
+    np.testing.assert_allclose(Ob2, Ob, atol=1e-12)
+    np.testing.assert_allclose(lse2, lse, atol=1e-12)
+    g1 = O.layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d)
+    g2 = O.upipe_backward(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, C, U)
+    for a, b in zip(g2, g1):
+        np.testing.assert_allclose(a, b, atol=1e-11)
+
+
+# ---------------------------------------------------------------- memory
+
+def test_memory_savings_paper_numbers(golden):
+    g = golden("memory_savings.json")["qwen3_32b"]
+    S, dh = 1 << 20, 128
+    u = O.memory_ulysses_mha(S, g["C"], g["H"], dh)
+    p = O.memory_upipe_mha(S, g["C"], g["U"], dh)
+    assert u == g["ulysses_coeff_S_dhead"] * S * dh
+    assert p == g["upipe_coeff_S_dhead"] * S * dh
+    assert 1 - p / u == pytest.approx(g["reduction"])
+
+
+def test_memory_mha_ratio_and_gqa_closed_form():
+    # MHA: UPipe/Ulysses intermediate ratio is exactly U/H
+    S, d = 1 << 20, 128
+    for H, C, U in ((32, 8, 8), (32, 4, 8), (64, 8, 16)):
+        assert O.intermediate_elems_gqa(S, C, H, H, d, U) / O.intermediate_elems_gqa(S, C, H, H, d, H) == U / H
+    # GQA (DESIGN A22): Llama3-8B CP8 U8 -> total 0.5, Q-path 0.25; 32B CP8 U8 -> 0.3
+    assert O.intermediate_elems_gqa(S, 8, 32, 8, d, 8) / O.intermediate_elems_gqa(S, 8, 32, 8, d, 32) == 0.5
+    assert O.intermediate_elems_gqa(S, 8, 64, 8, d, 8) / O.intermediate_elems_gqa(S, 8, 64, 8, d, 64) == pytest.approx(0.3)
+
+
+# ---------------------------------------------------------------- synth generator
+
+def test_synth_values_exact_bf16_and_deterministic():
+    v = synth.draw(0, synth.TID["x"], (1000,), 1)
+    bits = synth.to_bf16_bits(v)                      # raises if not exactly representable
+    np.testing.assert_array_equal(synth.from_bf16_bits(bits), v)
+    w = synth.draw(0, synth.TID["x"], (500,), 1, start=500)
+    np.testing.assert_array_equal(v[500:], w)         # global indexing: shards agree
+    assert abs(v.mean()) < 0.15 and 0.9 < v.std() / (2 / math.sqrt(3)) < 1.1
+    assert set(np.unique(synth.draw_codes(3, 2, 0, 100000))) == set(range(256))
