@@ -1,0 +1,194 @@
+/*
+ * upipe.h -- C ABI of libupipe: UPipe ("Untied Ulysses", arXiv 2602.21196), the
+ * headwise-chunked Ulysses context-parallel attention layer, forward and backward,
+ * for NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = PAPER.md line n (reference text of the paper), S:n = SPEC.md
+ * line n. Readings of points the paper leaves open are numbered A1..A25 in
+ * DESIGN.md ("Readings").
+ *
+ * What one layer call computes (§3.1, §3.3, §4.1):
+ * the input is sequence-sharded (rank r holds tokens [r*S_l, (r+1)*S_l), P:274;
+ * DESIGN A7). Heads are processed in nu = Hq/U stages of U heads. For
+ * each stage the layer projects Q/K/V for only that stage's heads, runs
+ * an all-to-all from sequence- to head-sharded layout (inp_all_to_all, P:317,
+ * Q then K then V), computes causal GQA attention over the full sequence
+ * for its U/C heads, runs the all-to-all back (out_all_to_all),
+ * fills the pre-allocated output and accumulates the output
+ * projection (BASELINE north_star). One chunk-sized buffer set in the caller's
+ * workspace is reused by every stage. K/V heads are sent once
+ * per super-stage and kept resident (GQA scheduling).
+ * chunk_heads == n_q_heads is DeepSpeed-Ulysses on the same kernels.
+ *
+ * The result equals un-sharded multi-head causal GQA attention with projections
+ * (SURVEY §8c c.1): U and C change only the order of the work.
+ *
+ * Conventions
+ *  - bf16 tensors are passed as uint16_t storage (upipe_bf16). fp32 is float.
+ *  - All tensor pointers are DEVICE pointers unless stated otherwise, 16-byte
+ *    aligned, row-major, owned by the caller (PyTorch). The library never frees
+ *    caller memory. Workspace is caller-owned too, so all activation memory is
+ *    visible to the caller's allocator.
+ *  - Weights use nn.Linear layout [out, in] (y = x W^T); q head h owns rows
+ *    [h*d, (h+1)*d) of Wq and columns [h*d, (h+1)*d) of Wo; kv head g rows
+ *    [g*d,(g+1)*d) of Wk/Wv; q head h reads kv head floor(h / (Hq/Hkv)) (A3, A4).
+ *  - Scale 1/sqrt(head_dim) (A1); causal: key j visible to query i iff j <= i in
+ *    the global token index (A2). No bias, RoPE, dropout (A6).
+ *  - Calls are asynchronous: work is enqueued on `stream` (the ctx's transport
+ *    may enqueue on it too) and outputs are valid when `stream` reaches that
+ *    point. Inputs must stay alive and unmodified until then.
+ *  - Errors: validation happens before anything is enqueued, so a failing call
+ *    has no side effects; upipe_last_error(ctx) names the violated constraint.
+ *    No C++ exception crosses the ABI. A ctx is not thread-safe; all ranks of a
+ *    CP group must make the same sequence of calls (collective contract).
+ */
+#ifndef UPIPE_H_
+#define UPIPE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define UPIPE_API __attribute__((visibility("default")))
+#else
+#define UPIPE_API
+#endif
+
+typedef uint16_t upipe_bf16;
+
+typedef enum {
+  UPIPE_OK = 0,
+  UPIPE_ERR_INVALID_ARG = 1, /* a documented precondition is violated (named in upipe_last_error) */
+  UPIPE_ERR_UNSUPPORTED = 2, /* valid for the method but not implemented (e.g. Hkv % C != 0, A9) */
+  UPIPE_ERR_CUDA = 3,        /* a CUDA runtime error (message in upipe_last_error) */
+  UPIPE_ERR_COMM = 4,        /* NCCL / fabric error or timeout */
+  UPIPE_ERR_WORKSPACE = 5,   /* ws_bytes smaller than upipe_workspace_size */
+  UPIPE_ERR_STATE = 6        /* ctx not initialised / already finalised */
+} upipe_status_t;
+
+typedef struct upipe_ctx_s* upipe_ctx_t;
+typedef struct upipe_fabric_s* upipe_fabric_t;
+
+/* Shape of one layer call on one rank. */
+typedef struct {
+  int64_t seq_local;   /* S_l = S / C tokens held by this rank (contiguous block r*S_l..); >= 1 */
+  int32_t hidden;      /* D, model width (independent of Hq*d, A5); multiple of 64 */
+  int32_t n_q_heads;   /* Hq */
+  int32_t n_kv_heads;  /* Hkv; Hq % Hkv == 0; Hkv % C == 0 (A9) */
+  int32_t head_dim;    /* d in {64, 128} */
+  int32_t chunk_heads; /* U: heads per stage; U % C == 0; Hq % U == 0; U/C and Hq/Hkv divide one another (A8) */
+  int32_t causal;      /* 1: causal mask (the paper's setting); 0: full attention */
+} upipe_shape_t;
+
+#define UPIPE_UID_BYTES 128
+
+/* flags for upipe_init / upipe_init_local */
+#define UPIPE_FLAG_NONE 0u
+#define UPIPE_FLAG_SYNC_COMM 1u /* run collectives on the compute stream (no side stream) */
+
+/* ---------------------------------------------------------------- lifecycle */
+
+/* Rank 0 creates the NCCL unique id that all CP ranks pass to upipe_init
+ * (the Python binding broadcasts it over the torch process group). */
+UPIPE_API upipe_status_t upipe_get_unique_id(uint8_t uid[UPIPE_UID_BYTES]);
+
+/* Create a context for CP rank `cp_rank` of `cp_size` processes (one GPU each)
+ * over NCCL (NVLink/NVSwitch). Collective across the group. cp_size == 1 needs no
+ * uid (may be NULL). The ctx owns the communicator, a comm stream and events. */
+UPIPE_API upipe_status_t upipe_init(upipe_ctx_t* ctx, const uint8_t uid[UPIPE_UID_BYTES], int cp_size, int cp_rank,
+                          int cuda_device, uint32_t flags);
+
+/* Single-process CP group: `cp_size` ranks driven by `cp_size` host threads of one
+ * process (each with its own ctx and stream, possibly on the same device). The
+ * all-to-alls are device-to-device copies between the ranks' buffers. Used to run
+ * and test the sharded path (C = 2..8) on one GPU. */
+UPIPE_API upipe_status_t upipe_fabric_create(upipe_fabric_t* fabric, int cp_size);
+UPIPE_API upipe_status_t upipe_fabric_destroy(upipe_fabric_t fabric);
+UPIPE_API upipe_status_t upipe_init_local(upipe_ctx_t* ctx, upipe_fabric_t fabric, int cp_rank, int cuda_device, uint32_t flags);
+
+UPIPE_API upipe_status_t upipe_finalize(upipe_ctx_t ctx);
+UPIPE_API const char* upipe_status_string(upipe_status_t s);
+UPIPE_API const char* upipe_last_error(upipe_ctx_t ctx); /* thread-local message if ctx == NULL */
+
+/* ---------------------------------------------------------------- planning (host only, no GPU) */
+
+/* Bytes of workspace one call needs (pass 0: forward, 1: backward). 256-byte aligned. */
+UPIPE_API upipe_status_t upipe_workspace_size(int cp_size, const upipe_shape_t* shape, int pass, size_t* bytes);
+
+/* Stage plan of the GQA schedule (A8): for stage s and device p the
+ * first local q head (q heads [q0, q0+qpd)), first resident kv head
+ * (kv heads [kv0, kv0+kv_res)) and whether the kv heads are sent in this stage. */
+typedef struct {
+  int32_t n_stages, qpd, kv_res, sigma;
+  int32_t q0, kv0, kv_sent;
+} upipe_stage_info_t;
+UPIPE_API upipe_status_t upipe_plan_stage(int cp_size, const upipe_shape_t* shape, int stage, int device,
+                                upipe_stage_info_t* out);
+/* Explain the first violated precondition of (cp_size, shape) into msg (may be NULL). */
+UPIPE_API upipe_status_t upipe_validate(int cp_size, const upipe_shape_t* shape, char* msg, size_t msg_len);
+
+/* ---------------------------------------------------------------- the layer */
+
+/* Forward.
+ *  x         [S_l, D]      bf16  this rank's sequence shard
+ *  wq        [Hq*d, D]     bf16  wk, wv [Hkv*d, D]; wo [D, Hq*d]  (replicated on every rank)
+ *  y         [S_l, D]      bf16  out
+ *  o_saved   [S_l, Hq*d]   bf16  out: attention output before Wo (saved for backward)
+ *  lse_saved [Hq/C, S]     fp32  out: natural-log LSE of this rank's heads, slot s*qpd + j
+ *                                for local head j of stage s (A12, A17)
+ *  workspace: >= upipe_workspace_size(C, shape, 0) bytes, 256-byte aligned. */
+UPIPE_API upipe_status_t upipe_attn_fwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const upipe_bf16* x, const upipe_bf16* wq,
+                              const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo, upipe_bf16* y,
+                              upipe_bf16* o_saved, float* lse_saved, void* workspace, size_t ws_bytes,
+                              void* stream);
+
+/* Backward, recomputing the stage projections (A12).
+ *  dy                 [S_l, D] bf16 cotangent of y
+ *  o_saved, lse_saved as produced by upipe_attn_fwd
+ *  dx                 [S_l, D] bf16 out
+ *  dwq dwk dwv dwo    fp32 out, weight shapes; if reduce_dw != 0 they are summed over
+ *                     all C ranks (the FSDP reduction of P:437, A14), else this rank's part.
+ *  workspace: >= upipe_workspace_size(C, shape, 1) bytes. */
+UPIPE_API upipe_status_t upipe_attn_bwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const upipe_bf16* x, const upipe_bf16* wq,
+                              const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo,
+                              const upipe_bf16* dy, const upipe_bf16* o_saved, const float* lse_saved,
+                              upipe_bf16* dx, float* dwq, float* dwk, float* dwv, float* dwo, int reduce_dw,
+                              void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- kernel-level entry points
+ * The individual steps of the hot path, exposed for per-kernel parity tests and
+ * roofline measurement. Same kernels the layer calls use. */
+
+/* Attention core (F3): q [S][nq][d] (token stride ldq), k/v [S][nkv][d] (stride ldkv),
+ * o at o + t*ldo + j*d, lse [nq][S] (stride ld_lse). */
+UPIPE_API upipe_status_t upipe_attn_core_fwd(const upipe_bf16* q, const upipe_bf16* k, const upipe_bf16* v, upipe_bf16* o,
+                                   float* lse, int64_t S, int nq, int nkv, int d, int causal, int64_t ldq,
+                                   int64_t ldkv, int64_t ldo, int64_t ld_lse, void* stream);
+/* Attention core backward (B4): dq_acc fp32 [S][nq][d] is ACCUMULATED into (zero it first);
+ * dk_acc/dv_acc fp32 [S][nkv][d] are written (accumulate != 0: added to their contents);
+ * delta [S][nq] (stride ld_delta) = rowsum(dO*O) in fp32. */
+UPIPE_API upipe_status_t upipe_attn_core_bwd(const upipe_bf16* q, const upipe_bf16* k, const upipe_bf16* v,
+                                   const upipe_bf16* dout, const float* lse, const float* delta, float* dq_acc,
+                                   float* dk_acc, float* dv_acc, int64_t S, int nq, int nkv, int d, int causal,
+                                   int64_t ldq, int64_t ldkv, int64_t ldo_grad, int64_t ld_lse, int64_t ld_delta,
+                                   int accumulate, void* stream);
+/* delta[t*ld_delta + j] = sum_e dO[t*ld_do + j*d + e] * O[t*ld_o + j*d + e] */
+UPIPE_API upipe_status_t upipe_rowdot(const upipe_bf16* dO, int64_t ld_do, const upipe_bf16* O, int64_t ld_o, float* delta,
+                            int64_t ld_delta, int64_t rows, int nheads, int d, void* stream);
+/* Plain projection GEMM on the tcgen05 kernel: y[M,N] = x[M,K] w[N,K]^T, bf16 out
+ * (mode 0) or fp32 out (mode 1). */
+UPIPE_API upipe_status_t upipe_gemm_xwT(const upipe_bf16* x, const upipe_bf16* w, void* y, int64_t M, int64_t N, int64_t K,
+                              int mode, void* stream);
+/* Device copy of the seeded synthetic input generator (synth/__init__.py):
+ * dst[i] = (2*m-255)/256 * 2^exponent, m = splitmix64(seed*G1 + tensor_id*G2 + start + i) >> 56. */
+UPIPE_API upipe_status_t upipe_synth_fill_bf16(upipe_bf16* dst, int64_t n, uint64_t seed, int tensor_id, int exponent,
+                                     int64_t start, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UPIPE_H_ */

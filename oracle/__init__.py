@@ -137,6 +137,16 @@ def attn_bwd(Q, K, V, dO, causal=True, kv_of_head=None):
     return dQ, dK, dV
 
 
+def rowdot(dO, O):
+    """D_i = <dO_i, O_i> per (row, head) (the D term of attn_bwd). [S,H,d] -> [S,H]."""
+    return np.sum(dO * O, axis=-1)
+
+
+def project(X, W):
+    """Projection of the input into heads, X W^T with nn.Linear W [out, in] (DESIGN A4)."""
+    return X @ W.T
+
+
 # ----------------------------------------------------------------------------
 # Layer = projections + attention + output projection (P:279-289 §3.1; P:316)
 # Weights are nn.Linear [out, in]; head h <-> rows [h d, (h+1) d) (DESIGN A4).

@@ -1,0 +1,371 @@
+// Causal GQA flash-attention backward for sm_100a (Table 4).
+//
+// KV-stationary: one CTA owns a 128-key tile of one KV head and loops over the
+// query tiles (of every local query head of that KV group) that can see it.
+// Per query tile, five tcgen05 MMAs (M=128, K=128 or d):
+//   S^T  = K Q^T          (TMEM cols [0,128))      P^T  = exp2(S^T*c - lse2)
+//   dP^T = V dO^T         (TMEM cols [128,256))    dS^T = P^T (dP^T - delta)
+//   dV  += P^T dO         (TMEM [256, 256+d))      P^T, dS^T staged in smem (bf16)
+//   dK  += dS^T Q         (TMEM [256+d, 256+2d))
+//   dQ   = dS K           (TMEM cols [128,128+d), reusing dP^T once consumed)
+// dQ is reduced across KV tiles with fp32 atomics into dq_acc (scaled by 1/sqrt(d));
+// dK/dV stay in TMEM for the whole CTA and are written (and optionally
+// accumulated across UPipe stages of one super-stage) at the end.
+// Warps: 0-3 compute (thread = one key row for S^T/dP^T, one query row for dQ),
+// 4 TMA producer, 5 MMA issuer.
+#include <cstdio>
+
+#include "kernels.h"
+#include "sm100.cuh"
+#include "tma_host.h"
+
+namespace upipe {
+namespace {
+
+using namespace dev;
+
+struct BwdArgs {
+  const float* lse;
+  const float* delta;
+  float* dq_acc;
+  float* dk_acc;
+  float* dv_acc;
+  __nv_bfloat16* dk_bf16;
+  __nv_bfloat16* dv_bf16;
+  long long S, ld_lse, ld_delta, ld_kvb;
+  int nq, nkv, causal, kv_accumulate, kv_write_acc;
+  float scale;       // 1/sqrt(d)
+  float scale_log2;  // log2(e)/sqrt(d)
+};
+
+__device__ __forceinline__ float ex2b(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int D>
+struct BwdCfg {
+  static constexpr int TB = 128 * D * 2;   // one 128 x D bf16 tile
+  static constexpr int PB = 128 * 128 * 2; // 128 x 128 bf16
+  static constexpr int OFF_K = 0, OFF_V = TB, OFF_Q = 2 * TB, OFF_DO = 3 * TB;
+  static constexpr int OFF_P = 4 * TB, OFF_DS = OFF_P + PB;
+  static constexpr int OFF_STAT = OFF_DS + PB;             // lse2[2][128], delta[2][128] fp32
+  static constexpr int OFF_BAR = OFF_STAT + 4 * 128 * 4;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 128, TM_DV = 256, TM_DK = 256 + D;
+};
+
+template <int D>
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                    const BwdArgs a) {
+  using C = BwdCfg<D>;
+  constexpr int NCH = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* s_lse2 = reinterpret_cast<float*>(smem + C::OFF_STAT);   // [2][128]
+  float* s_delta = s_lse2 + 256;                                  // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* q_full = bars + 1;
+  uint64_t* q_empty = bars + 2;
+  uint64_t* do_full = bars + 3;
+  uint64_t* do_empty = bars + 4;
+  uint64_t* sdp_full = bars + 5;
+  uint64_t* ds_full = bars + 6;
+  uint64_t* dq_full = bars + 7;
+  uint64_t* dq_empty = bars + 8;
+  uint64_t* dkv_full = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int jb = blockIdx.x;                      // key tile (small jb = most query tiles = longest)
+  const int g = blockIdx.y;                       // kv head
+  const int G = a.nq / a.nkv;
+  const int nT = (int)((a.S + 127) / 128);
+  const int qt_begin = a.causal ? jb : 0;
+  const int n_qt = nT - qt_begin;
+  const int N = G * n_qt;                         // (head, query tile) iterations
+
+  if (warp == 4 && lane == 0) {
+    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO);
+    for (int i = 0; i < 10; ++i) mbar_init(&bars[i], (i == 6 || i == 8) ? 128 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      mbar_arrive_expect_tx(kv_full, 2 * C::TB);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        tma_load_3d(smem + C::OFF_K + c * 16384, &tmK, kv_full, c * 64, g, jb * 128);
+        tma_load_3d(smem + C::OFF_V + c * 16384, &tmV, kv_full, c * 64, g, jb * 128);
+      }
+      for (int n = 0; n < N; ++n) {
+        const int h = g * G + n / n_qt;
+        const int qt = qt_begin + n % n_qt;
+        mbar_wait(q_empty, (n & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full, C::TB);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) tma_load_3d(smem + C::OFF_Q + c * 16384, &tmQ, q_full, c * 64, h, qt * 128);
+        mbar_wait(do_empty, (n & 1) ^ 1);
+        mbar_arrive_expect_tx(do_full, C::TB);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) tma_load_3d(smem + C::OFF_DO + c * 16384, &tmdO, do_full, c * 64, h, qt * 128);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t id_kk = idesc_bf16(128, 128, false, false);  // S^T, dP^T: both K-major over d
+      constexpr uint32_t id_kmn = idesc_bf16(128, D, false, true);    // dV, dK: A K-major (over q), B MN-major
+      constexpr uint32_t id_mnmn = idesc_bf16(128, D, true, true);    // dQ: A = dS^T viewed MN-major, B = K MN-major
+      const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
+      const uint32_t sQ = smem_u32(smem + C::OFF_Q), sdO = smem_u32(smem + C::OFF_DO);
+      const uint32_t sP = smem_u32(smem + C::OFF_P), sdS = smem_u32(smem + C::OFF_DS);
+      auto mma_kk = [&](uint32_t sa, uint32_t sb, uint32_t tm) {      // [128 x D] x [128 x D]^T
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ss(tm, desc_sw128(sa + c * 16384 + kk * 32, 16, 1024), desc_sw128(sb + c * 16384 + kk * 32, 16, 1024),
+                   id_kk, (c | kk) != 0);
+      };
+      auto mma_kmn = [&](uint32_t sa, uint32_t sb, uint32_t tm, bool acc) {  // A [128 x 128 q] K-major, B MN-major
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ss(tm, desc_sw128(sa + kb * 16384 + kk * 32, 16, 1024),
+                   desc_sw128(sb + kb * 8192 + kk * 2048, 16384, 1024), id_kmn, (acc || kb || kk) ? 1u : 0u);
+      };
+      auto mma_mnmn = [&](uint32_t sa, uint32_t sb, uint32_t tm) {  // dQ = dS K: K dim = keys (rows of both)
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ss(tm, desc_sw128(sa + kb * 8192 + kk * 2048, 16384, 1024),
+                   desc_sw128(sb + kb * 8192 + kk * 2048, 16384, 1024), id_mnmn, (kb | kk) != 0);
+      };
+      mbar_wait(kv_full, 0);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      mma_kk(sK, sQ, tmem + C::TM_S);
+      mbar_wait(do_full, 0);
+      tc_fence_after();
+      mma_kk(sV, sdO, tmem + C::TM_DP);
+      mma_commit(sdp_full);
+      for (int n = 0; n < N; ++n) {
+        mbar_wait(ds_full, n & 1);
+        tc_fence_after();
+        mma_kmn(sP, sdO, tmem + C::TM_DV, n > 0);
+        mma_commit(do_empty);
+        mma_kmn(sdS, sQ, tmem + C::TM_DK, n > 0);
+        mma_commit(q_empty);
+        mma_mnmn(sdS, sK, tmem + C::TM_DQ);
+        mma_commit(dq_full);
+        if (n + 1 < N) {
+          mbar_wait(q_full, (n + 1) & 1);
+          tc_fence_after();
+          mma_kk(sK, sQ, tmem + C::TM_S);
+          mbar_wait(dq_empty, n & 1);
+          mbar_wait(do_full, (n + 1) & 1);
+          tc_fence_after();
+          mma_kk(sV, sdO, tmem + C::TM_DP);
+          mma_commit(sdp_full);
+        }
+      }
+      mma_commit(dkv_full);
+    }
+  } else {
+    // ------------------------------------------------ compute warps 0-3
+    const int quad = warp;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const long long key = (long long)jb * 128 + r;
+    const float sl2 = a.scale_log2;
+    for (int n = 0; n < N; ++n) {
+      const int h = g * G + n / n_qt;
+      const int qt = qt_begin + n % n_qt;
+      const long long q0 = (long long)qt * 128;
+      float* lse2 = s_lse2 + (n & 1) * 128;
+      float* dl = s_delta + (n & 1) * 128;
+      {
+        const long long q = q0 + r;
+        float lv = 0.f, dv = 0.f;
+        if (q < a.S) {
+          lv = a.lse[(long long)h * a.ld_lse + q] * 1.4426950408889634f;
+          dv = a.delta[q * a.ld_delta + h];
+        }
+        lse2[r] = lv;
+        dl[r] = dv;
+      }
+      named_bar_sync(1, 128);
+      mbar_wait(sdp_full, n & 1);
+      tc_fence_after();
+      const bool diag = a.causal && qt == jb;
+      const bool tail = q0 + 128 > a.S || (long long)jb * 128 + 128 > a.S;
+      const uint32_t pbase = smem_u32(smem + C::OFF_P), dsbase = smem_u32(smem + C::OFF_DS);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rs[32], rp[32];
+        tmem_ld32(tmem + C::TM_S + lane_off + c * 32, rs);
+        tmem_ld32(tmem + C::TM_DP + lane_off + c * 32, rp);
+        tmem_wait_ld();
+        float p[32], ds[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int qi = c * 32 + i;
+          float pv = ex2b(__uint_as_float(rs[i]) * sl2 - lse2[qi]);
+          if (diag || tail) {
+            const long long q = q0 + qi;
+            if ((a.causal && key > q) || q >= a.S || key >= a.S) pv = 0.f;
+          }
+          p[i] = pv;
+          ds[i] = pv * (__uint_as_float(rp[i]) - dl[qi]);
+        }
+#pragma unroll
+        for (int v8 = 0; v8 < 4; ++v8) {
+          const int qc = c * 32 + v8 * 8;
+          const uint32_t off = (qc >> 6) * 16384 + sw128_offset(r, qc & 63);
+          st_shared_v4(pbase + off, pack_bf16(p[v8 * 8 + 0], p[v8 * 8 + 1]), pack_bf16(p[v8 * 8 + 2], p[v8 * 8 + 3]),
+                       pack_bf16(p[v8 * 8 + 4], p[v8 * 8 + 5]), pack_bf16(p[v8 * 8 + 6], p[v8 * 8 + 7]));
+          st_shared_v4(dsbase + off, pack_bf16(ds[v8 * 8 + 0], ds[v8 * 8 + 1]),
+                       pack_bf16(ds[v8 * 8 + 2], ds[v8 * 8 + 3]), pack_bf16(ds[v8 * 8 + 4], ds[v8 * 8 + 5]),
+                       pack_bf16(ds[v8 * 8 + 6], ds[v8 * 8 + 7]));
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+      // ---- dQ drain: TMEM lane = query row
+      mbar_wait(dq_full, n & 1);
+      tc_fence_after();
+      const long long q = q0 + r;
+      float* dqrow = a.dq_acc + q * (long long)a.nq * D + (long long)h * D;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t rq[32];
+        tmem_ld32(tmem + C::TM_DQ + lane_off + c * 32, rq);
+        tmem_wait_ld();
+        if (q < a.S) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float4 v = make_float4(__uint_as_float(rq[4 * i]) * a.scale, __uint_as_float(rq[4 * i + 1]) * a.scale,
+                                   __uint_as_float(rq[4 * i + 2]) * a.scale, __uint_as_float(rq[4 * i + 3]) * a.scale);
+            atomicAdd(reinterpret_cast<float4*>(dqrow + c * 32 + 4 * i), v);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(dq_empty);
+    }
+    // ---- dK / dV epilogue (TMEM lane = key row)
+    mbar_wait(dkv_full, 0);
+    tc_fence_after();
+    const long long ldacc = (long long)a.nkv * D;
+    for (int which = 0; which < 2; ++which) {          // 0: dV, 1: dK
+      const uint32_t tcol = which ? C::TM_DK : C::TM_DV;
+      const float sc = which ? a.scale : 1.f;
+      float* acc = (which ? a.dk_acc : a.dv_acc);
+      __nv_bfloat16* ob = which ? a.dk_bf16 : a.dv_bf16;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t rr[32];
+        tmem_ld32(tmem + tcol + lane_off + c * 32, rr);
+        tmem_wait_ld();
+        if (key >= a.S || N == 0) continue;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]) * sc;
+        float4* accp = acc ? reinterpret_cast<float4*>(acc + key * ldacc + (long long)g * D + c * 32) : nullptr;
+        if (a.kv_accumulate && accp) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 o = accp[i];
+            v[4 * i] += o.x; v[4 * i + 1] += o.y; v[4 * i + 2] += o.z; v[4 * i + 3] += o.w;
+          }
+        }
+        if (a.kv_write_acc && accp) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) accp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+        if (ob) {
+          uint4* dst = reinterpret_cast<uint4*>(ob + key * a.ld_kvb + (long long)g * D + c * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                                pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err, size_t errlen) {
+  if (p.S <= 0 || p.nkv <= 0) return cudaSuccess;
+  if ((p.d != 64 && p.d != 128) || p.nq % p.nkv) {
+    snprintf(err, errlen, "attn_bwd: unsupported head_dim %d or head counts %d/%d", p.d, p.nq, p.nkv);
+    return cudaErrorInvalidValue;
+  }
+  CUtensorMap tq, tk, tv, tdo;
+  if (!make_tmap_3d(&tq, p.q, p.d, p.nq, p.S, p.d, p.ldq, 64, 1, 128, err, errlen)) return cudaErrorInvalidValue;
+  if (!make_tmap_3d(&tk, p.k, p.d, p.nkv, p.S, p.d, p.ldkv, 64, 1, 128, err, errlen)) return cudaErrorInvalidValue;
+  if (!make_tmap_3d(&tv, p.v, p.d, p.nkv, p.S, p.d, p.ldkv, 64, 1, 128, err, errlen)) return cudaErrorInvalidValue;
+  if (!make_tmap_3d(&tdo, p.dout, p.d, p.nq, p.S, p.d, p.ldo_grad, 64, 1, 128, err, errlen))
+    return cudaErrorInvalidValue;
+  BwdArgs a;
+  a.lse = p.lse;
+  a.delta = p.delta;
+  a.dq_acc = p.dq_acc;
+  a.dk_acc = p.dk_acc;
+  a.dv_acc = p.dv_acc;
+  a.dk_bf16 = reinterpret_cast<__nv_bfloat16*>(p.dk_bf16);
+  a.dv_bf16 = reinterpret_cast<__nv_bfloat16*>(p.dv_bf16);
+  a.S = p.S;
+  a.ld_lse = p.ld_lse;
+  a.ld_delta = p.ld_delta;
+  a.ld_kvb = p.ld_kvb;
+  a.nq = p.nq;
+  a.nkv = p.nkv;
+  a.causal = p.causal;
+  a.kv_accumulate = p.kv_accumulate;
+  a.kv_write_acc = p.kv_write_acc;
+  a.scale = 1.f / sqrtf((float)p.d);
+  a.scale_log2 = 1.4426950408889634f / sqrtf((float)p.d);
+  const int nT = (int)((p.S + 127) / 128);
+  dim3 grid(nT, p.nkv);
+  cudaError_t e;
+  if (p.d == 128) {
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(attn_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<128>::SMEM);
+    if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
+    attn_bwd_kernel<128><<<grid, 192, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, a);
+  } else {
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<64>::SMEM);
+    if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
+    attn_bwd_kernel<64><<<grid, 192, BwdCfg<64>::SMEM, stream>>>(tq, tk, tv, tdo, a);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) snprintf(err, errlen, "attn_bwd launch: %s", cudaGetErrorString(e));
+  return e;
+}
+
+}  // namespace upipe

@@ -1,0 +1,348 @@
+// Causal GQA flash-attention forward for sm_100a.
+//
+// One CTA owns two consecutive 128-row query tiles (A, B) of one local head and
+// streams the KV tiles of the head's KV group through shared memory (TMA, 128B
+// swizzle). Warp roles (320 threads):
+//   warps 0-3  softmax for tile A  (thread = one query row: the 32x32b TMEM load
+//              gives each thread a whole S row, so row max / row sum are
+//              thread-local and need no shuffles)
+//   warps 4-7  softmax for tile B
+//   warp 8     TMA producer (Q once, then K and V per KV tile)
+//   warp 9     MMA issuer: S = Q K^T into TMEM, O += P V with P staged in smem
+// TMEM (512 columns): S_A | S_B | O_A | O_B (d = 128). While one warpgroup runs
+// its softmax the tensor core computes the other tile's S or PV (ping-pong).
+// Online softmax in the exp2 domain with the log2(e)/sqrt(d) scale folded into
+// one FFMA; O is rescaled only when the running max grows by more than 8 (2^8
+// headroom in fp32/bf16), which is exact: l and O always share the reference max.
+#include <cfloat>
+#include <cstdio>
+
+#include "kernels.h"
+#include "sm100.cuh"
+#include "tma_host.h"
+
+namespace upipe {
+namespace {
+
+using namespace dev;
+
+struct FwdArgs {
+  __nv_bfloat16* o;
+  float* lse;
+  long long S, ldo, ld_lse;
+  int nq, nkv, causal, n_pairs;
+  float scale_log2;  // log2(e) / sqrt(d)
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int D>
+struct FwdCfg {
+  static constexpr int TILE = 128;
+  static constexpr int QBYTES = TILE * D * 2;       // one 128 x D bf16 tile
+  static constexpr int KV_STAGES = (D == 64) ? 2 : 1;
+  static constexpr int PBYTES = TILE * TILE * 2;    // P tile 128 x 128 bf16
+  static constexpr int OFF_QA = 0;
+  static constexpr int OFF_QB = QBYTES;
+  static constexpr int OFF_K = 2 * QBYTES;
+  static constexpr int OFF_V = OFF_K + KV_STAGES * QBYTES;
+  static constexpr int OFF_PA = OFF_V + KV_STAGES * QBYTES;
+  static constexpr int OFF_PB = OFF_PA + PBYTES;
+  static constexpr int OFF_BAR = OFF_PB + PBYTES;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr uint32_t TM_SA = 0, TM_SB = 128, TM_OA = 256, TM_OB = 256 + D;
+};
+
+template <int D>
+__global__ void __launch_bounds__(320, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
+  using C = FwdCfg<D>;
+  constexpr int NCH = D / 64;  // 64-wide column chunks of a head
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;                    // [KV_STAGES]
+  uint64_t* k_empty = bars + 3;                   // [KV_STAGES]
+  uint64_t* v_full = bars + 5;                    // [KV_STAGES]
+  uint64_t* v_empty = bars + 7;                   // [KV_STAGES]
+  uint64_t* s_full = bars + 9;                    // [2] tile A/B
+  uint64_t* p_full = bars + 11;                   // [2]
+  uint64_t* o_full = bars + 13;                   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int pair = a.n_pairs - 1 - blockIdx.x;    // longest (causal) work first
+  const int head = blockIdx.y;
+  const int kvh = head / (a.nq / a.nkv);
+  const int qt0 = 2 * pair;                       // query tile index of A (B = qt0 + 1)
+  const int ntiles_kv = (int)((a.S + 127) / 128);
+  const int nA = a.causal ? min(qt0 + 1, ntiles_kv) : ntiles_kv;
+  const int nB = a.causal ? min(qt0 + 2, ntiles_kv) : ntiles_kv;
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::KV_STAGES; ++s) {
+      mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1); mbar_init(&p_full[t], 128); mbar_init(&o_full[t], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      mbar_arrive_expect_tx(q_full, 2 * C::QBYTES);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        tma_load_3d(smem + C::OFF_QA + c * 16384, &tmQ, q_full, c * 64, head, qt0 * 128);
+        tma_load_3d(smem + C::OFF_QB + c * 16384, &tmQ, q_full, c * 64, head, qt0 * 128 + 128);
+      }
+      for (int it = 0; it < nB; ++it) {
+        const int st = it % C::KV_STAGES;
+        const uint32_t ph = (it / C::KV_STAGES) & 1;
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&k_full[st], C::QBYTES);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+          tma_load_3d(smem + C::OFF_K + st * C::QBYTES + c * 16384, &tmK, &k_full[st], c * 64, kvh, it * 128);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&v_full[st], C::QBYTES);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+          tma_load_3d(smem + C::OFF_V + st * C::QBYTES + c * 16384, &tmV, &v_full[st], c * 64, kvh, it * 128);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idS = idesc_bf16(128, 128, false, false);  // Q (K-major) x K (K-major)
+      constexpr uint32_t idO = idesc_bf16(128, D, false, true);     // P (K-major) x V (MN-major)
+      const uint32_t sQA = smem_u32(smem + C::OFF_QA), sQB = smem_u32(smem + C::OFF_QB);
+      auto issue_S = [&](uint32_t sq, uint32_t sk, uint32_t tm) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ss(tm, desc_sw128(sq + c * 16384 + kk * 32, 16, 1024), desc_sw128(sk + c * 16384 + kk * 32, 16, 1024),
+                   idS, (c | kk) != 0);
+      };
+      auto issue_PV = [&](uint32_t sp, uint32_t sv, uint32_t tm, bool acc) {
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ss(tm, desc_sw128(sp + kb * 16384 + kk * 32, 16, 1024),
+                   desc_sw128(sv + kb * 8192 + kk * 2048, 16384, 1024), idO, (acc || kb || kk) ? 1u : 0u);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      issue_S(sQA, smem_u32(smem + C::OFF_K), tmem + C::TM_SA);
+      mma_commit(&s_full[0]);
+      issue_S(sQB, smem_u32(smem + C::OFF_K), tmem + C::TM_SB);
+      mma_commit(&s_full[1]);
+      mma_commit(&k_empty[0]);                    // K(0) consumed once both S MMAs complete
+      for (int it = 0; it < nB; ++it) {
+        const int st = it % C::KV_STAGES;
+        const uint32_t ph = (it / C::KV_STAGES) & 1;
+        const uint32_t sv = smem_u32(smem + C::OFF_V + st * C::QBYTES);
+        mbar_wait(&v_full[st], ph);
+        // ---- tile A
+        if (it < nA) {
+          mbar_wait(&p_full[0], it & 1);
+          tc_fence_after();
+          issue_PV(smem_u32(smem + C::OFF_PA), sv, tmem + C::TM_OA, it > 0);
+          mma_commit(&o_full[0]);
+        }
+        const bool more = it + 1 < nB;
+        const int st1 = (it + 1) % C::KV_STAGES;
+        const uint32_t ph1 = ((it + 1) / C::KV_STAGES) & 1;
+        if (more) mbar_wait(&k_full[st1], ph1);
+        tc_fence_after();
+        if (it + 1 < nA) {
+          issue_S(sQA, smem_u32(smem + C::OFF_K + st1 * C::QBYTES), tmem + C::TM_SA);
+          mma_commit(&s_full[0]);
+        }
+        // ---- tile B
+        mbar_wait(&p_full[1], it & 1);
+        tc_fence_after();
+        issue_PV(smem_u32(smem + C::OFF_PB), sv, tmem + C::TM_OB, it > 0);
+        mma_commit(&o_full[1]);
+        mma_commit(&v_empty[st]);
+        if (more) {
+          issue_S(sQB, smem_u32(smem + C::OFF_K + st1 * C::QBYTES), tmem + C::TM_SB);
+          mma_commit(&s_full[1]);
+          mma_commit(&k_empty[st1]);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ softmax warpgroups
+    const int wg = warp >> 2;                       // 0: tile A, 1: tile B
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const int qt = qt0 + wg;
+    const long long q = (long long)qt * 128 + row;  // global query token
+    const int n = wg ? nB : nA;
+    const uint32_t tS = tmem + (wg ? C::TM_SB : C::TM_SA) + ((uint32_t)(quad * 32) << 16);
+    const uint32_t tO = tmem + (wg ? C::TM_OB : C::TM_OA) + ((uint32_t)(quad * 32) << 16);
+    uint8_t* sP = smem + (wg ? C::OFF_PB : C::OFF_PA);
+    const float sl2 = a.scale_log2;
+    float m_ref = -INFINITY, l_run = 0.f;
+    for (int it = 0; it < n; ++it) {
+      mbar_wait(&s_full[wg], it & 1);
+      tc_fence_after();
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tS + c * 32, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]) * sl2;
+      }
+      const long long key0 = (long long)it * 128;
+      if (a.causal ? (it == qt) : (key0 + 128 > a.S)) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i) {
+          const long long key = key0 + i;
+          if ((a.causal && key > q) || key >= a.S) s[i] = -INFINITY;
+        }
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+      // lazy rescale: keep the old reference max unless the row max grew by > 8 (log2 units)
+      bool rescale = false;
+      float alpha = 1.f;
+      if (mx > m_ref + 8.f) {
+        alpha = ex2(m_ref - mx);                      // 0 when m_ref = -inf
+        rescale = it > 0;
+        m_ref = mx;
+      }
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        s[i] = ex2(s[i] - m_ref);
+        sum += s[i];
+      }
+      l_run = l_run * alpha + sum;
+      if (it > 0) {
+        mbar_wait(&o_full[wg], (it - 1) & 1);         // PV(it-1) done: O and sP free
+        tc_fence_after();
+      }
+      if (rescale) {
+#pragma unroll
+        for (int c = 0; c < D / 16; ++c) {
+          uint32_t r[16];
+          tmem_ld16(tO + c * 16, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          tmem_st16(tO + c * 16, r);
+        }
+        tmem_wait_st();
+      }
+      // P (bf16) -> smem, K-major 128B-swizzled [128 rows][128 keys] as two 64-key chunks
+      const uint32_t pbase = smem_u32(sP);
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {
+        const int k0 = ch * 8;
+        const uint32_t addr = pbase + (k0 >> 6) * 16384 + sw128_offset(row, k0 & 63);
+        st_shared_v4(addr, pack_bf16(s[k0], s[k0 + 1]), pack_bf16(s[k0 + 2], s[k0 + 3]),
+                     pack_bf16(s[k0 + 4], s[k0 + 5]), pack_bf16(s[k0 + 6], s[k0 + 7]));
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&p_full[wg]);
+    }
+    // ---- epilogue: O / l -> bf16, lse
+    mbar_wait(&o_full[wg], (n - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l_run;
+    const bool valid = q < a.S;
+    __nv_bfloat16* orow = a.o + q * a.ldo + (long long)head * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(tO + c * 32, r);
+      tmem_wait_ld();
+      if (valid) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(pack_bf16(__uint_as_float(r[8 * i + 0]) * inv, __uint_as_float(r[8 * i + 1]) * inv),
+                              pack_bf16(__uint_as_float(r[8 * i + 2]) * inv, __uint_as_float(r[8 * i + 3]) * inv),
+                              pack_bf16(__uint_as_float(r[8 * i + 4]) * inv, __uint_as_float(r[8 * i + 5]) * inv),
+                              pack_bf16(__uint_as_float(r[8 * i + 6]) * inv, __uint_as_float(r[8 * i + 7]) * inv));
+      }
+    }
+    if (valid) a.lse[(long long)head * a.ld_lse + q] = (m_ref + __log2f(l_run)) * 0.69314718055994531f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err, size_t errlen) {
+  if (p.S <= 0 || p.nq <= 0) return cudaSuccess;
+  if ((p.d != 64 && p.d != 128) || p.nkv <= 0 || p.nq % p.nkv) {
+    snprintf(err, errlen, "attn_fwd: unsupported head_dim %d or head counts %d/%d", p.d, p.nq, p.nkv);
+    return cudaErrorInvalidValue;
+  }
+  CUtensorMap tq, tk, tv;
+  // 3-D views {d, heads, S}: head stride d elements, token stride ld
+  if (!make_tmap_3d(&tq, p.q, p.d, p.nq, p.S, p.d, p.ldq, 64, 1, 128, err, errlen)) return cudaErrorInvalidValue;
+  if (!make_tmap_3d(&tk, p.k, p.d, p.nkv, p.S, p.d, p.ldkv, 64, 1, 128, err, errlen)) return cudaErrorInvalidValue;
+  if (!make_tmap_3d(&tv, p.v, p.d, p.nkv, p.S, p.d, p.ldkv, 64, 1, 128, err, errlen)) return cudaErrorInvalidValue;
+  FwdArgs a;
+  a.o = reinterpret_cast<__nv_bfloat16*>(p.o);
+  a.lse = p.lse;
+  a.S = p.S;
+  a.ldo = p.ldo;
+  a.ld_lse = p.ld_lse;
+  a.nq = p.nq;
+  a.nkv = p.nkv;
+  a.causal = p.causal;
+  const int ntiles = (int)((p.S + 127) / 128);
+  a.n_pairs = (ntiles + 1) / 2;
+  a.scale_log2 = 1.4426950408889634f / sqrtf((float)p.d);
+  dim3 grid(a.n_pairs, p.nq);
+  cudaError_t e;
+  if (p.d == 128) {
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<128>::SMEM);
+    if (attr != cudaSuccess) { snprintf(err, errlen, "attn_fwd attr: %s", cudaGetErrorString(attr)); return attr; }
+    attn_fwd_kernel<128><<<grid, 320, FwdCfg<128>::SMEM, stream>>>(tq, tk, tv, a);
+  } else {
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<64>::SMEM);
+    if (attr != cudaSuccess) { snprintf(err, errlen, "attn_fwd attr: %s", cudaGetErrorString(attr)); return attr; }
+    attn_fwd_kernel<64><<<grid, 320, FwdCfg<64>::SMEM, stream>>>(tq, tk, tv, a);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) snprintf(err, errlen, "attn_fwd launch: %s", cudaGetErrorString(e));
+  return e;
+}
+
+}  // namespace upipe

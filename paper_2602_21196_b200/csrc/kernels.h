@@ -1,0 +1,102 @@
+// Internal launcher declarations (host side). Not part of the C ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace upipe {
+
+// ---------------------------------------------------------------- GEMM
+// D[m, n] = alpha * sum_k A(m, k) * B(n, k)   (bf16 in, fp32 accumulate in TMEM)
+//
+// Every operand is a 2-D row-major bf16 tensor in HBM addressed through a TMA map
+// (inner dim contiguous). "K-major": the operand's K index runs along the inner
+// dim; "MN-major": its M (or N) index does. Operands may be gathered in 64-element
+// granules: for a logical outer index i and K index k,
+//   outer_coord = o_base + (i / o_len) * o_istride + i % o_len + (k / k_len) * o_kstride
+//   k_coord     = k_base + (k / k_len) * k_kstride + k % k_len + (i / o_len) * k_istride
+// (o_len, k_len multiples of 64). This is how the per-stage head gather of the
+// UPipe schedule (weights rows / columns of the stage's heads, the a2a buffers laid
+// out [C][S_l][...]) is expressed without any copy.
+struct OperandMap {
+  const void* ptr = nullptr;
+  int64_t inner = 0, outer = 0;  // tensor extents (elements): inner = contiguous dim
+  int64_t ld = 0;                // row stride in elements
+  bool mn_major = false;         // false: K along inner ; true: M/N along inner
+  int64_t o_base = 0, o_len = 1 << 30, o_istride = 0, o_kstride = 0;
+  int64_t k_base = 0, k_len = 1 << 30, k_kstride = 0, k_istride = 0;
+};
+
+// Output element (m, n) goes to
+//   row = r_base + (m / m_len) * r_mstride + m % m_len + (n / n_len) * r_nstride
+//   col = c_base + (n / n_len) * c_nstride + n % n_len + (m / m_len) * c_mstride
+enum class Epi : int {
+  kStoreBF16 = 0,     // out_bf16 = bf16(acc)
+  kStoreF32 = 1,      // out_f32 = acc
+  kAccF32 = 2,        // out_f32 += acc
+  kAccF32ToBF16 = 3,  // out_bf16 = bf16(out_f32 + acc)   (last accumulation step)
+};
+struct OutMap {
+  void* out_f32 = nullptr;
+  void* out_bf16 = nullptr;
+  int64_t ld_f32 = 0, ld_bf16 = 0;
+  int64_t r_base = 0, m_len = 1 << 30, r_mstride = 0, r_nstride = 0;
+  int64_t c_base = 0, n_len = 1 << 30, c_nstride = 0, c_mstride = 0;
+  Epi epi = Epi::kStoreBF16;
+};
+
+struct GemmProblem {
+  int64_t M = 0, N = 0, K = 0;
+  float alpha = 1.0f;
+  OperandMap a, b;
+  OutMap c;
+};
+
+cudaError_t gemm_run(const GemmProblem& p, cudaStream_t stream, char* err, size_t errlen);
+
+// ---------------------------------------------------------------- attention
+// Causal GQA flash attention over the full sequence for the heads local to this
+// device in one stage (head layout after the inp all-to-all).
+//   q   [S][nq][d] bf16 (token-major, heads contiguous per token: row stride ldq elems)
+//   k,v [S][nkv][d] bf16 (row stride ldkv)
+//   o   [S][nq][d] bf16 written at o + t*ldo + j*d
+//   lse [nq][S] fp32 natural-log log-sum-exp at lse + j*ld_lse + t
+// q head j uses kv head kv_of_q(j) = j / (nq / nkv).
+struct AttnFwdProblem {
+  const void* q; const void* k; const void* v;
+  void* o; float* lse;
+  int64_t S; int nq, nkv, d; int causal;
+  int64_t ldq, ldkv, ldo, ld_lse;
+};
+cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err, size_t errlen);
+
+// Backward: dq_acc fp32 [S][nq][d] (+= scale*dS K; must be zeroed by caller unless accumulate),
+// dk/dv: fp32 accumulators [S][nkv][d] (kv_mode: 0 store, 1 accumulate) and/or bf16 output
+// (kv_bf16 != null: write bf16(acc_prev + new) at kv_bf16 + t*ld_kvb + g*d).
+struct AttnBwdProblem {
+  const void* q; const void* k; const void* v; const void* dout;
+  const float* lse; const float* delta;       // [nq][S] (ld_lse), delta = rowsum(dO*O) [S][nq] (ld_delta)
+  float* dq_acc;                              // [S][nq][d]
+  float* dk_acc; float* dv_acc;               // [S][nkv][d]
+  void* dk_bf16; void* dv_bf16;               // optional bf16 outputs [S][nkv][d] row stride ld_kvb
+  int64_t S; int nq, nkv, d; int causal;
+  int64_t ldq, ldkv, ldo_grad, ld_lse, ld_delta, ld_kvb;
+  int kv_accumulate;                          // 1: add the previous dk_acc/dv_acc contents
+  int kv_write_acc;                           // 1: write fp32 accumulators back
+};
+cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err, size_t errlen);
+
+// ---------------------------------------------------------------- HBM-bound helpers
+// delta[t][j] = sum_e dO[t][j*d+e] * O[t][j*d+e] over bf16 inputs, fp32 result.
+cudaError_t rowdot_run(const void* dO, int64_t ld_do, const void* O, int64_t ld_o, float* delta, int64_t ld_delta,
+                       int64_t rows, int nheads, int d, cudaStream_t s);
+// bf16 = bf16(scale * f32) elementwise over a [rows][cols] block with strides.
+cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
+                             float scale, cudaStream_t s);
+// Column scatter: dst[t][col_of(seg)+e] = src[seg][t][e]   (unpack of the out all-to-all)
+cudaError_t unpack_cols_run(const void* src, int64_t rows, int nseg, int seg_cols, void* dst, int64_t ldd,
+                            int64_t col_base, int64_t col_stride, cudaStream_t s);
+cudaError_t synth_fill_bf16_run(void* dst, int64_t n, uint64_t seed, int tensor_id, int exponent, int64_t start,
+                                cudaStream_t s);
+
+}  // namespace upipe

@@ -1,0 +1,152 @@
+// HBM-bound helpers of the UPipe path: coalesced, 16-byte vectorised, grid sized
+// in multiples of the SM count (148) with grid-stride loops.
+//   rowdot      delta = rowsum(dO * O) per (token, head)      (DESIGN A13)
+//   cvt         fp32 accumulator -> bf16 (scaled)             (B5 dQ post, F7/B8 finalize)
+//   unpack_cols out-a2a receive [C][S_l][qpd d] -> o_saved    (F5)
+//   synth_fill  device copy of the counter-based input generator (synth/__init__.py)
+#include <cstdio>
+
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace upipe {
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(int64_t work, int per_block) {
+  int64_t b = (work + per_block - 1) / per_block;
+  const int64_t cap = 148 * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+// One group of LANES = d/8 threads per (token, head); 8 bf16 per thread per tensor.
+template <int LANES>
+__global__ void rowdot_kernel(const __nv_bfloat16* __restrict__ dO, long long ld_do,
+                              const __nv_bfloat16* __restrict__ O, long long ld_o, float* __restrict__ delta,
+                              long long ld_delta, long long rows, int nheads, int d) {
+  const long long groups = rows * nheads;
+  const int sub = threadIdx.x % LANES;
+  long long gidx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
+  const long long gstride = (long long)gridDim.x * blockDim.x / LANES;
+  for (; gidx < groups; gidx += gstride) {
+    const long long t = gidx / nheads;
+    const int j = (int)(gidx % nheads);
+    const uint4 a = *reinterpret_cast<const uint4*>(dO + t * ld_do + (long long)j * d + sub * 8);
+    const uint4 b = *reinterpret_cast<const uint4*>(O + t * ld_o + (long long)j * d + sub * 8);
+    float fa[8], fb[8];
+    bf16x8_to_f32(a, fa);
+    bf16x8_to_f32(b, fb);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s = fmaf(fa[i], fb[i], s);
+#pragma unroll
+    for (int off = LANES / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, LANES);
+    if (sub == 0) delta[t * ld_delta + j] = s;
+  }
+}
+
+__global__ void cvt_kernel(const float* __restrict__ src, long long lds, __nv_bfloat16* __restrict__ dst,
+                           long long ldd, long long rows, long long cols, float scale) {
+  const long long v8 = cols / 8;
+  const long long total = rows * v8;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / v8, c = (i % v8) * 8;
+    const float4 x = *reinterpret_cast<const float4*>(src + r * lds + c);
+    const float4 y = *reinterpret_cast<const float4*>(src + r * lds + c + 4);
+    *reinterpret_cast<uint4*>(dst + r * ldd + c) =
+        make_uint4(dev::pack_bf16(x.x * scale, x.y * scale), dev::pack_bf16(x.z * scale, x.w * scale),
+                   dev::pack_bf16(y.x * scale, y.y * scale), dev::pack_bf16(y.z * scale, y.w * scale));
+  }
+}
+
+__global__ void unpack_kernel(const uint4* __restrict__ src, long long rows, int nseg, int seg_v,
+                              __nv_bfloat16* __restrict__ dst, long long ldd, long long col_base,
+                              long long col_stride) {
+  const long long total = (long long)nseg * rows * seg_v;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long s = i / (rows * seg_v);
+    const long long rem = i % (rows * seg_v);
+    const long long t = rem / seg_v, e = (rem % seg_v) * 8;
+    *reinterpret_cast<uint4*>(dst + t * ldd + col_base + s * col_stride + e) = src[i];
+  }
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+__global__ void synth_kernel(__nv_bfloat16* __restrict__ dst, long long n, uint64_t base, float step) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint64_t z = splitmix64(base + (uint64_t)i);
+    const int m = (int)(z >> 56);
+    dst[i] = __float2bfloat16_rn((float)(2 * m - 255) * step);   // exact: <= 8 significant bits
+  }
+}
+
+}  // namespace
+
+cudaError_t rowdot_run(const void* dO, int64_t ld_do, const void* O, int64_t ld_o, float* delta, int64_t ld_delta,
+                       int64_t rows, int nheads, int d, cudaStream_t s) {
+  if (rows <= 0 || nheads <= 0) return cudaSuccess;
+  const int64_t groups = rows * nheads;
+  if (d == 128) {
+    rowdot_kernel<16><<<grid_for(groups * 16, kThreads), kThreads, 0, s>>>(
+        (const __nv_bfloat16*)dO, ld_do, (const __nv_bfloat16*)O, ld_o, delta, ld_delta, rows, nheads, d);
+  } else if (d == 64) {
+    rowdot_kernel<8><<<grid_for(groups * 8, kThreads), kThreads, 0, s>>>(
+        (const __nv_bfloat16*)dO, ld_do, (const __nv_bfloat16*)O, ld_o, delta, ld_delta, rows, nheads, d);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
+                             float scale, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  if (cols % 8) return cudaErrorInvalidValue;
+  cvt_kernel<<<grid_for(rows * cols / 8, kThreads), kThreads, 0, s>>>(src, lds, (__nv_bfloat16*)dst, ldd, rows,
+                                                                     cols, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t unpack_cols_run(const void* src, int64_t rows, int nseg, int seg_cols, void* dst, int64_t ldd,
+                            int64_t col_base, int64_t col_stride, cudaStream_t s) {
+  if (rows <= 0 || nseg <= 0) return cudaSuccess;
+  if (seg_cols % 8) return cudaErrorInvalidValue;
+  const int seg_v = seg_cols / 8;
+  unpack_kernel<<<grid_for((int64_t)nseg * rows * seg_v, kThreads), kThreads, 0, s>>>(
+      (const uint4*)src, rows, nseg, seg_v, (__nv_bfloat16*)dst, ldd, col_base, col_stride);
+  return cudaGetLastError();
+}
+
+cudaError_t synth_fill_bf16_run(void* dst, int64_t n, uint64_t seed, int tensor_id, int exponent, int64_t start,
+                                cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const uint64_t base = seed * 0x9E3779B97F4A7C15ull + (uint64_t)tensor_id * 0xD1B54A32D192ED03ull + (uint64_t)start;
+  const float step = ldexpf(1.0f, exponent - 8);
+  synth_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>((__nv_bfloat16*)dst, n, base, step);
+  return cudaGetLastError();
+}
+
+}  // namespace upipe

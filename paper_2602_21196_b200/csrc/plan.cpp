@@ -1,0 +1,119 @@
+// Shape validation, GQA stage plan and workspace layout (§8b preconditions).
+#include <cstdio>
+
+#include "upipe_internal.h"
+
+namespace upipe {
+
+namespace {
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+}  // namespace
+
+upipe_status_t validate_shape(int C, const upipe_shape_t* sh, std::string& msg) {
+  auto bad = [&](upipe_status_t st, const char* what) {
+    msg = what;
+    return st;
+  };
+  if (!sh) return bad(UPIPE_ERR_INVALID_ARG, "shape == NULL");
+  if (C < 1 || C > 64) return bad(UPIPE_ERR_INVALID_ARG, "cp_size must be in [1, 64]");
+  if (sh->seq_local < 1) return bad(UPIPE_ERR_INVALID_ARG, "seq_local >= 1 required (S = S_l * C, S:239)");
+  if (sh->n_q_heads < 1 || sh->n_kv_heads < 1) return bad(UPIPE_ERR_INVALID_ARG, "head counts must be >= 1");
+  if (sh->n_q_heads % sh->n_kv_heads) return bad(UPIPE_ERR_INVALID_ARG, "n_q_heads % n_kv_heads != 0 (S:37)");
+  if (sh->chunk_heads < 1) return bad(UPIPE_ERR_INVALID_ARG, "chunk_heads >= 1 required");
+  if (sh->chunk_heads % C) return bad(UPIPE_ERR_INVALID_ARG, "chunk_heads % cp_size != 0 (P:317: U must be divisible by C)");
+  if (sh->n_q_heads % sh->chunk_heads) return bad(UPIPE_ERR_INVALID_ARG, "n_q_heads % chunk_heads != 0 (H/U stages, P:315)");
+  if (sh->causal != 0 && sh->causal != 1) return bad(UPIPE_ERR_INVALID_ARG, "causal must be 0 or 1");
+  if (sh->head_dim != 64 && sh->head_dim != 128) return bad(UPIPE_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  if (sh->hidden < 64 || sh->hidden % 64) return bad(UPIPE_ERR_UNSUPPORTED, "hidden % 64 != 0 (TMA tile granule)");
+  if (sh->n_kv_heads % C)
+    return bad(UPIPE_ERR_UNSUPPORTED, "n_kv_heads % cp_size != 0 (GQA schedule needs whole kv heads per device, DESIGN A9)");
+  const int R = sh->n_q_heads / sh->n_kv_heads;
+  const int qpd = sh->chunk_heads / C;
+  if (R % qpd && qpd % R)
+    return bad(UPIPE_ERR_UNSUPPORTED, "chunk_heads/cp_size and n_q_heads/n_kv_heads must divide one another (DESIGN A8)");
+  const int64_t S = sh->seq_local * C;
+  if (S > (int64_t(1) << 31) - 256) return bad(UPIPE_ERR_UNSUPPORTED, "S >= 2^31 tokens (TMA coordinate range)");
+  if ((int64_t)sh->n_q_heads * sh->head_dim > 65536) return bad(UPIPE_ERR_UNSUPPORTED, "n_q_heads*head_dim > 65536");
+  msg.clear();
+  return UPIPE_OK;
+}
+
+Plan make_plan(int C, const upipe_shape_t& sh) {
+  Plan p;
+  p.C = C;
+  p.sh = sh;
+  p.S_l = sh.seq_local;
+  p.S = sh.seq_local * C;
+  p.Hq = sh.n_q_heads;
+  p.Hkv = sh.n_kv_heads;
+  p.d = sh.head_dim;
+  p.D = sh.hidden;
+  p.U = sh.chunk_heads;
+  p.R = p.Hq / p.Hkv;
+  p.qpd = p.U / C;
+  p.kv_res = p.qpd > p.R ? p.qpd / p.R : 1;
+  p.sigma = p.qpd < p.R ? p.R / p.qpd : 1;
+  p.nstages = p.Hq / p.U;
+  return p;
+}
+
+FwdWs fwd_workspace(const Plan& p) {
+  FwdWs w{};
+  const size_t qe = (size_t)p.S * p.qpd * p.d * 2;     // one Q-sized chunk, bf16
+  const size_t ke = (size_t)p.S * p.kv_res * p.d * 2;  // one K-sized chunk, bf16
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  const bool comm = p.C > 1;
+  w.qsend = take(qe);
+  w.qrecv = comm ? take(qe) : w.qsend;
+  w.ksend = take(ke);
+  w.krecv = comm ? take(ke) : w.ksend;
+  w.vsend = take(ke);
+  w.vrecv = comm ? take(ke) : w.vsend;
+  w.osend = comm ? take(qe) : 0;
+  w.orecv = comm ? take(qe) : 0;
+  w.yacc = p.nstages > 1 ? take((size_t)p.S_l * p.D * 4) : 0;
+  w.total = off;
+  return w;
+}
+
+BwdWs bwd_workspace(const Plan& p) {
+  BwdWs w{};
+  const size_t qe = (size_t)p.S * p.qpd * p.d * 2;
+  const size_t ke = (size_t)p.S * p.kv_res * p.d * 2;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  const bool comm = p.C > 1;
+  w.qsend = take(qe);
+  w.qrecv = comm ? take(qe) : w.qsend;
+  w.ksend = take(ke);
+  w.krecv = comm ? take(ke) : w.ksend;
+  w.vsend = take(ke);
+  w.vrecv = comm ? take(ke) : w.vsend;
+  w.dosend = take(qe);
+  w.dorecv = comm ? take(qe) : w.dosend;
+  w.dsend = take((size_t)p.S * p.qpd * 4);
+  w.drecv = comm ? take((size_t)p.S * p.qpd * 4) : w.dsend;
+  w.dqacc = take(qe * 2);
+  w.dqsend = take(qe);
+  w.dqrecv = comm ? take(qe) : w.dqsend;
+  w.dkacc = p.sigma > 1 ? take(ke * 2) : 0;
+  w.dvacc = p.sigma > 1 ? take(ke * 2) : 0;
+  w.dksend = take(ke);
+  w.dvsend = take(ke);
+  w.dkrecv = comm ? take(ke) : w.dksend;
+  w.dvrecv = comm ? take(ke) : w.dvsend;
+  w.dxacc = take((size_t)p.S_l * p.D * 4);
+  w.total = off;
+  return w;
+}
+
+}  // namespace upipe

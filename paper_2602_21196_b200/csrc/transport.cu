@@ -1,0 +1,257 @@
+// Collectives of the UPipe path.
+//
+//  * SelfTransport   C = 1: the all-to-alls are identities (A20: no a2a at C = 1).
+//  * NcclTransport   one process per GPU; equal-block all-to-all as one grouped
+//                    ncclSend/ncclRecv per peer over NVLink 5 / NVSwitch; fp32
+//                    all-reduce of dW.
+//  * FabricTransport C ranks as host threads of one process (each with its own
+//                    stream): peers' send buffers are read with device-to-device
+//                    copies ordered by CUDA events and host barriers. Runs the
+//                    sharded path (C = 2..8) on a single GPU for parity tests.
+#include <nccl.h>
+
+#include <chrono>
+#include <cstdio>
+
+#include "upipe_internal.h"
+
+namespace upipe {
+
+namespace {
+
+class SelfTransport final : public Transport {
+ public:
+  int size() const override { return 1; }
+  int rank() const override { return 0; }
+  upipe_status_t alltoall(const void* send, void* recv, size_t bytes, cudaStream_t s, std::string& err) override {
+    if (send == recv || bytes == 0) return UPIPE_OK;
+    cudaError_t e = cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return UPIPE_ERR_CUDA;
+    }
+    return UPIPE_OK;
+  }
+  upipe_status_t allreduce_sum_f32(float*, size_t, cudaStream_t, std::string&) override { return UPIPE_OK; }
+};
+
+class NcclTransport final : public Transport {
+ public:
+  NcclTransport(ncclComm_t c, int C, int r) : comm_(c), C_(C), rank_(r) {}
+  ~NcclTransport() override {
+    if (comm_) ncclCommDestroy(comm_);
+  }
+  int size() const override { return C_; }
+  int rank() const override { return rank_; }
+  upipe_status_t alltoall(const void* send, void* recv, size_t bytes, cudaStream_t s, std::string& err) override {
+    ncclResult_t r = ncclGroupStart();
+    for (int p = 0; p < C_ && r == ncclSuccess; ++p) {
+      r = ncclSend(static_cast<const char*>(send) + p * bytes, bytes, ncclUint8, p, comm_, s);
+      if (r == ncclSuccess) r = ncclRecv(static_cast<char*>(recv) + p * bytes, bytes, ncclUint8, p, comm_, s);
+    }
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess) {
+      err = std::string("NCCL all-to-all: ") + ncclGetErrorString(r != ncclSuccess ? r : r2);
+      return UPIPE_ERR_COMM;
+    }
+    return UPIPE_OK;
+  }
+  upipe_status_t allreduce_sum_f32(float* buf, size_t n, cudaStream_t s, std::string& err) override {
+    ncclResult_t r = ncclAllReduce(buf, buf, n, ncclFloat32, ncclSum, comm_, s);
+    if (r != ncclSuccess) {
+      err = std::string("NCCL all-reduce: ") + ncclGetErrorString(r);
+      return UPIPE_ERR_COMM;
+    }
+    return UPIPE_OK;
+  }
+
+ private:
+  ncclComm_t comm_;
+  int C_, rank_;
+};
+
+}  // namespace
+
+}  // namespace upipe
+
+// ------------------------------------------------------------------ fabric (single process, C threads)
+struct upipe_fabric_s {
+  int C = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t generation = 0;
+  std::vector<const void*> ptr;
+  std::vector<cudaEvent_t> ev_a, ev_b;
+  std::vector<int> device;
+
+  // Host barrier across the C ranks; false on timeout (a peer failed or never called).
+  bool barrier(int timeout_s = 120) {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t gen = generation;
+    if (++arrived == C) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+      return true;
+    }
+    return cv.wait_for(lk, std::chrono::seconds(timeout_s), [&] { return generation != gen; });
+  }
+};
+
+namespace upipe {
+namespace {
+
+__global__ void fabric_sum_kernel(float* const* bufs, int C, size_t begin, size_t end, float* dst) {
+  for (size_t i = begin + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < end; i += (size_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < C; ++p) s += bufs[p][i];
+    dst[i] = s;
+  }
+}
+
+class FabricTransport final : public Transport {
+ public:
+  FabricTransport(upipe_fabric_t f, int r) : f_(f), rank_(r) {}
+  ~FabricTransport() override {
+    if (dev_ptrs_) cudaFree(dev_ptrs_);
+  }
+  int size() const override { return f_->C; }
+  int rank() const override { return rank_; }
+
+  upipe_status_t alltoall(const void* send, void* recv, size_t bytes, cudaStream_t s, std::string& err) override {
+    const int C = f_->C;
+    if (!sync_publish(send, s, err)) return UPIPE_ERR_COMM;
+    for (int p = 0; p < C; ++p) {
+      if (p != rank_) cudaStreamWaitEvent(s, f_->ev_a[p], 0);
+      const char* src = static_cast<const char*>(f_->ptr[p]) + (size_t)rank_ * bytes;
+      cudaError_t e = cudaMemcpyAsync(static_cast<char*>(recv) + (size_t)p * bytes, src, bytes,
+                                      cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) {
+        err = cudaGetErrorString(e);
+        return UPIPE_ERR_CUDA;
+      }
+    }
+    return finish(s, err) ? UPIPE_OK : UPIPE_ERR_COMM;
+  }
+
+  upipe_status_t allreduce_sum_f32(float* buf, size_t n, cudaStream_t s, std::string& err) override {
+    const int C = f_->C;
+    if (!sync_publish(buf, s, err)) return UPIPE_ERR_COMM;
+    for (int p = 0; p < C; ++p)
+      if (p != rank_) cudaStreamWaitEvent(s, f_->ev_a[p], 0);
+    if (!dev_ptrs_ && cudaMalloc(&dev_ptrs_, sizeof(float*) * 64) != cudaSuccess) {
+      err = "fabric: cudaMalloc";
+      return UPIPE_ERR_CUDA;
+    }
+    std::vector<float*> h(C);
+    for (int p = 0; p < C; ++p) h[p] = const_cast<float*>(static_cast<const float*>(f_->ptr[p]));
+    cudaMemcpyAsync(dev_ptrs_, h.data(), sizeof(float*) * C, cudaMemcpyHostToDevice, s);
+    const size_t chunk = (n + C - 1) / C;
+    const size_t b = std::min(n, chunk * rank_), e = std::min(n, chunk * (rank_ + 1));
+    if (e > b) fabric_sum_kernel<<<148 * 4, 256, 0, s>>>(dev_ptrs_, C, b, e, buf);
+    // everyone's owned slice is reduced; then copy the other slices from their owners
+    if (!sync_publish(buf, s, err)) return UPIPE_ERR_COMM;
+    for (int p = 0; p < C; ++p) {
+      if (p == rank_) continue;
+      cudaStreamWaitEvent(s, f_->ev_a[p], 0);
+      const size_t pb = std::min(n, chunk * p), pe = std::min(n, chunk * (p + 1));
+      if (pe > pb)
+        cudaMemcpyAsync(buf + pb, static_cast<const float*>(f_->ptr[p]) + pb, (pe - pb) * 4, cudaMemcpyDeviceToDevice, s);
+    }
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) {
+      err = cudaGetErrorString(ce);
+      return UPIPE_ERR_CUDA;
+    }
+    return finish(s, err) ? UPIPE_OK : UPIPE_ERR_COMM;
+  }
+
+ private:
+  // Record "my buffer is ready" and publish its pointer; returns after all ranks did the same.
+  bool sync_publish(const void* p, cudaStream_t s, std::string& err) {
+    cudaEventRecord(f_->ev_a[rank_], s);
+    f_->ptr[rank_] = p;
+    if (!f_->barrier()) {
+      err = "fabric barrier timeout (a peer rank failed or never entered the collective)";
+      return false;
+    }
+    return true;
+  }
+  // Record "done reading peers" and make my stream wait until all peers finished reading my buffer.
+  bool finish(cudaStream_t s, std::string& err) {
+    cudaEventRecord(f_->ev_b[rank_], s);
+    if (!f_->barrier()) {
+      err = "fabric barrier timeout";
+      return false;
+    }
+    for (int p = 0; p < f_->C; ++p)
+      if (p != rank_) cudaStreamWaitEvent(s, f_->ev_b[p], 0);
+    if (!f_->barrier()) {
+      err = "fabric barrier timeout";
+      return false;
+    }
+    return true;
+  }
+  upipe_fabric_t f_;
+  int rank_;
+  float** dev_ptrs_ = nullptr;
+};
+
+}  // namespace
+
+std::unique_ptr<Transport> make_self_transport() { return std::make_unique<SelfTransport>(); }
+
+std::unique_ptr<Transport> make_nccl_transport(const uint8_t* uid, int C, int rank, std::string& err) {
+  ncclUniqueId id;
+  static_assert(sizeof(ncclUniqueId) <= UPIPE_UID_BYTES, "uid size");
+  std::memcpy(&id, uid, sizeof(id));
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = ncclCommInitRank(&comm, C, id, rank);
+  if (r != ncclSuccess) {
+    err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+    return nullptr;
+  }
+  return std::make_unique<NcclTransport>(comm, C, rank);
+}
+
+std::unique_ptr<Transport> make_fabric_transport(upipe_fabric_t f, int rank, int device, std::string& err) {
+  if (!f || rank < 0 || rank >= f->C) {
+    err = "fabric: bad rank";
+    return nullptr;
+  }
+  {
+    std::lock_guard<std::mutex> lk(f->mu);
+    if (cudaEventCreateWithFlags(&f->ev_a[rank], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&f->ev_b[rank], cudaEventDisableTiming) != cudaSuccess) {
+      err = "fabric: cudaEventCreate failed";
+      return nullptr;
+    }
+    f->device[rank] = device;
+  }
+  return std::make_unique<FabricTransport>(f, rank);
+}
+
+}  // namespace upipe
+
+extern "C" upipe_status_t upipe_fabric_create(upipe_fabric_t* fabric, int cp_size) {
+  if (!fabric || cp_size < 1 || cp_size > 64) return UPIPE_ERR_INVALID_ARG;
+  auto* f = new upipe_fabric_s();
+  f->C = cp_size;
+  f->ptr.assign(cp_size, nullptr);
+  f->ev_a.assign(cp_size, nullptr);
+  f->ev_b.assign(cp_size, nullptr);
+  f->device.assign(cp_size, 0);
+  *fabric = f;
+  return UPIPE_OK;
+}
+
+extern "C" upipe_status_t upipe_fabric_destroy(upipe_fabric_t f) {
+  if (!f) return UPIPE_ERR_INVALID_ARG;
+  for (int p = 0; p < f->C; ++p) {
+    if (f->ev_a[p]) cudaEventDestroy(f->ev_a[p]);
+    if (f->ev_b[p]) cudaEventDestroy(f->ev_b[p]);
+  }
+  delete f;
+  return UPIPE_OK;
+}

@@ -1,0 +1,76 @@
+// Internal host-side structures of libupipe (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <condition_variable>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/upipe.h"
+
+namespace upipe {
+
+// ------------------------------------------------------------------ plan (DESIGN A8)
+struct Plan {
+  int C = 1;
+  upipe_shape_t sh{};
+  int64_t S_l = 0, S = 0;
+  int R = 1, qpd = 1, kv_res = 1, sigma = 1, nstages = 1;
+  int d = 0, Hq = 0, Hkv = 0, D = 0, U = 0;
+
+  // GQA schedule, closed form: stage s = (super-stage b, position r); device p holds KV heads
+  // [(b*C + p)*kv_res, +kv_res) and q heads [kv0*R + r*qpd, +qpd).
+  int kv0(int s, int p) const { return ((s / sigma) * C + p) * kv_res; }
+  int q0(int s, int p) const { return kv0(s, p) * R + (s % sigma) * qpd; }
+  bool kv_sent(int s) const { return (s % sigma) == 0; }
+  bool kv_last(int s) const { return (s % sigma) == sigma - 1; }
+  // per-device step of the first q head / kv head between consecutive devices (same for every s)
+  int q_dev_stride() const { return kv_res * R; }
+  int kv_dev_stride() const { return kv_res; }
+};
+
+// Returns UPIPE_OK or the status of the first violated precondition, with msg naming it.
+upipe_status_t validate_shape(int C, const upipe_shape_t* sh, std::string& msg);
+Plan make_plan(int C, const upipe_shape_t& sh);
+
+// Workspace layout: byte offsets into the caller's workspace for one pass.
+struct FwdWs {
+  size_t qsend, qrecv, ksend, krecv, vsend, vrecv, osend, orecv, yacc, total;
+};
+struct BwdWs {
+  size_t qsend, qrecv, ksend, krecv, vsend, vrecv, dosend, dorecv, dsend, drecv, dqacc, dqsend, dqrecv, dkacc,
+      dvacc, dksend, dvsend, dkrecv, dvrecv, dxacc, total;
+};
+FwdWs fwd_workspace(const Plan& p);
+BwdWs bwd_workspace(const Plan& p);
+
+// ------------------------------------------------------------------ transport
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  virtual int size() const = 0;
+  virtual int rank() const = 0;
+  // Equal-block all-to-all: block p of `send` (bytes at send + p*bytes) goes to rank p, which stores
+  // it as block `rank()` of its `recv`. send and recv must not overlap (except C == 1).
+  virtual upipe_status_t alltoall(const void* send, void* recv, size_t bytes, cudaStream_t s, std::string& err) = 0;
+  virtual upipe_status_t allreduce_sum_f32(float* buf, size_t n, cudaStream_t s, std::string& err) = 0;
+};
+
+std::unique_ptr<Transport> make_self_transport();
+std::unique_ptr<Transport> make_nccl_transport(const uint8_t* uid, int C, int rank, std::string& err);
+std::unique_ptr<Transport> make_fabric_transport(upipe_fabric_t f, int rank, int device, std::string& err);
+
+}  // namespace upipe
+
+struct upipe_ctx_s {
+  int device = 0;
+  int C = 1, rank = 0;
+  uint32_t flags = 0;
+  std::unique_ptr<upipe::Transport> transport;
+  std::string last_error;
+  bool alive = true;
+};

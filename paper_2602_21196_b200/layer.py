@@ -1,0 +1,91 @@
+"""User-facing wrapper of the UPipe layer: owns a libupipe context and the
+workspace (allocated from the PyTorch caching allocator so it shows up in
+``torch.cuda.max_memory_allocated``). Marshalling only; the math runs in libupipe.
+
+    attn = UPipeAttention(n_q_heads=32, n_kv_heads=8, head_dim=128, hidden=4096,
+                          chunk_heads=8, process_group=pg)      # CP group = pg
+    y, saved = attn.forward(x_shard, wq, wk, wv, wo)
+    dx, dwq, dwk, dwv, dwo = attn.backward(x_shard, wq, wk, wv, wo, dy, saved)
+"""
+from __future__ import annotations
+
+import torch
+
+from . import upipe as U
+
+
+class UPipeAttention:
+    def __init__(self, n_q_heads: int, n_kv_heads: int, head_dim: int, hidden: int, chunk_heads: int,
+                 causal: bool = True, process_group=None, device=None, fabric=None, cp_rank: int | None = None,
+                 cp_size: int | None = None):
+        """CP group: ``process_group`` (torch.distributed, one process per GPU, NCCL transport),
+        or ``fabric`` + ``cp_rank`` + ``cp_size`` (single-process group driven by one host thread per rank),
+        or neither (C = 1)."""
+        self.Hq, self.Hkv, self.d, self.D, self.U = n_q_heads, n_kv_heads, head_dim, hidden, chunk_heads
+        self.causal = int(causal)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        if fabric is not None:
+            self.C = cp_size
+            self.ctx = U.upipe_init_local(fabric, cp_rank, dev_index)
+            self.rank = cp_rank
+        elif process_group is not None:
+            import torch.distributed as dist
+            self.C = dist.get_world_size(process_group)
+            self.rank = dist.get_rank(process_group)
+            obj = [U.upipe_get_unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(process_group, 0), group=process_group)
+            self.ctx = U.upipe_init(obj[0], self.C, self.rank, dev_index)
+        else:
+            self.C, self.rank = 1, 0
+            self.ctx = U.upipe_init(None, 1, 0, dev_index)
+        self._ws = {}
+
+    def shape(self, seq_local: int) -> U.upipe_shape_t:
+        return U.make_shape(seq_local, self.D, self.Hq, self.Hkv, self.d, self.U, self.causal)
+
+    def workspace(self, seq_local: int, pass_: int) -> torch.Tensor:
+        key = (seq_local, pass_)
+        if key not in self._ws:
+            n = U.upipe_workspace_size(self.C, self.shape(seq_local), pass_)
+            self._ws[key] = torch.empty(max(n, 256), dtype=torch.uint8, device=self.device)
+        return self._ws[key]
+
+    def release_workspace(self):
+        self._ws.clear()
+
+    def forward(self, x, wq, wk, wv, wo, stream=None):
+        S_l = x.shape[0]
+        sh = self.shape(S_l)
+        y = torch.empty((S_l, self.D), dtype=torch.bfloat16, device=x.device)
+        o_saved = torch.empty((S_l, self.Hq * self.d), dtype=torch.bfloat16, device=x.device)
+        lse = torch.empty((self.Hq // self.C, S_l * self.C), dtype=torch.float32, device=x.device)
+        ws = self.workspace(S_l, 0)
+        U.upipe_attn_fwd(self.ctx, sh, x, wq, wk, wv, wo, y, o_saved, lse, ws, stream=stream)
+        return y, (o_saved, lse)
+
+    def backward(self, x, wq, wk, wv, wo, dy, saved, reduce_dw: bool = True, stream=None):
+        o_saved, lse = saved
+        S_l = x.shape[0]
+        sh = self.shape(S_l)
+        dx = torch.empty_like(x)
+        dwq = torch.empty(wq.shape, dtype=torch.float32, device=x.device)
+        dwk = torch.empty(wk.shape, dtype=torch.float32, device=x.device)
+        dwv = torch.empty(wv.shape, dtype=torch.float32, device=x.device)
+        dwo = torch.empty(wo.shape, dtype=torch.float32, device=x.device)
+        ws = self.workspace(S_l, 1)
+        U.upipe_attn_bwd(self.ctx, sh, x, wq, wk, wv, wo, dy, o_saved, lse, dx, dwq, dwk, dwv, dwo, reduce_dw, ws,
+                         stream=stream)
+        return dx, dwq, dwk, dwv, dwo
+
+    def close(self):
+        if self.ctx is not None:
+            U.upipe_finalize(self.ctx)
+            self.ctx = None
+        self._ws.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,112 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every symbol
+include/upipe.h declares, validates shapes with named constraints, and its
+planner (closed-form GQA schedule, workspace layout) agrees with the oracle's
+independently written schedule and the closed forms of DESIGN A22."""
+import os
+import re
+import subprocess
+
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "upipe.h")
+
+
+@pytest.fixture(scope="module")
+def U():
+    from paper_2602_21196_b200 import upipe
+    upipe.lib()
+    return upipe
+
+
+def header_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"UPIPE_API\s+[\w\s\*]*?\b(upipe_\w+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol(U):
+    syms = header_symbols()
+    assert len(syms) >= 15
+    out = subprocess.run(["nm", "-D", "--defined-only", U.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (upipe_\w+)", out))
+    assert set(syms) <= exported, set(syms) - exported
+    assert set(U.EXPORTED) == set(syms)
+    for s in syms:
+        assert hasattr(U.lib(), s)
+
+
+def test_kernels_are_sm100a_tcgen05(U):
+    sass = subprocess.run(["cuobjdump", "-sass", U.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass or "UTCMMA" in sass, "no tcgen05 MMA in libupipe"
+    assert "UTMALDG" in sass, "no TMA loads in libupipe"
+    assert "LDTM" in sass
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", U.LIB_PATH], capture_output=True, text=True).stdout
+
+
+def test_status_strings(U):
+    assert U.upipe_status_string(0) == "UPIPE_OK"
+    assert U.upipe_status_string(5) == "UPIPE_ERR_WORKSPACE"
+
+
+@pytest.mark.parametrize("args,status,needle", [
+    ((2, 256, 512, 8, 2, 64, 3), 1, "P:317"),          # U % C
+    ((2, 256, 512, 8, 2, 64, 6), 1, "n_q_heads % chunk_heads"),
+    ((4, 256, 512, 8, 2, 64, 4), 2, "n_kv_heads % cp_size"),
+    ((1, 256, 512, 8, 2, 96, 2), 2, "head_dim"),
+    ((1, 256, 500, 8, 2, 64, 2), 2, "hidden"),
+    ((1, 0, 512, 8, 2, 64, 2), 1, "seq_local"),
+    ((1, 256, 512, 8, 3, 64, 2), 1, "S:37"),
+    ((2, 256, 512, 24, 2, 64, 10), 1, "n_q_heads % chunk_heads"),
+])
+def test_validation_names_constraint(U, args, status, needle):
+    C, *sh = args
+    st, msg = U.upipe_validate(C, U.make_shape(*sh))
+    assert st == status and needle in msg, (st, msg)
+
+
+GRID = [(Hq, Hkv, C, Uc) for Hq, Hkv in ((8, 2), (16, 4), (32, 8), (64, 8), (8, 8), (32, 32))
+        for C in (1, 2, 4, 8) for Uc in range(C, Hq + 1, C)
+        if Hkv % C == 0 and Hq % Uc == 0 and ((Uc // C) % (Hq // Hkv) == 0 or (Hq // Hkv) % (Uc // C) == 0)]
+
+
+@pytest.mark.parametrize("Hq,Hkv,C,Uc", GRID)
+def test_planner_matches_oracle_schedule(U, Hq, Hkv, C, Uc):
+    sh = U.make_shape(128, 256, Hq, Hkv, 64, Uc)
+    stages = oracle.gqa_schedule(Hq, Hkv, C, Uc)
+    info0 = U.upipe_plan_stage(C, sh, 0, 0)
+    assert info0.n_stages == len(stages)
+    for s, st in enumerate(stages):
+        for p in range(C):
+            info = U.upipe_plan_stage(C, sh, s, p)
+            assert list(range(info.q0, info.q0 + info.qpd)) == st.q_heads[p]
+            assert list(range(info.kv0, info.kv0 + info.kv_res)) == st.kv_heads[p]
+            assert bool(info.kv_sent) == bool(st.kv_sent[p])
+
+
+def test_workspace_closed_forms(U):
+    # forward chunk buffers (DESIGN A21/A22): UPipe holds U q heads and C*kv_res kv heads, send + recv
+    S_l, D, d = 4096, 4096, 128
+    for C, Uc, Hq, Hkv in ((8, 8, 32, 8), (8, 16, 32, 8), (8, 32, 32, 8), (8, 8, 64, 8), (4, 4, 32, 8)):
+        sh = U.make_shape(S_l, D, Hq, Hkv, d, Uc)
+        fwd = U.upipe_workspace_size(C, sh, 0)
+        qpd = Uc // C
+        R = Hq // Hkv
+        kv_res = max(1, qpd // R)
+        S = S_l * C
+        chunk = 2 * S * d * (2 * qpd + 2 * 2 * kv_res)          # Q,K,V send+recv (bf16)
+        o_bufs = 2 * 2 * S * qpd * d                             # O send+recv
+        yacc = 4 * S_l * D if Hq // Uc > 1 else 0
+        assert abs(fwd - (chunk + o_bufs + yacc)) <= 256 * 12
+        # Q-path (DESIGN A22) scales exactly with U: ratio vs Ulysses = U/Hq
+    shu = U.make_shape(S_l, D, 32, 8, d, 32)
+    shp = U.make_shape(S_l, D, 32, 8, d, 8)
+    assert U.upipe_workspace_size(8, shp, 0) < U.upipe_workspace_size(8, shu, 0)
+
+
+def test_workspace_c1_aliases_send_and_recv(U):
+    sh = U.make_shape(1024, 512, 8, 2, 64, 2)
+    w1 = U.upipe_workspace_size(1, sh, 0)
+    # C=1: Q,K,V single buffers (no a2a), no O buffers, + y accumulator
+    assert w1 == 1024 * 64 * 2 * (2 + 1 + 1) + 1024 * 512 * 4   # qpd=2 q heads, kv_res=1 K and V

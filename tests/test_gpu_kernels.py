@@ -1,0 +1,117 @@
+"""Per-kernel parity of the sm_100a kernels against the fp64 oracle on identical
+bf16 inputs (SURVEY §8c c.4 "sharp diagnostic gate"). Calls go through the C ABI."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import assert_close, dev, to_bf16, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def U():
+    from paper_2602_21196_b200 import upipe
+    upipe.lib()
+    return upipe
+
+
+# tolerances (tests/README in DESIGN.md §Parity): a single bf16 output rounding is 2^-9/sqrt(3) ~ 1.1e-3 relative
+GEMM_BF16_REL = 1.5e-3
+GEMM_F32_REL = 1e-5
+ATTN_REL = 3e-3        # O, dV
+ATTN_GRAD_REL = 4e-3   # dQ, dK (fp32 atomics + bf16 P/dS)
+ABS = 2e-2
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (300, 192, 256), (1024, 512, 4096), (257, 1024, 512)])
+def test_gemm_xwT(U, M, N, K):
+    x = synth.draw(1, 21, (M, K), 0)
+    w = synth.draw(1, 22, (N, K), -4)
+    X, W = to_bf16(x), to_bf16(w)
+    want = oracle.project(x, w)
+    y32 = torch.empty((M, N), dtype=torch.float32, device=dev())
+    U.upipe_gemm_xwT(X, W, y32, M, N, K, mode=1)
+    y16 = torch.empty((M, N), dtype=torch.bfloat16, device=dev())
+    U.upipe_gemm_xwT(X, W, y16, M, N, K, mode=0)
+    torch.cuda.synchronize()
+    assert_close("gemm f32", to_np(y32), want, GEMM_F32_REL, 1e-3)
+    assert_close("gemm bf16", to_np(y16), want, GEMM_BF16_REL, ABS)
+
+
+def _core(S, Hq, Hkv, d, score_std, seed=0):
+    c = synth.core_inputs(seed, S, Hq, Hkv, d, score_std)
+    return c
+
+
+def _run_fwd(U, c, S, Hq, Hkv, d, causal):
+    q, k, v = to_bf16(c["q"]), to_bf16(c["k"]), to_bf16(c["v"])
+    o = torch.empty((S, Hq, d), dtype=torch.bfloat16, device=dev())
+    lse = torch.empty((Hq, S), dtype=torch.float32, device=dev())
+    U.upipe_attn_core_fwd(q, k, v, o, lse, S, Hq, Hkv, d, causal, Hq * d, Hkv * d, Hq * d, S)
+    return q, k, v, o, lse
+
+
+FWD_CASES = [(128, 1, 1, 64, 1), (200, 2, 1, 64, 1), (512, 4, 1, 128, 1), (1000, 8, 2, 128, 1),
+             (384, 2, 2, 64, 0), (333, 4, 2, 128, 0), (2048, 2, 1, 128, 1)]
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,d,causal", FWD_CASES)
+def test_attn_fwd(U, S, Hq, Hkv, d, causal):
+    c = _core(S, Hq, Hkv, d, 1.0)
+    _, _, _, o, lse = _run_fwd(U, c, S, Hq, Hkv, d, causal)
+    torch.cuda.synchronize()
+    O, L = oracle.attn_fwd(c["q"], c["k"], c["v"], causal=bool(causal))
+    assert_close("O", to_np(o), O, ATTN_REL, ABS)
+    assert_close("lse", to_np(lse), L, 1e-4, 2e-4)
+
+
+def test_attn_fwd_causal_perturbation_bitwise(U):
+    S, Hq, Hkv, d, t = 640, 2, 1, 128, 300
+    c = _core(S, Hq, Hkv, d, 1.0)
+    _, _, _, o1, l1 = _run_fwd(U, c, S, Hq, Hkv, d, 1)
+    c2 = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in c.items()}
+    c2["k"][t:] = synth.draw(9, 12, c2["k"][t:].shape, 0)
+    c2["v"][t:] = synth.draw(9, 13, c2["v"][t:].shape, 0)
+    _, _, _, o2, l2 = _run_fwd(U, c2, S, Hq, Hkv, d, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(o1[:t], o2[:t])
+    assert torch.equal(l1[:, :t], l2[:, :t])
+    assert not torch.equal(o1[t:], o2[t:])
+
+
+BWD_CASES = [(128, 1, 1, 64, 1), (200, 2, 1, 64, 1), (512, 4, 1, 128, 1), (640, 4, 2, 128, 1),
+             (384, 2, 2, 64, 0), (1024, 2, 1, 128, 1)]
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,d,causal", BWD_CASES)
+def test_attn_bwd(U, S, Hq, Hkv, d, causal):
+    c = _core(S, Hq, Hkv, d, 1.0)
+    q, k, v, o, lse = _run_fwd(U, c, S, Hq, Hkv, d, causal)
+    do = to_bf16(c["do"])
+    delta = torch.empty((S, Hq), dtype=torch.float32, device=dev())
+    U.upipe_rowdot(do, Hq * d, o, Hq * d, delta, Hq, S, Hq, d)
+    dq = torch.zeros((S, Hq, d), dtype=torch.float32, device=dev())
+    dk = torch.empty((S, Hkv, d), dtype=torch.float32, device=dev())
+    dv = torch.empty((S, Hkv, d), dtype=torch.float32, device=dev())
+    U.upipe_attn_core_bwd(q, k, v, do, lse, delta, dq, dk, dv, S, Hq, Hkv, d, causal, Hq * d, Hkv * d, Hq * d, S, Hq)
+    torch.cuda.synchronize()
+    # rowdot against the oracle's D on the kernel's bf16 O (same inputs)
+    assert_close("delta", to_np(delta), oracle.rowdot(c["do"], to_np(o)), 1e-5, 1e-4)
+    dQ, dK, dV = oracle.attn_bwd(c["q"], c["k"], c["v"], c["do"], causal=bool(causal))
+    assert_close("dV", to_np(dv), dV, ATTN_REL, ABS)
+    assert_close("dQ", to_np(dq), dQ, ATTN_GRAD_REL, ABS)
+    assert_close("dK", to_np(dk), dK, ATTN_GRAD_REL, ABS)
+
+
+def test_synth_device_generator_bitwise(U):
+    n, seed, tid, e, start = 100003, 5, 3, -4, 12345
+    t = torch.empty(n, dtype=torch.bfloat16, device=dev())
+    U.upipe_synth_fill_bf16(t, n, seed, tid, e, start)
+    torch.cuda.synchronize()
+    host = synth.draw(seed, tid, (n,), e, start=start)
+    assert np.array_equal(to_np(t), host)

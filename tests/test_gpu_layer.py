@@ -1,0 +1,145 @@
+"""Layer-level parity: upipe_attn_fwd/bwd (through the C ABI) against the fp64
+oracle on the same seeded inputs, at C = 1 (one process) and C = 2/4 (the
+single-process fabric: one host thread + stream per CP rank on one GPU).
+Bar (BASELINE north_star): max|d| <= 2e-2 and relative L2 <= 5e-3 for y, dx, dW*."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import assert_close, dev, to_bf16, to_np
+
+pytestmark = pytest.mark.gpu
+
+REL, ABS = 5e-3, 2e-2
+
+
+def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", bwd=True):
+    """Run the layer on C ranks; returns (per-rank outputs, inputs)."""
+    from paper_2602_21196_b200 import UPipeAttention, upipe
+    inp = synth.layer_inputs(seed, S, D, Hq, Hkv, d, profile)
+    S_l = S // C
+    W = {k: to_bf16(inp[k]) for k in ("wq", "wk", "wv", "wo")}
+    xs = [to_bf16(inp["x"][r * S_l:(r + 1) * S_l]) for r in range(C)]
+    dys = [to_bf16(inp["dy"][r * S_l:(r + 1) * S_l]) for r in range(C)]
+    results = [None] * C
+    errors = []
+    fabric = upipe.upipe_fabric_create(C) if C > 1 else None
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                if C > 1:
+                    attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal, fabric=fabric, cp_rank=r, cp_size=C)
+                else:
+                    attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal)
+                y, saved = attn.forward(xs[r], W["wq"], W["wk"], W["wv"], W["wo"])
+                out = {"y": y, "o": saved[0], "lse": saved[1]}
+                if bwd:
+                    dx, dwq, dwk, dwv, dwo = attn.backward(xs[r], W["wq"], W["wk"], W["wv"], W["wo"], dys[r], saved)
+                    out.update(dx=dx, dwq=dwq, dwk=dwk, dwv=dwv, dwo=dwo)
+                stream.synchronize()
+                results[r] = {k: v.clone() for k, v in out.items()}
+                attn.close()
+        except Exception as e:  # surfaced below
+            errors.append((r, e))
+
+    if C == 1:
+        rank_main(0)
+    else:
+        th = [threading.Thread(target=rank_main, args=(r,)) for r in range(C)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        upipe.upipe_fabric_destroy(fabric)
+    if errors:
+        raise errors[0][1]
+    return results, inp
+
+
+def _check(results, inp, C, Hq, Hkv, d, U, causal=True, bwd=True):
+    x, wq, wk, wv, wo, dy = (inp[k] for k in ("x", "wq", "wk", "wv", "wo", "dy"))
+    Y, O, L = oracle.layer_fwd(x, wq, wk, wv, wo, Hq, Hkv, d, causal)
+    y = np.concatenate([to_np(r["y"]) for r in results], 0)
+    o = np.concatenate([to_np(r["o"]) for r in results], 0)
+    assert_close("y", y, Y, REL, ABS)
+    assert_close("o_saved", o, O, REL, ABS)
+    # lse: rank p holds its heads in slot order s*qpd + j (upipe.h)
+    from paper_2602_21196_b200 import upipe
+    sh = upipe.make_shape(x.shape[0] // C, x.shape[1], Hq, Hkv, d, U, int(causal))
+    info = upipe.upipe_plan_stage(C, sh, 0, 0)
+    for p in range(C):
+        lse_p = to_np(results[p]["lse"])
+        for s in range(info.n_stages):
+            q0 = upipe.upipe_plan_stage(C, sh, s, p).q0
+            for j in range(info.qpd):
+                assert_close(f"lse[p{p},h{q0 + j}]", lse_p[s * info.qpd + j], L[q0 + j], 1e-4, 2e-4)
+    if not bwd:
+        return
+    dX, dWq, dWk, dWv, dWo = oracle.layer_bwd(x, wq, wk, wv, wo, dy, Hq, Hkv, d, causal)
+    dx = np.concatenate([to_np(r["dx"]) for r in results], 0)
+    assert_close("dx", dx, dX, REL, ABS)
+    for name, want in (("dwq", dWq), ("dwk", dWk), ("dwv", dWv), ("dwo", dWo)):
+        for p in range(C):   # reduce_dw: every rank holds the sum over the CP group
+            assert_close(f"{name}[rank {p}]", to_np(results[p][name]), want, REL, ABS)
+
+
+# BASELINE configs[0]: S=512, 8 Q / 2 KV heads, d=64, hidden 512, CP=2, chunk=2 heads
+def test_config1_cp2_chunk2():
+    r, inp = _run_group(2, 512, 512, 8, 2, 64, 2)
+    _check(r, inp, 2, 8, 2, 64, 2)
+
+
+@pytest.mark.parametrize("U", [1, 2, 4, 8])
+def test_config1_shape_cp1_all_chunks(U):
+    r, inp = _run_group(1, 512, 512, 8, 2, 64, U)
+    _check(r, inp, 1, 8, 2, 64, U)
+
+
+@pytest.mark.parametrize("C,U", [(2, 8), (4, 4), (4, 8), (2, 4)])
+def test_config1_shape_cp_grid(C, U):
+    r, inp = _run_group(C, 512, 512, 8, 2, 64, U)
+    _check(r, inp, C, 8, 2, 64, U)
+
+
+def test_ragged_tail_cp2():
+    # S_l = 200 is not a multiple of the 128-row tile: partial tiles on every rank
+    r, inp = _run_group(2, 400, 256, 4, 2, 64, 2)
+    _check(r, inp, 2, 4, 2, 64, 2)
+
+
+def test_llama_shaped_small_cp1():
+    # Llama3-8B head shape (32 Q / 8 KV, d=128, hidden 4096) at S=1024, U=8 (paper U=C setting)
+    r, inp = _run_group(1, 1024, 4096, 32, 8, 128, 8)
+    _check(r, inp, 1, 32, 8, 128, 8)
+
+
+def test_llama_shaped_cp4_u4():
+    r, inp = _run_group(4, 1024, 1024, 32, 8, 128, 4, bwd=True)
+    _check(r, inp, 4, 32, 8, 128, 4)
+
+
+def test_non_causal_cp2():
+    r, inp = _run_group(2, 256, 256, 4, 2, 128, 2, causal=False)
+    _check(r, inp, 2, 4, 2, 128, 2, causal=False)
+
+
+def test_ulysses_equals_upipe_bitwise_forward():
+    # U = Hq (Ulysses) and U = C (UPipe) produce bitwise-identical O and y-inputs per head
+    ru, _ = _run_group(2, 512, 512, 8, 2, 64, 8, bwd=False)
+    rp, _ = _run_group(2, 512, 512, 8, 2, 64, 2, bwd=False)
+    for p in range(2):
+        assert torch.equal(ru[p]["o"], rp[p]["o"])
+
+
+def test_invalid_shape_named_error():
+    from paper_2602_21196_b200 import upipe
+    attn_shape = upipe.make_shape(256, 512, 8, 2, 64, 3, 1)   # U=3 not divisible by C=2
+    st, msg = upipe.upipe_validate(2, attn_shape)
+    assert st == 1 and "P:317" in msg
