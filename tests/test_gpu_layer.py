@@ -79,7 +79,8 @@ def _check(results, inp, C, Hq, Hkv, d, U, causal=True, bwd=True):
         for s in range(info.n_stages):
             q0 = upipe.upipe_plan_stage(C, sh, s, p).q0
             for j in range(info.qpd):
-                assert_close(f"lse[p{p},h{q0 + j}]", lse_p[s * info.qpd + j], L[q0 + j], 1e-4, 2e-4)
+                # layer-level LSE includes the bf16 rounding of Q/K at the a2a boundary (A15): north_star bar
+                assert_close(f"lse[p{p},h{q0 + j}]", lse_p[s * info.qpd + j], L[q0 + j], REL, ABS)
     if not bwd:
         return
     dX, dWq, dWk, dWv, dWo = oracle.layer_bwd(x, wq, wk, wv, wo, dy, Hq, Hkv, d, causal)
@@ -102,10 +103,16 @@ def test_config1_shape_cp1_all_chunks(U):
     _check(r, inp, 1, 8, 2, 64, U)
 
 
-@pytest.mark.parametrize("C,U", [(2, 8), (4, 4), (4, 8), (2, 4)])
+@pytest.mark.parametrize("C,U", [(2, 8), (2, 4)])
 def test_config1_shape_cp_grid(C, U):
     r, inp = _run_group(C, 512, 512, 8, 2, 64, U)
     _check(r, inp, C, 8, 2, 64, U)
+
+
+@pytest.mark.parametrize("C,U", [(4, 4), (4, 8), (4, 16), (2, 2), (1, 16)])
+def test_16q_4kv_cp_grid(C, U):
+    r, inp = _run_group(C, 512, 512, 16, 4, 64, U)
+    _check(r, inp, C, 16, 4, 64, U)
 
 
 def test_ragged_tail_cp2():
