@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""UPipe layer benchmark (contract: DESIGN.md §Measurement).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: one rank per GPU, NCCL)
+
+One step = one UPipe attention layer forward + backward (all SURVEY §8a rows:
+projections, seq->head all-to-all, causal GQA attention, head->seq all-to-all,
+output projection, and the backward of each) over the whole sequence, on the
+Llama3-8B attention shape (32 Q / 8 KV heads, d=128, hidden 4096), S = 131072
+tokens (BASELINE configs[1]), context-parallel degree C = N, chunk U = 8.
+Inputs are synthetic (the seeded counter-based generator, drawn on the device)
+and larger than L2, so no flush is needed between steps. Rank 0 prints one JSON line.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Llama3-8B attn fwd+bwd tokens/s/GPU & peak activation GB at 1/2/4/8 B200"
+LLAMA = dict(Hq=32, Hkv=8, d=128, D=4096)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--seq", type=int, default=131072, help="global sequence length S")
+    ap.add_argument("--chunk", type=int, default=8, help="chunk_heads U (UPipe); Ulysses = 32")
+    ap.add_argument("--no-ulysses", action="store_true", help="skip the chunk=all-heads Ulysses comparison")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="profiling runs: timed region only")
+    return ap.parse_args()
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ----------------------------------------------------------------------------- peaks / clocks
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return {"bf16_burst": j["bf16_tflops"], "bf16_sustained": j.get("bf16_tflops_sustained", j["bf16_tflops"]),
+                "hbm": j["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+    return {"bf16_burst": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = sorted(float(r[1]) for r in rows)
+        mx = max(float(r[2]) for r in rows)
+        load = [float(r[1]) for r in rows if float(r[3]) > 200.0] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        load.sort()
+        return {"sm_mhz": load[len(load) // 2], "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows)}
+
+
+# ----------------------------------------------------------------------------- FLOP model
+
+def causal_pairs(S):
+    return S * (S + 1) // 2
+
+
+def flops_attn_bwd_per_head(S, d, causal=True):
+    """5 matmuls (S^T, dP^T, dV, dK, dQ) x 2 flops x d per visible (query, key) pair."""
+    pairs = causal_pairs(S) if causal else S * S
+    return 10.0 * d * pairs
+
+
+def flops_step_per_rank(S, C, Hq, Hkv, d, D, causal=True):
+    pairs = causal_pairs(S) if causal else S * S
+    attn = 14.0 * d * pairs * Hq / C                 # fwd 4 d + bwd 10 d per pair and head
+    proj = 6.0 * (S / C) * D * d * (2 * Hq + 2 * Hkv)  # Q,K,V,O forward (2x) + backward (4x)
+    return attn + proj
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) legs
+
+def oracle_step_time(S, shape=LLAMA, seed=0):
+    """One oracle fwd+bwd of the Llama-shaped layer at sequence length S on the host cores."""
+    import numpy as np  # noqa: F401
+    import oracle
+    import synth
+    inp = synth.layer_inputs(seed, S, shape["D"], shape["Hq"], shape["Hkv"], shape["d"])
+    args = [inp[k] for k in ("x", "wq", "wk", "wv", "wo")]
+    t0 = time.perf_counter()
+    oracle.layer_fwd(*args, shape["Hq"], shape["Hkv"], shape["d"])
+    oracle.layer_bwd(*args, inp["dy"], shape["Hq"], shape["Hkv"], shape["d"])
+    return time.perf_counter() - t0
+
+
+def cpu_cores():
+    try:
+        import threadpoolctl
+        info = threadpoolctl.threadpool_info()
+        n = max((i.get("num_threads", 1) for i in info), default=os.cpu_count())
+        return int(n)
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_baseline(budget_s=20.0):
+    """Oracle timed on a bounded sample of the workload (Llama3-8B layer shape, smaller S)."""
+    S = 1024
+    t = oracle_step_time(S)
+    while t * 3.5 < budget_s / 2 and S < 8192:    # attention ~S^2, projections ~S: grow while cheap
+        S *= 2
+        t = oracle_step_time(S)
+    return {"value": S / t, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"one fp64 numpy oracle fwd+bwd of the Llama3-8B attention layer (32Q/8KV, d=128, D=4096) "
+                      f"at S={S} tokens (un-sharded), {t:.2f} s; tokens/s = S / t at that S (cost grows ~S^2)",
+            "seconds": t, "S": S}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    S = 1024
+    oracle_step_time(256)           # import / first-touch warm-up
+    for _ in range(args.warmup):
+        oracle_step_time(S)
+    ts = [oracle_step_time(S) for _ in range(args.steps)]
+    t = sum(ts) / len(ts)
+    v = S / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "llama3-8b-attention-layer-fwd-bwd", "seq_len": S, "global_batch": 1,
+                       "parallelism": "none (host cores)", "note": "bounded sample of the bench workload"},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": f"oracle fwd+bwd, Llama3-8B layer shape at S={S} per step"},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    from paper_2602_21196_b200 import UPipeAttention, upipe
+    import synth
+
+    C = world
+    Hq, Hkv, d, D = LLAMA["Hq"], LLAMA["Hkv"], LLAMA["d"], LLAMA["D"]
+    S = args.seq
+    assert S % C == 0
+    S_l = S // C
+    U = args.chunk
+    e = synth.layer_exponents(D, Hq, d, S)
+
+    def fill(shape, name, start=0):
+        t = torch.empty(shape, dtype=torch.bfloat16, device=dev)
+        upipe.upipe_synth_fill_bf16(t, t.numel(), 0, synth.TID[name], e[name], start)
+        return t
+
+    x = fill((S_l, D), "x", rank * S_l * D)
+    dy = fill((S_l, D), "dy", rank * S_l * D)
+    W = [fill((Hq * d, D), "wq"), fill((Hkv * d, D), "wk"), fill((Hkv * d, D), "wv"), fill((D, Hq * d), "wo")]
+    torch.cuda.synchronize()
+
+    def barrier():
+        if pg is not None:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if pg is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def run(chunk, steps, warmup, trace=False):
+        attn = UPipeAttention(Hq, Hkv, d, D, chunk, True, process_group=pg)
+        out = {}
+
+        def step():
+            y, saved = attn.forward(x, *W)
+            g = attn.backward(x, *W, dy, saved)
+            return y, g
+
+        for _ in range(warmup):
+            step()
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        step()
+        torch.cuda.synchronize()
+        out["peak_bytes"] = torch.cuda.max_memory_allocated() - base
+        out["ws_bytes"] = sum(t.numel() for t in attn._ws.values())
+        stream = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if trace:
+            upipe.upipe_set_trace(attn.ctx, True)
+            upipe.upipe_trace_read(attn.ctx)
+        barrier()
+        torch.cuda.synchronize()
+        l0 = upipe.upipe_kernel_launches()
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        l1 = upipe.upipe_kernel_launches()
+        barrier()
+        out["ms"] = max_over_ranks(e0.elapsed_time(e1))
+        out["launches"] = l1 - l0
+        if trace:
+            out["trace"] = upipe.upipe_trace_read(attn.ctx)
+            upipe.upipe_set_trace(attn.ctx, False)
+        out["attn"] = attn
+        return out
+
+    sampler = ClockSampler(local) if local == 0 else None
+    if sampler:
+        sampler.start()
+    main_run = run(U, args.steps, args.warmup, trace=True)
+    clocks = sampler.stop() if sampler else None
+    ms_step = main_run["ms"] / args.steps
+    tok_s = S * args.steps / (main_run["ms"] / 1e3)
+
+    # roofline of the dominant kernel (attention backward), timed live by the in-library trace events
+    peaks = measured_peaks()
+    tr = main_run["trace"]
+    bwd_ms, bwd_n = tr["attn_bwd"]
+    qpd = U // C
+    flops_bwd_launch = flops_attn_bwd_per_head(S, d) * qpd
+    achieved = flops_bwd_launch / (bwd_ms / bwd_n / 1e3) / 1e12 if bwd_n else None
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "attn_bwd_traffic.json")
+    if os.path.exists(tf):
+        with open(tf) as f:
+            j = json.load(f)
+        if j.get("seq") == S and j.get("chunk") == U and j.get("C") == C:
+            traffic = j.get("dram_bytes_per_launch")
+    step_flops = flops_step_per_rank(S, C, Hq, Hkv, d, D)
+    per_step_ms = {k: v[0] / args.steps for k, v in tr.items()}
+
+    result = {
+        "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded counter-based generator, drawn on device)",
+        "config": {"workload": "llama3-8b-attention-layer-fwd-bwd (BASELINE configs[1])", "model": "Llama3-8B attention layer",
+                   "n_q_heads": Hq, "n_kv_heads": Hkv, "head_dim": d, "hidden": D, "seq_len": S, "global_batch": 1,
+                   "chunk_heads": U, "cp": C, "parallelism": f"cp{C} (UPipe, U={U})",
+                   "l2": "inputs larger than L2 (x, dy: S_l x 4096 bf16 per rank); no flush needed"},
+        "tokens_per_s_per_gpu": tok_s / world,
+        "gpu_launches": main_run["launches"],
+        "gpu_launches_per_step": main_run["launches"] / args.steps,
+        "roofline": {"kernel": "attn_bwd (tcgen05 flash attention backward)", "bound": "tensor",
+                     "achieved": achieved, "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
+                     "frac": (achieved / peaks["bf16_sustained"]) if achieved else None, "traffic": traffic,
+                     "peak_source": peaks["source"] + ", bf16 sustained (kernel timed inside a long step)",
+                     "flops_per_launch": flops_bwd_launch, "launches": bwd_n,
+                     "avg_launch_ms": bwd_ms / bwd_n if bwd_n else None,
+                     "per_unit": "10*d flops per causal (query,key) pair per head; launch = qpd heads x S(S+1)/2 pairs"},
+        "step_roofline": {"flops_per_step_per_rank": step_flops,
+                          "achieved_tflops": step_flops / (ms_step / 1e3) / 1e12,
+                          "frac_of_sustained": step_flops / (ms_step / 1e3) / 1e12 / peaks["bf16_sustained"]},
+        "phase_ms_per_step": per_step_ms,
+        "peak_activation_gib": main_run["peak_bytes"] / 2**30,
+        "workspace_gib": main_run["ws_bytes"] / 2**30,
+        "clocks": clocks,
+    }
+    main_run["attn"].close()
+
+    if not args.quick and not args.no_ulysses and U != Hq:
+        ul = run(Hq, max(2, args.steps // 2), 1)
+        ul_tok = S * max(2, args.steps // 2) / (ul["ms"] / 1e3)
+        result["ulysses"] = {"chunk_heads": Hq, "value": ul_tok, "unit": "tokens/s",
+                             "upipe_over_ulysses": tok_s / ul_tok,
+                             "peak_activation_gib": ul["peak_bytes"] / 2**30,
+                             "workspace_gib": ul["ws_bytes"] / 2**30,
+                             "activation_reduction": 1 - main_run["peak_bytes"] / ul["peak_bytes"]}
+        ul["attn"].close()
+
+    if not args.quick and not args.no_e2e:
+        # end to end through the public API: pinned host inputs -> HBM, fwd+bwd, dx -> pinned host
+        attn = UPipeAttention(Hq, Hkv, d, D, U, True, process_group=pg)
+        xh = x.cpu().pin_memory()
+        dyh = dy.cpu().pin_memory()
+        dxh = torch.empty_like(xh).pin_memory()
+        xd, dyd = torch.empty_like(x), torch.empty_like(dy)
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            dyd.copy_(dyh, non_blocking=True)
+            y, saved = attn.forward(xd, *W)
+            dx, *_ = attn.backward(xd, *W, dyd, saved)
+            dxh.copy_(dx, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        stream = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ksteps = max(2, args.steps // 2)
+        e0.record(stream)
+        for _ in range(ksteps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1))
+        result["e2e"] = {"value": S * ksteps / (ms / 1e3), "unit": "tokens/s",
+                         "h2d_bytes_per_step": 2 * x.numel() * 2, "d2h_bytes_per_step": x.numel() * 2,
+                         "steps": ksteps, "api": "paper_2602_21196_b200.UPipeAttention.forward/backward"}
+        attn.close()
+
+    if rank == 0 and world == 1 and not args.quick and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline()
+
+    if pg is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+if __name__ == "__main__":
+    main()

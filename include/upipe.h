@@ -188,6 +188,26 @@ UPIPE_API upipe_status_t upipe_gemm_xwT(const upipe_bf16* x, const upipe_bf16* w
 UPIPE_API upipe_status_t upipe_synth_fill_bf16(upipe_bf16* dst, int64_t n, uint64_t seed, int tensor_id, int exponent,
                                      int64_t start, void* stream);
 
+/* ---------------------------------------------------------------- instrumentation */
+
+/* Kernel-launch counter: number of CUDA kernels this library has launched in the
+ * process so far (all contexts, including kernel-level entry points). */
+UPIPE_API upipe_status_t upipe_kernel_launches(uint64_t* count);
+
+/* Per-category device timing of the layer calls of one ctx. When tracing is on,
+ * every step of upipe_attn_fwd/bwd is bracketed by CUDA events recorded on the
+ * call's stream (the stream the kernels run on). upipe_trace_read waits for those
+ * events, returns accumulated milliseconds and counts per category since the last
+ * read, and clears them. Categories: */
+#define UPIPE_TRACE_GEMM 0      /* projection / output / gradient GEMMs (tcgen05) */
+#define UPIPE_TRACE_ATTN_FWD 1  /* attention forward kernel */
+#define UPIPE_TRACE_ATTN_BWD 2  /* attention backward kernel */
+#define UPIPE_TRACE_COMM 3      /* all-to-alls and the dW all-reduce */
+#define UPIPE_TRACE_AUX 4       /* rowdot, dQ convert, unpack, memsets */
+#define UPIPE_TRACE_NCAT 5
+UPIPE_API upipe_status_t upipe_set_trace(upipe_ctx_t ctx, int on);
+UPIPE_API upipe_status_t upipe_trace_read(upipe_ctx_t ctx, double ms[UPIPE_TRACE_NCAT], int64_t count[UPIPE_TRACE_NCAT]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -357,11 +357,13 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
         cudaFuncSetAttribute(attn_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<128>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
     attn_bwd_kernel<128><<<grid, 192, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, a);
+    count_launches(1);
   } else {
     static const cudaError_t attr =
         cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<64>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
     attn_bwd_kernel<64><<<grid, 192, BwdCfg<64>::SMEM, stream>>>(tq, tk, tv, tdo, a);
+    count_launches(1);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) snprintf(err, errlen, "attn_bwd launch: %s", cudaGetErrorString(e));

@@ -334,11 +334,13 @@ cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err
         cudaFuncSetAttribute(attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<128>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_fwd attr: %s", cudaGetErrorString(attr)); return attr; }
     attn_fwd_kernel<128><<<grid, 320, FwdCfg<128>::SMEM, stream>>>(tq, tk, tv, a);
+    count_launches(1);
   } else {
     static const cudaError_t attr =
         cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<64>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_fwd attr: %s", cudaGetErrorString(attr)); return attr; }
     attn_fwd_kernel<64><<<grid, 320, FwdCfg<64>::SMEM, stream>>>(tq, tk, tv, a);
+    count_launches(1);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) snprintf(err, errlen, "attn_fwd launch: %s", cudaGetErrorString(e));

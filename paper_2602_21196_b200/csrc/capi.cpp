@@ -3,6 +3,7 @@
 #include <nccl.h>
 
 #include <cstdio>
+#include <atomic>
 #include <new>
 
 #include "kernels.h"
@@ -16,6 +17,11 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, const upipe_bf16* x, c
                          const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo, const upipe_bf16* dy,
                          const upipe_bf16* o_saved, const float* lse_saved, upipe_bf16* dx, float* dwq, float* dwk,
                          float* dwv, float* dwo, int reduce_dw, char* ws, cudaStream_t st);
+}  // namespace upipe
+
+namespace upipe {
+static std::atomic<uint64_t> g_launches{0};
+void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 }  // namespace upipe
 
 using namespace upipe;
@@ -272,6 +278,41 @@ upipe_status_t upipe_synth_fill_bf16(upipe_bf16* dst, int64_t n, uint64_t seed, 
   if (!dst || n < 0) return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "synth_fill: bad arguments");
   return cuda_status(synth_fill_bf16_run(dst, n, seed, tensor_id, exponent, start, static_cast<cudaStream_t>(stream)),
                      "synth_fill");
+}
+
+upipe_status_t upipe_kernel_launches(uint64_t* count) {
+  if (!count) return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "count == NULL");
+  *count = g_launches.load();
+  return UPIPE_OK;
+}
+
+upipe_status_t upipe_set_trace(upipe_ctx_t ctx, int on) {
+  if (upipe_status_t st = check_ctx(ctx)) return st;
+  ctx->tracer.on = on != 0;
+  return UPIPE_OK;
+}
+
+upipe_status_t upipe_trace_read(upipe_ctx_t ctx, double ms[UPIPE_TRACE_NCAT], int64_t count[UPIPE_TRACE_NCAT]) {
+  if (upipe_status_t st = check_ctx(ctx)) return st;
+  if (!ms || !count) return set_err(ctx, UPIPE_ERR_INVALID_ARG, "ms/count == NULL");
+  for (int i = 0; i < UPIPE_TRACE_NCAT; ++i) {
+    ms[i] = 0;
+    count[i] = 0;
+  }
+  cudaSetDevice(ctx->device);
+  Tracer& T = ctx->tracer;
+  for (auto& r : T.recs) {
+    cudaError_t e = cudaEventSynchronize(r.b);
+    float t = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e != cudaSuccess) return set_err(ctx, UPIPE_ERR_CUDA, std::string("trace: ") + cudaGetErrorString(e));
+    ms[r.cat] += t;
+    count[r.cat] += 1;
+    T.pool.push_back(r.a);
+    T.pool.push_back(r.b);
+  }
+  T.recs.clear();
+  return UPIPE_OK;
 }
 
 }  // extern "C"

@@ -215,6 +215,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs&
   if (attr != cudaSuccess) return attr;
   dim3 grid((args.N + BN - 1) / BN, (args.M + BM - 1) / BM);
   kern<<<grid, 192, C::SMEM, s>>>(ta, tb, args);
+  count_launches(1);
   return cudaGetLastError();
 }
 

@@ -6,6 +6,9 @@
 
 namespace upipe {
 
+// process-wide kernel launch counter (upipe_kernel_launches)
+void count_launches(uint64_t n);
+
 // ---------------------------------------------------------------- GEMM
 // D[m, n] = alpha * sum_k A(m, k) * B(n, k)   (bf16 in, fp32 accumulate in TMEM)
 //

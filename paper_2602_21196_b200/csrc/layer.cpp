@@ -29,6 +29,33 @@ struct Err {
       return E.fail(UPIPE_ERR_CUDA, std::string(#expr ": ") + (errbuf[0] ? errbuf : cudaGetErrorString(_e))); \
   } while (0)
 
+// Brackets one step with trace events on the call's stream (no-op when tracing is off).
+struct Step {
+  upipe_ctx_s* ctx;
+  cudaStream_t st;
+  int cat;
+  cudaEvent_t a = nullptr;
+  Step(upipe_ctx_s* c, cudaStream_t s, int k) : ctx(c), st(s), cat(k) {
+    if (ctx->tracer.on) {
+      a = ctx->tracer.get();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~Step() {
+    if (a) {
+      cudaEvent_t b = ctx->tracer.get();
+      cudaEventRecord(b, st);
+      ctx->tracer.recs.push_back({cat, a, b});
+    }
+  }
+};
+
+#define UP_T(cat, macro, expr)            \
+  do {                                    \
+    Step _step(ctx, st, UPIPE_TRACE_##cat); \
+    macro(expr);                          \
+  } while (0)
+
 #define UP_COMM(expr)                                  \
   do {                                                 \
     std::string _m;                                    \
@@ -74,15 +101,15 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     const int64_t q0 = P.q0(s, 0), kv0 = P.kv0(s, 0);
     const int64_t qstep = (int64_t)P.q_dev_stride() * d;
     // F1: Q_s = x Wq[rows(s)]^T -> send layout
-    UP_CUDA(gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend), st, errbuf, sizeof errbuf));
+    UP_T(GEMM, UP_CUDA, gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend), st, errbuf, sizeof errbuf));
     // F2: inp_all_to_all, Q first, then K and V when this stage starts a super-stage
-    UP_COMM(T.alltoall(ws + W.qsend, ws + W.qrecv, qbytes, st, _m));
+    UP_T(COMM, UP_COMM, T.alltoall(ws + W.qsend, ws + W.qrecv, qbytes, st, _m));
     if (P.kv_sent(s)) {
       const int64_t kvrows = (int64_t)P.Hkv * d;
-      UP_CUDA(gemm_run(proj_to_send(P, x, wk, kvrows, kv0 * d, kseg, kseg, ws + W.ksend), st, errbuf, sizeof errbuf));
-      UP_COMM(T.alltoall(ws + W.ksend, ws + W.krecv, kbytes, st, _m));
-      UP_CUDA(gemm_run(proj_to_send(P, x, wv, kvrows, kv0 * d, kseg, kseg, ws + W.vsend), st, errbuf, sizeof errbuf));
-      UP_COMM(T.alltoall(ws + W.vsend, ws + W.vrecv, kbytes, st, _m));
+      UP_T(GEMM, UP_CUDA, gemm_run(proj_to_send(P, x, wk, kvrows, kv0 * d, kseg, kseg, ws + W.ksend), st, errbuf, sizeof errbuf));
+      UP_T(COMM, UP_COMM, T.alltoall(ws + W.ksend, ws + W.krecv, kbytes, st, _m));
+      UP_T(GEMM, UP_CUDA, gemm_run(proj_to_send(P, x, wv, kvrows, kv0 * d, kseg, kseg, ws + W.vsend), st, errbuf, sizeof errbuf));
+      UP_T(COMM, UP_COMM, T.alltoall(ws + W.vsend, ws + W.vrecv, kbytes, st, _m));
     }
     // F3: attention over the full sequence for this device's qpd heads
     AttnFwdProblem a{};
@@ -106,11 +133,11 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     a.ldq = qseg;
     a.ldkv = kseg;
     a.ld_lse = P.S;
-    UP_CUDA(attn_fwd_run(a, st, errbuf, sizeof errbuf));
+    UP_T(ATTN_FWD, UP_CUDA, attn_fwd_run(a, st, errbuf, sizeof errbuf));
     if (C > 1) {
       // F4: out_all_to_all, F5: fill the pre-allocated output o_saved
-      UP_COMM(T.alltoall(ws + W.osend, ws + W.orecv, qbytes, st, _m));
-      UP_CUDA(unpack_cols_run(ws + W.orecv, P.S_l, C, (int)qseg, o_saved, HqD, q0 * d, qstep, st));
+      UP_T(COMM, UP_COMM, T.alltoall(ws + W.osend, ws + W.orecv, qbytes, st, _m));
+      UP_T(AUX, UP_CUDA, unpack_cols_run(ws + W.orecv, P.S_l, C, (int)qseg, o_saved, HqD, q0 * d, qstep, st));
     }
     // F6: y (+)= O_s Wo[:, cols(s)]^T ; fp32 accumulator across stages, bf16 on the last stage (F7 fused)
     GemmProblem g;
@@ -132,7 +159,7 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     else if (s == 0) g.c.epi = Epi::kStoreF32;
     else if (s == P.nstages - 1) g.c.epi = Epi::kAccF32ToBF16;
     else g.c.epi = Epi::kAccF32;
-    UP_CUDA(gemm_run(g, st, errbuf, sizeof errbuf));
+    UP_T(GEMM, UP_CUDA, gemm_run(g, st, errbuf, sizeof errbuf));
   }
   return UPIPE_OK;
 }
@@ -161,7 +188,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     g.c.out_f32 = dwo;
     g.c.ld_f32 = HqD;
     g.c.epi = Epi::kStoreF32;
-    UP_CUDA(gemm_run(g, st, errbuf, sizeof errbuf));
+    UP_T(GEMM, UP_CUDA, gemm_run(g, st, errbuf, sizeof errbuf));
   }
   const int n_dx_terms = P.nstages + 2 * (P.nstages / P.sigma);
   int dx_term = 0;
@@ -213,13 +240,13 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   for (int s = 0; s < P.nstages; ++s) {
     const int64_t q0 = P.q0(s, 0), kv0 = P.kv0(s, 0);
     // B1: recompute the stage's projections and inp_all_to_all
-    UP_CUDA(gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend), st, errbuf, sizeof errbuf));
-    UP_COMM(T.alltoall(ws + W.qsend, ws + W.qrecv, qbytes, st, _m));
+    UP_T(GEMM, UP_CUDA, gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend), st, errbuf, sizeof errbuf));
+    UP_T(COMM, UP_COMM, T.alltoall(ws + W.qsend, ws + W.qrecv, qbytes, st, _m));
     if (P.kv_sent(s)) {
-      UP_CUDA(gemm_run(proj_to_send(P, x, wk, HkvD, kv0 * d, kseg, kseg, ws + W.ksend), st, errbuf, sizeof errbuf));
-      UP_COMM(T.alltoall(ws + W.ksend, ws + W.krecv, kbytes, st, _m));
-      UP_CUDA(gemm_run(proj_to_send(P, x, wv, HkvD, kv0 * d, kseg, kseg, ws + W.vsend), st, errbuf, sizeof errbuf));
-      UP_COMM(T.alltoall(ws + W.vsend, ws + W.vrecv, kbytes, st, _m));
+      UP_T(GEMM, UP_CUDA, gemm_run(proj_to_send(P, x, wk, HkvD, kv0 * d, kseg, kseg, ws + W.ksend), st, errbuf, sizeof errbuf));
+      UP_T(COMM, UP_COMM, T.alltoall(ws + W.ksend, ws + W.krecv, kbytes, st, _m));
+      UP_T(GEMM, UP_CUDA, gemm_run(proj_to_send(P, x, wv, HkvD, kv0 * d, kseg, kseg, ws + W.vsend), st, errbuf, sizeof errbuf));
+      UP_T(COMM, UP_COMM, T.alltoall(ws + W.vsend, ws + W.vrecv, kbytes, st, _m));
     }
     // B2: dO_s = dY Wo[:, cols(s)] straight into the send layout; delta = rowsum(dO*O) (A13)
     {
@@ -237,17 +264,17 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       g.c.n_len = qseg;
       g.c.r_nstride = P.S_l;
       g.c.epi = Epi::kStoreBF16;
-      UP_CUDA(gemm_run(g, st, errbuf, sizeof errbuf));
+      UP_T(GEMM, UP_CUDA, gemm_run(g, st, errbuf, sizeof errbuf));
       for (int p = 0; p < C; ++p)
-        UP_CUDA(rowdot_run((const upipe_bf16*)(ws + W.dosend) + (int64_t)p * P.S_l * qseg, qseg,
+        UP_T(AUX, UP_CUDA, rowdot_run((const upipe_bf16*)(ws + W.dosend) + (int64_t)p * P.S_l * qseg, qseg,
                            o_saved + (int64_t)P.q0(s, p) * d, HqD, (float*)(ws + W.dsend) + (int64_t)p * P.S_l * P.qpd,
                            P.qpd, P.S_l, P.qpd, d, st));
     }
     // B3: dO and delta seq->head ("during out_all_to_all", Table 4)
-    UP_COMM(T.alltoall(ws + W.dosend, ws + W.dorecv, qbytes, st, _m));
-    UP_COMM(T.alltoall(ws + W.dsend, ws + W.drecv, (size_t)P.S_l * P.qpd * 4, st, _m));
+    UP_T(COMM, UP_COMM, T.alltoall(ws + W.dosend, ws + W.dorecv, qbytes, st, _m));
+    UP_T(COMM, UP_COMM, T.alltoall(ws + W.dsend, ws + W.drecv, (size_t)P.S_l * P.qpd * 4, st, _m));
     // B4: attention backward; dK/dV accumulate over the sigma stages sharing the resident K/V
-    UP_CUDA(cudaMemsetAsync(ws + W.dqacc, 0, (size_t)P.S * qseg * 4, st));
+    UP_T(AUX, UP_CUDA, cudaMemsetAsync(ws + W.dqacc, 0, (size_t)P.S * qseg * 4, st));
     const int r = s % P.sigma;
     const bool last = P.kv_last(s);
     AttnBwdProblem b{};
@@ -275,29 +302,29 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     b.ld_kvb = kseg;
     b.kv_accumulate = r > 0;
     b.kv_write_acc = !last;
-    UP_CUDA(attn_bwd_run(b, st, errbuf, sizeof errbuf));
+    UP_T(ATTN_BWD, UP_CUDA, attn_bwd_run(b, st, errbuf, sizeof errbuf));
     // B5: dQ fp32 -> bf16 send layout, head->seq ("during inp_all_to_all")
-    UP_CUDA(cvt_f32_bf16_run((const float*)(ws + W.dqacc), qseg, ws + W.dqsend, qseg, P.S, qseg, 1.0f, st));
-    UP_COMM(T.alltoall(ws + W.dqsend, ws + W.dqrecv, qbytes, st, _m));
+    UP_T(AUX, UP_CUDA, cvt_f32_bf16_run((const float*)(ws + W.dqacc), qseg, ws + W.dqsend, qseg, P.S, qseg, 1.0f, st));
+    UP_T(COMM, UP_COMM, T.alltoall(ws + W.dqsend, ws + W.dqrecv, qbytes, st, _m));
     // B6: dX and dWq for the stage's q heads
-    UP_CUDA(gemm_run(dx_gemm(ws + W.dqrecv, qseg, wq, HqD, q0 * d, qstep), st, errbuf, sizeof errbuf));
-    UP_CUDA(gemm_run(dw_gemm(ws + W.dqrecv, qseg, dwq, q0 * d, qstep), st, errbuf, sizeof errbuf));
+    UP_T(GEMM, UP_CUDA, gemm_run(dx_gemm(ws + W.dqrecv, qseg, wq, HqD, q0 * d, qstep), st, errbuf, sizeof errbuf));
+    UP_T(GEMM, UP_CUDA, gemm_run(dw_gemm(ws + W.dqrecv, qseg, dwq, q0 * d, qstep), st, errbuf, sizeof errbuf));
     if (last) {
       // retire the super-stage's K/V: dK, dV head->seq, then their dX / dW terms
-      UP_COMM(T.alltoall(ws + W.dksend, ws + W.dkrecv, kbytes, st, _m));
-      UP_COMM(T.alltoall(ws + W.dvsend, ws + W.dvrecv, kbytes, st, _m));
-      UP_CUDA(gemm_run(dx_gemm(ws + W.dkrecv, kseg, wk, HkvD, kv0 * d, kseg), st, errbuf, sizeof errbuf));
-      UP_CUDA(gemm_run(dx_gemm(ws + W.dvrecv, kseg, wv, HkvD, kv0 * d, kseg), st, errbuf, sizeof errbuf));
-      UP_CUDA(gemm_run(dw_gemm(ws + W.dkrecv, kseg, dwk, kv0 * d, kseg), st, errbuf, sizeof errbuf));
-      UP_CUDA(gemm_run(dw_gemm(ws + W.dvrecv, kseg, dwv, kv0 * d, kseg), st, errbuf, sizeof errbuf));
+      UP_T(COMM, UP_COMM, T.alltoall(ws + W.dksend, ws + W.dkrecv, kbytes, st, _m));
+      UP_T(COMM, UP_COMM, T.alltoall(ws + W.dvsend, ws + W.dvrecv, kbytes, st, _m));
+      UP_T(GEMM, UP_CUDA, gemm_run(dx_gemm(ws + W.dkrecv, kseg, wk, HkvD, kv0 * d, kseg), st, errbuf, sizeof errbuf));
+      UP_T(GEMM, UP_CUDA, gemm_run(dx_gemm(ws + W.dvrecv, kseg, wv, HkvD, kv0 * d, kseg), st, errbuf, sizeof errbuf));
+      UP_T(GEMM, UP_CUDA, gemm_run(dw_gemm(ws + W.dkrecv, kseg, dwk, kv0 * d, kseg), st, errbuf, sizeof errbuf));
+      UP_T(GEMM, UP_CUDA, gemm_run(dw_gemm(ws + W.dvrecv, kseg, dwv, kv0 * d, kseg), st, errbuf, sizeof errbuf));
     }
   }
   // B7: dW summed over the CP group (the FSDP gradient reduction of P:437, A14)
   if (reduce_dw && C > 1) {
-    UP_COMM(T.allreduce_sum_f32(dwq, (size_t)HqD * P.D, st, _m));
-    UP_COMM(T.allreduce_sum_f32(dwk, (size_t)HkvD * P.D, st, _m));
-    UP_COMM(T.allreduce_sum_f32(dwv, (size_t)HkvD * P.D, st, _m));
-    UP_COMM(T.allreduce_sum_f32(dwo, (size_t)HqD * P.D, st, _m));
+    UP_T(COMM, UP_COMM, T.allreduce_sum_f32(dwq, (size_t)HqD * P.D, st, _m));
+    UP_T(COMM, UP_COMM, T.allreduce_sum_f32(dwk, (size_t)HkvD * P.D, st, _m));
+    UP_T(COMM, UP_COMM, T.allreduce_sum_f32(dwv, (size_t)HkvD * P.D, st, _m));
+    UP_T(COMM, UP_COMM, T.allreduce_sum_f32(dwo, (size_t)HqD * P.D, st, _m));
   }
   return UPIPE_OK;
 }

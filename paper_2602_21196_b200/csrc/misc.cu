@@ -118,6 +118,7 @@ cudaError_t rowdot_run(const void* dO, int64_t ld_do, const void* O, int64_t ld_
   } else {
     return cudaErrorInvalidValue;
   }
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -127,6 +128,7 @@ cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t l
   if (cols % 8) return cudaErrorInvalidValue;
   cvt_kernel<<<grid_for(rows * cols / 8, kThreads), kThreads, 0, s>>>(src, lds, (__nv_bfloat16*)dst, ldd, rows,
                                                                      cols, scale);
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -137,6 +139,7 @@ cudaError_t unpack_cols_run(const void* src, int64_t rows, int nseg, int seg_col
   const int seg_v = seg_cols / 8;
   unpack_kernel<<<grid_for((int64_t)nseg * rows * seg_v, kThreads), kThreads, 0, s>>>(
       (const uint4*)src, rows, nseg, seg_v, (__nv_bfloat16*)dst, ldd, col_base, col_stride);
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -146,6 +149,7 @@ cudaError_t synth_fill_bf16_run(void* dst, int64_t n, uint64_t seed, int tensor_
   const uint64_t base = seed * 0x9E3779B97F4A7C15ull + (uint64_t)tensor_id * 0xD1B54A32D192ED03ull + (uint64_t)start;
   const float step = ldexpf(1.0f, exponent - 8);
   synth_kernel<<<grid_for(n, kThreads), kThreads, 0, s>>>((__nv_bfloat16*)dst, n, base, step);
+  count_launches(1);
   return cudaGetLastError();
 }
 

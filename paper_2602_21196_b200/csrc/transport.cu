@@ -149,7 +149,10 @@ class FabricTransport final : public Transport {
     cudaMemcpyAsync(dev_ptrs_, h.data(), sizeof(float*) * C, cudaMemcpyHostToDevice, s);
     const size_t chunk = (n + C - 1) / C;
     const size_t b = std::min(n, chunk * rank_), e = std::min(n, chunk * (rank_ + 1));
-    if (e > b) fabric_sum_kernel<<<148 * 4, 256, 0, s>>>(dev_ptrs_, C, b, e, buf);
+    if (e > b) {
+      fabric_sum_kernel<<<148 * 4, 256, 0, s>>>(dev_ptrs_, C, b, e, buf);
+      count_launches(1);
+    }
     // everyone's owned slice is reduced; then copy the other slices from their owners
     if (!sync_publish(buf, s, err)) return UPIPE_ERR_COMM;
     for (int p = 0; p < C; ++p) {

@@ -64,9 +64,40 @@ std::unique_ptr<Transport> make_self_transport();
 std::unique_ptr<Transport> make_nccl_transport(const uint8_t* uid, int C, int rank, std::string& err);
 std::unique_ptr<Transport> make_fabric_transport(upipe_fabric_t f, int rank, int device, std::string& err);
 
+// Event-bracketed timing of layer steps (upipe_set_trace / upipe_trace_read).
+struct Tracer {
+  bool on = false;
+  struct Rec {
+    int cat;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  ~Tracer() {
+    for (auto& r : recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+void count_launches(uint64_t n);
+
 }  // namespace upipe
 
 struct upipe_ctx_s {
+  upipe::Tracer tracer;
   int device = 0;
   int C = 1, rank = 0;
   uint32_t flags = 0;

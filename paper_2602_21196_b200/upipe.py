@@ -67,6 +67,9 @@ def lib() -> ctypes.CDLL:
             "upipe_rowdot": (st, [P, c_int64, P, c_int64, P, c_int64, c_int64, c_int, c_int, P]),
             "upipe_gemm_xwT": (st, [P, P, P, c_int64, c_int64, c_int64, c_int, P]),
             "upipe_synth_fill_bf16": (st, [P, c_int64, c_uint64, c_int, c_int, c_int64, P]),
+            "upipe_kernel_launches": (st, [POINTER(c_uint64)]),
+            "upipe_set_trace": (st, [P, c_int]),
+            "upipe_trace_read": (st, [P, POINTER(ctypes.c_double), POINTER(c_int64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -79,7 +82,10 @@ def lib() -> ctypes.CDLL:
 EXPORTED = ("upipe_get_unique_id", "upipe_init", "upipe_fabric_create", "upipe_fabric_destroy", "upipe_init_local",
             "upipe_finalize", "upipe_status_string", "upipe_last_error", "upipe_workspace_size", "upipe_plan_stage",
             "upipe_validate", "upipe_attn_fwd", "upipe_attn_bwd", "upipe_attn_core_fwd", "upipe_attn_core_bwd",
-            "upipe_rowdot", "upipe_gemm_xwT", "upipe_synth_fill_bf16")
+            "upipe_rowdot", "upipe_gemm_xwT", "upipe_synth_fill_bf16", "upipe_kernel_launches", "upipe_set_trace",
+            "upipe_trace_read")
+
+TRACE_CATS = ("gemm", "attn_fwd", "attn_bwd", "comm", "aux")
 
 
 def _check(st: int, ctx=None):
@@ -215,3 +221,23 @@ def upipe_gemm_xwT(x, w, y, M, N, K, mode=0, stream=None):
 
 def upipe_synth_fill_bf16(dst, n, seed, tensor_id, exponent, start=0, stream=None):
     _check(lib().upipe_synth_fill_bf16(_ptr(dst), n, seed, tensor_id, exponent, start, _stream(stream)))
+
+
+# ------------------------------------------------------------------ instrumentation
+
+def upipe_kernel_launches() -> int:
+    n = c_uint64()
+    _check(lib().upipe_kernel_launches(ctypes.byref(n)))
+    return n.value
+
+
+def upipe_set_trace(ctx, on: bool) -> None:
+    _check(lib().upipe_set_trace(ctx, int(on)), ctx)
+
+
+def upipe_trace_read(ctx) -> dict:
+    """{category: (ms, count)} accumulated since the last read (waits for the events)."""
+    ms = (ctypes.c_double * len(TRACE_CATS))()
+    cnt = (c_int64 * len(TRACE_CATS))()
+    _check(lib().upipe_trace_read(ctx, ms, cnt), ctx)
+    return {k: (ms[i], cnt[i]) for i, k in enumerate(TRACE_CATS)}
