@@ -8,11 +8,15 @@
 //   dV  += P^T dO         (TMEM [256, 256+d))      P^T, dS^T staged in smem (bf16)
 //   dK  += dS^T Q         (TMEM [256+d, 256+2d))
 //   dQ   = dS K           (TMEM cols [128,128+d), reusing dP^T once consumed)
-// dQ is reduced across KV tiles with fp32 atomics into dq_acc (scaled by 1/sqrt(d));
-// dK/dV stay in TMEM for the whole CTA and are written (and optionally
-// accumulated across UPipe stages of one super-stage) at the end.
-// Warps: 0-3 compute (thread = one key row for S^T/dP^T, one query row for dQ),
-// 4 TMA producer, 5 MMA issuer.
+// dQ is reduced across KV tiles in HBM by TMA bulk reduce-add (fp32): the compute
+// warps drain it TMEM -> shared memory (re-using the P^T/dS^T buffers, which are
+// free once the dQ MMA has completed) and one thread per warpgroup issues
+// cp.reduce.async.bulk.tensor. dK/dV stay in TMEM for the whole CTA and are
+// written (and optionally accumulated across the UPipe stages of one
+// super-stage) at the end.
+// Warps: 0-7 compute (two warpgroups splitting the 128 query columns; thread =
+// one key row for S^T/dP^T, one query row for the dQ drain), 8 TMA producer,
+// 9 MMA issuer.
 #include <cstdio>
 
 #include "kernels.h"
@@ -27,7 +31,6 @@ using namespace dev;
 struct BwdArgs {
   const float* lse;
   const float* delta;
-  float* dq_acc;
   float* dk_acc;
   float* dv_acc;
   __nv_bfloat16* dk_bf16;
@@ -50,23 +53,23 @@ struct BwdCfg {
   static constexpr int PB = 128 * 128 * 2; // 128 x 128 bf16
   static constexpr int OFF_K = 0, OFF_V = TB, OFF_Q = 2 * TB, OFF_DO = 3 * TB;
   static constexpr int OFF_P = 4 * TB, OFF_DS = OFF_P + PB;
-  static constexpr int OFF_STAT = OFF_DS + PB;             // lse2[2][128], delta[2][128] fp32
-  static constexpr int OFF_BAR = OFF_STAT + 4 * 128 * 4;
+  static constexpr int OFF_BAR = OFF_DS + PB;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 128, TM_DV = 256, TM_DK = 256 + D;
+  static constexpr int DQ_BOXES = D / 64;  // 32-float boxes of dQ per warpgroup (each drains D/2 columns)
 };
 
 template <int D>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                    const BwdArgs a) {
+                    const __grid_constant__ CUtensorMap tmdQ, const BwdArgs a) {
   using C = BwdCfg<D>;
   constexpr int NCH = D / 64;
   extern __shared__ uint8_t smem_raw[];
+  __shared__ float s_lse2[2][128];
+  __shared__ float s_delta[2][128];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* s_lse2 = reinterpret_cast<float*>(smem + C::OFF_STAT);   // [2][128]
-  float* s_delta = s_lse2 + 256;                                  // [2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* kv_full = bars + 0;
   uint64_t* q_full = bars + 1;
@@ -89,18 +92,18 @@ __global__ void __launch_bounds__(192, 1)
   const int n_qt = nT - qt_begin;
   const int N = G * n_qt;                         // (head, query tile) iterations
 
-  if (warp == 4 && lane == 0) {
-    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO);
-    for (int i = 0; i < 10; ++i) mbar_init(&bars[i], (i == 6 || i == 8) ? 128 : 1);
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
+    for (int i = 0; i < 10; ++i) mbar_init(&bars[i], (i == 6 || i == 8) ? 256 : 1);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc<512>(tmem_slot);
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       mbar_arrive_expect_tx(kv_full, 2 * C::TB);
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int c = 0; c < NCH; ++c) tma_load_3d(smem + C::OFF_DO + c * 16384, &tmdO, do_full, c * 64, h, qt * 128);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0) {
       // ------------------------------------------------ MMA issuer
       constexpr uint32_t id_kk = idesc_bf16(128, 128, false, false);  // S^T, dP^T: both K-major over d
@@ -186,55 +189,54 @@ __global__ void __launch_bounds__(192, 1)
       mma_commit(dkv_full);
     }
   } else {
-    // ------------------------------------------------ compute warps 0-3
-    const int quad = warp;
+    // ------------------------------------------------ compute warpgroups (warps 0-7)
+    const int wg = warp >> 2;                         // query columns [64 wg, 64 wg + 64) ; dQ cols [wg D/2, ...)
+    const int quad = warp & 3;
     const int r = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const long long key = (long long)jb * 128 + r;
     const float sl2 = a.scale_log2;
+    const bool issuer = (warp & 3) == 0 && lane == 0;
+    uint8_t* staging = smem + (wg ? C::OFF_DS : C::OFF_P);  // free while the dQ reduce is in flight
+    const uint32_t pbase = smem_u32(smem + C::OFF_P), dsbase = smem_u32(smem + C::OFF_DS);
     for (int n = 0; n < N; ++n) {
       const int h = g * G + n / n_qt;
       const int qt = qt_begin + n % n_qt;
       const long long q0 = (long long)qt * 128;
-      float* lse2 = s_lse2 + (n & 1) * 128;
-      float* dl = s_delta + (n & 1) * 128;
+      const int sb = n & 1;
       {
         const long long q = q0 + r;
-        float lv = 0.f, dv = 0.f;
-        if (q < a.S) {
-          lv = a.lse[(long long)h * a.ld_lse + q] * 1.4426950408889634f;
-          dv = a.delta[q * a.ld_delta + h];
-        }
-        lse2[r] = lv;
-        dl[r] = dv;
+        if (wg == 0) s_lse2[sb][r] = q < a.S ? a.lse[(long long)h * a.ld_lse + q] * 1.4426950408889634f : 0.f;
+        else s_delta[sb][r] = q < a.S ? a.delta[q * a.ld_delta + h] : 0.f;
       }
-      named_bar_sync(1, 128);
+      if (issuer) bulk_wait_read0();                  // previous dQ reduce has finished reading the staging smem
+      named_bar_sync(1, 256);
       mbar_wait(sdp_full, n & 1);
       tc_fence_after();
       const bool diag = a.causal && qt == jb;
       const bool tail = q0 + 128 > a.S || (long long)jb * 128 + 128 > a.S;
-      const uint32_t pbase = smem_u32(smem + C::OFF_P), dsbase = smem_u32(smem + C::OFF_DS);
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int col0 = wg * 64 + c * 32;
         uint32_t rs[32], rp[32];
-        tmem_ld32(tmem + C::TM_S + lane_off + c * 32, rs);
-        tmem_ld32(tmem + C::TM_DP + lane_off + c * 32, rp);
+        tmem_ld32(tmem + C::TM_S + lane_off + col0, rs);
+        tmem_ld32(tmem + C::TM_DP + lane_off + col0, rp);
         tmem_wait_ld();
         float p[32], ds[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const int qi = c * 32 + i;
-          float pv = ex2b(__uint_as_float(rs[i]) * sl2 - lse2[qi]);
+          const int qi = col0 + i;
+          float pv = ex2b(__uint_as_float(rs[i]) * sl2 - s_lse2[sb][qi]);
           if (diag || tail) {
             const long long q = q0 + qi;
             if ((a.causal && key > q) || q >= a.S || key >= a.S) pv = 0.f;
           }
           p[i] = pv;
-          ds[i] = pv * (__uint_as_float(rp[i]) - dl[qi]);
+          ds[i] = pv * (__uint_as_float(rp[i]) - s_delta[sb][qi]);
         }
 #pragma unroll
         for (int v8 = 0; v8 < 4; ++v8) {
-          const int qc = c * 32 + v8 * 8;
+          const int qc = col0 + v8 * 8;
           const uint32_t off = (qc >> 6) * 16384 + sw128_offset(r, qc & 63);
           st_shared_v4(pbase + off, pack_bf16(p[v8 * 8 + 0], p[v8 * 8 + 1]), pack_bf16(p[v8 * 8 + 2], p[v8 * 8 + 3]),
                        pack_bf16(p[v8 * 8 + 4], p[v8 * 8 + 5]), pack_bf16(p[v8 * 8 + 6], p[v8 * 8 + 7]));
@@ -246,71 +248,79 @@ __global__ void __launch_bounds__(192, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(ds_full);
-      // ---- dQ drain: TMEM lane = query row
+      // ---- dQ drain: TMEM lane = query row; this warpgroup takes dQ columns [wg D/2, (wg+1) D/2)
       mbar_wait(dq_full, n & 1);
       tc_fence_after();
-      const long long q = q0 + r;
-      float* dqrow = a.dq_acc + q * (long long)a.nq * D + (long long)h * D;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t rq[32];
-        tmem_ld32(tmem + C::TM_DQ + lane_off + c * 32, rq);
-        tmem_wait_ld();
-        if (q < a.S) {
+      uint32_t rq[C::DQ_BOXES][32];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float4 v = make_float4(__uint_as_float(rq[4 * i]) * a.scale, __uint_as_float(rq[4 * i + 1]) * a.scale,
-                                   __uint_as_float(rq[4 * i + 2]) * a.scale, __uint_as_float(rq[4 * i + 3]) * a.scale);
-            atomicAdd(reinterpret_cast<float4*>(dqrow + c * 32 + 4 * i), v);
-          }
-        }
-      }
+      for (int b = 0; b < C::DQ_BOXES; ++b) tmem_ld32(tmem + C::TM_DQ + lane_off + wg * (D / 2) + b * 32, rq[b]);
+      tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(dq_empty);
+      const uint32_t stbase = smem_u32(staging);
+#pragma unroll
+      for (int b = 0; b < C::DQ_BOXES; ++b) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {     // 16-byte chunk j of the 128-byte row, swizzled by row % 8
+          const uint32_t addr = stbase + b * 16384 + r * 128 + ((j ^ (r & 7)) << 4);
+          st_shared_v4(addr, __float_as_uint(__uint_as_float(rq[b][4 * j + 0]) * a.scale),
+                       __float_as_uint(__uint_as_float(rq[b][4 * j + 1]) * a.scale),
+                       __float_as_uint(__uint_as_float(rq[b][4 * j + 2]) * a.scale),
+                       __float_as_uint(__uint_as_float(rq[b][4 * j + 3]) * a.scale));
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(2 + wg, 128);
+      if (issuer) {
+#pragma unroll
+        for (int b = 0; b < C::DQ_BOXES; ++b)
+          tma_reduce_add_2d(&tmdQ, staging + b * 16384, h * D + wg * (D / 2) + b * 32, (int)q0);
+        bulk_commit();
+      }
     }
-    // ---- dK / dV epilogue (TMEM lane = key row)
+    if (issuer) bulk_wait0();
+    // ---- dK / dV epilogue (TMEM lane = key row): warpgroup 0 writes dV, warpgroup 1 writes dK
     mbar_wait(dkv_full, 0);
     tc_fence_after();
     const long long ldacc = (long long)a.nkv * D;
-    for (int which = 0; which < 2; ++which) {          // 0: dV, 1: dK
-      const uint32_t tcol = which ? C::TM_DK : C::TM_DV;
-      const float sc = which ? a.scale : 1.f;
-      float* acc = (which ? a.dk_acc : a.dv_acc);
-      __nv_bfloat16* ob = which ? a.dk_bf16 : a.dv_bf16;
+    const int which = wg;
+    const uint32_t tcol = which ? C::TM_DK : C::TM_DV;
+    const float sc = which ? a.scale : 1.f;
+    float* acc = (which ? a.dk_acc : a.dv_acc);
+    __nv_bfloat16* ob = which ? a.dk_bf16 : a.dv_bf16;
 #pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t rr[32];
-        tmem_ld32(tmem + tcol + lane_off + c * 32, rr);
-        tmem_wait_ld();
-        if (key >= a.S || N == 0) continue;
-        float v[32];
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t rr[32];
+      tmem_ld32(tmem + tcol + lane_off + c * 32, rr);
+      tmem_wait_ld();
+      if (key >= a.S || N == 0) continue;
+      float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]) * sc;
-        float4* accp = acc ? reinterpret_cast<float4*>(acc + key * ldacc + (long long)g * D + c * 32) : nullptr;
-        if (a.kv_accumulate && accp) {
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]) * sc;
+      float4* accp = acc ? reinterpret_cast<float4*>(acc + key * ldacc + (long long)g * D + c * 32) : nullptr;
+      if (a.kv_accumulate && accp) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 o = accp[i];
-            v[4 * i] += o.x; v[4 * i + 1] += o.y; v[4 * i + 2] += o.z; v[4 * i + 3] += o.w;
-          }
+        for (int i = 0; i < 8; ++i) {
+          const float4 o = accp[i];
+          v[4 * i] += o.x; v[4 * i + 1] += o.y; v[4 * i + 2] += o.z; v[4 * i + 3] += o.w;
         }
-        if (a.kv_write_acc && accp) {
+      }
+      if (a.kv_write_acc && accp) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) accp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        }
-        if (ob) {
-          uint4* dst = reinterpret_cast<uint4*>(ob + key * a.ld_kvb + (long long)g * D + c * 32);
+        for (int i = 0; i < 8; ++i) accp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      }
+      if (ob) {
+        uint4* dst = reinterpret_cast<uint4*>(ob + key * a.ld_kvb + (long long)g * D + c * 32);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                                pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
-        }
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                              pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -324,16 +334,18 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
     snprintf(err, errlen, "attn_bwd: unsupported head_dim %d or head counts %d/%d", p.d, p.nq, p.nkv);
     return cudaErrorInvalidValue;
   }
-  CUtensorMap tq, tk, tv, tdo;
+  CUtensorMap tq, tk, tv, tdo, tdq;
   if (!make_tmap_3d(&tq, p.q, p.d, p.nq, p.S, p.d, p.ldq, 64, 1, 128, err, errlen)) return cudaErrorInvalidValue;
   if (!make_tmap_3d(&tk, p.k, p.d, p.nkv, p.S, p.d, p.ldkv, 64, 1, 128, err, errlen)) return cudaErrorInvalidValue;
   if (!make_tmap_3d(&tv, p.v, p.d, p.nkv, p.S, p.d, p.ldkv, 64, 1, 128, err, errlen)) return cudaErrorInvalidValue;
   if (!make_tmap_3d(&tdo, p.dout, p.d, p.nq, p.S, p.d, p.ldo_grad, 64, 1, 128, err, errlen))
     return cudaErrorInvalidValue;
+  // dq_acc fp32 [S][nq*d]: boxes of 32 columns x 128 rows, TMA reduce-add
+  if (!make_tmap_2d_f32(&tdq, p.dq_acc, (uint64_t)p.nq * p.d, p.S, (uint64_t)p.nq * p.d, 32, 128, err, errlen))
+    return cudaErrorInvalidValue;
   BwdArgs a;
   a.lse = p.lse;
   a.delta = p.delta;
-  a.dq_acc = p.dq_acc;
   a.dk_acc = p.dk_acc;
   a.dv_acc = p.dv_acc;
   a.dk_bf16 = reinterpret_cast<__nv_bfloat16*>(p.dk_bf16);
@@ -356,13 +368,13 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
     static const cudaError_t attr =
         cudaFuncSetAttribute(attn_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<128>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
-    attn_bwd_kernel<128><<<grid, 192, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, a);
+    attn_bwd_kernel<128><<<grid, 320, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
     count_launches(1);
   } else {
     static const cudaError_t attr =
         cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<64>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
-    attn_bwd_kernel<64><<<grid, 192, BwdCfg<64>::SMEM, stream>>>(tq, tk, tv, tdo, a);
+    attn_bwd_kernel<64><<<grid, 320, BwdCfg<64>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
     count_launches(1);
   }
   e = cudaGetLastError();

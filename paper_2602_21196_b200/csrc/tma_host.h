@@ -47,6 +47,28 @@ inline bool make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64
   return true;
 }
 
+// 2-D fp32 map with 128B swizzle (box inner <= 32 floats), for TMA reduce-add of fp32 tiles.
+inline bool make_tmap_2d_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                             uint32_t box_inner, uint32_t box_outer, char* err, size_t errlen) {
+  PFN_encodeTiled enc = get_encode_tiled();
+  if (!enc) {
+    snprintf(err, errlen, "cuTensorMapEncodeTiled entry point unavailable");
+    return false;
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 4};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(err, errlen, "cuTensorMapEncodeTiled(2d f32) failed: %d", (int)r);
+    return false;
+  }
+  return true;
+}
+
 // 3-D bf16 map: dims {d0, d1, d2}, strides (elements) s1 (dim1), s2 (dim2), box {b0, b1, b2}.
 inline bool make_tmap_3d(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
                          uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2, char* err, size_t errlen) {
