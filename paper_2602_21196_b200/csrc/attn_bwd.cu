@@ -3,17 +3,19 @@
 // KV-stationary: one CTA owns a 128-key tile of one KV head and loops over the
 // query tiles (of every local query head of that KV group) that can see it.
 // Per query tile, five tcgen05 MMAs (M=128, K=128 or d):
-//   S^T  = K Q^T          (TMEM cols [0,128))      P^T  = exp2(S^T*c - lse2)
-//   dP^T = V dO^T         (TMEM cols [128,256))    dS^T = P^T (dP^T - delta)
-//   dV  += P^T dO         (TMEM [256, 256+d))      P^T, dS^T staged in smem (bf16)
+//   S^T  = K Q^T          (TMEM cols [0,128))      P^T  = exp2(S^T*c - lse2) -> bf16, back into TMEM
+//   dP^T = V dO^T         (TMEM cols [128,256))    dS^T = P^T (dP^T - delta) -> bf16, smem
+//   dV  += P^T dO         (TMEM [256, 256+d))      A operand P^T read from TMEM (TS form)
 //   dK  += dS^T Q         (TMEM [256+d, 256+2d))
 //   dQ   = dS K           (TMEM cols [128,128+d), reusing dP^T once consumed)
+// P^T lives in the S^T columns it was computed from (two bf16 per 32-bit column),
+// which frees the shared memory for double-buffered Q / dO tiles: the TMA loads of
+// tile n+1 overlap the MMAs of tile n.
 // dQ is reduced across KV tiles in HBM by TMA bulk reduce-add (fp32): the compute
-// warps drain it TMEM -> shared memory (re-using the P^T/dS^T buffers, which are
-// free once the dQ MMA has completed) and one thread per warpgroup issues
-// cp.reduce.async.bulk.tensor. dK/dV stay in TMEM for the whole CTA and are
-// written (and optionally accumulated across the UPipe stages of one
-// super-stage) at the end.
+// warps drain it TMEM -> shared memory (the dS^T buffer, free once the dQ MMA has
+// completed) and one thread per warpgroup issues cp.reduce.async.bulk.tensor.
+// dK/dV stay in TMEM for the whole CTA and are written (and optionally accumulated
+// across the UPipe stages of one super-stage) at the end.
 // Warps: 0-7 compute (two warpgroups splitting the 128 query columns; thread =
 // one key row for S^T/dP^T, one query row for the dQ drain), 8 TMA producer,
 // 9 MMA issuer.
@@ -51,10 +53,11 @@ template <int D>
 struct BwdCfg {
   static constexpr int TB = 128 * D * 2;   // one 128 x D bf16 tile
   static constexpr int PB = 128 * 128 * 2; // 128 x 128 bf16
-  static constexpr int OFF_K = 0, OFF_V = TB, OFF_Q = 2 * TB, OFF_DO = 3 * TB;
-  static constexpr int OFF_P = 4 * TB, OFF_DS = OFF_P + PB;
+  static constexpr int OFF_K = 0, OFF_V = TB, OFF_Q = 2 * TB, OFF_DO = 4 * TB;  // Q, dO: 2 buffers each
+  static constexpr int OFF_DS = 6 * TB;
   static constexpr int OFF_BAR = OFF_DS + PB;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int OFF_STAT = OFF_BAR + 256;             // lse2[2][128], delta[2][128] fp32
+  static constexpr int SMEM = OFF_STAT + 2048;                // base is 1024-aligned (checked in-kernel)
   static constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 128, TM_DV = 256, TM_DK = 256 + D;
   static constexpr int DQ_BOXES = D / 64;  // 32-float boxes of dQ per warpgroup (each drains D/2 columns)
 };
@@ -66,22 +69,22 @@ __global__ void __launch_bounds__(320, 1)
                     const __grid_constant__ CUtensorMap tmdQ, const BwdArgs a) {
   using C = BwdCfg<D>;
   constexpr int NCH = D / 64;
-  extern __shared__ uint8_t smem_raw[];
-  __shared__ float s_lse2[2][128];
-  __shared__ float s_delta[2][128];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (smem_u32(smem) & 1023) __trap();               // 128B-swizzle atoms need 1024-byte alignment
+  float (*s_lse2)[128] = reinterpret_cast<float (*)[128]>(smem + C::OFF_STAT);
+  float (*s_delta)[128] = reinterpret_cast<float (*)[128]>(smem + C::OFF_STAT + 1024);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* kv_full = bars + 0;
-  uint64_t* q_full = bars + 1;
-  uint64_t* q_empty = bars + 2;
-  uint64_t* do_full = bars + 3;
-  uint64_t* do_empty = bars + 4;
-  uint64_t* sdp_full = bars + 5;
-  uint64_t* ds_full = bars + 6;
-  uint64_t* dq_full = bars + 7;
-  uint64_t* dq_empty = bars + 8;
-  uint64_t* dkv_full = bars + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* q_full = bars + 1;     // [2]
+  uint64_t* q_empty = bars + 3;    // [2]
+  uint64_t* do_full = bars + 5;    // [2]
+  uint64_t* do_empty = bars + 7;   // [2]
+  uint64_t* sdp_full = bars + 9;
+  uint64_t* ds_full = bars + 10;
+  uint64_t* dq_full = bars + 11;
+  uint64_t* dq_empty = bars + 12;
+  uint64_t* dkv_full = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = warp_id(), lane = lane_id();
   const int jb = blockIdx.x;                      // key tile (small jb = most query tiles = longest)
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(320, 1)
 
   if (warp == 8 && lane == 0) {
     tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
-    for (int i = 0; i < 10; ++i) mbar_init(&bars[i], (i == 6 || i == 8) ? 256 : 1);
+    for (int i = 0; i < 14; ++i) mbar_init(&bars[i], (i == 10 || i == 12) ? 256 : 1);
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc<512>(tmem_slot);
@@ -115,25 +118,29 @@ __global__ void __launch_bounds__(320, 1)
       for (int n = 0; n < N; ++n) {
         const int h = g * G + n / n_qt;
         const int qt = qt_begin + n % n_qt;
-        mbar_wait(q_empty, (n & 1) ^ 1);
-        mbar_arrive_expect_tx(q_full, C::TB);
+        const int b = n & 1;
+        const uint32_t ph = ((n >> 1) & 1) ^ 1;
+        mbar_wait(&q_empty[b], ph);
+        mbar_arrive_expect_tx(&q_full[b], C::TB);
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) tma_load_3d(smem + C::OFF_Q + c * 16384, &tmQ, q_full, c * 64, h, qt * 128);
-        mbar_wait(do_empty, (n & 1) ^ 1);
-        mbar_arrive_expect_tx(do_full, C::TB);
+        for (int c = 0; c < NCH; ++c)
+          tma_load_3d(smem + C::OFF_Q + b * C::TB + c * 16384, &tmQ, &q_full[b], c * 64, h, qt * 128);
+        mbar_wait(&do_empty[b], ph);
+        mbar_arrive_expect_tx(&do_full[b], C::TB);
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) tma_load_3d(smem + C::OFF_DO + c * 16384, &tmdO, do_full, c * 64, h, qt * 128);
+        for (int c = 0; c < NCH; ++c)
+          tma_load_3d(smem + C::OFF_DO + b * C::TB + c * 16384, &tmdO, &do_full[b], c * 64, h, qt * 128);
       }
     }
   } else if (warp == 9) {
     if (lane == 0) {
       // ------------------------------------------------ MMA issuer
       constexpr uint32_t id_kk = idesc_bf16(128, 128, false, false);  // S^T, dP^T: both K-major over d
-      constexpr uint32_t id_kmn = idesc_bf16(128, D, false, true);    // dV, dK: A K-major (over q), B MN-major
+      constexpr uint32_t id_kmn = idesc_bf16(128, D, false, true);    // dV (A in TMEM), dK: B MN-major
       constexpr uint32_t id_mnmn = idesc_bf16(128, D, true, true);    // dQ: A = dS^T viewed MN-major, B = K MN-major
       const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
-      const uint32_t sQ = smem_u32(smem + C::OFF_Q), sdO = smem_u32(smem + C::OFF_DO);
-      const uint32_t sP = smem_u32(smem + C::OFF_P), sdS = smem_u32(smem + C::OFF_DS);
+      const uint32_t sQ0 = smem_u32(smem + C::OFF_Q), sdO0 = smem_u32(smem + C::OFF_DO);
+      const uint32_t sdS = smem_u32(smem + C::OFF_DS);
       auto mma_kk = [&](uint32_t sa, uint32_t sb, uint32_t tm) {      // [128 x D] x [128 x D]^T
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
@@ -142,13 +149,21 @@ __global__ void __launch_bounds__(320, 1)
             mma_ss(tm, desc_sw128(sa + c * 16384 + kk * 32, 16, 1024), desc_sw128(sb + c * 16384 + kk * 32, 16, 1024),
                    id_kk, (c | kk) != 0);
       };
-      auto mma_kmn = [&](uint32_t sa, uint32_t sb, uint32_t tm, bool acc) {  // A [128 x 128 q] K-major, B MN-major
+      auto mma_kmn = [&](uint32_t sa, uint32_t sb, uint32_t tm, bool acc) {  // A [128 x 128 q] K-major smem
 #pragma unroll
         for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
             mma_ss(tm, desc_sw128(sa + kb * 16384 + kk * 32, 16, 1024),
                    desc_sw128(sb + kb * 8192 + kk * 2048, 16384, 1024), id_kmn, (acc || kb || kk) ? 1u : 0u);
+      };
+      auto mma_tmn = [&](uint32_t ta, uint32_t sb, uint32_t tm, bool acc) {  // A = P^T in TMEM (q 0-63 at +0, 64-127 at +64)
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ts(tm, ta + kb * 64 + kk * 8, desc_sw128(sb + kb * 8192 + kk * 2048, 16384, 1024), id_kmn,
+                   (acc || kb || kk) ? 1u : 0u);
       };
       auto mma_mnmn = [&](uint32_t sa, uint32_t sb, uint32_t tm) {  // dQ = dS K: K dim = keys (rows of both)
 #pragma unroll
@@ -159,30 +174,34 @@ __global__ void __launch_bounds__(320, 1)
                    desc_sw128(sb + kb * 8192 + kk * 2048, 16384, 1024), id_mnmn, (kb | kk) != 0);
       };
       mbar_wait(kv_full, 0);
-      mbar_wait(q_full, 0);
+      mbar_wait(&q_full[0], 0);
       tc_fence_after();
-      mma_kk(sK, sQ, tmem + C::TM_S);
-      mbar_wait(do_full, 0);
+      mma_kk(sK, sQ0, tmem + C::TM_S);
+      mbar_wait(&do_full[0], 0);
       tc_fence_after();
-      mma_kk(sV, sdO, tmem + C::TM_DP);
+      mma_kk(sV, sdO0, tmem + C::TM_DP);
       mma_commit(sdp_full);
       for (int n = 0; n < N; ++n) {
+        const int b = n & 1;
+        const uint32_t sQ = sQ0 + b * C::TB, sdO = sdO0 + b * C::TB;
         mbar_wait(ds_full, n & 1);
         tc_fence_after();
-        mma_kmn(sP, sdO, tmem + C::TM_DV, n > 0);
-        mma_commit(do_empty);
+        mma_tmn(tmem + C::TM_S, sdO, tmem + C::TM_DV, n > 0);
+        mma_commit(&do_empty[b]);
         mma_kmn(sdS, sQ, tmem + C::TM_DK, n > 0);
-        mma_commit(q_empty);
+        mma_commit(&q_empty[b]);
         mma_mnmn(sdS, sK, tmem + C::TM_DQ);
         mma_commit(dq_full);
         if (n + 1 < N) {
-          mbar_wait(q_full, (n + 1) & 1);
+          const int b1 = (n + 1) & 1;
+          const uint32_t ph1 = ((n + 1) >> 1) & 1;
+          mbar_wait(&q_full[b1], ph1);
           tc_fence_after();
-          mma_kk(sK, sQ, tmem + C::TM_S);
+          mma_kk(sK, sQ0 + b1 * C::TB, tmem + C::TM_S);   // in-order after dV(n), which reads P^T from these columns
           mbar_wait(dq_empty, n & 1);
-          mbar_wait(do_full, (n + 1) & 1);
+          mbar_wait(&do_full[b1], ph1);
           tc_fence_after();
-          mma_kk(sV, sdO, tmem + C::TM_DP);
+          mma_kk(sV, sdO0 + b1 * C::TB, tmem + C::TM_DP);
           mma_commit(sdp_full);
         }
       }
@@ -197,8 +216,8 @@ __global__ void __launch_bounds__(320, 1)
     const long long key = (long long)jb * 128 + r;
     const float sl2 = a.scale_log2;
     const bool issuer = (warp & 3) == 0 && lane == 0;
-    uint8_t* staging = smem + (wg ? C::OFF_DS : C::OFF_P);  // free while the dQ reduce is in flight
-    const uint32_t pbase = smem_u32(smem + C::OFF_P), dsbase = smem_u32(smem + C::OFF_DS);
+    uint8_t* staging = smem + C::OFF_DS + wg * 16384;  // this warpgroup's half of dS^T, free after the dQ MMA
+    const uint32_t dsbase = smem_u32(smem + C::OFF_DS);
     for (int n = 0; n < N; ++n) {
       const int h = g * G + n / n_qt;
       const int qt = qt_begin + n % n_qt;
@@ -209,7 +228,7 @@ __global__ void __launch_bounds__(320, 1)
         if (wg == 0) s_lse2[sb][r] = q < a.S ? a.lse[(long long)h * a.ld_lse + q] * 1.4426950408889634f : 0.f;
         else s_delta[sb][r] = q < a.S ? a.delta[q * a.ld_delta + h] : 0.f;
       }
-      if (issuer) bulk_wait_read0();                  // previous dQ reduce has finished reading the staging smem
+      if (issuer) bulk_wait_read0();                  // previous dQ reduce has finished reading dS^T smem
       named_bar_sync(1, 256);
       mbar_wait(sdp_full, n & 1);
       tc_fence_after();
@@ -234,17 +253,21 @@ __global__ void __launch_bounds__(320, 1)
           p[i] = pv;
           ds[i] = pv * (__uint_as_float(rp[i]) - s_delta[sb][qi]);
         }
+        // P^T (bf16 pairs) back into the S^T columns already read: q [col0, col0+32) -> cols wg*64 + c*16 + [0,16)
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(p[2 * i], p[2 * i + 1]);
+        tmem_st16(tmem + C::TM_S + lane_off + wg * 64 + c * 16, pk);
 #pragma unroll
         for (int v8 = 0; v8 < 4; ++v8) {
           const int qc = col0 + v8 * 8;
           const uint32_t off = (qc >> 6) * 16384 + sw128_offset(r, qc & 63);
-          st_shared_v4(pbase + off, pack_bf16(p[v8 * 8 + 0], p[v8 * 8 + 1]), pack_bf16(p[v8 * 8 + 2], p[v8 * 8 + 3]),
-                       pack_bf16(p[v8 * 8 + 4], p[v8 * 8 + 5]), pack_bf16(p[v8 * 8 + 6], p[v8 * 8 + 7]));
           st_shared_v4(dsbase + off, pack_bf16(ds[v8 * 8 + 0], ds[v8 * 8 + 1]),
                        pack_bf16(ds[v8 * 8 + 2], ds[v8 * 8 + 3]), pack_bf16(ds[v8 * 8 + 4], ds[v8 * 8 + 5]),
                        pack_bf16(ds[v8 * 8 + 6], ds[v8 * 8 + 7]));
         }
       }
+      tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(ds_full);
@@ -260,22 +283,24 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t stbase = smem_u32(staging);
 #pragma unroll
       for (int b = 0; b < C::DQ_BOXES; ++b) {
+        if (b > 0) {                      // staging holds one 32-column box: wait for the previous reduce to read it
+          if (issuer) bulk_wait_read0();
+          named_bar_sync(2 + wg, 128);
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {     // 16-byte chunk j of the 128-byte row, swizzled by row % 8
-          const uint32_t addr = stbase + b * 16384 + r * 128 + ((j ^ (r & 7)) << 4);
+          const uint32_t addr = stbase + r * 128 + ((j ^ (r & 7)) << 4);
           st_shared_v4(addr, __float_as_uint(__uint_as_float(rq[b][4 * j + 0]) * a.scale),
                        __float_as_uint(__uint_as_float(rq[b][4 * j + 1]) * a.scale),
                        __float_as_uint(__uint_as_float(rq[b][4 * j + 2]) * a.scale),
                        __float_as_uint(__uint_as_float(rq[b][4 * j + 3]) * a.scale));
         }
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(2 + wg, 128);
-      if (issuer) {
-#pragma unroll
-        for (int b = 0; b < C::DQ_BOXES; ++b)
-          tma_reduce_add_2d(&tmdQ, staging + b * 16384, h * D + wg * (D / 2) + b * 32, (int)q0);
-        bulk_commit();
+        fence_proxy_async_smem();
+        named_bar_sync(2 + wg, 128);
+        if (issuer) {
+          tma_reduce_add_2d(&tmdQ, staging, h * D + wg * (D / 2) + b * 32, (int)q0);
+          bulk_commit();
+        }
       }
     }
     if (issuer) bulk_wait0();
