@@ -8,18 +8,20 @@
 //   dV  += P^T dO         (TMEM [256, 256+d))      A operand P^T read from TMEM (TS form)
 //   dK  += dS^T Q         (TMEM [256+d, 256+2d))
 //   dQ   = dS K           (TMEM cols [128,128+d), reusing dP^T once consumed)
-// P^T lives in the S^T columns it was computed from (two bf16 per 32-bit column),
-// which frees the shared memory for double-buffered Q / dO tiles: the TMA loads of
-// tile n+1 overlap the MMAs of tile n.
-// dQ is reduced across KV tiles in HBM by TMA bulk reduce-add (fp32): the compute
-// warps drain it TMEM -> shared memory (the dS^T buffer, free once the dQ MMA has
-// completed) and one thread per warpgroup issues cp.reduce.async.bulk.tensor.
+// P^T lives in the S^T columns it was computed from (two bf16 per 32-bit column).
+// dQ is reduced across KV tiles in HBM by TMA bulk reduce-add (fp32): each compute
+// warpgroup drains its half of dQ TMEM -> shared memory (32-column boxes) and one
+// of its threads issues cp.reduce.async.bulk.tensor; the 1/sqrt(d) scale of dQ is
+// applied when the accumulator is converted to bf16.
 // dK/dV stay in TMEM for the whole CTA and are written (and optionally accumulated
 // across the UPipe stages of one super-stage) at the end.
-// Warps: 0-7 compute (two warpgroups splitting the 128 query columns; thread =
-// one key row for S^T/dP^T, one query row for the dQ drain), 8 TMA producer,
-// 9 MMA issuer.
+// Warps: 0-7 compute (two warpgroups, each owning 64 of the 128 query columns of
+// S^T/dP^T; thread = one key row there, one query row for the dQ drain), warp 8
+// TMA producer, warp 9 MMA issuer. The XU pipe executes both MUFU.EX2 and the bf16
+// packs at 16 lane-ops/clk/SM (measured), so 3 of 4 exponentials run as a
+// polynomial on the FMA pipe (ex2_fma) to balance the pipes.
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -41,6 +43,7 @@ struct BwdArgs {
   int nq, nkv, causal, kv_accumulate, kv_write_acc;
   float scale;       // 1/sqrt(d)
   float scale_log2;  // log2(e)/sqrt(d)
+  long long* dbg;    // optional per-role cycle breakdown of CTA (0,0) (UPIPE_BWD_TIMELINE=1)
 };
 
 __device__ __forceinline__ float ex2b(float x) {
@@ -49,21 +52,27 @@ __device__ __forceinline__ float ex2b(float x) {
   return y;
 }
 
+constexpr int kComputeWarps = 8;
+constexpr int kThreads = (kComputeWarps + 2) * 32;
+constexpr int kTmaWarp = kComputeWarps, kMmaWarp = kComputeWarps + 1;
+
 template <int D>
 struct BwdCfg {
   static constexpr int TB = 128 * D * 2;   // one 128 x D bf16 tile
   static constexpr int PB = 128 * 128 * 2; // 128 x 128 bf16
-  static constexpr int OFF_K = 0, OFF_V = TB, OFF_Q = 2 * TB, OFF_DO = 4 * TB;  // Q, dO: 2 buffers each
-  static constexpr int OFF_DS = 6 * TB;
-  static constexpr int OFF_BAR = OFF_DS + PB;
-  static constexpr int OFF_STAT = OFF_BAR + 256;             // lse2[2][128], delta[2][128] fp32
-  static constexpr int SMEM = OFF_STAT + 2048;                // base is 1024-aligned (checked in-kernel)
+  static constexpr int OFF_K = 0, OFF_V = TB, OFF_Q = 2 * TB;   // Q: 2 buffers
+  static constexpr int OFF_DO = 4 * TB;
+  static constexpr int OFF_DS = 5 * TB;
+  static constexpr int OFF_STG = OFF_DS + PB;                    // dQ staging slots 0,1 (16 KB each); 2,3 alias dS^T
+  static constexpr int OFF_BAR = OFF_STG + 32768;
+  static constexpr int OFF_STAT = OFF_BAR + 256;                 // lse2[2][128], delta[2][128] fp32
+  static constexpr int SMEM = OFF_STAT + 2048;                    // base is 1024-aligned (checked in-kernel)
   static constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 128, TM_DV = 256, TM_DK = 256 + D;
-  static constexpr int DQ_BOXES = D / 64;  // 32-float boxes of dQ per warpgroup (each drains D/2 columns)
+  static constexpr int DQ_BOXES = D / 32;                         // 32-column fp32 boxes of dQ per query tile
 };
 
 template <int D>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                     const __grid_constant__ CUtensorMap tmdQ, const BwdArgs a) {
@@ -77,13 +86,13 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* kv_full = bars + 0;
   uint64_t* q_full = bars + 1;     // [2]
   uint64_t* q_empty = bars + 3;    // [2]
-  uint64_t* do_full = bars + 5;    // [2]
-  uint64_t* do_empty = bars + 7;   // [2]
-  uint64_t* sdp_full = bars + 9;
-  uint64_t* ds_full = bars + 10;
-  uint64_t* dq_full = bars + 11;
-  uint64_t* dq_empty = bars + 12;
-  uint64_t* dkv_full = bars + 13;
+  uint64_t* do_full = bars + 5;
+  uint64_t* do_empty = bars + 6;
+  uint64_t* sdp_full = bars + 7;
+  uint64_t* ds_full = bars + 8;
+  uint64_t* dq_full = bars + 9;
+  uint64_t* dq_empty = bars + 10;
+  uint64_t* dkv_full = bars + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = warp_id(), lane = lane_id();
@@ -94,19 +103,20 @@ __global__ void __launch_bounds__(320, 1)
   const int qt_begin = a.causal ? jb : 0;
   const int n_qt = nT - qt_begin;
   const int N = G * n_qt;                         // (head, query tile) iterations
+  constexpr int kCompute = kComputeWarps * 32;
 
-  if (warp == 8 && lane == 0) {
+  if (warp == kTmaWarp && lane == 0) {
     tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
-    for (int i = 0; i < 14; ++i) mbar_init(&bars[i], (i == 10 || i == 12) ? 256 : 1);
+    for (int i = 0; i < 12; ++i) mbar_init(&bars[i], (i == 8 || i == 10) ? kCompute : 1);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == kTmaWarp) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       mbar_arrive_expect_tx(kv_full, 2 * C::TB);
@@ -119,27 +129,27 @@ __global__ void __launch_bounds__(320, 1)
         const int h = g * G + n / n_qt;
         const int qt = qt_begin + n % n_qt;
         const int b = n & 1;
-        const uint32_t ph = ((n >> 1) & 1) ^ 1;
-        mbar_wait(&q_empty[b], ph);
+        mbar_wait(&q_empty[b], ((n >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&q_full[b], C::TB);
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
           tma_load_3d(smem + C::OFF_Q + b * C::TB + c * 16384, &tmQ, &q_full[b], c * 64, h, qt * 128);
-        mbar_wait(&do_empty[b], ph);
-        mbar_arrive_expect_tx(&do_full[b], C::TB);
+        mbar_wait(do_empty, (n & 1) ^ 1);
+        mbar_arrive_expect_tx(do_full, C::TB);
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
-          tma_load_3d(smem + C::OFF_DO + b * C::TB + c * 16384, &tmdO, &do_full[b], c * 64, h, qt * 128);
+          tma_load_3d(smem + C::OFF_DO + c * 16384, &tmdO, do_full, c * 64, h, qt * 128);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaWarp) {
     if (lane == 0) {
       // ------------------------------------------------ MMA issuer
+      long long tl[5] = {0, 0, 0, 0, 0};
       constexpr uint32_t id_kk = idesc_bf16(128, 128, false, false);  // S^T, dP^T: both K-major over d
       constexpr uint32_t id_kmn = idesc_bf16(128, D, false, true);    // dV (A in TMEM), dK: B MN-major
       constexpr uint32_t id_mnmn = idesc_bf16(128, D, true, true);    // dQ: A = dS^T viewed MN-major, B = K MN-major
       const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
-      const uint32_t sQ0 = smem_u32(smem + C::OFF_Q), sdO0 = smem_u32(smem + C::OFF_DO);
+      const uint32_t sQ0 = smem_u32(smem + C::OFF_Q), sdO = smem_u32(smem + C::OFF_DO);
       const uint32_t sdS = smem_u32(smem + C::OFF_DS);
       auto mma_kk = [&](uint32_t sa, uint32_t sb, uint32_t tm) {      // [128 x D] x [128 x D]^T
 #pragma unroll
@@ -157,13 +167,12 @@ __global__ void __launch_bounds__(320, 1)
             mma_ss(tm, desc_sw128(sa + kb * 16384 + kk * 32, 16, 1024),
                    desc_sw128(sb + kb * 8192 + kk * 2048, 16384, 1024), id_kmn, (acc || kb || kk) ? 1u : 0u);
       };
-      auto mma_tmn = [&](uint32_t ta, uint32_t sb, uint32_t tm, bool acc) {  // A = P^T in TMEM (q 0-63 at +0, 64-127 at +64)
+      // A = P^T in TMEM: queries [16 ks, 16 ks + 16) are packed at TMEM cols 64 (ks / 4) + 8 (ks % 4)
+      auto mma_tmn = [&](uint32_t ta, uint32_t sb, uint32_t tm, bool acc) {
 #pragma unroll
-        for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_ts(tm, ta + kb * 64 + kk * 8, desc_sw128(sb + kb * 8192 + kk * 2048, 16384, 1024), id_kmn,
-                   (acc || kb || kk) ? 1u : 0u);
+        for (int ks = 0; ks < 8; ++ks)
+          mma_ts(tm, ta + (ks >> 2) * 64 + (ks & 3) * 8, desc_sw128(sb + (ks >> 2) * 8192 + (ks & 3) * 2048, 16384, 1024),
+                 id_kmn, (acc || ks) ? 1u : 0u);
       };
       auto mma_mnmn = [&](uint32_t sa, uint32_t sb, uint32_t tm) {  // dQ = dS K: K dim = keys (rows of both)
 #pragma unroll
@@ -177,152 +186,201 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(&q_full[0], 0);
       tc_fence_after();
       mma_kk(sK, sQ0, tmem + C::TM_S);
-      mbar_wait(&do_full[0], 0);
+      mbar_wait(do_full, 0);
       tc_fence_after();
-      mma_kk(sV, sdO0, tmem + C::TM_DP);
+      mma_kk(sV, sdO, tmem + C::TM_DP);
       mma_commit(sdp_full);
       for (int n = 0; n < N; ++n) {
         const int b = n & 1;
-        const uint32_t sQ = sQ0 + b * C::TB, sdO = sdO0 + b * C::TB;
+        long long t0 = clock64();
         mbar_wait(ds_full, n & 1);
+        long long t1 = clock64();
+        tl[0] += t1 - t0;
         tc_fence_after();
         mma_tmn(tmem + C::TM_S, sdO, tmem + C::TM_DV, n > 0);
-        mma_commit(&do_empty[b]);
-        mma_kmn(sdS, sQ, tmem + C::TM_DK, n > 0);
+        mma_commit(do_empty);
+        mma_kmn(sdS, sQ0 + b * C::TB, tmem + C::TM_DK, n > 0);
         mma_commit(&q_empty[b]);
         mma_mnmn(sdS, sK, tmem + C::TM_DQ);
         mma_commit(dq_full);
+        tl[1] += clock64() - t1;
         if (n + 1 < N) {
           const int b1 = (n + 1) & 1;
-          const uint32_t ph1 = ((n + 1) >> 1) & 1;
-          mbar_wait(&q_full[b1], ph1);
+          long long t2 = clock64();
+          mbar_wait(&q_full[b1], ((n + 1) >> 1) & 1);
+          tl[2] += clock64() - t2;
           tc_fence_after();
           mma_kk(sK, sQ0 + b1 * C::TB, tmem + C::TM_S);   // in-order after dV(n), which reads P^T from these columns
+          long long t3 = clock64();
           mbar_wait(dq_empty, n & 1);
-          mbar_wait(&do_full[b1], ph1);
+          long long t4 = clock64();
+          mbar_wait(do_full, (n + 1) & 1);
+          tl[3] += t4 - t3;
+          tl[4] += clock64() - t4;
           tc_fence_after();
-          mma_kk(sV, sdO0 + b1 * C::TB, tmem + C::TM_DP);
+          mma_kk(sV, sdO, tmem + C::TM_DP);
           mma_commit(sdp_full);
         }
       }
       mma_commit(dkv_full);
+      if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0)
+        for (int i = 0; i < 5; ++i) a.dbg[5 + i] = tl[i];
     }
   } else {
     // ------------------------------------------------ compute warpgroups (warps 0-7)
-    const int wg = warp >> 2;                         // query columns [64 wg, 64 wg + 64) ; dQ cols [wg D/2, ...)
+    const int wg = warp >> 2;                         // query columns [64 wg, 64 wg + 64) in two 32-column chunks
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const long long key = (long long)jb * 128 + r;
     const float sl2 = a.scale_log2;
-    const bool issuer = (warp & 3) == 0 && lane == 0;
-    uint8_t* staging = smem + C::OFF_DS + wg * 16384;  // this warpgroup's half of dS^T, free after the dQ MMA
-    const uint32_t dsbase = smem_u32(smem + C::OFF_DS);
+    const bool issuer = quad == 0 && lane == 0;
+    constexpr int kBoxesPerWg = C::DQ_BOXES / 2;      // dQ boxes (32 fp32 columns) drained per warpgroup
+    // staging slot of box b of this warpgroup: slots 0,1 = spare buffer, slots 2,3 = dS^T (free after the dQ MMA)
+    auto slot = [&](int b) -> uint8_t* {
+      const int s_ = wg * kBoxesPerWg + b;
+      return s_ < 2 ? smem + C::OFF_STG + s_ * 16384 : smem + C::OFF_DS + (s_ - 2) * 16384;
+    };
+    const uint32_t dsbase = smem_u32(smem + C::OFF_DS) + wg * 16384;   // dS^T chunk of this warpgroup's 64 queries
+    float stat_next = 0.f;                            // warpgroup 0 prefetches lse, warpgroup 1 delta, one tile ahead
+    auto load_stat = [&](int n) -> float {
+      const int h = g * G + n / n_qt;
+      const long long q = (long long)(qt_begin + n % n_qt) * 128 + r;
+      if (q >= a.S) return 0.f;
+      return wg == 0 ? a.lse[(long long)h * a.ld_lse + q] * 1.4426950408889634f : a.delta[q * a.ld_delta + h];
+    };
+    if (N > 0) stat_next = load_stat(0);
+    long long tl[5] = {0, 0, 0, 0, 0};
     for (int n = 0; n < N; ++n) {
       const int h = g * G + n / n_qt;
       const int qt = qt_begin + n % n_qt;
       const long long q0 = (long long)qt * 128;
       const int sb = n & 1;
-      {
-        const long long q = q0 + r;
-        if (wg == 0) s_lse2[sb][r] = q < a.S ? a.lse[(long long)h * a.ld_lse + q] * 1.4426950408889634f : 0.f;
-        else s_delta[sb][r] = q < a.S ? a.delta[q * a.ld_delta + h] : 0.f;
-      }
-      if (issuer) bulk_wait_read0();                  // previous dQ reduce has finished reading dS^T smem
-      named_bar_sync(1, 256);
+      if (wg == 0) s_lse2[sb][r] = stat_next;
+      else s_delta[sb][r] = stat_next;
+      if (n + 1 < N) stat_next = load_stat(n + 1);
+      if (issuer) bulk_wait_read0();                  // previous dQ reduces have finished reading the staging slots
+      long long c0 = clock64();
+      named_bar_sync(1, kCompute);
+      long long c1 = clock64();
       mbar_wait(sdp_full, n & 1);
+      long long c2 = clock64();
+      tl[0] += c1 - c0;
+      tl[1] += c2 - c1;
       tc_fence_after();
-      const bool diag = a.causal && qt == jb;
-      const bool tail = q0 + 128 > a.S || (long long)jb * 128 + 128 > a.S;
+      const bool need_mask = (a.causal && qt == jb) || q0 + 128 > a.S || (long long)jb * 128 + 128 > a.S;
+      const long long qmin = key >= a.S ? a.S : (a.causal ? key : 0);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int col0 = wg * 64 + c * 32;
         uint32_t rs[32], rp[32];
         tmem_ld32(tmem + C::TM_S + lane_off + col0, rs);
         tmem_ld32(tmem + C::TM_DP + lane_off + col0, rp);
+        const float4* l4 = reinterpret_cast<const float4*>(&s_lse2[sb][col0]);
+        const float4* d4 = reinterpret_cast<const float4*>(&s_delta[sb][col0]);
         tmem_wait_ld();
-        float p[32], ds[32];
+        // P = 2^(s*c - lse2): 1 in 4 on MUFU, 3 in 4 on the FMA pipe (the XU pipe also packs bf16)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int qi = col0 + i;
-          float pv = ex2b(__uint_as_float(rs[i]) * sl2 - s_lse2[sb][qi]);
-          if (diag || tail) {
-            const long long q = q0 + qi;
-            if ((a.causal && key > q) || q >= a.S || key >= a.S) pv = 0.f;
-          }
-          p[i] = pv;
-          ds[i] = pv * (__uint_as_float(rp[i]) - s_delta[sb][qi]);
+        for (int i4 = 0; i4 < 8; ++i4) {
+          const float4 x = l4[i4];
+          rs[4 * i4 + 0] = __float_as_uint(ex2b(fmaf(__uint_as_float(rs[4 * i4 + 0]), sl2, -x.x)));
+          rs[4 * i4 + 1] = __float_as_uint(ex2_fma(fmaf(__uint_as_float(rs[4 * i4 + 1]), sl2, -x.y)));
+          rs[4 * i4 + 2] = __float_as_uint(ex2_fma(fmaf(__uint_as_float(rs[4 * i4 + 2]), sl2, -x.z)));
+          rs[4 * i4 + 3] = __float_as_uint(ex2_fma(fmaf(__uint_as_float(rs[4 * i4 + 3]), sl2, -x.w)));
         }
-        // P^T (bf16 pairs) back into the S^T columns already read: q [col0, col0+32) -> cols wg*64 + c*16 + [0,16)
-        uint32_t pk[16];
+        if (need_mask) {                               // uniform branch: only diagonal / ragged tiles
 #pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(p[2 * i], p[2 * i + 1]);
-        tmem_st16(tmem + C::TM_S + lane_off + wg * 64 + c * 16, pk);
+          for (int i = 0; i < 32; ++i) {
+            const long long q = q0 + col0 + i;
+            rs[i] = (q >= qmin && q < a.S) ? rs[i] : 0u;
+          }
+        }
+#pragma unroll
+        for (int i4 = 0; i4 < 8; ++i4) {
+          const float4 y = d4[i4];
+          rp[4 * i4 + 0] = __float_as_uint(__uint_as_float(rs[4 * i4 + 0]) * (__uint_as_float(rp[4 * i4 + 0]) - y.x));
+          rp[4 * i4 + 1] = __float_as_uint(__uint_as_float(rs[4 * i4 + 1]) * (__uint_as_float(rp[4 * i4 + 1]) - y.y));
+          rp[4 * i4 + 2] = __float_as_uint(__uint_as_float(rs[4 * i4 + 2]) * (__uint_as_float(rp[4 * i4 + 2]) - y.z));
+          rp[4 * i4 + 3] = __float_as_uint(__uint_as_float(rs[4 * i4 + 3]) * (__uint_as_float(rp[4 * i4 + 3]) - y.w));
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          rs[i] = pack_bf16(__uint_as_float(rs[2 * i]), __uint_as_float(rs[2 * i + 1]));
+        // P^T (bf16 pairs) back into S^T columns already read: queries [col0, col0+32) -> cols 64 wg + 16 c
+        tmem_st16(tmem + C::TM_S + lane_off + wg * 64 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(rs));
 #pragma unroll
         for (int v8 = 0; v8 < 4; ++v8) {
-          const int qc = col0 + v8 * 8;
-          const uint32_t off = (qc >> 6) * 16384 + sw128_offset(r, qc & 63);
-          st_shared_v4(dsbase + off, pack_bf16(ds[v8 * 8 + 0], ds[v8 * 8 + 1]),
-                       pack_bf16(ds[v8 * 8 + 2], ds[v8 * 8 + 3]), pack_bf16(ds[v8 * 8 + 4], ds[v8 * 8 + 5]),
-                       pack_bf16(ds[v8 * 8 + 6], ds[v8 * 8 + 7]));
+          const int qc = c * 32 + v8 * 8;
+          st_shared_v4(dsbase + sw128_offset(r, qc),
+                       pack_bf16(__uint_as_float(rp[v8 * 8 + 0]), __uint_as_float(rp[v8 * 8 + 1])),
+                       pack_bf16(__uint_as_float(rp[v8 * 8 + 2]), __uint_as_float(rp[v8 * 8 + 3])),
+                       pack_bf16(__uint_as_float(rp[v8 * 8 + 4]), __uint_as_float(rp[v8 * 8 + 5])),
+                       pack_bf16(__uint_as_float(rp[v8 * 8 + 6]), __uint_as_float(rp[v8 * 8 + 7])));
         }
       }
       tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(ds_full);
-      // ---- dQ drain: TMEM lane = query row; this warpgroup takes dQ columns [wg D/2, (wg+1) D/2)
+      long long c3 = clock64();
+      tl[2] += c3 - c2;
+      // ---- dQ drain: TMEM lane = query row; this warpgroup drains dQ columns [wg D/2, (wg+1) D/2)
       mbar_wait(dq_full, n & 1);
+      long long c4 = clock64();
+      tl[3] += c4 - c3;
       tc_fence_after();
-      uint32_t rq[C::DQ_BOXES][32];
+      uint32_t rq[kBoxesPerWg][32];
 #pragma unroll
-      for (int b = 0; b < C::DQ_BOXES; ++b) tmem_ld32(tmem + C::TM_DQ + lane_off + wg * (D / 2) + b * 32, rq[b]);
+      for (int b = 0; b < kBoxesPerWg; ++b) tmem_ld32(tmem + C::TM_DQ + lane_off + (wg * kBoxesPerWg + b) * 32, rq[b]);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(dq_empty);
-      const uint32_t stbase = smem_u32(staging);
 #pragma unroll
-      for (int b = 0; b < C::DQ_BOXES; ++b) {
-        if (b > 0) {                      // staging holds one 32-column box: wait for the previous reduce to read it
-          if (issuer) bulk_wait_read0();
-          named_bar_sync(2 + wg, 128);
-        }
+      for (int b = 0; b < kBoxesPerWg; ++b) {
+        const uint32_t stbase = smem_u32(slot(b));
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {     // 16-byte chunk j of the 128-byte row, swizzled by row % 8
-          const uint32_t addr = stbase + r * 128 + ((j ^ (r & 7)) << 4);
-          st_shared_v4(addr, __float_as_uint(__uint_as_float(rq[b][4 * j + 0]) * a.scale),
+        for (int j = 0; j < 8; ++j)       // 16-byte chunk j of the 128-byte row, swizzled by row % 8
+          st_shared_v4(stbase + r * 128 + ((j ^ (r & 7)) << 4),
+                       __float_as_uint(__uint_as_float(rq[b][4 * j + 0]) * a.scale),
                        __float_as_uint(__uint_as_float(rq[b][4 * j + 1]) * a.scale),
                        __float_as_uint(__uint_as_float(rq[b][4 * j + 2]) * a.scale),
                        __float_as_uint(__uint_as_float(rq[b][4 * j + 3]) * a.scale));
-        }
-        fence_proxy_async_smem();
-        named_bar_sync(2 + wg, 128);
-        if (issuer) {
-          tma_reduce_add_2d(&tmdQ, staging, h * D + wg * (D / 2) + b * 32, (int)q0);
-          bulk_commit();
-        }
       }
+      fence_proxy_async_smem();
+      named_bar_sync(2 + wg, 128);
+      if (issuer) {
+#pragma unroll
+        for (int b = 0; b < kBoxesPerWg; ++b)
+          tma_reduce_add_2d(&tmdQ, slot(b), h * D + (wg * kBoxesPerWg + b) * 32, (int)q0);
+        bulk_commit();
+      }
+      tl[4] += clock64() - c4;
     }
     if (issuer) bulk_wait0();
-    // ---- dK / dV epilogue (TMEM lane = key row): warpgroup 0 writes dV, warpgroup 1 writes dK
+    if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && warp == 0 && lane == 0) {
+      for (int i = 0; i < 5; ++i) a.dbg[i] = tl[i];
+      a.dbg[10] = N;
+    }
+    // ---- dK / dV epilogue (TMEM lane = key row): warpgroup 0 writes dV, warpgroup 1 dK
     mbar_wait(dkv_full, 0);
     tc_fence_after();
     const long long ldacc = (long long)a.nkv * D;
-    const int which = wg;
+    const int which = wg;                           // 0: dV, 1: dK
+    const int cbeg = 0;
     const uint32_t tcol = which ? C::TM_DK : C::TM_DV;
     const float sc = which ? a.scale : 1.f;
     float* acc = (which ? a.dk_acc : a.dv_acc);
     __nv_bfloat16* ob = which ? a.dk_bf16 : a.dv_bf16;
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = cbeg; c < cbeg + D; c += 32) {
       uint32_t rr[32];
-      tmem_ld32(tmem + tcol + lane_off + c * 32, rr);
+      tmem_ld32(tmem + tcol + lane_off + c, rr);
       tmem_wait_ld();
       if (key >= a.S || N == 0) continue;
       float v[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]) * sc;
-      float4* accp = acc ? reinterpret_cast<float4*>(acc + key * ldacc + (long long)g * D + c * 32) : nullptr;
+      float4* accp = acc ? reinterpret_cast<float4*>(acc + key * ldacc + (long long)g * D + c) : nullptr;
       if (a.kv_accumulate && accp) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -335,7 +393,7 @@ __global__ void __launch_bounds__(320, 1)
         for (int i = 0; i < 8; ++i) accp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
       }
       if (ob) {
-        uint4* dst = reinterpret_cast<uint4*>(ob + key * a.ld_kvb + (long long)g * D + c * 32);
+        uint4* dst = reinterpret_cast<uint4*>(ob + key * a.ld_kvb + (long long)g * D + c);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           dst[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
@@ -345,7 +403,7 @@ __global__ void __launch_bounds__(320, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -386,6 +444,15 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   a.kv_write_acc = p.kv_write_acc;
   a.scale = 1.f / sqrtf((float)p.d);
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)p.d);
+  // UPIPE_BWD_TIMELINE=1: per-role cycle breakdown of CTA (0,0), printed to stderr after the launch
+  static long long* dbg_dev = nullptr;
+  const char* tlenv = getenv("UPIPE_BWD_TIMELINE");
+  a.dbg = nullptr;
+  if (tlenv && tlenv[0] == '1') {
+    if (!dbg_dev) cudaMalloc(&dbg_dev, 16 * sizeof(long long));
+    cudaMemsetAsync(dbg_dev, 0, 16 * sizeof(long long), stream);
+    a.dbg = dbg_dev;
+  }
   const int nT = (int)((p.S + 127) / 128);
   dim3 grid(nT, p.nkv);
   cudaError_t e;
@@ -393,17 +460,27 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
     static const cudaError_t attr =
         cudaFuncSetAttribute(attn_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<128>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
-    attn_bwd_kernel<128><<<grid, 320, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
+    attn_bwd_kernel<128><<<grid, kThreads, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
     count_launches(1);
   } else {
     static const cudaError_t attr =
         cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<64>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
-    attn_bwd_kernel<64><<<grid, 320, BwdCfg<64>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
+    attn_bwd_kernel<64><<<grid, kThreads, BwdCfg<64>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
     count_launches(1);
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) snprintf(err, errlen, "attn_bwd launch: %s", cudaGetErrorString(e));
+  if (a.dbg) {
+    long long h[16];
+    cudaMemcpyAsync(h, a.dbg, sizeof h, cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    fprintf(stderr,
+            "[attn_bwd timeline CTA(0,0) N=%lld cycles] compute: bar %lld wait_sdp %lld E %lld wait_dq %lld drain %lld | "
+            "mma: wait_ds %lld issue_3mma %lld wait_q %lld wait_dqempty %lld wait_do %lld | "
+            "E: ld %lld math %lld pack+st %lld wait_st %lld\n",
+            h[10], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[11], h[12], h[13], h[14]);
+  }
   return e;
 }
 

@@ -201,6 +201,28 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// bf16x2 RNE pack on the integer pipes (same bits as cvt.rn.bf16x2.f32 for finite inputs),
+// used to move conversions off the XU pipe, which also runs MUFU.EX2 (16 lane-ops/clk/SM each).
+__device__ __forceinline__ uint32_t pack_bf16_alu(float lo, float hi) {
+  uint32_t a = __float_as_uint(lo), b = __float_as_uint(hi);
+  a += 0x7FFFu + ((a >> 16) & 1u);
+  b += 0x7FFFu + ((b >> 16) & 1u);
+  return __byte_perm(a, b, 0x7632);
+}
+
+// 2^x on the FMA pipe (x <= 0 ... small positive): round-to-nearest split x = n + f, f in [-1/2, 1/2],
+// 2^f by a degree-3 minimax polynomial (max rel. error 1.1e-4, below bf16 resolution of P),
+// 2^n added to the exponent with one integer multiply-add. Inputs below -126 flush towards 0.
+__device__ __forceinline__ float ex2_fma(float x) {
+  x = fmaxf(x, -126.f);
+  const float r = x + 12582912.f;           // 1.5 * 2^23: low mantissa bits hold round(x)
+  const float f = x - (r - 12582912.f);
+  float p = fmaf(f, 0.055008927131519f, 0.242210991999625f);   // relative-error minimax fit on [-1/2, 1/2]
+  p = fmaf(p, f, 0.693282931500773f);
+  p = fmaf(p, f, 1.0f);
+  return __uint_as_float(__float_as_uint(p) + (__float_as_uint(r) << 23));
+}
+
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
