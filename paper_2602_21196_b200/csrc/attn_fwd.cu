@@ -2,13 +2,14 @@
 //
 // One CTA owns two consecutive 128-row query tiles (A, B) of one local head and
 // streams the KV tiles of the head's KV group through shared memory (TMA, 128B
-// swizzle). Warp roles (320 threads):
+// swizzle). Warp roles (384 threads; setmaxnreg: softmax 200 registers, others 56):
 //   warps 0-3  softmax for tile A  (thread = one query row: the 32x32b TMEM load
 //              gives each thread a whole S row, so row max / row sum are
 //              thread-local and need no shuffles)
 //   warps 4-7  softmax for tile B
 //   warp 8     TMA producer (Q once, then K and V per KV tile)
-//   warp 9     MMA issuer: S = Q K^T into TMEM, O += P V with P staged in smem
+//   warp 9     MMA issuer: S = Q K^T into TMEM, O += P V with P (bf16) read from TMEM
+//   warps 10-11 idle (complete the third warpgroup for setmaxnreg)
 // TMEM (512 columns): S_A | S_B | O_A | O_B (d = 128). While one warpgroup runs
 // its softmax the tensor core computes the other tile's S or PV (ping-pong).
 // Online softmax in the exp2 domain with the log2(e)/sqrt(d) scale folded into
@@ -34,6 +35,11 @@ struct FwdArgs {
   float scale_log2;  // log2(e) / sqrt(d)
 };
 
+template <uint32_t N>
+__device__ __forceinline__ void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+template <uint32_t N>
+__device__ __forceinline__ void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -44,21 +50,18 @@ template <int D>
 struct FwdCfg {
   static constexpr int TILE = 128;
   static constexpr int QBYTES = TILE * D * 2;       // one 128 x D bf16 tile
-  static constexpr int KV_STAGES = (D == 64) ? 2 : 1;
-  static constexpr int PBYTES = TILE * TILE * 2;    // P tile 128 x 128 bf16
+  static constexpr int KV_STAGES = 2;               // P lives in TMEM, so smem holds Q_A, Q_B and 2 K/V stages
   static constexpr int OFF_QA = 0;
   static constexpr int OFF_QB = QBYTES;
   static constexpr int OFF_K = 2 * QBYTES;
   static constexpr int OFF_V = OFF_K + KV_STAGES * QBYTES;
-  static constexpr int OFF_PA = OFF_V + KV_STAGES * QBYTES;
-  static constexpr int OFF_PB = OFF_PA + PBYTES;
-  static constexpr int OFF_BAR = OFF_PB + PBYTES;
+  static constexpr int OFF_BAR = OFF_V + KV_STAGES * QBYTES;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr uint32_t TM_SA = 0, TM_SB = 128, TM_OA = 256, TM_OB = 256 + D;
 };
 
 template <int D>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
   using C = FwdCfg<D>;
@@ -103,6 +106,7 @@ __global__ void __launch_bounds__(320, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  if (warp >= 8) regs_dec<56>();      // warpgroup 2 (TMA, MMA, 2 idle warps) gives registers to softmax
   if (warp == 8) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
@@ -131,7 +135,7 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       // ------------------------------------------------ MMA issuer
       constexpr uint32_t idS = idesc_bf16(128, 128, false, false);  // Q (K-major) x K (K-major)
-      constexpr uint32_t idO = idesc_bf16(128, D, false, true);     // P (K-major) x V (MN-major)
+      constexpr uint32_t idO = idesc_bf16(128, D, false, true);     // P (TMEM) x V (MN-major)
       const uint32_t sQA = smem_u32(smem + C::OFF_QA), sQB = smem_u32(smem + C::OFF_QB);
       auto issue_S = [&](uint32_t sq, uint32_t sk, uint32_t tm) {
 #pragma unroll
@@ -141,13 +145,12 @@ __global__ void __launch_bounds__(320, 1)
             mma_ss(tm, desc_sw128(sq + c * 16384 + kk * 32, 16, 1024), desc_sw128(sk + c * 16384 + kk * 32, 16, 1024),
                    idS, (c | kk) != 0);
       };
-      auto issue_PV = [&](uint32_t sp, uint32_t sv, uint32_t tm, bool acc) {
+      // O += P V with A = P in TMEM: keys [16 ks, 16 ks + 16) packed (bf16 pairs) at S columns 8 ks
+      auto issue_PV = [&](uint32_t tp, uint32_t sv, uint32_t tm, bool acc) {
 #pragma unroll
-        for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_ss(tm, desc_sw128(sp + kb * 16384 + kk * 32, 16, 1024),
-                   desc_sw128(sv + kb * 8192 + kk * 2048, 16384, 1024), idO, (acc || kb || kk) ? 1u : 0u);
+        for (int ks = 0; ks < 8; ++ks)
+          mma_ts(tm, tp + ks * 8, desc_sw128(sv + (ks >> 2) * 8192 + (ks & 3) * 2048, 16384, 1024), idO,
+                 (acc || ks) ? 1u : 0u);
       };
       mbar_wait(q_full, 0);
       mbar_wait(&k_full[0], 0);
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(320, 1)
         if (it < nA) {
           mbar_wait(&p_full[0], it & 1);
           tc_fence_after();
-          issue_PV(smem_u32(smem + C::OFF_PA), sv, tmem + C::TM_OA, it > 0);
+          issue_PV(tmem + C::TM_SA, sv, tmem + C::TM_OA, it > 0);
           mma_commit(&o_full[0]);
         }
         const bool more = it + 1 < nB;
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(320, 1)
         // ---- tile B
         mbar_wait(&p_full[1], it & 1);
         tc_fence_after();
-        issue_PV(smem_u32(smem + C::OFF_PB), sv, tmem + C::TM_OB, it > 0);
+        issue_PV(tmem + C::TM_SB, sv, tmem + C::TM_OB, it > 0);
         mma_commit(&o_full[1]);
         mma_commit(&v_empty[st]);
         if (more) {
@@ -191,8 +194,9 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
     }
-  } else {
+  } else if (warp < 8) {
     // ------------------------------------------------ softmax warpgroups
+    regs_inc<200>();
     const int wg = warp >> 2;                       // 0: tile A, 1: tile B
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
@@ -201,7 +205,6 @@ __global__ void __launch_bounds__(320, 1)
     const int n = wg ? nB : nA;
     const uint32_t tS = tmem + (wg ? C::TM_SB : C::TM_SA) + ((uint32_t)(quad * 32) << 16);
     const uint32_t tO = tmem + (wg ? C::TM_OB : C::TM_OA) + ((uint32_t)(quad * 32) << 16);
-    uint8_t* sP = smem + (wg ? C::OFF_PB : C::OFF_PA);
     const float sl2 = a.scale_log2;
     float m_ref = -INFINITY, l_run = 0.f;
     for (int it = 0; it < n; ++it) {
@@ -242,21 +245,14 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
       for (int i = 0; i < 128; ++i) {
         const float x = fmaf(s[i], sl2, -m_ref);
-        s[i] = ex2(x);
-      }
-      if (edge) {                                      // masked keys: exact zeros (ex2_fma floors at 2^-126)
-#pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          const long long key = key0 + i;
-          if ((a.causal && key > q) || key >= a.S) s[i] = 0.f;
-        }
+        s[i] = (i & 3) == 1 ? ex2_fma(x) : ex2(x);
       }
       float sum = 0.f;
 #pragma unroll
       for (int i = 0; i < 128; ++i) sum += s[i];
       l_run = l_run * alpha + sum;
       if (it > 0) {
-        mbar_wait(&o_full[wg], (it - 1) & 1);         // PV(it-1) done: O and sP free
+        mbar_wait(&o_full[wg], (it - 1) & 1);         // PV(it-1) done: O may be rescaled
         tc_fence_after();
       }
       if (rescale) {
@@ -271,16 +267,16 @@ __global__ void __launch_bounds__(320, 1)
         }
         tmem_wait_st();
       }
-      // P (bf16) -> smem, K-major 128B-swizzled [128 rows][128 keys] as two 64-key chunks
-      const uint32_t pbase = smem_u32(sP);
+      // P (bf16 pairs) -> TMEM over this tile's S columns (all S values are already in registers);
+      // the PV MMA reads it as its A operand. S(it+1) is issued after PV(it), so the overwrite is ordered.
 #pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {
-        const int k0 = ch * 8;
-        const uint32_t addr = pbase + (k0 >> 6) * 16384 + sw128_offset(row, k0 & 63);
-        st_shared_v4(addr, pack_bf16(s[k0], s[k0 + 1]), pack_bf16(s[k0 + 2], s[k0 + 3]),
-                     pack_bf16(s[k0 + 4], s[k0 + 5]), pack_bf16(s[k0 + 6], s[k0 + 7]));
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]);
+        tmem_st16(tS + c * 16, pk);
       }
-      fence_proxy_async_smem();
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[wg]);
     }
@@ -346,13 +342,13 @@ cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err
     static const cudaError_t attr =
         cudaFuncSetAttribute(attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<128>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_fwd attr: %s", cudaGetErrorString(attr)); return attr; }
-    attn_fwd_kernel<128><<<grid, 320, FwdCfg<128>::SMEM, stream>>>(tq, tk, tv, a);
+    attn_fwd_kernel<128><<<grid, 384, FwdCfg<128>::SMEM, stream>>>(tq, tk, tv, a);
     count_launches(1);
   } else {
     static const cudaError_t attr =
         cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<64>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_fwd attr: %s", cudaGetErrorString(attr)); return attr; }
-    attn_fwd_kernel<64><<<grid, 320, FwdCfg<64>::SMEM, stream>>>(tq, tk, tv, a);
+    attn_fwd_kernel<64><<<grid, 384, FwdCfg<64>::SMEM, stream>>>(tq, tk, tv, a);
     count_launches(1);
   }
   e = cudaGetLastError();
