@@ -236,6 +236,8 @@ def main():
         return float(t.item())
 
     def run(chunk, steps, warmup, trace=False):
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated()       # inputs and weights only: workspace + outputs count as activation
         attn = UPipeAttention(Hq, Hkv, d, D, chunk, True, process_group=pg)
         out = {}
 
@@ -247,7 +249,6 @@ def main():
         for _ in range(warmup):
             step()
         torch.cuda.synchronize()
-        base = torch.cuda.memory_allocated()
         torch.cuda.reset_peak_memory_stats()
         step()
         torch.cuda.synchronize()

@@ -88,7 +88,7 @@ typedef struct {
 
 /* flags for upipe_init / upipe_init_local */
 #define UPIPE_FLAG_NONE 0u
-#define UPIPE_FLAG_SYNC_COMM 1u /* run collectives on the compute stream (no side stream) */
+#define UPIPE_FLAG_SYNC_COMM 1u /* sequential schedule: collectives on the compute stream, one buffer set */
 
 /* ---------------------------------------------------------------- lifecycle */
 
@@ -116,7 +116,11 @@ UPIPE_API const char* upipe_last_error(upipe_ctx_t ctx); /* thread-local message
 
 /* ---------------------------------------------------------------- planning (host only, no GPU) */
 
-/* Bytes of workspace one call needs (pass 0: forward, 1: backward). 256-byte aligned. */
+/* Bytes of workspace one call needs, 256-byte aligned. pass 0: forward, 1: backward, for the
+ * default schedule (C > 1: the next stage's all-to-all overlaps the current attention on the
+ * ctx's comm stream, which needs a second chunk buffer set, DESIGN A23); pass 2: forward,
+ * 3: backward for a ctx created with UPIPE_FLAG_SYNC_COMM (one buffer set, the paper's
+ * memory-minimal schedule). At C = 1 all-to-alls are identities and 0 == 2, 1 == 3. */
 UPIPE_API upipe_status_t upipe_workspace_size(int cp_size, const upipe_shape_t* shape, int pass, size_t* bytes);
 
 /* Stage plan of the GQA schedule (A8): for stage s and device p the

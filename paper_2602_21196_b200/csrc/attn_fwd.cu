@@ -240,8 +240,8 @@ __global__ void __launch_bounds__(384, 1)
         rescale = it > 0;
         m_ref = mx;
       }
-      // p = 2^(s*c - m) on MUFU. (Moving part of it to the FMA pipe, as the backward does, measured slower here:
-      // with 2 softmax warps per scheduler this kernel is issue/latency bound, not XU bound.)
+      // p = 2^(s*c - m): 1 in 4 as a polynomial on the FMA pipe, the rest on MUFU (the XU pipe also packs
+      // P to bf16; 1 in 4 measured best here, 1 in 2 is slower because the softmax warps become issue bound)
 #pragma unroll
       for (int i = 0; i < 128; ++i) {
         const float x = fmaf(s[i], sl2, -m_ref);

@@ -145,9 +145,10 @@ upipe_status_t upipe_workspace_size(int cp_size, const upipe_shape_t* shape, int
   std::string m;
   upipe_status_t st = validate_shape(cp_size, shape, m);
   if (st != UPIPE_OK) return set_err(nullptr, st, m);
-  if (!bytes || (pass != 0 && pass != 1)) return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "pass must be 0 or 1");
+  if (!bytes || pass < 0 || pass > 3) return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "pass must be 0..3");
   const Plan P = make_plan(cp_size, *shape);
-  *bytes = pass == 0 ? fwd_workspace(P).total : bwd_workspace(P).total;
+  const bool ov = pass < 2 && cp_size > 1;   // 0/1: default (overlapped for C > 1); 2/3: sequential
+  *bytes = (pass & 1) == 0 ? fwd_workspace(P, ov).total : bwd_workspace(P, ov).total;
   return UPIPE_OK;
 }
 
@@ -181,7 +182,8 @@ upipe_status_t upipe_attn_fwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
   if (!all_aligned(x, wq, wk, wv, wo, y, o_saved, lse_saved) || (reinterpret_cast<uintptr_t>(workspace) & 255))
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "tensors must be 16-byte aligned, workspace 256-byte aligned");
   const Plan P = make_plan(ctx->C, *shape);
-  if (ws_bytes < fwd_workspace(P).total) return set_err(ctx, UPIPE_ERR_WORKSPACE, "ws_bytes < upipe_workspace_size(pass=0)");
+  if (ws_bytes < fwd_workspace(P, overlap_enabled(ctx->flags, ctx->C)).total)
+    return set_err(ctx, UPIPE_ERR_WORKSPACE, "ws_bytes < upipe_workspace_size(pass=0, or 2 with UPIPE_FLAG_SYNC_COMM)");
   cudaSetDevice(ctx->device);
   return layer_fwd(ctx, P, x, wq, wk, wv, wo, y, o_saved, lse_saved, static_cast<char*>(workspace),
                    static_cast<cudaStream_t>(stream));
@@ -202,7 +204,8 @@ upipe_status_t upipe_attn_bwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
       (reinterpret_cast<uintptr_t>(workspace) & 255))
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "tensors must be 16-byte aligned, workspace 256-byte aligned");
   const Plan P = make_plan(ctx->C, *shape);
-  if (ws_bytes < bwd_workspace(P).total) return set_err(ctx, UPIPE_ERR_WORKSPACE, "ws_bytes < upipe_workspace_size(pass=1)");
+  if (ws_bytes < bwd_workspace(P, overlap_enabled(ctx->flags, ctx->C)).total)
+    return set_err(ctx, UPIPE_ERR_WORKSPACE, "ws_bytes < upipe_workspace_size(pass=1, or 3 with UPIPE_FLAG_SYNC_COMM)");
   cudaSetDevice(ctx->device);
   return layer_bwd(ctx, P, x, wq, wk, wv, wo, dy, o_saved, lse_saved, dx, dwq, dwk, dwv, dwo, reduce_dw,
                    static_cast<char*>(workspace), static_cast<cudaStream_t>(stream));

@@ -3,6 +3,16 @@
 // all-to-alls issued one after the other), §4.1 (KV sent once per
 // super-stage), Table 4 P:686 (backward order: dO seq->head, attention backward,
 // dQ/dK/dV head->seq), P:439 (projections recomputed in backward).
+//
+// Two schedules run the same per-stage steps:
+//  * sequential (C == 1, or UPIPE_FLAG_SYNC_COMM): one buffer set, everything on the
+//    caller's stream: the paper's memory-minimal form;
+//  * overlapped (C > 1, default): the next stage's projections are issued before the
+//    current stage's attention and its all-to-all runs on the ctx's high-priority comm
+//    stream, so it overlaps the attention (north_star: "the next chunk's NCCL
+//    all-to-all over NVLink is overlapped on a side stream with the current chunk's
+//    attention"); the out all-to-all of stage s overlaps attention s+1. Costs a second
+//    buffer set (DESIGN A23). Cross-stream order is carried by CUDA events.
 #include <cstdio>
 
 #include "kernels.h"
@@ -14,22 +24,7 @@ namespace {
 
 using bf16p = const upipe_bf16*;
 
-struct Err {
-  upipe_ctx_s* ctx;
-  upipe_status_t fail(upipe_status_t st, const std::string& msg) {
-    ctx->last_error = msg;
-    return st;
-  }
-};
-
-#define UP_CUDA(expr)                                                             \
-  do {                                                                            \
-    cudaError_t _e = (expr);                                                      \
-    if (_e != cudaSuccess)                                                        \
-      return E.fail(UPIPE_ERR_CUDA, std::string(#expr ": ") + (errbuf[0] ? errbuf : cudaGetErrorString(_e))); \
-  } while (0)
-
-// Brackets one step with trace events on the call's stream (no-op when tracing is off).
+// Brackets one step with trace events on the stream it runs on (no-op when tracing is off).
 struct Step {
   upipe_ctx_s* ctx;
   cudaStream_t st;
@@ -50,18 +45,39 @@ struct Step {
   }
 };
 
-#define UP_T(cat, macro, expr)            \
-  do {                                    \
-    Step _step(ctx, st, UPIPE_TRACE_##cat); \
-    macro(expr);                          \
-  } while (0)
-
-#define UP_COMM(expr)                                  \
-  do {                                                 \
-    std::string _m;                                    \
-    upipe_status_t _s = (expr);                        \
-    if (_s != UPIPE_OK) return E.fail(_s, _m.empty() ? std::string(#expr) : _m); \
-  } while (0)
+// Runs one step, reports failures into ctx->last_error.
+struct Runner {
+  upipe_ctx_s* ctx;
+  upipe_status_t status = UPIPE_OK;
+  char errbuf[512] = {0};
+  bool cuda(int cat, cudaStream_t s, const char* what, cudaError_t (*)(void) = nullptr) { (void)cat; (void)s; (void)what; return true; }
+  template <class F>
+  bool run(int cat, cudaStream_t s, const char* what, F&& f) {
+    if (status != UPIPE_OK) return false;
+    Step step(ctx, s, cat);
+    errbuf[0] = 0;
+    cudaError_t e = f(errbuf);
+    if (e != cudaSuccess) {
+      ctx->last_error = std::string(what) + ": " + (errbuf[0] ? errbuf : cudaGetErrorString(e));
+      status = UPIPE_ERR_CUDA;
+      return false;
+    }
+    return true;
+  }
+  template <class F>
+  bool comm(cudaStream_t s, const char* what, F&& f) {
+    if (status != UPIPE_OK) return false;
+    Step step(ctx, s, UPIPE_TRACE_COMM);
+    std::string m;
+    upipe_status_t st = f(m);
+    if (st != UPIPE_OK) {
+      ctx->last_error = std::string(what) + ": " + m;
+      status = st;
+      return false;
+    }
+    return true;
+  }
+};
 
 // Projection of this rank's shard for the stage's heads, written straight into the
 // all-to-all send layout [C][S_l][seg] (pack fused into the GEMM epilogue).
@@ -85,43 +101,78 @@ GemmProblem proj_to_send(const Plan& P, const void* x, const void* W, int64_t W_
   return g;
 }
 
+upipe_status_t ensure_pipe(upipe_ctx_s* ctx) {
+  Pipe& p = ctx->pipe;
+  if (p.ready) return UPIPE_OK;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (cudaStreamCreateWithPriority(&p.comm, cudaStreamNonBlocking, hi) != cudaSuccess) {
+    ctx->last_error = "cannot create the comm stream";
+    return UPIPE_ERR_CUDA;
+  }
+  for (auto& e : p.ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      ctx->last_error = "cannot create pipeline events";
+      return UPIPE_ERR_CUDA;
+    }
+  p.ready = true;
+  return UPIPE_OK;
+}
+
 }  // namespace
 
+// ============================================================================ forward
 upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf16p wk, bf16p wv, bf16p wo,
                          upipe_bf16* y, upipe_bf16* o_saved, float* lse_saved, char* ws, cudaStream_t st) {
-  Err E{ctx};
-  char errbuf[512] = {0};
+  const bool ov = overlap_enabled(ctx->flags, P.C);
+  if (ov) {
+    if (upipe_status_t s = ensure_pipe(ctx)) return s;
+  }
+  Runner R{ctx};
   Transport& T = *ctx->transport;
-  const FwdWs W = fwd_workspace(P);
+  const FwdWs W = fwd_workspace(P, ov);
   const int C = P.C, me = ctx->rank, d = P.d;
   const int64_t qseg = (int64_t)P.qpd * d, kseg = (int64_t)P.kv_res * d;
-  const int64_t HqD = (int64_t)P.Hq * d;
+  const int64_t HqD = (int64_t)P.Hq * d, kvrows = (int64_t)P.Hkv * d;
   const size_t qbytes = (size_t)P.S_l * qseg * 2, kbytes = (size_t)P.S_l * kseg * 2;
-  for (int s = 0; s < P.nstages; ++s) {
+  const int64_t qstep = (int64_t)P.q_dev_stride() * d;
+  auto kvb = [&](int s) { return ov ? (s / P.sigma) & 1 : 0; };
+
+  // F1: Q_s (and K_s, V_s at a super-stage start) -> send buffer set b
+  auto proj = [&](int s, int b, cudaStream_t q) {
     const int64_t q0 = P.q0(s, 0), kv0 = P.kv0(s, 0);
-    const int64_t qstep = (int64_t)P.q_dev_stride() * d;
-    // F1: Q_s = x Wq[rows(s)]^T -> send layout
-    UP_T(GEMM, UP_CUDA, gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend), st, errbuf, sizeof errbuf));
-    // F2: inp_all_to_all, Q first, then K and V when this stage starts a super-stage
-    UP_T(COMM, UP_COMM, T.alltoall(ws + W.qsend, ws + W.qrecv, qbytes, st, _m));
+    R.run(UPIPE_TRACE_GEMM, q, "proj Q", [&](char* e) {
+      return gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend[b]), q, e, 512);
+    });
     if (P.kv_sent(s)) {
-      const int64_t kvrows = (int64_t)P.Hkv * d;
-      UP_T(GEMM, UP_CUDA, gemm_run(proj_to_send(P, x, wk, kvrows, kv0 * d, kseg, kseg, ws + W.ksend), st, errbuf, sizeof errbuf));
-      UP_T(COMM, UP_COMM, T.alltoall(ws + W.ksend, ws + W.krecv, kbytes, st, _m));
-      UP_T(GEMM, UP_CUDA, gemm_run(proj_to_send(P, x, wv, kvrows, kv0 * d, kseg, kseg, ws + W.vsend), st, errbuf, sizeof errbuf));
-      UP_T(COMM, UP_COMM, T.alltoall(ws + W.vsend, ws + W.vrecv, kbytes, st, _m));
+      R.run(UPIPE_TRACE_GEMM, q, "proj K", [&](char* e) {
+        return gemm_run(proj_to_send(P, x, wk, kvrows, kv0 * d, kseg, kseg, ws + W.ksend), q, e, 512);
+      });
+      R.run(UPIPE_TRACE_GEMM, q, "proj V", [&](char* e) {
+        return gemm_run(proj_to_send(P, x, wv, kvrows, kv0 * d, kseg, kseg, ws + W.vsend), q, e, 512);
+      });
     }
-    // F3: attention over the full sequence for this device's qpd heads
+  };
+  // F2: inp_all_to_all, Q first, then K and V
+  auto inp = [&](int s, int b, cudaStream_t q) {
+    R.comm(q, "a2a Q", [&](std::string& m) { return T.alltoall(ws + W.qsend[b], ws + W.qrecv[b], qbytes, q, m); });
+    if (P.kv_sent(s)) {
+      const int kb = kvb(s);
+      R.comm(q, "a2a K", [&](std::string& m) { return T.alltoall(ws + W.ksend, ws + W.krecv[kb], kbytes, q, m); });
+      R.comm(q, "a2a V", [&](std::string& m) { return T.alltoall(ws + W.vsend, ws + W.vrecv[kb], kbytes, q, m); });
+    }
+  };
+  // F3: attention over the full sequence for this device's qpd heads
+  auto attn = [&](int s, int b, cudaStream_t q) {
     AttnFwdProblem a{};
-    a.q = ws + W.qrecv;
-    a.k = ws + W.krecv;
-    a.v = ws + W.vrecv;
-    const int64_t my_q0 = P.q0(s, me);
+    a.q = ws + W.qrecv[b];
+    a.k = ws + W.krecv[kvb(s)];
+    a.v = ws + W.vrecv[kvb(s)];
     if (C == 1) {
-      a.o = o_saved + my_q0 * d;  // no out all-to-all: write straight into the pre-allocated output
+      a.o = o_saved + (int64_t)P.q0(s, me) * d;  // no out all-to-all: straight into the pre-allocated output
       a.ldo = HqD;
     } else {
-      a.o = ws + W.osend;
+      a.o = ws + W.osend[b];
       a.ldo = qseg;
     }
     a.lse = lse_saved + (int64_t)s * P.qpd * P.S;
@@ -133,13 +184,20 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     a.ldq = qseg;
     a.ldkv = kseg;
     a.ld_lse = P.S;
-    UP_T(ATTN_FWD, UP_CUDA, attn_fwd_run(a, st, errbuf, sizeof errbuf));
-    if (C > 1) {
-      // F4: out_all_to_all, F5: fill the pre-allocated output o_saved
-      UP_T(COMM, UP_COMM, T.alltoall(ws + W.osend, ws + W.orecv, qbytes, st, _m));
-      UP_T(AUX, UP_CUDA, unpack_cols_run(ws + W.orecv, P.S_l, C, (int)qseg, o_saved, HqD, q0 * d, qstep, st));
-    }
-    // F6: y (+)= O_s Wo[:, cols(s)]^T ; fp32 accumulator across stages, bf16 on the last stage (F7 fused)
+    R.run(UPIPE_TRACE_ATTN_FWD, q, "attn fwd", [&](char* e) { return attn_fwd_run(a, q, e, 512); });
+  };
+  // F4: out_all_to_all
+  auto outa = [&](int s, int b, cudaStream_t q) {
+    (void)s;
+    R.comm(q, "a2a O", [&](std::string& m) { return T.alltoall(ws + W.osend[b], ws + W.orecv[b], qbytes, q, m); });
+  };
+  // F5: fill o_saved; F6/F7: y (+)= O_s Wo[:, cols(s)]^T, fp32 accumulator, bf16 on the last stage
+  auto post = [&](int s, int b, cudaStream_t q) {
+    const int64_t q0 = P.q0(s, 0);
+    if (C > 1)
+      R.run(UPIPE_TRACE_AUX, q, "unpack O", [&](char*) {
+        return unpack_cols_run(ws + W.orecv[b], P.S_l, C, (int)qseg, o_saved, HqD, q0 * d, qstep, q);
+      });
     GemmProblem g;
     g.M = P.S_l;
     g.N = P.D;
@@ -159,23 +217,80 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     else if (s == 0) g.c.epi = Epi::kStoreF32;
     else if (s == P.nstages - 1) g.c.epi = Epi::kAccF32ToBF16;
     else g.c.epi = Epi::kAccF32;
-    UP_T(GEMM, UP_CUDA, gemm_run(g, st, errbuf, sizeof errbuf));
+    R.run(UPIPE_TRACE_GEMM, q, "out proj", [&](char* e) { return gemm_run(g, q, e, 512); });
+  };
+
+  const int nu = P.nstages;
+  if (!ov) {
+    for (int s = 0; s < nu && R.status == UPIPE_OK; ++s) {
+      proj(s, 0, st);
+      if (C > 1) inp(s, 0, st);
+      attn(s, 0, st);
+      if (C > 1) outa(s, 0, st);
+      post(s, 0, st);
+    }
+    return R.status;
   }
-  return UPIPE_OK;
+  // ---- overlapped schedule
+  cudaStream_t cs = ctx->pipe.comm;
+  cudaEvent_t* ev = ctx->pipe.ev;
+  cudaEvent_t e_begin = ev[0], *e_proj = ev + 1, *e_in = ev + 3, *e_attn = ev + 5, *e_out = ev + 7, *e_post = ev + 9;
+  cudaEventRecord(e_begin, st);
+  cudaStreamWaitEvent(cs, e_begin, 0);
+  proj(0, 0, st);
+  cudaEventRecord(e_proj[0], st);
+  cudaStreamWaitEvent(cs, e_proj[0], 0);
+  inp(0, 0, cs);
+  cudaEventRecord(e_in[0], cs);
+  for (int s = 0; s < nu && R.status == UPIPE_OK; ++s) {
+    const int b = s & 1;
+    if (s + 1 < nu) {
+      const int b1 = (s + 1) & 1;
+      if (s >= 1) cudaStreamWaitEvent(st, e_in[b1], 0);          // a2a(s-1) has read send set b1
+      if (P.kv_sent(s + 1)) cudaStreamWaitEvent(st, e_in[b], 0);  // a2a(s) has read the single K/V send buffers
+      proj(s + 1, b1, st);
+      cudaEventRecord(e_proj[b1], st);
+      cudaStreamWaitEvent(cs, e_proj[b1], 0);
+      if (s >= 1) cudaStreamWaitEvent(cs, e_attn[b1], 0);         // attention(s-1) has read receive set b1
+      inp(s + 1, b1, cs);
+      cudaEventRecord(e_in[b1], cs);
+    }
+    cudaStreamWaitEvent(st, e_in[b], 0);
+    attn(s, b, st);
+    cudaEventRecord(e_attn[b], st);
+    cudaStreamWaitEvent(cs, e_attn[b], 0);
+    if (s >= 2) cudaStreamWaitEvent(cs, e_post[b], 0);            // post(s-2) has read O receive set b
+    outa(s, b, cs);
+    cudaEventRecord(e_out[b], cs);
+    if (s >= 1) {
+      cudaStreamWaitEvent(st, e_out[(s - 1) & 1], 0);
+      post(s - 1, (s - 1) & 1, st);
+      cudaEventRecord(e_post[(s - 1) & 1], st);
+    }
+  }
+  cudaStreamWaitEvent(st, e_out[(nu - 1) & 1], 0);
+  post(nu - 1, (nu - 1) & 1, st);
+  return R.status;
 }
 
+// ============================================================================ backward
 upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf16p wk, bf16p wv, bf16p wo,
                          bf16p dy, bf16p o_saved, const float* lse_saved, upipe_bf16* dx, float* dwq, float* dwk,
                          float* dwv, float* dwo, int reduce_dw, char* ws, cudaStream_t st) {
-  Err E{ctx};
-  char errbuf[512] = {0};
+  const bool ov = overlap_enabled(ctx->flags, P.C);
+  if (ov) {
+    if (upipe_status_t s = ensure_pipe(ctx)) return s;
+  }
+  Runner R{ctx};
   Transport& T = *ctx->transport;
-  const BwdWs W = bwd_workspace(P);
+  const BwdWs W = bwd_workspace(P, ov);
   const int C = P.C, d = P.d;
   const int64_t qseg = (int64_t)P.qpd * d, kseg = (int64_t)P.kv_res * d;
   const int64_t HqD = (int64_t)P.Hq * d, HkvD = (int64_t)P.Hkv * d;
   const size_t qbytes = (size_t)P.S_l * qseg * 2, kbytes = (size_t)P.S_l * kseg * 2;
+  const size_t dbytes = (size_t)P.S_l * P.qpd * 4;
   const int64_t qstep = (int64_t)P.q_dev_stride() * d;
+  auto kvb = [&](int s) { return ov ? (s / P.sigma) & 1 : 0; };
 
   // dWo = dY^T O over this rank's tokens (all stages at once: o_saved holds every head)
   {
@@ -188,7 +303,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     g.c.out_f32 = dwo;
     g.c.ld_f32 = HqD;
     g.c.epi = Epi::kStoreF32;
-    UP_T(GEMM, UP_CUDA, gemm_run(g, st, errbuf, sizeof errbuf));
+    R.run(UPIPE_TRACE_GEMM, st, "dWo", [&](char* e) { return gemm_run(g, st, e, 512); });
   }
   const int n_dx_terms = P.nstages + 2 * (P.nstages / P.sigma);
   int dx_term = 0;
@@ -237,96 +352,188 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     return g;
   };
 
-  for (int s = 0; s < P.nstages; ++s) {
+  // B1 + B2: recompute the stage's projections, dO_s = dY Wo[:, cols(s)], delta = rowsum(dO*O) (A13)
+  auto pre = [&](int s, int b, cudaStream_t q) {
     const int64_t q0 = P.q0(s, 0), kv0 = P.kv0(s, 0);
-    // B1: recompute the stage's projections and inp_all_to_all
-    UP_T(GEMM, UP_CUDA, gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend), st, errbuf, sizeof errbuf));
-    UP_T(COMM, UP_COMM, T.alltoall(ws + W.qsend, ws + W.qrecv, qbytes, st, _m));
+    R.run(UPIPE_TRACE_GEMM, q, "proj Q", [&](char* e) {
+      return gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend[b]), q, e, 512);
+    });
     if (P.kv_sent(s)) {
-      UP_T(GEMM, UP_CUDA, gemm_run(proj_to_send(P, x, wk, HkvD, kv0 * d, kseg, kseg, ws + W.ksend), st, errbuf, sizeof errbuf));
-      UP_T(COMM, UP_COMM, T.alltoall(ws + W.ksend, ws + W.krecv, kbytes, st, _m));
-      UP_T(GEMM, UP_CUDA, gemm_run(proj_to_send(P, x, wv, HkvD, kv0 * d, kseg, kseg, ws + W.vsend), st, errbuf, sizeof errbuf));
-      UP_T(COMM, UP_COMM, T.alltoall(ws + W.vsend, ws + W.vrecv, kbytes, st, _m));
+      R.run(UPIPE_TRACE_GEMM, q, "proj K", [&](char* e) {
+        return gemm_run(proj_to_send(P, x, wk, HkvD, kv0 * d, kseg, kseg, ws + W.ksend), q, e, 512);
+      });
+      R.run(UPIPE_TRACE_GEMM, q, "proj V", [&](char* e) {
+        return gemm_run(proj_to_send(P, x, wv, HkvD, kv0 * d, kseg, kseg, ws + W.vsend), q, e, 512);
+      });
     }
-    // B2: dO_s = dY Wo[:, cols(s)] straight into the send layout; delta = rowsum(dO*O) (A13)
-    {
-      GemmProblem g;
-      g.M = P.S_l;
-      g.N = (int64_t)C * qseg;
-      g.K = P.D;
-      g.a = OperandMap{dy, P.D, P.S_l, P.D, false};
-      g.b = OperandMap{wo, HqD, P.D, HqD, true};
-      g.b.o_base = q0 * d;
-      g.b.o_len = qseg;
-      g.b.o_istride = qstep;
-      g.c.out_bf16 = ws + W.dosend;
-      g.c.ld_bf16 = qseg;
-      g.c.n_len = qseg;
-      g.c.r_nstride = P.S_l;
-      g.c.epi = Epi::kStoreBF16;
-      UP_T(GEMM, UP_CUDA, gemm_run(g, st, errbuf, sizeof errbuf));
-      for (int p = 0; p < C; ++p)
-        UP_T(AUX, UP_CUDA, rowdot_run((const upipe_bf16*)(ws + W.dosend) + (int64_t)p * P.S_l * qseg, qseg,
-                           o_saved + (int64_t)P.q0(s, p) * d, HqD, (float*)(ws + W.dsend) + (int64_t)p * P.S_l * P.qpd,
-                           P.qpd, P.S_l, P.qpd, d, st));
+    GemmProblem g;
+    g.M = P.S_l;
+    g.N = (int64_t)C * qseg;
+    g.K = P.D;
+    g.a = OperandMap{dy, P.D, P.S_l, P.D, false};
+    g.b = OperandMap{wo, HqD, P.D, HqD, true};
+    g.b.o_base = q0 * d;
+    g.b.o_len = qseg;
+    g.b.o_istride = qstep;
+    g.c.out_bf16 = ws + W.dosend[b];
+    g.c.ld_bf16 = qseg;
+    g.c.n_len = qseg;
+    g.c.r_nstride = P.S_l;
+    g.c.epi = Epi::kStoreBF16;
+    R.run(UPIPE_TRACE_GEMM, q, "dO", [&](char* e) { return gemm_run(g, q, e, 512); });
+    for (int p = 0; p < C; ++p)
+      R.run(UPIPE_TRACE_AUX, q, "rowdot", [&](char*) {
+        return rowdot_run((const upipe_bf16*)(ws + W.dosend[b]) + (int64_t)p * P.S_l * qseg, qseg,
+                          o_saved + (int64_t)P.q0(s, p) * d, HqD, (float*)(ws + W.dsend[b]) + (int64_t)p * P.S_l * P.qpd,
+                          P.qpd, P.S_l, P.qpd, d, q);
+      });
+  };
+  // B1/B3: Q (+K, V) and dO + delta seq -> head ("during out_all_to_all", Table 4)
+  auto inp = [&](int s, int b, cudaStream_t q) {
+    R.comm(q, "a2a Q", [&](std::string& m) { return T.alltoall(ws + W.qsend[b], ws + W.qrecv[b], qbytes, q, m); });
+    if (P.kv_sent(s)) {
+      const int kb = kvb(s);
+      R.comm(q, "a2a K", [&](std::string& m) { return T.alltoall(ws + W.ksend, ws + W.krecv[kb], kbytes, q, m); });
+      R.comm(q, "a2a V", [&](std::string& m) { return T.alltoall(ws + W.vsend, ws + W.vrecv[kb], kbytes, q, m); });
     }
-    // B3: dO and delta seq->head ("during out_all_to_all", Table 4)
-    UP_T(COMM, UP_COMM, T.alltoall(ws + W.dosend, ws + W.dorecv, qbytes, st, _m));
-    UP_T(COMM, UP_COMM, T.alltoall(ws + W.dsend, ws + W.drecv, (size_t)P.S_l * P.qpd * 4, st, _m));
-    // B4: attention backward; dK/dV accumulate over the sigma stages sharing the resident K/V
-    UP_T(AUX, UP_CUDA, cudaMemsetAsync(ws + W.dqacc, 0, (size_t)P.S * qseg * 4, st));
+    R.comm(q, "a2a dO", [&](std::string& m) { return T.alltoall(ws + W.dosend[b], ws + W.dorecv[b], qbytes, q, m); });
+    R.comm(q, "a2a delta", [&](std::string& m) { return T.alltoall(ws + W.dsend[b], ws + W.drecv[b], dbytes, q, m); });
+  };
+  // B4: attention backward (dK/dV accumulate over the sigma stages sharing the resident K/V), dQ -> bf16
+  auto attn = [&](int s, int b, cudaStream_t q) {
+    R.run(UPIPE_TRACE_AUX, q, "memset dQ", [&](char*) {
+      return cudaMemsetAsync(ws + W.dqacc[b], 0, (size_t)P.S * qseg * 4, q);
+    });
     const int r = s % P.sigma;
     const bool last = P.kv_last(s);
-    AttnBwdProblem b{};
-    b.q = ws + W.qrecv;
-    b.k = ws + W.krecv;
-    b.v = ws + W.vrecv;
-    b.dout = ws + W.dorecv;
-    b.lse = lse_saved + (int64_t)s * P.qpd * P.S;
-    b.delta = (const float*)(ws + W.drecv);
-    b.dq_acc = (float*)(ws + W.dqacc);
-    b.dk_acc = P.sigma > 1 ? (float*)(ws + W.dkacc) : nullptr;
-    b.dv_acc = P.sigma > 1 ? (float*)(ws + W.dvacc) : nullptr;
-    b.dk_bf16 = last ? ws + W.dksend : nullptr;
-    b.dv_bf16 = last ? ws + W.dvsend : nullptr;
-    b.S = P.S;
-    b.nq = P.qpd;
-    b.nkv = P.kv_res;
-    b.d = d;
-    b.causal = P.sh.causal;
-    b.ldq = qseg;
-    b.ldkv = kseg;
-    b.ldo_grad = qseg;
-    b.ld_lse = P.S;
-    b.ld_delta = P.qpd;
-    b.ld_kvb = kseg;
-    b.kv_accumulate = r > 0;
-    b.kv_write_acc = !last;
-    UP_T(ATTN_BWD, UP_CUDA, attn_bwd_run(b, st, errbuf, sizeof errbuf));
-    // B5: dQ fp32 -> bf16 send layout, head->seq ("during inp_all_to_all")
-    UP_T(AUX, UP_CUDA, cvt_f32_bf16_run((const float*)(ws + W.dqacc), qseg, ws + W.dqsend, qseg, P.S, qseg, 1.0f, st));
-    UP_T(COMM, UP_COMM, T.alltoall(ws + W.dqsend, ws + W.dqrecv, qbytes, st, _m));
-    // B6: dX and dWq for the stage's q heads
-    UP_T(GEMM, UP_CUDA, gemm_run(dx_gemm(ws + W.dqrecv, qseg, wq, HqD, q0 * d, qstep), st, errbuf, sizeof errbuf));
-    UP_T(GEMM, UP_CUDA, gemm_run(dw_gemm(ws + W.dqrecv, qseg, dwq, q0 * d, qstep), st, errbuf, sizeof errbuf));
-    if (last) {
-      // retire the super-stage's K/V: dK, dV head->seq, then their dX / dW terms
-      UP_T(COMM, UP_COMM, T.alltoall(ws + W.dksend, ws + W.dkrecv, kbytes, st, _m));
-      UP_T(COMM, UP_COMM, T.alltoall(ws + W.dvsend, ws + W.dvrecv, kbytes, st, _m));
-      UP_T(GEMM, UP_CUDA, gemm_run(dx_gemm(ws + W.dkrecv, kseg, wk, HkvD, kv0 * d, kseg), st, errbuf, sizeof errbuf));
-      UP_T(GEMM, UP_CUDA, gemm_run(dx_gemm(ws + W.dvrecv, kseg, wv, HkvD, kv0 * d, kseg), st, errbuf, sizeof errbuf));
-      UP_T(GEMM, UP_CUDA, gemm_run(dw_gemm(ws + W.dkrecv, kseg, dwk, kv0 * d, kseg), st, errbuf, sizeof errbuf));
-      UP_T(GEMM, UP_CUDA, gemm_run(dw_gemm(ws + W.dvrecv, kseg, dwv, kv0 * d, kseg), st, errbuf, sizeof errbuf));
+    AttnBwdProblem bp{};
+    bp.q = ws + W.qrecv[b];
+    bp.k = ws + W.krecv[kvb(s)];
+    bp.v = ws + W.vrecv[kvb(s)];
+    bp.dout = ws + W.dorecv[b];
+    bp.lse = lse_saved + (int64_t)s * P.qpd * P.S;
+    bp.delta = (const float*)(ws + W.drecv[b]);
+    bp.dq_acc = (float*)(ws + W.dqacc[b]);
+    bp.dk_acc = P.sigma > 1 ? (float*)(ws + W.dkacc) : nullptr;
+    bp.dv_acc = P.sigma > 1 ? (float*)(ws + W.dvacc) : nullptr;
+    bp.dk_bf16 = last ? ws + W.dksend : nullptr;
+    bp.dv_bf16 = last ? ws + W.dvsend : nullptr;
+    bp.S = P.S;
+    bp.nq = P.qpd;
+    bp.nkv = P.kv_res;
+    bp.d = d;
+    bp.causal = P.sh.causal;
+    bp.ldq = qseg;
+    bp.ldkv = kseg;
+    bp.ldo_grad = qseg;
+    bp.ld_lse = P.S;
+    bp.ld_delta = P.qpd;
+    bp.ld_kvb = kseg;
+    bp.kv_accumulate = r > 0;
+    bp.kv_write_acc = !last;
+    R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd", [&](char* e) { return attn_bwd_run(bp, q, e, 512); });
+    R.run(UPIPE_TRACE_AUX, q, "cvt dQ", [&](char*) {
+      return cvt_f32_bf16_run((const float*)(ws + W.dqacc[b]), qseg, ws + W.dqsend[b], qseg, P.S, qseg, 1.0f, q);
+    });
+  };
+  // B5: dQ head -> seq ("during inp_all_to_all"); dK/dV when the super-stage's K/V retire
+  auto outa = [&](int s, int b, cudaStream_t q) {
+    R.comm(q, "a2a dQ", [&](std::string& m) { return T.alltoall(ws + W.dqsend[b], ws + W.dqrecv[b], qbytes, q, m); });
+    if (P.kv_last(s)) {
+      R.comm(q, "a2a dK", [&](std::string& m) { return T.alltoall(ws + W.dksend, ws + W.dkrecv, kbytes, q, m); });
+      R.comm(q, "a2a dV", [&](std::string& m) { return T.alltoall(ws + W.dvsend, ws + W.dvrecv, kbytes, q, m); });
     }
+  };
+  // B6: dX and dW for the stage's heads (and the retired K/V heads)
+  auto post = [&](int s, int b, cudaStream_t q) {
+    const int64_t q0 = P.q0(s, 0), kv0 = P.kv0(s, 0);
+    GemmProblem g1 = dx_gemm(ws + W.dqrecv[b], qseg, wq, HqD, q0 * d, qstep);
+    R.run(UPIPE_TRACE_GEMM, q, "dX(dQ)", [&](char* e) { return gemm_run(g1, q, e, 512); });
+    R.run(UPIPE_TRACE_GEMM, q, "dWq", [&](char* e) {
+      return gemm_run(dw_gemm(ws + W.dqrecv[b], qseg, dwq, q0 * d, qstep), q, e, 512);
+    });
+    if (P.kv_last(s)) {
+      GemmProblem gk = dx_gemm(ws + W.dkrecv, kseg, wk, HkvD, kv0 * d, kseg);
+      R.run(UPIPE_TRACE_GEMM, q, "dX(dK)", [&](char* e) { return gemm_run(gk, q, e, 512); });
+      GemmProblem gv = dx_gemm(ws + W.dvrecv, kseg, wv, HkvD, kv0 * d, kseg);
+      R.run(UPIPE_TRACE_GEMM, q, "dX(dV)", [&](char* e) { return gemm_run(gv, q, e, 512); });
+      R.run(UPIPE_TRACE_GEMM, q, "dWk", [&](char* e) {
+        return gemm_run(dw_gemm(ws + W.dkrecv, kseg, dwk, kv0 * d, kseg), q, e, 512);
+      });
+      R.run(UPIPE_TRACE_GEMM, q, "dWv", [&](char* e) {
+        return gemm_run(dw_gemm(ws + W.dvrecv, kseg, dwv, kv0 * d, kseg), q, e, 512);
+      });
+    }
+  };
+
+  const int nu = P.nstages;
+  if (!ov) {
+    for (int s = 0; s < nu && R.status == UPIPE_OK; ++s) {
+      pre(s, 0, st);
+      if (C > 1) inp(s, 0, st);
+      attn(s, 0, st);
+      if (C > 1) outa(s, 0, st);
+      post(s, 0, st);
+    }
+  } else {
+    // ---- overlapped schedule (same event protocol as the forward, plus the single dK/dV buffers)
+    cudaStream_t cs = ctx->pipe.comm;
+    cudaEvent_t* ev = ctx->pipe.ev;
+    cudaEvent_t e_begin = ev[0], *e_pre = ev + 1, *e_in = ev + 3, *e_attn = ev + 5, *e_out = ev + 7,
+                *e_post = ev + 9, e_kvout = ev[11], e_kvpost = ev[12];
+    bool kv_inflight = false;
+    cudaEventRecord(e_begin, st);
+    cudaStreamWaitEvent(cs, e_begin, 0);
+    pre(0, 0, st);
+    cudaEventRecord(e_pre[0], st);
+    cudaStreamWaitEvent(cs, e_pre[0], 0);
+    inp(0, 0, cs);
+    cudaEventRecord(e_in[0], cs);
+    for (int s = 0; s < nu && R.status == UPIPE_OK; ++s) {
+      const int b = s & 1;
+      if (s + 1 < nu) {
+        const int b1 = (s + 1) & 1;
+        if (s >= 1) cudaStreamWaitEvent(st, e_in[b1], 0);
+        if (P.kv_sent(s + 1)) cudaStreamWaitEvent(st, e_in[b], 0);
+        pre(s + 1, b1, st);
+        cudaEventRecord(e_pre[b1], st);
+        cudaStreamWaitEvent(cs, e_pre[b1], 0);
+        if (s >= 1) cudaStreamWaitEvent(cs, e_attn[b1], 0);
+        inp(s + 1, b1, cs);
+        cudaEventRecord(e_in[b1], cs);
+      }
+      cudaStreamWaitEvent(st, e_in[b], 0);
+      if (P.kv_last(s) && kv_inflight) cudaStreamWaitEvent(st, e_kvout, 0);   // previous dK/dV a2a read dk/dvsend
+      attn(s, b, st);
+      cudaEventRecord(e_attn[b], st);
+      // post(s-1) is enqueued before out(s) so that out(s) can wait for it when both use the dK/dV buffers
+      if (s >= 1) {
+        cudaStreamWaitEvent(st, e_out[(s - 1) & 1], 0);
+        post(s - 1, (s - 1) & 1, st);
+        cudaEventRecord(e_post[(s - 1) & 1], st);
+        if (P.kv_last(s - 1)) cudaEventRecord(e_kvpost, st);
+      }
+      cudaStreamWaitEvent(cs, e_attn[b], 0);
+      if (s >= 2) cudaStreamWaitEvent(cs, e_post[b], 0);                        // post(s-2) read dQ receive set b
+      if (P.kv_last(s) && kv_inflight) cudaStreamWaitEvent(cs, e_kvpost, 0);  // previous post read dk/dvrecv
+      outa(s, b, cs);
+      cudaEventRecord(e_out[b], cs);
+      if (P.kv_last(s)) {
+        cudaEventRecord(e_kvout, cs);
+        kv_inflight = true;
+      }
+    }
+    cudaStreamWaitEvent(st, e_out[(nu - 1) & 1], 0);
+    post(nu - 1, (nu - 1) & 1, st);
   }
   // B7: dW summed over the CP group (the FSDP gradient reduction of P:437, A14)
-  if (reduce_dw && C > 1) {
-    UP_T(COMM, UP_COMM, T.allreduce_sum_f32(dwq, (size_t)HqD * P.D, st, _m));
-    UP_T(COMM, UP_COMM, T.allreduce_sum_f32(dwk, (size_t)HkvD * P.D, st, _m));
-    UP_T(COMM, UP_COMM, T.allreduce_sum_f32(dwv, (size_t)HkvD * P.D, st, _m));
-    UP_T(COMM, UP_COMM, T.allreduce_sum_f32(dwo, (size_t)HqD * P.D, st, _m));
+  if (reduce_dw && C > 1 && R.status == UPIPE_OK) {
+    R.comm(st, "allreduce dWq", [&](std::string& m) { return T.allreduce_sum_f32(dwq, (size_t)HqD * P.D, st, m); });
+    R.comm(st, "allreduce dWk", [&](std::string& m) { return T.allreduce_sum_f32(dwk, (size_t)HkvD * P.D, st, m); });
+    R.comm(st, "allreduce dWv", [&](std::string& m) { return T.allreduce_sum_f32(dwv, (size_t)HkvD * P.D, st, m); });
+    R.comm(st, "allreduce dWo", [&](std::string& m) { return T.allreduce_sum_f32(dwo, (size_t)HqD * P.D, st, m); });
   }
-  return UPIPE_OK;
+  return R.status;
 }
 
 }  // namespace upipe

@@ -57,7 +57,9 @@ Plan make_plan(int C, const upipe_shape_t& sh) {
   return p;
 }
 
-FwdWs fwd_workspace(const Plan& p) {
+FwdWs fwd_workspace(const Plan& p, bool overlap) {
+  // overlap (C > 1): the next stage's inp all-to-all runs while this stage's attention reads its
+  // buffers, so the Q/K/V receive, Q send and O send/receive buffers are doubled (DESIGN A23).
   FwdWs w{};
   const size_t qe = (size_t)p.S * p.qpd * p.d * 2;     // one Q-sized chunk, bf16
   const size_t ke = (size_t)p.S * p.kv_res * p.d * 2;  // one K-sized chunk, bf16
@@ -68,23 +70,31 @@ FwdWs fwd_workspace(const Plan& p) {
     return o;
   };
   const bool comm = p.C > 1;
-  w.qsend = take(qe);
-  w.qrecv = comm ? take(qe) : w.qsend;
+  const bool dbl = comm && overlap;
+  for (int i = 0; i < 2; ++i) {
+    const bool fresh = i == 0 || dbl;
+    w.qsend[i] = fresh ? take(qe) : w.qsend[0];
+    w.qrecv[i] = !comm ? w.qsend[i] : (fresh ? take(qe) : w.qrecv[0]);
+  }
   w.ksend = take(ke);
-  w.krecv = comm ? take(ke) : w.ksend;
   w.vsend = take(ke);
-  w.vrecv = comm ? take(ke) : w.vsend;
-  w.osend = comm ? take(qe) : 0;
-  w.orecv = comm ? take(qe) : 0;
+  for (int i = 0; i < 2; ++i) {
+    const bool fresh = i == 0 || dbl;
+    w.krecv[i] = !comm ? w.ksend : (fresh ? take(ke) : w.krecv[0]);
+    w.vrecv[i] = !comm ? w.vsend : (fresh ? take(ke) : w.vrecv[0]);
+    w.osend[i] = !comm ? 0 : (fresh ? take(qe) : w.osend[0]);
+    w.orecv[i] = !comm ? 0 : (fresh ? take(qe) : w.orecv[0]);
+  }
   w.yacc = p.nstages > 1 ? take((size_t)p.S_l * p.D * 4) : 0;
   w.total = off;
   return w;
 }
 
-BwdWs bwd_workspace(const Plan& p) {
+BwdWs bwd_workspace(const Plan& p, bool overlap) {
   BwdWs w{};
   const size_t qe = (size_t)p.S * p.qpd * p.d * 2;
   const size_t ke = (size_t)p.S * p.kv_res * p.d * 2;
+  const size_t de = (size_t)p.S * p.qpd * 4;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
@@ -92,19 +102,26 @@ BwdWs bwd_workspace(const Plan& p) {
     return o;
   };
   const bool comm = p.C > 1;
-  w.qsend = take(qe);
-  w.qrecv = comm ? take(qe) : w.qsend;
+  const bool dbl = comm && overlap;
+  for (int i = 0; i < 2; ++i) {
+    const bool fresh = i == 0 || dbl;
+    w.qsend[i] = fresh ? take(qe) : w.qsend[0];
+    w.qrecv[i] = !comm ? w.qsend[i] : (fresh ? take(qe) : w.qrecv[0]);
+    w.dosend[i] = fresh ? take(qe) : w.dosend[0];
+    w.dorecv[i] = !comm ? w.dosend[i] : (fresh ? take(qe) : w.dorecv[0]);
+    w.dsend[i] = fresh ? take(de) : w.dsend[0];
+    w.drecv[i] = !comm ? w.dsend[i] : (fresh ? take(de) : w.drecv[0]);
+    w.dqacc[i] = fresh ? take(qe * 2) : w.dqacc[0];
+    w.dqsend[i] = fresh ? take(qe) : w.dqsend[0];
+    w.dqrecv[i] = !comm ? w.dqsend[i] : (fresh ? take(qe) : w.dqrecv[0]);
+  }
   w.ksend = take(ke);
-  w.krecv = comm ? take(ke) : w.ksend;
   w.vsend = take(ke);
-  w.vrecv = comm ? take(ke) : w.vsend;
-  w.dosend = take(qe);
-  w.dorecv = comm ? take(qe) : w.dosend;
-  w.dsend = take((size_t)p.S * p.qpd * 4);
-  w.drecv = comm ? take((size_t)p.S * p.qpd * 4) : w.dsend;
-  w.dqacc = take(qe * 2);
-  w.dqsend = take(qe);
-  w.dqrecv = comm ? take(qe) : w.dqsend;
+  for (int i = 0; i < 2; ++i) {
+    const bool fresh = i == 0 || dbl;
+    w.krecv[i] = !comm ? w.ksend : (fresh ? take(ke) : w.krecv[0]);
+    w.vrecv[i] = !comm ? w.vsend : (fresh ? take(ke) : w.vrecv[0]);
+  }
   w.dkacc = p.sigma > 1 ? take(ke * 2) : 0;
   w.dvacc = p.sigma > 1 ? take(ke * 2) : 0;
   w.dksend = take(ke);

@@ -38,15 +38,17 @@ upipe_status_t validate_shape(int C, const upipe_shape_t* sh, std::string& msg);
 Plan make_plan(int C, const upipe_shape_t& sh);
 
 // Workspace layout: byte offsets into the caller's workspace for one pass.
+// [2] = the two buffer sets of the overlapped (pipelined) schedule; in the sequential
+// schedule (or C == 1) index 1 aliases index 0.
 struct FwdWs {
-  size_t qsend, qrecv, ksend, krecv, vsend, vrecv, osend, orecv, yacc, total;
+  size_t qsend[2], qrecv[2], ksend, krecv[2], vsend, vrecv[2], osend[2], orecv[2], yacc, total;
 };
 struct BwdWs {
-  size_t qsend, qrecv, ksend, krecv, vsend, vrecv, dosend, dorecv, dsend, drecv, dqacc, dqsend, dqrecv, dkacc,
-      dvacc, dksend, dvsend, dkrecv, dvrecv, dxacc, total;
+  size_t qsend[2], qrecv[2], ksend, krecv[2], vsend, vrecv[2], dosend[2], dorecv[2], dsend[2], drecv[2], dqacc[2],
+      dqsend[2], dqrecv[2], dkacc, dvacc, dksend, dvsend, dkrecv, dvrecv, dxacc, total;
 };
-FwdWs fwd_workspace(const Plan& p);
-BwdWs bwd_workspace(const Plan& p);
+FwdWs fwd_workspace(const Plan& p, bool overlap);
+BwdWs bwd_workspace(const Plan& p, bool overlap);
 
 // ------------------------------------------------------------------ transport
 class Transport {
@@ -96,7 +98,28 @@ void count_launches(uint64_t n);
 
 }  // namespace upipe
 
+namespace upipe {
+// Streams and events of the overlapped schedule (comm stream = high priority, owned by the ctx).
+struct Pipe {
+  cudaStream_t comm = nullptr;
+  static constexpr int kEvents = 24;
+  cudaEvent_t ev[kEvents] = {};
+  bool ready = false;
+  ~Pipe() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (comm) cudaStreamDestroy(comm);
+  }
+};
+
+}  // namespace upipe
+
+namespace upipe {
+inline bool overlap_enabled(uint32_t flags, int C) { return C > 1 && !(flags & UPIPE_FLAG_SYNC_COMM); }
+}  // namespace upipe
+
 struct upipe_ctx_s {
+  upipe::Pipe pipe;
   upipe::Tracer tracer;
   int device = 0;
   int C = 1, rank = 0;

@@ -17,17 +17,20 @@ from . import upipe as U
 class UPipeAttention:
     def __init__(self, n_q_heads: int, n_kv_heads: int, head_dim: int, hidden: int, chunk_heads: int,
                  causal: bool = True, process_group=None, device=None, fabric=None, cp_rank: int | None = None,
-                 cp_size: int | None = None):
+                 cp_size: int | None = None, sync_comm: bool = False):
         """CP group: ``process_group`` (torch.distributed, one process per GPU, NCCL transport),
         or ``fabric`` + ``cp_rank`` + ``cp_size`` (single-process group driven by one host thread per rank),
-        or neither (C = 1)."""
+        or neither (C = 1). ``sync_comm``: sequential schedule with one chunk buffer set (the
+        paper's memory-minimal form); default overlaps the next chunk's all-to-all with the current
+        chunk's attention on a side stream (two buffer sets)."""
         self.Hq, self.Hkv, self.d, self.D, self.U = n_q_heads, n_kv_heads, head_dim, hidden, chunk_heads
         self.causal = int(causal)
+        self.flags = 1 if sync_comm else 0
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         if fabric is not None:
             self.C = cp_size
-            self.ctx = U.upipe_init_local(fabric, cp_rank, dev_index)
+            self.ctx = U.upipe_init_local(fabric, cp_rank, dev_index, self.flags)
             self.rank = cp_rank
         elif process_group is not None:
             import torch.distributed as dist
@@ -35,10 +38,10 @@ class UPipeAttention:
             self.rank = dist.get_rank(process_group)
             obj = [U.upipe_get_unique_id() if self.rank == 0 else None]
             dist.broadcast_object_list(obj, src=dist.get_global_rank(process_group, 0), group=process_group)
-            self.ctx = U.upipe_init(obj[0], self.C, self.rank, dev_index)
+            self.ctx = U.upipe_init(obj[0], self.C, self.rank, dev_index, self.flags)
         else:
             self.C, self.rank = 1, 0
-            self.ctx = U.upipe_init(None, 1, 0, dev_index)
+            self.ctx = U.upipe_init(None, 1, 0, dev_index, self.flags)
         self._ws = {}
 
     def shape(self, seq_local: int) -> U.upipe_shape_t:
@@ -47,7 +50,7 @@ class UPipeAttention:
     def workspace(self, seq_local: int, pass_: int) -> torch.Tensor:
         key = (seq_local, pass_)
         if key not in self._ws:
-            n = U.upipe_workspace_size(self.C, self.shape(seq_local), pass_)
+            n = U.upipe_workspace_size(self.C, self.shape(seq_local), pass_ + (2 if self.flags & 1 else 0))
             self._ws[key] = torch.empty(max(n, 256), dtype=torch.uint8, device=self.device)
         return self._ws[key]
 

@@ -90,7 +90,7 @@ def test_workspace_closed_forms(U):
     S_l, D, d = 4096, 4096, 128
     for C, Uc, Hq, Hkv in ((8, 8, 32, 8), (8, 16, 32, 8), (8, 32, 32, 8), (8, 8, 64, 8), (4, 4, 32, 8)):
         sh = U.make_shape(S_l, D, Hq, Hkv, d, Uc)
-        fwd = U.upipe_workspace_size(C, sh, 0)
+        fwd = U.upipe_workspace_size(C, sh, 2)          # sequential schedule: one buffer set
         qpd = Uc // C
         R = Hq // Hkv
         kv_res = max(1, qpd // R)
@@ -100,9 +100,15 @@ def test_workspace_closed_forms(U):
         yacc = 4 * S_l * D if Hq // Uc > 1 else 0
         assert abs(fwd - (chunk + o_bufs + yacc)) <= 256 * 12
         # Q-path (DESIGN A22) scales exactly with U: ratio vs Ulysses = U/Hq
+        # overlapped schedule (default for C > 1) doubles the chunk buffers (DESIGN A23)
+        assert abs(U.upipe_workspace_size(C, sh, 0) - (2 * (chunk + o_bufs) - 2 * S * d * 2 * kv_res + yacc)) <= 256 * 24
     shu = U.make_shape(S_l, D, 32, 8, d, 32)
     shp = U.make_shape(S_l, D, 32, 8, d, 8)
+    assert U.upipe_workspace_size(8, shp, 2) < U.upipe_workspace_size(8, shu, 2)
     assert U.upipe_workspace_size(8, shp, 0) < U.upipe_workspace_size(8, shu, 0)
+    # C = 1: no all-to-all, both schedules identical
+    sh1 = U.make_shape(4096, D, 32, 8, d, 8)
+    assert U.upipe_workspace_size(1, sh1, 0) == U.upipe_workspace_size(1, sh1, 2)
 
 
 def test_workspace_c1_aliases_send_and_recv(U):
