@@ -33,6 +33,7 @@ namespace {
 using namespace dev;
 
 struct BwdArgs {
+  float* dq_acc;
   const float* lse;
   const float* delta;
   float* dk_acc;
@@ -53,6 +54,10 @@ __device__ __forceinline__ float ex2b(float x) {
 }
 
 constexpr int kComputeWarps = 8;
+#ifndef UPIPE_DQ_ATOMICS
+#define UPIPE_DQ_ATOMICS 0
+#endif
+constexpr bool kDqAtomics = UPIPE_DQ_ATOMICS;   // dQ drain: 0 = smem + TMA reduce (default, measured faster), 1 = red.global.add.v4.f32
 constexpr int kThreads = (kComputeWarps + 2) * 32;
 constexpr int kTmaWarp = kComputeWarps, kMmaWarp = kComputeWarps + 1;
 
@@ -335,6 +340,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(dq_empty);
+      if (kDqAtomics) {
+        // fire-and-forget fp32 vector reductions straight from registers (no shared-memory staging)
+        const long long q = q0 + r;
+        if (q < a.S) {
+          float* dst = a.dq_acc + q * (long long)a.nq * D + (long long)h * D + wg * kBoxesPerWg * 32;
+#pragma unroll
+          for (int b = 0; b < kBoxesPerWg; ++b)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              atomicAdd(reinterpret_cast<float4*>(dst + b * 32 + 4 * j),
+                        make_float4(__uint_as_float(rq[b][4 * j + 0]) * a.scale, __uint_as_float(rq[b][4 * j + 1]) * a.scale,
+                                    __uint_as_float(rq[b][4 * j + 2]) * a.scale, __uint_as_float(rq[b][4 * j + 3]) * a.scale));
+        }
+      } else {
 #pragma unroll
       for (int b = 0; b < kBoxesPerWg; ++b) {
         const uint32_t stbase = smem_u32(slot(b));
@@ -353,6 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int b = 0; b < kBoxesPerWg; ++b)
           tma_reduce_add_2d(&tmdQ, slot(b), h * D + (wg * kBoxesPerWg + b) * 32, (int)q0);
         bulk_commit();
+      }
       }
       tl[4] += clock64() - c4;
     }
@@ -427,6 +447,7 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   if (!make_tmap_2d_f32(&tdq, p.dq_acc, (uint64_t)p.nq * p.d, p.S, (uint64_t)p.nq * p.d, 32, 128, err, errlen))
     return cudaErrorInvalidValue;
   BwdArgs a;
+  a.dq_acc = p.dq_acc;
   a.lse = p.lse;
   a.delta = p.delta;
   a.dk_acc = p.dk_acc;

@@ -1,9 +1,10 @@
 // tcgen05 GEMM for the UPipe projections.
 //
-// One CTA computes a 128 x BN output tile: warp 0 issues TMA loads of 64-wide
+// Persistent CTAs (one per SM) walk 128 x BN output tiles: warp 0 issues TMA loads of 64-wide
 // granules into a STAGES-deep shared-memory ring (128B swizzle), warp 1 issues
 // tcgen05.mma (M=128, N=BN, K=16) into a TMEM accumulator, warps 2..5 drain TMEM
-// with tcgen05.ld (one accumulator row per thread) and run the epilogue
+// with tcgen05.ld (one accumulator row per thread; two accumulators so the epilogue
+// of one tile overlaps the next tile's main loop) and run the epilogue
 // (bf16 store into the all-to-all send layout, fp32 store, or fp32 accumulate).
 // The per-stage head gather of the UPipe schedule is folded into the TMA
 // coordinates (see OperandMap in kernels.h), so no pack kernel runs before the
@@ -62,19 +63,23 @@ struct Cfg {
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs g) {
+  // Persistent: CTA b processes tiles b, b + gridDim.x, ... (N fastest, so CTAs running at the
+  // same time share the A row block through L2). Two TMEM accumulators: the epilogue of tile i
+  // overlaps the main loop of tile i+1.
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
-  uint64_t* tmem_full = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* acc_full = empty + C::STAGES;   // [2]
+  uint64_t* acc_empty = acc_full + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int n0 = blockIdx.x * BN;
-  const int m0 = blockIdx.y * BM;
+  const int ntn = (g.N + BN - 1) / BN;
+  const int ntiles = ntn * ((g.M + BM - 1) / BM);
   const int nk = (g.K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -84,10 +89,13 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 128);
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<BN>(tmem_slot);
+  if (warp == 1) tmem_alloc<2 * BN>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -98,27 +106,30 @@ __global__ void __launch_bounds__(192, 1)
       // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sa = ring + stage * C::STAGE_BYTES;
-        uint8_t* sb = sa + C::A_BYTES;
-        const int k0 = kb * BK;
-        mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int m0 = (t / ntn) * BM, n0 = (t % ntn) * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = ring + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          const int k0 = kb * BK;
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
 #pragma unroll
-        for (int c = 0; c < BM / 64; ++c) {
-          const int i = m0 + c * 64;
-          const int oc = map_outer(g.a, i, k0), kc = map_k(g.a, i, k0);
-          if (A_MN) tma_load_2d(sa + c * GRANULE_BYTES, &tmA, &full[stage], oc, kc);
-          else      tma_load_2d(sa + c * GRANULE_BYTES, &tmA, &full[stage], kc, oc);
-        }
+          for (int c = 0; c < BM / 64; ++c) {
+            const int i = m0 + c * 64;
+            const int oc = map_outer(g.a, i, k0), kc = map_k(g.a, i, k0);
+            if (A_MN) tma_load_2d(sa + c * GRANULE_BYTES, &tmA, &full[stage], oc, kc);
+            else      tma_load_2d(sa + c * GRANULE_BYTES, &tmA, &full[stage], kc, oc);
+          }
 #pragma unroll
-        for (int c = 0; c < BN / 64; ++c) {
-          const int i = n0 + c * 64;
-          const int oc = map_outer(g.b, i, k0), kc = map_k(g.b, i, k0);
-          if (B_MN) tma_load_2d(sb + c * GRANULE_BYTES, &tmB, &full[stage], oc, kc);
-          else      tma_load_2d(sb + c * GRANULE_BYTES, &tmB, &full[stage], kc, oc);
+          for (int c = 0; c < BN / 64; ++c) {
+            const int i = n0 + c * 64;
+            const int oc = map_outer(g.b, i, k0), kc = map_k(g.b, i, k0);
+            if (B_MN) tma_load_2d(sb + c * GRANULE_BYTES, &tmB, &full[stage], oc, kc);
+            else      tma_load_2d(sb + c * GRANULE_BYTES, &tmB, &full[stage], kc, oc);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -127,78 +138,91 @@ __global__ void __launch_bounds__(192, 1)
       constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&full[stage], phase);
+      int i = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int ab = i & 1;
+        mbar_wait(&acc_empty[ab], ((i >> 1) & 1) ^ 1);     // the epilogue has drained this accumulator
         tc_fence_after();
-        const uint32_t sa = smem_u32(ring + stage * C::STAGE_BYTES);
-        const uint32_t sb = sa + C::A_BYTES;
+        const uint32_t acc = tmem + ab * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(ring + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint64_t da = A_MN ? desc_sw128(sa + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sa + kk * 32, 16, 1024);
-          const uint64_t db = B_MN ? desc_sw128(sb + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sb + kk * 32, 16, 1024);
-          mma_ss(tmem, da, db, idesc, (kb | kk) != 0);
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t da = A_MN ? desc_sw128(sa + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t db = B_MN ? desc_sw128(sb + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sb + kk * 32, 16, 1024);
+            mma_ss(acc, da, db, idesc, (kb | kk) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&empty[stage]);
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        mma_commit(&acc_full[ab]);
       }
-      mma_commit(tmem_full);
     }
   } else {
     // ---------------- epilogue warps 2..5: TMEM lane quadrant = warp % 4
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
-    const int m = m0 + row;
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const bool mvalid = m < g.M;
-    const long long mseg = mvalid ? m / g.c.m_len : 0, min_ = mvalid ? m % g.c.m_len : 0;
+    int i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int ab = i & 1;
+      const int m0 = (t / ntn) * BM, n0 = (t % ntn) * BN;
+      const int m = m0 + row;
+      mbar_wait(&acc_full[ab], (i >> 1) & 1);
+      tc_fence_after();
+      const bool mvalid = m < g.M;
+      const long long mseg = mvalid ? m / g.c.m_len : 0, min_ = mvalid ? m % g.c.m_len : 0;
 #pragma unroll 1
-    for (int c32 = 0; c32 < BN / 32; ++c32) {
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + c32 * 32, r);
-      tmem_wait_ld();
-      const int n = n0 + c32 * 32;
-      if (!mvalid || n >= g.N) continue;
-      const long long nseg = n / g.c.n_len, nin = n % g.c.n_len;
-      const long long orow = g.c.r_base + mseg * g.c.r_mstride + min_ + nseg * g.c.r_nstride;
-      const long long ocol = g.c.c_base + nseg * g.c.c_nstride + nin + mseg * g.c.c_mstride;
-      float v[32];
+      for (int c32 = 0; c32 < BN / 32; ++c32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ab * BN + ((uint32_t)(quad * 32) << 16) + c32 * 32, r);
+        tmem_wait_ld();
+        const int n = n0 + c32 * 32;
+        if (!mvalid || n >= g.N) continue;
+        const long long nseg = n / g.c.n_len, nin = n % g.c.n_len;
+        const long long orow = g.c.r_base + mseg * g.c.r_mstride + min_ + nseg * g.c.r_nstride;
+        const long long ocol = g.c.c_base + nseg * g.c.c_nstride + nin + mseg * g.c.c_mstride;
+        float v[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * g.alpha;
-      if (g.c.epi == (int)Epi::kStoreBF16) {
-        uint4* dst = reinterpret_cast<uint4*>(g.c.bf16 + orow * g.c.ld_bf16 + ocol);
+        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]) * g.alpha;
+        if (g.c.epi == (int)Epi::kStoreBF16) {
+          uint4* dst = reinterpret_cast<uint4*>(g.c.bf16 + orow * g.c.ld_bf16 + ocol);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                              pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
-      } else {
-        float4* dst = reinterpret_cast<float4*>(g.c.f32 + orow * g.c.ld_f32 + ocol);
-        if (g.c.epi != (int)Epi::kStoreF32) {
+          for (int q = 0; q < 4; ++q)
+            dst[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                                pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+        } else {
+          float4* dst = reinterpret_cast<float4*>(g.c.f32 + orow * g.c.ld_f32 + ocol);
+          if (g.c.epi != (int)Epi::kStoreF32) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 o = dst[i];
-            v[4 * i + 0] += o.x; v[4 * i + 1] += o.y; v[4 * i + 2] += o.z; v[4 * i + 3] += o.w;
+            for (int q = 0; q < 8; ++q) {
+              const float4 o = dst[q];
+              v[4 * q + 0] += o.x; v[4 * q + 1] += o.y; v[4 * q + 2] += o.z; v[4 * q + 3] += o.w;
+            }
+          }
+          if (g.c.epi == (int)Epi::kAccF32ToBF16) {
+            uint4* d2 = reinterpret_cast<uint4*>(g.c.bf16 + orow * g.c.ld_bf16 + ocol);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              d2[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                                 pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
           }
         }
-        if (g.c.epi == (int)Epi::kAccF32ToBF16) {
-          const long long orow2 = orow, ocol2 = ocol;
-          uint4* d2 = reinterpret_cast<uint4*>(g.c.bf16 + orow2 * g.c.ld_bf16 + ocol2);
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            d2[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                               pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        }
       }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[ab]);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<BN>(tmem);
+    tmem_dealloc<2 * BN>(tmem);
   }
 }
 
@@ -213,7 +237,14 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs&
   auto kern = gemm_kernel<BN, A_MN, B_MN>;
   static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (attr != cudaSuccess) return attr;
-  dim3 grid((args.N + BN - 1) / BN, (args.M + BM - 1) / BM);
+  static const int num_sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  const int ntiles = ((args.N + BN - 1) / BN) * ((args.M + BM - 1) / BM);
+  dim3 grid(ntiles < num_sms ? ntiles : num_sms);
   kern<<<grid, 192, C::SMEM, s>>>(ta, tb, args);
   count_launches(1);
   return cudaGetLastError();
