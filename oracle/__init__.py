@@ -183,6 +183,52 @@ def layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, causal=True):
     return dX, dWq, dWk, dWv, dWo
 
 
+def layer_fwd_rows(X_rows, rows, K, V, Wq, Wo, Hq, Hkv, d, causal=True):
+    """Row-sampled forward: y, O, lse of the given query rows only.
+
+    ``X_rows`` are those rows of X; ``K``, ``V`` = X Wk^T, X Wv^T for all tokens ([S, Hkv, d]).
+    Each row is computed exactly as in ``layer_fwd`` (rows of attention are independent).
+    """
+    Qr = (X_rows @ Wq.T).reshape(len(rows), Hq, d)
+    O, lse = attn_fwd(Qr, K, V, causal, rows=rows)
+    O2 = O.reshape(len(rows), Hq * d)
+    return O2 @ Wo.T, O2, lse
+
+
+def layer_bwd_tail(X_tail, dY_tail, K, V, Wq, Wk, Wv, Wo, Hq, Hkv, d):
+    """dX of the last w tokens of a causal layer (w = len(X_tail)), following the same
+    formulas as ``attn_bwd``/``layer_bwd``: with a causal mask, dK_j and dV_j of a key j in
+    the tail only receive contributions from queries i >= j, which are all in the tail;
+    dQ_i needs row i against all keys. So the tail's dX is exact from the tail rows alone."""
+    S = K.shape[0]
+    w = X_tail.shape[0]
+    t0 = S - w
+    R = Hq // Hkv
+    scale = 1.0 / math.sqrt(d)
+    Qt = (X_tail @ Wq.T).reshape(w, Hq, d)
+    dOt = (dY_tail @ Wo).reshape(w, Hq, d)
+    dQ = np.zeros((w, Hq, d))
+    dK = np.zeros((w, Hkv, d))
+    dV = np.zeros((w, Hkv, d))
+    qi = np.arange(t0, S)
+    keys = np.arange(S)
+    for h in range(Hq):
+        g = h // R
+        s = (Qt[:, h, :] @ K[:, g, :].T) * scale
+        s = np.where(keys[None, :] <= qi[:, None], s, -np.inf)
+        m = np.max(s, axis=1, keepdims=True)
+        P = np.exp(s - m)
+        P /= np.sum(P, axis=1, keepdims=True)
+        Ot = P @ V[:, g, :]
+        Dv = np.sum(dOt[:, h, :] * Ot, axis=1, keepdims=True)
+        dP = dOt[:, h, :] @ V[:, g, :].T
+        dS = P * (dP - Dv)
+        dQ[:, h, :] = (dS @ K[:, g, :]) * scale
+        dK[:, g, :] += (dS[:, t0:].T @ Qt[:, h, :]) * scale
+        dV[:, g, :] += P[:, t0:].T @ dOt[:, h, :]
+    return dQ.reshape(w, -1) @ Wq + dK.reshape(w, -1) @ Wk + dV.reshape(w, -1) @ Wv
+
+
 # ----------------------------------------------------------------------------
 # GQA schedule  (P:362-380 §4.1, Fig. 4 caption P:306; DESIGN A8)
 # ----------------------------------------------------------------------------

@@ -1,0 +1,72 @@
+"""Parity at BASELINE.json's full size, in the launch configuration bench.py times at N=1:
+Llama3-8B attention layer (32 Q / 8 KV heads, d=128, hidden 4096), S = 131072 tokens,
+C = 1, U = 8, inputs drawn on the device by the same seeded generator. The fp64 oracle
+cannot run the whole layer at this size, so it computes sampled outputs one by one
+(oracle.layer_fwd_rows: y / O / lse of chosen query rows, spread over tiles and the
+ends of the sequence; oracle.layer_bwd_tail: dX of the last w tokens, which a causal
+layer determines from the tail rows alone). Bar: the north_star tolerance."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import assert_close, dev, to_np
+
+pytestmark = pytest.mark.gpu
+
+S, D, Hq, Hkv, d, U = 131072, 4096, 32, 8, 128, 8
+ROWS = np.array([0, 1, 127, 128, 129, 4095, 65535, 65536, 100003, 131071])
+TAIL = 24
+REL, ABS = 5e-3, 2e-2
+
+
+def test_fullsize_bench_workload_sampled_rows():
+    from paper_2602_21196_b200 import UPipeAttention, upipe
+    e = synth.layer_exponents(D, Hq, d, S)
+
+    def fill(shape, name):
+        t = torch.empty(shape, dtype=torch.bfloat16, device=dev())
+        upipe.upipe_synth_fill_bf16(t, t.numel(), 0, synth.TID[name], e[name], 0)
+        return t
+
+    x, dy = fill((S, D), "x"), fill((S, D), "dy")
+    W = [fill((Hq * d, D), "wq"), fill((Hkv * d, D), "wk"), fill((Hkv * d, D), "wv"), fill((D, Hq * d), "wo")]
+    attn = UPipeAttention(Hq, Hkv, d, D, U)
+    y, saved = attn.forward(x, *W)
+    dx, *_ = attn.backward(x, *W, dy, saved)
+    torch.cuda.synchronize()
+    y_s = to_np(y[ROWS.tolist()])
+    o_s = to_np(saved[0][ROWS.tolist()])
+    lse_s = to_np(saved[1][:, ROWS.tolist()])
+    dx_t = to_np(dx[S - TAIL:])
+    attn.close()
+    del x, dy, y, saved, dx, W
+    torch.cuda.empty_cache()
+
+    # ---- oracle, fp64 on the host, from the same generator
+    wq = synth.draw(0, synth.TID["wq"], (Hq * d, D), e["wq"])
+    wk = synth.draw(0, synth.TID["wk"], (Hkv * d, D), e["wk"])
+    wv = synth.draw(0, synth.TID["wv"], (Hkv * d, D), e["wv"])
+    wo = synth.draw(0, synth.TID["wo"], (D, Hq * d), e["wo"])
+    K = np.empty((S, Hkv * d))
+    V = np.empty((S, Hkv * d))
+    chunk = 8192
+    for t0 in range(0, S, chunk):
+        xc = synth.draw(0, synth.TID["x"], (chunk, D), e["x"], start=t0 * D)
+        K[t0:t0 + chunk] = oracle.project(xc, wk)
+        V[t0:t0 + chunk] = oracle.project(xc, wv)
+    K = K.reshape(S, Hkv, d)
+    V = V.reshape(S, Hkv, d)
+    x_rows = synth.draw_rows(0, synth.TID["x"], D, ROWS, e["x"])
+    Y, Oo, L = oracle.layer_fwd_rows(x_rows, ROWS, K, V, wq, wo, Hq, Hkv, d)
+    assert_close("y rows", y_s, Y, REL, ABS)
+    assert_close("o_saved rows", o_s, Oo, REL, ABS)
+    # C = 1, U = 8: lse slot s*8 + j holds head 8 s + j, i.e. slot == head (upipe.h, DESIGN A8)
+    sh = upipe.make_shape(S, D, Hq, Hkv, d, U)
+    order = [upipe.upipe_plan_stage(1, sh, s, 0).q0 + j for s in range(Hq // U) for j in range(U)]
+    assert_close("lse rows", lse_s, L[order], REL, ABS)
+    x_tail = synth.draw(0, synth.TID["x"], (TAIL, D), e["x"], start=(S - TAIL) * D)
+    dy_tail = synth.draw(0, synth.TID["dy"], (TAIL, D), e["dy"], start=(S - TAIL) * D)
+    dX = oracle.layer_bwd_tail(x_tail, dy_tail, K, V, wq, wk, wv, wo, Hq, Hkv, d)
+    assert_close("dx tail rows", dx_t, dX, REL, ABS)

@@ -365,3 +365,21 @@ def test_synth_values_exact_bf16_and_deterministic():
     np.testing.assert_array_equal(v[500:], w)         # global indexing: shards agree
     assert abs(v.mean()) < 0.15 and 0.9 < v.std() / (2 / math.sqrt(3)) < 1.1
     assert set(np.unique(synth.draw_codes(3, 2, 0, 100000))) == set(range(256))
+
+
+def test_row_sampled_layer_matches_full():
+    # the row-sampled / tail modes used at full size equal the full oracle on a small case
+    S, D, Hq, Hkv, d = 150, 24, 4, 2, 8
+    X, Wq, Wk, Wv = rand(S, D), rand(Hq * d, D, scale=.3), rand(Hkv * d, D, scale=.3), rand(Hkv * d, D, scale=.3)
+    Wo, dY = rand(D, Hq * d, scale=.3), rand(S, D)
+    Y, Oo, L = O.layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d)
+    K = (X @ Wk.T).reshape(S, Hkv, d)
+    V = (X @ Wv.T).reshape(S, Hkv, d)
+    rows = np.array([0, 1, 63, 64, 100, 149])
+    y, o, lse = O.layer_fwd_rows(X[rows], rows, K, V, Wq, Wo, Hq, Hkv, d)
+    np.testing.assert_allclose(y, Y[rows], atol=1e-12)
+    np.testing.assert_allclose(lse, L[:, rows], atol=1e-12)
+    dX = O.layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d)[0]
+    w = 17
+    np.testing.assert_allclose(O.layer_bwd_tail(X[-w:], dY[-w:], K, V, Wq, Wk, Wv, Wo, Hq, Hkv, d), dX[-w:],
+                               atol=1e-11)
