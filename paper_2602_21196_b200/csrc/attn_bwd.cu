@@ -13,6 +13,11 @@
 // warpgroup drains its half of dQ TMEM -> shared memory (32-column boxes) and one
 // of its threads issues cp.reduce.async.bulk.tensor; the 1/sqrt(d) scale of dQ is
 // applied when the accumulator is converted to bf16.
+// Issue order per query tile n: dV(n), dQ(n), S(n+1), dP(n+1), dK(n). The TMEM budget
+// (S|dP|dV|dK = 512 columns at d = 128) rules out double-buffering S/dP, so the tile-to-tile
+// chain is E(n) -> 4 MMAs -> E(n+1); dK(n) is issued last and overlaps E(n+1) (which only
+// waits for it before overwriting dS^T in shared memory), and the dQ(n) drain overlaps
+// S(n+1)/dP(n+1).
 // dK/dV stay in TMEM for the whole CTA and are written (and optionally accumulated
 // across the UPipe stages of one super-stage) at the end.
 // Warps: 0-7 compute (two warpgroups, each owning 64 of the 128 query columns of
@@ -53,13 +58,11 @@ __device__ __forceinline__ float ex2b(float x) {
   return y;
 }
 
-constexpr int kComputeWarps = 8;
-#ifndef UPIPE_DQ_ATOMICS
-#define UPIPE_DQ_ATOMICS 0
-#endif
-constexpr bool kDqAtomics = UPIPE_DQ_ATOMICS;   // dQ drain: 0 = smem + TMA reduce (default, measured faster), 1 = red.global.add.v4.f32
-constexpr int kThreads = (kComputeWarps + 2) * 32;
-constexpr int kTmaWarp = kComputeWarps, kMmaWarp = kComputeWarps + 1;
+constexpr int kSoftmaxWarps = 8;                  // two warpgroups: P^T, dS^T (+ dK/dV epilogue)
+constexpr int kRegsSoftmax = 144, kRegsDrain = 168, kRegsOther = 48;   // setmaxnreg split of the 64K registers
+constexpr int kThreads = (kSoftmaxWarps + 8) * 32;  // + dQ drain warpgroup + {TMA, MMA, 2 idle}
+constexpr int kTmaWarp = kSoftmaxWarps + 4, kMmaWarp = kSoftmaxWarps + 5;
+static_assert(2 * 128 * kRegsSoftmax + 128 * kRegsDrain + 128 * kRegsOther <= 65536, "register split");
 
 template <int D>
 struct BwdCfg {
@@ -76,7 +79,11 @@ struct BwdCfg {
   static constexpr int DQ_BOXES = D / 32;                         // 32-column fp32 boxes of dQ per query tile
 };
 
-template <int D>
+// Cycle counters of the per-role timeline; compiled out unless the timeline variant is launched.
+template <bool TL>
+__device__ __forceinline__ long long tick() { if constexpr (TL) return clock64(); else return 0; }
+
+template <int D, bool TL>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -98,6 +105,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* dq_full = bars + 9;
   uint64_t* dq_empty = bars + 10;
   uint64_t* dkv_full = bars + 11;
+  uint64_t* ds_empty = bars + 12;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = warp_id(), lane = lane_id();
@@ -108,11 +116,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int qt_begin = a.causal ? jb : 0;
   const int n_qt = nT - qt_begin;
   const int N = G * n_qt;                         // (head, query tile) iterations
-  constexpr int kCompute = kComputeWarps * 32;
+  constexpr int kSoftmax = kSoftmaxWarps * 32;
 
   if (warp == kTmaWarp && lane == 0) {
     tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
-    for (int i = 0; i < 12; ++i) mbar_init(&bars[i], (i == 8 || i == 10) ? kCompute : 1);
+    for (int i = 0; i < 13; ++i) mbar_init(&bars[i], i == 8 ? kSoftmax : i == 10 ? 128 : 1);
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
@@ -121,6 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  if (warp >= kTmaWarp) regs_dec<kRegsOther>();   // warpgroup 3 hands registers to the others
   if (warp == kTmaWarp) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
@@ -156,36 +165,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
       const uint32_t sQ0 = smem_u32(smem + C::OFF_Q), sdO = smem_u32(smem + C::OFF_DO);
       const uint32_t sdS = smem_u32(smem + C::OFF_DS);
+      // Descriptor of (base + off) = descriptor of base + off / 16 (start-address field, bits 0-13).
+      // Rolled loops with running offsets keep the issuer within its register budget.
       auto mma_kk = [&](uint32_t sa, uint32_t sb, uint32_t tm) {      // [128 x D] x [128 x D]^T
-#pragma unroll
-        for (int c = 0; c < NCH; ++c)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_ss(tm, desc_sw128(sa + c * 16384 + kk * 32, 16, 1024), desc_sw128(sb + c * 16384 + kk * 32, 16, 1024),
-                   id_kk, (c | kk) != 0);
+        const uint64_t da = desc_sw128(sa, 16, 1024), db = desc_sw128(sb, 16, 1024);
+#pragma unroll 1
+        for (int i = 0; i < 4 * NCH; ++i) {
+          const uint32_t off = ((i >> 2) * 16384 + (i & 3) * 32) >> 4;
+          mma_ss(tm, da + off, db + off, id_kk, i != 0);
+        }
       };
       auto mma_kmn = [&](uint32_t sa, uint32_t sb, uint32_t tm, bool acc) {  // A [128 x 128 q] K-major smem
-#pragma unroll
-        for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_ss(tm, desc_sw128(sa + kb * 16384 + kk * 32, 16, 1024),
-                   desc_sw128(sb + kb * 8192 + kk * 2048, 16384, 1024), id_kmn, (acc || kb || kk) ? 1u : 0u);
+        const uint64_t da = desc_sw128(sa, 16, 1024), db = desc_sw128(sb, 16384, 1024);
+#pragma unroll 1
+        for (int i = 0; i < 8; ++i)
+          mma_ss(tm, da + (((i >> 2) * 16384 + (i & 3) * 32) >> 4), db + i * (2048 >> 4), id_kmn, (acc || i) ? 1u : 0u);
       };
       // A = P^T in TMEM: queries [16 ks, 16 ks + 16) are packed at TMEM cols 64 (ks / 4) + 8 (ks % 4)
       auto mma_tmn = [&](uint32_t ta, uint32_t sb, uint32_t tm, bool acc) {
-#pragma unroll
+        const uint64_t db = desc_sw128(sb, 16384, 1024);
+#pragma unroll 1
         for (int ks = 0; ks < 8; ++ks)
-          mma_ts(tm, ta + (ks >> 2) * 64 + (ks & 3) * 8, desc_sw128(sb + (ks >> 2) * 8192 + (ks & 3) * 2048, 16384, 1024),
-                 id_kmn, (acc || ks) ? 1u : 0u);
+          mma_ts(tm, ta + (ks >> 2) * 64 + (ks & 3) * 8, db + ks * (2048 >> 4), id_kmn, (acc || ks) ? 1u : 0u);
       };
       auto mma_mnmn = [&](uint32_t sa, uint32_t sb, uint32_t tm) {  // dQ = dS K: K dim = keys (rows of both)
-#pragma unroll
-        for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_ss(tm, desc_sw128(sa + kb * 8192 + kk * 2048, 16384, 1024),
-                   desc_sw128(sb + kb * 8192 + kk * 2048, 16384, 1024), id_mnmn, (kb | kk) != 0);
+        const uint64_t da = desc_sw128(sa, 16384, 1024), db = desc_sw128(sb, 16384, 1024);
+#pragma unroll 1
+        for (int i = 0; i < 8; ++i) mma_ss(tm, da + i * (2048 >> 4), db + i * (2048 >> 4), id_mnmn, i != 0);
       };
       mbar_wait(kv_full, 0);
       mbar_wait(&q_full[0], 0);
@@ -197,55 +203,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_commit(sdp_full);
       for (int n = 0; n < N; ++n) {
         const int b = n & 1;
-        long long t0 = clock64();
+        long long t0 = tick<TL>();
         mbar_wait(ds_full, n & 1);
-        long long t1 = clock64();
+        long long t1 = tick<TL>();
         tl[0] += t1 - t0;
         tc_fence_after();
         mma_tmn(tmem + C::TM_S, sdO, tmem + C::TM_DV, n > 0);
-        mma_commit(do_empty);
-        mma_kmn(sdS, sQ0 + b * C::TB, tmem + C::TM_DK, n > 0);
-        mma_commit(&q_empty[b]);
+        mma_commit(do_empty);                           // dO(n) consumed: the producer loads dO(n+1)
         mma_mnmn(sdS, sK, tmem + C::TM_DQ);
-        mma_commit(dq_full);
-        tl[1] += clock64() - t1;
+        mma_commit(dq_full);                            // drained while S(n+1), dP(n+1) run
+        tl[1] += tick<TL>() - t1;
         if (n + 1 < N) {
           const int b1 = (n + 1) & 1;
-          long long t2 = clock64();
+          long long t2 = tick<TL>();
           mbar_wait(&q_full[b1], ((n + 1) >> 1) & 1);
-          tl[2] += clock64() - t2;
+          tl[2] += tick<TL>() - t2;
           tc_fence_after();
           mma_kk(sK, sQ0 + b1 * C::TB, tmem + C::TM_S);   // in-order after dV(n), which reads P^T from these columns
-          long long t3 = clock64();
+          long long t3 = tick<TL>();
           mbar_wait(dq_empty, n & 1);
-          long long t4 = clock64();
+          long long t4 = tick<TL>();
           mbar_wait(do_full, (n + 1) & 1);
           tl[3] += t4 - t3;
-          tl[4] += clock64() - t4;
+          tl[4] += tick<TL>() - t4;
           tc_fence_after();
           mma_kk(sV, sdO, tmem + C::TM_DP);
           mma_commit(sdp_full);
         }
+        // dK(n) last: it runs on the tensor core while the compute warps start on tile n+1
+        mma_kmn(sdS, sQ0 + b * C::TB, tmem + C::TM_DK, n > 0);
+        mma_commit(&q_empty[b]);
+        mma_commit(ds_empty);                           // dS^T(n) consumed: tile n+1 may overwrite it
       }
       mma_commit(dkv_full);
       if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0)
         for (int i = 0; i < 5; ++i) a.dbg[5 + i] = tl[i];
     }
-  } else {
-    // ------------------------------------------------ compute warpgroups (warps 0-7)
+  } else if (warp < kSoftmaxWarps) {
+    // ------------------------------------------------ softmax-gradient warpgroups (warps 0-7)
+    regs_inc<kRegsSoftmax>();
     const int wg = warp >> 2;                         // query columns [64 wg, 64 wg + 64) in two 32-column chunks
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const long long key = (long long)jb * 128 + r;
     const float sl2 = a.scale_log2;
-    const bool issuer = quad == 0 && lane == 0;
-    constexpr int kBoxesPerWg = C::DQ_BOXES / 2;      // dQ boxes (32 fp32 columns) drained per warpgroup
-    // staging slot of box b of this warpgroup: slots 0,1 = spare buffer, slots 2,3 = dS^T (free after the dQ MMA)
-    auto slot = [&](int b) -> uint8_t* {
-      const int s_ = wg * kBoxesPerWg + b;
-      return s_ < 2 ? smem + C::OFF_STG + s_ * 16384 : smem + C::OFF_DS + (s_ - 2) * 16384;
-    };
     const uint32_t dsbase = smem_u32(smem + C::OFF_DS) + wg * 16384;   // dS^T chunk of this warpgroup's 64 queries
     float stat_next = 0.f;                            // warpgroup 0 prefetches lse, warpgroup 1 delta, one tile ahead
     auto load_stat = [&](int n) -> float {
@@ -255,21 +257,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       return wg == 0 ? a.lse[(long long)h * a.ld_lse + q] * 1.4426950408889634f : a.delta[q * a.ld_delta + h];
     };
     if (N > 0) stat_next = load_stat(0);
-    long long tl[5] = {0, 0, 0, 0, 0};
+    long long tl[4] = {0, 0, 0, 0};
     for (int n = 0; n < N; ++n) {
-      const int h = g * G + n / n_qt;
       const int qt = qt_begin + n % n_qt;
       const long long q0 = (long long)qt * 128;
       const int sb = n & 1;
       if (wg == 0) s_lse2[sb][r] = stat_next;
       else s_delta[sb][r] = stat_next;
       if (n + 1 < N) stat_next = load_stat(n + 1);
-      if (issuer) bulk_wait_read0();                  // previous dQ reduces have finished reading the staging slots
-      long long c0 = clock64();
-      named_bar_sync(1, kCompute);
-      long long c1 = clock64();
+      long long c0 = tick<TL>();
+      named_bar_sync(1, kSoftmax);
+      long long c1 = tick<TL>();
       mbar_wait(sdp_full, n & 1);
-      long long c2 = clock64();
+      long long c2 = tick<TL>();
       tl[0] += c1 - c0;
       tl[1] += c2 - c1;
       tc_fence_after();
@@ -313,6 +313,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           rs[i] = pack_bf16(__uint_as_float(rs[2 * i]), __uint_as_float(rs[2 * i + 1]));
         // P^T (bf16 pairs) back into S^T columns already read: queries [col0, col0+32) -> cols 64 wg + 16 c
         tmem_st16(tmem + C::TM_S + lane_off + wg * 64 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(rs));
+        if (c == 0 && n > 0) {                         // dK(n-1) has read dS^T(n-1)
+          long long w0 = tick<TL>();
+          mbar_wait(ds_empty, (n - 1) & 1);
+          tl[3] += tick<TL>() - w0;
+        }
 #pragma unroll
         for (int v8 = 0; v8 < 4; ++v8) {
           const int qc = c * 32 + v8 * 8;
@@ -327,58 +332,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(ds_full);
-      long long c3 = clock64();
-      tl[2] += c3 - c2;
-      // ---- dQ drain: TMEM lane = query row; this warpgroup drains dQ columns [wg D/2, (wg+1) D/2)
-      mbar_wait(dq_full, n & 1);
-      long long c4 = clock64();
-      tl[3] += c4 - c3;
-      tc_fence_after();
-      uint32_t rq[kBoxesPerWg][32];
-#pragma unroll
-      for (int b = 0; b < kBoxesPerWg; ++b) tmem_ld32(tmem + C::TM_DQ + lane_off + (wg * kBoxesPerWg + b) * 32, rq[b]);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(dq_empty);
-      if (kDqAtomics) {
-        // fire-and-forget fp32 vector reductions straight from registers (no shared-memory staging)
-        const long long q = q0 + r;
-        if (q < a.S) {
-          float* dst = a.dq_acc + q * (long long)a.nq * D + (long long)h * D + wg * kBoxesPerWg * 32;
-#pragma unroll
-          for (int b = 0; b < kBoxesPerWg; ++b)
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              atomicAdd(reinterpret_cast<float4*>(dst + b * 32 + 4 * j),
-                        make_float4(__uint_as_float(rq[b][4 * j + 0]) * a.scale, __uint_as_float(rq[b][4 * j + 1]) * a.scale,
-                                    __uint_as_float(rq[b][4 * j + 2]) * a.scale, __uint_as_float(rq[b][4 * j + 3]) * a.scale));
-        }
-      } else {
-#pragma unroll
-      for (int b = 0; b < kBoxesPerWg; ++b) {
-        const uint32_t stbase = smem_u32(slot(b));
-#pragma unroll
-        for (int j = 0; j < 8; ++j)       // 16-byte chunk j of the 128-byte row, swizzled by row % 8
-          st_shared_v4(stbase + r * 128 + ((j ^ (r & 7)) << 4),
-                       __float_as_uint(__uint_as_float(rq[b][4 * j + 0]) * a.scale),
-                       __float_as_uint(__uint_as_float(rq[b][4 * j + 1]) * a.scale),
-                       __float_as_uint(__uint_as_float(rq[b][4 * j + 2]) * a.scale),
-                       __float_as_uint(__uint_as_float(rq[b][4 * j + 3]) * a.scale));
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(2 + wg, 128);
-      if (issuer) {
-#pragma unroll
-        for (int b = 0; b < kBoxesPerWg; ++b)
-          tma_reduce_add_2d(&tmdQ, slot(b), h * D + (wg * kBoxesPerWg + b) * 32, (int)q0);
-        bulk_commit();
-      }
-      }
-      tl[4] += clock64() - c4;
+      tl[2] += tick<TL>() - c2;
     }
-    if (issuer) bulk_wait0();
     if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && warp == 0 && lane == 0) {
-      for (int i = 0; i < 5; ++i) a.dbg[i] = tl[i];
+      for (int i = 0; i < 3; ++i) a.dbg[i] = tl[i];
+      a.dbg[11] = tl[3];
       a.dbg[10] = N;
     }
     // ---- dK / dV epilogue (TMEM lane = key row): warpgroup 0 writes dV, warpgroup 1 dK
@@ -419,6 +377,58 @@ __global__ void __launch_bounds__(kThreads, 1)
           dst[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
                               pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
       }
+    }
+  } else if (warp < kSoftmaxWarps + 4) {
+    // ------------------------------------------------ dQ drain warpgroup (warps 8-11)
+    // TMEM lane = query row. The whole dQ tile is loaded to registers first so the MMA
+    // warp can reuse the columns for dP(n+1); it is then staged box by box (32 fp32
+    // columns) through two 16 KB shared-memory slots and reduced into dq_acc by TMA.
+    regs_inc<kRegsDrain>();
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const bool issuer = quad == 0 && lane == 0;
+    long long tl[2] = {0, 0};
+    for (int n = 0; n < N; ++n) {
+      const int h = g * G + n / n_qt;
+      const int q0 = (qt_begin + n % n_qt) * 128;
+      long long c0 = tick<TL>();
+      mbar_wait(dq_full, n & 1);
+      long long c1 = tick<TL>();
+      tc_fence_after();
+      uint32_t rq[C::DQ_BOXES][32];
+#pragma unroll
+      for (int b = 0; b < C::DQ_BOXES; ++b) tmem_ld32(tmem + C::TM_DQ + lane_off + b * 32, rq[b]);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(dq_empty);
+#pragma unroll
+      for (int b = 0; b < C::DQ_BOXES; ++b) {
+        uint8_t* const slot = smem + C::OFF_STG + (b & 1) * 16384;
+        if (issuer) bulk_wait_read1();   // the reduce that last used this slot (two groups back) has read it
+        named_bar_sync(2, 128);
+        const uint32_t stbase = smem_u32(slot);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)       // 16-byte chunk j of the 128-byte row, swizzled by row % 8
+          st_shared_v4(stbase + r * 128 + ((j ^ (r & 7)) << 4),
+                       __float_as_uint(__uint_as_float(rq[b][4 * j + 0]) * a.scale),
+                       __float_as_uint(__uint_as_float(rq[b][4 * j + 1]) * a.scale),
+                       __float_as_uint(__uint_as_float(rq[b][4 * j + 2]) * a.scale),
+                       __float_as_uint(__uint_as_float(rq[b][4 * j + 3]) * a.scale));
+        fence_proxy_async_smem();
+        named_bar_sync(2, 128);
+        if (issuer) {
+          tma_reduce_add_2d(&tmdQ, slot, h * D + b * 32, q0);
+          bulk_commit();
+        }
+      }
+      tl[0] += c1 - c0;
+      tl[1] += tick<TL>() - c1;
+    }
+    if (issuer) bulk_wait0();
+    if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && warp == kSoftmaxWarps && lane == 0) {
+      a.dbg[3] = tl[0];
+      a.dbg[4] = tl[1];
     }
   }
   tc_fence_before();
@@ -479,15 +489,19 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   cudaError_t e;
   if (p.d == 128) {
     static const cudaError_t attr =
-        cudaFuncSetAttribute(attn_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<128>::SMEM);
+        cudaFuncSetAttribute(attn_bwd_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<128>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
-    attn_bwd_kernel<128><<<grid, kThreads, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
+    static const cudaError_t attr2 =
+        cudaFuncSetAttribute(attn_bwd_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<128>::SMEM);
+    if (attr2 != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr2)); return attr2; }
+    if (a.dbg) attn_bwd_kernel<128, true><<<grid, kThreads, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
+    else attn_bwd_kernel<128, false><<<grid, kThreads, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
     count_launches(1);
   } else {
     static const cudaError_t attr =
-        cudaFuncSetAttribute(attn_bwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<64>::SMEM);
+        cudaFuncSetAttribute(attn_bwd_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<64>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
-    attn_bwd_kernel<64><<<grid, kThreads, BwdCfg<64>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
+    attn_bwd_kernel<64, false><<<grid, kThreads, BwdCfg<64>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
     count_launches(1);
   }
   e = cudaGetLastError();
@@ -497,10 +511,9 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
     cudaMemcpyAsync(h, a.dbg, sizeof h, cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
     fprintf(stderr,
-            "[attn_bwd timeline CTA(0,0) N=%lld cycles] compute: bar %lld wait_sdp %lld E %lld wait_dq %lld drain %lld | "
-            "mma: wait_ds %lld issue_3mma %lld wait_q %lld wait_dqempty %lld wait_do %lld | "
-            "E: ld %lld math %lld pack+st %lld wait_st %lld\n",
-            h[10], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[11], h[12], h[13], h[14]);
+            "[attn_bwd timeline CTA(0,0) N=%lld cycles] softmax: bar %lld wait_sdp %lld E %lld (wait_dsempty %lld) | "
+            "drain: wait_dq %lld drain %lld | mma: wait_ds %lld issue_dV_dQ %lld wait_q %lld wait_dqempty %lld wait_do %lld\n",
+            h[10], h[0], h[1], h[2], h[11], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
   }
   return e;
 }
