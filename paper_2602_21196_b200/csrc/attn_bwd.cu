@@ -59,7 +59,7 @@ __device__ __forceinline__ float ex2b(float x) {
 }
 
 constexpr int kSoftmaxWarps = 8;                  // two warpgroups: P^T, dS^T (+ dK/dV epilogue)
-constexpr int kRegsSoftmax = 144, kRegsDrain = 168, kRegsOther = 48;   // setmaxnreg split of the 64K registers
+constexpr int kRegsSoftmax = 144, kRegsDrain = 152, kRegsOther = 72;   // setmaxnreg split of the 64K registers
 constexpr int kThreads = (kSoftmaxWarps + 8) * 32;  // + dQ drain warpgroup + {TMA, MMA, 2 idle}
 constexpr int kTmaWarp = kSoftmaxWarps + 4, kMmaWarp = kSoftmaxWarps + 5;
 static_assert(2 * 128 * kRegsSoftmax + 128 * kRegsDrain + 128 * kRegsOther <= 65536, "register split");
@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
     for (int i = 0; i < 13; ++i) mbar_init(&bars[i], i == 8 ? kSoftmax : i == 10 ? 128 : 1);
     fence_barrier_init();
+    tmem_slot[1] = smem_u32(smem);
   }
   if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
@@ -156,42 +157,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == kMmaWarp) {
-    if (lane == 0) {
-      // ------------------------------------------------ MMA issuer
+    {
+      // ------------------------------------------------ MMA issuer (whole warp; elect.sync inside the MMA asm)
       long long tl[5] = {0, 0, 0, 0, 0};
       constexpr uint32_t id_kk = idesc_bf16(128, 128, false, false);  // S^T, dP^T: both K-major over d
       constexpr uint32_t id_kmn = idesc_bf16(128, D, false, true);    // dV (A in TMEM), dK: B MN-major
       constexpr uint32_t id_mnmn = idesc_bf16(128, D, true, true);    // dQ: A = dS^T viewed MN-major, B = K MN-major
-      const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
-      const uint32_t sQ0 = smem_u32(smem + C::OFF_Q), sdO = smem_u32(smem + C::OFF_DO);
-      const uint32_t sdS = smem_u32(smem + C::OFF_DS);
-      // Descriptor of (base + off) = descriptor of base + off / 16 (start-address field, bits 0-13).
-      // Rolled loops with running offsets keep the issuer within its register budget.
+      // Shared-memory bases are re-read (volatile) every tile so the compiler cannot hoist ~40
+      // loop-invariant 64-bit descriptors into this warp's small register budget; each MMA's
+      // descriptor is base + immediate, computed right before the instruction.
+      uint32_t sK, sV, sQ0, sdO, sdS;
+      auto load_bases = [&]() {
+        const uint32_t base = ld_volatile_shared_u32(tmem_slot + 1);
+        sK = base + C::OFF_K; sV = base + C::OFF_V; sQ0 = base + C::OFF_Q; sdO = base + C::OFF_DO; sdS = base + C::OFF_DS;
+      };
+      load_bases();
       auto mma_kk = [&](uint32_t sa, uint32_t sb, uint32_t tm) {      // [128 x D] x [128 x D]^T
         const uint64_t da = desc_sw128(sa, 16, 1024), db = desc_sw128(sb, 16, 1024);
-#pragma unroll 1
+#pragma unroll
         for (int i = 0; i < 4 * NCH; ++i) {
           const uint32_t off = ((i >> 2) * 16384 + (i & 3) * 32) >> 4;
-          mma_ss(tm, da + off, db + off, id_kk, i != 0);
+          mma_ss_w(tm, da + off, db + off, id_kk, i != 0);
         }
       };
       auto mma_kmn = [&](uint32_t sa, uint32_t sb, uint32_t tm, bool acc) {  // A [128 x 128 q] K-major smem
         const uint64_t da = desc_sw128(sa, 16, 1024), db = desc_sw128(sb, 16384, 1024);
-#pragma unroll 1
+#pragma unroll
         for (int i = 0; i < 8; ++i)
-          mma_ss(tm, da + (((i >> 2) * 16384 + (i & 3) * 32) >> 4), db + i * (2048 >> 4), id_kmn, (acc || i) ? 1u : 0u);
+          mma_ss_w(tm, da + (((i >> 2) * 16384 + (i & 3) * 32) >> 4), db + i * (2048 >> 4), id_kmn, (acc || i) ? 1u : 0u);
       };
       // A = P^T in TMEM: queries [16 ks, 16 ks + 16) are packed at TMEM cols 64 (ks / 4) + 8 (ks % 4)
       auto mma_tmn = [&](uint32_t ta, uint32_t sb, uint32_t tm, bool acc) {
         const uint64_t db = desc_sw128(sb, 16384, 1024);
-#pragma unroll 1
+#pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          mma_ts(tm, ta + (ks >> 2) * 64 + (ks & 3) * 8, db + ks * (2048 >> 4), id_kmn, (acc || ks) ? 1u : 0u);
+          mma_ts_w(tm, ta + (ks >> 2) * 64 + (ks & 3) * 8, db + ks * (2048 >> 4), id_kmn, (acc || ks) ? 1u : 0u);
       };
       auto mma_mnmn = [&](uint32_t sa, uint32_t sb, uint32_t tm) {  // dQ = dS K: K dim = keys (rows of both)
         const uint64_t da = desc_sw128(sa, 16384, 1024), db = desc_sw128(sb, 16384, 1024);
-#pragma unroll 1
-        for (int i = 0; i < 8; ++i) mma_ss(tm, da + i * (2048 >> 4), db + i * (2048 >> 4), id_mnmn, i != 0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mma_ss_w(tm, da + i * (2048 >> 4), db + i * (2048 >> 4), id_mnmn, i != 0);
       };
       mbar_wait(kv_full, 0);
       mbar_wait(&q_full[0], 0);
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(do_full, 0);
       tc_fence_after();
       mma_kk(sV, sdO, tmem + C::TM_DP);
-      mma_commit(sdp_full);
+      mma_commit_w(sdp_full);
       for (int n = 0; n < N; ++n) {
         const int b = n & 1;
         long long t0 = tick<TL>();
@@ -208,10 +213,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         long long t1 = tick<TL>();
         tl[0] += t1 - t0;
         tc_fence_after();
+        load_bases();
         mma_tmn(tmem + C::TM_S, sdO, tmem + C::TM_DV, n > 0);
-        mma_commit(do_empty);                           // dO(n) consumed: the producer loads dO(n+1)
+        mma_commit_w(do_empty);                           // dO(n) consumed: the producer loads dO(n+1)
         mma_mnmn(sdS, sK, tmem + C::TM_DQ);
-        mma_commit(dq_full);                            // drained while S(n+1), dP(n+1) run
+        mma_commit_w(dq_full);                            // drained while S(n+1), dP(n+1) run
         tl[1] += tick<TL>() - t1;
         if (n + 1 < N) {
           const int b1 = (n + 1) & 1;
@@ -228,15 +234,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           tl[4] += tick<TL>() - t4;
           tc_fence_after();
           mma_kk(sV, sdO, tmem + C::TM_DP);
-          mma_commit(sdp_full);
+          mma_commit_w(sdp_full);
         }
         // dK(n) last: it runs on the tensor core while the compute warps start on tile n+1
         mma_kmn(sdS, sQ0 + b * C::TB, tmem + C::TM_DK, n > 0);
-        mma_commit(&q_empty[b]);
-        mma_commit(ds_empty);                           // dS^T(n) consumed: tile n+1 may overwrite it
+        mma_commit_w(&q_empty[b]);
+        mma_commit_w(ds_empty);                           // dS^T(n) consumed: tile n+1 may overwrite it
       }
-      mma_commit(dkv_full);
-      if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0)
+      mma_commit_w(dkv_full);
+      if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0)
         for (int i = 0; i < 5; ++i) a.dbg[5 + i] = tl[i];
     }
   } else if (warp < kSoftmaxWarps) {

@@ -8,7 +8,7 @@ clock64 accumulators to stderr) and times the launch with CUDA events.
 import os
 import sys
 
-os.environ["UPIPE_BWD_TIMELINE"] = "1"
+os.environ.setdefault("UPIPE_BWD_TIMELINE", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
