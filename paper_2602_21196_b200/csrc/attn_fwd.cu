@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&s_full[t], 1); mbar_init(&p_full[t], 128); mbar_init(&o_full[t], 1);
     }
     fence_barrier_init();
+    tmem_slot[1] = smem_u32(smem);
   }
   if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
@@ -127,45 +128,48 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {
-      // ------------------------------------------------ MMA issuer
+    {
+      // ------------------------------------------------ MMA issuer (whole warp; elect.sync inside the MMA asm)
       constexpr uint32_t idS = idesc_bf16(128, 128, false, false);  // Q (K-major) x K (K-major)
       constexpr uint32_t idO = idesc_bf16(128, D, false, true);     // P (TMEM) x V (MN-major)
-      const uint32_t sQA = smem_u32(smem + C::OFF_QA), sQB = smem_u32(smem + C::OFF_QB);
+      // smem base re-read (volatile) per KV tile: descriptors are formed next to each MMA
+      // instead of being hoisted into registers (see mma_ss_w in sm100.cuh)
+      uint32_t base = ld_volatile_shared_u32(tmem_slot + 1);
       auto issue_S = [&](uint32_t sq, uint32_t sk, uint32_t tm) {
+        const uint64_t dq = desc_sw128(sq, 16, 1024), dk = desc_sw128(sk, 16, 1024);
 #pragma unroll
-        for (int c = 0; c < NCH; ++c)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_ss(tm, desc_sw128(sq + c * 16384 + kk * 32, 16, 1024), desc_sw128(sk + c * 16384 + kk * 32, 16, 1024),
-                   idS, (c | kk) != 0);
+        for (int i = 0; i < 4 * NCH; ++i) {
+          const uint32_t off = ((i >> 2) * 16384 + (i & 3) * 32) >> 4;
+          mma_ss_w(tm, dq + off, dk + off, idS, i != 0);
+        }
       };
       // O += P V with A = P in TMEM: keys [16 ks, 16 ks + 16) packed (bf16 pairs) at S columns 8 ks
       auto issue_PV = [&](uint32_t tp, uint32_t sv, uint32_t tm, bool acc) {
+        const uint64_t dv = desc_sw128(sv, 16384, 1024);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          mma_ts(tm, tp + ks * 8, desc_sw128(sv + (ks >> 2) * 8192 + (ks & 3) * 2048, 16384, 1024), idO,
-                 (acc || ks) ? 1u : 0u);
+          mma_ts_w(tm, tp + ks * 8, dv + (((ks >> 2) * 8192 + (ks & 3) * 2048) >> 4), idO, (acc || ks) ? 1u : 0u);
       };
       mbar_wait(q_full, 0);
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
-      issue_S(sQA, smem_u32(smem + C::OFF_K), tmem + C::TM_SA);
-      mma_commit(&s_full[0]);
-      issue_S(sQB, smem_u32(smem + C::OFF_K), tmem + C::TM_SB);
-      mma_commit(&s_full[1]);
-      mma_commit(&k_empty[0]);                    // K(0) consumed once both S MMAs complete
+      issue_S(base + C::OFF_QA, base + C::OFF_K, tmem + C::TM_SA);
+      mma_commit_w(&s_full[0]);
+      issue_S(base + C::OFF_QB, base + C::OFF_K, tmem + C::TM_SB);
+      mma_commit_w(&s_full[1]);
+      mma_commit_w(&k_empty[0]);                  // K(0) consumed once both S MMAs complete
       for (int it = 0; it < nB; ++it) {
         const int st = it % C::KV_STAGES;
         const uint32_t ph = (it / C::KV_STAGES) & 1;
-        const uint32_t sv = smem_u32(smem + C::OFF_V + st * C::QBYTES);
+        base = ld_volatile_shared_u32(tmem_slot + 1);
+        const uint32_t sv = base + C::OFF_V + st * C::QBYTES;
         mbar_wait(&v_full[st], ph);
         // ---- tile A
         if (it < nA) {
           mbar_wait(&p_full[0], it & 1);
           tc_fence_after();
           issue_PV(tmem + C::TM_SA, sv, tmem + C::TM_OA, it > 0);
-          mma_commit(&o_full[0]);
+          mma_commit_w(&o_full[0]);
         }
         const bool more = it + 1 < nB;
         const int st1 = (it + 1) % C::KV_STAGES;
@@ -173,19 +177,19 @@ __global__ void __launch_bounds__(384, 1)
         if (more) mbar_wait(&k_full[st1], ph1);
         tc_fence_after();
         if (it + 1 < nA) {
-          issue_S(sQA, smem_u32(smem + C::OFF_K + st1 * C::QBYTES), tmem + C::TM_SA);
-          mma_commit(&s_full[0]);
+          issue_S(base + C::OFF_QA, base + C::OFF_K + st1 * C::QBYTES, tmem + C::TM_SA);
+          mma_commit_w(&s_full[0]);
         }
         // ---- tile B
         mbar_wait(&p_full[1], it & 1);
         tc_fence_after();
         issue_PV(tmem + C::TM_SB, sv, tmem + C::TM_OB, it > 0);
-        mma_commit(&o_full[1]);
-        mma_commit(&v_empty[st]);
+        mma_commit_w(&o_full[1]);
+        mma_commit_w(&v_empty[st]);
         if (more) {
-          issue_S(sQB, smem_u32(smem + C::OFF_K + st1 * C::QBYTES), tmem + C::TM_SB);
-          mma_commit(&s_full[1]);
-          mma_commit(&k_empty[st1]);
+          issue_S(base + C::OFF_QB, base + C::OFF_K + st1 * C::QBYTES, tmem + C::TM_SB);
+          mma_commit_w(&s_full[1]);
+          mma_commit_w(&k_empty[st1]);
         }
       }
     }
