@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer (single thread)
+    {
+      // ---------------- MMA issuer (whole warp; elect.sync inside the MMA asm, see mma_ss_w)
       constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
@@ -153,12 +153,12 @@ __global__ void __launch_bounds__(192, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t da = A_MN ? desc_sw128(sa + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sa + kk * 32, 16, 1024);
             const uint64_t db = B_MN ? desc_sw128(sb + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sb + kk * 32, 16, 1024);
-            mma_ss(acc, da, db, idesc, (kb | kk) != 0);
+            mma_ss_w(acc, da, db, idesc, (kb | kk) != 0);
           }
-          mma_commit(&empty[stage]);
+          mma_commit_w(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&acc_full[ab]);
+        mma_commit_w(&acc_full[ab]);
       }
     }
   } else {
