@@ -4,6 +4,8 @@
 
 #include <cstdio>
 #include <atomic>
+#include <map>
+#include <string>
 #include <new>
 
 #include "kernels.h"
@@ -304,6 +306,9 @@ upipe_status_t upipe_trace_read(upipe_ctx_t ctx, double ms[UPIPE_TRACE_NCAT], in
   }
   cudaSetDevice(ctx->device);
   Tracer& T = ctx->tracer;
+  // UPIPE_TRACE_LABELS=1: also print per-step-label totals (debugging aid) to stderr
+  const char* lenv = getenv("UPIPE_TRACE_LABELS");
+  std::map<std::string, std::pair<double, int>> by_label;
   for (auto& r : T.recs) {
     cudaError_t e = cudaEventSynchronize(r.b);
     float t = 0.f;
@@ -311,10 +316,17 @@ upipe_status_t upipe_trace_read(upipe_ctx_t ctx, double ms[UPIPE_TRACE_NCAT], in
     if (e != cudaSuccess) return set_err(ctx, UPIPE_ERR_CUDA, std::string("trace: ") + cudaGetErrorString(e));
     ms[r.cat] += t;
     count[r.cat] += 1;
+    if (lenv && lenv[0] == '1') {
+      auto& v = by_label[r.label ? r.label : ""];
+      v.first += t;
+      v.second += 1;
+    }
     T.pool.push_back(r.a);
     T.pool.push_back(r.b);
   }
   T.recs.clear();
+  for (auto& kv : by_label)
+    fprintf(stderr, "[upipe trace] %-24s %4d x  %9.3f ms\n", kv.first.c_str(), kv.second.second, kv.second.first);
   return UPIPE_OK;
 }
 

@@ -32,11 +32,15 @@ struct DevOut {
   long long c_base, n_len, c_nstride, c_mstride;
   int epi;
 };
+constexpr int kMaxParts = 3;
 struct GemmArgs {
   int M, N, K;
   float alpha;
-  DevOpMap a, b;
-  DevOut c;
+  int nparts, kind;          // kind: 0 single / K-concatenation, 1 M-concatenation (see GemmGroup)
+  int kcum[kMaxParts + 1];   // K-concat: first K index of each part (multiples of BK)
+  int mcum[kMaxParts + 1];   // M-concat: first row of each part (multiples of BM)
+  DevOpMap a[kMaxParts], b[kMaxParts];
+  DevOut c[kMaxParts];
 };
 
 __device__ __forceinline__ int map_outer(const DevOpMap& m, int i, int k) {
@@ -62,7 +66,12 @@ struct Cfg {
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(192, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs g) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
+                const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB0,
+                const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2, const GemmArgs g) {
+  // Grouped forms (GemmGroup): K-concatenation sums the products of up to three (A, B) pairs
+  // into one accumulator (one epilogue pass); M-concatenation stacks up to three A operands
+  // (own output maps) against one B. The part of a k-block / tile selects the tensor maps.
   // Persistent: CTA b processes tiles b, b + gridDim.x, ... (N fastest, so CTAs running at the
   // same time share the A row block through L2). Two TMEM accumulators: the epilogue of tile i
   // overlaps the main loop of tile i+1.
@@ -82,9 +91,19 @@ __global__ void __launch_bounds__(192, 1)
   const int ntiles = ntn * ((g.M + BM - 1) / BM);
   const int nk = (g.K + BK - 1) / BK;
 
+  auto mapA = [&](int p) { return p == 0 ? &tmA0 : (p == 1 ? &tmA1 : &tmA2); };
+  auto mapB = [&](int p) { return p == 0 ? &tmB0 : (p == 1 ? &tmB1 : &tmB2); };
+  auto mpart = [&](int m0) {            // M-concat part of a tile
+    int p = 0;
+    if (g.kind == 1)
+      while (p + 1 < g.nparts && m0 >= g.mcum[p + 1]) ++p;
+    return p;
+  };
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
+    for (int p = 0; p < g.nparts; ++p) {
+      tma_prefetch(mapA(p));
+      tma_prefetch(mapB(p));
+    }
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -108,25 +127,35 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int m0 = (t / ntn) * BM, n0 = (t % ntn) * BN;
+        const int pm = mpart(m0);
+        const int ml0 = m0 - (g.kind == 1 ? g.mcum[pm] : 0);
+        int pk = 0;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = ring + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
-          const int k0 = kb * BK;
+          if (g.kind == 0)
+            while (pk + 1 < g.nparts && kb * BK >= g.kcum[pk + 1]) ++pk;
+          const int k0 = kb * BK - (g.kind == 0 ? g.kcum[pk] : 0);
+          const int pa = g.kind == 1 ? pm : pk, pb = g.kind == 1 ? 0 : pk;
+          const CUtensorMap* tA = mapA(pa);
+          const CUtensorMap* tB = mapB(pb);
+          const DevOpMap& am = g.a[pa];
+          const DevOpMap& bm = g.b[pb];
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
 #pragma unroll
           for (int c = 0; c < BM / 64; ++c) {
-            const int i = m0 + c * 64;
-            const int oc = map_outer(g.a, i, k0), kc = map_k(g.a, i, k0);
-            if (A_MN) tma_load_2d(sa + c * GRANULE_BYTES, &tmA, &full[stage], oc, kc);
-            else      tma_load_2d(sa + c * GRANULE_BYTES, &tmA, &full[stage], kc, oc);
+            const int i = ml0 + c * 64;
+            const int oc = map_outer(am, i, k0), kc = map_k(am, i, k0);
+            if (A_MN) tma_load_2d(sa + c * GRANULE_BYTES, tA, &full[stage], oc, kc);
+            else      tma_load_2d(sa + c * GRANULE_BYTES, tA, &full[stage], kc, oc);
           }
 #pragma unroll
           for (int c = 0; c < BN / 64; ++c) {
             const int i = n0 + c * 64;
-            const int oc = map_outer(g.b, i, k0), kc = map_k(g.b, i, k0);
-            if (B_MN) tma_load_2d(sb + c * GRANULE_BYTES, &tmB, &full[stage], oc, kc);
-            else      tma_load_2d(sb + c * GRANULE_BYTES, &tmB, &full[stage], kc, oc);
+            const int oc = map_outer(bm, i, k0), kc = map_k(bm, i, k0);
+            if (B_MN) tma_load_2d(sb + c * GRANULE_BYTES, tB, &full[stage], oc, kc);
+            else      tma_load_2d(sb + c * GRANULE_BYTES, tB, &full[stage], kc, oc);
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -169,11 +198,14 @@ __global__ void __launch_bounds__(192, 1)
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
       const int ab = i & 1;
       const int m0 = (t / ntn) * BM, n0 = (t % ntn) * BN;
+      const int pc = mpart(m0);
+      const DevOut& oc_ = g.c[pc];
       const int m = m0 + row;
+      const int ml = m - (g.kind == 1 ? g.mcum[pc] : 0);
       mbar_wait(&acc_full[ab], (i >> 1) & 1);
       tc_fence_after();
       const bool mvalid = m < g.M;
-      const long long mseg = mvalid ? m / g.c.m_len : 0, min_ = mvalid ? m % g.c.m_len : 0;
+      const long long mseg = mvalid ? ml / oc_.m_len : 0, min_ = mvalid ? ml % oc_.m_len : 0;
 #pragma unroll 1
       for (int c32 = 0; c32 < BN / 32; ++c32) {
         uint32_t r[32];
@@ -181,29 +213,29 @@ __global__ void __launch_bounds__(192, 1)
         tmem_wait_ld();
         const int n = n0 + c32 * 32;
         if (!mvalid || n >= g.N) continue;
-        const long long nseg = n / g.c.n_len, nin = n % g.c.n_len;
-        const long long orow = g.c.r_base + mseg * g.c.r_mstride + min_ + nseg * g.c.r_nstride;
-        const long long ocol = g.c.c_base + nseg * g.c.c_nstride + nin + mseg * g.c.c_mstride;
+        const long long nseg = n / oc_.n_len, nin = n % oc_.n_len;
+        const long long orow = oc_.r_base + mseg * oc_.r_mstride + min_ + nseg * oc_.r_nstride;
+        const long long ocol = oc_.c_base + nseg * oc_.c_nstride + nin + mseg * oc_.c_mstride;
         float v[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]) * g.alpha;
-        if (g.c.epi == (int)Epi::kStoreBF16) {
-          uint4* dst = reinterpret_cast<uint4*>(g.c.bf16 + orow * g.c.ld_bf16 + ocol);
+        if (oc_.epi == (int)Epi::kStoreBF16) {
+          uint4* dst = reinterpret_cast<uint4*>(oc_.bf16 + orow * oc_.ld_bf16 + ocol);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             dst[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
                                 pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
         } else {
-          float4* dst = reinterpret_cast<float4*>(g.c.f32 + orow * g.c.ld_f32 + ocol);
-          if (g.c.epi != (int)Epi::kStoreF32) {
+          float4* dst = reinterpret_cast<float4*>(oc_.f32 + orow * oc_.ld_f32 + ocol);
+          if (oc_.epi != (int)Epi::kStoreF32) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               const float4 o = dst[q];
               v[4 * q + 0] += o.x; v[4 * q + 1] += o.y; v[4 * q + 2] += o.z; v[4 * q + 3] += o.w;
             }
           }
-          if (g.c.epi == (int)Epi::kAccF32ToBF16) {
-            uint4* d2 = reinterpret_cast<uint4*>(g.c.bf16 + orow * g.c.ld_bf16 + ocol);
+          if (oc_.epi == (int)Epi::kAccF32ToBF16) {
+            uint4* d2 = reinterpret_cast<uint4*>(oc_.bf16 + orow * oc_.ld_bf16 + ocol);
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               d2[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
@@ -232,7 +264,7 @@ DevOpMap to_dev(const OperandMap& m) {
 }
 
 template <int BN, bool A_MN, bool B_MN>
-cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t s) {
+cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs& args, cudaStream_t s) {
   using C = Cfg<BN>;
   auto kern = gemm_kernel<BN, A_MN, B_MN>;
   static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -245,13 +277,13 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs&
   }();
   const int ntiles = ((args.N + BN - 1) / BN) * ((args.M + BM - 1) / BM);
   dim3 grid(ntiles < num_sms ? ntiles : num_sms);
-  kern<<<grid, 192, C::SMEM, s>>>(ta, tb, args);
+  kern<<<grid, 192, C::SMEM, s>>>(ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], args);
   count_launches(1);
   return cudaGetLastError();
 }
 
 template <int BN>
-cudaError_t dispatch_major(bool amn, bool bmn, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+cudaError_t dispatch_major(bool amn, bool bmn, const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs& a,
                            cudaStream_t s) {
   if (!amn && !bmn) return launch<BN, false, false>(ta, tb, a, s);
   if (!amn && bmn) return launch<BN, false, true>(ta, tb, a, s);
@@ -261,46 +293,102 @@ cudaError_t dispatch_major(bool amn, bool bmn, const CUtensorMap& ta, const CUte
 
 bool seg_ok(int64_t len) { return len % 64 == 0 && len > 0; }
 
+DevOut to_dev(const OutMap& c) {
+  return DevOut{reinterpret_cast<float*>(c.out_f32), reinterpret_cast<__nv_bfloat16*>(c.out_bf16), c.ld_f32, c.ld_bf16,
+                c.r_base, c.m_len, c.r_mstride, c.r_nstride, c.c_base, c.n_len, c.c_nstride, c.c_mstride, (int)c.epi};
+}
+
 }  // namespace
 
-cudaError_t gemm_run(const GemmProblem& p, cudaStream_t stream, char* err, size_t errlen) {
-  if (p.M <= 0 || p.N <= 0 || p.K <= 0) return cudaSuccess;
-  if (p.N % 64) {
-    snprintf(err, errlen, "gemm: N=%lld not a multiple of 64", (long long)p.N);
+cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cudaStream_t stream, char* err,
+                           size_t errlen) {
+  if (n < 1 || n > kMaxParts) {
+    snprintf(err, errlen, "gemm: %d parts (1..%d)", n, kMaxParts);
     return cudaErrorInvalidValue;
   }
-  for (const OperandMap* m : {&p.a, &p.b}) {
-    if (!seg_ok(m->o_len) || !seg_ok(m->k_len)) {
-      snprintf(err, errlen, "gemm: operand segment lengths must be multiples of 64");
+  const GemmProblem& p0 = parts[0];
+  int64_t M = p0.M, K = p0.K;
+  for (int i = 1; i < n; ++i) {
+    const GemmProblem& pi = parts[i];
+    if (pi.N != p0.N || pi.a.mn_major != p0.a.mn_major || pi.b.mn_major != p0.b.mn_major) {
+      snprintf(err, errlen, "gemm group: parts differ in N or operand majorness");
       return cudaErrorInvalidValue;
     }
+    if (kind == GemmGroup::kKConcat) {
+      if (pi.M != p0.M || p0.K % BK || parts[i - 1].K % BK) {
+        snprintf(err, errlen, "gemm K-concat: parts need equal M and K multiples of %d", BK);
+        return cudaErrorInvalidValue;
+      }
+      K += pi.K;
+    } else {
+      if (pi.K != p0.K || parts[i - 1].M % BM) {
+        snprintf(err, errlen, "gemm M-concat: parts need equal K and M multiples of %d", BM);
+        return cudaErrorInvalidValue;
+      }
+      M += pi.M;
+    }
   }
-  if (!seg_ok(p.c.n_len) || p.c.m_len <= 0) {
-    snprintf(err, errlen, "gemm: output segment lengths invalid");
+  if (M <= 0 || p0.N <= 0 || K <= 0) return cudaSuccess;
+  if (p0.N % 64) {
+    snprintf(err, errlen, "gemm: N=%lld not a multiple of 64", (long long)p0.N);
     return cudaErrorInvalidValue;
   }
   // Tile width: the widest of 256/128/64 that stays inside one B-outer and one output segment.
   int bn = 256;
-  while (bn > 64 && ((p.b.o_len % bn) || (p.c.n_len % bn) || (p.N % bn))) bn >>= 1;
-  CUtensorMap ta, tb;
-  if (!make_tmap_2d(&ta, p.a.ptr, p.a.inner, p.a.outer, p.a.ld, 64, 64, err, errlen)) return cudaErrorInvalidValue;
-  if (!make_tmap_2d(&tb, p.b.ptr, p.b.inner, p.b.outer, p.b.ld, 64, 64, err, errlen)) return cudaErrorInvalidValue;
+  auto bn_ok = [&](int w) {
+    if (p0.N % w) return false;
+    for (int i = 0; i < n; ++i)
+      if ((parts[i].b.o_len % w) || (parts[i].c.n_len % w)) return false;
+    return true;
+  };
+  while (bn > 64 && !bn_ok(bn)) bn >>= 1;
   GemmArgs args;
-  args.M = (int)p.M;
-  args.N = (int)p.N;
-  args.K = (int)p.K;
-  args.alpha = p.alpha;
-  args.a = to_dev(p.a);
-  args.b = to_dev(p.b);
-  args.c = DevOut{reinterpret_cast<float*>(p.c.out_f32), reinterpret_cast<__nv_bfloat16*>(p.c.out_bf16),
-                  p.c.ld_f32, p.c.ld_bf16, p.c.r_base, p.c.m_len, p.c.r_mstride, p.c.r_nstride,
-                  p.c.c_base, p.c.n_len, p.c.c_nstride, p.c.c_mstride, (int)p.c.epi};
+  args.M = (int)M;
+  args.N = (int)p0.N;
+  args.K = (int)K;
+  args.alpha = p0.alpha;
+  args.nparts = n;
+  args.kind = kind == GemmGroup::kMConcat ? 1 : 0;
+  CUtensorMap ta[kMaxParts], tb[kMaxParts];
+  int64_t kc = 0, mc = 0;
+  for (int i = 0; i < kMaxParts; ++i) {
+    const GemmProblem& pi = parts[i < n ? i : 0];
+    if (i < n) {
+      for (const OperandMap* m : {&pi.a, &pi.b}) {
+        if (!seg_ok(m->o_len) || !seg_ok(m->k_len)) {
+          snprintf(err, errlen, "gemm: operand segment lengths must be multiples of 64");
+          return cudaErrorInvalidValue;
+        }
+      }
+      if (!seg_ok(pi.c.n_len) || pi.c.m_len <= 0) {
+        snprintf(err, errlen, "gemm: output segment lengths invalid");
+        return cudaErrorInvalidValue;
+      }
+    }
+    if (!make_tmap_2d(&ta[i], pi.a.ptr, pi.a.inner, pi.a.outer, pi.a.ld, 64, 64, err, errlen)) return cudaErrorInvalidValue;
+    if (!make_tmap_2d(&tb[i], pi.b.ptr, pi.b.inner, pi.b.outer, pi.b.ld, 64, 64, err, errlen)) return cudaErrorInvalidValue;
+    args.a[i] = to_dev(pi.a);
+    args.b[i] = to_dev(pi.b);
+    args.c[i] = to_dev(pi.c);
+    args.kcum[i] = (int)kc;
+    args.mcum[i] = (int)mc;
+    if (i < n) {
+      kc += pi.K;
+      mc += pi.M;
+    }
+  }
+  args.kcum[kMaxParts] = (int)kc;
+  args.mcum[kMaxParts] = (int)mc;
   cudaError_t e;
-  if (bn == 256) e = dispatch_major<256>(p.a.mn_major, p.b.mn_major, ta, tb, args, stream);
-  else if (bn == 128) e = dispatch_major<128>(p.a.mn_major, p.b.mn_major, ta, tb, args, stream);
-  else e = dispatch_major<64>(p.a.mn_major, p.b.mn_major, ta, tb, args, stream);
+  if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, ta, tb, args, stream);
+  else if (bn == 128) e = dispatch_major<128>(p0.a.mn_major, p0.b.mn_major, ta, tb, args, stream);
+  else e = dispatch_major<64>(p0.a.mn_major, p0.b.mn_major, ta, tb, args, stream);
   if (e != cudaSuccess) snprintf(err, errlen, "gemm launch: %s", cudaGetErrorString(e));
   return e;
+}
+
+cudaError_t gemm_run(const GemmProblem& p, cudaStream_t stream, char* err, size_t errlen) {
+  return gemm_run_group(&p, 1, GemmGroup::kKConcat, stream, err, errlen);
 }
 
 }  // namespace upipe

@@ -57,6 +57,15 @@ struct GemmProblem {
 
 cudaError_t gemm_run(const GemmProblem& p, cudaStream_t stream, char* err, size_t errlen);
 
+// Grouped launches (one kernel, up to 3 parts):
+//  kKConcat: C = sum_i A_i B_i^T  (equal M and N; each K_i a multiple of 64; output map of part 0)
+//            e.g. dX = dQ Wq + dK Wk + dV Wv with one fp32 read-modify-write of dX;
+//  kMConcat: rows of part i = A_i B^T (equal N and K; each M_i but the last a multiple of 128;
+//            B operand of part 0; own output map per part), e.g. [dWq; dWk; dWv] = [dQ; dK; dV]^T X.
+enum class GemmGroup : int { kKConcat = 0, kMConcat = 1 };
+cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cudaStream_t stream, char* err,
+                           size_t errlen);
+
 // ---------------------------------------------------------------- attention
 // Causal GQA flash attention over the full sequence for the heads local to this
 // device in one stage (head layout after the inp all-to-all).

@@ -29,8 +29,9 @@ struct Step {
   upipe_ctx_s* ctx;
   cudaStream_t st;
   int cat;
+  const char* label;
   cudaEvent_t a = nullptr;
-  Step(upipe_ctx_s* c, cudaStream_t s, int k) : ctx(c), st(s), cat(k) {
+  Step(upipe_ctx_s* c, cudaStream_t s, int k, const char* l = "") : ctx(c), st(s), cat(k), label(l) {
     if (ctx->tracer.on) {
       a = ctx->tracer.get();
       cudaEventRecord(a, st);
@@ -40,7 +41,7 @@ struct Step {
     if (a) {
       cudaEvent_t b = ctx->tracer.get();
       cudaEventRecord(b, st);
-      ctx->tracer.recs.push_back({cat, a, b});
+      ctx->tracer.recs.push_back({cat, a, b, label});
     }
   }
 };
@@ -54,7 +55,7 @@ struct Runner {
   template <class F>
   bool run(int cat, cudaStream_t s, const char* what, F&& f) {
     if (status != UPIPE_OK) return false;
-    Step step(ctx, s, cat);
+    Step step(ctx, s, cat, what);
     errbuf[0] = 0;
     cudaError_t e = f(errbuf);
     if (e != cudaSuccess) {
@@ -67,7 +68,7 @@ struct Runner {
   template <class F>
   bool comm(cudaStream_t s, const char* what, F&& f) {
     if (status != UPIPE_OK) return false;
-    Step step(ctx, s, UPIPE_TRACE_COMM);
+    Step step(ctx, s, UPIPE_TRACE_COMM, what);
     std::string m;
     upipe_status_t st = f(m);
     if (st != UPIPE_OK) {
@@ -191,32 +192,26 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     (void)s;
     R.comm(q, "a2a O", [&](std::string& m) { return T.alltoall(ws + W.osend[b], ws + W.orecv[b], qbytes, q, m); });
   };
-  // F5: fill o_saved; F6/F7: y (+)= O_s Wo[:, cols(s)]^T, fp32 accumulator, bf16 on the last stage
+  // F5: fill o_saved from the stage's out all-to-all (C == 1: attention wrote it directly)
   auto post = [&](int s, int b, cudaStream_t q) {
     const int64_t q0 = P.q0(s, 0);
     if (C > 1)
       R.run(UPIPE_TRACE_AUX, q, "unpack O", [&](char*) {
         return unpack_cols_run(ws + W.orecv[b], P.S_l, C, (int)qseg, o_saved, HqD, q0 * d, qstep, q);
       });
+  };
+  // F6/F7: y = O Wo^T once every head's O is in the pre-allocated output: one GEMM
+  // with K = Hq*d and a bf16 epilogue, no fp32 accumulator across stages (DESIGN A24)
+  auto out_proj = [&](cudaStream_t q) {
     GemmProblem g;
     g.M = P.S_l;
     g.N = P.D;
-    g.K = (int64_t)P.U * d;
+    g.K = HqD;
     g.a = OperandMap{o_saved, HqD, P.S_l, HqD, false};
     g.b = OperandMap{wo, HqD, P.D, HqD, false};
-    for (OperandMap* m : {&g.a, &g.b}) {
-      m->k_base = q0 * d;
-      m->k_len = qseg;
-      m->k_kstride = qstep;
-    }
-    g.c.out_f32 = ws + W.yacc;
-    g.c.ld_f32 = P.D;
     g.c.out_bf16 = y;
     g.c.ld_bf16 = P.D;
-    if (P.nstages == 1) g.c.epi = Epi::kStoreBF16;
-    else if (s == 0) g.c.epi = Epi::kStoreF32;
-    else if (s == P.nstages - 1) g.c.epi = Epi::kAccF32ToBF16;
-    else g.c.epi = Epi::kAccF32;
+    g.c.epi = Epi::kStoreBF16;
     R.run(UPIPE_TRACE_GEMM, q, "out proj", [&](char* e) { return gemm_run(g, q, e, 512); });
   };
 
@@ -229,6 +224,7 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       if (C > 1) outa(s, 0, st);
       post(s, 0, st);
     }
+    out_proj(st);
     return R.status;
   }
   // ---- overlapped schedule
@@ -270,6 +266,7 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   }
   cudaStreamWaitEvent(st, e_out[(nu - 1) & 1], 0);
   post(nu - 1, (nu - 1) & 1, st);
+  out_proj(st);
   return R.status;
 }
 
@@ -305,14 +302,15 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     g.c.epi = Epi::kStoreF32;
     R.run(UPIPE_TRACE_GEMM, st, "dWo", [&](char* e) { return gemm_run(g, st, e, 512); });
   }
-  const int n_dx_terms = P.nstages + 2 * (P.nstages / P.sigma);
+  const int n_dx_terms = P.nstages;   // one K-concatenated dX GEMM per stage
   int dx_term = 0;
   auto dx_epi = [&](GemmProblem& g) {
     g.c.out_f32 = ws + W.dxacc;
     g.c.ld_f32 = P.D;
     g.c.out_bf16 = dx;
     g.c.ld_bf16 = P.D;
-    g.c.epi = dx_term == 0 ? Epi::kStoreF32 : (dx_term == n_dx_terms - 1 ? Epi::kAccF32ToBF16 : Epi::kAccF32);
+    if (n_dx_terms == 1) g.c.epi = Epi::kStoreBF16;
+    else g.c.epi = dx_term == 0 ? Epi::kStoreF32 : (dx_term == n_dx_terms - 1 ? Epi::kAccF32ToBF16 : Epi::kAccF32);
     ++dx_term;
   };
   // dX += dG_s W_s (G = Q, K or V): A = received gradient [C][S_l][seg], B = W rows (MN-major)
@@ -329,7 +327,6 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     g.b.k_base = row0;
     g.b.k_len = seg;
     g.b.k_kstride = row_step;
-    dx_epi(g);
     return g;
   };
   // dW rows of the stage's heads: dW[row0 + p*row_step + j][:] = sum_t grecv[p][t][j] x[t][:]
@@ -444,25 +441,34 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       R.comm(q, "a2a dV", [&](std::string& m) { return T.alltoall(ws + W.dvsend, ws + W.dvrecv, kbytes, q, m); });
     }
   };
-  // B6: dX and dW for the stage's heads (and the retired K/V heads)
+  // B6: dX and dW for the stage's heads (and the retired K/V heads). dX += dQ Wq + dK Wk + dV Wv is
+  // one K-concatenated GEMM (one fp32 read-modify-write of the dX accumulator per stage) and
+  // [dWq; dWk; dWv] = [dQ; dK; dV]^T X one M-concatenated GEMM (DESIGN A24).
   auto post = [&](int s, int b, cudaStream_t q) {
     const int64_t q0 = P.q0(s, 0), kv0 = P.kv0(s, 0);
-    GemmProblem g1 = dx_gemm(ws + W.dqrecv[b], qseg, wq, HqD, q0 * d, qstep);
-    R.run(UPIPE_TRACE_GEMM, q, "dX(dQ)", [&](char* e) { return gemm_run(g1, q, e, 512); });
-    R.run(UPIPE_TRACE_GEMM, q, "dWq", [&](char* e) {
-      return gemm_run(dw_gemm(ws + W.dqrecv[b], qseg, dwq, q0 * d, qstep), q, e, 512);
-    });
+    GemmProblem gx[3], gw[3];
+    int n = 1;
+    gx[0] = dx_gemm(ws + W.dqrecv[b], qseg, wq, HqD, q0 * d, qstep);
+    gw[0] = dw_gemm(ws + W.dqrecv[b], qseg, dwq, q0 * d, qstep);
     if (P.kv_last(s)) {
-      GemmProblem gk = dx_gemm(ws + W.dkrecv, kseg, wk, HkvD, kv0 * d, kseg);
-      R.run(UPIPE_TRACE_GEMM, q, "dX(dK)", [&](char* e) { return gemm_run(gk, q, e, 512); });
-      GemmProblem gv = dx_gemm(ws + W.dvrecv, kseg, wv, HkvD, kv0 * d, kseg);
-      R.run(UPIPE_TRACE_GEMM, q, "dX(dV)", [&](char* e) { return gemm_run(gv, q, e, 512); });
-      R.run(UPIPE_TRACE_GEMM, q, "dWk", [&](char* e) {
-        return gemm_run(dw_gemm(ws + W.dkrecv, kseg, dwk, kv0 * d, kseg), q, e, 512);
+      gx[1] = dx_gemm(ws + W.dkrecv, kseg, wk, HkvD, kv0 * d, kseg);
+      gx[2] = dx_gemm(ws + W.dvrecv, kseg, wv, HkvD, kv0 * d, kseg);
+      gw[1] = dw_gemm(ws + W.dkrecv, kseg, dwk, kv0 * d, kseg);
+      gw[2] = dw_gemm(ws + W.dvrecv, kseg, dwv, kv0 * d, kseg);
+      n = 3;
+    }
+    dx_epi(gx[0]);
+    R.run(UPIPE_TRACE_GEMM, q, "dX(dQ,dK,dV)", [&](char* e) {
+      return gemm_run_group(gx, n, GemmGroup::kKConcat, q, e, 512);
+    });
+    // M-concatenation needs the dWq / dWk row blocks in whole 128-row tiles
+    if (gw[0].M % 128 == 0 && (n == 1 || gw[1].M % 128 == 0)) {
+      R.run(UPIPE_TRACE_GEMM, q, "dW(q,k,v)", [&](char* e) {
+        return gemm_run_group(gw, n, GemmGroup::kMConcat, q, e, 512);
       });
-      R.run(UPIPE_TRACE_GEMM, q, "dWv", [&](char* e) {
-        return gemm_run(dw_gemm(ws + W.dvrecv, kseg, dwv, kv0 * d, kseg), q, e, 512);
-      });
+    } else {
+      for (int i = 0; i < n; ++i)
+        R.run(UPIPE_TRACE_GEMM, q, "dW", [&](char* e) { return gemm_run(gw[i], q, e, 512); });
     }
   };
 

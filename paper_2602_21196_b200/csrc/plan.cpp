@@ -85,7 +85,6 @@ FwdWs fwd_workspace(const Plan& p, bool overlap) {
     w.osend[i] = !comm ? 0 : (fresh ? take(qe) : w.osend[0]);
     w.orecv[i] = !comm ? 0 : (fresh ? take(qe) : w.orecv[0]);
   }
-  w.yacc = p.nstages > 1 ? take((size_t)p.S_l * p.D * 4) : 0;
   w.total = off;
   return w;
 }
@@ -128,7 +127,7 @@ BwdWs bwd_workspace(const Plan& p, bool overlap) {
   w.dvsend = take(ke);
   w.dkrecv = comm ? take(ke) : w.dksend;
   w.dvrecv = comm ? take(ke) : w.dvsend;
-  w.dxacc = take((size_t)p.S_l * p.D * 4);
+  w.dxacc = p.nstages > 1 ? take((size_t)p.S_l * p.D * 4) : 0;   // one stage: dX is stored in bf16 directly
   w.total = off;
   return w;
 }

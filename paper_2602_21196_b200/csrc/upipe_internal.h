@@ -41,7 +41,7 @@ Plan make_plan(int C, const upipe_shape_t& sh);
 // [2] = the two buffer sets of the overlapped (pipelined) schedule; in the sequential
 // schedule (or C == 1) index 1 aliases index 0.
 struct FwdWs {
-  size_t qsend[2], qrecv[2], ksend, krecv[2], vsend, vrecv[2], osend[2], orecv[2], yacc, total;
+  size_t qsend[2], qrecv[2], ksend, krecv[2], vsend, vrecv[2], osend[2], orecv[2], total;
 };
 struct BwdWs {
   size_t qsend[2], qrecv[2], ksend, krecv[2], vsend, vrecv[2], dosend[2], dorecv[2], dsend[2], drecv[2], dqacc[2],
@@ -72,6 +72,7 @@ struct Tracer {
   struct Rec {
     int cat;
     cudaEvent_t a, b;
+    const char* label;   // static string naming the step ("out proj", "dX(dQ)", ...)
   };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
