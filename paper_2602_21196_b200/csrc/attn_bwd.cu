@@ -22,9 +22,8 @@
 // across the UPipe stages of one super-stage) at the end.
 // Warps: 0-7 compute (two warpgroups, each owning 64 of the 128 query columns of
 // S^T/dP^T; thread = one key row there, one query row for the dQ drain), warp 8
-// TMA producer, warp 9 MMA issuer. The XU pipe executes both MUFU.EX2 and the bf16
-// packs at 16 lane-ops/clk/SM (measured), so 3 of 4 exponentials run as a
-// polynomial on the FMA pipe (ex2_fma) to balance the pipes.
+// TMA producer, warp 9 MMA issuer. The elementwise math runs on fp32 pairs (FFMA2/FADD2/FMUL2);
+// the exponentials take MUFU.EX2 (UPIPE_BWD_MUFU_EVERY selects a polynomial share on the FMA pipe).
 #include <cstdio>
 #include <cstdlib>
 
@@ -58,6 +57,12 @@ __device__ __forceinline__ float ex2b(float x) {
   return y;
 }
 
+#ifndef UPIPE_BWD_MUFU_EVERY
+// element pairs j with j % N == 0 take MUFU.EX2, the rest the FMA polynomial (ex2_fma2). Measured at
+// S = 32K (profiles/bwd_timeline.py): N = 1 (all MUFU) 5.39-5.44 ms, 2: 5.43, 4: 5.58, 8: 5.65; moving the
+// bf16 packs to the ALU pipe (round-half-away PRMT packs) was slower in every combination.
+#define UPIPE_BWD_MUFU_EVERY 1
+#endif
 constexpr int kSoftmaxWarps = 8;                  // two warpgroups: P^T, dS^T (+ dK/dV epilogue)
 constexpr int kRegsSoftmax = 144, kRegsDrain = 152, kRegsOther = 72;   // setmaxnreg split of the 64K registers
 constexpr int kThreads = (kSoftmaxWarps + 8) * 32;  // + dQ drain warpgroup + {TMA, MMA, 2 idle}
@@ -260,10 +265,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int h = g * G + n / n_qt;
       const long long q = (long long)(qt_begin + n % n_qt) * 128 + r;
       if (q >= a.S) return 0.f;
-      return wg == 0 ? a.lse[(long long)h * a.ld_lse + q] * 1.4426950408889634f : a.delta[q * a.ld_delta + h];
+      return wg == 0 ? a.lse[(long long)h * a.ld_lse + q] * -1.4426950408889634f : a.delta[q * a.ld_delta + h];
     };
     if (N > 0) stat_next = load_stat(0);
-    long long tl[4] = {0, 0, 0, 0};
+    long long tl[4] = {0, 0, 0, 0}, te[4] = {0, 0, 0, 0};   // te: E split into ld / math / store / wait_st
     for (int n = 0; n < N; ++n) {
       const int qt = qt_begin + n % n_qt;
       const long long q0 = (long long)qt * 128;
@@ -271,10 +276,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (wg == 0) s_lse2[sb][r] = stat_next;
       else s_delta[sb][r] = stat_next;
       if (n + 1 < N) stat_next = load_stat(n + 1);
+      // One warp polls the mbarrier; the others block in bar.sync (no issue slots spent spinning:
+      // every waiting warp's try_wait/nanosleep loop competes with the softmax math for issue)
       long long c0 = tick<TL>();
-      named_bar_sync(1, kSoftmax);
+      if (warp == 0) mbar_wait(sdp_full, n & 1);
       long long c1 = tick<TL>();
-      mbar_wait(sdp_full, n & 1);
+      named_bar_sync(1, kSoftmax);
       long long c2 = tick<TL>();
       tl[0] += c1 - c0;
       tl[1] += c2 - c1;
@@ -285,38 +292,68 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < 2; ++c) {
         const int col0 = wg * 64 + c * 32;
         uint32_t rs[32], rp[32];
+        const long long e0 = tick<TL>();
         tmem_ld32(tmem + C::TM_S + lane_off + col0, rs);
         tmem_ld32(tmem + C::TM_DP + lane_off + col0, rp);
         const float4* l4 = reinterpret_cast<const float4*>(&s_lse2[sb][col0]);
         const float4* d4 = reinterpret_cast<const float4*>(&s_delta[sb][col0]);
-        tmem_wait_ld();
-        // P = 2^(s*c - lse2): 1 in 4 on MUFU, 3 in 4 on the FMA pipe (the XU pipe also packs bf16)
+        // lse / delta (shared-memory broadcasts) are fetched while the TMEM loads are in flight
+        float4 lx[8], dl[8];
 #pragma unroll
-        for (int i4 = 0; i4 < 8; ++i4) {
-          const float4 x = l4[i4];
-          rs[4 * i4 + 0] = __float_as_uint(ex2b(fmaf(__uint_as_float(rs[4 * i4 + 0]), sl2, -x.x)));
-          rs[4 * i4 + 1] = __float_as_uint(ex2_fma(fmaf(__uint_as_float(rs[4 * i4 + 1]), sl2, -x.y)));
-          rs[4 * i4 + 2] = __float_as_uint(ex2_fma(fmaf(__uint_as_float(rs[4 * i4 + 2]), sl2, -x.z)));
-          rs[4 * i4 + 3] = __float_as_uint(ex2_fma(fmaf(__uint_as_float(rs[4 * i4 + 3]), sl2, -x.w)));
+        for (int i4 = 0; i4 < 8; ++i4) lx[i4] = l4[i4];
+        tmem_wait_ld();
+        const long long e1 = tick<TL>();
+        te[0] += e1 - e0;
+#pragma unroll
+        for (int i4 = 0; i4 < 8; ++i4) dl[i4] = d4[i4];
+        // P = 2^(s*c - lse2) on element pairs (FFMA2/FADD2/FMUL2 halve the issue slots); pairs with
+        // j % UPIPE_BWD_MUFU_EVERY == 0 on MUFU, the rest as the polynomial on the FMA pipe.
+        // s_lse2 holds -lse*log2(e).
+        const uint64_t sl2x2 = f2_pack(sl2, sl2);
+        uint64_t pp[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float4 x = lx[j >> 1];
+          const uint64_t nl = (j & 1) ? f2_pack(x.z, x.w) : f2_pack(x.x, x.y);
+          const uint64_t t = f2_fma(f2_pack(__uint_as_float(rs[2 * j]), __uint_as_float(rs[2 * j + 1])), sl2x2, nl);
+          if ((j % UPIPE_BWD_MUFU_EVERY) == 0) {
+            float t0, t1;
+            f2_unpack(t, t0, t1);
+            pp[j] = f2_pack(ex2b(t0), ex2b(t1));
+          } else {
+            pp[j] = ex2_fma2(t);
+          }
         }
         if (need_mask) {                               // uniform branch: only diagonal / ragged tiles
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const long long q = q0 + col0 + i;
-            rs[i] = (q >= qmin && q < a.S) ? rs[i] : 0u;
+          for (int j = 0; j < 16; ++j) {
+            float p0, p1;
+            f2_unpack(pp[j], p0, p1);
+            const long long qa = q0 + col0 + 2 * j;
+            p0 = (qa >= qmin && qa < a.S) ? p0 : 0.f;
+            p1 = (qa + 1 >= qmin && qa + 1 < a.S) ? p1 : 0.f;
+            pp[j] = f2_pack(p0, p1);
           }
         }
+        // dS = P (dP - delta)
 #pragma unroll
-        for (int i4 = 0; i4 < 8; ++i4) {
-          const float4 y = d4[i4];
-          rp[4 * i4 + 0] = __float_as_uint(__uint_as_float(rs[4 * i4 + 0]) * (__uint_as_float(rp[4 * i4 + 0]) - y.x));
-          rp[4 * i4 + 1] = __float_as_uint(__uint_as_float(rs[4 * i4 + 1]) * (__uint_as_float(rp[4 * i4 + 1]) - y.y));
-          rp[4 * i4 + 2] = __float_as_uint(__uint_as_float(rs[4 * i4 + 2]) * (__uint_as_float(rp[4 * i4 + 2]) - y.z));
-          rp[4 * i4 + 3] = __float_as_uint(__uint_as_float(rs[4 * i4 + 3]) * (__uint_as_float(rp[4 * i4 + 3]) - y.w));
+        for (int j = 0; j < 16; ++j) {
+          const float4 y = dl[j >> 1];
+          const uint64_t dlt = (j & 1) ? f2_pack(y.z, y.w) : f2_pack(y.x, y.y);
+          const uint64_t ds = f2_mul(pp[j], f2_sub(f2_pack(__uint_as_float(rp[2 * j]), __uint_as_float(rp[2 * j + 1])), dlt));
+          float d0, d1, p0, p1;
+          f2_unpack(ds, d0, d1);
+          f2_unpack(pp[j], p0, p1);
+          rp[2 * j] = __float_as_uint(d0);
+          rp[2 * j + 1] = __float_as_uint(d1);
+          rs[2 * j] = __float_as_uint(p0);
+          rs[2 * j + 1] = __float_as_uint(p1);
         }
 #pragma unroll
         for (int i = 0; i < 16; ++i)
           rs[i] = pack_bf16(__uint_as_float(rs[2 * i]), __uint_as_float(rs[2 * i + 1]));
+        const long long e2 = tick<TL>();
+        te[1] += e2 - e1;
         // P^T (bf16 pairs) back into S^T columns already read: queries [col0, col0+32) -> cols 64 wg + 16 c
         tmem_st16(tmem + C::TM_S + lane_off + wg * 64 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(rs));
         if (c == 0 && n > 0) {                         // dK(n-1) has read dS^T(n-1)
@@ -327,23 +364,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int v8 = 0; v8 < 4; ++v8) {
           const int qc = c * 32 + v8 * 8;
-          st_shared_v4(dsbase + sw128_offset(r, qc),
-                       pack_bf16(__uint_as_float(rp[v8 * 8 + 0]), __uint_as_float(rp[v8 * 8 + 1])),
-                       pack_bf16(__uint_as_float(rp[v8 * 8 + 2]), __uint_as_float(rp[v8 * 8 + 3])),
-                       pack_bf16(__uint_as_float(rp[v8 * 8 + 4]), __uint_as_float(rp[v8 * 8 + 5])),
-                       pack_bf16(__uint_as_float(rp[v8 * 8 + 6]), __uint_as_float(rp[v8 * 8 + 7])));
+          auto pk = [](uint32_t lo, uint32_t hi) { return pack_bf16(__uint_as_float(lo), __uint_as_float(hi)); };
+          st_shared_v4(dsbase + sw128_offset(r, qc), pk(rp[v8 * 8 + 0], rp[v8 * 8 + 1]), pk(rp[v8 * 8 + 2], rp[v8 * 8 + 3]),
+                       pk(rp[v8 * 8 + 4], rp[v8 * 8 + 5]), pk(rp[v8 * 8 + 6], rp[v8 * 8 + 7]));
         }
+        te[2] += tick<TL>() - e2;
       }
+      const long long e3 = tick<TL>();
       tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(ds_full);
+      te[3] += tick<TL>() - e3;
       tl[2] += tick<TL>() - c2;
     }
     if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && warp == 0 && lane == 0) {
       for (int i = 0; i < 3; ++i) a.dbg[i] = tl[i];
       a.dbg[11] = tl[3];
       a.dbg[10] = N;
+      for (int i = 0; i < 4; ++i) a.dbg[12 + i] = te[i];
     }
     // ---- dK / dV epilogue (TMEM lane = key row): warpgroup 0 writes dV, warpgroup 1 dK
     mbar_wait(dkv_full, 0);
@@ -399,7 +438,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int h = g * G + n / n_qt;
       const int q0 = (qt_begin + n % n_qt) * 128;
       long long c0 = tick<TL>();
-      mbar_wait(dq_full, n & 1);
+      if (quad == 0) mbar_wait(dq_full, n & 1);   // one polling warp, the others wait in bar.sync
+      named_bar_sync(2, 128);
       long long c1 = tick<TL>();
       tc_fence_after();
       uint32_t rq[C::DQ_BOXES][32];
@@ -518,8 +558,9 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
     cudaStreamSynchronize(stream);
     fprintf(stderr,
             "[attn_bwd timeline CTA(0,0) N=%lld cycles] softmax: bar %lld wait_sdp %lld E %lld (wait_dsempty %lld) | "
-            "drain: wait_dq %lld drain %lld | mma: wait_ds %lld issue_dV_dQ %lld wait_q %lld wait_dqempty %lld wait_do %lld\n",
-            h[10], h[0], h[1], h[2], h[11], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
+            "drain: wait_dq %lld drain %lld | mma: wait_ds %lld issue_dV_dQ %lld wait_q %lld wait_dqempty %lld wait_do %lld | "
+            "E: ld %lld math %lld store %lld wait_st %lld\n",
+            h[10], h[0], h[1], h[2], h[11], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[12], h[13], h[14], h[15]);
   }
   return e;
 }

@@ -41,6 +41,16 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+#ifndef UPIPE_FWD_POLY_EVERY
+#define UPIPE_FWD_POLY_EVERY 4   // exp pairs j with j % N == N - 1 use the FMA-pipe polynomial (0: none)
+#endif
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 template <int D>
 struct FwdCfg {
   static constexpr int TILE = 128;
@@ -227,9 +237,13 @@ __global__ void __launch_bounds__(384, 1)
           if ((a.causal && key > q) || key >= a.S) s[i] = -INFINITY;
         }
       }
-      float mx = s[0];
+      // row max with 3-input FMNMX3, four independent chains
+      float mq[4] = {fmaxf(s[0], s[1]), fmaxf(s[2], s[3]), fmaxf(s[4], s[5]), fmaxf(s[6], s[7])};
 #pragma unroll
-      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+      for (int i = 8; i < 128; i += 8)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mq[u] = fmax3(mq[u], s[i + 2 * u], s[i + 2 * u + 1]);
+      float mx = fmax3(mq[0], mq[1], fmaxf(mq[2], mq[3]));
       mx *= sl2;                                       // log2(e)/sqrt(d) > 0: max commutes with the scale
       // lazy rescale: keep the old reference max unless the row max grew by > 8 (log2 units)
       bool rescale = false;
@@ -239,16 +253,27 @@ __global__ void __launch_bounds__(384, 1)
         rescale = it > 0;
         m_ref = mx;
       }
-      // p = 2^(s*c - m): 1 in 4 as a polynomial on the FMA pipe, the rest on MUFU (the XU pipe also packs
-      // P to bf16; 1 in 4 measured best here, 1 in 2 is slower because the softmax warps become issue bound)
+      // p = 2^(s*c - m) on fp32 pairs (FFMA2): pairs j with j % UPIPE_FWD_POLY_EVERY == N - 1 as the
+      // polynomial on the FMA pipe, the rest on MUFU (XU also packs P to bf16); row sum with FADD2.
+      const uint64_t sl2x2 = f2_pack(sl2, sl2), nm2 = f2_pack(-m_ref, -m_ref);
+      uint64_t acc2[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        const float x = fmaf(s[i], sl2, -m_ref);
-        s[i] = (i & 3) == 1 ? ex2_fma(x) : ex2(x);
+      for (int j = 0; j < 64; ++j) {
+        const uint64_t t = f2_fma(f2_pack(s[2 * j], s[2 * j + 1]), sl2x2, nm2);
+        uint64_t e;
+        if (UPIPE_FWD_POLY_EVERY > 0 && (j % (UPIPE_FWD_POLY_EVERY > 0 ? UPIPE_FWD_POLY_EVERY : 1)) == UPIPE_FWD_POLY_EVERY - 1) {
+          e = ex2_fma2(t);
+        } else {
+          float t0, t1;
+          f2_unpack(t, t0, t1);
+          e = f2_pack(ex2(t0), ex2(t1));
+        }
+        acc2[j & 3] = f2_add(acc2[j & 3], e);
+        f2_unpack(e, s[2 * j], s[2 * j + 1]);
       }
-      float sum = 0.f;
-#pragma unroll
-      for (int i = 0; i < 128; ++i) sum += s[i];
+      float s1, s2;
+      f2_unpack(f2_add(f2_add(acc2[0], acc2[1]), f2_add(acc2[2], acc2[3])), s1, s2);
+      const float sum = s1 + s2;
       l_run = l_run * alpha + sum;
       if (it > 0) {
         mbar_wait(&o_full[wg], (it - 1) & 1);         // PV(it-1) done: O may be rescaled

@@ -302,6 +302,55 @@ __device__ __forceinline__ float ex2_fma(float x) {
   return __uint_as_float(__float_as_uint(p) + (__float_as_uint(r) << 23));
 }
 
+// ------------------------------------------------------------------ packed fp32x2 (FFMA2/FADD2/FMUL2)
+// sm_100 executes two fp32 operations per lane in one instruction; used where the softmax-style
+// elementwise work is issue-bound. A pair lives in one 64-bit register pair (lo = first element).
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t r, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// ex2_fma on a pair (same split and polynomial, two elements per FADD2/FFMA2).
+__device__ __forceinline__ uint64_t ex2_fma2(uint64_t x) {
+  float a, b;
+  f2_unpack(x, a, b);
+  x = f2_pack(fmaxf(a, -126.f), fmaxf(b, -126.f));
+  const uint64_t kC = f2_pack(12582912.f, 12582912.f);
+  const uint64_t r = f2_add(x, kC);
+  const uint64_t f = f2_sub(x, f2_sub(r, kC));
+  uint64_t p = f2_fma(f, f2_pack(0.055008927131519f, 0.055008927131519f), f2_pack(0.242210991999625f, 0.242210991999625f));
+  p = f2_fma(p, f, f2_pack(0.693282931500773f, 0.693282931500773f));
+  p = f2_fma(p, f, f2_pack(1.0f, 1.0f));
+  float plo, phi, rlo, rhi;
+  f2_unpack(p, plo, phi);
+  f2_unpack(r, rlo, rhi);
+  return f2_pack(__uint_as_float(__float_as_uint(plo) + (__float_as_uint(rlo) << 23)),
+                 __uint_as_float(__float_as_uint(phi) + (__float_as_uint(rhi) << 23)));
+}
+
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");

@@ -13,7 +13,7 @@ import os
 from ctypes import POINTER, c_char_p, c_float, c_int, c_int32, c_int64, c_size_t, c_uint8, c_uint32, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libupipe.so")
+LIB_PATH = os.environ.get("UPIPE_LIB") or os.path.join(_HERE, "libupipe.so")   # UPIPE_LIB: dev override (kernel variants)
 
 UPIPE_UID_BYTES = 128
 STATUS = {0: "UPIPE_OK", 1: "UPIPE_ERR_INVALID_ARG", 2: "UPIPE_ERR_UNSUPPORTED", 3: "UPIPE_ERR_CUDA",

@@ -62,3 +62,25 @@ def main(rep, obj, kname, n=30):
 
 if __name__ == "__main__":
     main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]) if len(sys.argv) > 4 else 30)
+
+
+def instr_by_pipe(rep, obj, kname):
+    """Executed warp-instructions of one kernel, by SASS opcode (for issue-slot budgets)."""
+    sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                          capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(sass)))
+    h = rows[1]
+    isrc, iex = h.index("Source"), h.index("Instructions Executed")
+    ops = {}
+    for r in rows[2:]:
+        try:
+            n = float(r[iex] or 0)
+        except ValueError:
+            continue
+        op = r[isrc].strip().split()
+        if not op:
+            continue
+        o = op[0] if not op[0].startswith("@") else op[1]
+        o = o.split(".")[0]
+        ops[o] = ops.get(o, 0) + n
+    return ops
