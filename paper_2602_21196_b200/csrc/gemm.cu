@@ -10,6 +10,7 @@
 // coordinates (see OperandMap in kernels.h), so no pack kernel runs before the
 // all-to-all: the projection epilogue writes the send buffer directly.
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -37,6 +38,9 @@ struct GemmArgs {
   int M, N, K;
   float alpha;
   int nparts, kind;          // kind: 0 single / K-concatenation, 1 M-concatenation (see GemmGroup)
+  long long* dbg;            // UPIPE_GEMM_TIMELINE=1: wait/issue cycle totals of CTA 0 (else null)
+  int dbg_mode;              // UPIPE_GEMM_TIMELINE=2: no TMA loads (MMA-only rate); 3: no MMAs (TMA-only rate)
+  int a_box_g, b_box_g;      // 64-row granules per TMA box (K-major operands: one box per operand tile)
   int kcum[kMaxParts + 1];   // K-concat: first K index of each part (multiples of BK)
   int mcum[kMaxParts + 1];   // M-concat: first row of each part (multiples of BM)
   DevOpMap a[kMaxParts], b[kMaxParts];
@@ -64,7 +68,7 @@ struct Cfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool MC>
 __global__ void __launch_bounds__(192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB0,
@@ -72,9 +76,13 @@ __global__ void __launch_bounds__(192, 1)
   // Grouped forms (GemmGroup): K-concatenation sums the products of up to three (A, B) pairs
   // into one accumulator (one epilogue pass); M-concatenation stacks up to three A operands
   // (own output maps) against one B. The part of a k-block / tile selects the tensor maps.
-  // Persistent: CTA b processes tiles b, b + gridDim.x, ... (N fastest, so CTAs running at the
-  // same time share the A row block through L2). Two TMEM accumulators: the epilogue of tile i
-  // overlaps the main loop of tile i+1.
+  // Persistent: work unit u = (m-block, n-block), N fastest (CTAs running at the same time share
+  // the A row block through L2). Two TMEM accumulators: the epilogue of tile i overlaps the main
+  // loop of tile i+1.
+  // MC (2-CTA clusters): the two CTAs of a cluster take the two 128-row tiles of one 256-row
+  // unit with the same n-block; each loads half of the shared B tile and multicasts it to both,
+  // so per SM the ring carries A (16 KB) + B/2 (BN*64 B) per k-block instead of A + B. Each
+  // CTA's MMA commit frees the stage in both CTAs (empty barriers count 2 arrivals).
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -88,8 +96,12 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = warp_id();
   const int lane = lane_id();
   const int ntn = (g.N + BN - 1) / BN;
-  const int ntiles = ntn * ((g.M + BM - 1) / BM);
+  const int ntm = (g.M + BM - 1) / BM;
+  const int crank = MC ? (int)cluster_ctarank() : 0;
+  const int unit0 = MC ? blockIdx.x / 2 : blockIdx.x, nunit_step = MC ? gridDim.x / 2 : gridDim.x;
+  const int nunits = ntn * (MC ? (ntm + 1) / 2 : ntm);
   const int nk = (g.K + BK - 1) / BK;
+  auto tile_m = [&](int u) { return MC ? (u / ntn) * 2 + crank : u / ntn; };   // m-block of unit u for this CTA
 
   auto mapA = [&](int p) { return p == 0 ? &tmA0 : (p == 1 ? &tmA1 : &tmA2); };
   auto mapB = [&](int p) { return p == 0 ? &tmB0 : (p == 1 ? &tmB1 : &tmB2); };
@@ -106,7 +118,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 2 : 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
@@ -117,64 +129,121 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_alloc<2 * BN>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync();                  // peer barriers initialised before any multicast arrives
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
+      long long tl_prod = 0;
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int m0 = (t / ntn) * BM, n0 = (t % ntn) * BN;
+      // TMA coordinates: the i-dependent parts of map_outer / map_k are formed once per tile (and
+      // operand part); the k-dependent parts advance incrementally (k / k_len, k % k_len) so the
+      // single producer thread does no integer division per k-block.
+      constexpr int GA = BM / 64, GB = BN / 64;       // A / B granules (64 rows each)
+      constexpr int GB0 = MC ? GB / 2 : GB;           // B granules this CTA loads (MC: its half)
+      for (int u = unit0; u < nunits; u += nunit_step) {
+        const int mt = tile_m(u);
+        const bool valid = mt < ntm;           // MC: the odd last m-block pairs with an empty tile
+        const int m0 = mt * BM, n0 = (u % ntn) * BN;
         const int pm = mpart(m0);
         const int ml0 = m0 - (g.kind == 1 ? g.mcum[pm] : 0);
-        int pk = 0;
+        const int cb0 = MC ? crank * GB0 : 0;
+        int pk = -1, pa = 0, pb = 0;
+        int a_out[GA], a_kb[GA], b_out[GB0], b_kb[GB0];
+        int ka_len = 1, kb_len = 1, kqa_o = 0, kqa_k = 0, kqb_o = 0, kqb_k = 0;
+        int kra = 0, krb = 0, kqa = 0, kqb = 0;
         for (int kb = 0; kb < nk; ++kb) {
+          const long long w0 = g.dbg ? clock64() : 0;
           mbar_wait(&empty[stage], phase ^ 1);
+          if (g.dbg) tl_prod += clock64() - w0;
           uint8_t* sa = ring + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
+          int npk = pk < 0 ? 0 : pk;
           if (g.kind == 0)
-            while (pk + 1 < g.nparts && kb * BK >= g.kcum[pk + 1]) ++pk;
-          const int k0 = kb * BK - (g.kind == 0 ? g.kcum[pk] : 0);
-          const int pa = g.kind == 1 ? pm : pk, pb = g.kind == 1 ? 0 : pk;
+            while (npk + 1 < g.nparts && kb * BK >= g.kcum[npk + 1]) ++npk;
+          if (npk != pk) {                     // new tile or new K part: per-(tile, part) constants
+            pk = npk;
+            pa = g.kind == 1 ? pm : pk;
+            pb = g.kind == 1 ? 0 : pk;
+            const DevOpMap& am = g.a[pa];
+            const DevOpMap& bm = g.b[pb];
+#pragma unroll
+            for (int c = 0; c < GA; ++c) {
+              const int ii = ml0 + c * 64;
+              a_out[c] = am.o_base + (ii / am.o_len) * am.o_istride + ii % am.o_len;
+              a_kb[c] = am.k_base + (ii / am.o_len) * am.k_istride;
+            }
+#pragma unroll
+            for (int c = 0; c < GB0; ++c) {
+              const int ii = n0 + (cb0 + c) * 64;
+              b_out[c] = bm.o_base + (ii / bm.o_len) * bm.o_istride + ii % bm.o_len;
+              b_kb[c] = bm.k_base + (ii / bm.o_len) * bm.k_istride;
+            }
+            ka_len = am.k_len; kqa_o = am.o_kstride; kqa_k = am.k_kstride;
+            kb_len = bm.k_len; kqb_o = bm.o_kstride; kqb_k = bm.k_kstride;
+            kqa = kqb = 0;
+            kra = krb = 0;                     // parts start at k = 0 (K-concat offsets are multiples of BK)
+          }
           const CUtensorMap* tA = mapA(pa);
           const CUtensorMap* tB = mapB(pb);
-          const DevOpMap& am = g.a[pa];
-          const DevOpMap& bm = g.b[pb];
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          if (g.dbg_mode == 2) {                // timeline experiment: MMA-only
+            mbar_arrive(&full[stage]);
+            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
+          mbar_arrive_expect_tx(&full[stage], (valid ? C::A_BYTES : 0) + C::B_BYTES);
+          if (valid) {
 #pragma unroll
-          for (int c = 0; c < BM / 64; ++c) {
-            const int i = ml0 + c * 64;
-            const int oc = map_outer(am, i, k0), kc = map_k(am, i, k0);
-            if (A_MN) tma_load_2d(sa + c * GRANULE_BYTES, tA, &full[stage], oc, kc);
-            else      tma_load_2d(sa + c * GRANULE_BYTES, tA, &full[stage], kc, oc);
+            for (int c = 0; c < GA; ++c) {
+              if (c % g.a_box_g) continue;       // covered by the previous (multi-granule) box
+              const int oc = a_out[c] + kqa * kqa_o, kc = a_kb[c] + kqa * kqa_k + kra;
+              if (A_MN) tma_load_2d(sa + c * GRANULE_BYTES, tA, &full[stage], oc, kc);
+              else      tma_load_2d(sa + c * GRANULE_BYTES, tA, &full[stage], kc, oc);
+            }
           }
 #pragma unroll
-          for (int c = 0; c < BN / 64; ++c) {
-            const int i = n0 + c * 64;
-            const int oc = map_outer(bm, i, k0), kc = map_k(bm, i, k0);
-            if (B_MN) tma_load_2d(sb + c * GRANULE_BYTES, tB, &full[stage], oc, kc);
-            else      tma_load_2d(sb + c * GRANULE_BYTES, tB, &full[stage], kc, oc);
+          for (int c = 0; c < GB0; ++c) {
+            if (c % g.b_box_g) continue;
+            const int oc = b_out[c] + kqb * kqb_o, kc = b_kb[c] + kqb * kqb_k + krb;
+            uint8_t* dst = sb + (cb0 + c) * GRANULE_BYTES;
+            if (MC) {
+              if (B_MN) tma_load_2d_mc(dst, tB, &full[stage], oc, kc, 0x3);
+              else      tma_load_2d_mc(dst, tB, &full[stage], kc, oc, 0x3);
+            } else {
+              if (B_MN) tma_load_2d(dst, tB, &full[stage], oc, kc);
+              else      tma_load_2d(dst, tB, &full[stage], kc, oc);
+            }
           }
+          if ((kra += BK) >= ka_len) { kra = 0; ++kqa; }
+          if ((krb += BK) >= kb_len) { krb = 0; ++kqb; }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
+      if (g.dbg && blockIdx.x == 0) g.dbg[0] = tl_prod;
     }
   } else if (warp == 1) {
     {
       // ---------------- MMA issuer (whole warp; elect.sync inside the MMA asm, see mma_ss_w)
       constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+      long long tl_full = 0, tl_acc = 0;
+      const long long t_start = clock64();
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      for (int u = unit0; u < nunits; u += nunit_step, ++i) {
         const int ab = i & 1;
+        const long long a0 = g.dbg ? clock64() : 0;
         mbar_wait(&acc_empty[ab], ((i >> 1) & 1) ^ 1);     // the epilogue has drained this accumulator
+        if (g.dbg) tl_acc += clock64() - a0;
         tc_fence_after();
         const uint32_t acc = tmem + ab * BN;
         for (int kb = 0; kb < nk; ++kb) {
+          const long long w0 = g.dbg ? clock64() : 0;
           mbar_wait(&full[stage], phase);
+          if (g.dbg) tl_full += clock64() - w0;
           tc_fence_after();
           const uint32_t sa = smem_u32(ring + stage * C::STAGE_BYTES);
           const uint32_t sb = sa + C::A_BYTES;
@@ -182,12 +251,19 @@ __global__ void __launch_bounds__(192, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t da = A_MN ? desc_sw128(sa + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sa + kk * 32, 16, 1024);
             const uint64_t db = B_MN ? desc_sw128(sb + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sb + kk * 32, 16, 1024);
-            mma_ss_w(acc, da, db, idesc, (kb | kk) != 0);
+            if (g.dbg_mode != 3) mma_ss_w(acc, da, db, idesc, (kb | kk) != 0);
           }
-          mma_commit_w(&empty[stage]);
+          if (MC) mma_commit_mc_w(&empty[stage], 0x3);   // frees the stage in both CTAs (B halves cross over)
+          else mma_commit_w(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
         mma_commit_w(&acc_full[ab]);
+      }
+      if (g.dbg && blockIdx.x == 0 && lane == 0) {
+        g.dbg[1] = tl_full;
+        g.dbg[2] = tl_acc;
+        g.dbg[3] = clock64() - t_start;
+        g.dbg[4] = i;
       }
     }
   } else {
@@ -195,9 +271,9 @@ __global__ void __launch_bounds__(192, 1)
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
     int i = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+    for (int u = unit0; u < nunits; u += nunit_step, ++i) {
       const int ab = i & 1;
-      const int m0 = (t / ntn) * BM, n0 = (t % ntn) * BN;
+      const int m0 = tile_m(u) * BM, n0 = (u % ntn) * BN;
       const int pc = mpart(m0);
       const DevOut& oc_ = g.c[pc];
       const int m = m0 + row;
@@ -252,6 +328,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (MC) cluster_sync();                  // no CTA leaves while its peer may still signal its barriers
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<2 * BN>(tmem);
@@ -263,10 +340,10 @@ DevOpMap to_dev(const OperandMap& m) {
                   (int)m.k_base, (int)m.k_len, (int)m.k_kstride, (int)m.k_istride};
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool MC>
 cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs& args, cudaStream_t s) {
   using C = Cfg<BN>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, MC>;
   static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (attr != cudaSuccess) return attr;
   static const int num_sms = [] {
@@ -275,20 +352,47 @@ cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs&
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
   }();
-  const int ntiles = ((args.N + BN - 1) / BN) * ((args.M + BM - 1) / BM);
-  dim3 grid(ntiles < num_sms ? ntiles : num_sms);
-  kern<<<grid, 192, C::SMEM, s>>>(ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], args);
+  const int ntn = (args.N + BN - 1) / BN, ntm = (args.M + BM - 1) / BM;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  if (MC) {
+    const int units = ntn * ((ntm + 1) / 2);
+    const int clusters = units < num_sms / 2 ? units : num_sms / 2;
+    cfg.gridDim = dim3(2 * clusters);
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  } else {
+    const int ntiles = ntn * ntm;
+    cfg.gridDim = dim3(ntiles < num_sms ? ntiles : num_sms);
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], args);
   count_launches(1);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 template <int BN>
-cudaError_t dispatch_major(bool amn, bool bmn, const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs& a,
-                           cudaStream_t s) {
-  if (!amn && !bmn) return launch<BN, false, false>(ta, tb, a, s);
-  if (!amn && bmn) return launch<BN, false, true>(ta, tb, a, s);
-  if (amn && !bmn) return launch<BN, true, false>(ta, tb, a, s);
-  return launch<BN, true, true>(ta, tb, a, s);
+cudaError_t dispatch_major(bool amn, bool bmn, bool mc, const CUtensorMap* ta, const CUtensorMap* tb,
+                           const GemmArgs& a, cudaStream_t s) {
+  if constexpr (BN >= 128) {
+    if (mc) {
+      if (!amn && !bmn) return launch<BN, false, false, true>(ta, tb, a, s);
+      if (!amn && bmn) return launch<BN, false, true, true>(ta, tb, a, s);
+      if (amn && !bmn) return launch<BN, true, false, true>(ta, tb, a, s);
+      return launch<BN, true, true, true>(ta, tb, a, s);
+    }
+  }
+  if (!amn && !bmn) return launch<BN, false, false, false>(ta, tb, a, s);
+  if (!amn && bmn) return launch<BN, false, true, false>(ta, tb, a, s);
+  if (amn && !bmn) return launch<BN, true, false, false>(ta, tb, a, s);
+  return launch<BN, true, true, false>(ta, tb, a, s);
 }
 
 bool seg_ok(int64_t len) { return len % 64 == 0 && len > 0; }
@@ -348,9 +452,42 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
   args.K = (int)K;
   args.alpha = p0.alpha;
   args.nparts = n;
+  static long long* dbg_dev = nullptr;
+  static const int tl_env = [] {
+    const char* e = getenv("UPIPE_GEMM_TIMELINE");
+    return e ? atoi(e) : 0;
+  }();
+  args.dbg = nullptr;
+  args.dbg_mode = tl_env;
+  if (tl_env) {
+    if (!dbg_dev) cudaMalloc(&dbg_dev, 8 * sizeof(long long));
+    cudaMemsetAsync(dbg_dev, 0, 8 * sizeof(long long), stream);
+    args.dbg = dbg_dev;
+  }
   args.kind = kind == GemmGroup::kMConcat ? 1 : 0;
+  // 2-CTA clusters with B multicast when there are at least two m-blocks and B splits into halves
+  // (UPIPE_GEMM_MC=0 disables; kept for A/B measurements)
+  static const bool mc_env = [] {
+    const char* e = getenv("UPIPE_GEMM_MC");
+    return !(e && e[0] == '0');
+  }();
+  const bool mc = mc_env && bn >= 128 && M > BM;
+  // TMA box rows: a K-major operand tile (rows x 64 k) goes in one box when its rows never cross an
+  // operand segment (fewer, larger TMA requests); MN-major tiles stay 64 x 64 granules (128B swizzle
+  // caps the inner box at 64 elements).
+  auto box_g = [&](bool is_a, int rows) {
+    int gr = rows / 64;
+    for (int i = 0; i < n; ++i) {
+      const OperandMap& m = is_a ? parts[i].a : parts[i].b;
+      if (m.mn_major || (m.o_len < (1 << 30) && m.o_len % rows)) return 1;
+    }
+    return gr;
+  };
+  const int a_g = box_g(true, BM), b_g = box_g(false, mc ? bn / 2 : bn);
+  args.a_box_g = a_g;
+  args.b_box_g = b_g;
   CUtensorMap ta[kMaxParts], tb[kMaxParts];
-  int64_t kc = 0, mc = 0;
+  int64_t kc = 0, mrow = 0;
   for (int i = 0; i < kMaxParts; ++i) {
     const GemmProblem& pi = parts[i < n ? i : 0];
     if (i < n) {
@@ -365,25 +502,32 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
         return cudaErrorInvalidValue;
       }
     }
-    if (!make_tmap_2d(&ta[i], pi.a.ptr, pi.a.inner, pi.a.outer, pi.a.ld, 64, 64, err, errlen)) return cudaErrorInvalidValue;
-    if (!make_tmap_2d(&tb[i], pi.b.ptr, pi.b.inner, pi.b.outer, pi.b.ld, 64, 64, err, errlen)) return cudaErrorInvalidValue;
+    if (!make_tmap_2d(&ta[i], pi.a.ptr, pi.a.inner, pi.a.outer, pi.a.ld, 64, 64 * a_g, err, errlen)) return cudaErrorInvalidValue;
+    if (!make_tmap_2d(&tb[i], pi.b.ptr, pi.b.inner, pi.b.outer, pi.b.ld, 64, 64 * b_g, err, errlen)) return cudaErrorInvalidValue;
     args.a[i] = to_dev(pi.a);
     args.b[i] = to_dev(pi.b);
     args.c[i] = to_dev(pi.c);
     args.kcum[i] = (int)kc;
-    args.mcum[i] = (int)mc;
+    args.mcum[i] = (int)mrow;
     if (i < n) {
       kc += pi.K;
-      mc += pi.M;
+      mrow += pi.M;
     }
   }
   args.kcum[kMaxParts] = (int)kc;
-  args.mcum[kMaxParts] = (int)mc;
+  args.mcum[kMaxParts] = (int)mrow;
   cudaError_t e;
-  if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, ta, tb, args, stream);
-  else if (bn == 128) e = dispatch_major<128>(p0.a.mn_major, p0.b.mn_major, ta, tb, args, stream);
-  else e = dispatch_major<64>(p0.a.mn_major, p0.b.mn_major, ta, tb, args, stream);
+  if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, mc, ta, tb, args, stream);
+  else if (bn == 128) e = dispatch_major<128>(p0.a.mn_major, p0.b.mn_major, mc, ta, tb, args, stream);
+  else e = dispatch_major<64>(p0.a.mn_major, p0.b.mn_major, false, ta, tb, args, stream);
   if (e != cudaSuccess) snprintf(err, errlen, "gemm launch: %s", cudaGetErrorString(e));
+  if (args.dbg) {
+    long long h[8];
+    cudaMemcpyAsync(h, args.dbg, sizeof h, cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    fprintf(stderr, "[gemm timeline CTA 0] M=%d N=%d K=%d BN=%d mc=%d tiles=%lld: producer wait_empty %lld | mma wait_full %lld "
+            "wait_acc_empty %lld total %lld cycles\n", args.M, args.N, args.K, bn, (int)mc, h[4], h[0], h[1], h[2], h[3]);
+  }
   return e;
 }
 

@@ -49,7 +49,10 @@ def main(rep, out, note=""):
         tot = 0.0
         for r in src[2:]:
             for i in cols:
-                v = float(r[i] or 0)
+                try:
+                    v = float(r[i] or 0) if i < len(r) else 0.0
+                except ValueError:       # header rows of the next kernel's section
+                    v = 0.0
                 stalls[h[i]] = stalls.get(h[i], 0.0) + v
                 tot += v
         stalls = {k: round(v / tot, 4) for k, v in sorted(stalls.items(), key=lambda x: -x[1])[:10]} if tot else {}
