@@ -26,6 +26,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Llama3-8B attn fwd+bwd tokens/s/GPU & peak activation GB at 1/2/4/8 B200"
 LLAMA = dict(Hq=32, Hkv=8, d=128, D=4096)
+MODELS = {   # BASELINE configs: Llama3-8B attention (configs 1-4) and the 32B-class GQA layer (config 5)
+    "llama3-8b": dict(LLAMA, name="Llama3-8B attention layer", workload="llama3-8b-attention-layer-fwd-bwd"),
+    "32b": dict(Hq=64, Hkv=8, d=128, D=5120, name="32B-class GQA attention layer (64Q/8KV, d=128, hidden 5120)",
+                workload="32b-gqa-attention-layer-fwd-bwd"),
+}
 
 
 def parse():
@@ -36,6 +41,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--seq", type=int, default=131072, help="global sequence length S")
     ap.add_argument("--chunk", type=int, default=8, help="chunk_heads U (UPipe); Ulysses = 32")
+    ap.add_argument("--model", choices=sorted(MODELS), default="llama3-8b",
+                    help="layer shape (default: BASELINE's headline Llama3-8B layer)")
     ap.add_argument("--no-ulysses", action="store_true", help="skip the chunk=all-heads Ulysses comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -207,7 +214,8 @@ def main():
     import synth
 
     C = world
-    Hq, Hkv, d, D = LLAMA["Hq"], LLAMA["Hkv"], LLAMA["d"], LLAMA["D"]
+    M = MODELS[args.model]
+    Hq, Hkv, d, D = M["Hq"], M["Hkv"], M["d"], M["D"]
     S = args.seq
     assert S % C == 0
     S_l = S // C
@@ -297,7 +305,7 @@ def main():
     if os.path.exists(tf):
         with open(tf) as f:
             j = json.load(f)
-        if j.get("seq") == S and j.get("chunk") == U and j.get("C") == C:
+        if j.get("seq") == S and j.get("chunk") == U and j.get("C") == C and j.get("model", "llama3-8b") == args.model:
             traffic = j.get("dram_bytes_per_launch")
     step_flops = flops_step_per_rank(S, C, Hq, Hkv, d, D)
     per_step_ms = {k: v[0] / args.steps for k, v in tr.items()}
@@ -306,10 +314,11 @@ def main():
         "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded counter-based generator, drawn on device)",
-        "config": {"workload": "llama3-8b-attention-layer-fwd-bwd (BASELINE configs[1])", "model": "Llama3-8B attention layer",
+        "config": {"workload": M["workload"] + (" (BASELINE configs[1])" if args.model == "llama3-8b" and S == 131072 else ""),
+                   "model": M["name"],
                    "n_q_heads": Hq, "n_kv_heads": Hkv, "head_dim": d, "hidden": D, "seq_len": S, "global_batch": 1,
                    "chunk_heads": U, "cp": C, "parallelism": f"cp{C} (UPipe, U={U})",
-                   "l2": "inputs larger than L2 (x, dy: S_l x 4096 bf16 per rank); no flush needed"},
+                   "l2": f"inputs larger than L2 (x, dy: S_l x {D} bf16 per rank); no flush needed"},
         "tokens_per_s_per_gpu": tok_s / world,
         "gpu_launches": main_run["launches"],
         "gpu_launches_per_step": main_run["launches"] / args.steps,

@@ -279,7 +279,11 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&o_full[wg], (it - 1) & 1);         // PV(it-1) done: O may be rescaled
         tc_fence_after();
       }
-      if (rescale) {
+      // tcgen05.ld/st are warp-collective (.sync.aligned): the rescale decision is per row, so the
+      // warp rescales if any of its rows needs it (alpha = 1 for the others). A per-thread branch
+      // here diverges the warp and hangs once rows' maxima grow at different tiles.
+      if (__any_sync(0xffffffffu, rescale)) {
+        if (!rescale) alpha = 1.f;
 #pragma unroll
         for (int c = 0; c < D / 16; ++c) {
           uint32_t r[16];

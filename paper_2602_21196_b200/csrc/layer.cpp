@@ -14,6 +14,7 @@
 //    attention"); the out all-to-all of stage s overlaps attention s+1. Costs a second
 //    buffer set (DESIGN A23). Cross-stream order is carried by CUDA events.
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "upipe_internal.h"
@@ -46,6 +47,14 @@ struct Step {
   }
 };
 
+bool debug_sync() {
+  static const bool on = [] {
+    const char* e = getenv("UPIPE_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // Runs one step, reports failures into ctx->last_error.
 struct Runner {
   upipe_ctx_s* ctx;
@@ -58,6 +67,12 @@ struct Runner {
     Step step(ctx, s, cat, what);
     errbuf[0] = 0;
     cudaError_t e = f(errbuf);
+    if (debug_sync()) {                  // UPIPE_DEBUG_SYNC=1: synchronise and log every step (hang triage)
+      fprintf(stderr, "[upipe step] %s ...", what);
+      cudaError_t e2 = cudaStreamSynchronize(s);
+      fprintf(stderr, " %s\n", cudaGetErrorString(e2));
+      if (e == cudaSuccess) e = e2;
+    }
     if (e != cudaSuccess) {
       ctx->last_error = std::string(what) + ": " + (errbuf[0] ? errbuf : cudaGetErrorString(e));
       status = UPIPE_ERR_CUDA;

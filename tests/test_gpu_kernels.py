@@ -84,6 +84,38 @@ def test_attn_fwd_causal_perturbation_bitwise(U):
     assert not torch.equal(o1[t:], o2[t:])
 
 
+@pytest.mark.timeout(300)
+def test_attn_fwd_rows_rescale_at_different_tiles(U):
+    # Odd query rows see their running max jump by ~16 (log2 units) at key tile 2, even rows never do,
+    # so the forward's lazy O rescale fires for some rows of a warp and not others. The TMEM
+    # load/store of the rescale are warp-collective; a per-row branch around them hangs the kernel
+    # (found with the 32B-class layer's inputs at S = 128K). Also checks the backward on these inputs.
+    S, Hq, Hkv, d = 512, 2, 1, 128
+    c = _core(S, Hq, Hkv, d, 1.0)
+    c["q"] = c["q"].copy()
+    c["k"] = c["k"].copy()
+    c["q"][1::2, :, 0] = 16.0
+    c["q"][0::2, :, 0] = 0.0
+    c["k"][:, :, 0] = 0.0
+    c["k"][256:, :, 0] = 8.0
+    q, k, v, o, lse = _run_fwd(U, c, S, Hq, Hkv, d, 1)
+    do = to_bf16(c["do"])
+    delta = torch.empty((S, Hq), dtype=torch.float32, device=dev())
+    U.upipe_rowdot(do, Hq * d, o, Hq * d, delta, Hq, S, Hq, d)
+    dq = torch.zeros((S, Hq, d), dtype=torch.float32, device=dev())
+    dk = torch.empty((S, Hkv, d), dtype=torch.float32, device=dev())
+    dv = torch.empty((S, Hkv, d), dtype=torch.float32, device=dev())
+    U.upipe_attn_core_bwd(q, k, v, do, lse, delta, dq, dk, dv, S, Hq, Hkv, d, 1, Hq * d, Hkv * d, Hq * d, S, Hq)
+    torch.cuda.synchronize()
+    O, L = oracle.attn_fwd(c["q"], c["k"], c["v"], causal=True)
+    assert_close("O", to_np(o), O, ATTN_REL, ABS)
+    assert_close("lse", to_np(lse), L, 1e-4, 2e-4)
+    dQ, dK, dV = oracle.attn_bwd(c["q"], c["k"], c["v"], c["do"], causal=True)
+    assert_close("dV", to_np(dv), dV, ATTN_REL, ABS)
+    assert_close("dQ", to_np(dq), dQ, ATTN_GRAD_REL, ABS)
+    assert_close("dK", to_np(dk), dK, ATTN_GRAD_REL, ABS)
+
+
 BWD_CASES = [(128, 1, 1, 64, 1), (200, 2, 1, 64, 1), (512, 4, 1, 128, 1), (640, 4, 2, 128, 1),
              (384, 2, 2, 64, 0), (1024, 2, 1, 128, 1)]
 
