@@ -17,6 +17,7 @@
 // headroom in fp32/bf16), which is exact: l and O always share the reference max.
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -33,7 +34,12 @@ struct FwdArgs {
   long long S, ldo, ld_lse;
   int nq, nkv, causal, n_pairs;
   float scale_log2;  // log2(e) / sqrt(d)
+  long long* dbg;    // UPIPE_FWD_TIMELINE=1: per-role cycle totals of CTA (0, 0)
 };
+
+// Cycle counters of the per-role timeline; compiled out unless the timeline variant is launched.
+template <bool TL>
+__device__ __forceinline__ long long tick() { if constexpr (TL) return clock64(); else return 0; }
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -65,7 +71,7 @@ struct FwdCfg {
   static constexpr uint32_t TM_SA = 0, TM_SB = 128, TM_OA = 256, TM_OB = 256 + D;
 };
 
-template <int D>
+template <int D, bool TL>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
@@ -160,6 +166,8 @@ __global__ void __launch_bounds__(384, 1)
         for (int ks = 0; ks < 8; ++ks)
           mma_ts_w(tm, tp + ks * 8, dv + (((ks >> 2) * 8192 + (ks & 3) * 2048) >> 4), idO, (acc || ks) ? 1u : 0u);
       };
+      long long tw[4] = {0, 0, 0, 0};   // wait p_full A, wait p_full B, wait K, wait V
+      const long long t_begin = tick<TL>();
       mbar_wait(q_full, 0);
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
@@ -173,10 +181,14 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t ph = (it / C::KV_STAGES) & 1;
         base = ld_volatile_shared_u32(tmem_slot + 1);
         const uint32_t sv = base + C::OFF_V + st * C::QBYTES;
+        long long w0 = tick<TL>();
         mbar_wait(&v_full[st], ph);
+        tw[3] += tick<TL>() - w0;
         // ---- tile A
         if (it < nA) {
+          w0 = tick<TL>();
           mbar_wait(&p_full[0], it & 1);
+          tw[0] += tick<TL>() - w0;
           tc_fence_after();
           issue_PV(tmem + C::TM_SA, sv, tmem + C::TM_OA, it > 0);
           mma_commit_w(&o_full[0]);
@@ -184,14 +196,18 @@ __global__ void __launch_bounds__(384, 1)
         const bool more = it + 1 < nB;
         const int st1 = (it + 1) % C::KV_STAGES;
         const uint32_t ph1 = ((it + 1) / C::KV_STAGES) & 1;
+        w0 = tick<TL>();
         if (more) mbar_wait(&k_full[st1], ph1);
+        tw[2] += tick<TL>() - w0;
         tc_fence_after();
         if (it + 1 < nA) {
           issue_S(base + C::OFF_QA, base + C::OFF_K + st1 * C::QBYTES, tmem + C::TM_SA);
           mma_commit_w(&s_full[0]);
         }
         // ---- tile B
+        w0 = tick<TL>();
         mbar_wait(&p_full[1], it & 1);
+        tw[1] += tick<TL>() - w0;
         tc_fence_after();
         issue_PV(tmem + C::TM_SB, sv, tmem + C::TM_OB, it > 0);
         mma_commit_w(&o_full[1]);
@@ -201,6 +217,11 @@ __global__ void __launch_bounds__(384, 1)
           mma_commit_w(&s_full[1]);
           mma_commit_w(&k_empty[st1]);
         }
+      }
+      if (TL && a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) {
+        for (int i = 0; i < 4; ++i) a.dbg[i] = tw[i];
+        a.dbg[4] = tick<TL>() - t_begin;
+        a.dbg[5] = nB;
       }
     }
   } else if (warp < 8) {
@@ -216,18 +237,21 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tO = tmem + (wg ? C::TM_OB : C::TM_OA) + ((uint32_t)(quad * 32) << 16);
     const float sl2 = a.scale_log2;
     float m_ref = -INFINITY, l_run = 0.f;
+    long long ts[5] = {0, 0, 0, 0, 0};   // wait S, TMEM load, max+exp+sum, O wait+rescale, P store+arrive
     for (int it = 0; it < n; ++it) {
+      const long long e0 = tick<TL>();
       mbar_wait(&s_full[wg], it & 1);
       tc_fence_after();
-      float s[128];
+      const long long e1 = tick<TL>();
+      ts[0] += e1 - e0;
+      // raw scores (scale folded below): the four 32-column loads are in flight together
+      uint32_t sr[128];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tS + c * 32, r);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);   // raw scores (scale folded below)
-      }
+      for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + c * 32));
+      tmem_wait_ld();
+      float* s = reinterpret_cast<float*>(sr);
+      const long long e2 = tick<TL>();
+      ts[1] += e2 - e1;
       const long long key0 = (long long)it * 128;
       const bool edge = a.causal ? (it == qt) : (key0 + 128 > a.S);
       if (edge) {
@@ -257,6 +281,7 @@ __global__ void __launch_bounds__(384, 1)
       // polynomial on the FMA pipe, the rest on MUFU (XU also packs P to bf16); row sum with FADD2.
       const uint64_t sl2x2 = f2_pack(sl2, sl2), nm2 = f2_pack(-m_ref, -m_ref);
       uint64_t acc2[4] = {0, 0, 0, 0};
+      uint32_t pk[16];
 #pragma unroll
       for (int j = 0; j < 64; ++j) {
         const uint64_t t = f2_fma(f2_pack(s[2 * j], s[2 * j + 1]), sl2x2, nm2);
@@ -269,12 +294,19 @@ __global__ void __launch_bounds__(384, 1)
           e = f2_pack(ex2(t0), ex2(t1));
         }
         acc2[j & 3] = f2_add(acc2[j & 3], e);
-        f2_unpack(e, s[2 * j], s[2 * j + 1]);
+        // P (bf16 pairs) -> TMEM over this tile's S columns as soon as 16 pairs are ready (the PV MMA
+        // reads it as its A operand; S(it+1) is issued after PV(it), so the overwrite is ordered)
+        float e0, e1;
+        f2_unpack(e, e0, e1);
+        pk[j & 15] = pack_bf16(e0, e1);
+        if ((j & 15) == 15) tmem_st16(tS + (j >> 4) * 16, pk);
       }
       float s1, s2;
       f2_unpack(f2_add(f2_add(acc2[0], acc2[1]), f2_add(acc2[2], acc2[3])), s1, s2);
       const float sum = s1 + s2;
       l_run = l_run * alpha + sum;
+      const long long e3 = tick<TL>();
+      ts[2] += e3 - e2;
       if (it > 0) {
         mbar_wait(&o_full[wg], (it - 1) & 1);         // PV(it-1) done: O may be rescaled
         tc_fence_after();
@@ -295,19 +327,15 @@ __global__ void __launch_bounds__(384, 1)
         }
         tmem_wait_st();
       }
-      // P (bf16 pairs) -> TMEM over this tile's S columns (all S values are already in registers);
-      // the PV MMA reads it as its A operand. S(it+1) is issued after PV(it), so the overwrite is ordered.
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]);
-        tmem_st16(tS + c * 16, pk);
-      }
+      const long long e4 = tick<TL>();
+      ts[3] += e4 - e3;
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[wg]);
+      ts[4] += tick<TL>() - e4;
     }
+    if (TL && a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && quad == 0)
+      for (int i = 0; i < 5; ++i) a.dbg[6 + wg * 5 + i] = ts[i];
     // ---- epilogue: O / l -> bf16, lse
     mbar_wait(&o_full[wg], (n - 1) & 1);
     tc_fence_after();
@@ -365,22 +393,37 @@ cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err
   a.n_pairs = (ntiles + 1) / 2;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)p.d);
   dim3 grid(a.n_pairs, p.nq);
-  cudaError_t e;
-  if (p.d == 128) {
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(attn_fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<128>::SMEM);
-    if (attr != cudaSuccess) { snprintf(err, errlen, "attn_fwd attr: %s", cudaGetErrorString(attr)); return attr; }
-    attn_fwd_kernel<128><<<grid, 384, FwdCfg<128>::SMEM, stream>>>(tq, tk, tv, a);
-    count_launches(1);
-  } else {
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(attn_fwd_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdCfg<64>::SMEM);
-    if (attr != cudaSuccess) { snprintf(err, errlen, "attn_fwd attr: %s", cudaGetErrorString(attr)); return attr; }
-    attn_fwd_kernel<64><<<grid, 384, FwdCfg<64>::SMEM, stream>>>(tq, tk, tv, a);
-    count_launches(1);
+  // UPIPE_FWD_TIMELINE=1: per-role cycle breakdown of CTA (0,0), printed to stderr after the launch
+  static long long* dbg_dev = nullptr;
+  const char* tlenv = getenv("UPIPE_FWD_TIMELINE");
+  a.dbg = nullptr;
+  if (tlenv && tlenv[0] == '1') {
+    if (!dbg_dev) cudaMalloc(&dbg_dev, 32 * sizeof(long long));
+    cudaMemsetAsync(dbg_dev, 0, 32 * sizeof(long long), stream);
+    a.dbg = dbg_dev;
   }
+  cudaError_t e;
+  auto go = [&](auto kern, int smem) -> cudaError_t {
+    cudaError_t at = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (at != cudaSuccess) { snprintf(err, errlen, "attn_fwd attr: %s", cudaGetErrorString(at)); return at; }
+    kern<<<grid, 384, smem, stream>>>(tq, tk, tv, a);
+    count_launches(1);
+    return cudaSuccess;
+  };
+  if (p.d == 128) e = a.dbg ? go(attn_fwd_kernel<128, true>, FwdCfg<128>::SMEM) : go(attn_fwd_kernel<128, false>, FwdCfg<128>::SMEM);
+  else e = go(attn_fwd_kernel<64, false>, FwdCfg<64>::SMEM);
+  if (e != cudaSuccess) return e;
   e = cudaGetLastError();
   if (e != cudaSuccess) snprintf(err, errlen, "attn_fwd launch: %s", cudaGetErrorString(e));
+  if (a.dbg) {
+    long long h[32];
+    cudaMemcpyAsync(h, a.dbg, sizeof h, cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    fprintf(stderr,
+            "[attn_fwd timeline CTA(0,0) nB=%lld total %lld cycles] mma: wait_pA %lld wait_pB %lld wait_K %lld wait_V %lld | "
+            "softmax A: wait_S %lld ld %lld math %lld O %lld store %lld | B: wait_S %lld ld %lld math %lld O %lld store %lld\n",
+            h[5], h[4], h[0], h[1], h[2], h[3], h[6], h[7], h[8], h[9], h[10], h[11], h[12], h[13], h[14], h[15]);
+  }
   return e;
 }
 
