@@ -262,6 +262,9 @@ def main():
         torch.cuda.synchronize()
         out["peak_bytes"] = torch.cuda.max_memory_allocated() - base
         out["ws_bytes"] = sum(t.numel() for t in attn._ws.values())
+        # chunk buffers = workspace minus the U-independent fp32 dX accumulator [S_l, D] (only allocated
+        # when there is more than one stage): the "intermediate tensors" of P:332-343 (DESIGN A21)
+        out["chunk_bytes"] = out["ws_bytes"] - (S_l * D * 4 if Hq // chunk > 1 else 0)
         stream = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if trace:
@@ -335,6 +338,7 @@ def main():
         "phase_ms_per_step": per_step_ms,
         "peak_activation_gib": main_run["peak_bytes"] / 2**30,
         "workspace_gib": main_run["ws_bytes"] / 2**30,
+        "chunk_buffers_gib": main_run["chunk_bytes"] / 2**30,
         "clocks": clocks,
     }
     main_run["attn"].close()
@@ -346,7 +350,10 @@ def main():
                              "upipe_over_ulysses": tok_s / ul_tok,
                              "peak_activation_gib": ul["peak_bytes"] / 2**30,
                              "workspace_gib": ul["ws_bytes"] / 2**30,
-                             "activation_reduction": 1 - main_run["peak_bytes"] / ul["peak_bytes"]}
+                             "chunk_buffers_gib": ul["chunk_bytes"] / 2**30,
+                             "activation_reduction": 1 - main_run["peak_bytes"] / ul["peak_bytes"],
+                             "chunk_buffer_reduction": 1 - main_run["chunk_bytes"] / ul["chunk_bytes"],
+                             "chunk_buffer_reduction_target": 1 - U / Hq}
         ul["attn"].close()
 
     if not args.quick and not args.no_e2e:

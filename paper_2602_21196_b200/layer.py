@@ -48,9 +48,12 @@ class UPipeAttention:
         return U.make_shape(seq_local, self.D, self.Hq, self.Hkv, self.d, self.U, self.causal)
 
     def workspace(self, seq_local: int, pass_: int) -> torch.Tensor:
-        key = (seq_local, pass_)
+        # One chunk-buffer workspace per sequence length, shared by the forward and the backward pass
+        # (they never run at the same time and nothing in it outlives a call): sized for the larger.
+        key = seq_local
         if key not in self._ws:
-            n = U.upipe_workspace_size(self.C, self.shape(seq_local), pass_ + (2 if self.flags & 1 else 0))
+            sync = 2 if self.flags & 1 else 0
+            n = max(U.upipe_workspace_size(self.C, self.shape(seq_local), p + sync) for p in (0, 1))
             self._ws[key] = torch.empty(max(n, 256), dtype=torch.uint8, device=self.device)
         return self._ws[key]
 
