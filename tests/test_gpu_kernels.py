@@ -25,6 +25,9 @@ GEMM_BF16_REL = 2.5e-3
 GEMM_F32_REL = 1e-5
 ATTN_REL = 3e-3        # O, dV
 ATTN_GRAD_REL = 4e-3   # dQ, dK (fp32 atomics + bf16 P/dS)
+# score std 4 ("peaky"): dQ/dK are sums of strongly cancelling dS K products, so the bf16 rounding
+# of dS (DESIGN A16) costs more relative to |dQ|; the north_star layer bar applies
+ATTN_GRAD_REL_PEAKY = 5e-3
 ABS = 2e-2
 
 
@@ -60,9 +63,11 @@ FWD_CASES = [(128, 1, 1, 64, 1), (200, 2, 1, 64, 1), (512, 4, 1, 128, 1), (1000,
              (384, 2, 2, 64, 0), (333, 4, 2, 128, 0), (2048, 2, 1, 128, 1)]
 
 
+@pytest.mark.parametrize("score_std", [1.0, 4.0])
 @pytest.mark.parametrize("S,Hq,Hkv,d,causal", FWD_CASES)
-def test_attn_fwd(U, S, Hq, Hkv, d, causal):
-    c = _core(S, Hq, Hkv, d, 1.0)
+def test_attn_fwd(U, S, Hq, Hkv, d, causal, score_std):
+    # score_std 4: the "peaky" regime (row maxima jump across key tiles; lazy rescale exercised)
+    c = _core(S, Hq, Hkv, d, score_std)
     _, _, _, o, lse = _run_fwd(U, c, S, Hq, Hkv, d, causal)
     torch.cuda.synchronize()
     O, L = oracle.attn_fwd(c["q"], c["k"], c["v"], causal=bool(causal))
@@ -120,9 +125,10 @@ BWD_CASES = [(128, 1, 1, 64, 1), (200, 2, 1, 64, 1), (512, 4, 1, 128, 1), (640, 
              (384, 2, 2, 64, 0), (1024, 2, 1, 128, 1)]
 
 
+@pytest.mark.parametrize("score_std", [1.0, 4.0])
 @pytest.mark.parametrize("S,Hq,Hkv,d,causal", BWD_CASES)
-def test_attn_bwd(U, S, Hq, Hkv, d, causal):
-    c = _core(S, Hq, Hkv, d, 1.0)
+def test_attn_bwd(U, S, Hq, Hkv, d, causal, score_std):
+    c = _core(S, Hq, Hkv, d, score_std)
     q, k, v, o, lse = _run_fwd(U, c, S, Hq, Hkv, d, causal)
     do = to_bf16(c["do"])
     delta = torch.empty((S, Hq), dtype=torch.float32, device=dev())
@@ -136,8 +142,9 @@ def test_attn_bwd(U, S, Hq, Hkv, d, causal):
     assert_close("delta", to_np(delta), oracle.rowdot(c["do"], to_np(o)), 1e-5, 1e-4)
     dQ, dK, dV = oracle.attn_bwd(c["q"], c["k"], c["v"], c["do"], causal=bool(causal))
     assert_close("dV", to_np(dv), dV, ATTN_REL, ABS)
-    assert_close("dQ", to_np(dq), dQ, ATTN_GRAD_REL, ABS)
-    assert_close("dK", to_np(dk), dK, ATTN_GRAD_REL, ABS)
+    gtol = ATTN_GRAD_REL if score_std <= 1.0 else ATTN_GRAD_REL_PEAKY
+    assert_close("dQ", to_np(dq), dQ, gtol, ABS)
+    assert_close("dK", to_np(dk), dK, gtol, ABS)
 
 
 def test_synth_device_generator_bitwise(U):
