@@ -68,7 +68,7 @@ struct Cfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
-template <int BN, bool A_MN, bool B_MN, bool MC>
+template <int BN, bool A_MN, bool B_MN, int CL>
 __global__ void __launch_bounds__(192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB0,
@@ -97,11 +97,21 @@ __global__ void __launch_bounds__(192, 1)
   const int lane = lane_id();
   const int ntn = (g.N + BN - 1) / BN;
   const int ntm = (g.M + BM - 1) / BM;
+  constexpr bool MC = CL > 1;
+  // cluster rank r: m-sub-block ms = r & 1 (CL >= 2), n-sub-block ns = r >> 1 (CL == 4)
   const int crank = MC ? (int)cluster_ctarank() : 0;
-  const int unit0 = MC ? blockIdx.x / 2 : blockIdx.x, nunit_step = MC ? gridDim.x / 2 : gridDim.x;
-  const int nunits = ntn * (MC ? (ntm + 1) / 2 : ntm);
+  const int ms = crank & 1, ns = CL == 4 ? crank >> 1 : 0;
+  const int unit0 = blockIdx.x / CL, nunit_step = gridDim.x / CL;
+  const int ntn_u = CL == 4 ? ntn / 2 : ntn;                     // n-units (CL = 4: pairs of n-blocks)
+  const int nunits = ntn_u * (MC ? (ntm + 1) / 2 : ntm);
   const int nk = (g.K + BK - 1) / BK;
-  auto tile_m = [&](int u) { return MC ? (u / ntn) * 2 + crank : u / ntn; };   // m-block of unit u for this CTA
+  auto tile_m = [&](int u) { return MC ? (u / ntn_u) * 2 + ms : u / ntn_u; };   // m-block of unit u for this CTA
+  auto tile_n = [&](int u) { return CL == 4 ? (u % ntn_u) * 2 + ns : u % ntn_u; };
+  // multicast masks: A to the CTAs sharing this m-block (CL = 4), B to those sharing this n-block;
+  // an MMA commit frees the stage in every CTA that writes into this CTA's ring
+  const uint16_t maskA = CL == 4 ? (uint16_t)((1u << crank) | (1u << (crank ^ 2))) : 0;
+  const uint16_t maskB = CL == 4 ? (uint16_t)((1u << crank) | (1u << (crank ^ 1))) : 0x3;
+  const uint16_t maskE = CL == 4 ? (uint16_t)(maskA | maskB) : 0x3;
 
   auto mapA = [&](int p) { return p == 0 ? &tmA0 : (p == 1 ? &tmA1 : &tmA2); };
   auto mapB = [&](int p) { return p == 0 ? &tmB0 : (p == 1 ? &tmB1 : &tmB2); };
@@ -118,7 +128,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MC ? 2 : 1);
+      mbar_init(&empty[s], CL == 4 ? 3 : (MC ? 2 : 1));
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
@@ -144,15 +154,17 @@ __global__ void __launch_bounds__(192, 1)
       // single producer thread does no integer division per k-block.
       constexpr int GA = BM / 64, GB = BN / 64;       // A / B granules (64 rows each)
       constexpr int GB0 = MC ? GB / 2 : GB;           // B granules this CTA loads (MC: its half)
+      constexpr int GA0 = CL == 4 ? GA / 2 : GA;      // A granules this CTA loads (CL = 4: its half)
       for (int u = unit0; u < nunits; u += nunit_step) {
         const int mt = tile_m(u);
         const bool valid = mt < ntm;           // MC: the odd last m-block pairs with an empty tile
-        const int m0 = mt * BM, n0 = (u % ntn) * BN;
+        const int m0 = mt * BM, n0 = tile_n(u) * BN;
         const int pm = mpart(m0);
         const int ml0 = m0 - (g.kind == 1 ? g.mcum[pm] : 0);
-        const int cb0 = MC ? crank * GB0 : 0;
+        const int cb0 = MC ? ms * GB0 : 0;
+        const int ca0 = CL == 4 ? ns * GA0 : 0;
         int pk = -1, pa = 0, pb = 0;
-        int a_out[GA], a_kb[GA], b_out[GB0], b_kb[GB0];
+        int a_out[GA0], a_kb[GA0], b_out[GB0], b_kb[GB0];
         int ka_len = 1, kb_len = 1, kqa_o = 0, kqa_k = 0, kqb_o = 0, kqb_k = 0;
         int kra = 0, krb = 0, kqa = 0, kqb = 0;
         for (int kb = 0; kb < nk; ++kb) {
@@ -171,8 +183,8 @@ __global__ void __launch_bounds__(192, 1)
             const DevOpMap& am = g.a[pa];
             const DevOpMap& bm = g.b[pb];
 #pragma unroll
-            for (int c = 0; c < GA; ++c) {
-              const int ii = ml0 + c * 64;
+            for (int c = 0; c < GA0; ++c) {
+              const int ii = ml0 + (ca0 + c) * 64;
               a_out[c] = am.o_base + (ii / am.o_len) * am.o_istride + ii % am.o_len;
               a_kb[c] = am.k_base + (ii / am.o_len) * am.k_istride;
             }
@@ -197,11 +209,17 @@ __global__ void __launch_bounds__(192, 1)
           mbar_arrive_expect_tx(&full[stage], (valid ? C::A_BYTES : 0) + C::B_BYTES);
           if (valid) {
 #pragma unroll
-            for (int c = 0; c < GA; ++c) {
+            for (int c = 0; c < GA0; ++c) {
               if (c % g.a_box_g) continue;       // covered by the previous (multi-granule) box
               const int oc = a_out[c] + kqa * kqa_o, kc = a_kb[c] + kqa * kqa_k + kra;
-              if (A_MN) tma_load_2d(sa + c * GRANULE_BYTES, tA, &full[stage], oc, kc);
-              else      tma_load_2d(sa + c * GRANULE_BYTES, tA, &full[stage], kc, oc);
+              uint8_t* dst = sa + (ca0 + c) * GRANULE_BYTES;
+              if (CL == 4) {
+                if (A_MN) tma_load_2d_mc(dst, tA, &full[stage], oc, kc, maskA);
+                else      tma_load_2d_mc(dst, tA, &full[stage], kc, oc, maskA);
+              } else {
+                if (A_MN) tma_load_2d(dst, tA, &full[stage], oc, kc);
+                else      tma_load_2d(dst, tA, &full[stage], kc, oc);
+              }
             }
           }
 #pragma unroll
@@ -210,8 +228,8 @@ __global__ void __launch_bounds__(192, 1)
             const int oc = b_out[c] + kqb * kqb_o, kc = b_kb[c] + kqb * kqb_k + krb;
             uint8_t* dst = sb + (cb0 + c) * GRANULE_BYTES;
             if (MC) {
-              if (B_MN) tma_load_2d_mc(dst, tB, &full[stage], oc, kc, 0x3);
-              else      tma_load_2d_mc(dst, tB, &full[stage], kc, oc, 0x3);
+              if (B_MN) tma_load_2d_mc(dst, tB, &full[stage], oc, kc, maskB);
+              else      tma_load_2d_mc(dst, tB, &full[stage], kc, oc, maskB);
             } else {
               if (B_MN) tma_load_2d(dst, tB, &full[stage], oc, kc);
               else      tma_load_2d(dst, tB, &full[stage], kc, oc);
@@ -253,7 +271,7 @@ __global__ void __launch_bounds__(192, 1)
             const uint64_t db = B_MN ? desc_sw128(sb + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sb + kk * 32, 16, 1024);
             if (g.dbg_mode != 3) mma_ss_w(acc, da, db, idesc, (kb | kk) != 0);
           }
-          if (MC) mma_commit_mc_w(&empty[stage], 0x3);   // frees the stage in both CTAs (B halves cross over)
+          if (MC) mma_commit_mc_w(&empty[stage], maskE);   // frees the stage in every CTA writing into ours
           else mma_commit_w(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -273,7 +291,7 @@ __global__ void __launch_bounds__(192, 1)
     int i = 0;
     for (int u = unit0; u < nunits; u += nunit_step, ++i) {
       const int ab = i & 1;
-      const int m0 = tile_m(u) * BM, n0 = (u % ntn) * BN;
+      const int m0 = tile_m(u) * BM, n0 = tile_n(u) * BN;
       const int pc = mpart(m0);
       const DevOut& oc_ = g.c[pc];
       const int m = m0 + row;
@@ -340,10 +358,10 @@ DevOpMap to_dev(const OperandMap& m) {
                   (int)m.k_base, (int)m.k_len, (int)m.k_kstride, (int)m.k_istride};
 }
 
-template <int BN, bool A_MN, bool B_MN, bool MC>
+template <int BN, bool A_MN, bool B_MN, int CL>
 cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs& args, cudaStream_t s) {
   using C = Cfg<BN>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, MC>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, CL>;
   static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (attr != cudaSuccess) return attr;
   static const int num_sms = [] {
@@ -358,41 +376,50 @@ cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs&
   cfg.blockDim = dim3(192);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
-  if (MC) {
-    const int units = ntn * ((ntm + 1) / 2);
-    const int clusters = units < num_sms / 2 ? units : num_sms / 2;
-    cfg.gridDim = dim3(2 * clusters);
+  const int units = (CL == 4 ? ntn / 2 : ntn) * (CL > 1 ? (ntm + 1) / 2 : ntm);
+  if (CL > 1) {
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.x = CL;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-  } else {
-    const int ntiles = ntn * ntm;
-    cfg.gridDim = dim3(ntiles < num_sms ? ntiles : num_sms);
   }
+  // persistent grid: no more clusters than can be co-resident (clusters must fit inside a GPC, so
+  // this can be below num_sms / CL; a second partial wave would double the tail)
+  static const int max_clusters = [&] {
+    if (CL == 1) return num_sms;
+    int n = 0;
+    cudaLaunchConfig_t q = cfg;
+    q.gridDim = dim3(CL * (num_sms / CL));
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n <= 0) n = num_sms / CL;
+    return n;
+  }();
+  const int clusters = units < max_clusters ? units : max_clusters;
+  cfg.gridDim = dim3(CL * clusters);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], args);
   count_launches(1);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
+template <int BN, int CL>
+cudaError_t dispatch_cl(bool amn, bool bmn, const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs& a,
+                        cudaStream_t s) {
+  if (!amn && !bmn) return launch<BN, false, false, CL>(ta, tb, a, s);
+  if (!amn && bmn) return launch<BN, false, true, CL>(ta, tb, a, s);
+  if (amn && !bmn) return launch<BN, true, false, CL>(ta, tb, a, s);
+  return launch<BN, true, true, CL>(ta, tb, a, s);
+}
+
 template <int BN>
-cudaError_t dispatch_major(bool amn, bool bmn, bool mc, const CUtensorMap* ta, const CUtensorMap* tb,
+cudaError_t dispatch_major(bool amn, bool bmn, int cl, const CUtensorMap* ta, const CUtensorMap* tb,
                            const GemmArgs& a, cudaStream_t s) {
   if constexpr (BN >= 128) {
-    if (mc) {
-      if (!amn && !bmn) return launch<BN, false, false, true>(ta, tb, a, s);
-      if (!amn && bmn) return launch<BN, false, true, true>(ta, tb, a, s);
-      if (amn && !bmn) return launch<BN, true, false, true>(ta, tb, a, s);
-      return launch<BN, true, true, true>(ta, tb, a, s);
-    }
+    if (cl == 4) return dispatch_cl<BN, 4>(amn, bmn, ta, tb, a, s);
+    if (cl == 2) return dispatch_cl<BN, 2>(amn, bmn, ta, tb, a, s);
   }
-  if (!amn && !bmn) return launch<BN, false, false, false>(ta, tb, a, s);
-  if (!amn && bmn) return launch<BN, false, true, false>(ta, tb, a, s);
-  if (amn && !bmn) return launch<BN, true, false, false>(ta, tb, a, s);
-  return launch<BN, true, true, false>(ta, tb, a, s);
+  return dispatch_cl<BN, 1>(amn, bmn, ta, tb, a, s);
 }
 
 bool seg_ok(int64_t len) { return len % 64 == 0 && len > 0; }
@@ -465,13 +492,17 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
     args.dbg = dbg_dev;
   }
   args.kind = kind == GemmGroup::kMConcat ? 1 : 0;
-  // 2-CTA clusters with B multicast when there are at least two m-blocks and B splits into halves
-  // (UPIPE_GEMM_MC=0 disables; kept for A/B measurements)
-  static const bool mc_env = [] {
+  // Clusters with operand multicast (UPIPE_GEMM_MC caps the cluster size: 1, 2 or 4; default 4):
+  // 2 CTAs share B (two m-blocks, same n-block); 4 CTAs (2 x 2) also share A. Needs BN >= 128 (B, A
+  // split into 64-row halves), two or more m-blocks, and for 4 an even number of n-blocks.
+  static const int mc_env = [] {
     const char* e = getenv("UPIPE_GEMM_MC");
-    return !(e && e[0] == '0');
+    return e ? atoi(e) : 4;
   }();
-  const bool mc = mc_env && bn >= 128 && M > BM;
+  const int ntn_all = (int)(p0.N / bn);
+  int cl = 1;
+  if (bn >= 128 && M > BM && mc_env >= 2) cl = (mc_env >= 4 && ntn_all % 2 == 0) ? 4 : 2;
+  const bool mc = cl > 1;
   // TMA box rows: a K-major operand tile (rows x 64 k) goes in one box when its rows never cross an
   // operand segment (fewer, larger TMA requests); MN-major tiles stay 64 x 64 granules (128B swizzle
   // caps the inner box at 64 elements).
@@ -483,7 +514,7 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
     }
     return gr;
   };
-  const int a_g = box_g(true, BM), b_g = box_g(false, mc ? bn / 2 : bn);
+  const int a_g = box_g(true, cl == 4 ? BM / 2 : BM), b_g = box_g(false, mc ? bn / 2 : bn);
   args.a_box_g = a_g;
   args.b_box_g = b_g;
   CUtensorMap ta[kMaxParts], tb[kMaxParts];
@@ -517,16 +548,16 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
   args.kcum[kMaxParts] = (int)kc;
   args.mcum[kMaxParts] = (int)mrow;
   cudaError_t e;
-  if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, mc, ta, tb, args, stream);
-  else if (bn == 128) e = dispatch_major<128>(p0.a.mn_major, p0.b.mn_major, mc, ta, tb, args, stream);
-  else e = dispatch_major<64>(p0.a.mn_major, p0.b.mn_major, false, ta, tb, args, stream);
+  if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, cl, ta, tb, args, stream);
+  else if (bn == 128) e = dispatch_major<128>(p0.a.mn_major, p0.b.mn_major, cl, ta, tb, args, stream);
+  else e = dispatch_major<64>(p0.a.mn_major, p0.b.mn_major, 1, ta, tb, args, stream);
   if (e != cudaSuccess) snprintf(err, errlen, "gemm launch: %s", cudaGetErrorString(e));
   if (args.dbg) {
     long long h[8];
     cudaMemcpyAsync(h, args.dbg, sizeof h, cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
     fprintf(stderr, "[gemm timeline CTA 0] M=%d N=%d K=%d BN=%d mc=%d tiles=%lld: producer wait_empty %lld | mma wait_full %lld "
-            "wait_acc_empty %lld total %lld cycles\n", args.M, args.N, args.K, bn, (int)mc, h[4], h[0], h[1], h[2], h[3]);
+            "wait_acc_empty %lld total %lld cycles\n", args.M, args.N, args.K, bn, cl, h[4], h[0], h[1], h[2], h[3]);
   }
   return e;
 }
