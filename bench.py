@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--seq", type=int, default=131072, help="global sequence length S")
     ap.add_argument("--chunk", type=int, default=8, help="chunk_heads U (UPipe); Ulysses = 32")
+    ap.add_argument("--naive-kv", action="store_true",
+                    help="ablation (SURVEY N1): re-send K/V every stage instead of once per GQA super-stage")
     ap.add_argument("--model", choices=sorted(MODELS), default="llama3-8b",
                     help="layer shape (default: BASELINE's headline Llama3-8B layer)")
     ap.add_argument("--no-ulysses", action="store_true", help="skip the chunk=all-heads Ulysses comparison")
@@ -246,7 +248,7 @@ def main():
     def run(chunk, steps, warmup, trace=False):
         torch.cuda.synchronize()
         base = torch.cuda.memory_allocated()       # inputs and weights only: workspace + outputs count as activation
-        attn = UPipeAttention(Hq, Hkv, d, D, chunk, True, process_group=pg)
+        attn = UPipeAttention(Hq, Hkv, d, D, chunk, True, process_group=pg, naive_kv=args.naive_kv)
         out = {}
 
         def step():
@@ -321,6 +323,7 @@ def main():
                    "model": M["name"],
                    "n_q_heads": Hq, "n_kv_heads": Hkv, "head_dim": d, "hidden": D, "seq_len": S, "global_batch": 1,
                    "chunk_heads": U, "cp": C, "parallelism": f"cp{C} (UPipe, U={U})",
+                   "kv_schedule": "naive (per-stage K/V resend)" if args.naive_kv else "GQA super-stage (P:362-380)",
                    "l2": f"inputs larger than L2 (x, dy: S_l x {D} bf16 per rank); no flush needed"},
         "tokens_per_s_per_gpu": tok_s / world,
         "gpu_launches": main_run["launches"],

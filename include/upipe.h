@@ -89,6 +89,8 @@ typedef struct {
 /* flags for upipe_init / upipe_init_local */
 #define UPIPE_FLAG_NONE 0u
 #define UPIPE_FLAG_SYNC_COMM 1u /* sequential schedule: collectives on the compute stream, one buffer set */
+#define UPIPE_FLAG_NAIVE_KV 2u  /* ablation: re-project and re-send the stage's K/V heads at every
+                                   stage instead of once per GQA super-stage ("naive" volume) */
 
 /* ---------------------------------------------------------------- lifecycle */
 

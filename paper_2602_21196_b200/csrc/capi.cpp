@@ -183,7 +183,8 @@ upipe_status_t upipe_attn_fwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "null tensor pointer");
   if (!all_aligned(x, wq, wk, wv, wo, y, o_saved, lse_saved) || (reinterpret_cast<uintptr_t>(workspace) & 255))
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "tensors must be 16-byte aligned, workspace 256-byte aligned");
-  const Plan P = make_plan(ctx->C, *shape);
+  Plan P = make_plan(ctx->C, *shape);
+  P.naive = (ctx->flags & UPIPE_FLAG_NAIVE_KV) != 0;
   if (ws_bytes < fwd_workspace(P, overlap_enabled(ctx->flags, ctx->C)).total)
     return set_err(ctx, UPIPE_ERR_WORKSPACE, "ws_bytes < upipe_workspace_size(pass=0, or 2 with UPIPE_FLAG_SYNC_COMM)");
   cudaSetDevice(ctx->device);
@@ -205,7 +206,8 @@ upipe_status_t upipe_attn_bwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
   if (!all_aligned(x, wq, wk, wv, wo, dy, o_saved, lse_saved, dx, dwq, dwk, dwv, dwo) ||
       (reinterpret_cast<uintptr_t>(workspace) & 255))
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "tensors must be 16-byte aligned, workspace 256-byte aligned");
-  const Plan P = make_plan(ctx->C, *shape);
+  Plan P = make_plan(ctx->C, *shape);
+  P.naive = (ctx->flags & UPIPE_FLAG_NAIVE_KV) != 0;
   if (ws_bytes < bwd_workspace(P, overlap_enabled(ctx->flags, ctx->C)).total)
     return set_err(ctx, UPIPE_ERR_WORKSPACE, "ws_bytes < upipe_workspace_size(pass=1, or 3 with UPIPE_FLAG_SYNC_COMM)");
   cudaSetDevice(ctx->device);

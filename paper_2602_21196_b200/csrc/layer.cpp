@@ -152,7 +152,7 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   const int64_t HqD = (int64_t)P.Hq * d, kvrows = (int64_t)P.Hkv * d;
   const size_t qbytes = (size_t)P.S_l * qseg * 2, kbytes = (size_t)P.S_l * kseg * 2;
   const int64_t qstep = (int64_t)P.q_dev_stride() * d;
-  auto kvb = [&](int s) { return ov ? (s / P.sigma) & 1 : 0; };
+  auto kvb = [&](int s) { return ov ? P.kv_group(s) & 1 : 0; };
 
   // F1: Q_s (and K_s, V_s at a super-stage start) -> send buffer set b
   auto proj = [&](int s, int b, cudaStream_t q) {
@@ -302,7 +302,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   const size_t qbytes = (size_t)P.S_l * qseg * 2, kbytes = (size_t)P.S_l * kseg * 2;
   const size_t dbytes = (size_t)P.S_l * P.qpd * 4;
   const int64_t qstep = (int64_t)P.q_dev_stride() * d;
-  auto kvb = [&](int s) { return ov ? (s / P.sigma) & 1 : 0; };
+  auto kvb = [&](int s) { return ov ? P.kv_group(s) & 1 : 0; };
 
   // dWo = dY^T O over this rank's tokens (all stages at once: o_saved holds every head)
   {
@@ -416,7 +416,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     R.run(UPIPE_TRACE_AUX, q, "memset dQ", [&](char*) {
       return cudaMemsetAsync(ws + W.dqacc[b], 0, (size_t)P.S * qseg * 4, q);
     });
-    const int r = s % P.sigma;
+    const int r = P.kv_pos(s);
     const bool last = P.kv_last(s);
     AttnBwdProblem bp{};
     bp.q = ws + W.qrecv[b];
@@ -426,8 +426,8 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     bp.lse = lse_saved + (int64_t)s * P.qpd * P.S;
     bp.delta = (const float*)(ws + W.drecv[b]);
     bp.dq_acc = (float*)(ws + W.dqacc[b]);
-    bp.dk_acc = P.sigma > 1 ? (float*)(ws + W.dkacc) : nullptr;
-    bp.dv_acc = P.sigma > 1 ? (float*)(ws + W.dvacc) : nullptr;
+    bp.dk_acc = P.sigma > 1 && !P.naive ? (float*)(ws + W.dkacc) : nullptr;
+    bp.dv_acc = P.sigma > 1 && !P.naive ? (float*)(ws + W.dvacc) : nullptr;
     bp.dk_bf16 = last ? ws + W.dksend : nullptr;
     bp.dv_bf16 = last ? ws + W.dvsend : nullptr;
     bp.S = P.S;
@@ -470,6 +470,8 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       gx[2] = dx_gemm(ws + W.dvrecv, kseg, wv, HkvD, kv0 * d, kseg);
       gw[1] = dw_gemm(ws + W.dkrecv, kseg, dwk, kv0 * d, kseg);
       gw[2] = dw_gemm(ws + W.dvrecv, kseg, dwv, kv0 * d, kseg);
+      if (P.naive && s % P.sigma != 0)      // naive schedule: later stages of a group add their partial dK/dV
+        gw[1].c.epi = gw[2].c.epi = Epi::kAccF32;
       n = 3;
     }
     dx_epi(gx[0]);

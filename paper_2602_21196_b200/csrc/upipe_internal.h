@@ -26,8 +26,13 @@ struct Plan {
   // [(b*C + p)*kv_res, +kv_res) and q heads [kv0*R + r*qpd, +qpd).
   int kv0(int s, int p) const { return ((s / sigma) * C + p) * kv_res; }
   int q0(int s, int p) const { return kv0(s, p) * R + (s % sigma) * qpd; }
-  bool kv_sent(int s) const { return (s % sigma) == 0; }
-  bool kv_last(int s) const { return (s % sigma) == sigma - 1; }
+  // naive (UPIPE_FLAG_NAIVE_KV): every stage re-projects and re-sends the K/V heads its
+  // queries read, and sends their gradients back at once (no super-stage reuse)
+  bool naive = false;
+  bool kv_sent(int s) const { return naive || (s % sigma) == 0; }
+  bool kv_last(int s) const { return naive || (s % sigma) == sigma - 1; }
+  int kv_group(int s) const { return naive ? s : s / sigma; }   // stages sharing one K/V receive buffer
+  int kv_pos(int s) const { return naive ? 0 : s % sigma; }     // position within that group
   // per-device step of the first q head / kv head between consecutive devices (same for every s)
   int q_dev_stride() const { return kv_res * R; }
   int kv_dev_stride() const { return kv_res; }

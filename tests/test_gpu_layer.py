@@ -17,7 +17,8 @@ pytestmark = pytest.mark.gpu
 REL, ABS = 5e-3, 2e-2
 
 
-def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", bwd=True, sync=False, exp_S=None):
+def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", bwd=True, sync=False, exp_S=None,
+               naive=False, comm_counts=None):
     """Run the layer on C ranks; returns (per-rank outputs, inputs). exp_S: draw the first S tokens of
     a length-exp_S sequence (its value scales), e.g. to keep dY's 1/sqrt(S) scale sane for tiny S."""
     from paper_2602_21196_b200 import UPipeAttention, upipe
@@ -40,10 +41,16 @@ def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", b
             with torch.cuda.stream(stream):
                 if C > 1:
                     attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal, fabric=fabric, cp_rank=r, cp_size=C,
-                                          sync_comm=sync)
+                                          sync_comm=sync, naive_kv=naive)
                 else:
-                    attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal)
+                    attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal, naive_kv=naive)
+                if comm_counts is not None:
+                    upipe.upipe_set_trace(attn.ctx, True)
                 y, saved = attn.forward(xs[r], W["wq"], W["wk"], W["wv"], W["wo"])
+                if comm_counts is not None:
+                    stream.synchronize()
+                    comm_counts[r] = upipe.upipe_trace_read(attn.ctx)["comm"][1]
+                    upipe.upipe_set_trace(attn.ctx, False)
                 out = {"y": y, "o": saved[0], "lse": saved[1]}
                 if bwd:
                     dx, dwq, dwk, dwv, dwo = attn.backward(xs[r], W["wq"], W["wk"], W["wv"], W["wo"], dys[r], saved)
@@ -193,3 +200,27 @@ def test_mha_one_kv_head_per_q_head():
     # Hkv = Hq (MHA, R = 1): every stage sends its own K/V heads (Fig. 3b schedule)
     r, inp = _run_group(2, 256, 256, 4, 4, 64, 2)
     _check(r, inp, 2, 4, 4, 64, 2)
+
+
+@pytest.mark.parametrize("sync", [False, True])
+def test_naive_kv_schedule_ablation(sync):
+    # UPIPE_FLAG_NAIVE_KV re-sends each stage's K/V heads instead of once per GQA
+    # super-stage. Forward outputs are bitwise those of the scheduled run; the backward sends partial
+    # dK/dV every stage (summed by the dX / dW GEMMs) and meets the bar; the forward's all-to-all
+    # head-slice volume matches P:373 (naive) and P:380 (scheduled).
+    C, S, D, Hq, Hkv, d, Uc = 2, 256, 256, 8, 2, 64, 2      # qpd = 1, R = 4: one super-stage of 4 stages
+    counts_s, counts_n = [0] * C, [0] * C
+    rs, _ = _run_group(C, S, D, Hq, Hkv, d, Uc, sync=sync, comm_counts=counts_s)
+    rn, inp = _run_group(C, S, D, Hq, Hkv, d, Uc, sync=sync, naive=True, comm_counts=counts_n)
+    for p in range(C):
+        for k in ("y", "o", "lse"):
+            assert torch.equal(rs[p][k], rn[p][k]), k
+    _check(rn, inp, C, Hq, Hkv, d, Uc)
+    nu, qpd = Hq // Uc, Uc // C
+    # fwd collectives per rank: Q + O per stage, K and V per super-stage (scheduled) or per stage (naive)
+    assert counts_s == [2 * nu + 2 * 1] * C and counts_n == [4 * nu] * C
+    # head-slices each device sends (kv_res = 1 K/V head per stage and device here)
+    vol_s = (nu * qpd + 2 * 1) * (C - 1)
+    vol_n = (nu * qpd + 2 * nu) * (C - 1)
+    assert vol_s == oracle.comm_volume_formula(Hq, Hkv, C, scheduled=True)
+    assert vol_n == oracle.comm_volume_formula(Hq, Hkv, C, scheduled=False)
