@@ -32,6 +32,10 @@ Functions and their pins (tests/test_oracle_*.py):
 * ``upipe_forward/backward`` (sharded simulation) -- pinned: equal to the
                        un-sharded oracle for every (C, U) (method exactness).
 * ``memory_*``      -- pinned: §3.4 numbers (96 -> 12 S d_head, 87.5 %).
+* ``rope``          -- pinned: complex-exponential form (each pair times e^{i p theta_i}),
+                       relative-position invariance of q.k, norm preservation, position 0 =
+                       identity, inverse o forward = identity; the RoPE layer's gradients by
+                       central finite differences.
 """
 from __future__ import annotations
 
@@ -153,28 +157,60 @@ def project(X, W):
 # ----------------------------------------------------------------------------
 
 
-def layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, causal=True):
-    """Y = O Wo^T with O = attn(X Wq^T, X Wk^T, X Wv^T).  Returns (Y, O [S,Hq*d], lse [Hq,S])."""
+def rope(T, positions, base, inverse=False):
+    """Rotary position embedding (the paper's RoPE) in the original
+    interleaved-pair form (RoFormer; Llama's reference ``apply_rotary_emb``): head-dim pairs
+    (2i, 2i+1), i < d/2, of the token at position p are rotated by the angle
+    p * base**(-2i/d):  (a, b) -> (a cos - b sin, a sin + b cos).  ``inverse`` rotates by the
+    negative angle (the transpose), which maps gradients w.r.t. rotated Q/K back (DESIGN A26).
+    T: [S, H, d]; positions: [S] (global token index)."""
+    d = T.shape[-1]
+    i = np.arange(d // 2, dtype=np.float64)
+    ang = np.asarray(positions, dtype=np.float64)[:, None] * base ** (-2.0 * i / d)   # [S, d/2]
+    c, s = np.cos(ang)[:, None, :], np.sin(ang)[:, None, :]
+    if inverse:
+        s = -s
+    a, b = T[..., 0::2], T[..., 1::2]
+    out = np.empty_like(T, dtype=np.float64)
+    out[..., 0::2] = a * c - b * s
+    out[..., 1::2] = a * s + b * c
+    return out
+
+
+def _qkv(X, Wq, Wk, Wv, Hq, Hkv, d, rope_base, pos0=0):
     S = X.shape[0]
     Q = (X @ Wq.T).reshape(S, Hq, d)
     K = (X @ Wk.T).reshape(S, Hkv, d)
     V = (X @ Wv.T).reshape(S, Hkv, d)
+    if rope_base:
+        pos = np.arange(pos0, pos0 + S)
+        Q, K = rope(Q, pos, rope_base), rope(K, pos, rope_base)
+    return Q, K, V
+
+
+def layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, causal=True, rope_base=None):
+    """Y = O Wo^T with O = attn(X Wq^T, X Wk^T, X Wv^T) (Q and K rotated by ``rope`` at their
+    token positions when ``rope_base`` is given).  Returns (Y, O [S,Hq*d], lse [Hq,S])."""
+    S = X.shape[0]
+    Q, K, V = _qkv(X, Wq, Wk, Wv, Hq, Hkv, d, rope_base)
     O, lse = attn_fwd(Q, K, V, causal)
     O2 = O.reshape(S, Hq * d)
     return O2 @ Wo.T, O2, lse
 
 
-def layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, causal=True):
-    """(dX, dWq, dWk, dWv, dWo) of the layer for cotangent dY."""
+def layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, causal=True, rope_base=None):
+    """(dX, dWq, dWk, dWv, dWo) of the layer for cotangent dY; with RoPE the
+    gradients w.r.t. the rotated Q/K are rotated back (chain rule through an orthogonal map)."""
     S = X.shape[0]
-    Q = (X @ Wq.T).reshape(S, Hq, d)
-    K = (X @ Wk.T).reshape(S, Hkv, d)
-    V = (X @ Wv.T).reshape(S, Hkv, d)
+    Q, K, V = _qkv(X, Wq, Wk, Wv, Hq, Hkv, d, rope_base)
     O, _ = attn_fwd(Q, K, V, causal)
     O2 = O.reshape(S, Hq * d)
     dWo = dY.T @ O2
     dO = (dY @ Wo).reshape(S, Hq, d)
     dQ, dK, dV = attn_bwd(Q, K, V, dO, causal)
+    if rope_base:
+        pos = np.arange(S)
+        dQ, dK = rope(dQ, pos, rope_base, inverse=True), rope(dK, pos, rope_base, inverse=True)
     dQ2, dK2, dV2 = dQ.reshape(S, -1), dK.reshape(S, -1), dV.reshape(S, -1)
     dWq = dQ2.T @ X
     dWk = dK2.T @ X

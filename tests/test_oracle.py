@@ -219,6 +219,60 @@ def test_layer_finite_differences():
         assert np.linalg.norm(num - g) <= 1e-6 * np.linalg.norm(g)
 
 
+# ---------------------------------------------------------------- RoPE (DESIGN A26)
+
+def test_rope_is_complex_rotation():
+    # each pair (2i, 2i+1) is the complex number a + ib multiplied by exp(1j * p * base**(-2i/d))
+    S, H, d, base = 7, 3, 8, 10000.0
+    T = rand(S, H, d)
+    pos = np.array([0, 1, 2, 5, 100, 4096, 131071])
+    got = O.rope(T, pos, base)
+    z = T[..., 0::2] + 1j * T[..., 1::2]
+    theta = np.array([base ** (-2.0 * i / d) for i in range(d // 2)])
+    w = z * np.exp(1j * pos[:, None, None] * theta[None, None, :])
+    np.testing.assert_allclose(got[..., 0::2], w.real, atol=1e-12)
+    np.testing.assert_allclose(got[..., 1::2], w.imag, atol=1e-12)
+
+
+def test_rope_relative_position_norm_identity_inverse():
+    d, base = 16, 500000.0
+    q, k = rand(1, 1, d), rand(1, 1, d)
+    def dot(m, n):
+        return float(np.sum(O.rope(q, [m], base) * O.rope(k, [n], base)))
+    # q_m . k_n depends on m - n only
+    for m, n, t in ((5, 2, 7), (100, 100, 1000), (1 << 20, 3, 12345)):
+        assert abs(dot(m, n) - dot(m + t, n + t)) < 1e-9
+    T = rand(9, 2, d)
+    pos = np.arange(9) * 1000
+    R = O.rope(T, pos, base)
+    np.testing.assert_allclose(np.linalg.norm(R, axis=-1), np.linalg.norm(T, axis=-1), rtol=1e-12)
+    np.testing.assert_allclose(O.rope(T, np.zeros(9), base), T, atol=0)
+    np.testing.assert_allclose(O.rope(R, pos, base, inverse=True), T, atol=1e-12)
+
+
+def test_rope_layer_finite_differences():
+    S, D, Hq, Hkv, d, base = 6, 5, 2, 1, 4, 100.0
+    X, Wq, Wk, Wv, Wo, dY = (rand(S, D), rand(Hq * d, D), rand(Hkv * d, D), rand(Hkv * d, D),
+                             rand(D, Hq * d), rand(S, D))
+    grads = O.layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, rope_base=base)
+    args = [X, Wq, Wk, Wv, Wo]
+    h = 1e-5
+
+    def loss(a):
+        return float(np.sum(O.layer_fwd(*a, Hq, Hkv, d, rope_base=base)[0] * dY))
+    for idx, g in enumerate(grads):
+        num = np.zeros_like(args[idx])
+        for i in np.ndindex(num.shape):
+            ap = [a.copy() for a in args]
+            am = [a.copy() for a in args]
+            ap[idx][i] += h
+            am[idx][i] -= h
+            num[i] = (loss(ap) - loss(am)) / (2 * h)
+        assert np.linalg.norm(num - g) <= 1e-6 * np.linalg.norm(g)
+    # and RoPE changes the layer (the rotation is not silently skipped)
+    assert not np.allclose(O.layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d)[0], O.layer_fwd(*args, Hq, Hkv, d, rope_base=base)[0])
+
+
 def test_output_projection_stage_decomposition():
     # sum over stages of O_s Wo_s^T equals O Wo^T (the accumulated output projection)
     S, D, Hq, d, U = 30, 16, 8, 4, 2
