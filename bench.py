@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--seq", type=int, default=131072, help="global sequence length S")
     ap.add_argument("--chunk", type=int, default=8, help="chunk_heads U (UPipe); Ulysses = 32")
+    ap.add_argument("--rope-base", type=float, default=0.0,
+                    help="RoPE on Q/K with this base (Llama3: 500000; SURVEY N3); 0 = off (north_star layer)")
     ap.add_argument("--naive-kv", action="store_true",
                     help="ablation (SURVEY N1): re-send K/V every stage instead of once per GQA super-stage")
     ap.add_argument("--model", choices=sorted(MODELS), default="llama3-8b",
@@ -248,7 +250,8 @@ def main():
     def run(chunk, steps, warmup, trace=False):
         torch.cuda.synchronize()
         base = torch.cuda.memory_allocated()       # inputs and weights only: workspace + outputs count as activation
-        attn = UPipeAttention(Hq, Hkv, d, D, chunk, True, process_group=pg, naive_kv=args.naive_kv)
+        attn = UPipeAttention(Hq, Hkv, d, D, chunk, True, process_group=pg, naive_kv=args.naive_kv,
+                              rope_base=args.rope_base)
         out = {}
 
         def step():
@@ -262,7 +265,7 @@ def main():
         torch.cuda.reset_peak_memory_stats()
         step()
         torch.cuda.synchronize()
-        out["peak_bytes"] = torch.cuda.max_memory_allocated() - base
+        out["peak_bytes"] = max_over_ranks(torch.cuda.max_memory_allocated() - base)   # max over ranks
         out["ws_bytes"] = sum(t.numel() for t in attn._ws.values())
         # chunk buffers = workspace minus the U-independent fp32 dX accumulator [S_l, D] (only allocated
         # when there is more than one stage): the "intermediate tensors" of P:332-343 (DESIGN A21)
@@ -324,6 +327,7 @@ def main():
                    "n_q_heads": Hq, "n_kv_heads": Hkv, "head_dim": d, "hidden": D, "seq_len": S, "global_batch": 1,
                    "chunk_heads": U, "cp": C, "parallelism": f"cp{C} (UPipe, U={U})",
                    "kv_schedule": "naive (per-stage K/V resend)" if args.naive_kv else "GQA super-stage (P:362-380)",
+                   "rope_base": args.rope_base,
                    "l2": f"inputs larger than L2 (x, dy: S_l x {D} bf16 per rank); no flush needed"},
         "tokens_per_s_per_gpu": tok_s / world,
         "gpu_launches": main_run["launches"],

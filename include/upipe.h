@@ -82,6 +82,9 @@ typedef struct {
   int32_t head_dim;    /* d in {64, 128} */
   int32_t chunk_heads; /* U: heads per stage; U % C == 0; Hq % U == 0; U/C and Hq/Hkv divide one another (A8) */
   int32_t causal;      /* 1: causal mask (the paper's setting); 0: full attention */
+  float rope_base;     /* 0: no rotary embedding; > 1: RoPE on Q and K at their global token positions
+                          with angles p * rope_base^(-2i/d) on head-dim pairs (2i, 2i+1) (P:241,
+                          SURVEY N3, DESIGN A26; Llama3: 500000). The ctx keeps the rotation tables. */
 } upipe_shape_t;
 
 #define UPIPE_UID_BYTES 128

@@ -48,6 +48,7 @@ struct BwdArgs {
   int nq, nkv, causal, kv_accumulate, kv_write_acc;
   float scale;       // 1/sqrt(d)
   float scale_log2;  // log2(e)/sqrt(d)
+  RopeRef rope;      // dK (bf16 output) rotated back by -angle(key) when set (RoPE on K, DESIGN A26)
   long long* dbg;    // optional per-role cycle breakdown of CTA (0,0) (UPIPE_BWD_TIMELINE=1)
 };
 
@@ -416,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 8; ++i) accp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
       }
       if (ob) {
+        if (which && a.rope.hi) rope_rotate<16>(v, a.rope.hi, a.rope.lo, D, a.rope.pos0 + key, c, -1.f);
         uint4* dst = reinterpret_cast<uint4*>(ob + key * a.ld_kvb + (long long)g * D + c);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -521,6 +523,7 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   a.kv_write_acc = p.kv_write_acc;
   a.scale = 1.f / sqrtf((float)p.d);
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)p.d);
+  a.rope = p.rope;
   // UPIPE_BWD_TIMELINE=1: per-role cycle breakdown of CTA (0,0), printed to stderr after the launch
   static long long* dbg_dev = nullptr;
   const char* tlenv = getenv("UPIPE_BWD_TIMELINE");

@@ -32,6 +32,7 @@ struct DevOut {
   long long r_base, m_len, r_mstride, r_nstride;
   long long c_base, n_len, c_nstride, c_mstride;
   int epi;
+  RopeRef rope;
 };
 constexpr int kMaxParts = 3;
 struct GemmArgs {
@@ -314,6 +315,8 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]) * g.alpha;
         if (oc_.epi == (int)Epi::kStoreBF16) {
+          // RoPE on the projected Q/K (row m = token pos0 + m, columns n.. = head dims n % d..)
+          if (oc_.rope.hi) rope_rotate<16>(v, oc_.rope.hi, oc_.rope.lo, oc_.rope.d, oc_.rope.pos0 + m, n % oc_.rope.d, 1.f);
           uint4* dst = reinterpret_cast<uint4*>(oc_.bf16 + orow * oc_.ld_bf16 + ocol);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
@@ -426,7 +429,8 @@ bool seg_ok(int64_t len) { return len % 64 == 0 && len > 0; }
 
 DevOut to_dev(const OutMap& c) {
   return DevOut{reinterpret_cast<float*>(c.out_f32), reinterpret_cast<__nv_bfloat16*>(c.out_bf16), c.ld_f32, c.ld_bf16,
-                c.r_base, c.m_len, c.r_mstride, c.r_nstride, c.c_base, c.n_len, c.c_nstride, c.c_mstride, (int)c.epi};
+                c.r_base, c.m_len, c.r_mstride, c.r_nstride, c.c_base, c.n_len, c.c_nstride, c.c_mstride, (int)c.epi,
+                c.rope};
 }
 
 }  // namespace

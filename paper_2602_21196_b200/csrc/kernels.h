@@ -39,6 +39,17 @@ enum class Epi : int {
   kAccF32 = 2,        // out_f32 += acc
   kAccF32ToBF16 = 3,  // out_bf16 = bf16(out_f32 + acc)   (last accumulation step)
 };
+// RoPE rotation tables (DESIGN A26), built once per (base, d, S) by the library in double precision:
+//   hi[h][i] = (cos, sin)(h * 1024 * f_i mod 2pi),  lo[l][i] = (cos, sin)(l * f_i),  f_i = base^(-2i/d),
+// so the angle of position p = 1024 h + l is composed exactly by one complex product (fp32 tables;
+// an fp32 angle p * f_i would lose ~0.1 rad at p ~ 1e6).
+struct RopeRef {
+  const float2* hi = nullptr;   // null: no rotation
+  const float2* lo = nullptr;
+  int d = 0;                    // head_dim; pair index i = (column % d) / 2
+  int64_t pos0 = 0;             // position of row 0
+};
+
 struct OutMap {
   void* out_f32 = nullptr;
   void* out_bf16 = nullptr;
@@ -46,6 +57,7 @@ struct OutMap {
   int64_t r_base = 0, m_len = 1 << 30, r_mstride = 0, r_nstride = 0;
   int64_t c_base = 0, n_len = 1 << 30, c_nstride = 0, c_mstride = 0;
   Epi epi = Epi::kStoreBF16;
+  RopeRef rope;                 // kStoreBF16 only: rotate column pairs by the row's position first
 };
 
 struct GemmProblem {
@@ -95,6 +107,7 @@ struct AttnBwdProblem {
   int64_t ldq, ldkv, ldo_grad, ld_lse, ld_delta, ld_kvb;
   int kv_accumulate;                          // 1: add the previous dk_acc/dv_acc contents
   int kv_write_acc;                           // 1: write fp32 accumulators back
+  RopeRef rope;                               // dk_bf16 is rotated back by -angle(key) (RoPE on K)
 };
 cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err, size_t errlen);
 
@@ -103,6 +116,8 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
 cudaError_t rowdot_run(const void* dO, int64_t ld_do, const void* O, int64_t ld_o, float* delta, int64_t ld_delta,
                        int64_t rows, int nheads, int d, cudaStream_t s);
 // bf16 = bf16(scale * f32) elementwise over a [rows][cols] block with strides.
+cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
+                             float scale, cudaStream_t s, const RopeRef& inverse_rope);
 cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
                              float scale, cudaStream_t s);
 // Column scatter: dst[t][col_of(seg)+e] = src[seg][t][e]   (unpack of the out all-to-all)

@@ -13,7 +13,9 @@
 //    all-to-all over NVLink is overlapped on a side stream with the current chunk's
 //    attention"); the out all-to-all of stage s overlaps attention s+1. Costs a second
 //    buffer set (DESIGN A23). Cross-stream order is carried by CUDA events.
+#include <cmath>
 #include <cstdio>
+#include <vector>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -99,7 +101,7 @@ struct Runner {
 // all-to-all send layout [C][S_l][seg] (pack fused into the GEMM epilogue).
 //   W rows of device p's heads start at row0 + p * row_step; seg = heads_per_device * d.
 GemmProblem proj_to_send(const Plan& P, const void* x, const void* W, int64_t W_rows, int64_t row0,
-                         int64_t row_step, int64_t seg, void* send) {
+                         int64_t row_step, int64_t seg, void* send, const RopeRef& rope = RopeRef{}) {
   GemmProblem g;
   g.M = P.S_l;
   g.N = (int64_t)P.C * seg;
@@ -114,7 +116,50 @@ GemmProblem proj_to_send(const Plan& P, const void* x, const void* W, int64_t W_
   g.c.n_len = seg;
   g.c.r_nstride = P.S_l;
   g.c.epi = Epi::kStoreBF16;
+  g.c.rope = rope;                       // Q/K: rotary embedding at the tokens' global positions
   return g;
+}
+
+// RoPE tables for angles p * base^(-2i/d), p < S (DESIGN A26): computed in double on the host once.
+upipe_status_t ensure_rope(upipe_ctx_s* ctx, const Plan& P, RopeRef& ref) {
+  ref = RopeRef{};
+  if (P.sh.rope_base == 0.f) return UPIPE_OK;
+  RopeTables& T = ctx->rope;
+  const int64_t n_hi = (P.S + 1023) / 1024;
+  if (T.base != P.sh.rope_base || T.d != P.d || T.n_hi < n_hi) {
+    if (T.hi) cudaFree(T.hi);
+    if (T.lo) cudaFree(T.lo);
+    T.hi = T.lo = nullptr;
+    const int h2 = P.d / 2;
+    std::vector<float2> hi((size_t)n_hi * h2), lo((size_t)1024 * h2);
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int i = 0; i < h2; ++i) {
+      const double f = std::pow((double)P.sh.rope_base, -2.0 * i / P.d);
+      for (int64_t h = 0; h < n_hi; ++h) {
+        const double a = std::fmod((double)h * 1024.0 * f, two_pi);
+        hi[(size_t)h * h2 + i] = make_float2((float)std::cos(a), (float)std::sin(a));
+      }
+      for (int l = 0; l < 1024; ++l) {
+        const double a = (double)l * f;
+        lo[(size_t)l * h2 + i] = make_float2((float)std::cos(a), (float)std::sin(a));
+      }
+    }
+    if (cudaMalloc(&T.hi, hi.size() * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&T.lo, lo.size() * sizeof(float2)) != cudaSuccess ||
+        cudaMemcpy(T.hi, hi.data(), hi.size() * sizeof(float2), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(T.lo, lo.data(), lo.size() * sizeof(float2), cudaMemcpyHostToDevice) != cudaSuccess) {
+      ctx->last_error = "cannot build the RoPE tables";
+      return UPIPE_ERR_CUDA;
+    }
+    T.base = P.sh.rope_base;
+    T.d = P.d;
+    T.n_hi = n_hi;
+  }
+  ref.hi = T.hi;
+  ref.lo = T.lo;
+  ref.d = P.d;
+  ref.pos0 = 0;
+  return UPIPE_OK;
 }
 
 upipe_status_t ensure_pipe(upipe_ctx_s* ctx) {
@@ -147,6 +192,9 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   Runner R{ctx};
   Transport& T = *ctx->transport;
   const FwdWs W = fwd_workspace(P, ov);
+  RopeRef rope_seq;                        // projections: rows are this rank's tokens me*S_l + t
+  if (upipe_status_t s = ensure_rope(ctx, P, rope_seq)) return s;
+  rope_seq.pos0 = (int64_t)ctx->rank * P.S_l;
   const int C = P.C, me = ctx->rank, d = P.d;
   const int64_t qseg = (int64_t)P.qpd * d, kseg = (int64_t)P.kv_res * d;
   const int64_t HqD = (int64_t)P.Hq * d, kvrows = (int64_t)P.Hkv * d;
@@ -158,11 +206,11 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   auto proj = [&](int s, int b, cudaStream_t q) {
     const int64_t q0 = P.q0(s, 0), kv0 = P.kv0(s, 0);
     R.run(UPIPE_TRACE_GEMM, q, "proj Q", [&](char* e) {
-      return gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend[b]), q, e, 512);
+      return gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend[b], rope_seq), q, e, 512);
     });
     if (P.kv_sent(s)) {
       R.run(UPIPE_TRACE_GEMM, q, "proj K", [&](char* e) {
-        return gemm_run(proj_to_send(P, x, wk, kvrows, kv0 * d, kseg, kseg, ws + W.ksend), q, e, 512);
+        return gemm_run(proj_to_send(P, x, wk, kvrows, kv0 * d, kseg, kseg, ws + W.ksend, rope_seq), q, e, 512);
       });
       R.run(UPIPE_TRACE_GEMM, q, "proj V", [&](char* e) {
         return gemm_run(proj_to_send(P, x, wv, kvrows, kv0 * d, kseg, kseg, ws + W.vsend), q, e, 512);
@@ -296,6 +344,10 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   Runner R{ctx};
   Transport& T = *ctx->transport;
   const BwdWs W = bwd_workspace(P, ov);
+  RopeRef rope_seq, rope_head;             // seq layout (projections) / head layout (rows = global tokens)
+  if (upipe_status_t s = ensure_rope(ctx, P, rope_seq)) return s;
+  rope_head = rope_seq;
+  rope_seq.pos0 = (int64_t)ctx->rank * P.S_l;
   const int C = P.C, d = P.d;
   const int64_t qseg = (int64_t)P.qpd * d, kseg = (int64_t)P.kv_res * d;
   const int64_t HqD = (int64_t)P.Hq * d, HkvD = (int64_t)P.Hkv * d;
@@ -368,11 +420,11 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   auto pre = [&](int s, int b, cudaStream_t q) {
     const int64_t q0 = P.q0(s, 0), kv0 = P.kv0(s, 0);
     R.run(UPIPE_TRACE_GEMM, q, "proj Q", [&](char* e) {
-      return gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend[b]), q, e, 512);
+      return gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend[b], rope_seq), q, e, 512);
     });
     if (P.kv_sent(s)) {
       R.run(UPIPE_TRACE_GEMM, q, "proj K", [&](char* e) {
-        return gemm_run(proj_to_send(P, x, wk, HkvD, kv0 * d, kseg, kseg, ws + W.ksend), q, e, 512);
+        return gemm_run(proj_to_send(P, x, wk, HkvD, kv0 * d, kseg, kseg, ws + W.ksend, rope_seq), q, e, 512);
       });
       R.run(UPIPE_TRACE_GEMM, q, "proj V", [&](char* e) {
         return gemm_run(proj_to_send(P, x, wv, HkvD, kv0 * d, kseg, kseg, ws + W.vsend), q, e, 512);
@@ -443,9 +495,11 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     bp.ld_kvb = kseg;
     bp.kv_accumulate = r > 0;
     bp.kv_write_acc = !last;
+    bp.rope = rope_head;
     R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd", [&](char* e) { return attn_bwd_run(bp, q, e, 512); });
     R.run(UPIPE_TRACE_AUX, q, "cvt dQ", [&](char*) {
-      return cvt_f32_bf16_run((const float*)(ws + W.dqacc[b]), qseg, ws + W.dqsend[b], qseg, P.S, qseg, 1.0f, q);
+      return cvt_f32_bf16_run((const float*)(ws + W.dqacc[b]), qseg, ws + W.dqsend[b], qseg, P.S, qseg, 1.0f, q,
+                              rope_head);
     });
   };
   // B5: dQ head -> seq ("during inp_all_to_all"); dK/dV when the super-stage's K/V retire

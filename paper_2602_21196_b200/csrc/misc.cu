@@ -58,7 +58,7 @@ __global__ void rowdot_kernel(const __nv_bfloat16* __restrict__ dO, long long ld
 }
 
 __global__ void cvt_kernel(const float* __restrict__ src, long long lds, __nv_bfloat16* __restrict__ dst,
-                           long long ldd, long long rows, long long cols, float scale) {
+                           long long ldd, long long rows, long long cols, float scale, RopeRef rope) {
   const long long v8 = cols / 8;
   const long long total = rows * v8;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -66,9 +66,12 @@ __global__ void cvt_kernel(const float* __restrict__ src, long long lds, __nv_bf
     const long long r = i / v8, c = (i % v8) * 8;
     const float4 x = *reinterpret_cast<const float4*>(src + r * lds + c);
     const float4 y = *reinterpret_cast<const float4*>(src + r * lds + c + 4);
+    float v[8] = {x.x * scale, x.y * scale, x.z * scale, x.w * scale, y.x * scale, y.y * scale, y.z * scale, y.w * scale};
+    // row r is token rope.pos0 + r (head layout [S][heads*d]); gradients rotate back by -angle
+    if (rope.hi) dev::rope_rotate<4>(v, rope.hi, rope.lo, rope.d, rope.pos0 + r, (int)(c % rope.d), -1.f);
     *reinterpret_cast<uint4*>(dst + r * ldd + c) =
-        make_uint4(dev::pack_bf16(x.x * scale, x.y * scale), dev::pack_bf16(x.z * scale, x.w * scale),
-                   dev::pack_bf16(y.x * scale, y.y * scale), dev::pack_bf16(y.z * scale, y.w * scale));
+        make_uint4(dev::pack_bf16(v[0], v[1]), dev::pack_bf16(v[2], v[3]), dev::pack_bf16(v[4], v[5]),
+                   dev::pack_bf16(v[6], v[7]));
   }
 }
 
@@ -123,13 +126,18 @@ cudaError_t rowdot_run(const void* dO, int64_t ld_do, const void* O, int64_t ld_
 }
 
 cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
-                             float scale, cudaStream_t s) {
+                             float scale, cudaStream_t s, const RopeRef& inverse_rope) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (cols % 8) return cudaErrorInvalidValue;
   cvt_kernel<<<grid_for(rows * cols / 8, kThreads), kThreads, 0, s>>>(src, lds, (__nv_bfloat16*)dst, ldd, rows,
-                                                                     cols, scale);
+                                                                     cols, scale, inverse_rope);
   count_launches(1);
   return cudaGetLastError();
+}
+
+cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
+                             float scale, cudaStream_t s) {
+  return cvt_f32_bf16_run(src, lds, dst, ldd, rows, cols, scale, s, RopeRef{});
 }
 
 cudaError_t unpack_cols_run(const void* src, int64_t rows, int nseg, int seg_cols, void* dst, int64_t ldd,

@@ -23,6 +23,8 @@ upipe_status_t validate_shape(int C, const upipe_shape_t* sh, std::string& msg) 
   if (sh->chunk_heads % C) return bad(UPIPE_ERR_INVALID_ARG, "chunk_heads % cp_size != 0 (P:317: U must be divisible by C)");
   if (sh->n_q_heads % sh->chunk_heads) return bad(UPIPE_ERR_INVALID_ARG, "n_q_heads % chunk_heads != 0 (H/U stages, P:315)");
   if (sh->causal != 0 && sh->causal != 1) return bad(UPIPE_ERR_INVALID_ARG, "causal must be 0 or 1");
+  if (!(sh->rope_base == 0.f || (sh->rope_base > 1.f && sh->rope_base < 1e30f)))
+    return bad(UPIPE_ERR_INVALID_ARG, "rope_base must be 0 (off) or a finite base > 1 (DESIGN A26)");
   if (sh->head_dim != 64 && sh->head_dim != 128) return bad(UPIPE_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
   if (sh->hidden < 64 || sh->hidden % 64) return bad(UPIPE_ERR_UNSUPPORTED, "hidden % 64 != 0 (TMA tile granule)");
   if (sh->n_kv_heads % C)

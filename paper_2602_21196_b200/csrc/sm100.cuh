@@ -380,6 +380,24 @@ __device__ __forceinline__ uint64_t ex2_fma2(uint64_t x) {
                  __uint_as_float(__float_as_uint(phi) + (__float_as_uint(rhi) << 23)));
 }
 
+// RoPE (DESIGN A26): rotate the column pairs (e, e+1), e = e0 + 2k, of 2n consecutive fp32 values of
+// one row at position pos, by +angle (sign = 1) or -angle (sign = -1, gradients). Tables: see RopeRef.
+template <int N2>
+__device__ __forceinline__ void rope_rotate(float* v, const float2* hi, const float2* lo, int d, long long pos,
+                                            int e0, float sign) {
+  const float2* th = hi + (pos >> 10) * (d / 2) + e0 / 2;
+  const float2* tl = lo + (pos & 1023) * (d / 2) + e0 / 2;
+#pragma unroll
+  for (int k = 0; k < N2; ++k) {
+    const float2 a = __ldg(th + k), b = __ldg(tl + k);
+    const float c = a.x * b.x - a.y * b.y;
+    const float s = (a.y * b.x + a.x * b.y) * sign;
+    const float x = v[2 * k], y = v[2 * k + 1];
+    v[2 * k] = x * c - y * s;
+    v[2 * k + 1] = x * s + y * c;
+  }
+}
+
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");

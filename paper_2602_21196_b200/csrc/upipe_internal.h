@@ -124,7 +124,24 @@ namespace upipe {
 inline bool overlap_enabled(uint32_t flags, int C) { return C > 1 && !(flags & UPIPE_FLAG_SYNC_COMM); }
 }  // namespace upipe
 
+namespace upipe {
+// RoPE rotation tables owned by the ctx (RopeRef in kernels.h), rebuilt when (base, d) change or a
+// longer sequence arrives. A few MB at most (hi: S/1024 x d/2, lo: 1024 x d/2 float2).
+struct RopeTables {
+  float base = 0.f;
+  int d = 0;
+  int64_t n_hi = 0;
+  float2* hi = nullptr;
+  float2* lo = nullptr;
+  ~RopeTables() {
+    if (hi) cudaFree(hi);
+    if (lo) cudaFree(lo);
+  }
+};
+}  // namespace upipe
+
 struct upipe_ctx_s {
+  upipe::RopeTables rope;
   upipe::Pipe pipe;
   upipe::Tracer tracer;
   int device = 0;

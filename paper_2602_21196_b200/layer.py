@@ -17,7 +17,8 @@ from . import upipe as U
 class UPipeAttention:
     def __init__(self, n_q_heads: int, n_kv_heads: int, head_dim: int, hidden: int, chunk_heads: int,
                  causal: bool = True, process_group=None, device=None, fabric=None, cp_rank: int | None = None,
-                 cp_size: int | None = None, sync_comm: bool = False, naive_kv: bool = False):
+                 cp_size: int | None = None, sync_comm: bool = False, naive_kv: bool = False,
+                 rope_base: float = 0.0):
         """CP group: ``process_group`` (torch.distributed, one process per GPU, NCCL transport),
         or ``fabric`` + ``cp_rank`` + ``cp_size`` (single-process group driven by one host thread per rank),
         or neither (C = 1). ``sync_comm``: sequential schedule with one chunk buffer set (the
@@ -25,6 +26,7 @@ class UPipeAttention:
         chunk's attention on a side stream (two buffer sets)."""
         self.Hq, self.Hkv, self.d, self.D, self.U = n_q_heads, n_kv_heads, head_dim, hidden, chunk_heads
         self.causal = int(causal)
+        self.rope_base = float(rope_base)    # 0: no RoPE; else rotary base (Llama3: 500000), DESIGN A26
         self.flags = (1 if sync_comm else 0) | (2 if naive_kv else 0)   # UPIPE_FLAG_SYNC_COMM, UPIPE_FLAG_NAIVE_KV
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
@@ -45,7 +47,7 @@ class UPipeAttention:
         self._ws = {}
 
     def shape(self, seq_local: int) -> U.upipe_shape_t:
-        return U.make_shape(seq_local, self.D, self.Hq, self.Hkv, self.d, self.U, self.causal)
+        return U.make_shape(seq_local, self.D, self.Hq, self.Hkv, self.d, self.U, self.causal, self.rope_base)
 
     def workspace(self, seq_local: int, pass_: int) -> torch.Tensor:
         # One chunk-buffer workspace per sequence length, shared by the forward and the backward pass

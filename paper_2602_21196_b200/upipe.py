@@ -28,7 +28,7 @@ class UpipeError(RuntimeError):
 
 class upipe_shape_t(ctypes.Structure):
     _fields_ = [("seq_local", c_int64), ("hidden", c_int32), ("n_q_heads", c_int32), ("n_kv_heads", c_int32),
-                ("head_dim", c_int32), ("chunk_heads", c_int32), ("causal", c_int32)]
+                ("head_dim", c_int32), ("chunk_heads", c_int32), ("causal", c_int32), ("rope_base", ctypes.c_float)]
 
 
 class upipe_stage_info_t(ctypes.Structure):
@@ -112,8 +112,10 @@ def _stream(stream):
     return stream.cuda_stream
 
 
-def make_shape(seq_local, hidden, n_q_heads, n_kv_heads, head_dim, chunk_heads, causal=1) -> upipe_shape_t:
-    return upipe_shape_t(seq_local, hidden, n_q_heads, n_kv_heads, head_dim, chunk_heads, int(causal))
+def make_shape(seq_local, hidden, n_q_heads, n_kv_heads, head_dim, chunk_heads, causal=1,
+               rope_base=0.0) -> upipe_shape_t:
+    return upipe_shape_t(seq_local, hidden, n_q_heads, n_kv_heads, head_dim, chunk_heads, int(causal),
+                         float(rope_base))
 
 
 # ------------------------------------------------------------------ lifecycle

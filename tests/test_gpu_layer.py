@@ -18,7 +18,7 @@ REL, ABS = 5e-3, 2e-2
 
 
 def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", bwd=True, sync=False, exp_S=None,
-               naive=False, comm_counts=None):
+               naive=False, comm_counts=None, rope_base=0.0):
     """Run the layer on C ranks; returns (per-rank outputs, inputs). exp_S: draw the first S tokens of
     a length-exp_S sequence (its value scales), e.g. to keep dY's 1/sqrt(S) scale sane for tiny S."""
     from paper_2602_21196_b200 import UPipeAttention, upipe
@@ -41,9 +41,9 @@ def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", b
             with torch.cuda.stream(stream):
                 if C > 1:
                     attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal, fabric=fabric, cp_rank=r, cp_size=C,
-                                          sync_comm=sync, naive_kv=naive)
+                                          sync_comm=sync, naive_kv=naive, rope_base=rope_base)
                 else:
-                    attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal, naive_kv=naive)
+                    attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal, naive_kv=naive, rope_base=rope_base)
                 if comm_counts is not None:
                     upipe.upipe_set_trace(attn.ctx, True)
                 y, saved = attn.forward(xs[r], W["wq"], W["wk"], W["wv"], W["wo"])
@@ -75,9 +75,9 @@ def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", b
     return results, inp
 
 
-def _check(results, inp, C, Hq, Hkv, d, U, causal=True, bwd=True):
+def _check(results, inp, C, Hq, Hkv, d, U, causal=True, bwd=True, rope_base=None):
     x, wq, wk, wv, wo, dy = (inp[k] for k in ("x", "wq", "wk", "wv", "wo", "dy"))
-    Y, O, L = oracle.layer_fwd(x, wq, wk, wv, wo, Hq, Hkv, d, causal)
+    Y, O, L = oracle.layer_fwd(x, wq, wk, wv, wo, Hq, Hkv, d, causal, rope_base=rope_base)
     y = np.concatenate([to_np(r["y"]) for r in results], 0)
     o = np.concatenate([to_np(r["o"]) for r in results], 0)
     assert_close("y", y, Y, REL, ABS)
@@ -100,7 +100,7 @@ def _check(results, inp, C, Hq, Hkv, d, U, causal=True, bwd=True):
                     f"lse[p{p},h{q0 + j}]: max|dLSE| {np.abs(dl).max():.3e}, rms(exp(dLSE)-1) {rms:.3e}"
     if not bwd:
         return
-    dX, dWq, dWk, dWv, dWo = oracle.layer_bwd(x, wq, wk, wv, wo, dy, Hq, Hkv, d, causal)
+    dX, dWq, dWk, dWv, dWo = oracle.layer_bwd(x, wq, wk, wv, wo, dy, Hq, Hkv, d, causal, rope_base=rope_base)
     dx = np.concatenate([to_np(r["dx"]) for r in results], 0)
     assert_close("dx", dx, dX, REL, ABS)
     for name, want in (("dwq", dWq), ("dwk", dWk), ("dwv", dWv), ("dwo", dWo)):
@@ -224,3 +224,13 @@ def test_naive_kv_schedule_ablation(sync):
     vol_n = (nu * qpd + 2 * nu) * (C - 1)
     assert vol_s == oracle.comm_volume_formula(Hq, Hkv, C, scheduled=True)
     assert vol_n == oracle.comm_volume_formula(Hq, Hkv, C, scheduled=False)
+
+
+@pytest.mark.parametrize("C,S,Hq,Hkv,d,Uc,base", [(1, 512, 8, 2, 64, 2, 10000.0), (2, 640, 8, 2, 128, 4, 500000.0),
+                                                   (4, 1024, 16, 4, 64, 4, 500000.0), (2, 2048, 8, 2, 64, 2, 100.0)])
+def test_rope_layer(C, S, Hq, Hkv, d, Uc, base):
+    # SURVEY N3 / DESIGN A26: RoPE on Q and K in the projection epilogues (global token positions across
+    # the CP shards), gradients rotated back in the dQ conversion and the dK epilogue. base 100 at
+    # S = 2048 gives angles up to ~2000 rad (table composition, not an fp32 angle).
+    r, inp = _run_group(C, S, 512, Hq, Hkv, d, Uc, rope_base=base)
+    _check(r, inp, C, Hq, Hkv, d, Uc, rope_base=base)
