@@ -219,19 +219,21 @@ def layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, causal=True, rope_base=None):
     return dX, dWq, dWk, dWv, dWo
 
 
-def layer_fwd_rows(X_rows, rows, K, V, Wq, Wo, Hq, Hkv, d, causal=True):
+def layer_fwd_rows(X_rows, rows, K, V, Wq, Wo, Hq, Hkv, d, causal=True, rope_base=None):
     """Row-sampled forward: y, O, lse of the given query rows only.
 
     ``X_rows`` are those rows of X; ``K``, ``V`` = X Wk^T, X Wv^T for all tokens ([S, Hkv, d]).
     Each row is computed exactly as in ``layer_fwd`` (rows of attention are independent).
     """
     Qr = (X_rows @ Wq.T).reshape(len(rows), Hq, d)
+    if rope_base:                        # K is passed already rotated (rope(X Wk^T, arange(S)))
+        Qr = rope(Qr, rows, rope_base)
     O, lse = attn_fwd(Qr, K, V, causal, rows=rows)
     O2 = O.reshape(len(rows), Hq * d)
     return O2 @ Wo.T, O2, lse
 
 
-def layer_bwd_tail(X_tail, dY_tail, K, V, Wq, Wk, Wv, Wo, Hq, Hkv, d):
+def layer_bwd_tail(X_tail, dY_tail, K, V, Wq, Wk, Wv, Wo, Hq, Hkv, d, rope_base=None):
     """dX of the last w tokens of a causal layer (w = len(X_tail)), following the same
     formulas as ``attn_bwd``/``layer_bwd``: with a causal mask, dK_j and dV_j of a key j in
     the tail only receive contributions from queries i >= j, which are all in the tail;
@@ -242,6 +244,8 @@ def layer_bwd_tail(X_tail, dY_tail, K, V, Wq, Wk, Wv, Wo, Hq, Hkv, d):
     R = Hq // Hkv
     scale = 1.0 / math.sqrt(d)
     Qt = (X_tail @ Wq.T).reshape(w, Hq, d)
+    if rope_base:                        # K is passed already rotated; Q of the tail rotated here
+        Qt = rope(Qt, np.arange(t0, S), rope_base)
     dOt = (dY_tail @ Wo).reshape(w, Hq, d)
     dQ = np.zeros((w, Hq, d))
     dK = np.zeros((w, Hkv, d))
@@ -262,6 +266,9 @@ def layer_bwd_tail(X_tail, dY_tail, K, V, Wq, Wk, Wv, Wo, Hq, Hkv, d):
         dQ[:, h, :] = (dS @ K[:, g, :]) * scale
         dK[:, g, :] += (dS[:, t0:].T @ Qt[:, h, :]) * scale
         dV[:, g, :] += P[:, t0:].T @ dOt[:, h, :]
+    if rope_base:
+        dQ = rope(dQ, np.arange(t0, S), rope_base, inverse=True)
+        dK = rope(dK, np.arange(t0, S), rope_base, inverse=True)
     return dQ.reshape(w, -1) @ Wq + dK.reshape(w, -1) @ Wk + dV.reshape(w, -1) @ Wv
 
 

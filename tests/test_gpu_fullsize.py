@@ -21,7 +21,9 @@ TAIL = 24
 REL, ABS = 5e-3, 2e-2
 
 
-def test_fullsize_bench_workload_sampled_rows():
+@pytest.mark.parametrize("rope_base", [0.0, 500000.0])
+def test_fullsize_bench_workload_sampled_rows(rope_base):
+    # rope_base 500000 (Llama3): rotary angles at positions up to 131071 (DESIGN A26)
     from paper_2602_21196_b200 import UPipeAttention, upipe
     e = synth.layer_exponents(D, Hq, d, S)
 
@@ -32,7 +34,7 @@ def test_fullsize_bench_workload_sampled_rows():
 
     x, dy = fill((S, D), "x"), fill((S, D), "dy")
     W = [fill((Hq * d, D), "wq"), fill((Hkv * d, D), "wk"), fill((Hkv * d, D), "wv"), fill((D, Hq * d), "wo")]
-    attn = UPipeAttention(Hq, Hkv, d, D, U)
+    attn = UPipeAttention(Hq, Hkv, d, D, U, rope_base=rope_base)
     y, saved = attn.forward(x, *W)
     dx, *_ = attn.backward(x, *W, dy, saved)
     torch.cuda.synchronize()
@@ -58,8 +60,11 @@ def test_fullsize_bench_workload_sampled_rows():
         V[t0:t0 + chunk] = oracle.project(xc, wv)
     K = K.reshape(S, Hkv, d)
     V = V.reshape(S, Hkv, d)
+    rb = rope_base or None
+    if rb:
+        K = oracle.rope(K, np.arange(S), rb)
     x_rows = synth.draw_rows(0, synth.TID["x"], D, ROWS, e["x"])
-    Y, Oo, L = oracle.layer_fwd_rows(x_rows, ROWS, K, V, wq, wo, Hq, Hkv, d)
+    Y, Oo, L = oracle.layer_fwd_rows(x_rows, ROWS, K, V, wq, wo, Hq, Hkv, d, rope_base=rb)
     assert_close("y rows", y_s, Y, REL, ABS)
     assert_close("o_saved rows", o_s, Oo, REL, ABS)
     # C = 1, U = 8: lse slot s*8 + j holds head 8 s + j, i.e. slot == head (upipe.h, DESIGN A8)
@@ -68,5 +73,5 @@ def test_fullsize_bench_workload_sampled_rows():
     assert_close("lse rows", lse_s, L[order], REL, ABS)
     x_tail = synth.draw(0, synth.TID["x"], (TAIL, D), e["x"], start=(S - TAIL) * D)
     dy_tail = synth.draw(0, synth.TID["dy"], (TAIL, D), e["dy"], start=(S - TAIL) * D)
-    dX = oracle.layer_bwd_tail(x_tail, dy_tail, K, V, wq, wk, wv, wo, Hq, Hkv, d)
+    dX = oracle.layer_bwd_tail(x_tail, dy_tail, K, V, wq, wk, wv, wo, Hq, Hkv, d, rope_base=rb)
     assert_close("dx tail rows", dx_t, dX, REL, ABS)

@@ -437,3 +437,20 @@ def test_row_sampled_layer_matches_full():
     w = 17
     np.testing.assert_allclose(O.layer_bwd_tail(X[-w:], dY[-w:], K, V, Wq, Wk, Wv, Wo, Hq, Hkv, d), dX[-w:],
                                atol=1e-11)
+
+
+def test_row_sampled_layer_matches_full_with_rope():
+    S, D, Hq, Hkv, d, base = 150, 24, 4, 2, 8, 50.0
+    X, Wq, Wk, Wv = rand(S, D), rand(Hq * d, D, scale=.3), rand(Hkv * d, D, scale=.3), rand(Hkv * d, D, scale=.3)
+    Wo, dY = rand(D, Hq * d, scale=.3), rand(S, D)
+    Y, Oo, L = O.layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, rope_base=base)
+    K = O.rope((X @ Wk.T).reshape(S, Hkv, d), np.arange(S), base)
+    V = (X @ Wv.T).reshape(S, Hkv, d)
+    rows = np.array([0, 1, 63, 64, 100, 149])
+    y, o, lse = O.layer_fwd_rows(X[rows], rows, K, V, Wq, Wo, Hq, Hkv, d, rope_base=base)
+    np.testing.assert_allclose(y, Y[rows], atol=1e-12)
+    np.testing.assert_allclose(lse, L[:, rows], atol=1e-12)
+    dX = O.layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, rope_base=base)[0]
+    w = 17
+    np.testing.assert_allclose(O.layer_bwd_tail(X[-w:], dY[-w:], K, V, Wq, Wk, Wv, Wo, Hq, Hkv, d, rope_base=base),
+                               dX[-w:], atol=1e-11)
