@@ -11,6 +11,8 @@
 #include "kernels.h"
 #include "upipe_internal.h"
 
+static_assert(sizeof(upipe_shape_t) == 40, "upipe_shape_t layout is part of the ABI (Python mirror in upipe.py)");
+
 namespace upipe {
 upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, const upipe_bf16* x, const upipe_bf16* wq,
                          const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo, upipe_bf16* y,

@@ -66,6 +66,23 @@ def test_validation_names_constraint(U, args, status, needle):
     assert st == status and needle in msg, (st, msg)
 
 
+@pytest.mark.parametrize("base,ok", [(0.0, True), (10000.0, True), (500000.0, True), (1.0, False), (0.5, False),
+                                     (-10.0, False), (float("inf"), False), (float("nan"), False)])
+def test_rope_base_validation(U, base, ok):
+    # DESIGN A26: 0 disables RoPE, otherwise a finite base > 1
+    st, msg = U.upipe_validate(1, U.make_shape(256, 512, 8, 2, 64, 2, 1, base))
+    assert (st == 0) == ok, (st, msg)
+    if not ok:
+        assert "rope_base" in msg
+
+
+def test_shape_struct_layout_matches_header(U):
+    # the ctypes mirror of upipe_shape_t: 8 + 6*4 + 4 bytes, rope_base last (include/upipe.h)
+    import ctypes
+    assert ctypes.sizeof(U.upipe_shape_t) == 40
+    assert U.upipe_shape_t.rope_base.offset == 32
+
+
 GRID = [(Hq, Hkv, C, Uc) for Hq, Hkv in ((8, 2), (16, 4), (32, 8), (64, 8), (8, 8), (32, 32))
         for C in (1, 2, 4, 8) for Uc in range(C, Hq + 1, C)
         if Hkv % C == 0 and Hq % Uc == 0 and ((Uc // C) % (Hq // Hkv) == 0 or (Hq // Hkv) % (Uc // C) == 0)]
