@@ -8,10 +8,11 @@
 //              thread-local and need no shuffles)
 //   warps 4-7  softmax for tile B
 //   warp 8     TMA producer (Q once, then K and V per KV tile)
-//   warp 9     MMA issuer: S = Q K^T into TMEM, O += P V with P (bf16) read from TMEM
+//   warp 9     MMA issuer: S = Q K^T into TMEM, O += P V with P (bf16) from shared memory
 //   warps 10-11 idle (complete the third warpgroup for setmaxnreg)
-// TMEM (512 columns): S_A | S_B | O_A | O_B (d = 128). While one warpgroup runs
-// its softmax the tensor core computes the other tile's S or PV (ping-pong).
+// TMEM (512 columns): S_A | S_B | O_A | O_B (d = 128). P (bf16) goes to shared memory, so S(it+1) of
+// a tile is issued as soon as its softmax has read S(it) into registers and only PV(it) waits for the
+// softmax; the tensor core alternates between the tiles' S and PV work (ping-pong).
 // Online softmax in the exp2 domain with the log2(e)/sqrt(d) scale folded into
 // one FFMA; O is rescaled only when the running max grows by more than 8 (2^8
 // headroom in fp32/bf16), which is exact: l and O always share the reference max.
@@ -61,14 +62,20 @@ template <int D>
 struct FwdCfg {
   static constexpr int TILE = 128;
   static constexpr int QBYTES = TILE * D * 2;       // one 128 x D bf16 tile
-  static constexpr int KV_STAGES = 2;               // P lives in TMEM, so smem holds Q_A, Q_B and 2 K/V stages
+  static constexpr int PBYTES = TILE * TILE * 2;    // one 128 x 128 bf16 P tile
+  // K single-buffered (K(it+1) has the whole previous iteration to land: S is issued early), V
+  // double-buffered (PV(it) is the late consumer and V(it+1) is needed right after it)
+  static constexpr int V_STAGES = 2;
   static constexpr int OFF_QA = 0;
   static constexpr int OFF_QB = QBYTES;
   static constexpr int OFF_K = 2 * QBYTES;
-  static constexpr int OFF_V = OFF_K + KV_STAGES * QBYTES;
-  static constexpr int OFF_BAR = OFF_V + KV_STAGES * QBYTES;
+  static constexpr int OFF_V = OFF_K + QBYTES;
+  static constexpr int OFF_PA = OFF_V + V_STAGES * QBYTES;   // P_A, P_B: bf16, K-major 128B-swizzled (A of PV)
+  static constexpr int OFF_PB = OFF_PA + PBYTES;
+  static constexpr int OFF_BAR = OFF_PB + PBYTES;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr uint32_t TM_SA = 0, TM_SB = 128, TM_OA = 256, TM_OB = 256 + D;
+  static_assert(SMEM <= 232448, "shared memory");
 };
 
 template <int D, bool TL>
@@ -81,13 +88,14 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;                    // [KV_STAGES]
-  uint64_t* k_empty = bars + 3;                   // [KV_STAGES]
-  uint64_t* v_full = bars + 5;                    // [KV_STAGES]
-  uint64_t* v_empty = bars + 7;                   // [KV_STAGES]
-  uint64_t* s_full = bars + 9;                    // [2] tile A/B
-  uint64_t* p_full = bars + 11;                   // [2]
-  uint64_t* o_full = bars + 13;                   // [2]
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = bars + 2;
+  uint64_t* v_full = bars + 3;                    // [V_STAGES]
+  uint64_t* v_empty = bars + 5;                   // [V_STAGES]
+  uint64_t* s_full = bars + 7;                    // [2] tile A/B: S(it) in TMEM
+  uint64_t* s_free = bars + 9;                    // [2] the softmax has read S(it) into registers
+  uint64_t* p_full = bars + 11;                   // [2] P(it) in smem and O rescaled
+  uint64_t* o_full = bars + 13;                   // [2] PV(it) done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = warp_id(), lane = lane_id();
@@ -102,12 +110,12 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 8 && lane == 0) {
     tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < C::KV_STAGES; ++s) {
-      mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1);
+    mbar_init(k_full, 1); mbar_init(k_empty, 1);
+    for (int s = 0; s < C::V_STAGES; ++s) {
       mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1);
     }
     for (int t = 0; t < 2; ++t) {
-      mbar_init(&s_full[t], 1); mbar_init(&p_full[t], 128); mbar_init(&o_full[t], 1);
+      mbar_init(&s_full[t], 1); mbar_init(&s_free[t], 128); mbar_init(&p_full[t], 128); mbar_init(&o_full[t], 1);
     }
     fence_barrier_init();
     tmem_slot[1] = smem_u32(smem);
@@ -129,25 +137,24 @@ __global__ void __launch_bounds__(384, 1)
         tma_load_3d(smem + C::OFF_QB + c * 16384, &tmQ, q_full, c * 64, head, qt0 * 128 + 128);
       }
       for (int it = 0; it < nB; ++it) {
-        const int st = it % C::KV_STAGES;
-        const uint32_t ph = (it / C::KV_STAGES) & 1;
-        mbar_wait(&k_empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&k_full[st], C::QBYTES);
+        mbar_wait(k_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(k_full, C::QBYTES);
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
-          tma_load_3d(smem + C::OFF_K + st * C::QBYTES + c * 16384, &tmK, &k_full[st], c * 64, kvh, it * 128);
-        mbar_wait(&v_empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&v_full[st], C::QBYTES);
+          tma_load_3d(smem + C::OFF_K + c * 16384, &tmK, k_full, c * 64, kvh, it * 128);
+        const int sv = it % C::V_STAGES;
+        mbar_wait(&v_empty[sv], ((it / C::V_STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&v_full[sv], C::QBYTES);
 #pragma unroll
         for (int c = 0; c < NCH; ++c)
-          tma_load_3d(smem + C::OFF_V + st * C::QBYTES + c * 16384, &tmV, &v_full[st], c * 64, kvh, it * 128);
+          tma_load_3d(smem + C::OFF_V + sv * C::QBYTES + c * 16384, &tmV, &v_full[sv], c * 64, kvh, it * 128);
       }
     }
   } else if (warp == 9) {
     {
       // ------------------------------------------------ MMA issuer (whole warp; elect.sync inside the MMA asm)
       constexpr uint32_t idS = idesc_bf16(128, 128, false, false);  // Q (K-major) x K (K-major)
-      constexpr uint32_t idO = idesc_bf16(128, D, false, true);     // P (TMEM) x V (MN-major)
+      constexpr uint32_t idO = idesc_bf16(128, D, false, true);     // P (smem, K-major) x V (MN-major)
       // smem base re-read (volatile) per KV tile: descriptors are formed next to each MMA
       // instead of being hoisted into registers (see mma_ss_w in sm100.cuh)
       uint32_t base = ld_volatile_shared_u32(tmem_slot + 1);
@@ -159,64 +166,67 @@ __global__ void __launch_bounds__(384, 1)
           mma_ss_w(tm, dq + off, dk + off, idS, i != 0);
         }
       };
-      // O += P V with A = P in TMEM: keys [16 ks, 16 ks + 16) packed (bf16 pairs) at S columns 8 ks
-      auto issue_PV = [&](uint32_t tp, uint32_t sv, uint32_t tm, bool acc) {
-        const uint64_t dv = desc_sw128(sv, 16384, 1024);
+      // O += P V: A = P in smem (K-major over keys), B = V (MN-major)
+      auto issue_PV = [&](uint32_t sp, uint32_t sv, uint32_t tm, bool acc) {
+        const uint64_t dp = desc_sw128(sp, 16, 1024), dv = desc_sw128(sv, 16384, 1024);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          mma_ts_w(tm, tp + ks * 8, dv + (((ks >> 2) * 8192 + (ks & 3) * 2048) >> 4), idO, (acc || ks) ? 1u : 0u);
+          mma_ss_w(tm, dp + (((ks >> 2) * 16384 + (ks & 3) * 32) >> 4), dv + (((ks >> 2) * 8192 + (ks & 3) * 2048) >> 4),
+                   idO, (acc || ks) ? 1u : 0u);
       };
-      long long tw[4] = {0, 0, 0, 0};   // wait p_full A, wait p_full B, wait K, wait V
+      long long tw[4] = {0, 0, 0, 0};   // wait s_free (A+B), wait p_full A, wait p_full B, wait K/V
       const long long t_begin = tick<TL>();
       mbar_wait(q_full, 0);
-      mbar_wait(&k_full[0], 0);
+      mbar_wait(k_full, 0);
       tc_fence_after();
       issue_S(base + C::OFF_QA, base + C::OFF_K, tmem + C::TM_SA);
       mma_commit_w(&s_full[0]);
       issue_S(base + C::OFF_QB, base + C::OFF_K, tmem + C::TM_SB);
       mma_commit_w(&s_full[1]);
-      mma_commit_w(&k_empty[0]);                  // K(0) consumed once both S MMAs complete
+      mma_commit_w(k_empty);                      // K(0) consumed once both S MMAs complete
+      // Per KV tile: S(it+1) of each tile is issued as soon as its softmax has read S(it) (P lives in
+      // smem, so the S columns are free), then PV(it) once P(it) is written. The softmax of a tile
+      // therefore never waits for its own PV + S round trip, only for the tensor core's queue.
       for (int it = 0; it < nB; ++it) {
-        const int st = it % C::KV_STAGES;
-        const uint32_t ph = (it / C::KV_STAGES) & 1;
         base = ld_volatile_shared_u32(tmem_slot + 1);
-        const uint32_t sv = base + C::OFF_V + st * C::QBYTES;
+        const bool more = it + 1 < nB;
         long long w0 = tick<TL>();
-        mbar_wait(&v_full[st], ph);
+        if (more) mbar_wait(k_full, (it + 1) & 1);
         tw[3] += tick<TL>() - w0;
-        // ---- tile A
+        w0 = tick<TL>();
+        if (it + 1 < nA) {
+          mbar_wait(&s_free[0], it & 1);
+          tc_fence_after();
+          issue_S(base + C::OFF_QA, base + C::OFF_K, tmem + C::TM_SA);
+          mma_commit_w(&s_full[0]);
+        }
+        if (more) {
+          mbar_wait(&s_free[1], it & 1);
+          tc_fence_after();
+          issue_S(base + C::OFF_QB, base + C::OFF_K, tmem + C::TM_SB);
+          mma_commit_w(&s_full[1]);
+          mma_commit_w(k_empty);
+        }
+        tw[0] += tick<TL>() - w0;
+        w0 = tick<TL>();
+        const int sv = it % C::V_STAGES;
+        mbar_wait(&v_full[sv], (it / C::V_STAGES) & 1);
+        tw[3] += tick<TL>() - w0;
         if (it < nA) {
           w0 = tick<TL>();
           mbar_wait(&p_full[0], it & 1);
-          tw[0] += tick<TL>() - w0;
+          tw[1] += tick<TL>() - w0;
           tc_fence_after();
-          issue_PV(tmem + C::TM_SA, sv, tmem + C::TM_OA, it > 0);
+          issue_PV(base + C::OFF_PA, base + C::OFF_V + sv * C::QBYTES, tmem + C::TM_OA, it > 0);
           mma_commit_w(&o_full[0]);
         }
-        const bool more = it + 1 < nB;
-        const int st1 = (it + 1) % C::KV_STAGES;
-        const uint32_t ph1 = ((it + 1) / C::KV_STAGES) & 1;
-        w0 = tick<TL>();
-        if (more) mbar_wait(&k_full[st1], ph1);
-        tw[2] += tick<TL>() - w0;
-        tc_fence_after();
-        if (it + 1 < nA) {
-          issue_S(base + C::OFF_QA, base + C::OFF_K + st1 * C::QBYTES, tmem + C::TM_SA);
-          mma_commit_w(&s_full[0]);
-        }
-        // ---- tile B
         w0 = tick<TL>();
         mbar_wait(&p_full[1], it & 1);
-        tw[1] += tick<TL>() - w0;
+        tw[2] += tick<TL>() - w0;
         tc_fence_after();
-        issue_PV(tmem + C::TM_SB, sv, tmem + C::TM_OB, it > 0);
+        issue_PV(base + C::OFF_PB, base + C::OFF_V + sv * C::QBYTES, tmem + C::TM_OB, it > 0);
         mma_commit_w(&o_full[1]);
-        mma_commit_w(&v_empty[st]);
-        if (more) {
-          issue_S(base + C::OFF_QB, base + C::OFF_K + st1 * C::QBYTES, tmem + C::TM_SB);
-          mma_commit_w(&s_full[1]);
-          mma_commit_w(&k_empty[st1]);
-        }
+        mma_commit_w(&v_empty[sv]);
       }
       if (TL && a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) {
         for (int i = 0; i < 4; ++i) a.dbg[i] = tw[i];
@@ -236,6 +246,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tS = tmem + (wg ? C::TM_SB : C::TM_SA) + ((uint32_t)(quad * 32) << 16);
     const uint32_t tO = tmem + (wg ? C::TM_OB : C::TM_OA) + ((uint32_t)(quad * 32) << 16);
     const float sl2 = a.scale_log2;
+    const uint32_t sP = smem_u32(smem + (wg ? C::OFF_PB : C::OFF_PA));
     float m_ref = -INFINITY, l_run = 0.f;
     long long ts[5] = {0, 0, 0, 0, 0};   // wait S, TMEM load, max+exp+sum, O wait+rescale, P store+arrive
     for (int it = 0; it < n; ++it) {
@@ -249,6 +260,8 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + c * 32));
       tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&s_free[wg]);                     // S(it) is in registers: the MMA warp may issue S(it+1)
       float* s = reinterpret_cast<float*>(sr);
       const long long e2 = tick<TL>();
       ts[1] += e2 - e1;
@@ -281,7 +294,11 @@ __global__ void __launch_bounds__(384, 1)
       // polynomial on the FMA pipe, the rest on MUFU (XU also packs P to bf16); row sum with FADD2.
       const uint64_t sl2x2 = f2_pack(sl2, sl2), nm2 = f2_pack(-m_ref, -m_ref);
       uint64_t acc2[4] = {0, 0, 0, 0};
-      uint32_t pk[16];
+      uint32_t pk[4];
+      if (it > 0) {
+        mbar_wait(&o_full[wg], (it - 1) & 1);         // PV(it-1) done: P buffer free, O may be rescaled
+        tc_fence_after();
+      }
 #pragma unroll
       for (int j = 0; j < 64; ++j) {
         const uint64_t t = f2_fma(f2_pack(s[2 * j], s[2 * j + 1]), sl2x2, nm2);
@@ -294,12 +311,15 @@ __global__ void __launch_bounds__(384, 1)
           e = f2_pack(ex2(t0), ex2(t1));
         }
         acc2[j & 3] = f2_add(acc2[j & 3], e);
-        // P (bf16 pairs) -> TMEM over this tile's S columns as soon as 16 pairs are ready (the PV MMA
-        // reads it as its A operand; S(it+1) is issued after PV(it), so the overwrite is ordered)
+        // P (bf16 pairs) -> smem row `row` (K-major, 128B swizzle: keys [64 kc, 64 kc + 64) in chunk kc),
+        // 16 bytes at a time
         float e0, e1;
         f2_unpack(e, e0, e1);
-        pk[j & 15] = pack_bf16(e0, e1);
-        if ((j & 15) == 15) tmem_st16(tS + (j >> 4) * 16, pk);
+        pk[j & 3] = pack_bf16(e0, e1);
+        if ((j & 3) == 3) {
+          const int g8 = j >> 2;                       // 8-key group: keys [8 g8, 8 g8 + 8)
+          st_shared_v4(sP + (g8 >> 3) * 16384 + sw128_offset(row, (g8 & 7) * 8), pk[0], pk[1], pk[2], pk[3]);
+        }
       }
       float s1, s2;
       f2_unpack(f2_add(f2_add(acc2[0], acc2[1]), f2_add(acc2[2], acc2[3])), s1, s2);
@@ -307,10 +327,6 @@ __global__ void __launch_bounds__(384, 1)
       l_run = l_run * alpha + sum;
       const long long e3 = tick<TL>();
       ts[2] += e3 - e2;
-      if (it > 0) {
-        mbar_wait(&o_full[wg], (it - 1) & 1);         // PV(it-1) done: O may be rescaled
-        tc_fence_after();
-      }
       // tcgen05.ld/st are warp-collective (.sync.aligned): the rescale decision is per row, so the
       // warp rescales if any of its rows needs it (alpha = 1 for the others). A per-thread branch
       // here diverges the warp and hangs once rows' maxima grow at different tiles.
@@ -329,7 +345,7 @@ __global__ void __launch_bounds__(384, 1)
       }
       const long long e4 = tick<TL>();
       ts[3] += e4 - e3;
-      tmem_wait_st();
+      fence_proxy_async_smem();                     // P writes visible to the tensor core (async proxy)
       tc_fence_before();
       mbar_arrive(&p_full[wg]);
       ts[4] += tick<TL>() - e4;

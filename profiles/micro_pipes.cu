@@ -31,6 +31,20 @@ __global__ void __launch_bounds__(512, 1) pipe_cost(long long* out, int iters, f
       if (MODE == 7) asm volatile("max.f32 %0, %0, %1, %0;" : "+f"(v[j]) : "f"(seed));
       if (MODE == 8) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(w[j]) : "l"(c2));
       if (MODE == 9) asm volatile("max.f32 %0, %0, %1;" : "+f"(v[j]) : "f"(seed));
+      // mixes: one MUFU.EX2 with 4 FFMA2 (10: pipes overlap -> 8 cycles; serialised -> 16), with 8 FFMA (11),
+      // with 4 F2FP (12)
+      if (MODE == 10) {
+        if (j == 0) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[j]));
+        else if (j <= 4) asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(w[j]) : "l"(c2));
+      }
+      if (MODE == 11) {
+        if (j == 0) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[j]));
+        else asm volatile("fma.rn.f32 %0, %0, %1, %1;" : "+f"(v[j]) : "f"(seed));
+      }
+      if (MODE == 12) {
+        if (j == 0) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v[j]));
+        else if (j <= 4) asm volatile("cvt.rn.bf16x2.f32 %0, %1, %1;" : "=r"(u[j]) : "f"(__uint_as_float(u[j])));
+      }
     }
   }
   __syncthreads();
@@ -70,5 +84,9 @@ int main() {
   run<6>("IADD", d);
   run<7>("FMNMX3", d);
   run<9>("FMNMX", d);
+  // for the mixes the printed number is cycles per 8-instruction group / 8
+  run<10>("mix MUFU + 4 FFMA2 (/8)", d);
+  run<11>("mix MUFU + 7 FFMA (/8)", d);
+  run<12>("mix MUFU + 4 F2FP (/8)", d);
   return 0;
 }
