@@ -295,10 +295,12 @@ __global__ void __launch_bounds__(384, 1)
       const uint64_t sl2x2 = f2_pack(sl2, sl2), nm2 = f2_pack(-m_ref, -m_ref);
       uint64_t acc2[4] = {0, 0, 0, 0};
       uint32_t pk[4];
+      const long long eo = tick<TL>();
       if (it > 0) {
         mbar_wait(&o_full[wg], (it - 1) & 1);         // PV(it-1) done: P buffer free, O may be rescaled
         tc_fence_after();
       }
+      ts[3] += tick<TL>() - eo;                     // (reported as "O": waiting for PV(it-1))
 #pragma unroll
       for (int j = 0; j < 64; ++j) {
         const uint64_t t = f2_fma(f2_pack(s[2 * j], s[2 * j + 1]), sl2x2, nm2);
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(384, 1)
         tmem_wait_st();
       }
       const long long e4 = tick<TL>();
-      ts[3] += e4 - e3;
+      ts[4] += e4 - e3;
       fence_proxy_async_smem();                     // P writes visible to the tensor core (async proxy)
       tc_fence_before();
       mbar_arrive(&p_full[wg]);
