@@ -12,6 +12,7 @@ using namespace upipe::dev;
 // mode 6: SS N64 alternating two accumulators
 // mode 7: SS N128, K-loop fully unrolled (descriptor offsets are immediates)
 // mode 8: as 7 but issued by the whole warp with elect.sync inside the asm (no compiler ELECT loop)
+// mode 9: as 8 with N = 64 (half query tiles of the backward)
 // sts_warps: warps 1..sts_warps store 16 B per lane per instruction into a separate smem region
 __global__ void __launch_bounds__(384, 1) mma_rate(long long* out, int iters, int mode, int sts_warps) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -26,8 +27,8 @@ __global__ void __launch_bounds__(384, 1) mma_rate(long long* out, int iters, in
   tc_fence_after();
   const uint32_t tm = slot;
   const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 65536);
-  if (warp == 0 && mode == 8) {
-    const uint32_t id = idesc_bf16(128, 128, false, false);
+  if (warp == 0 && (mode == 8 || mode == 9)) {
+    const uint32_t id = idesc_bf16(128, mode == 9 ? 64 : 128, false, false);
     const uint64_t da = desc_sw128(sa, 16, 1024), db = desc_sw128(sb, 16, 1024);
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
@@ -105,10 +106,10 @@ int main() {
   cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* names[] = {"SS N128 K-major", "SS N256 K-major", "TS N128", "SS N128 B MN-major",
                          "SS N128 2 accums", "TS N128 2 accums", "SS N64 2 accums", "SS N128 unrolled",
-                         "SS N128 warp-issued"};
+                         "SS N128 warp-issued", "SS N64 warp-issued"};
   const int iters = 4096;
   for (int sts : {0, 8}) {
-    for (int mode = 0; mode < 9; ++mode) {
+    for (int mode = 0; mode < 10; ++mode) {
       mma_rate<<<148, 384, smem>>>(d, iters, mode, sts);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
@@ -117,7 +118,7 @@ int main() {
       double avg = 0;
       for (int i = 0; i < 148; ++i) avg += h[i];
       avg /= 148.0 * iters * 8;
-      const double N = mode == 1 ? 256 : mode == 6 ? 64 : 128;
+      const double N = mode == 1 ? 256 : (mode == 6 || mode == 9) ? 64 : 128;
       printf("%-20s sts_warps=%d: %.1f cycles/MMA (floor %.0f), %.0f flop/clk/SM\n", names[mode], sts, avg,
              128 * N / 256, 2.0 * 128 * N * 16 / avg);
     }
