@@ -32,6 +32,15 @@ Functions and their pins (tests/test_oracle_*.py):
 * ``upipe_forward/backward`` (sharded simulation) -- pinned: equal to the
                        un-sharded oracle for every (C, U) (method exactness).
 * ``memory_*``      -- pinned: §3.4 numbers (96 -> 12 S d_head, 87.5 %).
+* ``merge_partials`` -- pinned: SPEC S:64-66 (empty partial is the identity,
+                       merge(p, p) = (p.out, p.lse + ln 2), two one-key partials = the
+                       brute-force two-key softmax).
+* ``attn_fwd_block``/``attn_bwd_block`` -- pinned: merged in ring order / summed over
+                       key blocks they reproduce ``attn_fwd`` / ``attn_bwd`` (themselves
+                       pinned above), causal and not, with fully masked blocks.
+* ``hybrid_forward/backward`` (UPipe x Ring) -- pinned: equal to the
+                       un-sharded layer for every (a, r, U) of a grid; a = C, r = 1 is
+                       bitwise ``upipe_forward``; a = 1 is pure ring attention.
 * ``rope``          -- pinned: complex-exponential form (each pair times e^{i p theta_i}),
                        relative-position invariance of q.k, norm preservation, position 0 =
                        identity, inverse o forward = identity; the RoPE layer's gradients by
@@ -515,6 +524,237 @@ def upipe_backward(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, C, U, causal=True, schedul
     retire(kv_state)
     tot = {k: sum(dW[r][k] for r in range(C)) for k in ("q", "k", "v", "o")}
     return np.concatenate(dX, 0), tot["q"], tot["k"], tot["v"], tot["o"]
+
+
+# ----------------------------------------------------------------------------
+# Ring attention blocks and the UPipe x Ring hybrid (§2.1,
+# P:172 "extends to hybrid schemes such as USP")
+# ----------------------------------------------------------------------------
+
+
+def attn_fwd_block(Q, K, V, q_pos0, k_pos0, causal=True, kv_of_head=None):
+    """Partial attention of one ring step: query rows at global positions q_pos0 + i
+    over the key block at k_pos0 + j ("a local attention ... then exchanges the
+    K, V shards among the devices in a ring fashion"). Plain softmax over the block's
+    visible keys. Rows that see no key of the block return O = 0 and lse = -inf (the
+    empty partial). Returns O [Sq, Hq, d], lse [Hq, Sq]."""
+    Sq, Hq, d = Q.shape
+    Skv, Hkv, _ = K.shape
+    kvh = _kv_map(Hq, Hkv, kv_of_head)
+    scale = 1.0 / math.sqrt(d)
+    qpos = q_pos0 + np.arange(Sq)
+    kpos = k_pos0 + np.arange(Skv)
+    vis = (kpos[None, :] <= qpos[:, None]) if causal else np.ones((Sq, Skv), dtype=bool)
+    O = np.zeros((Sq, Hq, d))
+    lse = np.full((Hq, Sq), -np.inf)
+    rows = np.nonzero(vis.any(axis=1))[0]
+    if len(rows) == 0:
+        return O, lse
+    for h in range(Hq):
+        g = kvh[h]
+        s = (Q[rows, h, :] @ K[:, g, :].T) * scale
+        s = np.where(vis[rows], s, -np.inf)
+        m = np.max(s, axis=1, keepdims=True)
+        l = np.sum(np.exp(s - m), axis=1, keepdims=True)
+        lse_b = m + np.log(l)
+        O[rows, h, :] = np.exp(s - lse_b) @ V[:, g, :]
+        lse[h, rows] = lse_b[:, 0]
+    return O, lse
+
+
+def merge_partials(Oa, lse_a, Ob, lse_b):
+    """Ring-step combine ("online softmax compatible version" of §2.1):
+    lse' = log(exp(lse_a) + exp(lse_b)) computed with max subtraction;
+    O' = exp(lse_a - lse') O_a + exp(lse_b - lse') O_b. O: [S, H, d], lse: [H, S].
+    An empty partial (lse = -inf) is the identity."""
+    m = np.maximum(lse_a, lse_b)
+    m_safe = np.where(np.isfinite(m), m, 0.0)
+    wa = np.exp(lse_a - m_safe)                 # exp(-inf) = 0 for an empty side
+    wb = np.exp(lse_b - m_safe)
+    tot = wa + wb
+    lse = np.where(tot > 0, m_safe + np.log(np.where(tot > 0, tot, 1.0)), -np.inf)
+    ca = np.where(tot > 0, wa / np.where(tot > 0, tot, 1.0), 0.0)
+    cb = np.where(tot > 0, wb / np.where(tot > 0, tot, 1.0), 0.0)
+    O = ca.T[:, :, None] * Oa + cb.T[:, :, None] * Ob
+    return O, lse
+
+
+def attn_bwd_block(Q, K, V, dO, lse, Dv, q_pos0, k_pos0, causal=True, kv_of_head=None):
+    """Gradient contributions of one ring step (the ring-attention backward): with the
+    final (merged) lse of the query rows and D_i = <dO_i, O_i> of the final O,
+    P_ij = exp(s_ij - lse_i) on the block's visible pairs, dV_j = sum_i P_ij dO_i,
+    dP_ij = <dO_i, V_j>, dS_ij = P_ij (dP_ij - D_i), dQ_i = (1/sqrt d) sum_j dS_ij K_j,
+    dK_j = (1/sqrt d) sum_i dS_ij Q_i (S:51-55 restricted to the block's keys; the sums
+    over blocks are the un-sharded gradients). lse: [Hq, Sq], Dv: [Sq, Hq].
+    Returns (dQ [Sq,Hq,d], dK [Skv,Hkv,d], dV [Skv,Hkv,d])."""
+    Sq, Hq, d = Q.shape
+    Skv, Hkv, _ = K.shape
+    kvh = _kv_map(Hq, Hkv, kv_of_head)
+    scale = 1.0 / math.sqrt(d)
+    qpos = q_pos0 + np.arange(Sq)
+    kpos = k_pos0 + np.arange(Skv)
+    vis = (kpos[None, :] <= qpos[:, None]) if causal else np.ones((Sq, Skv), dtype=bool)
+    dQ = np.zeros_like(Q)
+    dK = np.zeros_like(K)
+    dV = np.zeros_like(V)
+    for h in range(Hq):
+        g = kvh[h]
+        s = (Q[:, h, :] @ K[:, g, :].T) * scale
+        P = np.where(vis, np.exp(np.where(vis, s, 0.0) - lse[h][:, None]), 0.0)
+        dV[:, g, :] += P.T @ dO[:, h, :]
+        dP = dO[:, h, :] @ V[:, g, :].T
+        dS = P * (dP - Dv[:, h][:, None])
+        dQ[:, h, :] = (dS @ K[:, g, :]) * scale
+        dK[:, g, :] += (dS.T @ Q[:, h, :]) * scale
+    return dQ, dK, dV
+
+
+def _hybrid_groups(S, a, r):
+    """Rank g = i a + u (ring index i, Ulysses index u) holds tokens [g S_l, (g+1) S_l);
+    Ulysses group i = ranks i a .. i a + a - 1 holds the contiguous ring block
+    [i S_b, (i+1) S_b), S_b = S / r (DESIGN A27)."""
+    C = a * r
+    if S % C:
+        raise ValueError("S % (a r) != 0")
+    return S // C, S // r
+
+
+def hybrid_forward(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, a, r, U, causal=True):
+    """UPipe inside each Ulysses group of a ranks, Ring Attention across the r groups
+    (USP layout). Per stage (the GQA schedule of the group, C -> a):
+    the group's ranks project their shards, inp_all_to_all inside the group gives rank
+    (i, u) its heads over ring block i; the ring then visits the K/V blocks
+    j = i, i-1, ... (mod r) and merges the partials (merge_partials); blocks j > i are
+    invisible under the causal mask. out_all_to_all inside the group; O into the
+    pre-allocated output, Y accumulated. Returns (Y [S,D], O [S,Hq d], lse [Hq,S])."""
+    S, D = X.shape
+    Sl, Sb = _hybrid_groups(S, a, r)
+    stages = gqa_schedule(Hq, Hkv, a, U)
+    R = Hq // Hkv
+    Xs = [X[g * Sl:(g + 1) * Sl] for g in range(a * r)]
+    O_buf = [np.zeros((Sl, Hq * d)) for _ in range(a * r)]
+    Y_acc = [np.zeros((Sl, D)) for _ in range(a * r)]
+    lse_all = np.zeros((Hq, S))
+    kv_res = [[None] * a for _ in range(r)]
+    for st in stages:
+        Qh, Oh = [], []
+        for i in range(r):
+            grp = [Xs[i * a + u] for u in range(a)]
+            qsh = [{h: grp[u] @ Wq[h * d:(h + 1) * d].T for h in st.heads} for u in range(a)]
+            Qh.append(a2a_seq_to_head(qsh, st.q_heads))
+            if any(st.kv_sent[u] for u in range(a)):
+                kv_heads = [st.kv_heads[u] for u in range(a)]
+                all_kv = sorted({g for u in range(a) for g in kv_heads[u]})
+                ksh = [{g: grp[u] @ Wk[g * d:(g + 1) * d].T for g in all_kv} for u in range(a)]
+                vsh = [{g: grp[u] @ Wv[g * d:(g + 1) * d].T for g in all_kv} for u in range(a)]
+                Kh, Vh = a2a_seq_to_head(ksh, kv_heads), a2a_seq_to_head(vsh, kv_heads)
+                kv_res[i] = [(kv_heads[u], Kh[u], Vh[u]) for u in range(a)]
+        for i in range(r):
+            Oi = []
+            for u in range(a):
+                kvlist = kv_res[i][u][0]
+                kmap = [kvlist.index(h // R) for h in st.q_heads[u]]
+                Oacc, lacc = None, None
+                for t in range(r):                       # ring step t: block j = i - t (mod r)
+                    j = (i - t) % r
+                    _, Kj, Vj = kv_res[j][u]
+                    Op, lp = attn_fwd_block(Qh[i][u], Kj, Vj, i * Sb, j * Sb, causal, kmap)
+                    Oacc, lacc = (Op, lp) if t == 0 else merge_partials(Oacc, lacc, Op, lp)
+                Oi.append(Oacc)
+                for jj, h in enumerate(st.q_heads[u]):
+                    lse_all[h, i * Sb:(i + 1) * Sb] = lacc[jj]
+            Oh.append(Oi)
+        for i in range(r):
+            Os = a2a_head_to_seq(Oh[i], st.q_heads, a)
+            for u in range(a):
+                g = i * a + u
+                for h in st.heads:
+                    O_buf[g][:, h * d:(h + 1) * d] = Os[u][h]
+                    Y_acc[g] += Os[u][h] @ Wo[:, h * d:(h + 1) * d].T
+    return np.concatenate(Y_acc, 0), np.concatenate(O_buf, 0), lse_all
+
+
+def hybrid_backward(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, a, r, U, causal=True):
+    """Backward of hybrid_forward: per stage the group recomputes Q/K/V and sends
+    dO seq->head inside the group; D_i = <dO_i, O_i> from the final O; the ring visits
+    the K/V blocks again and each step adds its attn_bwd_block contributions to dQ of the
+    local rows and to dK/dV of the visiting block (which travel back to their owner);
+    dQ/dK/dV head->seq inside the group; dX, dW as in upipe_backward; dW summed over all
+    a r ranks. Returns (dX, dWq, dWk, dWv, dWo)."""
+    S, D = X.shape
+    Sl, Sb = _hybrid_groups(S, a, r)
+    C = a * r
+    R = Hq // Hkv
+    stages = gqa_schedule(Hq, Hkv, a, U)
+    _, O_full, lse_full = hybrid_forward(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, a, r, U, causal)
+    Xs = [X[g * Sl:(g + 1) * Sl] for g in range(C)]
+    dYs = [dY[g * Sl:(g + 1) * Sl] for g in range(C)]
+    Os = [O_full[g * Sl:(g + 1) * Sl] for g in range(C)]
+    dX = [np.zeros((Sl, D)) for _ in range(C)]
+    dW = dict(q=np.zeros_like(Wq), k=np.zeros_like(Wk), v=np.zeros_like(Wv), o=np.zeros_like(Wo))
+    kv_state = [None] * r
+
+    def retire(i):
+        heads_of = [s_[0] for s_ in kv_state[i]]
+        dKs = a2a_head_to_seq([s_[3] for s_ in kv_state[i]], heads_of, a)
+        dVs = a2a_head_to_seq([s_[4] for s_ in kv_state[i]], heads_of, a)
+        for u in range(a):
+            g = i * a + u
+            for kvh in sorted({k for hs in heads_of for k in hs}):
+                dX[g] += dKs[u][kvh] @ Wk[kvh * d:(kvh + 1) * d] + dVs[u][kvh] @ Wv[kvh * d:(kvh + 1) * d]
+                dW["k"][kvh * d:(kvh + 1) * d] += dKs[u][kvh].T @ Xs[g]
+                dW["v"][kvh * d:(kvh + 1) * d] += dVs[u][kvh].T @ Xs[g]
+
+    for st in stages:
+        if any(st.kv_sent[u] for u in range(a)):
+            for i in range(r):
+                if kv_state[i] is not None:
+                    retire(i)
+                grp = [Xs[i * a + u] for u in range(a)]
+                kv_heads = [st.kv_heads[u] for u in range(a)]
+                all_kv = sorted({g for u in range(a) for g in kv_heads[u]})
+                ksh = [{g: grp[u] @ Wk[g * d:(g + 1) * d].T for g in all_kv} for u in range(a)]
+                vsh = [{g: grp[u] @ Wv[g * d:(g + 1) * d].T for g in all_kv} for u in range(a)]
+                Kh, Vh = a2a_seq_to_head(ksh, kv_heads), a2a_seq_to_head(vsh, kv_heads)
+                kv_state[i] = [(kv_heads[u], Kh[u], Vh[u], np.zeros_like(Kh[u]), np.zeros_like(Vh[u]))
+                               for u in range(a)]
+        Qh, dOh, Dh = [], [], []
+        for i in range(r):
+            grp = [i * a + u for u in range(a)]
+            qsh = [{h: Xs[g] @ Wq[h * d:(h + 1) * d].T for h in st.heads} for g in grp]
+            dosh = [{h: dYs[g] @ Wo[:, h * d:(h + 1) * d] for h in st.heads} for g in grp]
+            osh = [{h: Os[g][:, h * d:(h + 1) * d] for h in st.heads} for g in grp]
+            Qh.append(a2a_seq_to_head(qsh, st.q_heads))
+            dOh.append(a2a_seq_to_head(dosh, st.q_heads))
+            Oh = a2a_seq_to_head(osh, st.q_heads)
+            Dh.append([rowdot(dOh[i][u], Oh[u]) for u in range(a)])
+        dQh = [[None] * a for _ in range(r)]
+        for i in range(r):
+            for u in range(a):
+                kvlist = kv_state[i][u][0]
+                kmap = [kvlist.index(h // R) for h in st.q_heads[u]]
+                lse_i = np.stack([lse_full[h, i * Sb:(i + 1) * Sb] for h in st.q_heads[u]])
+                dq = np.zeros_like(Qh[i][u])
+                for t in range(r):
+                    j = (i - t) % r
+                    _, Kj, Vj, dKj, dVj = kv_state[j][u]
+                    bq, bk, bv = attn_bwd_block(Qh[i][u], Kj, Vj, dOh[i][u], lse_i, Dh[i][u],
+                                                i * Sb, j * Sb, causal, kmap)
+                    dq += bq
+                    dKj += bk
+                    dVj += bv
+                dQh[i][u] = dq
+        for i in range(r):
+            dQs = a2a_head_to_seq(dQh[i], st.q_heads, a)
+            for u in range(a):
+                g = i * a + u
+                for h in st.heads:
+                    dX[g] += dQs[u][h] @ Wq[h * d:(h + 1) * d]
+                    dW["q"][h * d:(h + 1) * d] += dQs[u][h].T @ Xs[g]
+                    dW["o"][:, h * d:(h + 1) * d] += dYs[g].T @ Os[g][:, h * d:(h + 1) * d]
+    for i in range(r):
+        retire(i)
+    return np.concatenate(dX, 0), dW["q"], dW["k"], dW["v"], dW["o"]
 
 
 # ----------------------------------------------------------------------------

@@ -454,3 +454,127 @@ def test_row_sampled_layer_matches_full_with_rope():
     w = 17
     np.testing.assert_allclose(O.layer_bwd_tail(X[-w:], dY[-w:], K, V, Wq, Wk, Wv, Wo, Hq, Hkv, d, rope_base=base),
                                dX[-w:], atol=1e-11)
+
+
+# ---------------------------------------------------------------- ring blocks and the hybrid (N4)
+
+def _partial(rng_rows, H=2, d=3):
+    return rand(rng_rows, H, d), rand(H, rng_rows)
+
+
+def test_merge_empty_partial_is_identity():
+    # merge(p, empty-sentinel) = p (both argument orders)
+    Op, lp = _partial(5)
+    empty_O, empty_l = np.zeros_like(Op), np.full_like(lp, -np.inf)
+    for a, b in (((Op, lp), (empty_O, empty_l)), ((empty_O, empty_l), (Op, lp))):
+        Om, lm = O.merge_partials(*a, *b)
+        np.testing.assert_array_equal(lm, lp)
+        np.testing.assert_allclose(Om, Op, rtol=0, atol=0)
+    Om, lm = O.merge_partials(empty_O, empty_l, empty_O, empty_l)
+    assert np.all(np.isneginf(lm)) and np.all(Om == 0)
+
+
+def test_merge_equal_halves():
+    # merge(p, p) has lse' = lse + ln 2 and out' = out
+    Op, lp = _partial(7)
+    Om, lm = O.merge_partials(Op, lp, Op, lp)
+    np.testing.assert_allclose(lm, lp + math.log(2.0), rtol=0, atol=1e-14)
+    np.testing.assert_allclose(Om, Op, rtol=0, atol=1e-14)
+
+
+def test_merge_two_single_key_partials_is_two_key_softmax():
+    # partials of one key each == softmax attention over both keys (brute force)
+    d = 4
+    q, k0, k1, v0, v1 = (rand(d) for _ in range(5))
+    s0, s1 = q @ k0 / math.sqrt(d), q @ k1 / math.sqrt(d)
+    # a single-key partial: O = v, lse = s (softmax over one key)
+    Om, lm = O.merge_partials(v0[None, None], np.array([[s0]]), v1[None, None], np.array([[s1]]))
+    w0, w1 = math.exp(s0), math.exp(s1)
+    np.testing.assert_allclose(Om[0, 0], (w0 * v0 + w1 * v1) / (w0 + w1), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(lm[0, 0], math.log(w0 + w1), rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("cuts", [(0, 6, 13, 20), (0, 10, 20), (0, 3, 4, 17, 20)])
+def test_blocks_merge_to_full_attention(causal, cuts):
+    # merging the per-key-block partials in ring order (own block first) reproduces attn_fwd over
+    # all keys (the method exactness of ring attention); blocks after the query block are
+    # fully masked under causality and merge as the identity
+    S, Hq, Hkv, d = 20, 4, 2, 3
+    Q, K, V = rand(S, Hq, d), rand(S, Hkv, d), rand(S, Hkv, d)
+    Of, lf = O.attn_fwd(Q, K, V, causal)
+    nb = len(cuts) - 1
+    for i in range(nb):
+        q0, q1 = cuts[i], cuts[i + 1]
+        Oacc = lacc = None
+        for t in range(nb):
+            j = (i - t) % nb
+            k0, k1 = cuts[j], cuts[j + 1]
+            Op, lp = O.attn_fwd_block(Q[q0:q1], K[k0:k1], V[k0:k1], q0, k0, causal)
+            Oacc, lacc = (Op, lp) if t == 0 else O.merge_partials(Oacc, lacc, Op, lp)
+        np.testing.assert_allclose(Oacc, Of[q0:q1], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(lacc, lf[:, q0:q1], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_block_gradients_sum_to_attn_bwd(causal):
+    # the ring backward: per (query block, key block) contributions with the FINAL lse and D sum
+    # to attn_bwd (itself pinned by finite differences and torch autograd)
+    S, Hq, Hkv, d = 18, 4, 2, 3
+    Q, K, V, dO = rand(S, Hq, d), rand(S, Hkv, d), rand(S, Hkv, d), rand(S, Hq, d)
+    gq, gk, gv = O.attn_bwd(Q, K, V, dO, causal)
+    Of, lf = O.attn_fwd(Q, K, V, causal)
+    Dv = O.rowdot(dO, Of)
+    cuts = (0, 5, 12, 18)
+    dQ, dK, dV = np.zeros_like(Q), np.zeros_like(K), np.zeros_like(V)
+    for i in range(3):
+        q0, q1 = cuts[i], cuts[i + 1]
+        for j in range(3):
+            k0, k1 = cuts[j], cuts[j + 1]
+            bq, bk, bv = O.attn_bwd_block(Q[q0:q1], K[k0:k1], V[k0:k1], dO[q0:q1], lf[:, q0:q1], Dv[q0:q1],
+                                          q0, k0, causal)
+            dQ[q0:q1] += bq
+            dK[k0:k1] += bk
+            dV[k0:k1] += bv
+    np.testing.assert_allclose(dQ, gq, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(dK, gk, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(dV, gv, rtol=0, atol=1e-12)
+
+
+HYB = [(8, 2, 1, 2, 2), (8, 2, 2, 2, 2), (8, 2, 2, 2, 4), (8, 4, 1, 4, 4), (8, 4, 2, 2, 2),
+       (16, 4, 2, 2, 8), (8, 8, 4, 1, 4), (8, 2, 2, 1, 2)]
+
+
+@pytest.mark.parametrize("Hq,Hkv,a,r,U", HYB)
+def test_hybrid_sim_equals_unsharded(Hq, Hkv, a, r, U):
+    # UPipe x Ring (a Ulysses ranks per group, r ring groups) is exact: equal to the
+    # un-sharded layer for every split, forward and backward
+    S, D, d = 16, 12, 4
+    X, Wq, Wk, Wv = rand(S, D), rand(Hq * d, D, scale=.4), rand(Hkv * d, D, scale=.4), rand(Hkv * d, D, scale=.4)
+    Wo, dY = rand(D, Hq * d, scale=.4), rand(S, D)
+    Y, Ob, lse = O.layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d)
+    Y2, Ob2, lse2 = O.hybrid_forward(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, a, r, U)
+    np.testing.assert_allclose(Y2, Y, atol=1e-12)
+    np.testing.assert_allclose(Ob2, Ob, atol=1e-12)
+    np.testing.assert_allclose(lse2, lse, atol=1e-12)
+    g1 = O.layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d)
+    g2 = O.hybrid_backward(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, a, r, U)
+    for x2, x1 in zip(g2, g1):
+        np.testing.assert_allclose(x2, x1, atol=1e-11)
+
+
+def test_hybrid_degenerate_compositions():
+    # a = C, r = 1 is UPipe/Ulysses itself (bitwise: same operations in the same order);
+    # a = 1, r = C is pure ring attention (equal to the oracle)
+    Hq, Hkv, d, S, D = 8, 2, 4, 16, 12
+    X, Wq, Wk, Wv = rand(S, D), rand(Hq * d, D, scale=.4), rand(Hkv * d, D, scale=.4), rand(Hkv * d, D, scale=.4)
+    Wo = rand(D, Hq * d, scale=.4)
+    for U in (2, 4, 8):
+        a = O.hybrid_forward(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, 2, 1, U)
+        b = O.upipe_forward(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, 2, U)
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
+    ring = O.hybrid_forward(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, 1, 4, 8)
+    ref = O.layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d)
+    for x, y in zip(ring, ref):
+        np.testing.assert_allclose(x, y, atol=1e-12)
