@@ -85,6 +85,14 @@ typedef struct {
   float rope_base;     /* 0: no rotary embedding; > 1: RoPE on Q and K at their global token positions
                           with angles p * rope_base^(-2i/d) on head-dim pairs (2i, 2i+1) (P:241,
                           SURVEY N3, DESIGN A26; Llama3: 500000). The ctx keeps the rotation tables. */
+  int32_t ring_degree; /* r: UPipe x Ring hybrid (P:166 USP; DESIGN A27). 0 or 1:
+                          plain UPipe over all C ranks. r > 1: C % r == 0; ranks g = i*a + u (a = C/r)
+                          form r Ulysses groups of a consecutive ranks; group i holds the contiguous
+                          ring block [i*S_b, (i+1)*S_b), S_b = a*S_l. Every constraint above that
+                          names C then applies to a (U % a, Hkv % a, ...). Heads are resharded by
+                          all-to-all inside the group; K/V blocks (and, in backward, their fp32
+                          gradient accumulators) travel around the ring of the r ranks that share u,
+                          and the partial outputs are merged by their log-sum-exp. */
 } upipe_shape_t;
 
 #define UPIPE_UID_BYTES 128
@@ -148,7 +156,8 @@ UPIPE_API upipe_status_t upipe_validate(int cp_size, const upipe_shape_t* shape,
  *  y         [S_l, D]      bf16  out
  *  o_saved   [S_l, Hq*d]   bf16  out: attention output before Wo (saved for backward)
  *  lse_saved [Hq/C, S]     fp32  out: natural-log LSE of this rank's heads, slot s*qpd + j
- *                                for local head j of stage s (A12, A17)
+ *                                for local head j of stage s (A12, A17). Ring hybrid (r > 1):
+ *                                [Hq/a, S_b] over the rank's ring block (same element count)
  *  workspace: >= upipe_workspace_size(C, shape, 0) bytes, 256-byte aligned. */
 UPIPE_API upipe_status_t upipe_attn_fwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const upipe_bf16* x, const upipe_bf16* wq,
                               const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo, upipe_bf16* y,

@@ -31,8 +31,9 @@ using namespace dev;
 
 struct FwdArgs {
   __nv_bfloat16* o;
+  float* o32;        // non-null: O written in fp32 here instead (ring-hybrid partials, merged by LSE)
   float* lse;
-  long long S, ldo, ld_lse;
+  long long S, ldo, ldo32, ld_lse;
   int nq, nkv, causal, n_pairs;
   float scale_log2;  // log2(e) / sqrt(d)
   long long* dbg;    // UPIPE_FWD_TIMELINE=1: per-role cycle totals of CTA (0, 0)
@@ -365,7 +366,13 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t r[32];
       tmem_ld32(tO + c * 32, r);
       tmem_wait_ld();
-      if (valid) {
+      if (valid && a.o32) {
+        float4* dst = reinterpret_cast<float4*>(a.o32 + q * a.ldo32 + (long long)head * D + c * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          dst[i] = make_float4(__uint_as_float(r[4 * i + 0]) * inv, __uint_as_float(r[4 * i + 1]) * inv,
+                               __uint_as_float(r[4 * i + 2]) * inv, __uint_as_float(r[4 * i + 3]) * inv);
+      } else if (valid) {
         uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -400,9 +407,11 @@ cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err
   if (!make_tmap_3d(&tv, p.v, p.d, p.nkv, p.S, p.d, p.ldkv, 64, 1, 128, err, errlen)) return cudaErrorInvalidValue;
   FwdArgs a;
   a.o = reinterpret_cast<__nv_bfloat16*>(p.o);
+  a.o32 = p.o32;
   a.lse = p.lse;
   a.S = p.S;
   a.ldo = p.ldo;
+  a.ldo32 = p.ldo32;
   a.ld_lse = p.ld_lse;
   a.nq = p.nq;
   a.nkv = p.nkv;

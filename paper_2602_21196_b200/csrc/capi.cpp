@@ -151,7 +151,7 @@ upipe_status_t upipe_workspace_size(int cp_size, const upipe_shape_t* shape, int
   if (st != UPIPE_OK) return set_err(nullptr, st, m);
   if (!bytes || pass < 0 || pass > 3) return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "pass must be 0..3");
   const Plan P = make_plan(cp_size, *shape);
-  const bool ov = pass < 2 && cp_size > 1;   // 0/1: default (overlapped for C > 1); 2/3: sequential
+  const bool ov = pass < 2 && P.C > 1 && P.ring == 1;   // 0/1: default (overlapped for C > 1); 2/3: sequential
   *bytes = (pass & 1) == 0 ? fwd_workspace(P, ov).total : bwd_workspace(P, ov).total;
   return UPIPE_OK;
 }
@@ -162,7 +162,7 @@ upipe_status_t upipe_plan_stage(int cp_size, const upipe_shape_t* shape, int sta
   upipe_status_t st = validate_shape(cp_size, shape, m);
   if (st != UPIPE_OK) return set_err(nullptr, st, m);
   const Plan P = make_plan(cp_size, *shape);
-  if (!out || stage < 0 || stage >= P.nstages || device < 0 || device >= cp_size)
+  if (!out || stage < 0 || stage >= P.nstages || device < 0 || device >= P.C)   // device: Ulysses index
     return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "stage or device out of range");
   out->n_stages = P.nstages;
   out->qpd = P.qpd;
@@ -187,7 +187,7 @@ upipe_status_t upipe_attn_fwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "tensors must be 16-byte aligned, workspace 256-byte aligned");
   Plan P = make_plan(ctx->C, *shape);
   P.naive = (ctx->flags & UPIPE_FLAG_NAIVE_KV) != 0;
-  if (ws_bytes < fwd_workspace(P, overlap_enabled(ctx->flags, ctx->C)).total)
+  if (ws_bytes < fwd_workspace(P, overlap_enabled(ctx->flags, P)).total)
     return set_err(ctx, UPIPE_ERR_WORKSPACE, "ws_bytes < upipe_workspace_size(pass=0, or 2 with UPIPE_FLAG_SYNC_COMM)");
   cudaSetDevice(ctx->device);
   return layer_fwd(ctx, P, x, wq, wk, wv, wo, y, o_saved, lse_saved, static_cast<char*>(workspace),
@@ -210,7 +210,7 @@ upipe_status_t upipe_attn_bwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "tensors must be 16-byte aligned, workspace 256-byte aligned");
   Plan P = make_plan(ctx->C, *shape);
   P.naive = (ctx->flags & UPIPE_FLAG_NAIVE_KV) != 0;
-  if (ws_bytes < bwd_workspace(P, overlap_enabled(ctx->flags, ctx->C)).total)
+  if (ws_bytes < bwd_workspace(P, overlap_enabled(ctx->flags, P)).total)
     return set_err(ctx, UPIPE_ERR_WORKSPACE, "ws_bytes < upipe_workspace_size(pass=1, or 3 with UPIPE_FLAG_SYNC_COMM)");
   cudaSetDevice(ctx->device);
   return layer_bwd(ctx, P, x, wq, wk, wv, wo, dy, o_saved, lse_saved, dx, dwq, dwk, dwv, dwo, reduce_dw,

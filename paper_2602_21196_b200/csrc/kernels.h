@@ -91,6 +91,8 @@ struct AttnFwdProblem {
   void* o; float* lse;
   int64_t S; int nq, nkv, d; int causal;
   int64_t ldq, ldkv, ldo, ld_lse;
+  float* o32 = nullptr;        // non-null: O in fp32 at o32 + t*ldo32 + j*d instead of bf16 (ring partials)
+  int64_t ldo32 = 0;
 };
 cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err, size_t errlen);
 
@@ -120,6 +122,11 @@ cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t l
                              float scale, cudaStream_t s, const RopeRef& inverse_rope);
 cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
                              float scale, cudaStream_t s);
+// Ring-step combine (DESIGN A27), per row t and head j of [rows][nheads][d]:
+//   lse' = log(e^lse_acc + e^lse_part) (max-subtracted), O' = e^(lse_acc-lse') O_acc + e^(lse_part-lse') O_part,
+// O fp32, lse [nheads][ld_lse]; writes o_acc and lse_acc in place.
+cudaError_t merge_partials_run(float* o_acc, const float* o_part, int64_t ld_o, float* lse_acc, const float* lse_part,
+                               int64_t ld_lse, int64_t rows, int nheads, int d, cudaStream_t s);
 // Column scatter: dst[t][col_of(seg)+e] = src[seg][t][e]   (unpack of the out all-to-all)
 cudaError_t unpack_cols_run(const void* src, int64_t rows, int nseg, int seg_cols, void* dst, int64_t ldd,
                             int64_t col_base, int64_t col_stride, cudaStream_t s);

@@ -125,7 +125,7 @@ upipe_status_t ensure_rope(upipe_ctx_s* ctx, const Plan& P, RopeRef& ref) {
   ref = RopeRef{};
   if (P.sh.rope_base == 0.f) return UPIPE_OK;
   RopeTables& T = ctx->rope;
-  const int64_t n_hi = (P.S + 1023) / 1024;
+  const int64_t n_hi = (P.S * P.ring + 1023) / 1024;     // positions of the whole sequence (all ring blocks)
   if (T.base != P.sh.rope_base || T.d != P.d || T.n_hi < n_hi) {
     if (T.hi) cudaFree(T.hi);
     if (T.lo) cudaFree(T.lo);
@@ -185,17 +185,22 @@ upipe_status_t ensure_pipe(upipe_ctx_s* ctx) {
 // ============================================================================ forward
 upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf16p wk, bf16p wv, bf16p wo,
                          upipe_bf16* y, upipe_bf16* o_saved, float* lse_saved, char* ws, cudaStream_t st) {
-  const bool ov = overlap_enabled(ctx->flags, P.C);
+  const bool ov = overlap_enabled(ctx->flags, P);
   if (ov) {
     if (upipe_status_t s = ensure_pipe(ctx)) return s;
   }
   Runner R{ctx};
   Transport& T = *ctx->transport;
   const FwdWs W = fwd_workspace(P, ov);
-  RopeRef rope_seq;                        // projections: rows are this rank's tokens me*S_l + t
+  RopeRef rope_seq;                        // projections: rows are this rank's tokens rank*S_l + t
   if (upipe_status_t s = ensure_rope(ctx, P, rope_seq)) return s;
   rope_seq.pos0 = (int64_t)ctx->rank * P.S_l;
-  const int C = P.C, me = ctx->rank, d = P.d;
+  // Ulysses group of the ring hybrid (DESIGN A27): ranks [first, first + C); plain UPipe: first = 0, C = cp_size
+  const int C = P.C, me = ctx->rank % P.C, d = P.d;
+  const int ring_i = ctx->rank / P.C, first = ring_i * P.C;
+  auto a2a = [&](const char* what, const void* snd, void* rcv, size_t bytes, cudaStream_t q) {
+    R.comm(q, what, [&](std::string& m) { return T.alltoall_group(snd, rcv, bytes, first, C, q, m); });
+  };
   const int64_t qseg = (int64_t)P.qpd * d, kseg = (int64_t)P.kv_res * d;
   const int64_t HqD = (int64_t)P.Hq * d, kvrows = (int64_t)P.Hkv * d;
   const size_t qbytes = (size_t)P.S_l * qseg * 2, kbytes = (size_t)P.S_l * kseg * 2;
@@ -219,11 +224,11 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   };
   // F2: inp_all_to_all, Q first, then K and V
   auto inp = [&](int s, int b, cudaStream_t q) {
-    R.comm(q, "a2a Q", [&](std::string& m) { return T.alltoall(ws + W.qsend[b], ws + W.qrecv[b], qbytes, q, m); });
+    a2a("a2a Q", ws + W.qsend[b], ws + W.qrecv[b], qbytes, q);
     if (P.kv_sent(s)) {
       const int kb = kvb(s);
-      R.comm(q, "a2a K", [&](std::string& m) { return T.alltoall(ws + W.ksend, ws + W.krecv[kb], kbytes, q, m); });
-      R.comm(q, "a2a V", [&](std::string& m) { return T.alltoall(ws + W.vsend, ws + W.vrecv[kb], kbytes, q, m); });
+      a2a("a2a K", ws + W.ksend, ws + W.krecv[kb], kbytes, q);
+      a2a("a2a V", ws + W.vsend, ws + W.vrecv[kb], kbytes, q);
     }
   };
   // F3: attention over the full sequence for this device's qpd heads
@@ -248,12 +253,53 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     a.ldq = qseg;
     a.ldkv = kseg;
     a.ld_lse = P.S;
-    R.run(UPIPE_TRACE_ATTN_FWD, q, "attn fwd", [&](char* e) { return attn_fwd_run(a, q, e, 512); });
+    if (P.ring == 1) {
+      R.run(UPIPE_TRACE_ATTN_FWD, q, "attn fwd", [&](char* e) { return attn_fwd_run(a, q, e, 512); });
+      return;
+    }
+    // Ring hybrid (DESIGN A27): this rank's heads over ring block ring_i. Step t visits K/V
+    // block j = ring_i - t (mod r), passed around the ring of the r ranks with the same Ulysses index;
+    // each visible block's partial (fp32 O, lse) is merged by its LSE. Own block first (causal).
+    void* const o_dst = a.o;
+    const int64_t ld_dst = a.ldo;
+    float* const lse_acc = a.lse;
+    a.o32 = (float*)(ws + W.oacc);
+    a.ldo32 = qseg;
+    R.run(UPIPE_TRACE_ATTN_FWD, q, "attn fwd (ring own block)", [&](char* e) { return attn_fwd_run(a, q, e, 512); });
+    const int r = P.ring;
+    const int nxt = ((ring_i + 1) % r) * C + me, prv = ((ring_i + r - 1) % r) * C + me;
+    const size_t kvbytes = (size_t)P.S * kseg * 2;
+    const void* kc = a.k;
+    const void* vc = a.v;
+    for (int t = 1; t < r && R.status == UPIPE_OK; ++t) {
+      char* kn = ws + W.kring[t & 1];
+      char* vn = ws + W.vring[t & 1];
+      R.comm(q, "ring K", [&](std::string& m) { return T.sendrecv(kc, nxt, kn, prv, kvbytes, q, m); });
+      R.comm(q, "ring V", [&](std::string& m) { return T.sendrecv(vc, nxt, vn, prv, kvbytes, q, m); });
+      kc = kn;
+      vc = vn;
+      const int j = (ring_i + r - t) % r;
+      if (P.sh.causal && j > ring_i) continue;           // the whole block lies after every local query
+      AttnFwdProblem b2 = a;
+      b2.k = kn;
+      b2.v = vn;
+      b2.causal = 0;                                      // j < i: every key precedes every local query
+      b2.o32 = (float*)(ws + W.opart);
+      b2.lse = (float*)(ws + W.lsepart);
+      R.run(UPIPE_TRACE_ATTN_FWD, q, "attn fwd (ring block)", [&](char* e) { return attn_fwd_run(b2, q, e, 512); });
+      R.run(UPIPE_TRACE_AUX, q, "merge partials", [&](char*) {
+        return merge_partials_run((float*)(ws + W.oacc), (const float*)(ws + W.opart), qseg, lse_acc,
+                                  (const float*)(ws + W.lsepart), P.S, P.S, P.qpd, d, q);
+      });
+    }
+    R.run(UPIPE_TRACE_AUX, q, "O fp32 -> bf16", [&](char*) {
+      return cvt_f32_bf16_run((const float*)(ws + W.oacc), qseg, o_dst, ld_dst, P.S, qseg, 1.0f, q);
+    });
   };
   // F4: out_all_to_all
   auto outa = [&](int s, int b, cudaStream_t q) {
     (void)s;
-    R.comm(q, "a2a O", [&](std::string& m) { return T.alltoall(ws + W.osend[b], ws + W.orecv[b], qbytes, q, m); });
+    a2a("a2a O", ws + W.osend[b], ws + W.orecv[b], qbytes, q);
   };
   // F5: fill o_saved from the stage's out all-to-all (C == 1: attention wrote it directly)
   auto post = [&](int s, int b, cudaStream_t q) {
@@ -337,18 +383,23 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
 upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf16p wk, bf16p wv, bf16p wo,
                          bf16p dy, bf16p o_saved, const float* lse_saved, upipe_bf16* dx, float* dwq, float* dwk,
                          float* dwv, float* dwo, int reduce_dw, char* ws, cudaStream_t st) {
-  const bool ov = overlap_enabled(ctx->flags, P.C);
+  const bool ov = overlap_enabled(ctx->flags, P);
   if (ov) {
     if (upipe_status_t s = ensure_pipe(ctx)) return s;
   }
   Runner R{ctx};
   Transport& T = *ctx->transport;
   const BwdWs W = bwd_workspace(P, ov);
-  RopeRef rope_seq, rope_head;             // seq layout (projections) / head layout (rows = global tokens)
+  const int C = P.C, me = ctx->rank % P.C, d = P.d;
+  const int ring_i = ctx->rank / P.C, first = ring_i * P.C;   // Ulysses group (DESIGN A27)
+  RopeRef rope_seq, rope_head;             // seq layout (projections) / head layout (rows = the group's tokens)
   if (upipe_status_t s = ensure_rope(ctx, P, rope_seq)) return s;
   rope_head = rope_seq;
+  rope_head.pos0 = (int64_t)ring_i * P.S;
   rope_seq.pos0 = (int64_t)ctx->rank * P.S_l;
-  const int C = P.C, d = P.d;
+  auto a2a = [&](const char* what, const void* snd, void* rcv, size_t bytes, cudaStream_t q) {
+    R.comm(q, what, [&](std::string& m) { return T.alltoall_group(snd, rcv, bytes, first, C, q, m); });
+  };
   const int64_t qseg = (int64_t)P.qpd * d, kseg = (int64_t)P.kv_res * d;
   const int64_t HqD = (int64_t)P.Hq * d, HkvD = (int64_t)P.Hkv * d;
   const size_t qbytes = (size_t)P.S_l * qseg * 2, kbytes = (size_t)P.S_l * kseg * 2;
@@ -454,14 +505,14 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   };
   // B1/B3: Q (+K, V) and dO + delta seq -> head ("during out_all_to_all", Table 4)
   auto inp = [&](int s, int b, cudaStream_t q) {
-    R.comm(q, "a2a Q", [&](std::string& m) { return T.alltoall(ws + W.qsend[b], ws + W.qrecv[b], qbytes, q, m); });
+    a2a("a2a Q", ws + W.qsend[b], ws + W.qrecv[b], qbytes, q);
     if (P.kv_sent(s)) {
       const int kb = kvb(s);
-      R.comm(q, "a2a K", [&](std::string& m) { return T.alltoall(ws + W.ksend, ws + W.krecv[kb], kbytes, q, m); });
-      R.comm(q, "a2a V", [&](std::string& m) { return T.alltoall(ws + W.vsend, ws + W.vrecv[kb], kbytes, q, m); });
+      a2a("a2a K", ws + W.ksend, ws + W.krecv[kb], kbytes, q);
+      a2a("a2a V", ws + W.vsend, ws + W.vrecv[kb], kbytes, q);
     }
-    R.comm(q, "a2a dO", [&](std::string& m) { return T.alltoall(ws + W.dosend[b], ws + W.dorecv[b], qbytes, q, m); });
-    R.comm(q, "a2a delta", [&](std::string& m) { return T.alltoall(ws + W.dsend[b], ws + W.drecv[b], dbytes, q, m); });
+    a2a("a2a dO", ws + W.dosend[b], ws + W.dorecv[b], qbytes, q);
+    a2a("a2a delta", ws + W.dsend[b], ws + W.drecv[b], dbytes, q);
   };
   // B4: attention backward (dK/dV accumulate over the sigma stages sharing the resident K/V), dQ -> bf16
   auto attn = [&](int s, int b, cudaStream_t q) {
@@ -496,7 +547,61 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     bp.kv_accumulate = r > 0;
     bp.kv_write_acc = !last;
     bp.rope = rope_head;
-    R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd", [&](char* e) { return attn_bwd_run(bp, q, e, 512); });
+    if (P.ring == 1) {
+      R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd", [&](char* e) { return attn_bwd_run(bp, q, e, 512); });
+    } else {
+      // Ring hybrid (DESIGN A27): the super-stage's fp32 dK/dV accumulators travel with their K/V block;
+      // each rank adds the contributions of its queries (final lse and delta), dQ accumulates locally
+      // (TMA reduce-add), and after the last hop every accumulator is back with its owner.
+      const int rr = P.ring;
+      const int nxt = ((ring_i + 1) % rr) * C + me, prv = ((ring_i + rr - 1) % rr) * C + me;
+      const size_t kvbytes = (size_t)P.S * kseg * 2;
+      bp.dk_acc = (float*)(ws + W.dkacc);
+      bp.dv_acc = (float*)(ws + W.dvacc);
+      bp.dk_bf16 = bp.dv_bf16 = nullptr;
+      bp.kv_write_acc = 1;
+      R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd (ring own block)", [&](char* e) { return attn_bwd_run(bp, q, e, 512); });
+      const void* kc = bp.k;
+      const void* vc = bp.v;
+      const float* dkc = bp.dk_acc;
+      const float* dvc = bp.dv_acc;
+      for (int t = 1; t <= rr && R.status == UPIPE_OK; ++t) {
+        const bool home = t == rr;                        // last hop: the accumulators return to their owner
+        char* kn = ws + W.kring[t & 1];
+        char* vn = ws + W.vring[t & 1];
+        float* dkn = home ? (float*)(ws + W.dkacc) : (float*)(ws + W.dkring[t & 1]);
+        float* dvn = home ? (float*)(ws + W.dvacc) : (float*)(ws + W.dvring[t & 1]);
+        if (!home) {
+          R.comm(q, "ring K", [&](std::string& m) { return T.sendrecv(kc, nxt, kn, prv, kvbytes, q, m); });
+          R.comm(q, "ring V", [&](std::string& m) { return T.sendrecv(vc, nxt, vn, prv, kvbytes, q, m); });
+        }
+        R.comm(q, "ring dK", [&](std::string& m) { return T.sendrecv(dkc, nxt, dkn, prv, kvbytes * 2, q, m); });
+        R.comm(q, "ring dV", [&](std::string& m) { return T.sendrecv(dvc, nxt, dvn, prv, kvbytes * 2, q, m); });
+        kc = kn;
+        vc = vn;
+        dkc = dkn;
+        dvc = dvn;
+        const int j = (ring_i + rr - t) % rr;
+        if (home || (P.sh.causal && j > ring_i)) continue;
+        AttnBwdProblem b2 = bp;
+        b2.k = kn;
+        b2.v = vn;
+        b2.dk_acc = dkn;
+        b2.dv_acc = dvn;
+        b2.causal = 0;
+        b2.kv_accumulate = 1;
+        R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd (ring block)", [&](char* e) { return attn_bwd_run(b2, q, e, 512); });
+      }
+      if (last) {
+        RopeRef rope_k = rope_head;                       // dK rows are the ring block's keys
+        R.run(UPIPE_TRACE_AUX, q, "cvt dK", [&](char*) {
+          return cvt_f32_bf16_run((const float*)(ws + W.dkacc), kseg, ws + W.dksend, kseg, P.S, kseg, 1.0f, q, rope_k);
+        });
+        R.run(UPIPE_TRACE_AUX, q, "cvt dV", [&](char*) {
+          return cvt_f32_bf16_run((const float*)(ws + W.dvacc), kseg, ws + W.dvsend, kseg, P.S, kseg, 1.0f, q);
+        });
+      }
+    }
     R.run(UPIPE_TRACE_AUX, q, "cvt dQ", [&](char*) {
       return cvt_f32_bf16_run((const float*)(ws + W.dqacc[b]), qseg, ws + W.dqsend[b], qseg, P.S, qseg, 1.0f, q,
                               rope_head);
@@ -504,10 +609,10 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   };
   // B5: dQ head -> seq ("during inp_all_to_all"); dK/dV when the super-stage's K/V retire
   auto outa = [&](int s, int b, cudaStream_t q) {
-    R.comm(q, "a2a dQ", [&](std::string& m) { return T.alltoall(ws + W.dqsend[b], ws + W.dqrecv[b], qbytes, q, m); });
+    a2a("a2a dQ", ws + W.dqsend[b], ws + W.dqrecv[b], qbytes, q);
     if (P.kv_last(s)) {
-      R.comm(q, "a2a dK", [&](std::string& m) { return T.alltoall(ws + W.dksend, ws + W.dkrecv, kbytes, q, m); });
-      R.comm(q, "a2a dV", [&](std::string& m) { return T.alltoall(ws + W.dvsend, ws + W.dvrecv, kbytes, q, m); });
+      a2a("a2a dK", ws + W.dksend, ws + W.dkrecv, kbytes, q);
+      a2a("a2a dV", ws + W.dvsend, ws + W.dvrecv, kbytes, q);
     }
   };
   // B6: dX and dW for the stage's heads (and the retired K/V heads). dX += dQ Wq + dK Wk + dV Wv is
@@ -604,7 +709,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     post(nu - 1, (nu - 1) & 1, st);
   }
   // B7: dW summed over the CP group (the FSDP gradient reduction of P:437, A14)
-  if (reduce_dw && C > 1 && R.status == UPIPE_OK) {
+  if (reduce_dw && T.size() > 1 && R.status == UPIPE_OK) {
     R.comm(st, "allreduce dWq", [&](std::string& m) { return T.allreduce_sum_f32(dwq, (size_t)HqD * P.D, st, m); });
     R.comm(st, "allreduce dWk", [&](std::string& m) { return T.allreduce_sum_f32(dwk, (size_t)HkvD * P.D, st, m); });
     R.comm(st, "allreduce dWv", [&](std::string& m) { return T.allreduce_sum_f32(dwv, (size_t)HkvD * P.D, st, m); });

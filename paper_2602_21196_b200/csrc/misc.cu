@@ -4,6 +4,7 @@
 //   cvt         fp32 accumulator -> bf16 (scaled)             (B5 dQ post, F7/B8 finalize)
 //   unpack_cols out-a2a receive [C][S_l][qpd d] -> o_saved    (F5)
 //   synth_fill  device copy of the counter-based input generator (synth/__init__.py)
+//   merge       ring-step combine of two attention partials by their LSE
 #include <cstdio>
 
 #include "kernels.h"
@@ -54,6 +55,34 @@ __global__ void rowdot_kernel(const __nv_bfloat16* __restrict__ dO, long long ld
 #pragma unroll
     for (int off = LANES / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, LANES);
     if (sub == 0) delta[t * ld_delta + j] = s;
+  }
+}
+
+// One group of LANES = d/4 threads per (token, head), 4 fp32 per thread. Empty partials (lse = -inf)
+// carry weight 0; both empty stays empty.
+template <int LANES>
+__global__ void merge_kernel(float* __restrict__ o_acc, const float* __restrict__ o_part, long long ld_o,
+                             float* __restrict__ lse_acc, const float* __restrict__ lse_part, long long ld_lse,
+                             long long rows, int nheads, int d) {
+  const long long groups = rows * nheads;
+  const int sub = threadIdx.x % LANES;
+  long long gidx = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LANES;
+  const long long gstride = (long long)gridDim.x * blockDim.x / LANES;
+  for (; gidx < groups; gidx += gstride) {
+    const long long t = gidx / nheads;
+    const int j = (int)(gidx % nheads);
+    const float la = lse_acc[(long long)j * ld_lse + t], lb = lse_part[(long long)j * ld_lse + t];
+    const float m = fmaxf(la, lb);
+    const float ms = m == -INFINITY ? 0.f : m;
+    const float wa = expf(la - ms), wb = expf(lb - ms);
+    const float tot = wa + wb;
+    const float ca = tot > 0.f ? wa / tot : 0.f, cb = tot > 0.f ? wb / tot : 0.f;
+    float4* pa = reinterpret_cast<float4*>(o_acc + t * ld_o + (long long)j * d) + sub;
+    const float4 b = *(reinterpret_cast<const float4*>(o_part + t * ld_o + (long long)j * d) + sub);
+    const float4 a = *pa;
+    *pa = make_float4(ca * a.x + cb * b.x, ca * a.y + cb * b.y, ca * a.z + cb * b.z, ca * a.w + cb * b.w);
+    __syncwarp((LANES == 32) ? 0xffffffffu : (((1u << LANES) - 1u) << ((threadIdx.x & 31) / LANES * LANES)));
+    if (sub == 0) lse_acc[(long long)j * ld_lse + t] = tot > 0.f ? ms + logf(tot) : -INFINITY;
   }
 }
 
@@ -118,6 +147,23 @@ cudaError_t rowdot_run(const void* dO, int64_t ld_do, const void* O, int64_t ld_
   } else if (d == 64) {
     rowdot_kernel<8><<<grid_for(groups * 8, kThreads), kThreads, 0, s>>>(
         (const __nv_bfloat16*)dO, ld_do, (const __nv_bfloat16*)O, ld_o, delta, ld_delta, rows, nheads, d);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t merge_partials_run(float* o_acc, const float* o_part, int64_t ld_o, float* lse_acc, const float* lse_part,
+                               int64_t ld_lse, int64_t rows, int nheads, int d, cudaStream_t s) {
+  if (rows <= 0 || nheads <= 0) return cudaSuccess;
+  const int64_t groups = rows * nheads;
+  if (d == 128) {
+    merge_kernel<32><<<grid_for(groups * 32, kThreads), kThreads, 0, s>>>(o_acc, o_part, ld_o, lse_acc, lse_part,
+                                                                          ld_lse, rows, nheads, d);
+  } else if (d == 64) {
+    merge_kernel<16><<<grid_for(groups * 16, kThreads), kThreads, 0, s>>>(o_acc, o_part, ld_o, lse_acc, lse_part,
+                                                                          ld_lse, rows, nheads, d);
   } else {
     return cudaErrorInvalidValue;
   }

@@ -16,6 +16,12 @@ upipe_status_t validate_shape(int C, const upipe_shape_t* sh, std::string& msg) 
   };
   if (!sh) return bad(UPIPE_ERR_INVALID_ARG, "shape == NULL");
   if (C < 1 || C > 64) return bad(UPIPE_ERR_INVALID_ARG, "cp_size must be in [1, 64]");
+  // UPipe x Ring (DESIGN A27): the UPipe constraints below apply to the Ulysses degree a = C / r
+  if (sh->ring_degree < 0 || sh->ring_degree > C) return bad(UPIPE_ERR_INVALID_ARG, "ring_degree must be in [0, cp_size]");
+  const int ring = sh->ring_degree > 1 ? sh->ring_degree : 1;
+  if (C % ring) return bad(UPIPE_ERR_INVALID_ARG, "cp_size % ring_degree != 0 (C = Ulysses degree x ring degree)");
+  const int C_total = C;
+  C /= ring;
   if (sh->seq_local < 1) return bad(UPIPE_ERR_INVALID_ARG, "seq_local >= 1 required (S = S_l * C, S:239)");
   if (sh->n_q_heads < 1 || sh->n_kv_heads < 1) return bad(UPIPE_ERR_INVALID_ARG, "head counts must be >= 1");
   if (sh->n_q_heads % sh->n_kv_heads) return bad(UPIPE_ERR_INVALID_ARG, "n_q_heads % n_kv_heads != 0 (S:37)");
@@ -33,7 +39,7 @@ upipe_status_t validate_shape(int C, const upipe_shape_t* sh, std::string& msg) 
   const int qpd = sh->chunk_heads / C;
   if (R % qpd && qpd % R)
     return bad(UPIPE_ERR_UNSUPPORTED, "chunk_heads/cp_size and n_q_heads/n_kv_heads must divide one another (DESIGN A8)");
-  const int64_t S = sh->seq_local * C;
+  const int64_t S = sh->seq_local * C_total;
   if (S > (int64_t(1) << 31) - 256) return bad(UPIPE_ERR_UNSUPPORTED, "S >= 2^31 tokens (TMA coordinate range)");
   if ((int64_t)sh->n_q_heads * sh->head_dim > 65536) return bad(UPIPE_ERR_UNSUPPORTED, "n_q_heads*head_dim > 65536");
   msg.clear();
@@ -42,10 +48,12 @@ upipe_status_t validate_shape(int C, const upipe_shape_t* sh, std::string& msg) 
 
 Plan make_plan(int C, const upipe_shape_t& sh) {
   Plan p;
+  p.ring = sh.ring_degree > 1 ? sh.ring_degree : 1;
+  C /= p.ring;                              // the UPipe stage loop runs inside a Ulysses group of a = C / r ranks
   p.C = C;
   p.sh = sh;
   p.S_l = sh.seq_local;
-  p.S = sh.seq_local * C;
+  p.S = sh.seq_local * C;                   // tokens of the group's ring block (all tokens when r = 1)
   p.Hq = sh.n_q_heads;
   p.Hkv = sh.n_kv_heads;
   p.d = sh.head_dim;
@@ -87,6 +95,15 @@ FwdWs fwd_workspace(const Plan& p, bool overlap) {
     w.osend[i] = !comm ? 0 : (fresh ? take(qe) : w.osend[0]);
     w.orecv[i] = !comm ? 0 : (fresh ? take(qe) : w.orecv[0]);
   }
+  if (p.ring > 1) {                         // ring hybrid (sequential schedule): visiting K/V blocks, fp32 O
+    for (int i = 0; i < 2; ++i) {
+      w.kring[i] = take(ke);
+      w.vring[i] = take(ke);
+    }
+    w.oacc = take(qe * 2);
+    w.opart = take(qe * 2);
+    w.lsepart = take((size_t)p.S * p.qpd * 4);
+  }
   w.total = off;
   return w;
 }
@@ -123,8 +140,16 @@ BwdWs bwd_workspace(const Plan& p, bool overlap) {
     w.krecv[i] = !comm ? w.ksend : (fresh ? take(ke) : w.krecv[0]);
     w.vrecv[i] = !comm ? w.vsend : (fresh ? take(ke) : w.vrecv[0]);
   }
-  w.dkacc = p.sigma > 1 ? take(ke * 2) : 0;
-  w.dvacc = p.sigma > 1 ? take(ke * 2) : 0;
+  w.dkacc = p.sigma > 1 || p.ring > 1 ? take(ke * 2) : 0;
+  w.dvacc = p.sigma > 1 || p.ring > 1 ? take(ke * 2) : 0;
+  if (p.ring > 1) {                         // visiting K/V blocks and their travelling fp32 dK/dV accumulators
+    for (int i = 0; i < 2; ++i) {
+      w.kring[i] = take(ke);
+      w.vring[i] = take(ke);
+      w.dkring[i] = take(ke * 2);
+      w.dvring[i] = take(ke * 2);
+    }
+  }
   w.dksend = take(ke);
   w.dvsend = take(ke);
   w.dkrecv = comm ? take(ke) : w.dksend;

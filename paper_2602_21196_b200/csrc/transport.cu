@@ -23,7 +23,17 @@ class SelfTransport final : public Transport {
  public:
   int size() const override { return 1; }
   int rank() const override { return 0; }
-  upipe_status_t alltoall(const void* send, void* recv, size_t bytes, cudaStream_t s, std::string& err) override {
+  upipe_status_t alltoall_group(const void* send, void* recv, size_t bytes, int, int, cudaStream_t s,
+                                std::string& err) override {
+    return copy(send, recv, bytes, s, err);
+  }
+  upipe_status_t sendrecv(const void* send, int, void* recv, int, size_t bytes, cudaStream_t s, std::string& err) override {
+    return copy(send, recv, bytes, s, err);
+  }
+  upipe_status_t allreduce_sum_f32(float*, size_t, cudaStream_t, std::string&) override { return UPIPE_OK; }
+
+ private:
+  static upipe_status_t copy(const void* send, void* recv, size_t bytes, cudaStream_t s, std::string& err) {
     if (send == recv || bytes == 0) return UPIPE_OK;
     cudaError_t e = cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) {
@@ -32,7 +42,6 @@ class SelfTransport final : public Transport {
     }
     return UPIPE_OK;
   }
-  upipe_status_t allreduce_sum_f32(float*, size_t, cudaStream_t, std::string&) override { return UPIPE_OK; }
 };
 
 class NcclTransport final : public Transport {
@@ -43,15 +52,28 @@ class NcclTransport final : public Transport {
   }
   int size() const override { return C_; }
   int rank() const override { return rank_; }
-  upipe_status_t alltoall(const void* send, void* recv, size_t bytes, cudaStream_t s, std::string& err) override {
+  upipe_status_t alltoall_group(const void* send, void* recv, size_t bytes, int first, int n, cudaStream_t s,
+                                std::string& err) override {
     ncclResult_t r = ncclGroupStart();
-    for (int p = 0; p < C_ && r == ncclSuccess; ++p) {
-      r = ncclSend(static_cast<const char*>(send) + p * bytes, bytes, ncclUint8, p, comm_, s);
-      if (r == ncclSuccess) r = ncclRecv(static_cast<char*>(recv) + p * bytes, bytes, ncclUint8, p, comm_, s);
+    for (int p = 0; p < n && r == ncclSuccess; ++p) {
+      r = ncclSend(static_cast<const char*>(send) + p * bytes, bytes, ncclUint8, first + p, comm_, s);
+      if (r == ncclSuccess) r = ncclRecv(static_cast<char*>(recv) + p * bytes, bytes, ncclUint8, first + p, comm_, s);
     }
     ncclResult_t r2 = ncclGroupEnd();
     if (r != ncclSuccess || r2 != ncclSuccess) {
       err = std::string("NCCL all-to-all: ") + ncclGetErrorString(r != ncclSuccess ? r : r2);
+      return UPIPE_ERR_COMM;
+    }
+    return UPIPE_OK;
+  }
+  upipe_status_t sendrecv(const void* send, int dst, void* recv, int src, size_t bytes, cudaStream_t s,
+                          std::string& err) override {
+    ncclResult_t r = ncclGroupStart();
+    if (r == ncclSuccess) r = ncclSend(send, bytes, ncclUint8, dst, comm_, s);
+    if (r == ncclSuccess) r = ncclRecv(recv, bytes, ncclUint8, src, comm_, s);
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess) {
+      err = std::string("NCCL ring send/recv: ") + ncclGetErrorString(r != ncclSuccess ? r : r2);
       return UPIPE_ERR_COMM;
     }
     return UPIPE_OK;
@@ -119,18 +141,32 @@ class FabricTransport final : public Transport {
   int size() const override { return f_->C; }
   int rank() const override { return rank_; }
 
-  upipe_status_t alltoall(const void* send, void* recv, size_t bytes, cudaStream_t s, std::string& err) override {
-    const int C = f_->C;
+  upipe_status_t alltoall_group(const void* send, void* recv, size_t bytes, int first, int n, cudaStream_t s,
+                                std::string& err) override {
     if (!sync_publish(send, s, err)) return UPIPE_ERR_COMM;
-    for (int p = 0; p < C; ++p) {
-      if (p != rank_) cudaStreamWaitEvent(s, f_->ev_a[p], 0);
-      const char* src = static_cast<const char*>(f_->ptr[p]) + (size_t)rank_ * bytes;
+    for (int p = 0; p < n; ++p) {
+      const int peer = first + p;
+      if (peer != rank_) cudaStreamWaitEvent(s, f_->ev_a[peer], 0);
+      const char* src = static_cast<const char*>(f_->ptr[peer]) + (size_t)(rank_ - first) * bytes;
       cudaError_t e = cudaMemcpyAsync(static_cast<char*>(recv) + (size_t)p * bytes, src, bytes,
                                       cudaMemcpyDeviceToDevice, s);
       if (e != cudaSuccess) {
         err = cudaGetErrorString(e);
         return UPIPE_ERR_CUDA;
       }
+    }
+    return finish(s, err) ? UPIPE_OK : UPIPE_ERR_COMM;
+  }
+
+  upipe_status_t sendrecv(const void* send, int dst, void* recv, int src, size_t bytes, cudaStream_t s,
+                          std::string& err) override {
+    (void)dst;                                    // the receiver pulls: rank dst reads our published buffer
+    if (!sync_publish(send, s, err)) return UPIPE_ERR_COMM;
+    if (src != rank_) cudaStreamWaitEvent(s, f_->ev_a[src], 0);
+    cudaError_t e = cudaMemcpyAsync(recv, f_->ptr[src], bytes, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return UPIPE_ERR_CUDA;
     }
     return finish(s, err) ? UPIPE_OK : UPIPE_ERR_COMM;
   }

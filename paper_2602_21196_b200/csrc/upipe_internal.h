@@ -16,7 +16,8 @@ namespace upipe {
 
 // ------------------------------------------------------------------ plan (DESIGN A8)
 struct Plan {
-  int C = 1;
+  int C = 1;                  // Ulysses degree: ranks of one all-to-all group (= cp_size unless ring > 1)
+  int ring = 1;               // ring degree r of the UPipe x Ring hybrid (DESIGN A27); cp_size = C * ring
   upipe_shape_t sh{};
   int64_t S_l = 0, S = 0;
   int R = 1, qpd = 1, kv_res = 1, sigma = 1, nstages = 1;
@@ -46,11 +47,15 @@ Plan make_plan(int C, const upipe_shape_t& sh);
 // [2] = the two buffer sets of the overlapped (pipelined) schedule; in the sequential
 // schedule (or C == 1) index 1 aliases index 0.
 struct FwdWs {
-  size_t qsend[2], qrecv[2], ksend, krecv[2], vsend, vrecv[2], osend[2], orecv[2], total;
+  size_t qsend[2], qrecv[2], ksend, krecv[2], vsend, vrecv[2], osend[2], orecv[2];
+  size_t kring[2], vring[2], oacc, opart, lsepart;   // ring hybrid only
+  size_t total;
 };
 struct BwdWs {
   size_t qsend[2], qrecv[2], ksend, krecv[2], vsend, vrecv[2], dosend[2], dorecv[2], dsend[2], drecv[2], dqacc[2],
-      dqsend[2], dqrecv[2], dkacc, dvacc, dksend, dvsend, dkrecv, dvrecv, dxacc, total;
+      dqsend[2], dqrecv[2], dkacc, dvacc, dksend, dvsend, dkrecv, dvrecv, dxacc;
+  size_t kring[2], vring[2], dkring[2], dvring[2];   // ring hybrid only
+  size_t total;
 };
 FwdWs fwd_workspace(const Plan& p, bool overlap);
 BwdWs bwd_workspace(const Plan& p, bool overlap);
@@ -63,7 +68,17 @@ class Transport {
   virtual int rank() const = 0;
   // Equal-block all-to-all: block p of `send` (bytes at send + p*bytes) goes to rank p, which stores
   // it as block `rank()` of its `recv`. send and recv must not overlap (except C == 1).
-  virtual upipe_status_t alltoall(const void* send, void* recv, size_t bytes, cudaStream_t s, std::string& err) = 0;
+  upipe_status_t alltoall(const void* send, void* recv, size_t bytes, cudaStream_t s, std::string& err) {
+    return alltoall_group(send, recv, bytes, 0, size(), s, err);
+  }
+  // The same inside the group of ranks [first, first + n) (a Ulysses group of the ring hybrid):
+  // block p goes to rank first + p, which stores it as block rank() - first.
+  virtual upipe_status_t alltoall_group(const void* send, void* recv, size_t bytes, int first, int n, cudaStream_t s,
+                                        std::string& err) = 0;
+  // Ring step: `bytes` of `send` go to rank dst while `bytes` from rank src land in `recv` (every
+  // rank calls it together; send and recv must not overlap).
+  virtual upipe_status_t sendrecv(const void* send, int dst, void* recv, int src, size_t bytes, cudaStream_t s,
+                                  std::string& err) = 0;
   virtual upipe_status_t allreduce_sum_f32(float* buf, size_t n, cudaStream_t s, std::string& err) = 0;
 };
 
@@ -121,7 +136,10 @@ struct Pipe {
 }  // namespace upipe
 
 namespace upipe {
-inline bool overlap_enabled(uint32_t flags, int C) { return C > 1 && !(flags & UPIPE_FLAG_SYNC_COMM); }
+// The ring hybrid runs the sequential schedule (its ring steps are issued on the compute stream).
+inline bool overlap_enabled(uint32_t flags, const Plan& P) {
+  return P.C > 1 && P.ring == 1 && !(flags & UPIPE_FLAG_SYNC_COMM);
+}
 }  // namespace upipe
 
 namespace upipe {

@@ -28,7 +28,8 @@ class UpipeError(RuntimeError):
 
 class upipe_shape_t(ctypes.Structure):
     _fields_ = [("seq_local", c_int64), ("hidden", c_int32), ("n_q_heads", c_int32), ("n_kv_heads", c_int32),
-                ("head_dim", c_int32), ("chunk_heads", c_int32), ("causal", c_int32), ("rope_base", ctypes.c_float)]
+                ("head_dim", c_int32), ("chunk_heads", c_int32), ("causal", c_int32), ("rope_base", ctypes.c_float),
+                ("ring_degree", c_int32)]
 
 
 class upipe_stage_info_t(ctypes.Structure):
@@ -113,9 +114,9 @@ def _stream(stream):
 
 
 def make_shape(seq_local, hidden, n_q_heads, n_kv_heads, head_dim, chunk_heads, causal=1,
-               rope_base=0.0) -> upipe_shape_t:
+               rope_base=0.0, ring_degree=0) -> upipe_shape_t:
     return upipe_shape_t(seq_local, hidden, n_q_heads, n_kv_heads, head_dim, chunk_heads, int(causal),
-                         float(rope_base))
+                         float(rope_base), int(ring_degree))
 
 
 # ------------------------------------------------------------------ lifecycle

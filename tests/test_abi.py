@@ -77,10 +77,11 @@ def test_rope_base_validation(U, base, ok):
 
 
 def test_shape_struct_layout_matches_header(U):
-    # the ctypes mirror of upipe_shape_t: 8 + 6*4 + 4 bytes, rope_base last (include/upipe.h)
+    # the ctypes mirror of upipe_shape_t: 8 + 6*4 + 4 + 4 bytes, ring_degree last (include/upipe.h)
     import ctypes
     assert ctypes.sizeof(U.upipe_shape_t) == 40
     assert U.upipe_shape_t.rope_base.offset == 32
+    assert U.upipe_shape_t.ring_degree.offset == 36
 
 
 GRID = [(Hq, Hkv, C, Uc) for Hq, Hkv in ((8, 2), (16, 4), (32, 8), (64, 8), (8, 8), (32, 32))
@@ -133,3 +134,40 @@ def test_workspace_c1_aliases_send_and_recv(U):
     w1 = U.upipe_workspace_size(1, sh, 0)
     # C=1: Q,K,V single buffers (no a2a), no O buffers, no y accumulator (DESIGN A24)
     assert w1 == 1024 * 64 * 2 * (2 + 1 + 1)   # qpd=2 q heads, kv_res=1 K and V
+
+
+# ---------------------------------------------------------------- UPipe x Ring hybrid (DESIGN A27)
+
+@pytest.mark.parametrize("C,ring,shape,status,needle", [
+    (4, 3, (256, 512, 8, 2, 64, 2), 1, "ring_degree"),        # C % r
+    (2, 4, (256, 512, 8, 2, 64, 2), 1, "ring_degree"),        # r > C
+    (2, -1, (256, 512, 8, 2, 64, 2), 1, "ring_degree"),
+    (8, 2, (256, 512, 8, 2, 64, 4), 2, "n_kv_heads % cp_size"),   # the UPipe constraints apply to a = C / r = 4
+    (8, 2, (256, 512, 8, 2, 64, 3), 1, "P:317"),              # U % a
+    (8, 4, (256, 512, 8, 2, 64, 2), 0, ""),                   # a = 2: valid
+    (4, 4, (256, 512, 8, 2, 64, 1), 0, ""),                   # pure ring, a = 1: any U dividing Hq
+])
+def test_ring_validation(U, C, ring, shape, status, needle):
+    st, msg = U.upipe_validate(C, U.make_shape(*shape, 1, 0.0, ring))
+    assert st == status and needle in msg, (st, msg)
+
+
+def test_ring_plan_and_workspace(U):
+    # the stage plan of a ring hybrid is the UPipe plan of one Ulysses group (C -> a); the workspace holds
+    # the group's chunk buffers over the ring block (S_b = a S_l), the sequential schedule, two visiting
+    # K/V blocks, fp32 O accumulator + partial and the partial's lse
+    S_l, D, Hq, Hkv, d, Uc = 1024, 512, 8, 2, 64, 2
+    sh_r = U.make_shape(S_l, D, Hq, Hkv, d, Uc, 1, 0.0, 2)      # C = 4 = 2 x 2
+    sh_g = U.make_shape(S_l, D, Hq, Hkv, d, Uc)                 # one group: C = 2
+    for s in range(4):
+        for p in range(2):
+            a, b = U.upipe_plan_stage(4, sh_r, s, p), U.upipe_plan_stage(2, sh_g, s, p)
+            assert (a.q0, a.kv0, a.kv_sent, a.qpd, a.n_stages) == (b.q0, b.kv0, b.kv_sent, b.qpd, b.n_stages)
+    base = U.upipe_workspace_size(2, sh_g, 2)
+    S_b, qpd, kv_res = 2 * S_l, 1, 1
+    extra = 4 * S_b * kv_res * d * 2 + 2 * S_b * qpd * d * 4 + S_b * qpd * 4
+    assert abs(U.upipe_workspace_size(4, sh_r, 0) - (base + extra)) <= 256 * 6
+    # backward: + fp32 dK/dV accumulators, two visiting K/V blocks and their travelling fp32 accumulators
+    bw = U.upipe_workspace_size(2, sh_g, 3)
+    extra_b = 4 * S_b * kv_res * d * 2 + 4 * S_b * kv_res * d * 4 + (2 * S_b * kv_res * d * 4 if qpd >= Hq // Hkv else 0)
+    assert abs(U.upipe_workspace_size(4, sh_r, 1) - (bw + extra_b)) <= 256 * 12

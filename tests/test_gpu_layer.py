@@ -18,7 +18,7 @@ REL, ABS = 5e-3, 2e-2
 
 
 def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", bwd=True, sync=False, exp_S=None,
-               naive=False, comm_counts=None, rope_base=0.0):
+               naive=False, comm_counts=None, rope_base=0.0, ring=1):
     """Run the layer on C ranks; returns (per-rank outputs, inputs). exp_S: draw the first S tokens of
     a length-exp_S sequence (its value scales), e.g. to keep dY's 1/sqrt(S) scale sane for tiny S."""
     from paper_2602_21196_b200 import UPipeAttention, upipe
@@ -41,7 +41,7 @@ def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", b
             with torch.cuda.stream(stream):
                 if C > 1:
                     attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal, fabric=fabric, cp_rank=r, cp_size=C,
-                                          sync_comm=sync, naive_kv=naive, rope_base=rope_base)
+                                          sync_comm=sync, naive_kv=naive, rope_base=rope_base, ring_degree=ring)
                 else:
                     attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal, naive_kv=naive, rope_base=rope_base)
                 if comm_counts is not None:
@@ -75,7 +75,7 @@ def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", b
     return results, inp
 
 
-def _check(results, inp, C, Hq, Hkv, d, U, causal=True, bwd=True, rope_base=None):
+def _check(results, inp, C, Hq, Hkv, d, U, causal=True, bwd=True, rope_base=None, ring=1):
     x, wq, wk, wv, wo, dy = (inp[k] for k in ("x", "wq", "wk", "wv", "wo", "dy"))
     Y, O, L = oracle.layer_fwd(x, wq, wk, wv, wo, Hq, Hkv, d, causal, rope_base=rope_base)
     y = np.concatenate([to_np(r["y"]) for r in results], 0)
@@ -84,17 +84,20 @@ def _check(results, inp, C, Hq, Hkv, d, U, causal=True, bwd=True, rope_base=None
     assert_close("o_saved", o, O, REL, ABS)
     # lse: rank p holds its heads in slot order s*qpd + j (upipe.h)
     from paper_2602_21196_b200 import upipe
-    sh = upipe.make_shape(x.shape[0] // C, x.shape[1], Hq, Hkv, d, U, int(causal))
+    sh = upipe.make_shape(x.shape[0] // C, x.shape[1], Hq, Hkv, d, U, int(causal), ring_degree=ring)
     info = upipe.upipe_plan_stage(C, sh, 0, 0)
+    a = C // ring                       # ring hybrid: rank i*a + u holds its heads over ring block i
+    Sb = x.shape[0] // ring
     for p in range(C):
         lse_p = to_np(results[p]["lse"])
+        blk = slice((p // a) * Sb, (p // a + 1) * Sb)
         for s in range(info.n_stages):
-            q0 = upipe.upipe_plan_stage(C, sh, s, p).q0
+            q0 = upipe.upipe_plan_stage(C, sh, s, p % a).q0
             for j in range(info.qpd):
                 # layer-level LSE includes the bf16 rounding of Q/K at the a2a boundary (A15). LSE is a log:
                 # the north_star relative bar applies to the normaliser it encodes, rms(exp(dLSE) - 1) <= REL,
                 # with |dLSE| <= ABS (a relative L2 of the log itself is undefined near 0, S = 1)
-                dl = lse_p[s * info.qpd + j] - L[q0 + j]
+                dl = lse_p[s * info.qpd + j] - L[q0 + j][blk]
                 rms = float(np.sqrt(np.mean(np.expm1(dl) ** 2)))
                 assert np.abs(dl).max() <= ABS and rms <= REL, \
                     f"lse[p{p},h{q0 + j}]: max|dLSE| {np.abs(dl).max():.3e}, rms(exp(dLSE)-1) {rms:.3e}"
@@ -234,3 +237,32 @@ def test_rope_layer(C, S, Hq, Hkv, d, Uc, base):
     # S = 2048 gives angles up to ~2000 rad (table composition, not an fp32 angle).
     r, inp = _run_group(C, S, 512, Hq, Hkv, d, Uc, rope_base=base)
     _check(r, inp, C, Hq, Hkv, d, Uc, rope_base=base)
+
+
+# ---------------------------------------------------------------- UPipe x Ring hybrid (DESIGN A27)
+
+@pytest.mark.parametrize("C,ring,U,S,Hq,Hkv,d,D,causal", [
+    (2, 2, 8, 512, 8, 2, 64, 512, True),      # pure ring (a = 1), BASELINE config 1 shape
+    (4, 2, 2, 1024, 8, 2, 64, 512, True),     # 2 Ulysses x 2 ring, UPipe U = a
+    (4, 2, 8, 1024, 8, 2, 128, 256, True),    # 2 x 2, Ulysses within the group (U = Hq), d = 128
+    (4, 4, 4, 1024, 8, 2, 64, 256, True),     # pure ring over 4 blocks
+    (4, 2, 2, 768, 8, 2, 64, 256, False),     # non-causal: every block is visited
+    (8, 2, 4, 1024, 8, 4, 64, 256, True),     # 4 x 2
+])
+def test_ring_hybrid_matches_oracle(C, ring, U, S, Hq, Hkv, d, D, causal):
+    r, inp = _run_group(C, S, D, Hq, Hkv, d, U, causal=causal, ring=ring)
+    _check(r, inp, C, Hq, Hkv, d, U, causal=causal, ring=ring)
+
+
+def test_ring_hybrid_rope():
+    r, inp = _run_group(4, 1024, 256, 8, 2, 64, 2, ring=2, rope_base=10000.0)
+    _check(r, inp, 4, 8, 2, 64, 2, rope_base=10000.0, ring=2)
+
+
+def test_ring_degree_one_is_upipe_bitwise():
+    # ring_degree = 1 is plain UPipe: identical outputs (same kernels, same order)
+    a, _ = _run_group(2, 512, 256, 8, 2, 64, 2, ring=1, sync=True)
+    b, _ = _run_group(2, 512, 256, 8, 2, 64, 2, sync=True)
+    for ra, rb in zip(a, b):
+        for k in ra:
+            assert torch.equal(ra[k], rb[k]), k
