@@ -47,6 +47,8 @@ def parse():
                     help="ablation (SURVEY N1): re-send K/V every stage instead of once per GQA super-stage")
     ap.add_argument("--model", choices=sorted(MODELS), default="llama3-8b",
                     help="layer shape (default: BASELINE's headline Llama3-8B layer)")
+    ap.add_argument("--ring", type=int, default=1,
+                    help="ring degree r of the UPipe x Ring hybrid (N > 1: Ulysses groups of N/r ranks; SURVEY N4)")
     ap.add_argument("--no-ulysses", action="store_true", help="skip the chunk=all-heads Ulysses comparison")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -251,7 +253,7 @@ def main():
         torch.cuda.synchronize()
         base = torch.cuda.memory_allocated()       # inputs and weights only: workspace + outputs count as activation
         attn = UPipeAttention(Hq, Hkv, d, D, chunk, True, process_group=pg, naive_kv=args.naive_kv,
-                              rope_base=args.rope_base)
+                              rope_base=args.rope_base, ring_degree=args.ring)
         out = {}
 
         def step():
@@ -305,8 +307,15 @@ def main():
     peaks = measured_peaks()
     tr = main_run["trace"]
     bwd_ms, bwd_n = tr["attn_bwd"]
-    qpd = U // C
-    flops_bwd_launch = flops_attn_bwd_per_head(S, d) * qpd
+    a_deg = C // args.ring                          # Ulysses degree (C unless the ring hybrid is on)
+    qpd = U // a_deg
+    if args.ring == 1:
+        flops_bwd_launch = flops_attn_bwd_per_head(S, d) * qpd
+    else:
+        # ring hybrid, this rank (ring block i = rank // a): per stage its own causal block plus i full
+        # blocks of S_b = S / r keys; report the mean over those launches
+        S_b, ring_i = S // args.ring, rank // a_deg
+        flops_bwd_launch = 10.0 * d * qpd * (causal_pairs(S_b) + ring_i * S_b * S_b) / (1 + ring_i)
     achieved = flops_bwd_launch / (bwd_ms / bwd_n / 1e3) / 1e12 if bwd_n else None
     traffic = None
     tf = os.path.join(ROOT, "profiles", "attn_bwd_traffic.json")
@@ -325,7 +334,9 @@ def main():
         "config": {"workload": M["workload"] + (" (BASELINE configs[1])" if args.model == "llama3-8b" and S == 131072 else ""),
                    "model": M["name"],
                    "n_q_heads": Hq, "n_kv_heads": Hkv, "head_dim": d, "hidden": D, "seq_len": S, "global_batch": 1,
-                   "chunk_heads": U, "cp": C, "parallelism": f"cp{C} (UPipe, U={U})",
+                   "chunk_heads": U, "cp": C,
+                   "parallelism": f"cp{C} (UPipe, U={U})" if args.ring == 1 else
+                   f"cp{C} = ulysses{C // args.ring} x ring{args.ring} (UPipe x Ring, U={U})",
                    "kv_schedule": "naive (per-stage K/V resend)" if args.naive_kv else "GQA super-stage (P:362-380)",
                    "rope_base": args.rope_base,
                    "l2": f"inputs larger than L2 (x, dy: S_l x {D} bf16 per rank); no flush needed"},
