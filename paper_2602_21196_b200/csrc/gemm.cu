@@ -58,18 +58,21 @@ __device__ __forceinline__ int map_k(const DevOpMap& m, int i, int k) {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int GRANULE_BYTES = 64 * 64 * 2;  // one TMA box: 64 x 64 bf16
-constexpr int RING_BYTES = 192 * 1024;
+#ifndef UPIPE_GEMM_RING_KB
+#define UPIPE_GEMM_RING_KB 192
+#endif
+constexpr int RING_BYTES = UPIPE_GEMM_RING_KB * 1024;
 
-template <int BN>
+template <int BN, bool PAIR = false>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;   // PAIR: this CTA's half of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = RING_BYTES / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
-template <int BN, bool A_MN, bool B_MN, int CL>
+template <int BN, bool A_MN, bool B_MN, int CL, bool PAIR>
 __global__ void __launch_bounds__(192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB0,
@@ -84,7 +87,18 @@ __global__ void __launch_bounds__(192, 1)
   // unit with the same n-block; each loads half of the shared B tile and multicasts it to both,
   // so per SM the ring carries A (16 KB) + B/2 (BN*64 B) per k-block instead of A + B. Each
   // CTA's MMA commit frees the stage in both CTAs (empty barriers count 2 arrivals).
-  using C = Cfg<BN>;
+  // PAIR (cta_group::2, CL = 2): the two CTAs of a cluster run one M = 256 MMA per k-step; each loads
+  // its 128 rows of A and its half of B (no multicast) into its own ring, both loads completing on
+  // the leader's full barrier; the leader issues the MMAs, its commits free the stage in both CTAs and
+  // mark both CTAs' accumulators full; both epilogues release the accumulator to the leader. Per SM
+  // the ring carries A + B/2 per k-block and the tensor pipe works on 128 x BN of a 256 x BN tile.
+  // PAIR with CL = 4: two pairs (ranks 0,1 and 2,3) on four consecutive m-blocks of one n-block share
+  // the B tile: CTA r loads a quarter of B (its pair-half q = r & 1, quarter p = r >> 1) and multicasts it
+  // to itself and CTA r ^ 2 (same half in the other pair); every stage is then written by both pairs,
+  // so each pair leader's commit frees it in all four CTAs (empty barriers count 2 arrivals).
+  static_assert(!PAIR || CL == 2 || CL == 4, "CTA pairs: clusters of 2 or 4");
+  constexpr bool P4 = PAIR && CL == 4;
+  using C = Cfg<BN, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
@@ -103,11 +117,12 @@ __global__ void __launch_bounds__(192, 1)
   const int crank = MC ? (int)cluster_ctarank() : 0;
   const int ms = crank & 1, ns = CL == 4 ? crank >> 1 : 0;
   const int unit0 = blockIdx.x / CL, nunit_step = gridDim.x / CL;
-  const int ntn_u = CL == 4 ? ntn / 2 : ntn;                     // n-units (CL = 4: pairs of n-blocks)
-  const int nunits = ntn_u * (MC ? (ntm + 1) / 2 : ntm);
+  const int ntn_u = CL == 4 && !P4 ? ntn / 2 : ntn;              // n-units (CL = 4: pairs of n-blocks)
+  const int nunits = ntn_u * (P4 ? (ntm + 3) / 4 : (MC ? (ntm + 1) / 2 : ntm));
   const int nk = (g.K + BK - 1) / BK;
-  auto tile_m = [&](int u) { return MC ? (u / ntn_u) * 2 + ms : u / ntn_u; };   // m-block of unit u for this CTA
-  auto tile_n = [&](int u) { return CL == 4 ? (u % ntn_u) * 2 + ns : u % ntn_u; };
+  auto tile_m = [&](int u) { return P4 ? (u / ntn_u) * 4 + crank : (MC ? (u / ntn_u) * 2 + ms : u / ntn_u); };
+  auto tile_n = [&](int u) { return CL == 4 && !P4 ? (u % ntn_u) * 2 + ns : u % ntn_u; };
+  const uint32_t leader = crank & ~1u;                            // PAIR: rank of this CTA's pair leader
   // multicast masks: A to the CTAs sharing this m-block (CL = 4), B to those sharing this n-block;
   // an MMA commit frees the stage in every CTA that writes into this CTA's ring
   const uint16_t maskA = CL == 4 ? (uint16_t)((1u << crank) | (1u << (crank ^ 2))) : 0;
@@ -129,15 +144,18 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL == 4 ? 3 : (MC ? 2 : 1));
+      mbar_init(&empty[s], P4 ? 2 : (PAIR ? 1 : (CL == 4 ? 3 : (MC ? 2 : 1))));
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 128);
+      mbar_init(&acc_empty[i], PAIR ? 256 : 128);   // PAIR: both CTAs' epilogues release the leader's accumulator
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<2 * BN>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_pair<2 * BN>(tmem_slot);
+    else tmem_alloc<2 * BN>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
   if (MC) cluster_sync();                  // peer barriers initialised before any multicast arrives
@@ -154,16 +172,18 @@ __global__ void __launch_bounds__(192, 1)
       // operand part); the k-dependent parts advance incrementally (k / k_len, k % k_len) so the
       // single producer thread does no integer division per k-block.
       constexpr int GA = BM / 64, GB = BN / 64;       // A / B granules (64 rows each)
-      constexpr int GB0 = MC ? GB / 2 : GB;           // B granules this CTA loads (MC: its half)
-      constexpr int GA0 = CL == 4 ? GA / 2 : GA;      // A granules this CTA loads (CL = 4: its half)
+      constexpr int GB0 = P4 ? GB / 4 : (MC ? GB / 2 : GB);   // B granules this CTA loads (MC: half, P4: quarter)
+      constexpr int GA0 = CL == 4 && !P4 ? GA / 2 : GA;       // A granules this CTA loads (CL = 4: its half)
+      static_assert(!P4 || GB0 >= 1, "P4 needs BN = 256");
       for (int u = unit0; u < nunits; u += nunit_step) {
         const int mt = tile_m(u);
         const bool valid = mt < ntm;           // MC: the odd last m-block pairs with an empty tile
         const int m0 = mt * BM, n0 = tile_n(u) * BN;
         const int pm = mpart(m0);
         const int ml0 = m0 - (g.kind == 1 ? g.mcum[pm] : 0);
-        const int cb0 = MC ? ms * GB0 : 0;
-        const int ca0 = CL == 4 ? ns * GA0 : 0;
+        const int cb0 = P4 ? ms * (GB / 2) + ns * GB0 : (MC ? ms * GB0 : 0);   // first B granule (tile rows / 64)
+        const int cbd = P4 ? ns * GB0 : (PAIR ? 0 : cb0);                        // its granule in this CTA's ring
+        const int ca0 = CL == 4 && !P4 ? ns * GA0 : 0;
         int pk = -1, pa = 0, pb = 0;
         int a_out[GA0], a_kb[GA0], b_out[GB0], b_kb[GB0];
         int ka_len = 1, kb_len = 1, kqa_o = 0, kqa_k = 0, kqb_o = 0, kqb_k = 0;
@@ -207,14 +227,23 @@ __global__ void __launch_bounds__(192, 1)
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
             continue;
           }
-          mbar_arrive_expect_tx(&full[stage], (valid ? C::A_BYTES : 0) + C::B_BYTES);
+          const uint32_t full_leader = PAIR ? mapa_shared(&full[stage], leader) : 0;
+          if (!PAIR) {
+            mbar_arrive_expect_tx(&full[stage], (valid ? C::A_BYTES : 0) + C::B_BYTES);
+          } else if (crank == leader) {         // the pair leader expects both CTAs' bytes
+            const bool valid1 = tile_m(u) + 1 < ntm;
+            mbar_arrive_expect_tx(&full[stage], ((valid ? 1 : 0) + (valid1 ? 1 : 0)) * C::A_BYTES + 2 * C::B_BYTES);
+          }
           if (valid) {
 #pragma unroll
             for (int c = 0; c < GA0; ++c) {
               if (c % g.a_box_g) continue;       // covered by the previous (multi-granule) box
               const int oc = a_out[c] + kqa * kqa_o, kc = a_kb[c] + kqa * kqa_k + kra;
               uint8_t* dst = sa + (ca0 + c) * GRANULE_BYTES;
-              if (CL == 4) {
+              if (PAIR) {
+                if (A_MN) tma_load_2d_pair(dst, tA, full_leader, oc, kc);
+                else      tma_load_2d_pair(dst, tA, full_leader, kc, oc);
+              } else if (CL == 4) {
                 if (A_MN) tma_load_2d_mc(dst, tA, &full[stage], oc, kc, maskA);
                 else      tma_load_2d_mc(dst, tA, &full[stage], kc, oc, maskA);
               } else {
@@ -227,8 +256,15 @@ __global__ void __launch_bounds__(192, 1)
           for (int c = 0; c < GB0; ++c) {
             if (c % g.b_box_g) continue;
             const int oc = b_out[c] + kqb * kqb_o, kc = b_kb[c] + kqb * kqb_k + krb;
-            uint8_t* dst = sb + (cb0 + c) * GRANULE_BYTES;
-            if (MC) {
+            uint8_t* dst = sb + (cbd + c) * GRANULE_BYTES;
+            if (P4) {                           // to both pairs; each copy completes on its pair leader's barrier
+              const uint16_t mk = (uint16_t)((1u << crank) | (1u << (crank ^ 2)));
+              if (B_MN) tma_load_2d_pair_mc(dst, tB, &full[stage], oc, kc, mk);
+              else      tma_load_2d_pair_mc(dst, tB, &full[stage], kc, oc, mk);
+            } else if (PAIR) {
+              if (B_MN) tma_load_2d_pair(dst, tB, full_leader, oc, kc);
+              else      tma_load_2d_pair(dst, tB, full_leader, kc, oc);
+            } else if (MC) {
               if (B_MN) tma_load_2d_mc(dst, tB, &full[stage], oc, kc, maskB);
               else      tma_load_2d_mc(dst, tB, &full[stage], kc, oc, maskB);
             } else {
@@ -244,9 +280,9 @@ __global__ void __launch_bounds__(192, 1)
       if (g.dbg && blockIdx.x == 0) g.dbg[0] = tl_prod;
     }
   } else if (warp == 1) {
-    {
+    if (!PAIR || crank == leader) {
       // ---------------- MMA issuer (whole warp; elect.sync inside the MMA asm, see mma_ss_w)
-      constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+      constexpr uint32_t idesc = idesc_bf16(PAIR ? 2 * BM : BM, BN, A_MN, B_MN);
       long long tl_full = 0, tl_acc = 0;
       const long long t_start = clock64();
       int stage = 0;
@@ -270,13 +306,17 @@ __global__ void __launch_bounds__(192, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t da = A_MN ? desc_sw128(sa + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sa + kk * 32, 16, 1024);
             const uint64_t db = B_MN ? desc_sw128(sb + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sb + kk * 32, 16, 1024);
-            if (g.dbg_mode != 3) mma_ss_w(acc, da, db, idesc, (kb | kk) != 0);
+            if (g.dbg_mode == 3) continue;
+            if (PAIR) mma_ss_pair_w(acc, da, db, idesc, (kb | kk) != 0);
+            else mma_ss_w(acc, da, db, idesc, (kb | kk) != 0);
           }
-          if (MC) mma_commit_mc_w(&empty[stage], maskE);   // frees the stage in every CTA writing into ours
+          if (PAIR) mma_commit_pair_w(&empty[stage], P4 ? 0xF : 0x3);  // frees the stage where this pair's data lives
+          else if (MC) mma_commit_mc_w(&empty[stage], maskE);   // frees the stage in every CTA writing into ours
           else mma_commit_w(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit_w(&acc_full[ab]);
+        if (PAIR) mma_commit_pair_w(&acc_full[ab], (uint16_t)(0x3u << leader));
+        else mma_commit_w(&acc_full[ab]);
       }
       if (g.dbg && blockIdx.x == 0 && lane == 0) {
         g.dbg[1] = tl_full;
@@ -344,7 +384,8 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&acc_empty[ab]);
+      if (PAIR && crank != leader) mbar_arrive_cluster(mapa_shared(&acc_empty[ab], leader));
+      else mbar_arrive(&acc_empty[ab]);
     }
   }
   tc_fence_before();
@@ -352,7 +393,8 @@ __global__ void __launch_bounds__(192, 1)
   if (MC) cluster_sync();                  // no CTA leaves while its peer may still signal its barriers
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<2 * BN>(tmem);
+    if constexpr (PAIR) tmem_dealloc_pair<2 * BN>(tmem);
+    else tmem_dealloc<2 * BN>(tmem);
   }
 }
 
@@ -361,10 +403,10 @@ DevOpMap to_dev(const OperandMap& m) {
                   (int)m.k_base, (int)m.k_len, (int)m.k_kstride, (int)m.k_istride};
 }
 
-template <int BN, bool A_MN, bool B_MN, int CL>
+template <int BN, bool A_MN, bool B_MN, int CL, bool PAIR>
 cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs& args, cudaStream_t s) {
-  using C = Cfg<BN>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, CL>;
+  using C = Cfg<BN, PAIR>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, CL, PAIR>;
   static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (attr != cudaSuccess) return attr;
   static const int num_sms = [] {
@@ -379,7 +421,8 @@ cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs&
   cfg.blockDim = dim3(192);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
-  const int units = (CL == 4 ? ntn / 2 : ntn) * (CL > 1 ? (ntm + 1) / 2 : ntm);
+  const int units = PAIR && CL == 4 ? ntn * ((ntm + 3) / 4)
+                                    : (CL == 4 ? ntn / 2 : ntn) * (CL > 1 ? (ntm + 1) / 2 : ntm);
   if (CL > 1) {
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CL;
@@ -406,19 +449,22 @@ cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs&
   return cudaGetLastError();
 }
 
-template <int BN, int CL>
+template <int BN, int CL, bool PAIR = false>
 cudaError_t dispatch_cl(bool amn, bool bmn, const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs& a,
                         cudaStream_t s) {
-  if (!amn && !bmn) return launch<BN, false, false, CL>(ta, tb, a, s);
-  if (!amn && bmn) return launch<BN, false, true, CL>(ta, tb, a, s);
-  if (amn && !bmn) return launch<BN, true, false, CL>(ta, tb, a, s);
-  return launch<BN, true, true, CL>(ta, tb, a, s);
+  if (!amn && !bmn) return launch<BN, false, false, CL, PAIR>(ta, tb, a, s);
+  if (!amn && bmn) return launch<BN, false, true, CL, PAIR>(ta, tb, a, s);
+  if (amn && !bmn) return launch<BN, true, false, CL, PAIR>(ta, tb, a, s);
+  return launch<BN, true, true, CL, PAIR>(ta, tb, a, s);
 }
 
 template <int BN>
 cudaError_t dispatch_major(bool amn, bool bmn, int cl, const CUtensorMap* ta, const CUtensorMap* tb,
                            const GemmArgs& a, cudaStream_t s) {
   if constexpr (BN >= 128) {
+    if (cl == -2) return dispatch_cl<BN, 2, true>(amn, bmn, ta, tb, a, s);
+    if constexpr (BN == 256)
+      if (cl == -4) return dispatch_cl<BN, 4, true>(amn, bmn, ta, tb, a, s);
     if (cl == 4) return dispatch_cl<BN, 4>(amn, bmn, ta, tb, a, s);
     if (cl == 2) return dispatch_cl<BN, 2>(amn, bmn, ta, tb, a, s);
   }
@@ -503,9 +549,18 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
     const char* e = getenv("UPIPE_GEMM_MC");
     return e ? atoi(e) : 4;
   }();
+  // UPIPE_GEMM_PAIR=1 (default): CTA pairs (cta_group::2, M = 256 per MMA) instead of multicast clusters
+  static const int pair_env = [] {
+    const char* e = getenv("UPIPE_GEMM_PAIR");
+    return e ? atoi(e) : 1;
+  }();
   const int ntn_all = (int)(p0.N / bn);
   int cl = 1;
   if (bn >= 128 && M > BM && mc_env >= 2) cl = (mc_env >= 4 && ntn_all % 2 == 0) ? 4 : 2;
+  // UPIPE_GEMM_PAIR=2: two pairs per cluster sharing B by multicast (BN = 256, four or more m-blocks)
+  const bool pair = cl > 1 && pair_env;
+  const bool pair4 = pair && pair_env >= 2 && bn == 256 && M > 3 * BM;
+  if (pair) cl = pair4 ? 4 : 2;
   const bool mc = cl > 1;
   // TMA box rows: a K-major operand tile (rows x 64 k) goes in one box when its rows never cross an
   // operand segment (fewer, larger TMA requests); MN-major tiles stay 64 x 64 granules (128B swizzle
@@ -518,7 +573,7 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
     }
     return gr;
   };
-  const int a_g = box_g(true, cl == 4 ? BM / 2 : BM), b_g = box_g(false, mc ? bn / 2 : bn);
+  const int a_g = box_g(true, cl == 4 && !pair ? BM / 2 : BM), b_g = box_g(false, pair4 ? bn / 4 : (mc ? bn / 2 : bn));
   args.a_box_g = a_g;
   args.b_box_g = b_g;
   CUtensorMap ta[kMaxParts], tb[kMaxParts];
@@ -552,8 +607,9 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
   args.kcum[kMaxParts] = (int)kc;
   args.mcum[kMaxParts] = (int)mrow;
   cudaError_t e;
-  if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, cl, ta, tb, args, stream);
-  else if (bn == 128) e = dispatch_major<128>(p0.a.mn_major, p0.b.mn_major, cl, ta, tb, args, stream);
+  const int clk = pair4 ? -4 : (pair ? -2 : cl);
+  if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, args, stream);
+  else if (bn == 128) e = dispatch_major<128>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, args, stream);
   else e = dispatch_major<64>(p0.a.mn_major, p0.b.mn_major, 1, ta, tb, args, stream);
   if (e != cudaSuccess) snprintf(err, errlen, "gemm launch: %s", cudaGetErrorString(e));
   if (args.dbg) {
