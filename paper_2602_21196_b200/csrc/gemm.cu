@@ -98,6 +98,13 @@ __global__ void __launch_bounds__(192, 1)
   // so each pair leader's commit frees it in all four CTAs (empty barriers count 2 arrivals).
   static_assert(!PAIR || CL == 2 || CL == 4, "CTA pairs: clusters of 2 or 4");
   constexpr bool P4 = PAIR && CL == 4;
+  // BN = 512 (PAIR only): each CTA owns a 128 x 512 output (the whole TMEM, one accumulator, so the
+  // epilogue is not overlapped) computed as two N = 256 pair MMAs per k-step; per SM the ring carries
+  // A + 256 B rows per k-block for twice the FLOPs of BN = 256 (L2->SM delivery is the GEMM's limit).
+  constexpr bool WIDE = BN > 256;
+  static_assert(!WIDE || (PAIR && CL == 2 && BN == 512), "BN = 512 needs CTA pairs");
+  constexpr int NMMA = WIDE ? BN / 256 : 1, MMA_N = BN / NMMA;
+  constexpr int NACC = WIDE ? 1 : 2;                 // TMEM accumulators (512 columns in total)
   using C = Cfg<BN, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -153,8 +160,8 @@ __global__ void __launch_bounds__(192, 1)
     fence_barrier_init();
   }
   if (warp == 1) {
-    if constexpr (PAIR) tmem_alloc_pair<2 * BN>(tmem_slot);
-    else tmem_alloc<2 * BN>(tmem_slot);
+    if constexpr (PAIR) tmem_alloc_pair<NACC * BN>(tmem_slot);
+    else tmem_alloc<NACC * BN>(tmem_slot);
   }
   tc_fence_before();
   __syncthreads();
@@ -211,7 +218,8 @@ __global__ void __launch_bounds__(192, 1)
             }
 #pragma unroll
             for (int c = 0; c < GB0; ++c) {
-              const int ii = n0 + (cb0 + c) * 64;
+              // WIDE: granule c of this CTA = half ms of MMA (c / 2)'s 256 B rows
+              const int ii = n0 + (WIDE ? (c >> 1) * (GB / NMMA) + ms * 2 + (c & 1) : cb0 + c) * 64;
               b_out[c] = bm.o_base + (ii / bm.o_len) * bm.o_istride + ii % bm.o_len;
               b_kb[c] = bm.k_base + (ii / bm.o_len) * bm.k_istride;
             }
@@ -282,16 +290,16 @@ __global__ void __launch_bounds__(192, 1)
   } else if (warp == 1) {
     if (!PAIR || crank == leader) {
       // ---------------- MMA issuer (whole warp; elect.sync inside the MMA asm, see mma_ss_w)
-      constexpr uint32_t idesc = idesc_bf16(PAIR ? 2 * BM : BM, BN, A_MN, B_MN);
+      constexpr uint32_t idesc = idesc_bf16(PAIR ? 2 * BM : BM, MMA_N, A_MN, B_MN);
       long long tl_full = 0, tl_acc = 0;
       const long long t_start = clock64();
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
       for (int u = unit0; u < nunits; u += nunit_step, ++i) {
-        const int ab = i & 1;
+        const int ab = i % NACC;
         const long long a0 = g.dbg ? clock64() : 0;
-        mbar_wait(&acc_empty[ab], ((i >> 1) & 1) ^ 1);     // the epilogue has drained this accumulator
+        mbar_wait(&acc_empty[ab], ((i / NACC) & 1) ^ 1);   // the epilogue has drained this accumulator
         if (g.dbg) tl_acc += clock64() - a0;
         tc_fence_after();
         const uint32_t acc = tmem + ab * BN;
@@ -307,8 +315,13 @@ __global__ void __launch_bounds__(192, 1)
             const uint64_t da = A_MN ? desc_sw128(sa + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sa + kk * 32, 16, 1024);
             const uint64_t db = B_MN ? desc_sw128(sb + kk * 2048, GRANULE_BYTES, 1024) : desc_sw128(sb + kk * 32, 16, 1024);
             if (g.dbg_mode == 3) continue;
-            if (PAIR) mma_ss_pair_w(acc, da, db, idesc, (kb | kk) != 0);
-            else mma_ss_w(acc, da, db, idesc, (kb | kk) != 0);
+            if (PAIR) {
+#pragma unroll
+              for (int j = 0; j < NMMA; ++j)             // MMA j: TMEM columns [256 j, 256 j + 256), B sub-tile j
+                mma_ss_pair_w(acc + j * MMA_N, da, db + ((j * (MMA_N / 2) * BK * 2) >> 4), idesc, (kb | kk) != 0);
+            } else {
+              mma_ss_w(acc, da, db, idesc, (kb | kk) != 0);
+            }
           }
           if (PAIR) mma_commit_pair_w(&empty[stage], P4 ? 0xF : 0x3);  // frees the stage where this pair's data lives
           else if (MC) mma_commit_mc_w(&empty[stage], maskE);   // frees the stage in every CTA writing into ours
@@ -331,13 +344,13 @@ __global__ void __launch_bounds__(192, 1)
     const int row = quad * 32 + lane;
     int i = 0;
     for (int u = unit0; u < nunits; u += nunit_step, ++i) {
-      const int ab = i & 1;
+      const int ab = i % NACC;
       const int m0 = tile_m(u) * BM, n0 = tile_n(u) * BN;
       const int pc = mpart(m0);
       const DevOut& oc_ = g.c[pc];
       const int m = m0 + row;
       const int ml = m - (g.kind == 1 ? g.mcum[pc] : 0);
-      mbar_wait(&acc_full[ab], (i >> 1) & 1);
+      mbar_wait(&acc_full[ab], (i / NACC) & 1);
       tc_fence_after();
       const bool mvalid = m < g.M;
       const long long mseg = mvalid ? ml / oc_.m_len : 0, min_ = mvalid ? ml % oc_.m_len : 0;
@@ -393,8 +406,8 @@ __global__ void __launch_bounds__(192, 1)
   if (MC) cluster_sync();                  // no CTA leaves while its peer may still signal its barriers
   if (warp == 1) {
     tc_fence_after();
-    if constexpr (PAIR) tmem_dealloc_pair<2 * BN>(tmem);
-    else tmem_dealloc<2 * BN>(tmem);
+    if constexpr (PAIR) tmem_dealloc_pair<NACC * BN>(tmem);
+    else tmem_dealloc<NACC * BN>(tmem);
   }
 }
 
@@ -461,14 +474,18 @@ cudaError_t dispatch_cl(bool amn, bool bmn, const CUtensorMap* ta, const CUtenso
 template <int BN>
 cudaError_t dispatch_major(bool amn, bool bmn, int cl, const CUtensorMap* ta, const CUtensorMap* tb,
                            const GemmArgs& a, cudaStream_t s) {
-  if constexpr (BN >= 128) {
+  if constexpr (BN == 512) {
+    return dispatch_cl<BN, 2, true>(amn, bmn, ta, tb, a, s);
+  } else if constexpr (BN >= 128) {
     if (cl == -2) return dispatch_cl<BN, 2, true>(amn, bmn, ta, tb, a, s);
     if constexpr (BN == 256)
       if (cl == -4) return dispatch_cl<BN, 4, true>(amn, bmn, ta, tb, a, s);
     if (cl == 4) return dispatch_cl<BN, 4>(amn, bmn, ta, tb, a, s);
     if (cl == 2) return dispatch_cl<BN, 2>(amn, bmn, ta, tb, a, s);
+    return dispatch_cl<BN, 1>(amn, bmn, ta, tb, a, s);
+  } else {
+    return dispatch_cl<BN, 1>(amn, bmn, ta, tb, a, s);
   }
-  return dispatch_cl<BN, 1>(amn, bmn, ta, tb, a, s);
 }
 
 bool seg_ok(int64_t len) { return len % 64 == 0 && len > 0; }
@@ -559,6 +576,17 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
   if (bn >= 128 && M > BM && mc_env >= 2) cl = (mc_env >= 4 && ntn_all % 2 == 0) ? 4 : 2;
   // UPIPE_GEMM_PAIR=2: two pairs per cluster sharing B by multicast (BN = 256, four or more m-blocks)
   const bool pair = cl > 1 && pair_env;
+  // UPIPE_GEMM_WIDE=1 (default): 128 x 512 tiles per CTA (two N = 256 pair MMAs) where N allows
+  static const int wide_env = [] {
+    const char* e = getenv("UPIPE_GEMM_WIDE");
+    return e ? atoi(e) : 1;
+  }();
+  // ... and only with store epilogues: an fp32 read-modify-write epilogue (dX accumulation) is too long
+  // to leave un-overlapped (measured: dX 17.4 -> 21.1 ms per step at 128K with BN = 512)
+  bool store_epi = true;
+  for (int i = 0; i < n; ++i)
+    store_epi = store_epi && (parts[i].c.epi == Epi::kStoreBF16 || parts[i].c.epi == Epi::kStoreF32);
+  if (pair && wide_env && pair_env == 1 && bn == 256 && store_epi && bn_ok(512)) bn = 512;
   const bool pair4 = pair && pair_env >= 2 && bn == 256 && M > 3 * BM;
   if (pair) cl = pair4 ? 4 : 2;
   const bool mc = cl > 1;
@@ -573,7 +601,8 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
     }
     return gr;
   };
-  const int a_g = box_g(true, cl == 4 && !pair ? BM / 2 : BM), b_g = box_g(false, pair4 ? bn / 4 : (mc ? bn / 2 : bn));
+  const int a_g = box_g(true, cl == 4 && !pair ? BM / 2 : BM),
+            b_g = box_g(false, bn == 512 ? 128 : (pair4 ? bn / 4 : (mc ? bn / 2 : bn)));
   args.a_box_g = a_g;
   args.b_box_g = b_g;
   CUtensorMap ta[kMaxParts], tb[kMaxParts];
@@ -608,7 +637,8 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
   args.mcum[kMaxParts] = (int)mrow;
   cudaError_t e;
   const int clk = pair4 ? -4 : (pair ? -2 : cl);
-  if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, args, stream);
+  if (bn == 512) e = dispatch_major<512>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, args, stream);
+  else if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, args, stream);
   else if (bn == 128) e = dispatch_major<128>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, args, stream);
   else e = dispatch_major<64>(p0.a.mn_major, p0.b.mn_major, 1, ta, tb, args, stream);
   if (e != cudaSuccess) snprintf(err, errlen, "gemm launch: %s", cudaGetErrorString(e));

@@ -31,7 +31,8 @@ ATTN_GRAD_REL_PEAKY = 5e-3
 ABS = 2e-2
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (300, 192, 256), (1024, 512, 4096), (257, 1024, 512)])
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (300, 192, 256), (1024, 512, 4096), (257, 1024, 512),
+                                   (384, 1536, 640), (2048, 4096, 1024), (640, 256, 512)])
 def test_gemm_xwT(U, M, N, K):
     x = synth.draw(1, 21, (M, K), 0)
     w = synth.draw(1, 22, (N, K), -4)
