@@ -42,6 +42,8 @@ struct GemmArgs {
   long long* dbg;            // UPIPE_GEMM_TIMELINE=1: wait/issue cycle totals of CTA 0 (else null)
   int dbg_mode;              // UPIPE_GEMM_TIMELINE=2: no TMA loads (MMA-only rate); 3: no MMAs (TMA-only rate)
   int a_box_g, b_box_g;      // 64-row granules per TMA box (K-major operands: one box per operand tile)
+  int c_tma;                 // 1: part 0's fp32 store / accumulate goes through shared memory and TMA
+                             //    (bulk tensor store / reduce-add into L2) instead of per-thread global RMW
   int kcum[kMaxParts + 1];   // K-concat: first K index of each part (multiples of BK)
   int mcum[kMaxParts + 1];   // M-concat: first row of each part (multiples of BM)
   DevOpMap a[kMaxParts], b[kMaxParts];
@@ -69,14 +71,17 @@ struct Cfg {
   static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;   // PAIR: this CTA's half of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = RING_BYTES / STAGE_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int STG = STAGES * STAGE_BYTES;          // two 16 KB epilogue staging boxes (128 rows x 32 fp32)
+  static constexpr int SMEM = STG + 32768 + 1024 + 256;
+  static_assert(SMEM <= 232448, "shared memory");
 };
 
 template <int BN, bool A_MN, bool B_MN, int CL, bool PAIR>
 __global__ void __launch_bounds__(192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB0,
-                const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2, const GemmArgs g) {
+                const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
+                const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
   // Grouped forms (GemmGroup): K-concatenation sums the products of up to three (A, B) pairs
   // into one accumulator (one epilogue pass); M-concatenation stacks up to three A operands
   // (own output maps) against one B. The part of a k-block / tile selects the tensor maps.
@@ -109,7 +114,7 @@ __global__ void __launch_bounds__(192, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STG + 32768);
   uint64_t* empty = full + C::STAGES;
   uint64_t* acc_full = empty + C::STAGES;   // [2]
   uint64_t* acc_empty = acc_full + 2;       // [2]
@@ -360,7 +365,31 @@ __global__ void __launch_bounds__(192, 1)
         tmem_ld32(tmem + ab * BN + ((uint32_t)(quad * 32) << 16) + c32 * 32, r);
         tmem_wait_ld();
         const int n = n0 + c32 * 32;
-        if (!mvalid || n >= g.N) continue;
+        if (n >= g.N) continue;                 // uniform across the CTA
+        if (g.c_tma && pc == 0 && (oc_.epi == (int)Epi::kStoreF32 || oc_.epi == (int)Epi::kAccF32)) {
+          // fp32 tile column box -> swizzled staging slot -> one TMA store / reduce-add by warp 2 lane 0
+          // (L2 performs the accumulation: no global read by the SM, no per-thread RMW latency)
+          const bool issuer = warp == 2 && lane == 0;
+          uint8_t* slot = smem + C::STG + (c32 & 1) * 16384;
+          if (issuer) bulk_wait_read1();      // the op that last used this slot has read it
+          named_bar_sync(1, 128);
+          const uint32_t sb = smem_u32(slot) + row * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(sb + ((j ^ (row & 7)) << 4), __float_as_uint(__uint_as_float(r[4 * j + 0]) * g.alpha),
+                         __float_as_uint(__uint_as_float(r[4 * j + 1]) * g.alpha),
+                         __float_as_uint(__uint_as_float(r[4 * j + 2]) * g.alpha),
+                         __float_as_uint(__uint_as_float(r[4 * j + 3]) * g.alpha));
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (issuer) {
+            if (oc_.epi == (int)Epi::kAccF32) tma_reduce_add_2d(&tmC, slot, n, m0);
+            else tma_store_2d(&tmC, slot, n, m0);
+            bulk_commit();
+          }
+          continue;
+        }
+        if (!mvalid) continue;
         const long long nseg = n / oc_.n_len, nin = n % oc_.n_len;
         const long long orow = oc_.r_base + mseg * oc_.r_mstride + min_ + nseg * oc_.r_nstride;
         const long long ocol = oc_.c_base + nseg * oc_.c_nstride + nin + mseg * oc_.c_mstride;
@@ -400,6 +429,7 @@ __global__ void __launch_bounds__(192, 1)
       if (PAIR && crank != leader) mbar_arrive_cluster(mapa_shared(&acc_empty[ab], leader));
       else mbar_arrive(&acc_empty[ab]);
     }
+    if (g.c_tma && warp == 2 && lane == 0) bulk_wait0();   // staged boxes fully written before exit
   }
   tc_fence_before();
   __syncthreads();
@@ -417,7 +447,8 @@ DevOpMap to_dev(const OperandMap& m) {
 }
 
 template <int BN, bool A_MN, bool B_MN, int CL, bool PAIR>
-cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs& args, cudaStream_t s) {
+cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorMap* tc, const GemmArgs& args,
+                   cudaStream_t s) {
   using C = Cfg<BN, PAIR>;
   auto kern = gemm_kernel<BN, A_MN, B_MN, CL, PAIR>;
   static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -456,35 +487,35 @@ cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs&
   }();
   const int clusters = units < max_clusters ? units : max_clusters;
   cfg.gridDim = dim3(CL * clusters);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], args);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], *tc, args);
   count_launches(1);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 template <int BN, int CL, bool PAIR = false>
-cudaError_t dispatch_cl(bool amn, bool bmn, const CUtensorMap* ta, const CUtensorMap* tb, const GemmArgs& a,
-                        cudaStream_t s) {
-  if (!amn && !bmn) return launch<BN, false, false, CL, PAIR>(ta, tb, a, s);
-  if (!amn && bmn) return launch<BN, false, true, CL, PAIR>(ta, tb, a, s);
-  if (amn && !bmn) return launch<BN, true, false, CL, PAIR>(ta, tb, a, s);
-  return launch<BN, true, true, CL, PAIR>(ta, tb, a, s);
+cudaError_t dispatch_cl(bool amn, bool bmn, const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorMap* tc,
+                        const GemmArgs& a, cudaStream_t s) {
+  if (!amn && !bmn) return launch<BN, false, false, CL, PAIR>(ta, tb, tc, a, s);
+  if (!amn && bmn) return launch<BN, false, true, CL, PAIR>(ta, tb, tc, a, s);
+  if (amn && !bmn) return launch<BN, true, false, CL, PAIR>(ta, tb, tc, a, s);
+  return launch<BN, true, true, CL, PAIR>(ta, tb, tc, a, s);
 }
 
 template <int BN>
 cudaError_t dispatch_major(bool amn, bool bmn, int cl, const CUtensorMap* ta, const CUtensorMap* tb,
-                           const GemmArgs& a, cudaStream_t s) {
+                           const CUtensorMap* tc, const GemmArgs& a, cudaStream_t s) {
   if constexpr (BN == 512) {
-    return dispatch_cl<BN, 2, true>(amn, bmn, ta, tb, a, s);
+    return dispatch_cl<BN, 2, true>(amn, bmn, ta, tb, tc, a, s);
   } else if constexpr (BN >= 128) {
-    if (cl == -2) return dispatch_cl<BN, 2, true>(amn, bmn, ta, tb, a, s);
+    if (cl == -2) return dispatch_cl<BN, 2, true>(amn, bmn, ta, tb, tc, a, s);
     if constexpr (BN == 256)
-      if (cl == -4) return dispatch_cl<BN, 4, true>(amn, bmn, ta, tb, a, s);
-    if (cl == 4) return dispatch_cl<BN, 4>(amn, bmn, ta, tb, a, s);
-    if (cl == 2) return dispatch_cl<BN, 2>(amn, bmn, ta, tb, a, s);
-    return dispatch_cl<BN, 1>(amn, bmn, ta, tb, a, s);
+      if (cl == -4) return dispatch_cl<BN, 4, true>(amn, bmn, ta, tb, tc, a, s);
+    if (cl == 4) return dispatch_cl<BN, 4>(amn, bmn, ta, tb, tc, a, s);
+    if (cl == 2) return dispatch_cl<BN, 2>(amn, bmn, ta, tb, tc, a, s);
+    return dispatch_cl<BN, 1>(amn, bmn, ta, tb, tc, a, s);
   } else {
-    return dispatch_cl<BN, 1>(amn, bmn, ta, tb, a, s);
+    return dispatch_cl<BN, 1>(amn, bmn, ta, tb, tc, a, s);
   }
 }
 
@@ -635,12 +666,31 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
   }
   args.kcum[kMaxParts] = (int)kc;
   args.mcum[kMaxParts] = (int)mrow;
+  // TMA epilogue for part 0's fp32 store / accumulate when its output map is a plain row-major matrix
+  // (the dX accumulator, dWo): UPIPE_GEMM_TMA_EPI=0 disables it
+  static const int tma_epi_env = [] {
+    const char* e = getenv("UPIPE_GEMM_TMA_EPI");
+    return e ? atoi(e) : 1;
+  }();
+  CUtensorMap tc = ta[0];
+  args.c_tma = 0;
+  {
+    const OutMap& c0 = p0.c;
+    const bool plain = c0.r_base == 0 && c0.c_base == 0 && c0.m_len >= M && c0.n_len >= p0.N && c0.r_mstride == 0 &&
+                       c0.r_nstride == 0 && c0.c_nstride == 0 && c0.c_mstride == 0;
+    if (tma_epi_env && kind == GemmGroup::kKConcat && (c0.epi == Epi::kStoreF32 || c0.epi == Epi::kAccF32) && plain &&
+        c0.out_f32 && (reinterpret_cast<uintptr_t>(c0.out_f32) & 15) == 0 && c0.ld_f32 % 4 == 0 && p0.alpha == 1.0f) {
+      if (!make_tmap_2d_f32(&tc, c0.out_f32, (uint64_t)p0.N, (uint64_t)M, (uint64_t)c0.ld_f32, 32, 128, err, errlen))
+        return cudaErrorInvalidValue;
+      args.c_tma = 1;
+    }
+  }
   cudaError_t e;
   const int clk = pair4 ? -4 : (pair ? -2 : cl);
-  if (bn == 512) e = dispatch_major<512>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, args, stream);
-  else if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, args, stream);
-  else if (bn == 128) e = dispatch_major<128>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, args, stream);
-  else e = dispatch_major<64>(p0.a.mn_major, p0.b.mn_major, 1, ta, tb, args, stream);
+  if (bn == 512) e = dispatch_major<512>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, &tc, args, stream);
+  else if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, &tc, args, stream);
+  else if (bn == 128) e = dispatch_major<128>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, &tc, args, stream);
+  else e = dispatch_major<64>(p0.a.mn_major, p0.b.mn_major, 1, ta, tb, &tc, args, stream);
   if (e != cudaSuccess) snprintf(err, errlen, "gemm launch: %s", cudaGetErrorString(e));
   if (args.dbg) {
     long long h[8];
