@@ -487,6 +487,342 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Q64 variant (d = 128): 64-query tiles in two TMEM slots, so one slot's softmax-gradient work
+// overlaps the other slot's MMAs (ping-pong, as in the forward). TMEM: S_A | dP_A | S_B | dP_B
+// (64 columns each) | dV | dK; per tile n in slot x = n & 1 the tensor core runs
+//   dV(n) += P^T dO, dQ^T(n) = K^T dS (into dP_x), dK(n) += dS^T Q, S(n+2), dP(n+2)
+// where S / dP / dQ^T are N = 64 MMAs. dQ^T leaves TMEM with one dimension per lane and is staged
+// transposed (one 64 x 32 fp32 box per drain warp) for the TMA reduce-add into dq_acc.
+struct Q64Cfg {
+  static constexpr int D = 128;
+  static constexpr int KT = 128 * D * 2;            // K or V tile: 128 keys x 128 d bf16 (two 16 KB chunks)
+  static constexpr int QT = 64 * D * 2;             // Q or dO tile: 64 queries x 128 d (two 8 KB chunks)
+  static constexpr int NQ = 3;                      // Q / dO ring depth
+  static constexpr int OFF_K = 0, OFF_V = KT, OFF_Q = 2 * KT, OFF_DO = OFF_Q + NQ * QT;
+  static constexpr int OFF_DS = OFF_DO + NQ * QT;   // dS^T [128 keys][64 q] bf16 per slot (16 KB)
+  static constexpr int OFF_STG = OFF_DS + 2 * 16384; // dQ^T staging: 4 warps x (64 q x 32 d fp32 = 8 KB)
+  static constexpr int OFF_STAT = OFF_STG + 32768;  // [slot][parity] lse2[64], delta[64]
+  static constexpr int OFF_BAR = OFF_STAT + 2048;
+  static constexpr int SMEM = OFF_BAR + 256;
+  static_assert(SMEM <= 232448, "shared memory");
+  static constexpr uint32_t TM_S0 = 0, TM_DP0 = 64, TM_S1 = 128, TM_DP1 = 192, TM_DV = 256, TM_DK = 384;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_q64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                        const __grid_constant__ CUtensorMap tmdQ, const BwdArgs a) {
+  using C = Q64Cfg;
+  constexpr int D = C::D;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (smem_u32(smem) & 1023) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* q_full = bars + 1;      // [3]
+  uint64_t* q_empty = bars + 4;     // [3]
+  uint64_t* do_full = bars + 7;     // [3]
+  uint64_t* do_empty = bars + 10;   // [3]
+  uint64_t* sdp_full = bars + 13;   // [2] S(n), dP(n) of slot n & 1 in TMEM
+  uint64_t* ds_full = bars + 15;    // [2] P^T in TMEM, dS^T in smem (128 arrivals)
+  uint64_t* dq_full = bars + 17;    // [2]
+  uint64_t* dq_empty = bars + 19;   // [2] (128 arrivals)
+  uint64_t* dkv_full = bars + 21;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+  float* stats = reinterpret_cast<float*>(smem + C::OFF_STAT);   // [(slot*2 + parity)*2 + {lse2, delta}][64]
+
+  const int warp = warp_id(), lane = lane_id();
+  const int jb = blockIdx.x;
+  const int g = blockIdx.y;
+  const int G = a.nq / a.nkv;
+  const int nT64 = (int)((a.S + 63) / 64);
+  const int qt_begin = a.causal ? 2 * jb : 0;
+  const int n_qt = nT64 - qt_begin;
+  const int N = G * n_qt;
+  constexpr int kWg = 128;
+
+  if (warp == kTmaWarp && lane == 0) {
+    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
+    for (int i = 0; i < 22; ++i) mbar_init(&bars[i], (i == 15 || i == 16 || i == 19 || i == 20) ? kWg : 1);
+    fence_barrier_init();
+    tmem_slot[1] = smem_u32(smem);
+  }
+  if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= kTmaWarp) regs_dec<kRegsOther>();
+  if (warp == kTmaWarp) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * C::KT);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        tma_load_3d(smem + C::OFF_K + c * 16384, &tmK, kv_full, c * 64, g, jb * 128);
+        tma_load_3d(smem + C::OFF_V + c * 16384, &tmV, kv_full, c * 64, g, jb * 128);
+      }
+      for (int n = 0; n < N; ++n) {
+        const int h = g * G + n / n_qt;
+        const int qt = qt_begin + n % n_qt;
+        const int st = n % C::NQ;
+        const uint32_t ph = ((n / C::NQ) & 1) ^ 1;
+        mbar_wait(&q_empty[st], ph);
+        mbar_arrive_expect_tx(&q_full[st], C::QT);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) tma_load_3d(smem + C::OFF_Q + st * C::QT + c * 8192, &tmQ, &q_full[st], c * 64, h, qt * 64);
+        mbar_wait(&do_empty[st], ph);
+        mbar_arrive_expect_tx(&do_full[st], C::QT);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          tma_load_3d(smem + C::OFF_DO + st * C::QT + c * 8192, &tmdO, &do_full[st], c * 64, h, qt * 64);
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    constexpr uint32_t id_sp = idesc_bf16(128, 64, false, false);    // S^T, dP^T: K-major A (K/V) and B (Q/dO)
+    constexpr uint32_t id_kmn = idesc_bf16(128, D, false, true);     // dV (A in TMEM), dK: B = Q / dO MN-major
+    constexpr uint32_t id_dq = idesc_bf16(128, 64, true, true);      // dQ^T = K^T dS: both MN-major
+    uint32_t base;
+    auto load_base = [&]() { base = ld_volatile_shared_u32(tmem_slot + 1); };
+    load_base();
+    auto mma_sp = [&](uint32_t skv, uint32_t sqt, uint32_t tm) {   // [128 keys x d] x [64 q x d]^T
+      const uint64_t da = desc_sw128(skv, 16, 1024), db = desc_sw128(sqt, 16, 1024);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        mma_ss_w(tm, da + (((i >> 2) * 16384 + (i & 3) * 32) >> 4), db + (((i >> 2) * 8192 + (i & 3) * 32) >> 4),
+                 id_sp, i != 0);
+    };
+    auto mma_dv = [&](uint32_t tp, uint32_t sdo, bool acc) {       // dV += P^T dO: A = P^T (TMEM, 64 q)
+      const uint64_t db = desc_sw128(sdo, 8192, 1024);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+        mma_ts_w(tmem + C::TM_DV, tp + ks * 8, db + ks * (2048 >> 4), id_kmn, (acc || ks) ? 1u : 0u);
+    };
+    auto mma_dk = [&](uint32_t sds, uint32_t sq, bool acc) {       // dK += dS^T Q: A = dS^T (K-major, 64 q)
+      const uint64_t da = desc_sw128(sds, 16, 1024), db = desc_sw128(sq, 8192, 1024);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+        mma_ss_w(tmem + C::TM_DK, da + ((ks * 32) >> 4), db + ks * (2048 >> 4), id_kmn, (acc || ks) ? 1u : 0u);
+    };
+    auto mma_dq = [&](uint32_t sk, uint32_t sds, uint32_t tm) {    // dQ^T = K^T dS over the 128 keys
+      const uint64_t da = desc_sw128(sk, 16384, 1024), db = desc_sw128(sds, 8192, 1024);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mma_ss_w(tm, da + i * (2048 >> 4), db + i * (2048 >> 4), id_dq, i != 0);
+    };
+    auto slot_s = [](int x) { return x ? C::TM_S1 : C::TM_S0; };
+    auto slot_dp = [](int x) { return x ? C::TM_DP1 : C::TM_DP0; };
+    mbar_wait(kv_full, 0);
+    for (int t = 0; t < 2 && t < N; ++t) {
+      mbar_wait(&q_full[t], 0);
+      tc_fence_after();
+      mma_sp(base + C::OFF_K, base + C::OFF_Q + t * C::QT, tmem + slot_s(t));
+      mbar_wait(&do_full[t], 0);
+      tc_fence_after();
+      mma_sp(base + C::OFF_V, base + C::OFF_DO + t * C::QT, tmem + slot_dp(t));
+      mma_commit_w(&sdp_full[t]);
+    }
+    for (int n = 0; n < N; ++n) {
+      const int x = n & 1;
+      const int st = n % C::NQ;
+      mbar_wait(&ds_full[x], (n >> 1) & 1);
+      tc_fence_after();
+      load_base();
+      const uint32_t sds = base + C::OFF_DS + x * 16384;
+      mma_dv(tmem + slot_s(x), base + C::OFF_DO + st * C::QT, n > 0);
+      mma_commit_w(&do_empty[st]);
+      mma_dq(base + C::OFF_K, sds, tmem + slot_dp(x));
+      mma_commit_w(&dq_full[x]);
+      mma_dk(sds, base + C::OFF_Q + st * C::QT, n > 0);
+      mma_commit_w(&q_empty[st]);
+      if (n + 2 < N) {
+        const int st2 = (n + 2) % C::NQ;
+        const uint32_t ph2 = ((n + 2) / C::NQ) & 1;
+        mbar_wait(&q_full[st2], ph2);
+        tc_fence_after();
+        mma_sp(base + C::OFF_K, base + C::OFF_Q + st2 * C::QT, tmem + slot_s(x));   // after dV(n) read P^T
+        mbar_wait(&dq_empty[x], (n >> 1) & 1);                                        // dQ^T(n) drained
+        mbar_wait(&do_full[st2], ph2);
+        tc_fence_after();
+        mma_sp(base + C::OFF_V, base + C::OFF_DO + st2 * C::QT, tmem + slot_dp(x));
+        mma_commit_w(&sdp_full[x]);
+      }
+    }
+    mma_commit_w(dkv_full);
+  } else if (warp < kSoftmaxWarps) {
+    // ------------------------------------------------ softmax-gradient warpgroups: WG x owns slot x
+    regs_inc<kRegsSoftmax>();
+    const int x = warp >> 2;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;                   // key row of the tile
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const long long key = (long long)jb * 128 + r;
+    const float sl2 = a.scale_log2;
+    const uint32_t tS = tmem + (x ? C::TM_S1 : C::TM_S0) + lane_off;
+    const uint32_t tP = tmem + (x ? C::TM_DP1 : C::TM_DP0) + lane_off;
+    const uint32_t dsbase = smem_u32(smem + C::OFF_DS + x * 16384);
+    auto load_stat = [&](int n) -> float {            // threads 0-63: -lse*log2e of query r, 64-127: delta
+      const int h = g * G + n / n_qt;
+      const long long q = (long long)(qt_begin + n % n_qt) * 64 + (r & 63);
+      if (q >= a.S) return 0.f;
+      return r < 64 ? a.lse[(long long)h * a.ld_lse + q] * -1.4426950408889634f : a.delta[q * a.ld_delta + h];
+    };
+    float stat_next = x < N ? load_stat(x) : 0.f;
+    for (int n = x; n < N; n += 2) {
+      const int qt = qt_begin + n % n_qt;
+      const long long q0 = (long long)qt * 64;
+      const int par = (n >> 1) & 1;
+      float* s_lse2 = stats + ((x * 2 + par) * 2 + 0) * 64;
+      float* s_delta = stats + ((x * 2 + par) * 2 + 1) * 64;
+      (r < 64 ? s_lse2 : s_delta)[r & 63] = stat_next;
+      if (n + 2 < N) stat_next = load_stat(n + 2);
+      if (quad == 0) mbar_wait(&sdp_full[x], (n >> 1) & 1);
+      named_bar_sync(1 + x, kWg);
+      tc_fence_after();
+      const bool need_mask = (a.causal && (qt >> 1) == jb) || q0 + 64 > a.S || (long long)jb * 128 + 128 > a.S;
+      const long long qmin = key >= a.S ? a.S : (a.causal ? key : 0);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int col0 = c * 32;
+        uint32_t rs[32], rp[32];
+        tmem_ld32(tS + col0, rs);
+        tmem_ld32(tP + col0, rp);
+        const float4* l4 = reinterpret_cast<const float4*>(s_lse2 + col0);
+        const float4* d4 = reinterpret_cast<const float4*>(s_delta + col0);
+        float4 lx[8], dl[8];
+#pragma unroll
+        for (int i4 = 0; i4 < 8; ++i4) lx[i4] = l4[i4];
+        tmem_wait_ld();
+#pragma unroll
+        for (int i4 = 0; i4 < 8; ++i4) dl[i4] = d4[i4];
+        const uint64_t sl2x2 = f2_pack(sl2, sl2);
+        uint64_t pp[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float4 xx = lx[j >> 1];
+          const uint64_t nl = (j & 1) ? f2_pack(xx.z, xx.w) : f2_pack(xx.x, xx.y);
+          const uint64_t t = f2_fma(f2_pack(__uint_as_float(rs[2 * j]), __uint_as_float(rs[2 * j + 1])), sl2x2, nl);
+          float t0, t1;
+          f2_unpack(t, t0, t1);
+          pp[j] = f2_pack(ex2b(t0), ex2b(t1));
+        }
+        if (need_mask) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float p0, p1;
+            f2_unpack(pp[j], p0, p1);
+            const long long qa = q0 + col0 + 2 * j;
+            p0 = (qa >= qmin && qa < a.S) ? p0 : 0.f;
+            p1 = (qa + 1 >= qmin && qa + 1 < a.S) ? p1 : 0.f;
+            pp[j] = f2_pack(p0, p1);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float4 y = dl[j >> 1];
+          const uint64_t dlt = (j & 1) ? f2_pack(y.z, y.w) : f2_pack(y.x, y.y);
+          const uint64_t ds = f2_mul(pp[j], f2_sub(f2_pack(__uint_as_float(rp[2 * j]), __uint_as_float(rp[2 * j + 1])), dlt));
+          float d0, d1, p0, p1;
+          f2_unpack(ds, d0, d1);
+          f2_unpack(pp[j], p0, p1);
+          rp[j] = pack_bf16(d0, d1);
+          rs[j] = pack_bf16(p0, p1);
+        }
+        // P^T (bf16 pairs) into the S^T columns already read: queries [col0, col0+32) -> cols 16 c
+        tmem_st16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(rs));
+#pragma unroll
+        for (int v8 = 0; v8 < 4; ++v8)
+          st_shared_v4(dsbase + sw128_offset(r, col0 + v8 * 8), rp[4 * v8], rp[4 * v8 + 1], rp[4 * v8 + 2], rp[4 * v8 + 3]);
+      }
+      tmem_wait_st();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&ds_full[x]);
+    }
+    // ---- dK / dV epilogue (TMEM lane = key row): warpgroup 0 writes dV, warpgroup 1 dK
+    mbar_wait(dkv_full, 0);
+    tc_fence_after();
+    const long long ldacc = (long long)a.nkv * D;
+    const int which = x;
+    const uint32_t tcol = which ? C::TM_DK : C::TM_DV;
+    const float sc = which ? a.scale : 1.f;
+    float* acc = (which ? a.dk_acc : a.dv_acc);
+    __nv_bfloat16* ob = which ? a.dk_bf16 : a.dv_bf16;
+#pragma unroll 1
+    for (int c = 0; c < D; c += 32) {
+      uint32_t rr[32];
+      tmem_ld32(tmem + tcol + lane_off + c, rr);
+      tmem_wait_ld();
+      if (key >= a.S || N == 0) continue;
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]) * sc;
+      float4* accp = acc ? reinterpret_cast<float4*>(acc + key * ldacc + (long long)g * D + c) : nullptr;
+      if (a.kv_accumulate && accp) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 o = accp[i];
+          v[4 * i] += o.x; v[4 * i + 1] += o.y; v[4 * i + 2] += o.z; v[4 * i + 3] += o.w;
+        }
+      }
+      if (a.kv_write_acc && accp) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) accp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      }
+      if (ob) {
+        if (which && a.rope.hi) rope_rotate<16>(v, a.rope.hi, a.rope.lo, D, a.rope.pos0 + key, c, -1.f);
+        uint4* dst = reinterpret_cast<uint4*>(ob + key * a.ld_kvb + (long long)g * D + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                              pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+      }
+    }
+  } else if (warp < kSoftmaxWarps + 4) {
+    // ------------------------------------------------ dQ drain (warps 8-11): TMEM lane = head dim
+    regs_inc<kRegsDrain>();
+    const int quad = warp & 3;                        // dims [32 quad, 32 quad + 32) = this warp's box
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    uint8_t* const box = smem + C::OFF_STG + quad * 8192;
+    const uint32_t bbase = smem_u32(box);
+    for (int n = 0; n < N; ++n) {
+      const int x = n & 1;
+      const int h = g * G + n / n_qt;
+      const int q0 = (qt_begin + n % n_qt) * 64;
+      if (lane == 0) mbar_wait(&dq_full[x], (n >> 1) & 1);
+      __syncwarp();
+      tc_fence_after();
+      uint32_t rq[2][32];
+      const uint32_t tq = tmem + (x ? C::TM_DP1 : C::TM_DP0) + lane_off;
+      tmem_ld32(tq, rq[0]);
+      tmem_ld32(tq + 32, rq[1]);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&dq_empty[x]);
+      if (lane == 0) bulk_wait_read0();               // this warp's previous box has been read by its reduce
+      __syncwarp();
+      // row q (query), column lane (dim): 128B-swizzled rows of 32 fp32
+#pragma unroll
+      for (int q = 0; q < 64; ++q)
+        st_shared_f32(bbase + q * 128 + ((((uint32_t)lane >> 2) ^ ((uint32_t)q & 7)) << 4) + (lane & 3) * 4,
+                      __uint_as_float(rq[q >> 5][q & 31]) * a.scale);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_reduce_add_2d(&tmdQ, box, h * D + quad * 32, q0);
+        bulk_commit();
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 }  // namespace
 
 cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err, size_t errlen) {
@@ -536,6 +872,28 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   const int nT = (int)((p.S + 127) / 128);
   dim3 grid(nT, p.nkv);
   cudaError_t e;
+  // d = 128: the 64-query ping-pong kernel (default; UPIPE_BWD_Q64=0 selects the 128-query kernel,
+  // which also serves d = 64 and the UPIPE_BWD_TIMELINE diagnostics)
+  static const bool q64 = [] {
+    const char* v = getenv("UPIPE_BWD_Q64");
+    return !(v && v[0] == '0');
+  }();
+  if (p.d == 128 && q64 && !a.dbg) {
+    CUtensorMap tq64, tdo64, tdq64;
+    if (!make_tmap_3d(&tq64, p.q, p.d, p.nq, p.S, p.d, p.ldq, 64, 1, 64, err, errlen)) return cudaErrorInvalidValue;
+    if (!make_tmap_3d(&tdo64, p.dout, p.d, p.nq, p.S, p.d, p.ldo_grad, 64, 1, 64, err, errlen))
+      return cudaErrorInvalidValue;
+    if (!make_tmap_2d_f32(&tdq64, p.dq_acc, (uint64_t)p.nq * p.d, p.S, (uint64_t)p.nq * p.d, 32, 64, err, errlen))
+      return cudaErrorInvalidValue;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(attn_bwd_q64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Q64Cfg::SMEM);
+    if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd_q64 attr: %s", cudaGetErrorString(attr)); return attr; }
+    attn_bwd_q64_kernel<<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
+    count_launches(1);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) snprintf(err, errlen, "attn_bwd_q64 launch: %s", cudaGetErrorString(e));
+    return e;
+  }
   if (p.d == 128) {
     static const cudaError_t attr =
         cudaFuncSetAttribute(attn_bwd_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<128>::SMEM);
