@@ -510,6 +510,7 @@ struct Q64Cfg {
   static constexpr uint32_t TM_S0 = 0, TM_DP0 = 64, TM_S1 = 128, TM_DP1 = 192, TM_DV = 256, TM_DK = 384;
 };
 
+template <bool TL>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_q64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -622,10 +623,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_sp(base + C::OFF_V, base + C::OFF_DO + t * C::QT, tmem + slot_dp(t));
       mma_commit_w(&sdp_full[t]);
     }
+    long long tw[5] = {0, 0, 0, 0, 0};               // wait dS, wait Q, wait dQ drained, wait dO, total
+    const long long tbeg = tick<TL>();
     for (int n = 0; n < N; ++n) {
       const int x = n & 1;
       const int st = n % C::NQ;
+      long long w0 = tick<TL>();
       mbar_wait(&ds_full[x], (n >> 1) & 1);
+      tw[0] += tick<TL>() - w0;
       tc_fence_after();
       load_base();
       const uint32_t sds = base + C::OFF_DS + x * 16384;
@@ -638,17 +643,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (n + 2 < N) {
         const int st2 = (n + 2) % C::NQ;
         const uint32_t ph2 = ((n + 2) / C::NQ) & 1;
+        long long w1 = tick<TL>();
         mbar_wait(&q_full[st2], ph2);
+        tw[1] += tick<TL>() - w1;
         tc_fence_after();
         mma_sp(base + C::OFF_K, base + C::OFF_Q + st2 * C::QT, tmem + slot_s(x));   // after dV(n) read P^T
+        w1 = tick<TL>();
         mbar_wait(&dq_empty[x], (n >> 1) & 1);                                        // dQ^T(n) drained
+        tw[2] += tick<TL>() - w1;
+        w1 = tick<TL>();
         mbar_wait(&do_full[st2], ph2);
+        tw[3] += tick<TL>() - w1;
         tc_fence_after();
         mma_sp(base + C::OFF_V, base + C::OFF_DO + st2 * C::QT, tmem + slot_dp(x));
         mma_commit_w(&sdp_full[x]);
       }
     }
     mma_commit_w(dkv_full);
+    tw[4] = tick<TL>() - tbeg;
+    if (TL && a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0)
+      for (int i = 0; i < 5; ++i) a.dbg[i] = tw[i];
   } else if (warp < kSoftmaxWarps) {
     // ------------------------------------------------ softmax-gradient warpgroups: WG x owns slot x
     regs_inc<kRegsSoftmax>();
@@ -668,6 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       return r < 64 ? a.lse[(long long)h * a.ld_lse + q] * -1.4426950408889634f : a.delta[q * a.ld_delta + h];
     };
     float stat_next = x < N ? load_stat(x) : 0.f;
+    long long te[2] = {0, 0};                         // wait S/dP, E
     for (int n = x; n < N; n += 2) {
       const int qt = qt_begin + n % n_qt;
       const long long q0 = (long long)qt * 64;
@@ -676,8 +691,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* s_delta = stats + ((x * 2 + par) * 2 + 1) * 64;
       (r < 64 ? s_lse2 : s_delta)[r & 63] = stat_next;
       if (n + 2 < N) stat_next = load_stat(n + 2);
+      const long long e0 = tick<TL>();
       if (quad == 0) mbar_wait(&sdp_full[x], (n >> 1) & 1);
       named_bar_sync(1 + x, kWg);
+      const long long e1 = tick<TL>();
+      te[0] += e1 - e0;
       tc_fence_after();
       const bool need_mask = (a.causal && (qt >> 1) == jb) || q0 + 64 > a.S || (long long)jb * 128 + 128 > a.S;
       const long long qmin = key >= a.S ? a.S : (a.causal ? key : 0);
@@ -738,6 +756,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&ds_full[x]);
+      te[1] += tick<TL>() - e1;
+    }
+    if (TL && a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && quad == 0 && lane == 0) {
+      a.dbg[5 + 2 * x] = te[0];
+      a.dbg[6 + 2 * x] = te[1];
     }
     // ---- dK / dV epilogue (TMEM lane = key row): warpgroup 0 writes dV, warpgroup 1 dK
     mbar_wait(dkv_full, 0);
@@ -785,12 +808,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     uint8_t* const box = smem + C::OFF_STG + quad * 8192;
     const uint32_t bbase = smem_u32(box);
+    long long td[1] = {0};
     for (int n = 0; n < N; ++n) {
       const int x = n & 1;
       const int h = g * G + n / n_qt;
       const int q0 = (qt_begin + n % n_qt) * 64;
+      const long long d0 = tick<TL>();
       if (lane == 0) mbar_wait(&dq_full[x], (n >> 1) & 1);
       __syncwarp();
+      td[0] += tick<TL>() - d0;
       tc_fence_after();
       uint32_t rq[2][32];
       const uint32_t tq = tmem + (x ? C::TM_DP1 : C::TM_DP0) + lane_off;
@@ -814,6 +840,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (lane == 0) bulk_wait0();
+    if (TL && a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && quad == 0 && lane == 0) {
+      a.dbg[9] = td[0];
+      a.dbg[10] = N;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -878,7 +908,7 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
     const char* v = getenv("UPIPE_BWD_Q64");
     return !(v && v[0] == '0');
   }();
-  if (p.d == 128 && q64 && !a.dbg) {
+  if (p.d == 128 && q64) {
     CUtensorMap tq64, tdo64, tdq64;
     if (!make_tmap_3d(&tq64, p.q, p.d, p.nq, p.S, p.d, p.ldq, 64, 1, 64, err, errlen)) return cudaErrorInvalidValue;
     if (!make_tmap_3d(&tdo64, p.dout, p.d, p.nq, p.S, p.d, p.ldo_grad, 64, 1, 64, err, errlen))
@@ -886,12 +916,26 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
     if (!make_tmap_2d_f32(&tdq64, p.dq_acc, (uint64_t)p.nq * p.d, p.S, (uint64_t)p.nq * p.d, 32, 64, err, errlen))
       return cudaErrorInvalidValue;
     static const cudaError_t attr =
-        cudaFuncSetAttribute(attn_bwd_q64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Q64Cfg::SMEM);
+        cudaFuncSetAttribute(attn_bwd_q64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q64Cfg::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd_q64 attr: %s", cudaGetErrorString(attr)); return attr; }
-    attn_bwd_q64_kernel<<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
+    static const cudaError_t attr2 =
+        cudaFuncSetAttribute(attn_bwd_q64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q64Cfg::SMEM);
+    if (attr2 != cudaSuccess) { snprintf(err, errlen, "attn_bwd_q64 attr: %s", cudaGetErrorString(attr2)); return attr2; }
+    if (a.dbg) attn_bwd_q64_kernel<true><<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
+    else attn_bwd_q64_kernel<false><<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
     count_launches(1);
     e = cudaGetLastError();
     if (e != cudaSuccess) snprintf(err, errlen, "attn_bwd_q64 launch: %s", cudaGetErrorString(e));
+    if (a.dbg) {
+      long long h[16];
+      cudaMemcpyAsync(h, a.dbg, sizeof h, cudaMemcpyDeviceToHost, stream);
+      cudaStreamSynchronize(stream);
+      fprintf(stderr,
+              "[attn_bwd_q64 timeline CTA(0,0) N=%lld 64-query tiles, cycles] mma: wait_dS %lld wait_Q %lld "
+              "wait_dQdrain %lld wait_dO %lld total %lld | WG0: wait_SdP %lld E %lld | WG1: wait_SdP %lld E %lld | "
+              "drain: wait_dQ %lld\n",
+              h[10], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
+    }
     return e;
   }
   if (p.d == 128) {
