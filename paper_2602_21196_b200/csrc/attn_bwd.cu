@@ -1,4 +1,7 @@
 // Causal GQA flash-attention backward for sm_100a (Table 4).
+// Two kernels: attn_bwd_q64_kernel (below the first, d = 128, the default: 64-query tiles in two TMEM
+// slots, ping-pong) and attn_bwd_kernel<d> (128-query tiles; d = 64, and d = 128 with UPIPE_BWD_Q64=0),
+// described here.
 //
 // KV-stationary: one CTA owns a 128-key tile of one KV head and loops over the
 // query tiles (of every local query head of that KV group) that can see it.
