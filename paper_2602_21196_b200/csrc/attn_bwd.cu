@@ -905,12 +905,15 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   const int nT = (int)((p.S + 127) / 128);
   dim3 grid(nT, p.nkv);
   cudaError_t e;
-  // d = 128: the 64-query ping-pong kernel (default; UPIPE_BWD_Q64=0 selects the 128-query kernel,
-  // which also serves d = 64 and the UPIPE_BWD_TIMELINE diagnostics)
-  static const bool q64 = [] {
+  // d = 128: the 64-query ping-pong kernel up to S = 256K, the 128-query kernel beyond. Under the
+  // 1000 W power cap the 64-query kernel runs at lower SM clocks (its tensor pipe is busier and it
+  // issues more instructions): it wins at 128K (attn bwd 375 -> 348 ms per step) but loses at 512K
+  // (6005 -> 6091 ms; profiles/r01_ab_bwd_q64_512k.txt). UPIPE_BWD_Q64=1 / 0 forces either kernel.
+  static const int q64_env = [] {
     const char* v = getenv("UPIPE_BWD_Q64");
-    return !(v && v[0] == '0');
+    return v ? (v[0] == '1' ? 1 : 0) : -1;
   }();
+  const bool q64 = q64_env >= 0 ? q64_env == 1 : p.S <= 262144;
   if (p.d == 128 && q64) {
     CUtensorMap tq64, tdo64, tdq64;
     if (!make_tmap_3d(&tq64, p.q, p.d, p.nq, p.S, p.d, p.ldq, 64, 1, 64, err, errlen)) return cudaErrorInvalidValue;
