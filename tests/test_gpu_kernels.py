@@ -155,3 +155,19 @@ def test_synth_device_generator_bitwise(U):
     torch.cuda.synchronize()
     host = synth.draw(seed, tid, (n,), e, start=start)
     assert np.array_equal(to_np(t), host)
+
+
+def test_bwd_128_query_kernel_subprocess():
+    # d = 128 runs the 64-query backward kernel up to S = 256K and the 128-query kernel beyond;
+    # the kernel choice is read once per process, so the 128-query kernel's parity runs in a child process
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("UPIPE_BWD_Q64") == "0":
+        pytest.skip("already the 128-query kernel")
+    env = dict(os.environ, UPIPE_BWD_Q64="0")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_kernels.py"), "-q", "-x",
+                        "-m", "gpu", "-k", "bwd and not subprocess"], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
