@@ -186,7 +186,7 @@ upipe_status_t ensure_pipe(upipe_ctx_s* ctx) {
 upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf16p wk, bf16p wv, bf16p wo,
                          upipe_bf16* y, upipe_bf16* o_saved, float* lse_saved, char* ws, cudaStream_t st) {
   const bool ov = overlap_enabled(ctx->flags, P);
-  if (ov) {
+  if (ov || P.ring > 1) {                               // the ring hybrid overlaps its transfers on the comm stream
     if (upipe_status_t s = ensure_pipe(ctx)) return s;
   }
   Runner R{ctx};
@@ -269,28 +269,49 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     const int r = P.ring;
     const int nxt = ((ring_i + 1) % r) * C + me, prv = ((ring_i + r - 1) % r) * C + me;
     const size_t kvbytes = (size_t)P.S * kseg * 2;
-    const void* kc = a.k;
-    const void* vc = a.v;
+    // The ring transfers run on the ctx's comm stream, one step ahead of the attention on q: step t+1's
+    // K/V block travels while step t's block is attended (double-buffered ring buffers; the comm stream
+    // waits until the attention of step t-1 has read the buffer it receives into). Every collective of
+    // the ring is issued on the comm stream, in the same order on every rank.
+    cudaStream_t cs = ctx->pipe.comm;
+    cudaEvent_t* rev = ctx->pipe.ev + 13;               // [0] own block ready, [1..2] received, [3..4] read
+    auto ring_step = [&](int t, const void* ks, const void* vs) {   // receive block of step t into set t & 1
+      char* kn = ws + W.kring[t & 1];
+      char* vn = ws + W.vring[t & 1];
+      if (t >= 3) cudaStreamWaitEvent(cs, rev[3 + (t & 1)], 0);   // attention of step t-2 read this set
+      R.comm(cs, "ring K", [&](std::string& m) { return T.sendrecv(ks, nxt, kn, prv, kvbytes, cs, m); });
+      R.comm(cs, "ring V", [&](std::string& m) { return T.sendrecv(vs, nxt, vn, prv, kvbytes, cs, m); });
+      cudaEventRecord(rev[1 + (t & 1)], cs);
+    };
+    if (r > 1) {
+      cudaEventRecord(rev[0], q);                       // own K/V block (and the stage's a2a) complete
+      cudaStreamWaitEvent(cs, rev[0], 0);
+      ring_step(1, a.k, a.v);
+    }
     for (int t = 1; t < r && R.status == UPIPE_OK; ++t) {
       char* kn = ws + W.kring[t & 1];
       char* vn = ws + W.vring[t & 1];
-      R.comm(q, "ring K", [&](std::string& m) { return T.sendrecv(kc, nxt, kn, prv, kvbytes, q, m); });
-      R.comm(q, "ring V", [&](std::string& m) { return T.sendrecv(vc, nxt, vn, prv, kvbytes, q, m); });
-      kc = kn;
-      vc = vn;
+      if (t + 1 < r) ring_step(t + 1, kn, vn);          // forward block t while it is attended (read-only)
+      cudaStreamWaitEvent(q, rev[1 + (t & 1)], 0);
       const int j = (ring_i + r - t) % r;
-      if (P.sh.causal && j > ring_i) continue;           // the whole block lies after every local query
-      AttnFwdProblem b2 = a;
-      b2.k = kn;
-      b2.v = vn;
-      b2.causal = 0;                                      // j < i: every key precedes every local query
-      b2.o32 = (float*)(ws + W.opart);
-      b2.lse = (float*)(ws + W.lsepart);
-      R.run(UPIPE_TRACE_ATTN_FWD, q, "attn fwd (ring block)", [&](char* e) { return attn_fwd_run(b2, q, e, 512); });
-      R.run(UPIPE_TRACE_AUX, q, "merge partials", [&](char*) {
-        return merge_partials_run((float*)(ws + W.oacc), (const float*)(ws + W.opart), qseg, lse_acc,
-                                  (const float*)(ws + W.lsepart), P.S, P.S, P.qpd, d, q);
-      });
+      if (!(P.sh.causal && j > ring_i)) {                // else the whole block lies after every local query
+        AttnFwdProblem b2 = a;
+        b2.k = kn;
+        b2.v = vn;
+        b2.causal = 0;                                    // j < i: every key precedes every local query
+        b2.o32 = (float*)(ws + W.opart);
+        b2.lse = (float*)(ws + W.lsepart);
+        R.run(UPIPE_TRACE_ATTN_FWD, q, "attn fwd (ring block)", [&](char* e) { return attn_fwd_run(b2, q, e, 512); });
+        R.run(UPIPE_TRACE_AUX, q, "merge partials", [&](char*) {
+          return merge_partials_run((float*)(ws + W.oacc), (const float*)(ws + W.opart), qseg, lse_acc,
+                                    (const float*)(ws + W.lsepart), P.S, P.S, P.qpd, d, q);
+        });
+      }
+      cudaEventRecord(rev[3 + (t & 1)], q);             // step t's buffers read
+    }
+    if (r > 1) {                                        // the comm stream's work is done before the next stage
+      cudaEventRecord(rev[0], cs);
+      cudaStreamWaitEvent(q, rev[0], 0);
     }
     R.run(UPIPE_TRACE_AUX, q, "O fp32 -> bf16", [&](char*) {
       return cvt_f32_bf16_run((const float*)(ws + W.oacc), qseg, o_dst, ld_dst, P.S, qseg, 1.0f, q);
@@ -384,7 +405,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
                          bf16p dy, bf16p o_saved, const float* lse_saved, upipe_bf16* dx, float* dwq, float* dwk,
                          float* dwv, float* dwo, int reduce_dw, char* ws, cudaStream_t st) {
   const bool ov = overlap_enabled(ctx->flags, P);
-  if (ov) {
+  if (ov || P.ring > 1) {                               // the ring hybrid overlaps its transfers on the comm stream
     if (upipe_status_t s = ensure_pipe(ctx)) return s;
   }
   Runner R{ctx};
@@ -560,38 +581,53 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       bp.dv_acc = (float*)(ws + W.dvacc);
       bp.dk_bf16 = bp.dv_bf16 = nullptr;
       bp.kv_write_acc = 1;
+      // Overlapped ring (all ring collectives on the ctx's comm stream, same order on every rank): the
+      // accumulators of step t travel right after this rank's attention of step t-1 (that dependency is
+      // inherent), then step t+1's K/V block is forwarded while step t is attended.
+      cudaStream_t cs = ctx->pipe.comm;
+      cudaEvent_t* rev = ctx->pipe.ev + 13;             // [0] join, [1..2] step received, [3..4] step computed
+      cudaEventRecord(rev[0], q);                       // the stage's K/V, dO, delta are in place
+      cudaStreamWaitEvent(cs, rev[0], 0);
+      R.comm(cs, "ring K", [&](std::string& m) { return T.sendrecv(bp.k, nxt, ws + W.kring[1], prv, kvbytes, cs, m); });
+      R.comm(cs, "ring V", [&](std::string& m) { return T.sendrecv(bp.v, nxt, ws + W.vring[1], prv, kvbytes, cs, m); });
       R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd (ring own block)", [&](char* e) { return attn_bwd_run(bp, q, e, 512); });
-      const void* kc = bp.k;
-      const void* vc = bp.v;
-      const float* dkc = bp.dk_acc;
-      const float* dvc = bp.dv_acc;
+      cudaEventRecord(rev[3], q);                       // step 0 computed (rev[3 + (t & 1)] for step t)
       for (int t = 1; t <= rr && R.status == UPIPE_OK; ++t) {
-        const bool home = t == rr;                        // last hop: the accumulators return to their owner
-        char* kn = ws + W.kring[t & 1];
-        char* vn = ws + W.vring[t & 1];
+        const bool home = t == rr;                      // last hop: the accumulators return to their owner
+        const float* dks = t == 1 ? (const float*)(ws + W.dkacc) : (const float*)(ws + W.dkring[(t - 1) & 1]);
+        const float* dvs = t == 1 ? (const float*)(ws + W.dvacc) : (const float*)(ws + W.dvring[(t - 1) & 1]);
         float* dkn = home ? (float*)(ws + W.dkacc) : (float*)(ws + W.dkring[t & 1]);
         float* dvn = home ? (float*)(ws + W.dvacc) : (float*)(ws + W.dvring[t & 1]);
-        if (!home) {
-          R.comm(q, "ring K", [&](std::string& m) { return T.sendrecv(kc, nxt, kn, prv, kvbytes, q, m); });
-          R.comm(q, "ring V", [&](std::string& m) { return T.sendrecv(vc, nxt, vn, prv, kvbytes, q, m); });
+        cudaStreamWaitEvent(cs, rev[3 + ((t - 1) & 1)], 0);   // this rank's step t-1 contributions are in
+        R.comm(cs, "ring dK", [&](std::string& m) { return T.sendrecv(dks, nxt, dkn, prv, kvbytes * 2, cs, m); });
+        R.comm(cs, "ring dV", [&](std::string& m) { return T.sendrecv(dvs, nxt, dvn, prv, kvbytes * 2, cs, m); });
+        cudaEventRecord(rev[1 + (t & 1)], cs);
+        if (home) break;
+        char* kn = ws + W.kring[t & 1];
+        char* vn = ws + W.vring[t & 1];
+        if (t + 1 < rr) {                               // forward block t while it is attended (read-only)
+          R.comm(cs, "ring K", [&](std::string& m) {
+            return T.sendrecv(kn, nxt, ws + W.kring[(t + 1) & 1], prv, kvbytes, cs, m);
+          });
+          R.comm(cs, "ring V", [&](std::string& m) {
+            return T.sendrecv(vn, nxt, ws + W.vring[(t + 1) & 1], prv, kvbytes, cs, m);
+          });
         }
-        R.comm(q, "ring dK", [&](std::string& m) { return T.sendrecv(dkc, nxt, dkn, prv, kvbytes * 2, q, m); });
-        R.comm(q, "ring dV", [&](std::string& m) { return T.sendrecv(dvc, nxt, dvn, prv, kvbytes * 2, q, m); });
-        kc = kn;
-        vc = vn;
-        dkc = dkn;
-        dvc = dvn;
+        cudaStreamWaitEvent(q, rev[1 + (t & 1)], 0);
         const int j = (ring_i + rr - t) % rr;
-        if (home || (P.sh.causal && j > ring_i)) continue;
-        AttnBwdProblem b2 = bp;
-        b2.k = kn;
-        b2.v = vn;
-        b2.dk_acc = dkn;
-        b2.dv_acc = dvn;
-        b2.causal = 0;
-        b2.kv_accumulate = 1;
-        R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd (ring block)", [&](char* e) { return attn_bwd_run(b2, q, e, 512); });
+        if (!(P.sh.causal && j > ring_i)) {
+          AttnBwdProblem b2 = bp;
+          b2.k = kn;
+          b2.v = vn;
+          b2.dk_acc = dkn;
+          b2.dv_acc = dvn;
+          b2.causal = 0;
+          b2.kv_accumulate = 1;
+          R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd (ring block)", [&](char* e) { return attn_bwd_run(b2, q, e, 512); });
+        }
+        cudaEventRecord(rev[3 + (t & 1)], q);
       }
+      cudaStreamWaitEvent(q, rev[1 + (rr & 1)], 0);     // the home hop has landed
       if (last) {
         RopeRef rope_k = rope_head;                       // dK rows are the ring block's keys
         R.run(UPIPE_TRACE_AUX, q, "cvt dK", [&](char*) {
