@@ -362,7 +362,17 @@ def main():
     main_run["attn"].close()
 
     if not args.quick and not args.no_ulysses and U != Hq:
-        ul = run(Hq, max(2, args.steps // 2), 1)
+        try:
+            ul = run(Hq, max(2, args.steps // 2), 1)
+        except torch.OutOfMemoryError as exc:       # the max-context regime: Ulysses' full-head buffers do not fit
+            main_run["attn"].close()
+            torch.cuda.empty_cache()
+            result["ulysses"] = {"chunk_heads": Hq, "oom": True, "error": str(exc).splitlines()[0][:200],
+                                 "gpu_total_gib": torch.cuda.get_device_properties(dev).total_memory / 2**30}
+            ul = None
+    else:
+        ul = None
+    if ul is not None:
         ul_tok = S * max(2, args.steps // 2) / (ul["ms"] / 1e3)
         result["ulysses"] = {"chunk_heads": Hq, "value": ul_tok, "unit": "tokens/s",
                              "upipe_over_ulysses": tok_s / ul_tok,
