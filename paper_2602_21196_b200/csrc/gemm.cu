@@ -50,13 +50,6 @@ struct GemmArgs {
   DevOut c[kMaxParts];
 };
 
-__device__ __forceinline__ int map_outer(const DevOpMap& m, int i, int k) {
-  return m.o_base + (i / m.o_len) * m.o_istride + i % m.o_len + (k / m.k_len) * m.o_kstride;
-}
-__device__ __forceinline__ int map_k(const DevOpMap& m, int i, int k) {
-  return m.k_base + (k / m.k_len) * m.k_kstride + k % m.k_len + (i / m.o_len) * m.k_istride;
-}
-
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int GRANULE_BYTES = 64 * 64 * 2;  // one TMA box: 64 x 64 bf16

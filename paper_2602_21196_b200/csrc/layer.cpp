@@ -62,7 +62,6 @@ struct Runner {
   upipe_ctx_s* ctx;
   upipe_status_t status = UPIPE_OK;
   char errbuf[512] = {0};
-  bool cuda(int cat, cudaStream_t s, const char* what, cudaError_t (*)(void) = nullptr) { (void)cat; (void)s; (void)what; return true; }
   template <class F>
   bool run(int cat, cudaStream_t s, const char* what, F&& f) {
     if (status != UPIPE_OK) return false;
