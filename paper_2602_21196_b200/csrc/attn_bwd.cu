@@ -544,6 +544,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int qt_begin = a.causal ? 2 * jb : 0;
   const int n_qt = nT64 - qt_begin;
   const int N = G * n_qt;
+  // Query tiles are visited from the last one down to the diagonal: CTAs that run at the same time then
+  // reduce their dQ partials into the same rows of dq_acc (L2 hits) instead of each starting at its own
+  // diagonal and sweeping a different region (measured: the dQ reduce-adds dominated the energy)
   constexpr int kWg = 128;
 
   if (warp == kTmaWarp && lane == 0) {
@@ -569,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int n = 0; n < N; ++n) {
         const int h = g * G + n / n_qt;
-        const int qt = qt_begin + n % n_qt;
+        const int qt = nT64 - 1 - n % n_qt;
         const int st = n % C::NQ;
         const uint32_t ph = ((n / C::NQ) & 1) ^ 1;
         mbar_wait(&q_empty[st], ph);
@@ -680,14 +683,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t dsbase = smem_u32(smem + C::OFF_DS + x * 16384);
     auto load_stat = [&](int n) -> float {            // threads 0-63: -lse*log2e of query r, 64-127: delta
       const int h = g * G + n / n_qt;
-      const long long q = (long long)(qt_begin + n % n_qt) * 64 + (r & 63);
+      const long long q = (long long)(nT64 - 1 - n % n_qt) * 64 + (r & 63);
       if (q >= a.S) return 0.f;
       return r < 64 ? a.lse[(long long)h * a.ld_lse + q] * -1.4426950408889634f : a.delta[q * a.ld_delta + h];
     };
     float stat_next = x < N ? load_stat(x) : 0.f;
     long long te[2] = {0, 0};                         // wait S/dP, E
     for (int n = x; n < N; n += 2) {
-      const int qt = qt_begin + n % n_qt;
+      const int qt = nT64 - 1 - n % n_qt;
       const long long q0 = (long long)qt * 64;
       const int par = (n >> 1) & 1;
       float* s_lse2 = stats + ((x * 2 + par) * 2 + 0) * 64;
@@ -815,7 +818,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int n = 0; n < N; ++n) {
       const int x = n & 1;
       const int h = g * G + n / n_qt;
-      const int q0 = (qt_begin + n % n_qt) * 64;
+      const int q0 = (nT64 - 1 - n % n_qt) * 64;
       const long long d0 = tick<TL>();
       if (lane == 0) mbar_wait(&dq_full[x], (n >> 1) & 1);
       __syncwarp();
