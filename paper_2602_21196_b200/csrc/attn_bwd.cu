@@ -52,6 +52,7 @@ struct BwdArgs {
   float scale;       // 1/sqrt(d)
   float scale_log2;  // log2(e)/sqrt(d)
   RopeRef rope;      // dK (bf16 output) rotated back by -angle(key) when set (RoPE on K, DESIGN A26)
+  int dq_dim_major;  // q64 kernel: dq_acc is [nq*d][S] (TMA boxes of 32 dims x 32 tokens)
   long long* dbg;    // optional per-role cycle breakdown of CTA (0,0) (UPIPE_BWD_TIMELINE=1)
 };
 
@@ -833,6 +834,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&dq_empty[x]);
       if (lane == 0) bulk_wait_read0();               // this warp's previous box has been read by its reduce
       __syncwarp();
+      if (a.dq_dim_major) {
+        // dim-major accumulator: row lane (dim) of two 32-token boxes, 16-byte chunks, 128B swizzle
+#pragma unroll
+        for (int bx = 0; bx < 2; ++bx)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(bbase + bx * 4096 + lane * 128 + ((j ^ (lane & 7)) << 4),
+                         __float_as_uint(__uint_as_float(rq[bx][4 * j + 0]) * a.scale),
+                         __float_as_uint(__uint_as_float(rq[bx][4 * j + 1]) * a.scale),
+                         __float_as_uint(__uint_as_float(rq[bx][4 * j + 2]) * a.scale),
+                         __float_as_uint(__uint_as_float(rq[bx][4 * j + 3]) * a.scale));
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_2d(&tmdQ, box, q0, h * D + quad * 32);
+          tma_reduce_add_2d(&tmdQ, box + 4096, q0 + 32, h * D + quad * 32);
+          bulk_commit();
+        }
+        continue;
+      }
       // row q (query), column lane (dim): 128B-swizzled rows of 32 fp32
 #pragma unroll
       for (int q = 0; q < 64; ++q)
@@ -859,7 +880,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// d = 128: the 64-query ping-pong kernel up to S = 256K, the 128-query kernel beyond. Under the
+// 1000 W power cap the 64-query kernel runs at lower SM clocks (its tensor pipe is busier and it
+// issues more instructions): it wins at 128K (attn bwd 375 -> 348 ms per step) but loses at 512K
+// (6005 -> 6091 ms; profiles/r01_ab_bwd_q64_512k.txt). UPIPE_BWD_Q64=1 / 0 forces either kernel.
+bool use_q64(const AttnBwdProblem& p) {
+  static const int q64_env = [] {
+    const char* v = getenv("UPIPE_BWD_Q64");
+    return v ? (v[0] == '1' ? 1 : 0) : -1;
+  }();
+  if (p.d != 128) return false;
+  return q64_env >= 0 ? q64_env == 1 : p.S <= 262144;
+}
+
 }  // namespace
+
+bool attn_bwd_dq_dim_major(const AttnBwdProblem& p) {
+  static const bool off = [] {
+    const char* v = getenv("UPIPE_DQ_DIM_MAJOR");
+    return v && v[0] == '0';
+  }();
+  return !off && use_q64(p);
+}
 
 cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err, size_t errlen) {
   if (p.S <= 0 || p.nkv <= 0) return cudaSuccess;
@@ -896,6 +938,7 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   a.scale = 1.f / sqrtf((float)p.d);
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)p.d);
   a.rope = p.rope;
+  a.dq_dim_major = 0;
   // UPIPE_BWD_TIMELINE=1: per-role cycle breakdown of CTA (0,0), printed to stderr after the launch
   static long long* dbg_dev = nullptr;
   const char* tlenv = getenv("UPIPE_BWD_TIMELINE");
@@ -908,22 +951,23 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   const int nT = (int)((p.S + 127) / 128);
   dim3 grid(nT, p.nkv);
   cudaError_t e;
-  // d = 128: the 64-query ping-pong kernel up to S = 256K, the 128-query kernel beyond. Under the
-  // 1000 W power cap the 64-query kernel runs at lower SM clocks (its tensor pipe is busier and it
-  // issues more instructions): it wins at 128K (attn bwd 375 -> 348 ms per step) but loses at 512K
-  // (6005 -> 6091 ms; profiles/r01_ab_bwd_q64_512k.txt). UPIPE_BWD_Q64=1 / 0 forces either kernel.
-  static const int q64_env = [] {
-    const char* v = getenv("UPIPE_BWD_Q64");
-    return v ? (v[0] == '1' ? 1 : 0) : -1;
-  }();
-  const bool q64 = q64_env >= 0 ? q64_env == 1 : p.S <= 262144;
-  if (p.d == 128 && q64) {
+  if (use_q64(p)) {
+    if (p.dq_dim_major && p.ld_dqt < p.S) {
+      snprintf(err, errlen, "attn_bwd: dim-major dq_acc needs ld_dqt >= S");
+      return cudaErrorInvalidValue;
+    }
+    a.dq_dim_major = p.dq_dim_major;
     CUtensorMap tq64, tdo64, tdq64;
     if (!make_tmap_3d(&tq64, p.q, p.d, p.nq, p.S, p.d, p.ldq, 64, 1, 64, err, errlen)) return cudaErrorInvalidValue;
     if (!make_tmap_3d(&tdo64, p.dout, p.d, p.nq, p.S, p.d, p.ldo_grad, 64, 1, 64, err, errlen))
       return cudaErrorInvalidValue;
-    if (!make_tmap_2d_f32(&tdq64, p.dq_acc, (uint64_t)p.nq * p.d, p.S, (uint64_t)p.nq * p.d, 32, 64, err, errlen))
+    if (p.dq_dim_major) {
+      if (!make_tmap_2d_f32(&tdq64, p.dq_acc, p.S, (uint64_t)p.nq * p.d, p.ld_dqt, 32, 32, err, errlen))
+        return cudaErrorInvalidValue;
+    } else if (!make_tmap_2d_f32(&tdq64, p.dq_acc, (uint64_t)p.nq * p.d, p.S, (uint64_t)p.nq * p.d, 32, 64, err,
+                                 errlen)) {
       return cudaErrorInvalidValue;
+    }
     static const cudaError_t attr =
         cudaFuncSetAttribute(attn_bwd_q64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q64Cfg::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd_q64 attr: %s", cudaGetErrorString(attr)); return attr; }

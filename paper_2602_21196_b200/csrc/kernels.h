@@ -110,8 +110,13 @@ struct AttnBwdProblem {
   int kv_accumulate;                          // 1: add the previous dk_acc/dv_acc contents
   int kv_write_acc;                           // 1: write fp32 accumulators back
   RopeRef rope;                               // dk_bf16 is rotated back by -angle(key) (RoPE on K)
+  int dq_dim_major = 0;                       // 1 (only where attn_bwd_dq_dim_major() allows): dq_acc is
+  int64_t ld_dqt = 0;                         //   [nq*d][S] fp32, row stride ld_dqt (tokens contiguous)
 };
 cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err, size_t errlen);
+// Whether attn_bwd_run can accumulate dQ dim-major for this problem (the 64-query kernel, whose dQ^T
+// tile has one head dimension per TMEM lane, then stages 16-byte vectors instead of transposing).
+bool attn_bwd_dq_dim_major(const AttnBwdProblem& p);
 
 // ---------------------------------------------------------------- HBM-bound helpers
 // delta[t][j] = sum_e dO[t][j*d+e] * O[t][j*d+e] over bf16 inputs, fp32 result.
@@ -122,6 +127,10 @@ cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t l
                              float scale, cudaStream_t s, const RopeRef& inverse_rope);
 cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
                              float scale, cudaStream_t s);
+// The same from a dim-major source: dst[t][c] = bf16(scale * src[c][t]) (src row stride lds, tokens
+// contiguous), with the inverse RoPE of token rope.pos0 + t on column pairs; cols % 64 == 0.
+cudaError_t cvt_dimmajor_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows,
+                                      int64_t cols, float scale, cudaStream_t s, const RopeRef& inverse_rope);
 // Ring-step combine (DESIGN A27), per row t and head j of [rows][nheads][d]:
 //   lse' = log(e^lse_acc + e^lse_part) (max-subtracted), O' = e^(lse_acc-lse') O_acc + e^(lse_part-lse') O_part,
 // O fp32, lse [nheads][ld_lse]; writes o_acc and lse_acc in place.

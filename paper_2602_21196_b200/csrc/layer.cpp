@@ -567,6 +567,8 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     bp.kv_accumulate = r > 0;
     bp.kv_write_acc = !last;
     bp.rope = rope_head;
+    bp.dq_dim_major = attn_bwd_dq_dim_major(bp) ? 1 : 0;   // [qpd*d][S] accumulator (64-query kernel)
+    bp.ld_dqt = P.S;
     if (P.ring == 1) {
       R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd", [&](char* e) { return attn_bwd_run(bp, q, e, 512); });
     } else {
@@ -638,6 +640,9 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       }
     }
     R.run(UPIPE_TRACE_AUX, q, "cvt dQ", [&](char*) {
+      if (bp.dq_dim_major)
+        return cvt_dimmajor_f32_bf16_run((const float*)(ws + W.dqacc[b]), P.S, ws + W.dqsend[b], qseg, P.S, qseg,
+                                         1.0f, q, rope_head);
       return cvt_f32_bf16_run((const float*)(ws + W.dqacc[b]), qseg, ws + W.dqsend[b], qseg, P.S, qseg, 1.0f, q,
                               rope_head);
     });

@@ -104,6 +104,38 @@ __global__ void cvt_kernel(const float* __restrict__ src, long long lds, __nv_bf
   }
 }
 
+// 32 tokens x 64 dims per tile through shared memory: coalesced 128-byte reads along tokens, 16-byte
+// bf16 writes along dims (RoPE pairs are adjacent dims of one token).
+__global__ void cvt_dimmajor_kernel(const float* __restrict__ src, long long lds, __nv_bfloat16* __restrict__ dst,
+                                    long long ldd, long long rows, long long cols, float scale, RopeRef rope) {
+  __shared__ float tile[64][33];
+  const long long ntt = (rows + 31) / 32, nct = cols / 64;
+  const int t = threadIdx.x;
+  for (long long blk = blockIdx.x; blk < ntt * nct; blk += gridDim.x) {
+    const long long t0 = (blk / nct) * 32, c0 = (blk % nct) * 64;
+    {
+      const int c = t >> 2, tk = (t & 3) * 8;       // dim c of the tile, tokens tk..tk+7
+      const float* sp = src + (c0 + c) * lds + t0 + tk;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) tile[c][tk + i] = (t0 + tk + i < rows) ? sp[i] : 0.f;
+    }
+    __syncthreads();
+    {
+      const int tk = t >> 3, cg = (t & 7) * 8;      // token tk, dims cg..cg+7
+      if (t0 + tk < rows) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = tile[cg + i][tk] * scale;
+        if (rope.hi) dev::rope_rotate<4>(v, rope.hi, rope.lo, rope.d, rope.pos0 + t0 + tk, (int)((c0 + cg) % rope.d), -1.f);
+        *reinterpret_cast<uint4*>(dst + (t0 + tk) * ldd + c0 + cg) =
+            make_uint4(dev::pack_bf16(v[0], v[1]), dev::pack_bf16(v[2], v[3]), dev::pack_bf16(v[4], v[5]),
+                       dev::pack_bf16(v[6], v[7]));
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void unpack_kernel(const uint4* __restrict__ src, long long rows, int nseg, int seg_v,
                               __nv_bfloat16* __restrict__ dst, long long ldd, long long col_base,
                               long long col_stride) {
@@ -184,6 +216,17 @@ cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t l
 cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
                              float scale, cudaStream_t s) {
   return cvt_f32_bf16_run(src, lds, dst, ldd, rows, cols, scale, s, RopeRef{});
+}
+
+cudaError_t cvt_dimmajor_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows,
+                                      int64_t cols, float scale, cudaStream_t s, const RopeRef& inverse_rope) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  if (cols % 64) return cudaErrorInvalidValue;
+  const long long tiles = ((rows + 31) / 32) * (cols / 64);
+  const int grid = (int)(tiles < 148 * 8 ? tiles : 148 * 8);
+  cvt_dimmajor_kernel<<<grid, 256, 0, s>>>(src, lds, (__nv_bfloat16*)dst, ldd, rows, cols, scale, inverse_rope);
+  count_launches(1);
+  return cudaGetLastError();
 }
 
 cudaError_t unpack_cols_run(const void* src, int64_t rows, int nseg, int seg_cols, void* dst, int64_t ldd,
