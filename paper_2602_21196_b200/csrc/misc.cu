@@ -116,8 +116,14 @@ __global__ void cvt_dimmajor_kernel(const float* __restrict__ src, long long lds
     {
       const int c = t >> 2, tk = (t & 3) * 8;       // dim c of the tile, tokens tk..tk+7
       const float* sp = src + (c0 + c) * lds + t0 + tk;
+      if ((lds & 3) == 0 && t0 + tk + 8 <= rows) {   // 2 x 16-byte loads (rows of 4-aligned length)
+        const float4 x = *reinterpret_cast<const float4*>(sp), y = *reinterpret_cast<const float4*>(sp + 4);
+        tile[c][tk + 0] = x.x; tile[c][tk + 1] = x.y; tile[c][tk + 2] = x.z; tile[c][tk + 3] = x.w;
+        tile[c][tk + 4] = y.x; tile[c][tk + 5] = y.y; tile[c][tk + 6] = y.z; tile[c][tk + 7] = y.w;
+      } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) tile[c][tk + i] = (t0 + tk + i < rows) ? sp[i] : 0.f;
+        for (int i = 0; i < 8; ++i) tile[c][tk + i] = (t0 + tk + i < rows) ? sp[i] : 0.f;
+      }
     }
     __syncthreads();
     {
