@@ -880,17 +880,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// d = 128: the 64-query ping-pong kernel up to S = 256K, the 128-query kernel beyond. Under the
-// 1000 W power cap the 64-query kernel runs at lower SM clocks (its tensor pipe is busier and it
-// issues more instructions): it wins at 128K (attn bwd 375 -> 348 ms per step) but loses at 512K
-// (6005 -> 6091 ms; profiles/r01_ab_bwd_q64_512k.txt). UPIPE_BWD_Q64=1 / 0 forces either kernel.
+// d = 128: the 64-query ping-pong kernel. Under the 1000 W power cap it runs at lower SM clocks than
+// the 128-query kernel (busier tensor pipe), yet with the dim-major dQ accumulator and last-to-first
+// query order it is ahead at every length measured: attn bwd per step 375 -> 340 ms at 128K, 5940 ->
+// 5618 ms at 512K, 24184 -> 24066 ms at 1M (profiles/r01_ab_bwd_q64_dimmajor_512k_1m.txt). Before those
+// two changes it lost at 512K (6005 vs 6091 ms). UPIPE_BWD_Q64=0 selects the 128-query kernel.
 bool use_q64(const AttnBwdProblem& p) {
   static const int q64_env = [] {
     const char* v = getenv("UPIPE_BWD_Q64");
     return v ? (v[0] == '1' ? 1 : 0) : -1;
   }();
   if (p.d != 128) return false;
-  return q64_env >= 0 ? q64_env == 1 : p.S <= 262144;
+  return q64_env != 0;
 }
 
 }  // namespace
