@@ -158,8 +158,8 @@ def test_synth_device_generator_bitwise(U):
 
 
 def test_bwd_128_query_kernel_subprocess():
-    # d = 128 runs the 64-query backward kernel; the 128-query kernel (d = 64, and UPIPE_BWD_Q64=0);
-    # the kernel choice is read once per process, so the 128-query kernel's parity runs in a child process
+    # d = 128 runs the 64-query backward kernel; the 128-query kernel serves d = 64 and UPIPE_BWD_Q64=0
+    # (DESIGN §7). The choice is read once per process, so its d = 128 parity runs in a child process.
     import os
     import subprocess
     import sys
