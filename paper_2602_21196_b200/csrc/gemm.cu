@@ -352,6 +352,47 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const bool mvalid = m < g.M;
       const long long mseg = mvalid ? ml / oc_.m_len : 0, min_ = mvalid ? ml % oc_.m_len : 0;
+      if (g.c_tma == 2 && pc == 0) {
+        // bf16 store through shared memory: each warp stages its 32 rows x 64 columns (128B swizzle,
+        // two 4 KB slots) and issues one TMA store per box into the output's 3-D view {col, row, segment}
+        // (full-line writes instead of 32 rows x 16 bytes per store instruction)
+#pragma unroll 1
+        for (int c64 = 0; c64 < BN / 64; ++c64) {
+          const int n = n0 + c64 * 64;
+          if (n >= g.N) break;                          // uniform across the CTA
+          uint32_t r[64];
+          tmem_ld32(tmem + ab * BN + ((uint32_t)(quad * 32) << 16) + c64 * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
+          tmem_ld32(tmem + ab * BN + ((uint32_t)(quad * 32) << 16) + c64 * 64 + 32,
+                    *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+          tmem_wait_ld();
+          float v[64];
+#pragma unroll
+          for (int q = 0; q < 64; ++q) v[q] = __uint_as_float(r[q]) * g.alpha;
+          if (oc_.rope.hi) {
+            rope_rotate<16>(v, oc_.rope.hi, oc_.rope.lo, oc_.rope.d, oc_.rope.pos0 + m, n % oc_.rope.d, 1.f);
+            rope_rotate<16>(v + 32, oc_.rope.hi, oc_.rope.lo, oc_.rope.d, oc_.rope.pos0 + m, (n + 32) % oc_.rope.d, 1.f);
+          }
+          const uint32_t slot = smem_u32(smem + C::STG + quad * 8192 + (c64 & 1) * 4096);
+          if (lane == 0) bulk_wait_read1();             // the store that last used this slot has read it
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(slot + lane * 128 + ((j ^ (lane & 7)) << 4), pack_bf16(v[8 * j + 0], v[8 * j + 1]),
+                         pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                         pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const long long seg = n / oc_.n_len, nin = n % oc_.n_len;
+            tma_store_3d(&tmC, smem + C::STG + quad * 8192 + (c64 & 1) * 4096, (int)nin, m0 + quad * 32, (int)seg);
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        if (PAIR && crank != leader) mbar_arrive_cluster(mapa_shared(&acc_empty[ab], leader));
+        else mbar_arrive(&acc_empty[ab]);
+        continue;
+      }
 #pragma unroll 1
       for (int c32 = 0; c32 < BN / 32; ++c32) {
         uint32_t r[32];
@@ -359,7 +400,7 @@ __global__ void __launch_bounds__(192, 1)
         tmem_wait_ld();
         const int n = n0 + c32 * 32;
         if (n >= g.N) continue;                 // uniform across the CTA
-        if (g.c_tma && pc == 0 && (oc_.epi == (int)Epi::kStoreF32 || oc_.epi == (int)Epi::kAccF32)) {
+        if (g.c_tma == 1 && pc == 0 && (oc_.epi == (int)Epi::kStoreF32 || oc_.epi == (int)Epi::kAccF32)) {
           // fp32 tile column box -> swizzled staging slot -> one TMA store / reduce-add by warp 2 lane 0
           // (L2 performs the accumulation: no global read by the SM, no per-thread RMW latency)
           const bool issuer = warp == 2 && lane == 0;
@@ -422,7 +463,7 @@ __global__ void __launch_bounds__(192, 1)
       if (PAIR && crank != leader) mbar_arrive_cluster(mapa_shared(&acc_empty[ab], leader));
       else mbar_arrive(&acc_empty[ab]);
     }
-    if (g.c_tma && warp == 2 && lane == 0) bulk_wait0();   // staged boxes fully written before exit
+    if ((g.c_tma == 1 && warp == 2 && lane == 0) || (g.c_tma == 2 && lane == 0)) bulk_wait0();   // staged boxes written
   }
   tc_fence_before();
   __syncthreads();
@@ -676,6 +717,25 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
       if (!make_tmap_2d_f32(&tc, c0.out_f32, (uint64_t)p0.N, (uint64_t)M, (uint64_t)c0.ld_f32, 32, 128, err, errlen))
         return cudaErrorInvalidValue;
       args.c_tma = 1;
+    }
+    // bf16 stores (projections into the a2a send layout, the output projection): 3-D view {col within
+    // the segment, row, segment} so boxes clip at the segment's last row (ragged S_l)
+    static const int tma_bf16_env = [] {
+      const char* e = getenv("UPIPE_GEMM_TMA_BF16");
+      return e ? atoi(e) : 1;
+    }();
+    const bool seg_rows_ok = c0.r_mstride == 0 && c0.m_len >= M && c0.r_base == 0 && c0.c_base == 0 &&
+                             c0.c_nstride == 0 && c0.c_mstride == 0;
+    const int64_t nlen = c0.n_len < p0.N ? c0.n_len : p0.N;
+    const int64_t nseg = (p0.N + nlen - 1) / nlen;
+    if (tma_epi_env && tma_bf16_env && !args.c_tma && kind == GemmGroup::kKConcat && c0.epi == Epi::kStoreBF16 &&
+        seg_rows_ok && c0.out_bf16 && (reinterpret_cast<uintptr_t>(c0.out_bf16) & 15) == 0 && c0.ld_bf16 % 8 == 0 &&
+        nlen % 64 == 0 && (nseg == 1 || c0.r_nstride >= M)) {
+      const int64_t s2 = nseg > 1 ? c0.r_nstride * c0.ld_bf16 : (int64_t)M * c0.ld_bf16;
+      if (!make_tmap_3d(&tc, c0.out_bf16, (uint64_t)nlen, (uint64_t)M, (uint64_t)nseg, (uint64_t)c0.ld_bf16,
+                        (uint64_t)s2, 64, 32, 1, err, errlen))
+        return cudaErrorInvalidValue;
+      args.c_tma = 2;
     }
   }
   cudaError_t e;
