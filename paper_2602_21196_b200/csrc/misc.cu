@@ -104,30 +104,36 @@ __global__ void cvt_kernel(const float* __restrict__ src, long long lds, __nv_bf
   }
 }
 
-// 32 tokens x 64 dims per tile through shared memory: coalesced 128-byte reads along tokens, 16-byte
-// bf16 writes along dims (RoPE pairs are adjacent dims of one token).
+// 64 tokens x 64 dims per tile through shared memory: coalesced 256-byte reads along tokens (four
+// 16-byte loads in flight per thread), 16-byte bf16 writes along dims (RoPE pairs are adjacent dims).
 __global__ void cvt_dimmajor_kernel(const float* __restrict__ src, long long lds, __nv_bfloat16* __restrict__ dst,
                                     long long ldd, long long rows, long long cols, float scale, RopeRef rope) {
-  __shared__ float tile[64][33];
-  const long long ntt = (rows + 31) / 32, nct = cols / 64;
+  __shared__ float tile[64][65];
+  const long long ntt = (rows + 63) / 64, nct = cols / 64;
   const int t = threadIdx.x;
   for (long long blk = blockIdx.x; blk < ntt * nct; blk += gridDim.x) {
-    const long long t0 = (blk / nct) * 32, c0 = (blk % nct) * 64;
+    const long long t0 = (blk / nct) * 64, c0 = (blk % nct) * 64;
     {
-      const int c = t >> 2, tk = (t & 3) * 8;       // dim c of the tile, tokens tk..tk+7
+      const int c = t >> 2, tk = (t & 3) * 16;      // dim c of the tile, tokens tk..tk+15
       const float* sp = src + (c0 + c) * lds + t0 + tk;
-      if ((lds & 3) == 0 && t0 + tk + 8 <= rows) {   // 2 x 16-byte loads (rows of 4-aligned length)
-        const float4 x = *reinterpret_cast<const float4*>(sp), y = *reinterpret_cast<const float4*>(sp + 4);
-        tile[c][tk + 0] = x.x; tile[c][tk + 1] = x.y; tile[c][tk + 2] = x.z; tile[c][tk + 3] = x.w;
-        tile[c][tk + 4] = y.x; tile[c][tk + 5] = y.y; tile[c][tk + 6] = y.z; tile[c][tk + 7] = y.w;
+      if ((lds & 3) == 0 && t0 + tk + 16 <= rows) {
+        float4 x[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = *reinterpret_cast<const float4*>(sp + 4 * k);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          tile[c][tk + 4 * k + 0] = x[k].x; tile[c][tk + 4 * k + 1] = x[k].y;
+          tile[c][tk + 4 * k + 2] = x[k].z; tile[c][tk + 4 * k + 3] = x[k].w;
+        }
       } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) tile[c][tk + i] = (t0 + tk + i < rows) ? sp[i] : 0.f;
+        for (int i = 0; i < 16; ++i) tile[c][tk + i] = (t0 + tk + i < rows) ? sp[i] : 0.f;
       }
     }
     __syncthreads();
-    {
-      const int tk = t >> 3, cg = (t & 7) * 8;      // token tk, dims cg..cg+7
+#pragma unroll
+    for (int it = t; it < 512; it += 256) {
+      const int tk = it >> 3, cg = (it & 7) * 8;    // token tk, dims cg..cg+7
       if (t0 + tk < rows) {
         float v[8];
 #pragma unroll
@@ -228,7 +234,7 @@ cudaError_t cvt_dimmajor_f32_bf16_run(const float* src, int64_t lds, void* dst, 
                                       int64_t cols, float scale, cudaStream_t s, const RopeRef& inverse_rope) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (cols % 64) return cudaErrorInvalidValue;
-  const long long tiles = ((rows + 31) / 32) * (cols / 64);
+  const long long tiles = ((rows + 63) / 64) * (cols / 64);
   const int grid = (int)(tiles < 148 * 8 ? tiles : 148 * 8);
   cvt_dimmajor_kernel<<<grid, 256, 0, s>>>(src, lds, (__nv_bfloat16*)dst, ldd, rows, cols, scale, inverse_rope);
   count_launches(1);
