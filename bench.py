@@ -188,14 +188,14 @@ def run_reference(args):
     ts = [oracle_step_time(S) for _ in range(args.steps)]
     t = sum(ts) / len(ts)
     v = S / t
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s/GPU", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "llama3-8b-attention-layer-fwd-bwd", "seq_len": S, "global_batch": 1,
                        "parallelism": "none (host cores)", "note": "bounded sample of the bench workload"},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
                              "sample": f"oracle fwd+bwd, Llama3-8B layer shape at S={S} per step"},
-            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": v, "unit": "tokens/s/GPU", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -301,7 +301,8 @@ def main():
     main_run = run(U, args.steps, args.warmup, trace=True)
     clocks = sampler.stop() if sampler else None
     ms_step = main_run["ms"] / args.steps
-    tok_s = S * args.steps / (main_run["ms"] / 1e3)
+    tok_s_total = S * args.steps / (main_run["ms"] / 1e3)    # the whole job (all C ranks share one sequence)
+    tok_s = tok_s_total / world                                # the metric: tokens/s/GPU (P:388 normalisation)
 
     # roofline of the dominant kernel (attention backward), timed live by the in-library trace events
     peaks = measured_peaks()
@@ -328,7 +329,7 @@ def main():
     per_step_ms = {k: v[0] / args.steps for k, v in tr.items()}
 
     result = {
-        "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": tok_s, "unit": "tokens/s/GPU", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded counter-based generator, drawn on device)",
         "config": {"workload": M["workload"] + (" (BASELINE configs[1])" if args.model == "llama3-8b" and S == 131072 else ""),
@@ -340,7 +341,9 @@ def main():
                    "kv_schedule": "naive (per-stage K/V resend)" if args.naive_kv else "GQA super-stage (P:362-380)",
                    "rope_base": args.rope_base,
                    "l2": f"inputs larger than L2 (x, dy: S_l x {D} bf16 per rank); no flush needed"},
-        "tokens_per_s_per_gpu": tok_s / world,
+        "tokens_per_s_total": tok_s_total,
+        "value_definition": "S / (C * max-over-ranks device time of one fwd+bwd step): tokens/s/GPU as BASELINE's "
+                            "metric names it; tokens_per_s_total = S / time",
         "gpu_launches": main_run["launches"],
         "gpu_launches_per_step": main_run["launches"] / args.steps,
         "roofline": {"kernel": "attn_bwd (tcgen05 flash attention backward)", "bound": "tensor",
@@ -373,8 +376,8 @@ def main():
     else:
         ul = None
     if ul is not None:
-        ul_tok = S * max(2, args.steps // 2) / (ul["ms"] / 1e3)
-        result["ulysses"] = {"chunk_heads": Hq, "value": ul_tok, "unit": "tokens/s",
+        ul_tok = S * max(2, args.steps // 2) / (ul["ms"] / 1e3) / world
+        result["ulysses"] = {"chunk_heads": Hq, "value": ul_tok, "unit": "tokens/s/GPU",
                              "upipe_over_ulysses": tok_s / ul_tok,
                              "peak_activation_gib": ul["peak_bytes"] / 2**30,
                              "workspace_gib": ul["ws_bytes"] / 2**30,
@@ -390,10 +393,12 @@ def main():
         # the timed region. The copies run on two copy streams (H2D, D2H) with double-buffered device
         # inputs, so step i+1's upload overlaps step i's backward and step i's download overlaps step
         # i+1's forward (the usual input pipeline of a training loop); nothing is skipped or cached.
-        attn = UPipeAttention(Hq, Hkv, d, D, U, True, process_group=pg)
+        attn = UPipeAttention(Hq, Hkv, d, D, U, True, process_group=pg, naive_kv=args.naive_kv,
+                              rope_base=args.rope_base, ring_degree=args.ring)
         xh = [x.cpu().pin_memory() for _ in range(2)]
         dyh = [dy.cpu().pin_memory() for _ in range(2)]
         dxh = [torch.empty_like(xh[0]).pin_memory() for _ in range(2)]
+        yh = [torch.empty_like(xh[0]).pin_memory() for _ in range(2)]
         xd = [torch.empty_like(x) for _ in range(2)]
         dyd = [torch.empty_like(dy) for _ in range(2)]
         main_s = torch.cuda.current_stream()
@@ -421,7 +426,9 @@ def main():
             with torch.cuda.stream(d2h):
                 d2h.wait_event(bwd_done[b])
                 dx.record_stream(d2h)
+                y.record_stream(d2h)
                 dxh[b].copy_(dx, non_blocking=True)
+                yh[b].copy_(y, non_blocking=True)
 
         e2e_step(0)
         e2e_step(1)
@@ -437,11 +444,12 @@ def main():
         e1.record(main_s)
         torch.cuda.synchronize()
         ms = max_over_ranks(e0.elapsed_time(e1))
-        result["e2e"] = {"value": S * ksteps / (ms / 1e3), "unit": "tokens/s",
-                         "h2d_bytes_per_step": 2 * x.numel() * 2, "d2h_bytes_per_step": x.numel() * 2,
+        result["e2e"] = {"value": S * ksteps / (ms / 1e3) / world, "unit": "tokens/s/GPU",
+                         "h2d_bytes_per_step": 2 * x.numel() * 2, "d2h_bytes_per_step": 2 * x.numel() * 2,
                          "steps": ksteps, "api": "paper_2602_21196_b200.UPipeAttention.forward/backward",
-                         "copies": "pinned host x, dY -> HBM and dx -> pinned host every step, on H2D/D2H copy "
-                                   "streams overlapping the neighbouring steps' compute (double-buffered inputs)"}
+                         "copies": "pinned host x, dY -> HBM and y, dx -> pinned host every step, on H2D/D2H copy "
+                                   "streams overlapping the neighbouring steps' compute (double-buffered inputs); "
+                                   "dW stays in HBM for the optimizer (per rank, bytes counted per rank)"}
         attn.close()
 
     if rank == 0 and world == 1 and not args.quick and not args.no_cpu_baseline:

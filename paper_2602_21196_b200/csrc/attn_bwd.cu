@@ -969,11 +969,9 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
                                  errlen)) {
       return cudaErrorInvalidValue;
     }
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(attn_bwd_q64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q64Cfg::SMEM);
+    const cudaError_t attr = set_smem_attr((const void*)attn_bwd_q64_kernel<false>, Q64Cfg::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd_q64 attr: %s", cudaGetErrorString(attr)); return attr; }
-    static const cudaError_t attr2 =
-        cudaFuncSetAttribute(attn_bwd_q64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Q64Cfg::SMEM);
+    const cudaError_t attr2 = set_smem_attr((const void*)attn_bwd_q64_kernel<true>, Q64Cfg::SMEM);
     if (attr2 != cudaSuccess) { snprintf(err, errlen, "attn_bwd_q64 attr: %s", cudaGetErrorString(attr2)); return attr2; }
     if (a.dbg) attn_bwd_q64_kernel<true><<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
     else attn_bwd_q64_kernel<false><<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
@@ -993,18 +991,15 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
     return e;
   }
   if (p.d == 128) {
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(attn_bwd_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<128>::SMEM);
+    const cudaError_t attr = set_smem_attr((const void*)attn_bwd_kernel<128, false>, BwdCfg<128>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
-    static const cudaError_t attr2 =
-        cudaFuncSetAttribute(attn_bwd_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<128>::SMEM);
+    const cudaError_t attr2 = set_smem_attr((const void*)attn_bwd_kernel<128, true>, BwdCfg<128>::SMEM);
     if (attr2 != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr2)); return attr2; }
     if (a.dbg) attn_bwd_kernel<128, true><<<grid, kThreads, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
     else attn_bwd_kernel<128, false><<<grid, kThreads, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
     count_launches(1);
   } else {
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(attn_bwd_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdCfg<64>::SMEM);
+    const cudaError_t attr = set_smem_attr((const void*)attn_bwd_kernel<64, false>, BwdCfg<64>::SMEM);
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
     attn_bwd_kernel<64, false><<<grid, kThreads, BwdCfg<64>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
     count_launches(1);

@@ -485,14 +485,11 @@ cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorM
                    cudaStream_t s) {
   using C = Cfg<BN, PAIR>;
   auto kern = gemm_kernel<BN, A_MN, B_MN, CL, PAIR>;
-  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  const cudaError_t attr = set_smem_attr((const void*)kern, C::SMEM);
   if (attr != cudaSuccess) return attr;
-  static const int num_sms = [] {
-    int dev = 0, n = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
-  }();
+  int dev = 0, num_sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   const int ntn = (args.N + BN - 1) / BN, ntm = (args.M + BM - 1) / BM;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
@@ -511,14 +508,28 @@ cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorM
   }
   // persistent grid: no more clusters than can be co-resident (clusters must fit inside a GPC, so
   // this can be below num_sms / CL; a second partial wave would double the tail)
-  static const int max_clusters = [&] {
-    if (CL == 1) return num_sms;
-    int n = 0;
-    cudaLaunchConfig_t q = cfg;
-    q.gridDim = dim3(CL * (num_sms / CL));
-    if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n <= 0) n = num_sms / CL;
-    return n;
-  }();
+  // cached per (kernel, device): occupancy is a property of the device the launch goes to
+  static std::mutex mc_mu;
+  static std::map<int, int> mc_by_dev;
+  int max_clusters = 0;
+  {
+    std::lock_guard<std::mutex> lk(mc_mu);
+    auto it = mc_by_dev.find(dev);
+    if (it != mc_by_dev.end()) {
+      max_clusters = it->second;
+    } else {
+      if (CL == 1) {
+        max_clusters = num_sms;
+      } else {
+        int n = 0;
+        cudaLaunchConfig_t q = cfg;
+        q.gridDim = dim3(CL * (num_sms / CL));
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n <= 0) n = num_sms / CL;
+        max_clusters = n;
+      }
+      mc_by_dev[dev] = max_clusters;
+    }
+  }
   const int clusters = units < max_clusters ? units : max_clusters;
   cfg.gridDim = dim3(CL * clusters);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], *tc, args);

@@ -264,7 +264,6 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     float* const lse_acc = a.lse;
     a.o32 = (float*)(ws + W.oacc);
     a.ldo32 = qseg;
-    R.run(UPIPE_TRACE_ATTN_FWD, q, "attn fwd (ring own block)", [&](char* e) { return attn_fwd_run(a, q, e, 512); });
     const int r = P.ring;
     const int nxt = ((ring_i + 1) % r) * C + me, prv = ((ring_i + r - 1) % r) * C + me;
     const size_t kvbytes = (size_t)P.S * kseg * 2;
@@ -282,11 +281,12 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       R.comm(cs, "ring V", [&](std::string& m) { return T.sendrecv(vs, nxt, vn, prv, kvbytes, cs, m); });
       cudaEventRecord(rev[1 + (t & 1)], cs);
     };
-    if (r > 1) {
+    if (r > 1) {                                        // the first hop overlaps the own-block attention
       cudaEventRecord(rev[0], q);                       // own K/V block (and the stage's a2a) complete
       cudaStreamWaitEvent(cs, rev[0], 0);
-      ring_step(1, a.k, a.v);
+      ring_step(1, a.k, a.v);                           // K/V are read-only for the attention below
     }
+    R.run(UPIPE_TRACE_ATTN_FWD, q, "attn fwd (ring own block)", [&](char* e) { return attn_fwd_run(a, q, e, 512); });
     for (int t = 1; t < r && R.status == UPIPE_OK; ++t) {
       char* kn = ws + W.kring[t & 1];
       char* vn = ws + W.vring[t & 1];

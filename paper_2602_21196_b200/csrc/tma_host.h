@@ -5,8 +5,27 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace upipe {
+
+// Kernel attributes (max dynamic shared memory) belong to the current device's context, so they are
+// set once per (kernel, device), not once per process: a process that drives several GPUs must raise
+// the limit on each of them.
+inline cudaError_t set_smem_attr(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, cudaError_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = done.find({kern, dev});
+  if (it != done.end()) return it->second;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done[{kern, dev}] = e;
+  return e;
+}
 
 using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,

@@ -136,7 +136,9 @@ struct Pipe {
 }  // namespace upipe
 
 namespace upipe {
-// The ring hybrid runs the sequential schedule (its ring steps are issued on the compute stream).
+// Overlapped UPipe schedule (double-buffered chunk set, next stage's all-to-all on the comm stream).
+// The ring hybrid runs its Ulysses all-to-alls sequentially on the compute stream; its ring transfers
+// are issued on the ctx's comm stream one step ahead of the attention (layer.cpp).
 inline bool overlap_enabled(uint32_t flags, const Plan& P) {
   return P.C > 1 && P.ring == 1 && !(flags & UPIPE_FLAG_SYNC_COMM);
 }

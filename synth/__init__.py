@@ -6,7 +6,7 @@ so that both sides can draw the same inputs:
 
 * the oracle and the tests call :func:`draw` (numpy, host);
 * the CUDA path has its own implementation of the same counter-based generator
-  (``paper_2602_21196_b200/csrc/synth.cu``, exported as ``upipe_synth_fill_bf16``),
+  (``paper_2602_21196_b200/csrc/misc.cu:synth_kernel``, exported as ``upipe_synth_fill_bf16``),
   used by ``bench.py`` to create large inputs directly in HBM.
 
 Generator (DESIGN.md "Input recipe"):
