@@ -102,6 +102,9 @@ typedef struct {
 #define UPIPE_FLAG_SYNC_COMM 1u /* sequential schedule: collectives on the compute stream, one buffer set */
 #define UPIPE_FLAG_NAIVE_KV 2u  /* ablation: re-project and re-send the stage's K/V heads at every
                                    stage instead of once per GQA super-stage ("naive" volume) */
+#define UPIPE_FLAG_DETERMINISTIC 4u /* bitwise-reproducible backward: the attention backward
+                                   adds the dQ partials of its key tiles in key-tile order (semaphores in
+                                   the workspace) instead of in arrival order; slower */
 
 /* ---------------------------------------------------------------- lifecycle */
 
@@ -186,14 +189,25 @@ UPIPE_API upipe_status_t upipe_attn_bwd(upipe_ctx_t ctx, const upipe_shape_t* sh
 UPIPE_API upipe_status_t upipe_attn_core_fwd(const upipe_bf16* q, const upipe_bf16* k, const upipe_bf16* v, upipe_bf16* o,
                                    float* lse, int64_t S, int nq, int nkv, int d, int causal, int64_t ldq,
                                    int64_t ldkv, int64_t ldo, int64_t ld_lse, void* stream);
-/* Attention core backward (B4): dq_acc fp32 [S][nq][d] is ACCUMULATED into (zero it first);
- * dk_acc/dv_acc fp32 [S][nkv][d] are written (accumulate != 0: added to their contents);
- * delta [S][nq] (stride ld_delta) = rowsum(dO*O) in fp32. */
+/* Attention core backward (B4): dq_acc fp32 is ACCUMULATED into (zero it first) with dQ = (1/sqrt(d)) dS K;
+ * layout [S][nq][d] (token-major), or with UPIPE_CORE_DQ_DIM_MAJOR [nq*d][S]
+ * (dims-major, row stride S: the layer's layout for the 64-query kernel at d = 128);
+ * dk_acc/dv_acc fp32 [S][nkv][d] are written (UPIPE_CORE_ACCUMULATE: added to their contents);
+ * delta [S][nq] (stride ld_delta) = rowsum(dO*O) in fp32.
+ * flags: UPIPE_CORE_ACCUMULATE | UPIPE_CORE_DQ_DIM_MAJOR (d = 128 only) | UPIPE_CORE_DETERMINISTIC
+ * (dQ partials of the key tiles are added in key-tile order, so results are bitwise reproducible;
+ * needs dq_sem: >= upipe_core_bwd_sem_count(S, nq) int32 of device memory, zeroed before the call;
+ * may be NULL otherwise). */
+#define UPIPE_CORE_ACCUMULATE 1
+#define UPIPE_CORE_DQ_DIM_MAJOR 2
+#define UPIPE_CORE_DETERMINISTIC 4
 UPIPE_API upipe_status_t upipe_attn_core_bwd(const upipe_bf16* q, const upipe_bf16* k, const upipe_bf16* v,
                                    const upipe_bf16* dout, const float* lse, const float* delta, float* dq_acc,
                                    float* dk_acc, float* dv_acc, int64_t S, int nq, int nkv, int d, int causal,
                                    int64_t ldq, int64_t ldkv, int64_t ldo_grad, int64_t ld_lse, int64_t ld_delta,
-                                   int accumulate, void* stream);
+                                   int flags, int32_t* dq_sem, void* stream);
+/* Number of int32 semaphores the deterministic backward needs for (S, nq). */
+UPIPE_API int64_t upipe_core_bwd_sem_count(int64_t S, int nq);
 /* delta[t*ld_delta + j] = sum_e dO[t*ld_do + j*d + e] * O[t*ld_o + j*d + e] */
 UPIPE_API upipe_status_t upipe_rowdot(const upipe_bf16* dO, int64_t ld_do, const upipe_bf16* O, int64_t ld_o, float* delta,
                             int64_t ld_delta, int64_t rows, int nheads, int d, void* stream);
@@ -205,6 +219,34 @@ UPIPE_API upipe_status_t upipe_gemm_xwT(const upipe_bf16* x, const upipe_bf16* w
  * dst[i] = (2*m-255)/256 * 2^exponent, m = splitmix64(seed*G1 + tensor_id*G2 + start + i) >> 56. */
 UPIPE_API upipe_status_t upipe_synth_fill_bf16(upipe_bf16* dst, int64_t n, uint64_t seed, int tensor_id, int exponent,
                                      int64_t start, void* stream);
+
+/* ---------------------------------------------------------------- test-only layout probes
+ * Not part of the public API (SURVEY §8b "test-only"). They make the integer permutations of the
+ * hot path observable through the REAL layer code (projection epilogue -> transport -> receive
+ * buffers, attention-output injection -> out all-to-all -> unpack into o_saved) so tests can check
+ * them bit-exactly against the oracle's maps (§3.1 layout; SPEC S:150-152 round trip).
+ * While a probe is set on a ctx, every upipe_attn_fwd / upipe_attn_bwd call of that ctx:
+ *   - after the stage's inp all-to-all, copies the receive buffers of stage `stage` into the non-null
+ *     outputs (q_recv [S][qpd*d], k_recv / v_recv [S][kv_res*d] when the stage sends K/V; in backward
+ *     also do_recv [S][qpd*d] bf16 and delta_recv [S][qpd] fp32), S = tokens of the Ulysses group;
+ *   - forward, o_head != NULL: SKIPS the stage's attention and uses o_head [S][qpd*d] (head layout,
+ *     this device's heads) as its output, which then goes through the out all-to-all and the unpack
+ *     into o_saved (lse of that stage is not written);
+ *   - backward, dq_head != NULL: SKIPS the stage's attention backward and dQ conversion and sends
+ *     dq_head [S][qpd*d] (and dk_head / dv_head [S][kv_res*d] at the stage that retires its K/V heads)
+ *     head -> seq; dq_recv [C][S_l][qpd*d] (dk_recv / dv_recv [C][S_l][kv_res*d]) receive copies.
+ * All pointers are device pointers owned by the caller; stage = -1 turns the probe off. The copies
+ * are enqueued on the stream the probed step runs on; they are complete when the call's stream is. */
+typedef struct {
+  int32_t stage;
+  upipe_bf16 *q_recv, *k_recv, *v_recv;
+  const upipe_bf16* o_head;
+  upipe_bf16* do_recv;
+  float* delta_recv;
+  const upipe_bf16 *dq_head, *dk_head, *dv_head;
+  upipe_bf16 *dq_recv, *dk_recv, *dv_recv;
+} upipe_probe_t;
+UPIPE_API upipe_status_t upipe_test_set_probe(upipe_ctx_t ctx, const upipe_probe_t* probe);
 
 /* ---------------------------------------------------------------- instrumentation */
 

@@ -188,9 +188,9 @@ def rope(T, positions, base, inverse=False):
 
 def _qkv(X, Wq, Wk, Wv, Hq, Hkv, d, rope_base, pos0=0):
     S = X.shape[0]
-    Q = (X @ Wq.T).reshape(S, Hq, d)
-    K = (X @ Wk.T).reshape(S, Hkv, d)
-    V = (X @ Wv.T).reshape(S, Hkv, d)
+    Q = project(X, Wq).reshape(S, Hq, d)
+    K = project(X, Wk).reshape(S, Hkv, d)
+    V = project(X, Wv).reshape(S, Hkv, d)
     if rope_base:
         pos = np.arange(pos0, pos0 + S)
         Q, K = rope(Q, pos, rope_base), rope(K, pos, rope_base)
@@ -204,7 +204,7 @@ def layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, causal=True, rope_base=None):
     Q, K, V = _qkv(X, Wq, Wk, Wv, Hq, Hkv, d, rope_base)
     O, lse = attn_fwd(Q, K, V, causal)
     O2 = O.reshape(S, Hq * d)
-    return O2 @ Wo.T, O2, lse
+    return project(O2, Wo), O2, lse
 
 
 def layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, causal=True, rope_base=None):
@@ -234,12 +234,12 @@ def layer_fwd_rows(X_rows, rows, K, V, Wq, Wo, Hq, Hkv, d, causal=True, rope_bas
     ``X_rows`` are those rows of X; ``K``, ``V`` = X Wk^T, X Wv^T for all tokens ([S, Hkv, d]).
     Each row is computed exactly as in ``layer_fwd`` (rows of attention are independent).
     """
-    Qr = (X_rows @ Wq.T).reshape(len(rows), Hq, d)
+    Qr = project(X_rows, Wq).reshape(len(rows), Hq, d)
     if rope_base:                        # K is passed already rotated (rope(X Wk^T, arange(S)))
         Qr = rope(Qr, rows, rope_base)
     O, lse = attn_fwd(Qr, K, V, causal, rows=rows)
     O2 = O.reshape(len(rows), Hq * d)
-    return O2 @ Wo.T, O2, lse
+    return project(O2, Wo), O2, lse
 
 
 def layer_bwd_tail(X_tail, dY_tail, K, V, Wq, Wk, Wv, Wo, Hq, Hkv, d, rope_base=None):
@@ -252,7 +252,7 @@ def layer_bwd_tail(X_tail, dY_tail, K, V, Wq, Wk, Wv, Wo, Hq, Hkv, d, rope_base=
     t0 = S - w
     R = Hq // Hkv
     scale = 1.0 / math.sqrt(d)
-    Qt = (X_tail @ Wq.T).reshape(w, Hq, d)
+    Qt = project(X_tail, Wq).reshape(w, Hq, d)
     if rope_base:                        # K is passed already rotated; Q of the tail rotated here
         Qt = rope(Qt, np.arange(t0, S), rope_base)
     dOt = (dY_tail @ Wo).reshape(w, Hq, d)
@@ -434,13 +434,13 @@ def upipe_forward(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, C, U, causal=True, schedule=Non
     lse_all = np.zeros((Hq, S))
     kv_res = [None] * C                                      # resident K/V per device
     for st in stages:
-        qsh = [{h: Xs[r] @ Wq[h * d:(h + 1) * d].T for h in st.heads} for r in range(C)]
+        qsh = [{h: project(Xs[r], Wq[h * d:(h + 1) * d]) for h in st.heads} for r in range(C)]
         Qh = a2a_seq_to_head(qsh, st.q_heads)
         if any(st.kv_sent[p] for p in range(C)):
             kv_heads = [st.kv_heads[p] for p in range(C)]
             all_kv = sorted({g for p in range(C) for g in kv_heads[p]})
-            ksh = [{g: Xs[r] @ Wk[g * d:(g + 1) * d].T for g in all_kv} for r in range(C)]
-            vsh = [{g: Xs[r] @ Wv[g * d:(g + 1) * d].T for g in all_kv} for r in range(C)]
+            ksh = [{g: project(Xs[r], Wk[g * d:(g + 1) * d]) for g in all_kv} for r in range(C)]
+            vsh = [{g: project(Xs[r], Wv[g * d:(g + 1) * d]) for g in all_kv} for r in range(C)]
             Kh = a2a_seq_to_head(ksh, kv_heads)
             Vh = a2a_seq_to_head(vsh, kv_heads)
             kv_res = [(kv_heads[p], Kh[p], Vh[p]) for p in range(C)]
@@ -456,7 +456,7 @@ def upipe_forward(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, C, U, causal=True, schedule=Non
         for r in range(C):
             for h in st.heads:
                 O_buf[r][:, h * d:(h + 1) * d] = Os[r][h]
-                Y_acc[r] += Os[r][h] @ Wo[:, h * d:(h + 1) * d].T
+                Y_acc[r] += project(Os[r][h], Wo[:, h * d:(h + 1) * d])
     return np.concatenate(Y_acc, 0), np.concatenate(O_buf, 0), lse_all
 
 
@@ -497,13 +497,13 @@ def upipe_backward(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, C, U, causal=True, schedul
                 retire(kv_state)
             kv_heads = [st.kv_heads[p] for p in range(C)]
             all_kv = sorted({g for p in range(C) for g in kv_heads[p]})
-            ksh = [{g: Xs[r] @ Wk[g * d:(g + 1) * d].T for g in all_kv} for r in range(C)]
-            vsh = [{g: Xs[r] @ Wv[g * d:(g + 1) * d].T for g in all_kv} for r in range(C)]
+            ksh = [{g: project(Xs[r], Wk[g * d:(g + 1) * d]) for g in all_kv} for r in range(C)]
+            vsh = [{g: project(Xs[r], Wv[g * d:(g + 1) * d]) for g in all_kv} for r in range(C)]
             Kh = a2a_seq_to_head(ksh, kv_heads)
             Vh = a2a_seq_to_head(vsh, kv_heads)
             kv_state = [(kv_heads[p], Kh[p], Vh[p], np.zeros_like(Kh[p]), np.zeros_like(Vh[p]))
                         for p in range(C)]
-        qsh = [{h: Xs[r] @ Wq[h * d:(h + 1) * d].T for h in st.heads} for r in range(C)]
+        qsh = [{h: project(Xs[r], Wq[h * d:(h + 1) * d]) for h in st.heads} for r in range(C)]
         dosh = [{h: dYs[r] @ Wo[:, h * d:(h + 1) * d] for h in st.heads} for r in range(C)]
         Qh = a2a_seq_to_head(qsh, st.q_heads)
         dOh = a2a_seq_to_head(dosh, st.q_heads)

@@ -53,6 +53,10 @@ struct BwdArgs {
   float scale_log2;  // log2(e)/sqrt(d)
   RopeRef rope;      // dK (bf16 output) rotated back by -angle(key) when set (RoPE on K, DESIGN A26)
   int dq_dim_major;  // q64 kernel: dq_acc is [nq*d][S] (TMA boxes of 32 dims x 32 tokens)
+  int* dq_sem;       // deterministic dQ (UPIPE_FLAG_DETERMINISTIC): per (head, query tile, box group) the
+                     // number of key tiles that have added their partial; key tile jb adds when it reads jb
+  int head_inner;    // visiting order (head, query tile): 1 = heads inner, so every CTA of the launch is at
+                     // the same query tile at the same step (needed by dq_sem, whose waits then chain in lockstep)
   long long* dbg;    // optional per-role cycle breakdown of CTA (0,0) (UPIPE_BWD_TIMELINE=1)
 };
 
@@ -127,6 +131,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_qt = nT - qt_begin;
   const int N = G * n_qt;                         // (head, query tile) iterations
   constexpr int kSoftmax = kSoftmaxWarps * 32;
+  // visiting order: heads outer, query tiles up from the diagonal (default), or heads inner and query
+  // tiles down to the diagonal (a.head_inner: all CTAs of the launch in lockstep, for dq_sem)
+  auto tile_h = [&](int n) { return g * G + (a.head_inner ? n % G : n / n_qt); };
+  auto tile_qt = [&](int n) { return a.head_inner ? nT - 1 - n / G : qt_begin + n % n_qt; };
 
   if (warp == kTmaWarp && lane == 0) {
     tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
@@ -151,8 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(smem + C::OFF_V + c * 16384, &tmV, kv_full, c * 64, g, jb * 128);
       }
       for (int n = 0; n < N; ++n) {
-        const int h = g * G + n / n_qt;
-        const int qt = qt_begin + n % n_qt;
+        const int h = tile_h(n);
+        const int qt = tile_qt(n);
         const int b = n & 1;
         mbar_wait(&q_empty[b], ((n >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&q_full[b], C::TB);
@@ -267,15 +275,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t dsbase = smem_u32(smem + C::OFF_DS) + wg * 16384;   // dS^T chunk of this warpgroup's 64 queries
     float stat_next = 0.f;                            // warpgroup 0 prefetches lse, warpgroup 1 delta, one tile ahead
     auto load_stat = [&](int n) -> float {
-      const int h = g * G + n / n_qt;
-      const long long q = (long long)(qt_begin + n % n_qt) * 128 + r;
+      const int h = tile_h(n);
+      const long long q = (long long)tile_qt(n) * 128 + r;
       if (q >= a.S) return 0.f;
       return wg == 0 ? a.lse[(long long)h * a.ld_lse + q] * -1.4426950408889634f : a.delta[q * a.ld_delta + h];
     };
     if (N > 0) stat_next = load_stat(0);
     long long tl[4] = {0, 0, 0, 0}, te[4] = {0, 0, 0, 0};   // te: E split into ld / math / store / wait_st
     for (int n = 0; n < N; ++n) {
-      const int qt = qt_begin + n % n_qt;
+      const int qt = tile_qt(n);
       const long long q0 = (long long)qt * 128;
       const int sb = n & 1;
       if (wg == 0) s_lse2[sb][r] = stat_next;
@@ -440,9 +448,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const bool issuer = quad == 0 && lane == 0;
     long long tl[2] = {0, 0};
+    int* sem_prev = nullptr;                          // deterministic dQ (see the q64 kernel's drain)
     for (int n = 0; n < N; ++n) {
-      const int h = g * G + n / n_qt;
-      const int q0 = (qt_begin + n % n_qt) * 128;
+      const int h = tile_h(n);
+      const int q0 = tile_qt(n) * 128;
+      int* const sem = a.dq_sem ? a.dq_sem + (long long)h * nT + q0 / 128 : nullptr;
       long long c0 = tick<TL>();
       if (quad == 0) mbar_wait(dq_full, n & 1);   // one polling warp, the others wait in bar.sync
       named_bar_sync(2, 128);
@@ -470,14 +480,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         named_bar_sync(2, 128);
         if (issuer) {
+          if (b == 0 && sem) sem_wait_eq(sem, jb);
           tma_reduce_add_2d(&tmdQ, slot, h * D + b * 32, q0);
           bulk_commit();
+          if (b == C::DQ_BOXES - 1) {
+            if (sem_prev) {                             // the previous tile's boxes have completed
+              bulk_wait_n<C::DQ_BOXES>();
+              fence_proxy_async_global();
+              st_release_gpu(sem_prev, jb + 1);
+            }
+            sem_prev = sem;
+          }
         }
       }
       tl[0] += c1 - c0;
       tl[1] += tick<TL>() - c1;
     }
-    if (issuer) bulk_wait0();
+    if (issuer) {
+      bulk_wait0();
+      if (sem_prev) {
+        fence_proxy_async_global();
+        st_release_gpu(sem_prev, jb + 1);
+      }
+    }
     if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && warp == kSoftmaxWarps && lane == 0) {
       a.dbg[3] = tl[0];
       a.dbg[4] = tl[1];
@@ -547,7 +572,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int N = G * n_qt;
   // Query tiles are visited from the last one down to the diagonal: CTAs that run at the same time then
   // reduce their dQ partials into the same rows of dq_acc (L2 hits) instead of each starting at its own
-  // diagonal and sweeping a different region (measured: the dQ reduce-adds dominated the energy)
+  // diagonal and sweeping a different region (measured: the dQ reduce-adds dominated the energy).
+  // Heads of the KV group outer (default) or inner (a.head_inner).
+  auto tile_h = [&](int n) { return g * G + (a.head_inner ? n % G : n / n_qt); };
+  auto tile_qt = [&](int n) { return nT64 - 1 - (a.head_inner ? n / G : n % n_qt); };
   constexpr int kWg = 128;
 
   if (warp == kTmaWarp && lane == 0) {
@@ -572,8 +600,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(smem + C::OFF_V + c * 16384, &tmV, kv_full, c * 64, g, jb * 128);
       }
       for (int n = 0; n < N; ++n) {
-        const int h = g * G + n / n_qt;
-        const int qt = nT64 - 1 - n % n_qt;
+        const int h = tile_h(n);
+        const int qt = tile_qt(n);
         const int st = n % C::NQ;
         const uint32_t ph = ((n / C::NQ) & 1) ^ 1;
         mbar_wait(&q_empty[st], ph);
@@ -683,15 +711,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tP = tmem + (x ? C::TM_DP1 : C::TM_DP0) + lane_off;
     const uint32_t dsbase = smem_u32(smem + C::OFF_DS + x * 16384);
     auto load_stat = [&](int n) -> float {            // threads 0-63: -lse*log2e of query r, 64-127: delta
-      const int h = g * G + n / n_qt;
-      const long long q = (long long)(nT64 - 1 - n % n_qt) * 64 + (r & 63);
+      const int h = tile_h(n);
+      const long long q = (long long)tile_qt(n) * 64 + (r & 63);
       if (q >= a.S) return 0.f;
       return r < 64 ? a.lse[(long long)h * a.ld_lse + q] * -1.4426950408889634f : a.delta[q * a.ld_delta + h];
     };
     float stat_next = x < N ? load_stat(x) : 0.f;
     long long te[2] = {0, 0};                         // wait S/dP, E
     for (int n = x; n < N; n += 2) {
-      const int qt = nT64 - 1 - n % n_qt;
+      const int qt = tile_qt(n);
       const long long q0 = (long long)qt * 64;
       const int par = (n >> 1) & 1;
       float* s_lse2 = stats + ((x * 2 + par) * 2 + 0) * 64;
@@ -816,10 +844,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* const box = smem + C::OFF_STG + quad * 8192;
     const uint32_t bbase = smem_u32(box);
     long long td[1] = {0};
+    int* sem_prev = nullptr;                          // deterministic dQ: released one step late (below)
     for (int n = 0; n < N; ++n) {
       const int x = n & 1;
-      const int h = g * G + n / n_qt;
-      const int q0 = (nT64 - 1 - n % n_qt) * 64;
+      const int h = tile_h(n);
+      const int q0 = tile_qt(n) * 64;
+      int* const sem = a.dq_sem ? a.dq_sem + ((long long)h * nT64 + q0 / 64) * 4 + quad : nullptr;
+      // Deterministic dQ: key tile jb adds after key tiles 0..jb-1 (every earlier key tile contributes to
+      // every query tile this CTA visits); the release of step n waits for its reduce to COMPLETE, which is
+      // done one step later (wait_group 1) so the drain never idles on its own reduce.
+      auto issue = [&](auto&& do_reduce) {
+        if (sem) sem_wait_eq(sem, jb);
+        do_reduce();
+        bulk_commit();
+        if (sem_prev) {
+          bulk_wait1();
+          fence_proxy_async_global();
+          st_release_gpu(sem_prev, jb + 1);
+        }
+        sem_prev = sem;
+      };
       const long long d0 = tick<TL>();
       if (lane == 0) mbar_wait(&dq_full[x], (n >> 1) & 1);
       __syncwarp();
@@ -847,11 +891,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                          __float_as_uint(__uint_as_float(rq[bx][4 * j + 3]) * a.scale));
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
-          tma_reduce_add_2d(&tmdQ, box, q0, h * D + quad * 32);
-          tma_reduce_add_2d(&tmdQ, box + 4096, q0 + 32, h * D + quad * 32);
-          bulk_commit();
-        }
+        if (lane == 0)
+          issue([&] {
+            tma_reduce_add_2d(&tmdQ, box, q0, h * D + quad * 32);
+            tma_reduce_add_2d(&tmdQ, box + 4096, q0 + 32, h * D + quad * 32);
+          });
         continue;
       }
       // row q (query), column lane (dim): 128B-swizzled rows of 32 fp32
@@ -861,12 +905,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                       __uint_as_float(rq[q >> 5][q & 31]) * a.scale);
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        tma_reduce_add_2d(&tmdQ, box, h * D + quad * 32, q0);
-        bulk_commit();
+      if (lane == 0) issue([&] { tma_reduce_add_2d(&tmdQ, box, h * D + quad * 32, q0); });
+    }
+    if (lane == 0) {
+      bulk_wait0();
+      if (sem_prev) {
+        fence_proxy_async_global();
+        st_release_gpu(sem_prev, jb + 1);
       }
     }
-    if (lane == 0) bulk_wait0();
     if (TL && a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && quad == 0 && lane == 0) {
       a.dbg[9] = td[0];
       a.dbg[10] = N;
@@ -940,6 +987,13 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)p.d);
   a.rope = p.rope;
   a.dq_dim_major = 0;
+  a.dq_sem = p.dq_sem;
+  // deterministic dQ needs the lockstep order; UPIPE_BWD_HEAD_INNER=1 selects it otherwise too (A/B)
+  static const bool head_inner_env = [] {
+    const char* v = getenv("UPIPE_BWD_HEAD_INNER");
+    return v && v[0] == '1';
+  }();
+  a.head_inner = (p.dq_sem || head_inner_env) ? 1 : 0;
   // UPIPE_BWD_TIMELINE=1: per-role cycle breakdown of CTA (0,0), printed to stderr after the launch
   static long long* dbg_dev = nullptr;
   const char* tlenv = getenv("UPIPE_BWD_TIMELINE");

@@ -12,6 +12,7 @@
 #include "upipe_internal.h"
 
 static_assert(sizeof(upipe_shape_t) == 40, "upipe_shape_t layout is part of the ABI (Python mirror in upipe.py)");
+static_assert(sizeof(upipe_probe_t) == 104, "upipe_probe_t layout (Python mirror in upipe.py)");
 
 namespace upipe {
 upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, const upipe_bf16* x, const upipe_bf16* wq,
@@ -233,7 +234,7 @@ upipe_status_t upipe_attn_core_bwd(const upipe_bf16* q, const upipe_bf16* k, con
                                    const upipe_bf16* dout, const float* lse, const float* delta, float* dq_acc,
                                    float* dk_acc, float* dv_acc, int64_t S, int nq, int nkv, int d, int causal,
                                    int64_t ldq, int64_t ldkv, int64_t ldo_grad, int64_t ld_lse, int64_t ld_delta,
-                                   int accumulate, void* stream) {
+                                   int flags, int32_t* dq_sem, void* stream) {
   if (!q || !k || !v || !dout || !lse || !delta || !dq_acc || !dk_acc || !dv_acc || S < 1 || nq < 1 || nkv < 1 ||
       nq % nkv)
     return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "attn_core_bwd: bad arguments");
@@ -244,11 +245,23 @@ upipe_status_t upipe_attn_core_bwd(const upipe_bf16* q, const upipe_bf16* k, con
   p.dq_acc = dq_acc; p.dk_acc = dk_acc; p.dv_acc = dv_acc;
   p.S = S; p.nq = nq; p.nkv = nkv; p.d = d; p.causal = causal;
   p.ldq = ldq; p.ldkv = ldkv; p.ldo_grad = ldo_grad; p.ld_lse = ld_lse; p.ld_delta = ld_delta; p.ld_kvb = 0;
-  p.kv_accumulate = accumulate ? 1 : 0;
+  p.kv_accumulate = (flags & UPIPE_CORE_ACCUMULATE) ? 1 : 0;
   p.kv_write_acc = 1;
+  if (flags & UPIPE_CORE_DQ_DIM_MAJOR) {
+    p.dq_dim_major = 1;
+    p.ld_dqt = S;
+    if (!attn_bwd_dq_dim_major(p))
+      return set_err(nullptr, UPIPE_ERR_UNSUPPORTED, "attn_core_bwd: dim-major dQ needs the 64-query kernel (d = 128)");
+  }
+  if (flags & UPIPE_CORE_DETERMINISTIC) {
+    if (!dq_sem) return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "attn_core_bwd: deterministic mode needs dq_sem");
+    p.dq_sem = dq_sem;
+  }
   char err[512] = {0};
   return cuda_status(attn_bwd_run(p, static_cast<cudaStream_t>(stream), err, sizeof err), "attn_bwd", err);
 }
+
+int64_t upipe_core_bwd_sem_count(int64_t S, int nq) { return S < 1 || nq < 1 ? 0 : attn_bwd_sem_count(S, nq); }
 
 upipe_status_t upipe_rowdot(const upipe_bf16* dO, int64_t ld_do, const upipe_bf16* O, int64_t ld_o, float* delta,
                             int64_t ld_delta, int64_t rows, int nheads, int d, void* stream) {
@@ -292,6 +305,13 @@ upipe_status_t upipe_synth_fill_bf16(upipe_bf16* dst, int64_t n, uint64_t seed, 
 upipe_status_t upipe_kernel_launches(uint64_t* count) {
   if (!count) return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "count == NULL");
   *count = g_launches.load();
+  return UPIPE_OK;
+}
+
+upipe_status_t upipe_test_set_probe(upipe_ctx_t ctx, const upipe_probe_t* probe) {
+  if (upipe_status_t st = check_ctx(ctx)) return st;
+  if (!probe) return set_err(ctx, UPIPE_ERR_INVALID_ARG, "probe == NULL");
+  ctx->probe = *probe;
   return UPIPE_OK;
 }
 

@@ -112,7 +112,10 @@ struct AttnBwdProblem {
   RopeRef rope;                               // dk_bf16 is rotated back by -angle(key) (RoPE on K)
   int dq_dim_major = 0;                       // 1 (only where attn_bwd_dq_dim_major() allows): dq_acc is
   int64_t ld_dqt = 0;                         //   [nq*d][S] fp32, row stride ld_dqt (tokens contiguous)
+  int* dq_sem = nullptr;                      // non-null: deterministic dQ order (attn_bwd_sem_count ints, zeroed)
 };
+// int32 semaphores the deterministic backward needs: one per (q head, 64-query tile, 32-dim box group).
+inline int64_t attn_bwd_sem_count(int64_t S, int nq) { return (int64_t)nq * ((S + 63) / 64) * 4; }
 cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err, size_t errlen);
 // Whether attn_bwd_run can accumulate dQ dim-major for this problem (the 64-query kernel, whose dQ^T
 // tile has one head dimension per TMEM lane, then stages 16-byte vectors instead of transposing).

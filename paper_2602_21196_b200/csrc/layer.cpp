@@ -179,6 +179,12 @@ upipe_status_t ensure_pipe(upipe_ctx_s* ctx) {
   return UPIPE_OK;
 }
 
+// Test-only layout probe copies (upipe_test_set_probe): no-op for a null destination.
+cudaError_t probe_copy(void* dst, const void* src, size_t bytes, cudaStream_t q) {
+  if (!dst || !src || bytes == 0) return cudaSuccess;
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, q);
+}
+
 }  // namespace
 
 // ============================================================================ forward
@@ -221,6 +227,16 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       });
     }
   };
+  const upipe_probe_t& pr = ctx->probe;   // test-only layout probe (stage -1: off)
+  auto probe_in = [&](int s, int b, cudaStream_t q) {
+    if (pr.stage != s) return;
+    R.run(UPIPE_TRACE_AUX, q, "probe recv", [&](char*) {
+      cudaError_t e = probe_copy(pr.q_recv, ws + W.qrecv[b], (size_t)P.S * qseg * 2, q);
+      if (e == cudaSuccess && P.kv_sent(s)) e = probe_copy(pr.k_recv, ws + W.krecv[kvb(s)], (size_t)P.S * kseg * 2, q);
+      if (e == cudaSuccess && P.kv_sent(s)) e = probe_copy(pr.v_recv, ws + W.vrecv[kvb(s)], (size_t)P.S * kseg * 2, q);
+      return e;
+    });
+  };
   // F2: inp_all_to_all, Q first, then K and V
   auto inp = [&](int s, int b, cudaStream_t q) {
     a2a("a2a Q", ws + W.qsend[b], ws + W.qrecv[b], qbytes, q);
@@ -229,9 +245,19 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       a2a("a2a K", ws + W.ksend, ws + W.krecv[kb], kbytes, q);
       a2a("a2a V", ws + W.vsend, ws + W.vrecv[kb], kbytes, q);
     }
+    probe_in(s, b, q);
   };
   // F3: attention over the full sequence for this device's qpd heads
   auto attn = [&](int s, int b, cudaStream_t q) {
+    if (pr.stage == s && pr.o_head) {      // test probe: the injected head-layout O replaces the attention
+      R.run(UPIPE_TRACE_AUX, q, "probe inject O", [&](char*) {
+        if (C == 1)
+          return cudaMemcpy2DAsync(o_saved + (int64_t)P.q0(s, me) * d, HqD * 2, pr.o_head, qseg * 2, qseg * 2, P.S,
+                                   cudaMemcpyDeviceToDevice, q);
+        return probe_copy(ws + W.osend[b], pr.o_head, (size_t)P.S * qseg * 2, q);
+      });
+      return;
+    }
     AttnFwdProblem a{};
     a.q = ws + W.qrecv[b];
     a.k = ws + W.krecv[kvb(s)];
@@ -349,6 +375,7 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     for (int s = 0; s < nu && R.status == UPIPE_OK; ++s) {
       proj(s, 0, st);
       if (C > 1) inp(s, 0, st);
+      else probe_in(s, 0, st);
       attn(s, 0, st);
       if (C > 1) outa(s, 0, st);
       post(s, 0, st);
@@ -523,6 +550,27 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
                           P.qpd, P.S_l, P.qpd, d, q);
       });
   };
+  const upipe_probe_t& pr = ctx->probe;   // test-only layout probe (stage -1: off)
+  auto probe_in = [&](int s, int b, cudaStream_t q) {
+    if (pr.stage != s) return;
+    R.run(UPIPE_TRACE_AUX, q, "probe recv", [&](char*) {
+      cudaError_t e = probe_copy(pr.q_recv, ws + W.qrecv[b], (size_t)P.S * qseg * 2, q);
+      if (e == cudaSuccess && P.kv_sent(s)) e = probe_copy(pr.k_recv, ws + W.krecv[kvb(s)], (size_t)P.S * kseg * 2, q);
+      if (e == cudaSuccess && P.kv_sent(s)) e = probe_copy(pr.v_recv, ws + W.vrecv[kvb(s)], (size_t)P.S * kseg * 2, q);
+      if (e == cudaSuccess) e = probe_copy(pr.do_recv, ws + W.dorecv[b], (size_t)P.S * qseg * 2, q);
+      if (e == cudaSuccess) e = probe_copy(pr.delta_recv, ws + W.drecv[b], (size_t)P.S * P.qpd * 4, q);
+      return e;
+    });
+  };
+  auto probe_out = [&](int s, int b, cudaStream_t q) {
+    if (pr.stage != s) return;
+    R.run(UPIPE_TRACE_AUX, q, "probe send back", [&](char*) {
+      cudaError_t e = probe_copy(pr.dq_recv, ws + W.dqrecv[b], (size_t)P.S * qseg * 2, q);
+      if (e == cudaSuccess && P.kv_last(s)) e = probe_copy(pr.dk_recv, ws + W.dkrecv, (size_t)P.S * kseg * 2, q);
+      if (e == cudaSuccess && P.kv_last(s)) e = probe_copy(pr.dv_recv, ws + W.dvrecv, (size_t)P.S * kseg * 2, q);
+      return e;
+    });
+  };
   // B1/B3: Q (+K, V) and dO + delta seq -> head ("during out_all_to_all", Table 4)
   auto inp = [&](int s, int b, cudaStream_t q) {
     a2a("a2a Q", ws + W.qsend[b], ws + W.qrecv[b], qbytes, q);
@@ -533,9 +581,19 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     }
     a2a("a2a dO", ws + W.dosend[b], ws + W.dorecv[b], qbytes, q);
     a2a("a2a delta", ws + W.dsend[b], ws + W.drecv[b], dbytes, q);
+    probe_in(s, b, q);
   };
   // B4: attention backward (dK/dV accumulate over the sigma stages sharing the resident K/V), dQ -> bf16
   auto attn = [&](int s, int b, cudaStream_t q) {
+    if (pr.stage == s && pr.dq_head) {     // test probe: injected head-layout dQ (dK, dV) replace the kernel's
+      R.run(UPIPE_TRACE_AUX, q, "probe inject dQ", [&](char*) {
+        cudaError_t e = probe_copy(ws + W.dqsend[b], pr.dq_head, (size_t)P.S * qseg * 2, q);
+        if (e == cudaSuccess && P.kv_last(s)) e = probe_copy(ws + W.dksend, pr.dk_head, (size_t)P.S * kseg * 2, q);
+        if (e == cudaSuccess && P.kv_last(s)) e = probe_copy(ws + W.dvsend, pr.dv_head, (size_t)P.S * kseg * 2, q);
+        return e;
+      });
+      return;
+    }
     R.run(UPIPE_TRACE_AUX, q, "memset dQ", [&](char*) {
       return cudaMemsetAsync(ws + W.dqacc[b], 0, (size_t)P.S * qseg * 4, q);
     });
@@ -569,8 +627,18 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     bp.rope = rope_head;
     bp.dq_dim_major = attn_bwd_dq_dim_major(bp) ? 1 : 0;   // [qpd*d][S] accumulator (64-query kernel)
     bp.ld_dqt = P.S;
+    // UPIPE_FLAG_DETERMINISTIC: dQ partials added in key-tile order; fresh semaphores per launch
+    const bool det = (ctx->flags & UPIPE_FLAG_DETERMINISTIC) != 0;
+    bp.dq_sem = det ? (int*)(ws + W.dqsem) : nullptr;
+    auto bwd_launch = [&](const AttnBwdProblem& pb, const char* what) {
+      if (det)
+        R.run(UPIPE_TRACE_AUX, q, "memset dQ semaphores", [&](char*) {
+          return cudaMemsetAsync(ws + W.dqsem, 0, (size_t)attn_bwd_sem_count(P.S, P.qpd) * 4, q);
+        });
+      R.run(UPIPE_TRACE_ATTN_BWD, q, what, [&](char* e) { return attn_bwd_run(pb, q, e, 512); });
+    };
     if (P.ring == 1) {
-      R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd", [&](char* e) { return attn_bwd_run(bp, q, e, 512); });
+      bwd_launch(bp, "attn bwd");
     } else {
       // Ring hybrid (DESIGN A27): the super-stage's fp32 dK/dV accumulators travel with their K/V block;
       // each rank adds the contributions of its queries (final lse and delta), dQ accumulates locally
@@ -591,7 +659,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       cudaStreamWaitEvent(cs, rev[0], 0);
       R.comm(cs, "ring K", [&](std::string& m) { return T.sendrecv(bp.k, nxt, ws + W.kring[1], prv, kvbytes, cs, m); });
       R.comm(cs, "ring V", [&](std::string& m) { return T.sendrecv(bp.v, nxt, ws + W.vring[1], prv, kvbytes, cs, m); });
-      R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd (ring own block)", [&](char* e) { return attn_bwd_run(bp, q, e, 512); });
+      bwd_launch(bp, "attn bwd (ring own block)");
       cudaEventRecord(rev[3], q);                       // step 0 computed (rev[3 + (t & 1)] for step t)
       for (int t = 1; t <= rr && R.status == UPIPE_OK; ++t) {
         const bool home = t == rr;                      // last hop: the accumulators return to their owner
@@ -624,7 +692,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
           b2.dv_acc = dvn;
           b2.causal = 0;
           b2.kv_accumulate = 1;
-          R.run(UPIPE_TRACE_ATTN_BWD, q, "attn bwd (ring block)", [&](char* e) { return attn_bwd_run(b2, q, e, 512); });
+          bwd_launch(b2, "attn bwd (ring block)");
         }
         cudaEventRecord(rev[3 + (t & 1)], q);
       }
@@ -654,6 +722,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       a2a("a2a dK", ws + W.dksend, ws + W.dkrecv, kbytes, q);
       a2a("a2a dV", ws + W.dvsend, ws + W.dvrecv, kbytes, q);
     }
+    probe_out(s, b, q);
   };
   // B6: dX and dW for the stage's heads (and the retired K/V heads). dX += dQ Wq + dK Wk + dV Wv is
   // one K-concatenated GEMM (one fp32 read-modify-write of the dX accumulator per stage) and
@@ -693,8 +762,10 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     for (int s = 0; s < nu && R.status == UPIPE_OK; ++s) {
       pre(s, 0, st);
       if (C > 1) inp(s, 0, st);
+      else probe_in(s, 0, st);
       attn(s, 0, st);
       if (C > 1) outa(s, 0, st);
+      else probe_out(s, 0, st);
       post(s, 0, st);
     }
   } else {

@@ -1,6 +1,7 @@
 // Shape validation, GQA stage plan and workspace layout (§8b preconditions).
 #include <cstdio>
 
+#include "kernels.h"
 #include "upipe_internal.h"
 
 namespace upipe {
@@ -155,6 +156,7 @@ BwdWs bwd_workspace(const Plan& p, bool overlap) {
   w.dkrecv = comm ? take(ke) : w.dksend;
   w.dvrecv = comm ? take(ke) : w.dvsend;
   w.dxacc = p.nstages > 1 ? take((size_t)p.S_l * p.D * 4) : 0;   // one stage: dX is stored in bf16 directly
+  w.dqsem = take((size_t)attn_bwd_sem_count(p.S, p.qpd) * 4);     // deterministic mode (a few hundred KB)
   w.total = off;
   return w;
 }

@@ -130,6 +130,28 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait1() { asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_n() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
+// Global-memory semaphores that order async-proxy (TMA) reductions of different CTAs
+// (deterministic dQ): the producer completes its bulk group, fences the proxies and releases;
+// the consumer acquires, fences, then issues its own bulk reduction.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Spin until *p == v (one thread), then order the async proxy after the acquire.
+__device__ __forceinline__ void sem_wait_eq(const int* p, int v) {
+  while (ld_acquire_gpu(p) != v) __nanosleep(64);
+  fence_proxy_async_global();
+}
 
 // ------------------------------------------------------------------ tcgen05
 template <uint32_t kCols>

@@ -54,6 +54,7 @@ struct FwdWs {
 struct BwdWs {
   size_t qsend[2], qrecv[2], ksend, krecv[2], vsend, vrecv[2], dosend[2], dorecv[2], dsend[2], drecv[2], dqacc[2],
       dqsend[2], dqrecv[2], dkacc, dvacc, dksend, dvsend, dkrecv, dvrecv, dxacc;
+  size_t dqsem;                                       // UPIPE_FLAG_DETERMINISTIC dQ-order semaphores (int32)
   size_t kring[2], vring[2], dkring[2], dvring[2];   // ring hybrid only
   size_t total;
 };
@@ -161,6 +162,8 @@ struct RopeTables {
 }  // namespace upipe
 
 struct upipe_ctx_s {
+  upipe_probe_t probe{-1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                      nullptr, nullptr, nullptr};   // test-only layout probe (upipe_test_set_probe)
   upipe::RopeTables rope;
   upipe::Pipe pipe;
   upipe::Tracer tracer;

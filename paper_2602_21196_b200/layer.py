@@ -18,18 +18,20 @@ class UPipeAttention:
     def __init__(self, n_q_heads: int, n_kv_heads: int, head_dim: int, hidden: int, chunk_heads: int,
                  causal: bool = True, process_group=None, device=None, fabric=None, cp_rank: int | None = None,
                  cp_size: int | None = None, sync_comm: bool = False, naive_kv: bool = False,
-                 rope_base: float = 0.0, ring_degree: int = 1):
+                 rope_base: float = 0.0, ring_degree: int = 1, deterministic: bool = False):
         """CP group: ``process_group`` (torch.distributed, one process per GPU, NCCL transport),
         or ``fabric`` + ``cp_rank`` + ``cp_size`` (single-process group driven by one host thread per rank),
         or neither (C = 1). ``sync_comm``: sequential schedule with one chunk buffer set (the
         paper's memory-minimal form); default overlaps the next chunk's all-to-all with the current
         chunk's attention on a side stream (two buffer sets). ``ring_degree`` r > 1: UPipe x Ring hybrid
-        (DESIGN A27): Ulysses groups of C/r consecutive ranks, Ring Attention across the r groups."""
+        (DESIGN A27): Ulysses groups of C/r consecutive ranks, Ring Attention across the r groups.
+        ``deterministic``: bitwise-reproducible backward (dQ partials added in key-tile order; slower)."""
         self.Hq, self.Hkv, self.d, self.D, self.U = n_q_heads, n_kv_heads, head_dim, hidden, chunk_heads
         self.causal = int(causal)
         self.rope_base = float(rope_base)    # 0: no RoPE; else rotary base (Llama3: 500000), DESIGN A26
         self.ring = max(1, int(ring_degree))
-        self.flags = (1 if sync_comm else 0) | (2 if naive_kv else 0)   # UPIPE_FLAG_SYNC_COMM, UPIPE_FLAG_NAIVE_KV
+        # UPIPE_FLAG_SYNC_COMM, UPIPE_FLAG_NAIVE_KV, UPIPE_FLAG_DETERMINISTIC
+        self.flags = (1 if sync_comm else 0) | (2 if naive_kv else 0) | (4 if deterministic else 0)
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         if fabric is not None:

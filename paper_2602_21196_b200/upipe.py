@@ -37,6 +37,14 @@ class upipe_stage_info_t(ctypes.Structure):
                 ("q0", c_int32), ("kv0", c_int32), ("kv_sent", c_int32)]
 
 
+class upipe_probe_t(ctypes.Structure):
+    """Test-only layout probe (include/upipe.h upipe_test_set_probe)."""
+    _fields_ = [("stage", c_int32), ("q_recv", c_void_p), ("k_recv", c_void_p), ("v_recv", c_void_p),
+                ("o_head", c_void_p), ("do_recv", c_void_p), ("delta_recv", c_void_p), ("dq_head", c_void_p),
+                ("dk_head", c_void_p), ("dv_head", c_void_p), ("dq_recv", c_void_p), ("dk_recv", c_void_p),
+                ("dv_recv", c_void_p)]
+
+
 _lib = None
 
 
@@ -64,13 +72,15 @@ def lib() -> ctypes.CDLL:
             "upipe_attn_fwd": (st, [P, POINTER(upipe_shape_t)] + [P] * 8 + [P, c_size_t, P]),
             "upipe_attn_bwd": (st, [P, POINTER(upipe_shape_t)] + [P] * 13 + [c_int, P, c_size_t, P]),
             "upipe_attn_core_fwd": (st, [P] * 5 + [c_int64, c_int, c_int, c_int, c_int] + [c_int64] * 4 + [P]),
-            "upipe_attn_core_bwd": (st, [P] * 9 + [c_int64, c_int, c_int, c_int, c_int] + [c_int64] * 5 + [c_int, P]),
+            "upipe_attn_core_bwd": (st, [P] * 9 + [c_int64, c_int, c_int, c_int, c_int] + [c_int64] * 5 + [c_int, P, P]),
+            "upipe_core_bwd_sem_count": (c_int64, [c_int64, c_int]),
             "upipe_rowdot": (st, [P, c_int64, P, c_int64, P, c_int64, c_int64, c_int, c_int, P]),
             "upipe_gemm_xwT": (st, [P, P, P, c_int64, c_int64, c_int64, c_int, P]),
             "upipe_synth_fill_bf16": (st, [P, c_int64, c_uint64, c_int, c_int, c_int64, P]),
             "upipe_kernel_launches": (st, [POINTER(c_uint64)]),
             "upipe_set_trace": (st, [P, c_int]),
             "upipe_trace_read": (st, [P, POINTER(ctypes.c_double), POINTER(c_int64)]),
+            "upipe_test_set_probe": (st, [P, POINTER(upipe_probe_t)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -82,9 +92,9 @@ def lib() -> ctypes.CDLL:
 
 EXPORTED = ("upipe_get_unique_id", "upipe_init", "upipe_fabric_create", "upipe_fabric_destroy", "upipe_init_local",
             "upipe_finalize", "upipe_status_string", "upipe_last_error", "upipe_workspace_size", "upipe_plan_stage",
-            "upipe_validate", "upipe_attn_fwd", "upipe_attn_bwd", "upipe_attn_core_fwd", "upipe_attn_core_bwd",
+            "upipe_validate", "upipe_attn_fwd", "upipe_attn_bwd", "upipe_attn_core_fwd", "upipe_attn_core_bwd", "upipe_core_bwd_sem_count",
             "upipe_rowdot", "upipe_gemm_xwT", "upipe_synth_fill_bf16", "upipe_kernel_launches", "upipe_set_trace",
-            "upipe_trace_read")
+            "upipe_trace_read", "upipe_test_set_probe")
 
 TRACE_CATS = ("gemm", "attn_fwd", "attn_bwd", "comm", "aux")
 
@@ -206,11 +216,22 @@ def upipe_attn_core_fwd(q, k, v, o, lse, S, nq, nkv, d, causal, ldq, ldkv, ldo, 
                                      ldq, ldkv, ldo, ld_lse, _stream(stream)))
 
 
+CORE_ACCUMULATE, CORE_DQ_DIM_MAJOR, CORE_DETERMINISTIC = 1, 2, 4     # upipe_attn_core_bwd flags
+
+
 def upipe_attn_core_bwd(q, k, v, dout, lse, delta, dq_acc, dk_acc, dv_acc, S, nq, nkv, d, causal, ldq, ldkv,
-                        ldo_grad, ld_lse, ld_delta, accumulate=0, stream=None):
+                        ldo_grad, ld_lse, ld_delta, accumulate=0, stream=None, dq_dim_major=False, dq_sem=None):
+    """dq_dim_major: dq_acc is [nq*d][S]; dq_sem (zeroed int32 tensor of upipe_core_bwd_sem_count ints):
+    deterministic dQ order."""
+    flags = (CORE_ACCUMULATE if accumulate else 0) | (CORE_DQ_DIM_MAJOR if dq_dim_major else 0) | \
+        (CORE_DETERMINISTIC if dq_sem is not None else 0)
     _check(lib().upipe_attn_core_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(dout), _ptr(lse), _ptr(delta), _ptr(dq_acc),
                                      _ptr(dk_acc), _ptr(dv_acc), S, nq, nkv, d, int(causal), ldq, ldkv, ldo_grad,
-                                     ld_lse, ld_delta, int(accumulate), _stream(stream)))
+                                     ld_lse, ld_delta, flags, _ptr(dq_sem), _stream(stream)))
+
+
+def upipe_core_bwd_sem_count(S: int, nq: int) -> int:
+    return int(lib().upipe_core_bwd_sem_count(S, nq))
 
 
 def upipe_rowdot(dO, ld_do, O, ld_o, delta, ld_delta, rows, nheads, d, stream=None):
@@ -244,3 +265,17 @@ def upipe_trace_read(ctx) -> dict:
     cnt = (c_int64 * len(TRACE_CATS))()
     _check(lib().upipe_trace_read(ctx, ms, cnt), ctx)
     return {k: (ms[i], cnt[i]) for i, k in enumerate(TRACE_CATS)}
+
+
+# ------------------------------------------------------------------ test-only
+
+def upipe_test_set_probe(ctx, stage: int = -1, **bufs) -> None:
+    """Set (stage >= 0) or clear (stage = -1) the ctx's layout probe; bufs: torch tensors or None for the
+    fields of upipe_probe_t (q_recv, k_recv, v_recv, o_head, do_recv, delta_recv, dq_head, dk_head,
+    dv_head, dq_recv, dk_recv, dv_recv)."""
+    names = [f for f, _ in upipe_probe_t._fields_][1:]
+    unknown = set(bufs) - set(names)
+    if unknown:
+        raise TypeError(f"unknown probe fields {sorted(unknown)}")
+    p = upipe_probe_t(stage, *[_ptr(bufs.get(n)) for n in names])
+    _check(lib().upipe_test_set_probe(ctx, ctypes.byref(p)), ctx)

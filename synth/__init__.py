@@ -161,3 +161,18 @@ def core_inputs(seed: int, S: int, Hq: int, Hkv: int, d: int, score_std: float =
         "do": draw(seed, TID["do"], (S, Hq, d), 0),
         "exponents": {"q": eq, "k": eq, "v": 0, "do": 0},
     }
+
+
+def payload_bits(seed: int, tensor_id: int, shape, start: int = 0) -> np.ndarray:
+    """Index payloads for the bit-exact layout tests: a bf16 bit pattern per global element index,
+    finite and normal (sign from the hash, biased exponent in [112, 143], 7 hashed mantissa bits:
+    8192 distinct values), so a misplaced element is caught with probability ~1 - 1/8192 each.
+    Values pass unchanged through a copy, a one-hot projection (x * 1 + zeros) or an all-to-all."""
+    count = int(np.prod(shape)) if len(shape) else 1
+    base = (seed * _G1 + tensor_id * _G2 + start) & _M64
+    with np.errstate(over="ignore"):
+        z = _splitmix64(np.arange(count, dtype=np.uint64) + np.uint64(base))
+    sign = (z >> np.uint64(63)) << np.uint64(15)
+    expo = (np.uint64(112) + ((z >> np.uint64(40)) & np.uint64(31))) << np.uint64(7)
+    mant = (z >> np.uint64(20)) & np.uint64(0x7F)
+    return (sign | expo | mant).astype(np.uint16).reshape(shape)

@@ -27,7 +27,16 @@ def errs(got, want):
     return rel, float(np.abs(got - want).max())
 
 
+# Every assert_close records its achieved errors; tests/conftest.py writes them to
+# $UPIPE_PARITY_REPORT (JSON) at the end of the session (the committed profiles/parity_r02.json).
+RECORDS = []
+
+
 def assert_close(name, got, want, rel_tol, abs_tol):
+    import os
     rel, mx = errs(got, want)
+    RECORDS.append({"test": os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0], "tensor": name,
+                    "rel_l2": float(rel), "max_abs": mx, "rel_tol": rel_tol, "abs_tol": abs_tol,
+                    "ok": bool(np.isfinite(rel) and rel <= rel_tol and mx <= abs_tol)})
     assert np.isfinite(rel) and rel <= rel_tol and mx <= abs_tol, f"{name}: rel L2 {rel:.3e} (tol {rel_tol}), max|d| {mx:.3e} (tol {abs_tol})"
     return rel, mx

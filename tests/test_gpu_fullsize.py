@@ -75,3 +75,40 @@ def test_fullsize_bench_workload_sampled_rows(rope_base):
     dy_tail = synth.draw(0, synth.TID["dy"], (TAIL, D), e["dy"], start=(S - TAIL) * D)
     dX = oracle.layer_bwd_tail(x_tail, dy_tail, K, V, wq, wk, wv, wo, Hq, Hkv, d, rope_base=rb)
     assert_close("dx tail rows", dx_t, dX, REL, ABS)
+
+
+@pytest.mark.timeout(3600)
+@pytest.mark.parametrize("nq,nkv", [(8, 2), (1, 1)])
+def test_attn_core_32k_full_tensor(nq, nkv):
+    # Full-tensor elementwise attention parity at S = 32K (the oracle's BLAS-backed blocks finish in
+    # minutes): the bench's per-stage launch shape at CP 1 (8 Q / 2 KV heads of the stage, d 128) and the
+    # CP 8 per-rank shape (1 / 1), forward and the 64-query backward with the dim-major dQ accumulator
+    # (the layer's configuration), every element of O, LSE, dQ, dK, dV against the fp64 oracle.
+    from paper_2602_21196_b200 import upipe
+    S, d = 32768, 128
+    c = synth.core_inputs(0, S, nq, nkv, d, 1.0)
+    from gpu_util import to_bf16
+    q, k, v, do = (to_bf16(c[n]) for n in ("q", "k", "v", "do"))
+    o = torch.empty((S, nq, d), dtype=torch.bfloat16, device=dev())
+    lse = torch.empty((nq, S), dtype=torch.float32, device=dev())
+    upipe.upipe_attn_core_fwd(q, k, v, o, lse, S, nq, nkv, d, 1, nq * d, nkv * d, nq * d, S)
+    delta = torch.empty((S, nq), dtype=torch.float32, device=dev())
+    upipe.upipe_rowdot(do, nq * d, o, nq * d, delta, nq, S, nq, d)
+    dq = torch.zeros((nq * d, S), dtype=torch.float32, device=dev())
+    dk = torch.empty((S, nkv, d), dtype=torch.float32, device=dev())
+    dv = torch.empty((S, nkv, d), dtype=torch.float32, device=dev())
+    upipe.upipe_attn_core_bwd(q, k, v, do, lse, delta, dq, dk, dv, S, nq, nkv, d, 1, nq * d, nkv * d, nq * d, S, nq,
+                              dq_dim_major=True)
+    torch.cuda.synchronize()
+    o_np, lse_np = to_np(o), to_np(lse)
+    dq_np = to_np(dq.reshape(nq, d, S).permute(2, 0, 1))
+    dk_np, dv_np = to_np(dk), to_np(dv)
+    del q, k, v, do, o, lse, delta, dq, dk, dv
+    torch.cuda.empty_cache()
+    O, L = oracle.attn_fwd(c["q"], c["k"], c["v"], causal=True)
+    assert_close("O 32K", o_np, O, 3e-3, ABS)
+    assert_close("lse 32K", lse_np, L, 1e-4, 2e-4)
+    dQ, dK, dV = oracle.attn_bwd(c["q"], c["k"], c["v"], c["do"], causal=True)
+    assert_close("dV 32K", dv_np, dV, 3e-3, ABS)
+    assert_close("dQ 32K", dq_np, dQ, 4e-3, ABS)
+    assert_close("dK 32K", dk_np, dK, 4e-3, ABS)

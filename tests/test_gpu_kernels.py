@@ -171,3 +171,56 @@ def test_bwd_128_query_kernel_subprocess():
                         "-m", "gpu", "-k", "bwd and not subprocess"], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def _bwd_inputs(U, S, Hq, Hkv, d, causal, score_std=1.0, seed=0):
+    c = _core(S, Hq, Hkv, d, score_std, seed)
+    q, k, v, o, lse = _run_fwd(U, c, S, Hq, Hkv, d, causal)
+    do = to_bf16(c["do"])
+    delta = torch.empty((S, Hq), dtype=torch.float32, device=dev())
+    U.upipe_rowdot(do, Hq * d, o, Hq * d, delta, Hq, S, Hq, d)
+    return c, (q, k, v, do, lse, delta)
+
+
+def _bwd(U, t, S, Hq, Hkv, d, causal, dim_major=False, det=False):
+    q, k, v, do, lse, delta = t
+    dq = torch.zeros((Hq * d, S) if dim_major else (S, Hq, d), dtype=torch.float32, device=dev())
+    dk = torch.empty((S, Hkv, d), dtype=torch.float32, device=dev())
+    dv = torch.empty((S, Hkv, d), dtype=torch.float32, device=dev())
+    sem = torch.zeros(U.upipe_core_bwd_sem_count(S, Hq), dtype=torch.int32, device=dev()) if det else None
+    U.upipe_attn_core_bwd(q, k, v, do, lse, delta, dq, dk, dv, S, Hq, Hkv, d, causal, Hq * d, Hkv * d, Hq * d, S, Hq,
+                          dq_dim_major=dim_major, dq_sem=sem)
+    if dim_major:
+        dq = dq.reshape(Hq, d, S).permute(2, 0, 1).contiguous()
+    return dq, dk, dv
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,causal", [(1000, 8, 2, 1), (640, 4, 1, 1), (384, 2, 2, 0)])
+def test_attn_bwd_dim_major_dq(U, S, Hq, Hkv, causal):
+    # the layer's launch configuration at d = 128: the 64-query kernel with the dim-major dQ accumulator
+    c, t = _bwd_inputs(U, S, Hq, Hkv, 128, causal)
+    dq, dk, dv = _bwd(U, t, S, Hq, Hkv, 128, causal, dim_major=True)
+    torch.cuda.synchronize()
+    dQ, dK, dV = oracle.attn_bwd(c["q"], c["k"], c["v"], c["do"], causal=bool(causal))
+    assert_close("dV", to_np(dv), dV, ATTN_REL, ABS)
+    assert_close("dQ", to_np(dq), dQ, ATTN_GRAD_REL, ABS)
+    assert_close("dK", to_np(dk), dK, ATTN_GRAD_REL, ABS)
+
+
+@pytest.mark.parametrize("S,Hq,Hkv,d,causal,dim_major", [(2000, 8, 2, 128, 1, True), (1500, 4, 2, 128, 1, False),
+                                                         (1024, 4, 1, 64, 1, False), (777, 2, 1, 128, 0, True),
+                                                         (900, 4, 2, 64, 0, False)])
+def test_attn_bwd_deterministic_bitwise(U, S, Hq, Hkv, d, causal, dim_major):
+    # UPIPE_CORE_DETERMINISTIC: key tiles add their dQ partials in key-tile order, so
+    # repeated launches are bitwise identical; the result still meets the kernel parity bar
+    c, t = _bwd_inputs(U, S, Hq, Hkv, d, causal)
+    runs = [_bwd(U, t, S, Hq, Hkv, d, causal, dim_major=dim_major, det=True) for _ in range(3)]
+    torch.cuda.synchronize()
+    for r in runs[1:]:
+        for a, b in zip(runs[0], r):
+            assert torch.equal(a, b)
+    dQ, dK, dV = oracle.attn_bwd(c["q"], c["k"], c["v"], c["do"], causal=bool(causal))
+    dq, dk, dv = runs[0]
+    assert_close("dV", to_np(dv), dV, ATTN_REL, ABS)
+    assert_close("dQ", to_np(dq), dQ, ATTN_GRAD_REL, ABS)
+    assert_close("dK", to_np(dk), dK, ATTN_GRAD_REL, ABS)

@@ -18,7 +18,7 @@ REL, ABS = 5e-3, 2e-2
 
 
 def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", bwd=True, sync=False, exp_S=None,
-               naive=False, comm_counts=None, rope_base=0.0, ring=1):
+               naive=False, comm_counts=None, rope_base=0.0, ring=1, det=False):
     """Run the layer on C ranks; returns (per-rank outputs, inputs). exp_S: draw the first S tokens of
     a length-exp_S sequence (its value scales), e.g. to keep dY's 1/sqrt(S) scale sane for tiny S."""
     from paper_2602_21196_b200 import UPipeAttention, upipe
@@ -41,9 +41,11 @@ def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", b
             with torch.cuda.stream(stream):
                 if C > 1:
                     attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal, fabric=fabric, cp_rank=r, cp_size=C,
-                                          sync_comm=sync, naive_kv=naive, rope_base=rope_base, ring_degree=ring)
+                                          sync_comm=sync, naive_kv=naive, rope_base=rope_base, ring_degree=ring,
+                                          deterministic=det)
                 else:
-                    attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal, naive_kv=naive, rope_base=rope_base)
+                    attn = UPipeAttention(Hq, Hkv, d, D, Uc, causal, naive_kv=naive, rope_base=rope_base,
+                                          deterministic=det)
                 if comm_counts is not None:
                     upipe.upipe_set_trace(attn.ctx, True)
                 y, saved = attn.forward(xs[r], W["wq"], W["wk"], W["wv"], W["wo"])
@@ -75,9 +77,29 @@ def _run_group(C, S, D, Hq, Hkv, d, Uc, seed=0, causal=True, profile="benign", b
     return results, inp
 
 
+_ORACLE_CACHE = {}
+
+
+def _oracle(inp, Hq, Hkv, d, causal, rope_base, bwd):
+    """The un-sharded fp64 oracle of the layer on these inputs (cached: several (C, U) runs of one
+    test module share inputs, and the result does not depend on C or U)."""
+    x, wq, wk, wv, wo, dy = (inp[k] for k in ("x", "wq", "wk", "wv", "wo", "dy"))
+    key = (x.shape, float(x.sum()), float(wq.sum()), float(wo.sum()), float(dy.sum()), Hq, Hkv, d, causal, rope_base)
+    hit = _ORACLE_CACHE.get(key)
+    if hit is None or (bwd and "bwd" not in hit):
+        hit = {"fwd": oracle.layer_fwd(x, wq, wk, wv, wo, Hq, Hkv, d, causal, rope_base=rope_base)}
+        if bwd:
+            hit["bwd"] = oracle.layer_bwd(x, wq, wk, wv, wo, dy, Hq, Hkv, d, causal, rope_base=rope_base)
+        if len(_ORACLE_CACHE) > 4:
+            _ORACLE_CACHE.clear()
+        _ORACLE_CACHE[key] = hit
+    return hit
+
+
 def _check(results, inp, C, Hq, Hkv, d, U, causal=True, bwd=True, rope_base=None, ring=1):
     x, wq, wk, wv, wo, dy = (inp[k] for k in ("x", "wq", "wk", "wv", "wo", "dy"))
-    Y, O, L = oracle.layer_fwd(x, wq, wk, wv, wo, Hq, Hkv, d, causal, rope_base=rope_base)
+    ref = _oracle(inp, Hq, Hkv, d, causal, rope_base, bwd)
+    Y, O, L = ref["fwd"]
     y = np.concatenate([to_np(r["y"]) for r in results], 0)
     o = np.concatenate([to_np(r["o"]) for r in results], 0)
     assert_close("y", y, Y, REL, ABS)
@@ -103,7 +125,7 @@ def _check(results, inp, C, Hq, Hkv, d, U, causal=True, bwd=True, rope_base=None
                     f"lse[p{p},h{q0 + j}]: max|dLSE| {np.abs(dl).max():.3e}, rms(exp(dLSE)-1) {rms:.3e}"
     if not bwd:
         return
-    dX, dWq, dWk, dWv, dWo = oracle.layer_bwd(x, wq, wk, wv, wo, dy, Hq, Hkv, d, causal, rope_base=rope_base)
+    dX, dWq, dWk, dWv, dWo = ref["bwd"]
     dx = np.concatenate([to_np(r["dx"]) for r in results], 0)
     assert_close("dx", dx, dX, REL, ABS)
     for name, want in (("dwq", dWq), ("dwk", dWk), ("dwv", dWv), ("dwo", dWo)):
@@ -181,13 +203,17 @@ def test_invalid_shape_named_error():
 @pytest.mark.parametrize("C,Hq,Hkv,U", [(2, 8, 2, 2), (4, 16, 4, 4), (4, 16, 4, 16), (2, 8, 2, 8), (4, 32, 8, 8)])
 def test_overlapped_schedule_equals_sequential_bitwise(C, Hq, Hkv, U):
     # The overlapped schedule (next chunk's all-to-all on the comm stream during the current attention,
-    # double buffers) only reorders independent work: every output is bitwise identical to the sequential one.
+    # double buffers) only reorders independent work: the forward outputs are bitwise identical to the
+    # sequential ones. The backward's dQ is a cross-CTA fp32 reduction whose order depends on timing
+    # (TMA reduce-add), so dx and dW are compared with the oracle instead (and bitwise only in the
+    # deterministic mode, test_deterministic_backward_bitwise).
     ro, inp = _run_group(C, 512, 256, Hq, Hkv, 64, U)
     rs, _ = _run_group(C, 512, 256, Hq, Hkv, 64, U, sync=True)
     for p in range(C):
-        for k in ro[p]:
+        for k in ("y", "o", "lse"):
             assert torch.equal(ro[p][k], rs[p][k]), (p, k)
     _check(ro, inp, C, Hq, Hkv, 64, U)
+    _check(rs, inp, C, Hq, Hkv, 64, U)
 
 
 # ---- degenerate and boundary cases of the method
@@ -260,9 +286,55 @@ def test_ring_hybrid_rope():
 
 
 def test_ring_degree_one_is_upipe_bitwise():
-    # ring_degree = 1 is plain UPipe: identical outputs (same kernels, same order)
-    a, _ = _run_group(2, 512, 256, 8, 2, 64, 2, ring=1, sync=True)
+    # ring_degree = 1 is plain UPipe: identical forward outputs (same kernels, same order); the backward
+    # meets the bar (its dQ reduction order is timing-dependent, see above)
+    a, inp = _run_group(2, 512, 256, 8, 2, 64, 2, ring=1, sync=True)
     b, _ = _run_group(2, 512, 256, 8, 2, 64, 2, sync=True)
     for ra, rb in zip(a, b):
-        for k in ra:
+        for k in ("y", "o", "lse"):
             assert torch.equal(ra[k], rb[k]), k
+    _check(a, inp, 2, 8, 2, 64, 2)
+
+
+# ---------------------------------------------------------------- the BASELINE configs' exact schedules
+# (CP 8 per-rank shapes on the single-process fabric; the oracle runs the un-sharded layer)
+
+@pytest.mark.timeout(1200)
+@pytest.mark.parametrize("U", [8, 16, 32])
+def test_llama3_8b_cp8_schedules(U):
+    # BASELINE configs[1]/[2]: Llama3-8B attention (32 Q / 8 KV, d 128, hidden 4096) at CP 8 with
+    # chunk 8 / 16 / 32 (qpd = 1, sigma = 4 / qpd = 2, sigma = 2 / qpd = 4 = R, Ulysses), S = 2048
+    r, inp = _run_group(8, 2048, 4096, 32, 8, 128, U)
+    _check(r, inp, 8, 32, 8, 128, U)
+
+
+@pytest.mark.timeout(1200)
+@pytest.mark.parametrize("C", [8, 1])
+def test_32b_class_layer(C):
+    # BASELINE configs[4]: 64 Q / 8 KV heads (R = 8), d 128, hidden 5120 (D != Hq d) at chunk 8:
+    # CP 8 gives qpd = 1, sigma = 8 (eight stages share each resident KV head); CP 1 gives 8 stages of 8
+    r, inp = _run_group(C, 1024, 5120, 64, 8, 128, 8)
+    _check(r, inp, C, 64, 8, 128, 8)
+
+
+@pytest.mark.timeout(1200)
+def test_mha_control_cp8():
+    # SURVEY §8d control: MHA 32/32 at CP 8, chunk 8 (R = 1: every stage sends its own K/V heads)
+    r, inp = _run_group(8, 1024, 4096, 32, 32, 128, 8)
+    _check(r, inp, 8, 32, 32, 128, 8)
+
+
+@pytest.mark.parametrize("C,Hq,Hkv,d,U,ring", [(2, 8, 2, 64, 2, 1), (4, 32, 8, 128, 8, 1), (1, 8, 2, 128, 4, 1),
+                                               (4, 8, 2, 64, 2, 2)])
+def test_deterministic_backward_bitwise(C, Hq, Hkv, d, U, ring):
+    # UPIPE_FLAG_DETERMINISTIC: the backward is bitwise reproducible, run to run and
+    # between the overlapped and the sequential schedule, and meets the north_star bar
+    S = 1024
+    r1, inp = _run_group(C, S, 512, Hq, Hkv, d, U, det=True, ring=ring)
+    r2, _ = _run_group(C, S, 512, Hq, Hkv, d, U, det=True, ring=ring)
+    r3, _ = _run_group(C, S, 512, Hq, Hkv, d, U, det=True, ring=ring, sync=True)
+    for p in range(C):
+        for k in r1[p]:
+            assert torch.equal(r1[p][k], r2[p][k]), (p, k, "run to run")
+            assert torch.equal(r1[p][k], r3[p][k]), (p, k, "overlapped vs sequential")
+    _check(r1, inp, C, Hq, Hkv, d, U, ring=ring)

@@ -19,6 +19,48 @@ def rand(*shape, scale=1.0):
     return RNG.standard_normal(shape) * scale
 
 
+# ---------------------------------------------------------------- projection (DESIGN A4)
+
+def test_project_brute_force_sum():
+    # plain definition of nn.Linear without bias: y[i, j] = sum_k x[i, k] W[j, k], summed exactly (fsum)
+    X, W = rand(5, 7), rand(3, 7)
+    Y = O.project(X, W)
+    assert Y.shape == (5, 3)
+    for i in range(5):
+        for j in range(3):
+            assert abs(Y[i, j] - math.fsum(X[i, k] * W[j, k] for k in range(7))) <= 1e-13
+
+
+def test_project_one_hot_rows_gather_columns_bitwise():
+    # W row j = e_{c_j}: output column j is exactly input column c_j (catches a transposed operand
+    # or a row/column mix-up; this is also how the GPU layout probes build exact payloads)
+    S, D = 6, 9
+    cols = [4, 0, 8, 4, 2]
+    X = rand(S, D)
+    W = np.zeros((len(cols), D))
+    W[np.arange(len(cols)), cols] = 1.0
+    assert np.array_equal(O.project(X, W), X[:, cols])
+
+
+def test_project_matches_torch_linear():
+    X, W = rand(33, 48), rand(20, 48)
+    ref = F.linear(torch.from_numpy(X), torch.from_numpy(W)).numpy()
+    np.testing.assert_allclose(O.project(X, W), ref, rtol=0, atol=1e-12)
+
+
+def test_layer_uses_projection_per_head_rows():
+    # head h of Q is X Wq[h d:(h+1) d]^T (DESIGN A4): the layer's O for head h only changes when
+    # rows of head h (or its kv head) change
+    S, D, Hq, Hkv, d = 16, 12, 4, 2, 3
+    X, Wq, Wk, Wv, Wo = rand(S, D), rand(Hq * d, D), rand(Hkv * d, D), rand(Hkv * d, D), rand(D, Hq * d)
+    _, O1, _ = O.layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d)
+    Wq2 = Wq.copy()
+    Wq2[2 * d:3 * d] += 1.0                       # rows of q head 2
+    _, O2, _ = O.layer_fwd(X, Wq2, Wk, Wv, Wo, Hq, Hkv, d)
+    changed = [not np.array_equal(O1[:, h * d:(h + 1) * d], O2[:, h * d:(h + 1) * d]) for h in range(Hq)]
+    assert changed == [False, False, True, False]
+
+
 # ---------------------------------------------------------------- attention fwd
 
 def test_spec_s2_example(golden):
