@@ -126,9 +126,46 @@ UPIPE_API upipe_status_t upipe_fabric_create(upipe_fabric_t* fabric, int cp_size
 UPIPE_API upipe_status_t upipe_fabric_destroy(upipe_fabric_t fabric);
 UPIPE_API upipe_status_t upipe_init_local(upipe_ctx_t* ctx, upipe_fabric_t fabric, int cp_rank, int cuda_device, uint32_t flags);
 
+/* Direct-to-peer transport. One process per rank (one GPU each; several
+ * ranks may share a GPU, e.g. in tests). The ctx allocates a symmetric region (cudaMalloc, the same
+ * layout on every rank) that holds the layer's whole workspace -- every receive buffer at the same
+ * offset on every rank -- plus synchronisation flags and the dW all-reduce scratch; peers map it with
+ * CUDA IPC and PUSH their blocks straight into the owner's receive buffers (the projection GEMM's
+ * epilogue, the attention epilogue and the dQ conversion write there directly; the remaining transfers
+ * use the copy engines), ordered by flags the GPU front end writes and waits on. No NCCL, no send
+ * buffers for the fused steps. Two phases; the caller exchanges the opaque handles (e.g. all_gather
+ * over a torch process group):
+ *   upipe_ipc_create(&ctx, C, rank, device, flags, max_shape, my_handle)
+ *   upipe_ipc_connect(ctx, handles)   handles: [cp_size][UPIPE_IPC_HANDLE_BYTES], rank order
+ * The region is sized for shapes up to `max_shape` (same heads, seq_local <= max_shape->seq_local);
+ * upipe_attn_fwd / upipe_attn_bwd on such a ctx use it and ignore `workspace` (may be NULL, 0).
+ * The region is library memory (not the caller's allocator): upipe_ipc_region_size reports it. */
+#define UPIPE_IPC_HANDLE_BYTES 128
+UPIPE_API upipe_status_t upipe_ipc_region_size(int cp_size, const upipe_shape_t* max_shape, uint32_t flags,
+                                               size_t* bytes);
+UPIPE_API upipe_status_t upipe_ipc_create(upipe_ctx_t* ctx, int cp_size, int cp_rank, int cuda_device, uint32_t flags,
+                                          const upipe_shape_t* max_shape, uint8_t handle[UPIPE_IPC_HANDLE_BYTES]);
+UPIPE_API upipe_status_t upipe_ipc_connect(upipe_ctx_t ctx, const uint8_t* handles);
+
 UPIPE_API upipe_status_t upipe_finalize(upipe_ctx_t ctx);
 UPIPE_API const char* upipe_status_string(upipe_status_t s);
 UPIPE_API const char* upipe_last_error(upipe_ctx_t ctx); /* thread-local message if ctx == NULL */
+
+/* Failure detection. Waits until `stream` has completed the work enqueued so far while
+ * polling the ctx's communicator for asynchronous errors (NCCL: ncclCommGetAsyncError). An error, or
+ * no completion within timeout_ms (a dead or stalled peer; <= 0: no limit), aborts the communicator
+ * (ncclCommAbort: this rank's pending collectives return instead of hanging) and returns
+ * UPIPE_ERR_COMM with the reason in upipe_last_error; the ctx must then be finalized. */
+UPIPE_API upipe_status_t upipe_wait(upipe_ctx_t ctx, void* stream, int64_t timeout_ms);
+
+/* What the ctx is connected to (for checking a launch: every rank should see nranks == cp_size). */
+typedef struct {
+  int32_t nranks, rank;
+  int32_t cuda_device;  /* the communicator's device (NCCL) or the ctx's device */
+  int32_t transport;    /* 0: none (C = 1), 1: NCCL, 2: single-process fabric, 3: IPC direct-to-peer */
+  int32_t max_ctas;     /* NCCL CTA cap (UPIPE_NCCL_MAX_CTAS, default 16); 0 if not NCCL */
+} upipe_comm_info_t;
+UPIPE_API upipe_status_t upipe_comm_info(upipe_ctx_t ctx, upipe_comm_info_t* info);
 
 /* ---------------------------------------------------------------- planning (host only, no GPU) */
 

@@ -2,6 +2,7 @@
 // status codes, no exceptions across the ABI.
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <atomic>
 #include <map>
@@ -44,7 +45,17 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 upipe_status_t check_ctx(upipe_ctx_t ctx) {
   if (!ctx || !ctx->alive || !ctx->transport) return set_err(nullptr, UPIPE_ERR_STATE, "ctx not initialised or finalised");
+  if (ctx->ipc_pending) return set_err(ctx, UPIPE_ERR_STATE, "IPC ctx not connected (upipe_ipc_connect)");
   return UPIPE_OK;
+}
+
+// The layer's workspace: the ctx's symmetric region for an IPC ctx, else the caller's.
+bool resolve_ws(upipe_ctx_t ctx, void*& ws, size_t& ws_bytes) {
+  if (char* w = ctx->transport->workspace()) {
+    ws = w;
+    ws_bytes = ctx->transport->workspace_bytes();
+  }
+  return ws != nullptr;
 }
 
 upipe_status_t cuda_status(cudaError_t e, const char* what, const char* detail = nullptr) {
@@ -130,11 +141,91 @@ upipe_status_t upipe_init_local(upipe_ctx_t* out, upipe_fabric_t fabric, int cp_
   return UPIPE_OK;
 }
 
+namespace {
+// workspace + dW scratch of an IPC ctx for shapes up to sh
+void ipc_sizes(int C, const upipe_shape_t& sh, uint32_t flags, size_t* ws, size_t* scratch) {
+  Plan P = make_plan(C, sh);
+  P.naive = (flags & UPIPE_FLAG_NAIVE_KV) != 0;
+  const bool ov = overlap_enabled(flags, P);
+  *ws = std::max(fwd_workspace(P, ov).total, bwd_workspace(P, ov).total);
+  const size_t hq = (size_t)sh.n_q_heads * sh.head_dim, hkv = (size_t)sh.n_kv_heads * sh.head_dim;
+  *scratch = std::max(hq, hkv) * (size_t)sh.hidden * 4;
+}
+}  // namespace
+
+upipe_status_t upipe_ipc_region_size(int cp_size, const upipe_shape_t* shape, uint32_t flags, size_t* bytes) {
+  std::string m;
+  if (upipe_status_t st = validate_shape(cp_size, shape, m)) return set_err(nullptr, st, m);
+  if (!bytes) return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "bytes == NULL");
+  size_t ws = 0, sc = 0;
+  ipc_sizes(cp_size, *shape, flags, &ws, &sc);
+  *bytes = ipc_region_bytes(ws, sc);
+  return UPIPE_OK;
+}
+
+upipe_status_t upipe_ipc_create(upipe_ctx_t* out, int cp_size, int cp_rank, int cuda_device, uint32_t flags,
+                                const upipe_shape_t* shape, uint8_t handle[UPIPE_IPC_HANDLE_BYTES]) {
+  if (!out || !handle) return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "ctx or handle == NULL");
+  *out = nullptr;
+  if (cp_size < 1 || cp_rank < 0 || cp_rank >= cp_size)
+    return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "cp_rank must be in [0, cp_size)");
+  std::string m;
+  if (upipe_status_t st = validate_shape(cp_size, shape, m)) return set_err(nullptr, st, m);
+  cudaError_t e = cudaSetDevice(cuda_device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+  size_t ws = 0, sc = 0;
+  ipc_sizes(cp_size, *shape, flags, &ws, &sc);
+  std::string err;
+  auto t = make_ipc_transport(cp_size, cp_rank, cuda_device, ws, sc, handle, err);
+  if (!t) return set_err(nullptr, UPIPE_ERR_CUDA, err);
+  auto* c = new (std::nothrow) upipe_ctx_s();
+  if (!c) return set_err(nullptr, UPIPE_ERR_STATE, "out of host memory");
+  c->device = cuda_device;
+  c->C = cp_size;
+  c->rank = cp_rank;
+  c->flags = flags;
+  c->transport = std::move(t);
+  c->ipc_pending = true;
+  *out = c;
+  return UPIPE_OK;
+}
+
+upipe_status_t upipe_ipc_connect(upipe_ctx_t ctx, const uint8_t* handles) {
+  if (!ctx || !ctx->transport) return set_err(nullptr, UPIPE_ERR_STATE, "ctx not initialised");
+  if (!handles) return set_err(ctx, UPIPE_ERR_INVALID_ARG, "handles == NULL");
+  cudaSetDevice(ctx->device);
+  std::string err;
+  if (upipe_status_t st = ipc_connect(ctx->transport.get(), handles, err)) return set_err(ctx, st, err);
+  ctx->ipc_pending = false;
+  return UPIPE_OK;
+}
+
 upipe_status_t upipe_finalize(upipe_ctx_t ctx) {
   if (!ctx) return set_err(nullptr, UPIPE_ERR_STATE, "ctx == NULL");
   ctx->transport.reset();
   ctx->alive = false;
   delete ctx;
+  return UPIPE_OK;
+}
+
+upipe_status_t upipe_wait(upipe_ctx_t ctx, void* stream, int64_t timeout_ms) {
+  if (upipe_status_t st = check_ctx(ctx)) return st;
+  cudaSetDevice(ctx->device);
+  std::string err;
+  const upipe_status_t st = ctx->transport->wait(static_cast<cudaStream_t>(stream), timeout_ms / 1000.0, err);
+  if (st != UPIPE_OK) return set_err(ctx, st, "upipe_wait: " + err);
+  return UPIPE_OK;
+}
+
+upipe_status_t upipe_comm_info(upipe_ctx_t ctx, upipe_comm_info_t* info) {
+  if (upipe_status_t st = check_ctx(ctx)) return st;
+  if (!info) return set_err(ctx, UPIPE_ERR_INVALID_ARG, "info == NULL");
+  info->nranks = ctx->transport->size();
+  info->rank = ctx->transport->rank();
+  const int dev = ctx->transport->device();
+  info->cuda_device = dev >= 0 ? dev : ctx->device;
+  info->transport = ctx->transport->kind();
+  info->max_ctas = ctx->transport->max_ctas();
   return UPIPE_OK;
 }
 
@@ -182,7 +273,7 @@ upipe_status_t upipe_attn_fwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
   if (upipe_status_t st = check_ctx(ctx)) return st;
   std::string m;
   if (upipe_status_t st = validate_shape(ctx->C, shape, m)) return set_err(ctx, st, m);
-  if (!x || !wq || !wk || !wv || !wo || !y || !o_saved || !lse_saved || !workspace)
+  if (!x || !wq || !wk || !wv || !wo || !y || !o_saved || !lse_saved || !resolve_ws(ctx, workspace, ws_bytes))
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "null tensor pointer");
   if (!all_aligned(x, wq, wk, wv, wo, y, o_saved, lse_saved) || (reinterpret_cast<uintptr_t>(workspace) & 255))
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "tensors must be 16-byte aligned, workspace 256-byte aligned");
@@ -204,7 +295,7 @@ upipe_status_t upipe_attn_bwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
   std::string m;
   if (upipe_status_t st = validate_shape(ctx->C, shape, m)) return set_err(ctx, st, m);
   if (!x || !wq || !wk || !wv || !wo || !dy || !o_saved || !lse_saved || !dx || !dwq || !dwk || !dwv || !dwo ||
-      !workspace)
+      !resolve_ws(ctx, workspace, ws_bytes))
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "null tensor pointer");
   if (!all_aligned(x, wq, wk, wv, wo, dy, o_saved, lse_saved, dx, dwq, dwk, dwv, dwo) ||
       (reinterpret_cast<uintptr_t>(workspace) & 255))

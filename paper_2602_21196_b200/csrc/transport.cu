@@ -12,10 +12,31 @@
 
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
+#include <thread>
 
 #include "upipe_internal.h"
 
 namespace upipe {
+
+// Default failure detection: poll the stream until it drains or the timeout passes.
+upipe_status_t Transport::wait(cudaStream_t s, double timeout_s, std::string& err) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return UPIPE_OK;
+    if (q != cudaErrorNotReady) {
+      err = std::string("stream: ") + cudaGetErrorString(q);
+      return UPIPE_ERR_CUDA;
+    }
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_s > 0 && el > timeout_s) {
+      err = "timeout waiting for the stream";
+      return UPIPE_ERR_COMM;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+}
 
 namespace {
 
@@ -23,6 +44,7 @@ class SelfTransport final : public Transport {
  public:
   int size() const override { return 1; }
   int rank() const override { return 0; }
+  int kind() const override { return 0; }
   upipe_status_t alltoall_group(const void* send, void* recv, size_t bytes, int, int, cudaStream_t s,
                                 std::string& err) override {
     return copy(send, recv, bytes, s, err);
@@ -46,12 +68,54 @@ class SelfTransport final : public Transport {
 
 class NcclTransport final : public Transport {
  public:
-  NcclTransport(ncclComm_t c, int C, int r) : comm_(c), C_(C), rank_(r) {}
+  NcclTransport(ncclComm_t c, int C, int r, int max_ctas, int dev)
+      : comm_(c), C_(C), rank_(r), max_ctas_(max_ctas), dev_(dev) {}
   ~NcclTransport() override {
-    if (comm_) ncclCommDestroy(comm_);
+    if (comm_) {
+      if (aborted_) return;                      // ncclCommAbort already released it
+      ncclCommDestroy(comm_);
+    }
   }
   int size() const override { return C_; }
   int rank() const override { return rank_; }
+  int kind() const override { return 1; }
+  int max_ctas() const override { return max_ctas_; }
+  int device() const override { return dev_; }
+  // Watchdog (SURVEY §5 failure detection): ncclCommGetAsyncError is polled while the stream drains;
+  // an asynchronous error (e.g. a peer's network/process failure) or a timeout aborts the communicator,
+  // which makes this rank's pending NCCL kernels return, so the rank fails instead of hanging.
+  upipe_status_t wait(cudaStream_t s, double timeout_s, std::string& err) override {
+    if (aborted_) {
+      err = "communicator was aborted";
+      return UPIPE_ERR_COMM;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      ncclResult_t ae = ncclSuccess;
+      ncclResult_t r = ncclCommGetAsyncError(comm_, &ae);
+      if (r != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress)) {
+        err = std::string("NCCL asynchronous error: ") + ncclGetErrorString(r != ncclSuccess ? r : ae);
+        abort_comm();
+        return UPIPE_ERR_COMM;
+      }
+      const cudaError_t q = cudaStreamQuery(s);
+      if (q == cudaSuccess) return UPIPE_OK;
+      if (q != cudaErrorNotReady) {
+        err = std::string("stream: ") + cudaGetErrorString(q);
+        return UPIPE_ERR_CUDA;
+      }
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (timeout_s > 0 && el > timeout_s) {
+        char m[160];
+        snprintf(m, sizeof m, "rank %d: no progress for %.1f s (a peer failed or stalled); communicator aborted",
+                 rank_, el);
+        err = m;
+        abort_comm();
+        return UPIPE_ERR_COMM;
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+  }
   upipe_status_t alltoall_group(const void* send, void* recv, size_t bytes, int first, int n, cudaStream_t s,
                                 std::string& err) override {
     ncclResult_t r = ncclGroupStart();
@@ -88,8 +152,13 @@ class NcclTransport final : public Transport {
   }
 
  private:
+  void abort_comm() {
+    if (!aborted_ && comm_) ncclCommAbort(comm_);
+    aborted_ = true;
+  }
   ncclComm_t comm_;
-  int C_, rank_;
+  int C_, rank_, max_ctas_, dev_;
+  bool aborted_ = false;
 };
 
 }  // namespace
@@ -140,6 +209,8 @@ class FabricTransport final : public Transport {
   }
   int size() const override { return f_->C; }
   int rank() const override { return rank_; }
+  int kind() const override { return 2; }
+  int device() const override { return f_->device[rank_]; }
 
   upipe_status_t alltoall_group(const void* send, void* recv, size_t bytes, int first, int n, cudaStream_t s,
                                 std::string& err) override {
@@ -245,13 +316,37 @@ std::unique_ptr<Transport> make_nccl_transport(const uint8_t* uid, int C, int ra
   ncclUniqueId id;
   static_assert(sizeof(ncclUniqueId) <= UPIPE_UID_BYTES, "uid size");
   std::memcpy(&id, uid, sizeof(id));
+  // CTA cap: the all-to-all of the next chunk runs while the attention kernels hold
+  // one CTA per SM with all of its shared memory, so NCCL's CTAs cannot share SMs with them; an
+  // uncapped communicator could park many CTAs on SMs while it waits for a late peer. NVLink 5 needs
+  // only a few channels per peer for these message sizes (MBs), so cap them (UPIPE_NCCL_MAX_CTAS,
+  // default 16 of 148 SMs).
+  int max_ctas = 16;
+  if (const char* e = getenv("UPIPE_NCCL_MAX_CTAS")) max_ctas = atoi(e) > 0 ? atoi(e) : max_ctas;
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  cfg.blocking = 1;
+  cfg.maxCTAs = max_ctas;
+  cfg.minCTAs = max_ctas < 4 ? max_ctas : 4;
+  cfg.commName = "upipe";
   ncclComm_t comm = nullptr;
-  ncclResult_t r = ncclCommInitRank(&comm, C, id, rank);
+  ncclResult_t r = ncclCommInitRankConfig(&comm, C, id, rank, &cfg);
   if (r != ncclSuccess) {
-    err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+    err = std::string("ncclCommInitRankConfig: ") + ncclGetErrorString(r);
     return nullptr;
   }
-  return std::make_unique<NcclTransport>(comm, C, rank);
+  int n = 0, me = -1, dev = -1, ver = 0;
+  ncclCommCount(comm, &n);
+  ncclCommUserRank(comm, &me);
+  ncclCommCuDevice(comm, &dev);
+  ncclGetVersion(&ver);
+  if (!(getenv("UPIPE_QUIET") && getenv("UPIPE_QUIET")[0] == '1'))
+    fprintf(stderr, "[upipe] NCCL %d communicator: rank %d of %d on cuda:%d, max CTAs %d\n", ver, me, n, dev, max_ctas);
+  if (n != C || me != rank) {
+    err = "NCCL communicator does not match (cp_size, cp_rank)";
+    ncclCommDestroy(comm);
+    return nullptr;
+  }
+  return std::make_unique<NcclTransport>(comm, C, rank, max_ctas, dev);
 }
 
 std::unique_ptr<Transport> make_fabric_transport(upipe_fabric_t f, int rank, int device, std::string& err) {

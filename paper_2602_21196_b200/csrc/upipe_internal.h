@@ -81,7 +81,38 @@ class Transport {
   virtual upipe_status_t sendrecv(const void* send, int dst, void* recv, int src, size_t bytes, cudaStream_t s,
                                   std::string& err) = 0;
   virtual upipe_status_t allreduce_sum_f32(float* buf, size_t n, cudaStream_t s, std::string& err) = 0;
+  // Failure detection (upipe_wait): wait for `s` while checking the transport for asynchronous errors;
+  // on an error or after timeout_s (<= 0: none) the transport aborts its communicator (so this rank's
+  // collectives return instead of waiting for a dead peer forever) and reports UPIPE_ERR_COMM.
+  virtual upipe_status_t wait(cudaStream_t s, double timeout_s, std::string& err);
+  virtual int kind() const = 0;          // upipe_comm_info_t.transport
+  virtual int max_ctas() const { return 0; }
+  virtual int device() const { return -1; }
+
+  // ---- direct-to-peer (IpcTransport in ipc.cu). A transport with peer memory owns the
+  // layer's workspace (a symmetric region: every buffer at the same offset on every rank) and lets
+  // producers write straight into the owners' receive buffers between push_begin and push_end.
+  virtual char* workspace() { return nullptr; }            // non-null: the layer's workspace lives here
+  virtual size_t workspace_bytes() const { return 0; }
+  virtual bool peer_capable() const { return false; }
+  virtual void* peer_ptr(int p, const void* local) const { (void)p; (void)local; return nullptr; }
+  virtual uint32_t next_epoch() { return 0; }
+  virtual upipe_status_t signal_ready(uint32_t, int, int, cudaStream_t, std::string& err) { err = "no peer memory"; return UPIPE_ERR_STATE; }
+  virtual upipe_status_t wait_ready(uint32_t, int, cudaStream_t, std::string& err) { err = "no peer memory"; return UPIPE_ERR_STATE; }
+  virtual upipe_status_t signal_done(uint32_t, int, cudaStream_t, std::string& err) { err = "no peer memory"; return UPIPE_ERR_STATE; }
+  virtual upipe_status_t wait_done(uint32_t, int, int, cudaStream_t, std::string& err) { err = "no peer memory"; return UPIPE_ERR_STATE; }
+  // all group peers have reached this collective (their receive buffers are free) ...
+  virtual upipe_status_t push_begin(int, int, cudaStream_t, uint32_t*, std::string& err) { err = "no peer memory"; return UPIPE_ERR_STATE; }
+  // ... this rank's pushes are complete (signalled to each peer) and every peer's pushes have landed here
+  virtual upipe_status_t push_end(uint32_t, int, int, cudaStream_t, std::string& err) { err = "no peer memory"; return UPIPE_ERR_STATE; }
 };
+
+constexpr size_t kIpcFlagBytes = 64 * 1024;   // ready / done flags: 2 x 64 epoch slots x 64 ranks x 4 B
+constexpr uint32_t kIpcSlots = 64;
+size_t ipc_region_bytes(size_t ws_bytes, size_t scratch_bytes);
+std::unique_ptr<Transport> make_ipc_transport(int C, int rank, int device, size_t ws_bytes, size_t scratch_bytes,
+                                              uint8_t* handle_out, std::string& err);
+upipe_status_t ipc_connect(Transport* t, const uint8_t* handles, std::string& err);
 
 std::unique_ptr<Transport> make_self_transport();
 std::unique_ptr<Transport> make_nccl_transport(const uint8_t* uid, int C, int rank, std::string& err);
@@ -173,4 +204,5 @@ struct upipe_ctx_s {
   std::unique_ptr<upipe::Transport> transport;
   std::string last_error;
   bool alive = true;
+  bool ipc_pending = false;   // upipe_ipc_create done, upipe_ipc_connect not yet
 };

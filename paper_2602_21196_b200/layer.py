@@ -18,15 +18,21 @@ class UPipeAttention:
     def __init__(self, n_q_heads: int, n_kv_heads: int, head_dim: int, hidden: int, chunk_heads: int,
                  causal: bool = True, process_group=None, device=None, fabric=None, cp_rank: int | None = None,
                  cp_size: int | None = None, sync_comm: bool = False, naive_kv: bool = False,
-                 rope_base: float = 0.0, ring_degree: int = 1, deterministic: bool = False):
+                 rope_base: float = 0.0, ring_degree: int = 1, deterministic: bool = False,
+                 transport: str = "nccl", max_seq_local: int | None = None):
         """CP group: ``process_group`` (torch.distributed, one process per GPU, NCCL transport),
         or ``fabric`` + ``cp_rank`` + ``cp_size`` (single-process group driven by one host thread per rank),
         or neither (C = 1). ``sync_comm``: sequential schedule with one chunk buffer set (the
         paper's memory-minimal form); default overlaps the next chunk's all-to-all with the current
         chunk's attention on a side stream (two buffer sets). ``ring_degree`` r > 1: UPipe x Ring hybrid
         (DESIGN A27): Ulysses groups of C/r consecutive ranks, Ring Attention across the r groups.
-        ``deterministic``: bitwise-reproducible backward (dQ partials added in key-tile order; slower)."""
+        ``deterministic``: bitwise-reproducible backward (dQ partials added in key-tile order; slower).
+        ``transport="ipc"`` (with ``process_group`` and ``max_seq_local``): direct-to-peer all-to-alls over
+        CUDA IPC peer memory instead of NCCL; the handles are exchanged over the group (any
+        backend, gloo included), the library owns the symmetric workspace (sized for ``max_seq_local``)."""
         self.Hq, self.Hkv, self.d, self.D, self.U = n_q_heads, n_kv_heads, head_dim, hidden, chunk_heads
+        self.ipc = False
+        self.region_bytes = 0
         self.causal = int(causal)
         self.rope_base = float(rope_base)    # 0: no RoPE; else rotary base (Llama3: 500000), DESIGN A26
         self.ring = max(1, int(ring_degree))
@@ -38,6 +44,18 @@ class UPipeAttention:
             self.C = cp_size
             self.ctx = U.upipe_init_local(fabric, cp_rank, dev_index, self.flags)
             self.rank = cp_rank
+        elif process_group is not None and transport == "ipc":
+            import torch.distributed as dist
+            if max_seq_local is None:
+                raise ValueError("transport='ipc' needs max_seq_local (the symmetric region is sized once)")
+            self.C = dist.get_world_size(process_group)
+            self.rank = dist.get_rank(process_group)
+            self.ctx, h = U.upipe_ipc_create(self.C, self.rank, dev_index, self.flags, self.shape(max_seq_local))
+            handles = [None] * self.C
+            dist.all_gather_object(handles, h, group=process_group)
+            U.upipe_ipc_connect(self.ctx, handles)
+            self.ipc = True
+            self.region_bytes = U.upipe_ipc_region_size(self.C, self.shape(max_seq_local), self.flags)
         elif process_group is not None:
             import torch.distributed as dist
             self.C = dist.get_world_size(process_group)
@@ -74,7 +92,7 @@ class UPipeAttention:
         o_saved = torch.empty((S_l, self.Hq * self.d), dtype=torch.bfloat16, device=x.device)
         a = self.C // self.ring                  # Ulysses degree; lse covers the rank's heads over its group's tokens
         lse = torch.empty((self.Hq // a, S_l * a), dtype=torch.float32, device=x.device)
-        ws = self.workspace(S_l, 0)
+        ws = None if self.ipc else self.workspace(S_l, 0)     # IPC: the library's symmetric region
         U.upipe_attn_fwd(self.ctx, sh, x, wq, wk, wv, wo, y, o_saved, lse, ws, stream=stream)
         return y, (o_saved, lse)
 
@@ -87,10 +105,18 @@ class UPipeAttention:
         dwk = torch.empty(wk.shape, dtype=torch.float32, device=x.device)
         dwv = torch.empty(wv.shape, dtype=torch.float32, device=x.device)
         dwo = torch.empty(wo.shape, dtype=torch.float32, device=x.device)
-        ws = self.workspace(S_l, 1)
+        ws = None if self.ipc else self.workspace(S_l, 1)
         U.upipe_attn_bwd(self.ctx, sh, x, wq, wk, wv, wo, dy, o_saved, lse, dx, dwq, dwk, dwv, dwo, reduce_dw, ws,
                          stream=stream)
         return dx, dwq, dwk, dwv, dwo
+
+    def wait(self, timeout_s: float = 0.0, stream=None):
+        """Block until this rank's enqueued layer work is done, failing (UpipeError, communicator aborted)
+        on a communicator error or after ``timeout_s`` seconds without completion (a dead peer)."""
+        U.upipe_wait(self.ctx, stream, int(timeout_s * 1000))
+
+    def comm_info(self) -> dict:
+        return U.upipe_comm_info(self.ctx)
 
     def close(self):
         if self.ctx is not None:

@@ -16,6 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("UPIPE_LIB") or os.path.join(_HERE, "libupipe.so")   # UPIPE_LIB: dev override (kernel variants)
 
 UPIPE_UID_BYTES = 128
+UPIPE_IPC_HANDLE_BYTES = 128
 STATUS = {0: "UPIPE_OK", 1: "UPIPE_ERR_INVALID_ARG", 2: "UPIPE_ERR_UNSUPPORTED", 3: "UPIPE_ERR_CUDA",
           4: "UPIPE_ERR_COMM", 5: "UPIPE_ERR_WORKSPACE", 6: "UPIPE_ERR_STATE"}
 
@@ -35,6 +36,11 @@ class upipe_shape_t(ctypes.Structure):
 class upipe_stage_info_t(ctypes.Structure):
     _fields_ = [("n_stages", c_int32), ("qpd", c_int32), ("kv_res", c_int32), ("sigma", c_int32),
                 ("q0", c_int32), ("kv0", c_int32), ("kv_sent", c_int32)]
+
+
+class upipe_comm_info_t(ctypes.Structure):
+    _fields_ = [("nranks", c_int32), ("rank", c_int32), ("cuda_device", c_int32), ("transport", c_int32),
+                ("max_ctas", c_int32)]
 
 
 class upipe_probe_t(ctypes.Structure):
@@ -81,6 +87,12 @@ def lib() -> ctypes.CDLL:
             "upipe_set_trace": (st, [P, c_int]),
             "upipe_trace_read": (st, [P, POINTER(ctypes.c_double), POINTER(c_int64)]),
             "upipe_test_set_probe": (st, [P, POINTER(upipe_probe_t)]),
+            "upipe_wait": (st, [P, P, c_int64]),
+            "upipe_ipc_region_size": (st, [c_int, POINTER(upipe_shape_t), c_uint32, POINTER(c_size_t)]),
+            "upipe_ipc_create": (st, [POINTER(c_void_p), c_int, c_int, c_int, c_uint32, POINTER(upipe_shape_t),
+                                      POINTER(c_uint8)]),
+            "upipe_ipc_connect": (st, [P, POINTER(c_uint8)]),
+            "upipe_comm_info": (st, [P, POINTER(upipe_comm_info_t)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -94,7 +106,8 @@ EXPORTED = ("upipe_get_unique_id", "upipe_init", "upipe_fabric_create", "upipe_f
             "upipe_finalize", "upipe_status_string", "upipe_last_error", "upipe_workspace_size", "upipe_plan_stage",
             "upipe_validate", "upipe_attn_fwd", "upipe_attn_bwd", "upipe_attn_core_fwd", "upipe_attn_core_bwd", "upipe_core_bwd_sem_count",
             "upipe_rowdot", "upipe_gemm_xwT", "upipe_synth_fill_bf16", "upipe_kernel_launches", "upipe_set_trace",
-            "upipe_trace_read", "upipe_test_set_probe")
+            "upipe_trace_read", "upipe_test_set_probe", "upipe_wait", "upipe_comm_info",
+            "upipe_ipc_region_size", "upipe_ipc_create", "upipe_ipc_connect")
 
 TRACE_CATS = ("gemm", "attn_fwd", "attn_bwd", "comm", "aux")
 
@@ -160,6 +173,26 @@ def upipe_init_local(fabric, cp_rank: int, cuda_device: int, flags: int = 0) -> 
     return ctx
 
 
+def upipe_ipc_region_size(cp_size: int, max_shape: upipe_shape_t, flags: int = 0) -> int:
+    n = c_size_t()
+    _check(lib().upipe_ipc_region_size(cp_size, ctypes.byref(max_shape), flags, ctypes.byref(n)))
+    return n.value
+
+
+def upipe_ipc_create(cp_size: int, cp_rank: int, cuda_device: int, flags: int, max_shape: upipe_shape_t):
+    """Phase 1 of the direct-to-peer ctx: returns (ctx, this rank's IPC handle bytes)."""
+    ctx = c_void_p()
+    h = (c_uint8 * UPIPE_IPC_HANDLE_BYTES)()
+    _check(lib().upipe_ipc_create(ctypes.byref(ctx), cp_size, cp_rank, cuda_device, flags, ctypes.byref(max_shape), h))
+    return ctx, bytes(h)
+
+
+def upipe_ipc_connect(ctx, handles: list) -> None:
+    """Phase 2: handles of every rank, in rank order."""
+    buf = (c_uint8 * (UPIPE_IPC_HANDLE_BYTES * len(handles))).from_buffer_copy(b"".join(handles))
+    _check(lib().upipe_ipc_connect(ctx, buf), ctx)
+
+
 def upipe_finalize(ctx) -> None:
     _check(lib().upipe_finalize(ctx))
 
@@ -171,6 +204,20 @@ def upipe_status_string(st: int) -> str:
 def upipe_last_error(ctx=None) -> str:
     m = lib().upipe_last_error(ctx)
     return m.decode() if m else ""
+
+
+def upipe_wait(ctx, stream=None, timeout_ms: int = 0) -> None:
+    """Wait for `stream` with communicator error polling; raises UpipeError (UPIPE_ERR_COMM) on a
+    communicator error or timeout (the communicator is then aborted)."""
+    _check(lib().upipe_wait(ctx, _stream(stream), int(timeout_ms)), ctx)
+
+
+def upipe_comm_info(ctx) -> dict:
+    i = upipe_comm_info_t()
+    _check(lib().upipe_comm_info(ctx, ctypes.byref(i)), ctx)
+    return {"nranks": i.nranks, "rank": i.rank, "cuda_device": i.cuda_device,
+            "transport": {0: "none", 1: "nccl", 2: "fabric", 3: "ipc"}.get(i.transport, i.transport),
+            "max_ctas": i.max_ctas}
 
 
 # ------------------------------------------------------------------ planning
@@ -195,15 +242,21 @@ def upipe_validate(cp_size: int, shape: upipe_shape_t) -> tuple[int, str]:
 
 # ------------------------------------------------------------------ layer
 
+def _ws_bytes(workspace, ws_bytes):
+    if ws_bytes is not None:
+        return ws_bytes
+    return 0 if workspace is None else workspace.numel() * workspace.element_size()
+
+
 def upipe_attn_fwd(ctx, shape, x, wq, wk, wv, wo, y, o_saved, lse_saved, workspace, ws_bytes=None, stream=None):
-    wsb = workspace.numel() * workspace.element_size() if ws_bytes is None else ws_bytes
+    wsb = _ws_bytes(workspace, ws_bytes)
     _check(lib().upipe_attn_fwd(ctx, ctypes.byref(shape), _ptr(x), _ptr(wq), _ptr(wk), _ptr(wv), _ptr(wo), _ptr(y),
                                 _ptr(o_saved), _ptr(lse_saved), _ptr(workspace), wsb, _stream(stream)), ctx)
 
 
 def upipe_attn_bwd(ctx, shape, x, wq, wk, wv, wo, dy, o_saved, lse_saved, dx, dwq, dwk, dwv, dwo, reduce_dw,
                    workspace, ws_bytes=None, stream=None):
-    wsb = workspace.numel() * workspace.element_size() if ws_bytes is None else ws_bytes
+    wsb = _ws_bytes(workspace, ws_bytes)
     _check(lib().upipe_attn_bwd(ctx, ctypes.byref(shape), _ptr(x), _ptr(wq), _ptr(wk), _ptr(wv), _ptr(wo), _ptr(dy),
                                 _ptr(o_saved), _ptr(lse_saved), _ptr(dx), _ptr(dwq), _ptr(dwk), _ptr(dwv), _ptr(dwo),
                                 int(reduce_dw), _ptr(workspace), wsb, _stream(stream)), ctx)
