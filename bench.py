@@ -362,6 +362,28 @@ def main():
         "chunk_buffers_gib": main_run["chunk_bytes"] / 2**30,
         "clocks": clocks,
     }
+    if C > 1 and args.ring == 1:
+        # all-to-all volume of one fwd+bwd step on this rank (the plan's per-stage buffers; each rank keeps
+        # 1/C of every block), its event-timed duration on the comm stream, the bus bandwidth against
+        # NVLink 5's 900 GB/s per direction, and the share of that time hidden behind compute
+        qpd_, R_ = U // C, Hq // Hkv
+        kv_res = max(1, qpd_ // R_)
+        sigma = max(1, R_ // qpd_) if not args.naive_kv else 1
+        stages = Hq // U
+        qb = S_l * qpd_ * d * 2 * C                                  # one Q-sized chunk (all C blocks)
+        kb = S_l * kv_res * d * 2 * C
+        kv_events = stages // sigma
+        fwd_b = stages * 2 * qb + kv_events * 2 * kb                 # Q, O per stage; K, V per super-stage
+        bwd_b = stages * (3 * qb + S_l * qpd_ * 4 * C) + kv_events * 4 * kb   # Q, dO, dQ, delta; K, V, dK, dV
+        off_rank = (fwd_b + bwd_b) * (C - 1) / C
+        comm_ms = per_step_ms.get("comm", 0.0)
+        compute_ms = sum(v for k, v in per_step_ms.items() if k != "comm")
+        result["a2a"] = {"bytes_per_step_off_rank": off_rank, "ms_per_step": comm_ms,
+                         "bus_gbps": off_rank / (comm_ms / 1e3) / 1e9 if comm_ms > 0 else None, "peak_gbps": 900.0,
+                         "overlap_fraction": min(1.0, max(0.0, (compute_ms + comm_ms - ms_step) / comm_ms))
+                         if comm_ms > 0 else None,
+                         "note": "comm-stream event time includes waiting for peers; overlap = share of it "
+                                 "hidden behind the compute stream's kernels"}
     main_run["attn"].close()
 
     if not args.quick and not args.no_ulysses and U != Hq:

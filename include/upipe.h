@@ -105,6 +105,15 @@ typedef struct {
 #define UPIPE_FLAG_DETERMINISTIC 4u /* bitwise-reproducible backward: the attention backward
                                    adds the dQ partials of its key tiles in key-tile order (semaphores in
                                    the workspace) instead of in arrival order; slower */
+#define UPIPE_FLAG_DIRECT 8u    /* direct-to-peer all-to-alls (P:296 the a2a buffers set the
+                                   peak, "we only need buffers for 2 heads"): the producing kernels
+                                   write straight into the owners' receive buffers over peer memory -- Q/K/V
+                                   projection and dO projection epilogues (TMA stores), the attention
+                                   epilogue (O, dK, dV), the dQ conversion -- so no send buffers exist and no
+                                   copy or NCCL kernel moves the chunk; ordering by GPU front-end flags.
+                                   Needs a ctx from upipe_ipc_create/connect, C <= 8, ring_degree 1; one
+                                   buffer set (the transfers overlap inside the kernels, not on a side
+                                   stream). Ignored at C = 1. */
 
 /* ---------------------------------------------------------------- lifecycle */
 
@@ -173,7 +182,9 @@ UPIPE_API upipe_status_t upipe_comm_info(upipe_ctx_t ctx, upipe_comm_info_t* inf
  * default schedule (C > 1: the next stage's all-to-all overlaps the current attention on the
  * ctx's comm stream, which needs a second chunk buffer set, DESIGN A23); pass 2: forward,
  * 3: backward for a ctx created with UPIPE_FLAG_SYNC_COMM (one buffer set, the paper's
- * memory-minimal schedule). At C = 1 all-to-alls are identities and 0 == 2, 1 == 3. */
+ * memory-minimal schedule). At C = 1 all-to-alls are identities and 0 == 2, 1 == 3.
+ * 4 / 5: forward / backward with UPIPE_FLAG_DIRECT (receive buffers only, one set; an IPC ctx holds
+ * it in its symmetric region, see upipe_ipc_region_size). */
 UPIPE_API upipe_status_t upipe_workspace_size(int cp_size, const upipe_shape_t* shape, int pass, size_t* bytes);
 
 /* Stage plan of the GQA schedule (A8): for stage s and device p the
@@ -227,8 +238,9 @@ UPIPE_API upipe_status_t upipe_attn_core_fwd(const upipe_bf16* q, const upipe_bf
                                    float* lse, int64_t S, int nq, int nkv, int d, int causal, int64_t ldq,
                                    int64_t ldkv, int64_t ldo, int64_t ld_lse, void* stream);
 /* Attention core backward (B4): dq_acc fp32 is ACCUMULATED into (zero it first) with dQ = (1/sqrt(d)) dS K;
- * layout [S][nq][d] (token-major), or with UPIPE_CORE_DQ_DIM_MAJOR [nq*d][S]
- * (dims-major, row stride S: the layer's layout for the 64-query kernel at d = 128);
+ * layout [S][nq][d] (token-major), or with UPIPE_CORE_DQ_DIM_MAJOR [nq*d][S4]
+ * (dims-major, row stride S4 = S rounded up to a multiple of 4 floats (TMA strides are 16-byte
+ * multiples): the layer's layout for the 64-query kernel at d = 128);
  * dk_acc/dv_acc fp32 [S][nkv][d] are written (UPIPE_CORE_ACCUMULATE: added to their contents);
  * delta [S][nq] (stride ld_delta) = rowsum(dO*O) in fp32.
  * flags: UPIPE_CORE_ACCUMULATE | UPIPE_CORE_DQ_DIM_MAJOR (d = 128 only) | UPIPE_CORE_DETERMINISTIC

@@ -58,7 +58,19 @@ struct BwdArgs {
   int head_inner;    // visiting order (head, query tile): 1 = heads inner, so every CTA of the launch is at
                      // the same query tile at the same step (needed by dq_sem, whose waits then chain in lockstep)
   long long* dbg;    // optional per-role cycle breakdown of CTA (0,0) (UPIPE_BWD_TIMELINE=1)
+  // N2 (nkvseg > 0): bf16 dK / dV row t -> {dk,dv}seg[t / kvseg_rows] + (t % kvseg_rows) * ld_kvb (a peer's
+  // receive block) instead of dk_bf16 / dv_bf16
+  __nv_bfloat16* dkseg[kMaxSeg];
+  __nv_bfloat16* dvseg[kMaxSeg];
+  long long kvseg_rows;
+  int nkvseg;
 };
+
+// Destination row of the bf16 dK / dV epilogue (plain or N2 segmented); key < S.
+__device__ __forceinline__ __nv_bfloat16* kv_out_row(const BwdArgs& a, int which, long long key) {
+  if (a.nkvseg) return (which ? a.dkseg : a.dvseg)[key / a.kvseg_rows] + (key % a.kvseg_rows) * a.ld_kvb;
+  return (which ? a.dk_bf16 : a.dv_bf16) + key * a.ld_kvb;
+}
 
 __device__ __forceinline__ float ex2b(float x) {
   float y;
@@ -97,7 +109,9 @@ struct BwdCfg {
 template <bool TL>
 __device__ __forceinline__ long long tick() { if constexpr (TL) return clock64(); else return 0; }
 
-template <int D, bool TL>
+// DET (UPIPE_FLAG_DETERMINISTIC): heads-inner lockstep order and the dQ semaphores; compiled out of the
+// default variant (measured: carrying them as runtime branches cost the q64 kernel ~20 %).
+template <int D, bool TL, bool DET = false>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -133,8 +147,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kSoftmax = kSoftmaxWarps * 32;
   // visiting order: heads outer, query tiles up from the diagonal (default), or heads inner and query
   // tiles down to the diagonal (a.head_inner: all CTAs of the launch in lockstep, for dq_sem)
-  auto tile_h = [&](int n) { return g * G + (a.head_inner ? n % G : n / n_qt); };
-  auto tile_qt = [&](int n) { return a.head_inner ? nT - 1 - n / G : qt_begin + n % n_qt; };
+  auto tile_h = [&](int n) { return g * G + (DET ? n % G : n / n_qt); };
+  auto tile_qt = [&](int n) { return DET ? nT - 1 - n / G : qt_begin + n % n_qt; };
 
   if (warp == kTmaWarp && lane == 0) {
     tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
@@ -406,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tcol = which ? C::TM_DK : C::TM_DV;
     const float sc = which ? a.scale : 1.f;
     float* acc = (which ? a.dk_acc : a.dv_acc);
-    __nv_bfloat16* ob = which ? a.dk_bf16 : a.dv_bf16;
+    const bool ob = a.nkvseg ? true : (which ? a.dk_bf16 : a.dv_bf16) != nullptr;
 #pragma unroll 1
     for (int c = cbeg; c < cbeg + D; c += 32) {
       uint32_t rr[32];
@@ -430,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (ob) {
         if (which && a.rope.hi) rope_rotate<16>(v, a.rope.hi, a.rope.lo, D, a.rope.pos0 + key, c, -1.f);
-        uint4* dst = reinterpret_cast<uint4*>(ob + key * a.ld_kvb + (long long)g * D + c);
+        uint4* dst = reinterpret_cast<uint4*>(kv_out_row(a, which, key) + (long long)g * D + c);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           dst[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
@@ -452,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int n = 0; n < N; ++n) {
       const int h = tile_h(n);
       const int q0 = tile_qt(n) * 128;
-      int* const sem = a.dq_sem ? a.dq_sem + (long long)h * nT + q0 / 128 : nullptr;
+      int* const sem = DET ? a.dq_sem + (long long)h * nT + q0 / 128 : nullptr;
       long long c0 = tick<TL>();
       if (quad == 0) mbar_wait(dq_full, n & 1);   // one polling warp, the others wait in bar.sync
       named_bar_sync(2, 128);
@@ -539,7 +553,7 @@ struct Q64Cfg {
   static constexpr uint32_t TM_S0 = 0, TM_DP0 = 64, TM_S1 = 128, TM_DP1 = 192, TM_DV = 256, TM_DK = 384;
 };
 
-template <bool TL>
+template <bool TL, bool DET = false>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_q64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -574,8 +588,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // reduce their dQ partials into the same rows of dq_acc (L2 hits) instead of each starting at its own
   // diagonal and sweeping a different region (measured: the dQ reduce-adds dominated the energy).
   // Heads of the KV group outer (default) or inner (a.head_inner).
-  auto tile_h = [&](int n) { return g * G + (a.head_inner ? n % G : n / n_qt); };
-  auto tile_qt = [&](int n) { return nT64 - 1 - (a.head_inner ? n / G : n % n_qt); };
+  auto tile_h = [&](int n) { return g * G + (DET ? n % G : n / n_qt); };
+  auto tile_qt = [&](int n) { return nT64 - 1 - (DET ? n / G : n % n_qt); };
   constexpr int kWg = 128;
 
   if (warp == kTmaWarp && lane == 0) {
@@ -805,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tcol = which ? C::TM_DK : C::TM_DV;
     const float sc = which ? a.scale : 1.f;
     float* acc = (which ? a.dk_acc : a.dv_acc);
-    __nv_bfloat16* ob = which ? a.dk_bf16 : a.dv_bf16;
+    const bool ob = a.nkvseg ? true : (which ? a.dk_bf16 : a.dv_bf16) != nullptr;
 #pragma unroll 1
     for (int c = 0; c < D; c += 32) {
       uint32_t rr[32];
@@ -829,7 +843,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (ob) {
         if (which && a.rope.hi) rope_rotate<16>(v, a.rope.hi, a.rope.lo, D, a.rope.pos0 + key, c, -1.f);
-        uint4* dst = reinterpret_cast<uint4*>(ob + key * a.ld_kvb + (long long)g * D + c);
+        uint4* dst = reinterpret_cast<uint4*>(kv_out_row(a, which, key) + (long long)g * D + c);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
           dst[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
@@ -849,7 +863,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int x = n & 1;
       const int h = tile_h(n);
       const int q0 = tile_qt(n) * 64;
-      int* const sem = a.dq_sem ? a.dq_sem + ((long long)h * nT64 + q0 / 64) * 4 + quad : nullptr;
+      int* const sem = DET ? a.dq_sem + ((long long)h * nT64 + q0 / 64) * 4 + quad : nullptr;
       // Deterministic dQ: key tile jb adds after key tiles 0..jb-1 (every earlier key tile contributes to
       // every query tile this CTA visits); the release of step n waits for its reduce to COMPLETE, which is
       // done one step later (wait_group 1) so the drain never idles on its own reduce.
@@ -974,6 +988,17 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   a.dv_acc = p.dv_acc;
   a.dk_bf16 = reinterpret_cast<__nv_bfloat16*>(p.dk_bf16);
   a.dv_bf16 = reinterpret_cast<__nv_bfloat16*>(p.dv_bf16);
+  a.nkvseg = p.dk_seg.n;
+  a.kvseg_rows = p.dk_seg.rows > 0 ? p.dk_seg.rows : 1;
+  for (int i = 0; i < kMaxSeg; ++i) {
+    a.dkseg[i] = reinterpret_cast<__nv_bfloat16*>(p.dk_seg.p[i]);
+    a.dvseg[i] = reinterpret_cast<__nv_bfloat16*>(p.dv_seg.p[i]);
+  }
+  if (a.nkvseg && (p.dv_seg.n != p.dk_seg.n || p.dv_seg.rows != p.dk_seg.rows || p.dk_seg.rows <= 0 ||
+                   p.dk_seg.n > kMaxSeg || (p.S + p.dk_seg.rows - 1) / p.dk_seg.rows > p.dk_seg.n)) {
+    snprintf(err, errlen, "attn_bwd: segmented dK/dV need matching segments covering S");
+    return cudaErrorInvalidValue;
+  }
   a.S = p.S;
   a.ld_lse = p.ld_lse;
   a.ld_delta = p.ld_delta;
@@ -988,12 +1013,7 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   a.rope = p.rope;
   a.dq_dim_major = 0;
   a.dq_sem = p.dq_sem;
-  // deterministic dQ needs the lockstep order; UPIPE_BWD_HEAD_INNER=1 selects it otherwise too (A/B)
-  static const bool head_inner_env = [] {
-    const char* v = getenv("UPIPE_BWD_HEAD_INNER");
-    return v && v[0] == '1';
-  }();
-  a.head_inner = (p.dq_sem || head_inner_env) ? 1 : 0;
+  a.head_inner = p.dq_sem ? 1 : 0;   // the deterministic variant's lockstep order (DET template)
   // UPIPE_BWD_TIMELINE=1: per-role cycle breakdown of CTA (0,0), printed to stderr after the launch
   static long long* dbg_dev = nullptr;
   const char* tlenv = getenv("UPIPE_BWD_TIMELINE");
@@ -1023,11 +1043,14 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
                                  errlen)) {
       return cudaErrorInvalidValue;
     }
-    const cudaError_t attr = set_smem_attr((const void*)attn_bwd_q64_kernel<false>, Q64Cfg::SMEM);
+    const cudaError_t attr = set_smem_attr((const void*)attn_bwd_q64_kernel<false>, Q64Cfg::SMEM) == cudaSuccess
+                                 ? set_smem_attr((const void*)attn_bwd_q64_kernel<false, true>, Q64Cfg::SMEM)
+                                 : cudaErrorInvalidValue;
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd_q64 attr: %s", cudaGetErrorString(attr)); return attr; }
     const cudaError_t attr2 = set_smem_attr((const void*)attn_bwd_q64_kernel<true>, Q64Cfg::SMEM);
     if (attr2 != cudaSuccess) { snprintf(err, errlen, "attn_bwd_q64 attr: %s", cudaGetErrorString(attr2)); return attr2; }
     if (a.dbg) attn_bwd_q64_kernel<true><<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
+    else if (a.dq_sem) attn_bwd_q64_kernel<false, true><<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
     else attn_bwd_q64_kernel<false><<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
     count_launches(1);
     e = cudaGetLastError();
@@ -1045,17 +1068,23 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
     return e;
   }
   if (p.d == 128) {
-    const cudaError_t attr = set_smem_attr((const void*)attn_bwd_kernel<128, false>, BwdCfg<128>::SMEM);
+    const cudaError_t attr = set_smem_attr((const void*)attn_bwd_kernel<128, false>, BwdCfg<128>::SMEM) == cudaSuccess
+                                 ? set_smem_attr((const void*)attn_bwd_kernel<128, false, true>, BwdCfg<128>::SMEM)
+                                 : cudaErrorInvalidValue;
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
     const cudaError_t attr2 = set_smem_attr((const void*)attn_bwd_kernel<128, true>, BwdCfg<128>::SMEM);
     if (attr2 != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr2)); return attr2; }
     if (a.dbg) attn_bwd_kernel<128, true><<<grid, kThreads, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
+    else if (a.dq_sem) attn_bwd_kernel<128, false, true><<<grid, kThreads, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
     else attn_bwd_kernel<128, false><<<grid, kThreads, BwdCfg<128>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
     count_launches(1);
   } else {
-    const cudaError_t attr = set_smem_attr((const void*)attn_bwd_kernel<64, false>, BwdCfg<64>::SMEM);
+    const cudaError_t attr = set_smem_attr((const void*)attn_bwd_kernel<64, false>, BwdCfg<64>::SMEM) == cudaSuccess
+                                 ? set_smem_attr((const void*)attn_bwd_kernel<64, false, true>, BwdCfg<64>::SMEM)
+                                 : cudaErrorInvalidValue;
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd attr: %s", cudaGetErrorString(attr)); return attr; }
-    attn_bwd_kernel<64, false><<<grid, kThreads, BwdCfg<64>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
+    if (a.dq_sem) attn_bwd_kernel<64, false, true><<<grid, kThreads, BwdCfg<64>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
+    else attn_bwd_kernel<64, false><<<grid, kThreads, BwdCfg<64>::SMEM, stream>>>(tq, tk, tv, tdo, tdq, a);
     count_launches(1);
   }
   e = cudaGetLastError();

@@ -37,6 +37,9 @@ struct FwdArgs {
   int nq, nkv, causal, n_pairs;
   float scale_log2;  // log2(e) / sqrt(d)
   long long* dbg;    // UPIPE_FWD_TIMELINE=1: per-role cycle totals of CTA (0, 0)
+  __nv_bfloat16* oseg[kMaxSeg];   // N2 (noseg > 0): row q of O -> oseg[q / oseg_rows] + (q % oseg_rows) * ldo
+  long long oseg_rows;
+  int noseg;
 };
 
 // Cycle counters of the per-role timeline; compiled out unless the timeline variant is launched.
@@ -360,7 +363,8 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     const float inv = 1.f / l_run;
     const bool valid = q < a.S;
-    __nv_bfloat16* orow = a.o + q * a.ldo + (long long)head * D;
+    __nv_bfloat16* orow = (a.noseg ? a.oseg[valid ? q / a.oseg_rows : 0] + (q % a.oseg_rows) * a.ldo : a.o + q * a.ldo) +
+                          (long long)head * D;   // N2: straight into the owner rank's O receive block
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       uint32_t r[32];
@@ -407,6 +411,13 @@ cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err
   if (!make_tmap_3d(&tv, p.v, p.d, p.nkv, p.S, p.d, p.ldkv, 64, 1, 128, err, errlen)) return cudaErrorInvalidValue;
   FwdArgs a;
   a.o = reinterpret_cast<__nv_bfloat16*>(p.o);
+  a.noseg = p.o_seg.n;
+  a.oseg_rows = p.o_seg.rows > 0 ? p.o_seg.rows : 1;
+  for (int i = 0; i < kMaxSeg; ++i) a.oseg[i] = reinterpret_cast<__nv_bfloat16*>(p.o_seg.p[i]);
+  if (a.noseg && (p.o32 || p.o_seg.rows <= 0 || p.o_seg.n > kMaxSeg || (p.S + p.o_seg.rows - 1) / p.o_seg.rows > p.o_seg.n)) {
+    snprintf(err, errlen, "attn_fwd: segmented O needs bf16 output and segments covering S");
+    return cudaErrorInvalidValue;
+  }
   a.o32 = p.o32;
   a.lse = p.lse;
   a.S = p.S;

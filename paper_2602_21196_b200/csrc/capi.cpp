@@ -146,8 +146,8 @@ namespace {
 void ipc_sizes(int C, const upipe_shape_t& sh, uint32_t flags, size_t* ws, size_t* scratch) {
   Plan P = make_plan(C, sh);
   P.naive = (flags & UPIPE_FLAG_NAIVE_KV) != 0;
-  const bool ov = overlap_enabled(flags, P);
-  *ws = std::max(fwd_workspace(P, ov).total, bwd_workspace(P, ov).total);
+  const bool ov = overlap_enabled(flags, P), dir = direct_enabled(flags, P);
+  *ws = std::max(fwd_workspace(P, ov, dir).total, bwd_workspace(P, ov, dir).total);
   const size_t hq = (size_t)sh.n_q_heads * sh.head_dim, hkv = (size_t)sh.n_kv_heads * sh.head_dim;
   *scratch = std::max(hq, hkv) * (size_t)sh.hidden * 4;
 }
@@ -241,10 +241,11 @@ upipe_status_t upipe_workspace_size(int cp_size, const upipe_shape_t* shape, int
   std::string m;
   upipe_status_t st = validate_shape(cp_size, shape, m);
   if (st != UPIPE_OK) return set_err(nullptr, st, m);
-  if (!bytes || pass < 0 || pass > 3) return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "pass must be 0..3");
+  if (!bytes || pass < 0 || pass > 5) return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "pass must be 0..5");
   const Plan P = make_plan(cp_size, *shape);
   const bool ov = pass < 2 && P.C > 1 && P.ring == 1;   // 0/1: default (overlapped for C > 1); 2/3: sequential
-  *bytes = (pass & 1) == 0 ? fwd_workspace(P, ov).total : bwd_workspace(P, ov).total;
+  const bool dir = pass >= 4 && direct_enabled(UPIPE_FLAG_DIRECT, P);   // 4/5: UPIPE_FLAG_DIRECT
+  *bytes = (pass & 1) == 0 ? fwd_workspace(P, ov, dir).total : bwd_workspace(P, ov, dir).total;
   return UPIPE_OK;
 }
 
@@ -279,7 +280,7 @@ upipe_status_t upipe_attn_fwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "tensors must be 16-byte aligned, workspace 256-byte aligned");
   Plan P = make_plan(ctx->C, *shape);
   P.naive = (ctx->flags & UPIPE_FLAG_NAIVE_KV) != 0;
-  if (ws_bytes < fwd_workspace(P, overlap_enabled(ctx->flags, P)).total)
+  if (ws_bytes < fwd_workspace(P, overlap_enabled(ctx->flags, P), direct_enabled(ctx->flags, P)).total)
     return set_err(ctx, UPIPE_ERR_WORKSPACE, "ws_bytes < upipe_workspace_size(pass=0, or 2 with UPIPE_FLAG_SYNC_COMM)");
   cudaSetDevice(ctx->device);
   return layer_fwd(ctx, P, x, wq, wk, wv, wo, y, o_saved, lse_saved, static_cast<char*>(workspace),
@@ -302,7 +303,7 @@ upipe_status_t upipe_attn_bwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "tensors must be 16-byte aligned, workspace 256-byte aligned");
   Plan P = make_plan(ctx->C, *shape);
   P.naive = (ctx->flags & UPIPE_FLAG_NAIVE_KV) != 0;
-  if (ws_bytes < bwd_workspace(P, overlap_enabled(ctx->flags, P)).total)
+  if (ws_bytes < bwd_workspace(P, overlap_enabled(ctx->flags, P), direct_enabled(ctx->flags, P)).total)
     return set_err(ctx, UPIPE_ERR_WORKSPACE, "ws_bytes < upipe_workspace_size(pass=1, or 3 with UPIPE_FLAG_SYNC_COMM)");
   cudaSetDevice(ctx->device);
   return layer_bwd(ctx, P, x, wq, wk, wv, wo, dy, o_saved, lse_saved, dx, dwq, dwk, dwv, dwo, reduce_dw,
@@ -340,7 +341,7 @@ upipe_status_t upipe_attn_core_bwd(const upipe_bf16* q, const upipe_bf16* k, con
   p.kv_write_acc = 1;
   if (flags & UPIPE_CORE_DQ_DIM_MAJOR) {
     p.dq_dim_major = 1;
-    p.ld_dqt = S;
+    p.ld_dqt = (S + 3) & ~int64_t(3);   // TMA: 16-byte row stride
     if (!attn_bwd_dq_dim_major(p))
       return set_err(nullptr, UPIPE_ERR_UNSUPPORTED, "attn_core_bwd: dim-major dQ needs the 64-query kernel (d = 128)");
   }

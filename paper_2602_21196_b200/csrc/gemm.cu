@@ -11,6 +11,7 @@
 // all-to-all: the projection epilogue writes the send buffer directly.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -35,6 +36,16 @@ struct DevOut {
   RopeRef rope;
 };
 constexpr int kMaxParts = 3;
+struct DevDot {              // RowDot (kernels.h): fused delta of the dO projection, part 0
+  const __nv_bfloat16* o;    // null: off
+  long long ld_o, col0, col_stride, dst_stride;
+  float* dst[kMaxSeg];
+  int ld_dst, d;
+};
+// N2 direct-to-peer bf16 stores of part 0: one 2-D map per destination segment ({col, row}, 64 x 32 boxes)
+struct SegMaps {
+  CUtensorMap m[kMaxSeg];
+};
 struct GemmArgs {
   int M, N, K;
   float alpha;
@@ -48,6 +59,9 @@ struct GemmArgs {
   int mcum[kMaxParts + 1];   // M-concat: first row of each part (multiples of BM)
   DevOpMap a[kMaxParts], b[kMaxParts];
   DevOut c[kMaxParts];
+  DevDot dot;
+  __nv_bfloat16* segp[kMaxSeg];   // N2: part 0's bf16 output segment bases (nsegp > 0), see OutMap::seg
+  int nsegp;
 };
 
 constexpr int BM = 128;
@@ -74,7 +88,7 @@ __global__ void __launch_bounds__(192, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB0,
                 const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
-                const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ SegMaps tmSeg, const GemmArgs g) {
   // Grouped forms (GemmGroup): K-concatenation sums the products of up to three (A, B) pairs
   // into one accumulator (one epilogue pass); M-concatenation stacks up to three A operands
   // (own output maps) against one B. The part of a k-block / tile selects the tensor maps.
@@ -355,7 +369,9 @@ __global__ void __launch_bounds__(192, 1)
       if (g.c_tma == 2 && pc == 0) {
         // bf16 store through shared memory: each warp stages its 32 rows x 64 columns (128B swizzle,
         // two 4 KB slots) and issues one TMA store per box into the output's 3-D view {col, row, segment}
-        // (full-line writes instead of 32 rows x 16 bytes per store instruction)
+        // (full-line writes instead of 32 rows x 16 bytes per store instruction). N2: one 2-D map per
+        // destination segment (a peer's receive block). RowDot: delta of each head from the rounded values.
+        float dot_acc = 0.f;
 #pragma unroll 1
         for (int c64 = 0; c64 < BN / 64; ++c64) {
           const int n = n0 + c64 * 64;
@@ -372,6 +388,20 @@ __global__ void __launch_bounds__(192, 1)
             rope_rotate<16>(v, oc_.rope.hi, oc_.rope.lo, oc_.rope.d, oc_.rope.pos0 + m, n % oc_.rope.d, 1.f);
             rope_rotate<16>(v + 32, oc_.rope.hi, oc_.rope.lo, oc_.rope.d, oc_.rope.pos0 + m, (n + 32) % oc_.rope.d, 1.f);
           }
+          if (g.dot.o) {
+            const long long seg = n / oc_.n_len, nin = n % oc_.n_len;
+            if (mvalid) {
+              const uint4* orow = reinterpret_cast<const uint4*>(g.dot.o + (long long)ml * g.dot.ld_o + g.dot.col0 +
+                                                                 seg * g.dot.col_stride + nin);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) dot_acc += dot8_rounded(v + 8 * j, orow[j]);
+            }
+            if ((nin + 64) % g.dot.d == 0) {              // the head's last 64 columns
+              float* dd = g.dot.dst_stride ? g.dot.dst[0] + seg * g.dot.dst_stride : g.dot.dst[seg];
+              if (mvalid) dd[(long long)ml * g.dot.ld_dst + nin / g.dot.d] = dot_acc;
+              dot_acc = 0.f;
+            }
+          }
           const uint32_t slot = smem_u32(smem + C::STG + quad * 8192 + (c64 & 1) * 4096);
           if (lane == 0) bulk_wait_read1();             // the store that last used this slot has read it
           __syncwarp();
@@ -384,7 +414,8 @@ __global__ void __launch_bounds__(192, 1)
           __syncwarp();
           if (lane == 0) {
             const long long seg = n / oc_.n_len, nin = n % oc_.n_len;
-            tma_store_3d(&tmC, smem + C::STG + quad * 8192 + (c64 & 1) * 4096, (int)nin, m0 + quad * 32, (int)seg);
+            if (g.nsegp) tma_store_2d(&tmSeg.m[seg], smem + C::STG + quad * 8192 + (c64 & 1) * 4096, (int)nin, m0 + quad * 32);
+            else tma_store_3d(&tmC, smem + C::STG + quad * 8192 + (c64 & 1) * 4096, (int)nin, m0 + quad * 32, (int)seg);
             bulk_commit();
           }
         }
@@ -393,6 +424,7 @@ __global__ void __launch_bounds__(192, 1)
         else mbar_arrive(&acc_empty[ab]);
         continue;
       }
+      float dot_acc = 0.f;
 #pragma unroll 1
       for (int c32 = 0; c32 < BN / 32; ++c32) {
         uint32_t r[32];
@@ -433,7 +465,19 @@ __global__ void __launch_bounds__(192, 1)
         if (oc_.epi == (int)Epi::kStoreBF16) {
           // RoPE on the projected Q/K (row m = token pos0 + m, columns n.. = head dims n % d..)
           if (oc_.rope.hi) rope_rotate<16>(v, oc_.rope.hi, oc_.rope.lo, oc_.rope.d, oc_.rope.pos0 + m, n % oc_.rope.d, 1.f);
-          uint4* dst = reinterpret_cast<uint4*>(oc_.bf16 + orow * oc_.ld_bf16 + ocol);
+          if (pc == 0 && g.dot.o) {                       // fused row-dot (see the TMA path)
+            const uint4* orw = reinterpret_cast<const uint4*>(g.dot.o + (long long)ml * g.dot.ld_o + g.dot.col0 +
+                                                              nseg * g.dot.col_stride + nin);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dot_acc += dot8_rounded(v + 8 * j, orw[j]);
+            if ((nin + 32) % g.dot.d == 0) {
+              float* dd = g.dot.dst_stride ? g.dot.dst[0] + nseg * g.dot.dst_stride : g.dot.dst[nseg];
+              dd[(long long)ml * g.dot.ld_dst + nin / g.dot.d] = dot_acc;
+              dot_acc = 0.f;
+            }
+          }
+          uint4* dst = reinterpret_cast<uint4*>(pc == 0 && g.nsegp ? g.segp[nseg] + (long long)ml * oc_.ld_bf16 + nin
+                                                                     : oc_.bf16 + orow * oc_.ld_bf16 + ocol);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             dst[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
@@ -481,8 +525,8 @@ DevOpMap to_dev(const OperandMap& m) {
 }
 
 template <int BN, bool A_MN, bool B_MN, int CL, bool PAIR>
-cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorMap* tc, const GemmArgs& args,
-                   cudaStream_t s) {
+cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorMap* tc, const SegMaps& sm,
+                   const GemmArgs& args, cudaStream_t s) {
   using C = Cfg<BN, PAIR>;
   auto kern = gemm_kernel<BN, A_MN, B_MN, CL, PAIR>;
   const cudaError_t attr = set_smem_attr((const void*)kern, C::SMEM);
@@ -532,7 +576,7 @@ cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorM
   }
   const int clusters = units < max_clusters ? units : max_clusters;
   cfg.gridDim = dim3(CL * clusters);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], *tc, args);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], *tc, sm, args);
   count_launches(1);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -540,27 +584,27 @@ cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorM
 
 template <int BN, int CL, bool PAIR = false>
 cudaError_t dispatch_cl(bool amn, bool bmn, const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorMap* tc,
-                        const GemmArgs& a, cudaStream_t s) {
-  if (!amn && !bmn) return launch<BN, false, false, CL, PAIR>(ta, tb, tc, a, s);
-  if (!amn && bmn) return launch<BN, false, true, CL, PAIR>(ta, tb, tc, a, s);
-  if (amn && !bmn) return launch<BN, true, false, CL, PAIR>(ta, tb, tc, a, s);
-  return launch<BN, true, true, CL, PAIR>(ta, tb, tc, a, s);
+                        const SegMaps& sm, const GemmArgs& a, cudaStream_t s) {
+  if (!amn && !bmn) return launch<BN, false, false, CL, PAIR>(ta, tb, tc, sm, a, s);
+  if (!amn && bmn) return launch<BN, false, true, CL, PAIR>(ta, tb, tc, sm, a, s);
+  if (amn && !bmn) return launch<BN, true, false, CL, PAIR>(ta, tb, tc, sm, a, s);
+  return launch<BN, true, true, CL, PAIR>(ta, tb, tc, sm, a, s);
 }
 
 template <int BN>
 cudaError_t dispatch_major(bool amn, bool bmn, int cl, const CUtensorMap* ta, const CUtensorMap* tb,
-                           const CUtensorMap* tc, const GemmArgs& a, cudaStream_t s) {
+                           const CUtensorMap* tc, const SegMaps& sm, const GemmArgs& a, cudaStream_t s) {
   if constexpr (BN == 512) {
-    return dispatch_cl<BN, 2, true>(amn, bmn, ta, tb, tc, a, s);
+    return dispatch_cl<BN, 2, true>(amn, bmn, ta, tb, tc, sm, a, s);
   } else if constexpr (BN >= 128) {
-    if (cl == -2) return dispatch_cl<BN, 2, true>(amn, bmn, ta, tb, tc, a, s);
+    if (cl == -2) return dispatch_cl<BN, 2, true>(amn, bmn, ta, tb, tc, sm, a, s);
     if constexpr (BN == 256)
-      if (cl == -4) return dispatch_cl<BN, 4, true>(amn, bmn, ta, tb, tc, a, s);
-    if (cl == 4) return dispatch_cl<BN, 4>(amn, bmn, ta, tb, tc, a, s);
-    if (cl == 2) return dispatch_cl<BN, 2>(amn, bmn, ta, tb, tc, a, s);
-    return dispatch_cl<BN, 1>(amn, bmn, ta, tb, tc, a, s);
+      if (cl == -4) return dispatch_cl<BN, 4, true>(amn, bmn, ta, tb, tc, sm, a, s);
+    if (cl == 4) return dispatch_cl<BN, 4>(amn, bmn, ta, tb, tc, sm, a, s);
+    if (cl == 2) return dispatch_cl<BN, 2>(amn, bmn, ta, tb, tc, sm, a, s);
+    return dispatch_cl<BN, 1>(amn, bmn, ta, tb, tc, sm, a, s);
   } else {
-    return dispatch_cl<BN, 1>(amn, bmn, ta, tb, tc, a, s);
+    return dispatch_cl<BN, 1>(amn, bmn, ta, tb, tc, sm, a, s);
   }
 }
 
@@ -741,22 +785,74 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
                              c0.c_nstride == 0 && c0.c_mstride == 0;
     const int64_t nlen = c0.n_len < p0.N ? c0.n_len : p0.N;
     const int64_t nseg = (p0.N + nlen - 1) / nlen;
+    const bool segd = c0.seg.n > 0;           // N2: per-segment destinations (peers' receive blocks)
     if (tma_epi_env && tma_bf16_env && !args.c_tma && kind == GemmGroup::kKConcat && c0.epi == Epi::kStoreBF16 &&
-        seg_rows_ok && c0.out_bf16 && (reinterpret_cast<uintptr_t>(c0.out_bf16) & 15) == 0 && c0.ld_bf16 % 8 == 0 &&
-        nlen % 64 == 0 && (nseg == 1 || c0.r_nstride >= M)) {
-      const int64_t s2 = nseg > 1 ? c0.r_nstride * c0.ld_bf16 : (int64_t)M * c0.ld_bf16;
-      if (!make_tmap_3d(&tc, c0.out_bf16, (uint64_t)nlen, (uint64_t)M, (uint64_t)nseg, (uint64_t)c0.ld_bf16,
-                        (uint64_t)s2, 64, 32, 1, err, errlen))
-        return cudaErrorInvalidValue;
+        seg_rows_ok && (segd || (c0.out_bf16 && (reinterpret_cast<uintptr_t>(c0.out_bf16) & 15) == 0)) &&
+        c0.ld_bf16 % 8 == 0 && nlen % 64 == 0 && (segd || nseg == 1 || c0.r_nstride >= M)) {
+      if (!segd) {
+        const int64_t s2 = nseg > 1 ? c0.r_nstride * c0.ld_bf16 : (int64_t)M * c0.ld_bf16;
+        if (!make_tmap_3d(&tc, c0.out_bf16, (uint64_t)nlen, (uint64_t)M, (uint64_t)nseg, (uint64_t)c0.ld_bf16,
+                          (uint64_t)s2, 64, 32, 1, err, errlen))
+          return cudaErrorInvalidValue;
+      }
       args.c_tma = 2;
+    }
+  }
+  // N2 direct-to-peer segments and the fused row-dot (part 0 of a single GEMM)
+  SegMaps sm;
+  std::memset(&sm, 0, sizeof sm);
+  args.nsegp = 0;
+  std::memset(&args.segp, 0, sizeof args.segp);
+  std::memset(&args.dot, 0, sizeof args.dot);
+  {
+    const OutMap& c0 = p0.c;
+    if (c0.seg.n > 0) {
+      const int64_t nlen = c0.n_len < p0.N ? c0.n_len : p0.N;
+      if (n != 1 || c0.epi != Epi::kStoreBF16 || c0.seg.n > kMaxSeg || c0.seg.n * nlen < p0.N ||
+          c0.r_mstride != 0 || c0.m_len < M || c0.r_base != 0 || c0.c_base != 0 || c0.c_nstride != 0 ||
+          c0.c_mstride != 0 || c0.ld_bf16 % 8) {
+        snprintf(err, errlen, "gemm: segmented (direct-to-peer) output needs a single bf16-store GEMM with "
+                              "plain segments covering N (%d segments of %lld columns, N = %lld)",
+                 c0.seg.n, (long long)nlen, (long long)p0.N);
+        return cudaErrorInvalidValue;
+      }
+      for (int q = 0; q < c0.seg.n; ++q) {
+        if (!c0.seg.p[q] || (reinterpret_cast<uintptr_t>(c0.seg.p[q]) & 15)) {
+          snprintf(err, errlen, "gemm: segment %d destination null or not 16-byte aligned", q);
+          return cudaErrorInvalidValue;
+        }
+        args.segp[q] = reinterpret_cast<__nv_bfloat16*>(c0.seg.p[q]);
+        if (args.c_tma == 2 &&
+            !make_tmap_2d(&sm.m[q], c0.seg.p[q], (uint64_t)nlen, (uint64_t)M, (uint64_t)c0.ld_bf16, 64, 32, err, errlen))
+          return cudaErrorInvalidValue;
+      }
+      args.nsegp = c0.seg.n;
+    }
+    if (c0.dot.o) {
+      const RowDot& r = c0.dot;
+      const int w = args.c_tma == 2 ? 64 : 32;          // the epilogue's column chunk
+      if (n != 1 || c0.epi != Epi::kStoreBF16 || r.d <= 0 || r.d % w || bn % r.d || c0.n_len % r.d ||
+          (reinterpret_cast<uintptr_t>(r.o) & 15) || r.ld_o % 8 || r.col0 % 8 || r.col_stride % 8 || p0.alpha != 1.0f) {
+        snprintf(err, errlen, "gemm: fused row-dot needs a single bf16-store GEMM with head-aligned tiles "
+                              "(d = %d, BN = %d) and 16-byte aligned O columns", r.d, bn);
+        return cudaErrorInvalidValue;
+      }
+      args.dot.o = reinterpret_cast<const __nv_bfloat16*>(r.o);
+      args.dot.ld_o = r.ld_o;
+      args.dot.col0 = r.col0;
+      args.dot.col_stride = r.col_stride;
+      args.dot.dst_stride = r.dst_stride;
+      for (int q = 0; q < kMaxSeg; ++q) args.dot.dst[q] = r.dst[q];
+      args.dot.ld_dst = r.ld_dst;
+      args.dot.d = r.d;
     }
   }
   cudaError_t e;
   const int clk = pair4 ? -4 : (pair ? -2 : cl);
-  if (bn == 512) e = dispatch_major<512>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, &tc, args, stream);
-  else if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, &tc, args, stream);
-  else if (bn == 128) e = dispatch_major<128>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, &tc, args, stream);
-  else e = dispatch_major<64>(p0.a.mn_major, p0.b.mn_major, 1, ta, tb, &tc, args, stream);
+  if (bn == 512) e = dispatch_major<512>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, &tc, sm, args, stream);
+  else if (bn == 256) e = dispatch_major<256>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, &tc, sm, args, stream);
+  else if (bn == 128) e = dispatch_major<128>(p0.a.mn_major, p0.b.mn_major, clk, ta, tb, &tc, sm, args, stream);
+  else e = dispatch_major<64>(p0.a.mn_major, p0.b.mn_major, 1, ta, tb, &tc, sm, args, stream);
   if (e != cudaSuccess) snprintf(err, errlen, "gemm launch: %s", cudaGetErrorString(e));
   if (args.dbg) {
     long long h[8];

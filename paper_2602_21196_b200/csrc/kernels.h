@@ -50,6 +50,30 @@ struct RopeRef {
   int64_t pos0 = 0;             // position of row 0
 };
 
+// Direct-to-peer destinations: a producer kernel writes block `seg` of its output
+// straight into the receive buffer of the rank that owns it (a CUDA-IPC mapping of that rank's
+// symmetric workspace) instead of into a local send buffer. kMaxSeg bounds the group (one box: 8 GPUs).
+constexpr int kMaxSeg = 8;
+struct SegPtrs {
+  void* p[kMaxSeg] = {};        // base of segment 0..n-1 (n = 0: not segmented)
+  int n = 0;
+  int64_t rows = 0;             // row-segmented outputs (attention O, dQ/dK/dV): rows per segment (S_l)
+};
+
+// Fused delta = rowsum(bf16(out) * O) per (row, head) in the bf16 store epilogue of the dO projection
+// (DESIGN A13): the epilogue thread of row m holds the stored (bf16-rounded) dO values of
+// its columns and reads the matching O columns of o_saved, so dO is never re-read from HBM.
+//   output column n = (seg, nin) (seg = n / n_len) <-> O column col0 + seg * col_stride + nin of row m;
+//   delta of (m, head nin / d) -> dst(seg)[m * ld_dst + nin / d], dst(seg) = dst[seg] if dst_stride == 0
+//   else dst[0] + seg * dst_stride. Needs head-aligned tiles (the GEMM checks BN % d == 0).
+struct RowDot {
+  const void* o = nullptr;
+  int64_t ld_o = 0, col0 = 0, col_stride = 0;
+  float* dst[kMaxSeg] = {};
+  int64_t dst_stride = 0;
+  int ld_dst = 0, d = 0;
+};
+
 struct OutMap {
   void* out_f32 = nullptr;
   void* out_bf16 = nullptr;
@@ -58,6 +82,10 @@ struct OutMap {
   int64_t c_base = 0, n_len = 1 << 30, c_nstride = 0, c_mstride = 0;
   Epi epi = Epi::kStoreBF16;
   RopeRef rope;                 // kStoreBF16 only: rotate column pairs by the row's position first
+  // kStoreBF16, N2: column segment n / n_len goes to seg.p[n / n_len] + m * ld_bf16 + n % n_len (a peer's
+  // receive block; replaces out_bf16 / r_nstride). Part 0 of a single (non-grouped) GEMM only.
+  SegPtrs seg;
+  RowDot dot;                   // part 0 of a single GEMM, kStoreBF16: fused row-dot (dot.o non-null)
 };
 
 struct GemmProblem {
@@ -93,6 +121,7 @@ struct AttnFwdProblem {
   int64_t ldq, ldkv, ldo, ld_lse;
   float* o32 = nullptr;        // non-null: O in fp32 at o32 + t*ldo32 + j*d instead of bf16 (ring partials)
   int64_t ldo32 = 0;
+  SegPtrs o_seg;               // N2 (n > 0): row t of O goes to o_seg.p[t / rows] + (t % rows)*ldo + j*d
 };
 cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err, size_t errlen);
 
@@ -113,6 +142,7 @@ struct AttnBwdProblem {
   int dq_dim_major = 0;                       // 1 (only where attn_bwd_dq_dim_major() allows): dq_acc is
   int64_t ld_dqt = 0;                         //   [nq*d][S] fp32, row stride ld_dqt (tokens contiguous)
   int* dq_sem = nullptr;                      // non-null: deterministic dQ order (attn_bwd_sem_count ints, zeroed)
+  SegPtrs dk_seg, dv_seg;                     // N2 (n > 0): bf16 dK / dV row t -> seg.p[t / rows] + (t % rows)*ld_kvb
 };
 // int32 semaphores the deterministic backward needs: one per (q head, 64-query tile, 32-dim box group).
 inline int64_t attn_bwd_sem_count(int64_t S, int nq) { return (int64_t)nq * ((S + 63) / 64) * 4; }
@@ -133,7 +163,11 @@ cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t l
 // The same from a dim-major source: dst[t][c] = bf16(scale * src[c][t]) (src row stride lds, tokens
 // contiguous), with the inverse RoPE of token rope.pos0 + t on column pairs; cols % 64 == 0.
 cudaError_t cvt_dimmajor_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows,
-                                      int64_t cols, float scale, cudaStream_t s, const RopeRef& inverse_rope);
+                                      int64_t cols, float scale, cudaStream_t s, const RopeRef& inverse_rope,
+                                      const SegPtrs* dst_seg = nullptr);
+// N2 form of cvt_f32_bf16_run: dst row t -> dst_seg.p[t / dst_seg.rows] + (t % dst_seg.rows) * ldd.
+cudaError_t cvt_f32_bf16_seg_run(const float* src, int64_t lds, const SegPtrs& dst_seg, int64_t ldd, int64_t rows,
+                                 int64_t cols, float scale, cudaStream_t s, const RopeRef& inverse_rope);
 // Ring-step combine (DESIGN A27), per row t and head j of [rows][nheads][d]:
 //   lse' = log(e^lse_acc + e^lse_part) (max-subtracted), O' = e^(lse_acc-lse') O_acc + e^(lse_part-lse') O_part,
 // O fp32, lse [nheads][ld_lse]; writes o_acc and lse_acc in place.

@@ -185,18 +185,49 @@ cudaError_t probe_copy(void* dst, const void* src, size_t bytes, cudaStream_t q)
   return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, q);
 }
 
+// UPIPE_FLAG_DIRECT: checks the transport can write peer memory.
+upipe_status_t check_direct(upipe_ctx_s* ctx, const Plan& P) {
+  if (!direct_enabled(ctx->flags, P)) return UPIPE_OK;
+  if (!ctx->transport->peer_capable()) {
+    ctx->last_error = "UPIPE_FLAG_DIRECT needs a ctx with peer memory (upipe_ipc_create + upipe_ipc_connect)";
+    return UPIPE_ERR_STATE;
+  }
+  if (P.C > kMaxSeg) {
+    ctx->last_error = "UPIPE_FLAG_DIRECT: Ulysses degree > 8 (one box) is not supported";
+    return UPIPE_ERR_UNSUPPORTED;
+  }
+  return UPIPE_OK;
+}
+
+// Block `me` of every group peer's copy of the receive buffer `local_recv` (same offset in each rank's
+// symmetric region): segment p of a producer's output goes to peer first + p. rows = rows per block.
+bool peer_blocks(Transport& T, int first, int C, int me, const char* local_recv, size_t block_bytes, int64_t rows,
+                 SegPtrs& out) {
+  out = SegPtrs{};
+  out.n = C;
+  out.rows = rows;
+  for (int p = 0; p < C; ++p) {
+    char* b = static_cast<char*>(T.peer_ptr(first + p, local_recv));
+    if (!b) return false;
+    out.p[p] = b + (size_t)me * block_bytes;
+  }
+  return true;
+}
+
 }  // namespace
 
 // ============================================================================ forward
 upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf16p wk, bf16p wv, bf16p wo,
                          upipe_bf16* y, upipe_bf16* o_saved, float* lse_saved, char* ws, cudaStream_t st) {
   const bool ov = overlap_enabled(ctx->flags, P);
+  const bool dir = direct_enabled(ctx->flags, P);        // N2: producers write the peers' receive buffers
+  if (upipe_status_t s = check_direct(ctx, P)) return s;
   if (ov || P.ring > 1) {                               // the ring hybrid overlaps its transfers on the comm stream
     if (upipe_status_t s = ensure_pipe(ctx)) return s;
   }
   Runner R{ctx};
   Transport& T = *ctx->transport;
-  const FwdWs W = fwd_workspace(P, ov);
+  const FwdWs W = fwd_workspace(P, ov, dir);
   RopeRef rope_seq;                        // projections: rows are this rank's tokens rank*S_l + t
   if (upipe_status_t s = ensure_rope(ctx, P, rope_seq)) return s;
   rope_seq.pos0 = (int64_t)ctx->rank * P.S_l;
@@ -211,21 +242,46 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   const size_t qbytes = (size_t)P.S_l * qseg * 2, kbytes = (size_t)P.S_l * kseg * 2;
   const int64_t qstep = (int64_t)P.q_dev_stride() * d;
   auto kvb = [&](int s) { return ov ? P.kv_group(s) & 1 : 0; };
+  // N2: the projection epilogues store block p of their output into block `me` of peer p's receive buffer
+  auto direct_to = [&](GemmProblem g, const char* recv, size_t block_bytes, char* e) -> GemmProblem {
+    if (!peer_blocks(T, first, C, me, recv, block_bytes, P.S_l, g.c.seg))
+      snprintf(e, 512, "receive buffer outside the symmetric region");
+    g.c.out_bf16 = nullptr;
+    g.c.r_nstride = 0;
+    return g;
+  };
 
-  // F1: Q_s (and K_s, V_s at a super-stage start) -> send buffer set b
+  // F1: Q_s (and K_s, V_s at a super-stage start) -> send buffer set b (N2: the peers' receive set b)
   auto proj = [&](int s, int b, cudaStream_t q) {
     const int64_t q0 = P.q0(s, 0), kv0 = P.kv0(s, 0);
     R.run(UPIPE_TRACE_GEMM, q, "proj Q", [&](char* e) {
-      return gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend[b], rope_seq), q, e, 512);
+      GemmProblem g = proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend[b], rope_seq);
+      if (dir) g = direct_to(g, ws + W.qrecv[b], qbytes, e);
+      return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
     });
     if (P.kv_sent(s)) {
+      const int kb = kvb(s);
       R.run(UPIPE_TRACE_GEMM, q, "proj K", [&](char* e) {
-        return gemm_run(proj_to_send(P, x, wk, kvrows, kv0 * d, kseg, kseg, ws + W.ksend, rope_seq), q, e, 512);
+        GemmProblem g = proj_to_send(P, x, wk, kvrows, kv0 * d, kseg, kseg, ws + W.ksend, rope_seq);
+        if (dir) g = direct_to(g, ws + W.krecv[kb], kbytes, e);
+        return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
       });
       R.run(UPIPE_TRACE_GEMM, q, "proj V", [&](char* e) {
-        return gemm_run(proj_to_send(P, x, wv, kvrows, kv0 * d, kseg, kseg, ws + W.vsend), q, e, 512);
+        GemmProblem g = proj_to_send(P, x, wv, kvrows, kv0 * d, kseg, kseg, ws + W.vsend);
+        if (dir) g = direct_to(g, ws + W.vrecv[kb], kbytes, e);
+        return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
       });
     }
+  };
+  // N2 handshake around a collective whose producers push into the peers: every group peer's receive
+  // buffers are free (ready flags), ... the producers run ..., every peer's pushes have landed here
+  auto push_begin = [&](const char* what, cudaStream_t q) {
+    uint32_t e = 0;
+    R.comm(q, what, [&](std::string& m) { return T.push_begin(first, C, q, &e, m); });
+    return e;
+  };
+  auto push_end = [&](uint32_t e, const char* what, cudaStream_t q) {
+    R.comm(q, what, [&](std::string& m) { return T.push_end(e, first, C, q, m); });
   };
   const upipe_probe_t& pr = ctx->probe;   // test-only layout probe (stage -1: off)
   auto probe_in = [&](int s, int b, cudaStream_t q) {
@@ -250,6 +306,11 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   // F3: attention over the full sequence for this device's qpd heads
   auto attn = [&](int s, int b, cudaStream_t q) {
     if (pr.stage == s && pr.o_head) {      // test probe: the injected head-layout O replaces the attention
+      if (dir) {
+        ctx->last_error = "layout probe O injection is not available with UPIPE_FLAG_DIRECT";
+        R.status = UPIPE_ERR_INVALID_ARG;
+        return;
+      }
       R.run(UPIPE_TRACE_AUX, q, "probe inject O", [&](char*) {
         if (C == 1)
           return cudaMemcpy2DAsync(o_saved + (int64_t)P.q0(s, me) * d, HqD * 2, pr.o_head, qseg * 2, qseg * 2, P.S,
@@ -265,6 +326,14 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     if (C == 1) {
       a.o = o_saved + (int64_t)P.q0(s, me) * d;  // no out all-to-all: straight into the pre-allocated output
       a.ldo = HqD;
+    } else if (dir) {                      // N2: rows of rank p's tokens -> block `me` of p's O receive buffer
+      a.o = nullptr;
+      a.ldo = qseg;
+      if (!peer_blocks(T, first, C, me, ws + W.orecv[b], qbytes, P.S_l, a.o_seg)) {
+        ctx->last_error = "attn fwd: O receive buffer outside the symmetric region";
+        R.status = UPIPE_ERR_STATE;
+        return;
+      }
     } else {
       a.o = ws + W.osend[b];
       a.ldo = qseg;
@@ -371,6 +440,22 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   };
 
   const int nu = P.nstages;
+  if (dir) {
+    // N2: one stream, one buffer set; each all-to-all happens inside its producer (projection / attention
+    // epilogues writing peer memory), bracketed by the ready/done flag handshake
+    for (int s = 0; s < nu && R.status == UPIPE_OK; ++s) {
+      const uint32_t e_in = push_begin("direct QKV begin", st);
+      proj(s, 0, st);
+      push_end(e_in, "direct QKV end", st);
+      probe_in(s, 0, st);
+      const uint32_t e_o = push_begin("direct O begin", st);
+      attn(s, 0, st);
+      push_end(e_o, "direct O end", st);
+      post(s, 0, st);
+    }
+    out_proj(st);
+    return R.status;
+  }
   if (!ov) {
     for (int s = 0; s < nu && R.status == UPIPE_OK; ++s) {
       proj(s, 0, st);
@@ -431,12 +516,14 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
                          bf16p dy, bf16p o_saved, const float* lse_saved, upipe_bf16* dx, float* dwq, float* dwk,
                          float* dwv, float* dwo, int reduce_dw, char* ws, cudaStream_t st) {
   const bool ov = overlap_enabled(ctx->flags, P);
+  const bool dir = direct_enabled(ctx->flags, P);        // N2: producers write the peers' receive buffers
+  if (upipe_status_t s = check_direct(ctx, P)) return s;
   if (ov || P.ring > 1) {                               // the ring hybrid overlaps its transfers on the comm stream
     if (upipe_status_t s = ensure_pipe(ctx)) return s;
   }
   Runner R{ctx};
   Transport& T = *ctx->transport;
-  const BwdWs W = bwd_workspace(P, ov);
+  const BwdWs W = bwd_workspace(P, ov, dir);
   const int C = P.C, me = ctx->rank % P.C, d = P.d;
   const int ring_i = ctx->rank / P.C, first = ring_i * P.C;   // Ulysses group (DESIGN A27)
   RopeRef rope_seq, rope_head;             // seq layout (projections) / head layout (rows = the group's tokens)
@@ -453,6 +540,21 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   const size_t dbytes = (size_t)P.S_l * P.qpd * 4;
   const int64_t qstep = (int64_t)P.q_dev_stride() * d;
   auto kvb = [&](int s) { return ov ? P.kv_group(s) & 1 : 0; };
+  auto direct_to = [&](GemmProblem g, const char* recv, size_t block_bytes, char* e) -> GemmProblem {
+    if (!peer_blocks(T, first, C, me, recv, block_bytes, P.S_l, g.c.seg))
+      snprintf(e, 512, "receive buffer outside the symmetric region");
+    g.c.out_bf16 = nullptr;
+    g.c.r_nstride = 0;
+    return g;
+  };
+  auto push_begin = [&](const char* what, cudaStream_t q) {
+    uint32_t e = 0;
+    R.comm(q, what, [&](std::string& m) { return T.push_begin(first, C, q, &e, m); });
+    return e;
+  };
+  auto push_end = [&](uint32_t e, const char* what, cudaStream_t q) {
+    R.comm(q, what, [&](std::string& m) { return T.push_end(e, first, C, q, m); });
+  };
 
   // dWo = dY^T O over this rank's tokens (all stages at once: o_saved holds every head)
   {
@@ -518,14 +620,21 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   auto pre = [&](int s, int b, cudaStream_t q) {
     const int64_t q0 = P.q0(s, 0), kv0 = P.kv0(s, 0);
     R.run(UPIPE_TRACE_GEMM, q, "proj Q", [&](char* e) {
-      return gemm_run(proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend[b], rope_seq), q, e, 512);
+      GemmProblem g = proj_to_send(P, x, wq, HqD, q0 * d, qstep, qseg, ws + W.qsend[b], rope_seq);
+      if (dir) g = direct_to(g, ws + W.qrecv[b], qbytes, e);
+      return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
     });
     if (P.kv_sent(s)) {
+      const int kb = kvb(s);
       R.run(UPIPE_TRACE_GEMM, q, "proj K", [&](char* e) {
-        return gemm_run(proj_to_send(P, x, wk, HkvD, kv0 * d, kseg, kseg, ws + W.ksend, rope_seq), q, e, 512);
+        GemmProblem g = proj_to_send(P, x, wk, HkvD, kv0 * d, kseg, kseg, ws + W.ksend, rope_seq);
+        if (dir) g = direct_to(g, ws + W.krecv[kb], kbytes, e);
+        return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
       });
       R.run(UPIPE_TRACE_GEMM, q, "proj V", [&](char* e) {
-        return gemm_run(proj_to_send(P, x, wv, HkvD, kv0 * d, kseg, kseg, ws + W.vsend), q, e, 512);
+        GemmProblem g = proj_to_send(P, x, wv, HkvD, kv0 * d, kseg, kseg, ws + W.vsend);
+        if (dir) g = direct_to(g, ws + W.vrecv[kb], kbytes, e);
+        return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
       });
     }
     GemmProblem g;
@@ -542,13 +651,29 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     g.c.n_len = qseg;
     g.c.r_nstride = P.S_l;
     g.c.epi = Epi::kStoreBF16;
-    R.run(UPIPE_TRACE_GEMM, q, "dO", [&](char* e) { return gemm_run(g, q, e, 512); });
-    for (int p = 0; p < C; ++p)
-      R.run(UPIPE_TRACE_AUX, q, "rowdot", [&](char*) {
-        return rowdot_run((const upipe_bf16*)(ws + W.dosend[b]) + (int64_t)p * P.S_l * qseg, qseg,
-                          o_saved + (int64_t)P.q0(s, p) * d, HqD, (float*)(ws + W.dsend[b]) + (int64_t)p * P.S_l * P.qpd,
-                          P.qpd, P.S_l, P.qpd, d, q);
-      });
+    // delta = rowsum(dO * O) fused into the epilogue (A13): dO column (p, nin) <-> o_saved column
+    // q0(s, p) d + nin = q0 d + p qstep + nin; delta of (token t, head j) -> block p of the delta send
+    // buffer [C][S_l][qpd] (N2: block `me` of peer p's delta receive buffer)
+    g.c.dot.o = o_saved;
+    g.c.dot.ld_o = HqD;
+    g.c.dot.col0 = q0 * d;
+    g.c.dot.col_stride = qstep;
+    g.c.dot.ld_dst = P.qpd;
+    g.c.dot.d = d;
+    R.run(UPIPE_TRACE_GEMM, q, "dO + delta", [&](char* e) {
+      if (dir) {
+        g = direct_to(g, ws + W.dorecv[b], qbytes, e);
+        SegPtrs ds;
+        if (!e[0] && !peer_blocks(T, first, C, me, ws + W.drecv[b], dbytes, P.S_l, ds))
+          snprintf(e, 512, "delta receive buffer outside the symmetric region");
+        for (int p = 0; p < C; ++p) g.c.dot.dst[p] = static_cast<float*>(ds.p[p]);
+        g.c.dot.dst_stride = 0;
+      } else {
+        g.c.dot.dst[0] = (float*)(ws + W.dsend[b]);
+        g.c.dot.dst_stride = (int64_t)P.S_l * P.qpd;
+      }
+      return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
+    });
   };
   const upipe_probe_t& pr = ctx->probe;   // test-only layout probe (stage -1: off)
   auto probe_in = [&](int s, int b, cudaStream_t q) {
@@ -586,6 +711,11 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   // B4: attention backward (dK/dV accumulate over the sigma stages sharing the resident K/V), dQ -> bf16
   auto attn = [&](int s, int b, cudaStream_t q) {
     if (pr.stage == s && pr.dq_head) {     // test probe: injected head-layout dQ (dK, dV) replace the kernel's
+      if (dir) {
+        ctx->last_error = "layout probe dQ injection is not available with UPIPE_FLAG_DIRECT";
+        R.status = UPIPE_ERR_INVALID_ARG;
+        return;
+      }
       R.run(UPIPE_TRACE_AUX, q, "probe inject dQ", [&](char*) {
         cudaError_t e = probe_copy(ws + W.dqsend[b], pr.dq_head, (size_t)P.S * qseg * 2, q);
         if (e == cudaSuccess && P.kv_last(s)) e = probe_copy(ws + W.dksend, pr.dk_head, (size_t)P.S * kseg * 2, q);
@@ -595,7 +725,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       return;
     }
     R.run(UPIPE_TRACE_AUX, q, "memset dQ", [&](char*) {
-      return cudaMemsetAsync(ws + W.dqacc[b], 0, (size_t)P.S * qseg * 4, q);
+      return cudaMemsetAsync(ws + W.dqacc[b], 0, (size_t)((P.S + 3) & ~int64_t(3)) * qseg * 4, q);
     });
     const int r = P.kv_pos(s);
     const bool last = P.kv_last(s);
@@ -611,6 +741,20 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     bp.dv_acc = P.sigma > 1 && !P.naive ? (float*)(ws + W.dvacc) : nullptr;
     bp.dk_bf16 = last ? ws + W.dksend : nullptr;
     bp.dv_bf16 = last ? ws + W.dvsend : nullptr;
+    SegPtrs dq_seg;                                   // N2: dQ / dK / dV rows of rank p's tokens -> peer p
+    if (dir) {
+      bool ok = peer_blocks(T, first, C, me, ws + W.dqrecv[b], qbytes, P.S_l, dq_seg);
+      if (last) {
+        ok = ok && peer_blocks(T, first, C, me, ws + W.dkrecv, kbytes, P.S_l, bp.dk_seg) &&
+             peer_blocks(T, first, C, me, ws + W.dvrecv, kbytes, P.S_l, bp.dv_seg);
+        bp.dk_bf16 = bp.dv_bf16 = nullptr;
+      }
+      if (!ok) {
+        ctx->last_error = "attn bwd: receive buffer outside the symmetric region";
+        R.status = UPIPE_ERR_STATE;
+        return;
+      }
+    }
     bp.S = P.S;
     bp.nq = P.qpd;
     bp.nkv = P.kv_res;
@@ -626,7 +770,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     bp.kv_write_acc = !last;
     bp.rope = rope_head;
     bp.dq_dim_major = attn_bwd_dq_dim_major(bp) ? 1 : 0;   // [qpd*d][S] accumulator (64-query kernel)
-    bp.ld_dqt = P.S;
+    bp.ld_dqt = (P.S + 3) & ~int64_t(3);                  // 16-byte TMA row stride
     // UPIPE_FLAG_DETERMINISTIC: dQ partials added in key-tile order; fresh semaphores per launch
     const bool det = (ctx->flags & UPIPE_FLAG_DETERMINISTIC) != 0;
     bp.dq_sem = det ? (int*)(ws + W.dqsem) : nullptr;
@@ -709,8 +853,10 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     }
     R.run(UPIPE_TRACE_AUX, q, "cvt dQ", [&](char*) {
       if (bp.dq_dim_major)
-        return cvt_dimmajor_f32_bf16_run((const float*)(ws + W.dqacc[b]), P.S, ws + W.dqsend[b], qseg, P.S, qseg,
-                                         1.0f, q, rope_head);
+        return cvt_dimmajor_f32_bf16_run((const float*)(ws + W.dqacc[b]), bp.ld_dqt, dir ? nullptr : ws + W.dqsend[b], qseg,
+                                         P.S, qseg, 1.0f, q, rope_head, dir ? &dq_seg : nullptr);
+      if (dir)
+        return cvt_f32_bf16_seg_run((const float*)(ws + W.dqacc[b]), qseg, dq_seg, qseg, P.S, qseg, 1.0f, q, rope_head);
       return cvt_f32_bf16_run((const float*)(ws + W.dqacc[b]), qseg, ws + W.dqsend[b], qseg, P.S, qseg, 1.0f, q,
                               rope_head);
     });
@@ -758,7 +904,21 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   };
 
   const int nu = P.nstages;
-  if (!ov) {
+  if (dir) {
+    // N2 (see the forward): Q/K/V and dO (+ delta) pushed by their projection epilogues, dQ by its
+    // conversion, dK/dV by the attention-backward epilogue at the super-stage end
+    for (int s = 0; s < nu && R.status == UPIPE_OK; ++s) {
+      const uint32_t e_in = push_begin("direct Q/K/V/dO begin", st);
+      pre(s, 0, st);
+      push_end(e_in, "direct Q/K/V/dO end", st);
+      probe_in(s, 0, st);
+      const uint32_t e_out = push_begin("direct dQ/dK/dV begin", st);
+      attn(s, 0, st);
+      push_end(e_out, "direct dQ/dK/dV end", st);
+      probe_out(s, 0, st);
+      post(s, 0, st);
+    }
+  } else if (!ov) {
     for (int s = 0; s < nu && R.status == UPIPE_OK; ++s) {
       pre(s, 0, st);
       if (C > 1) inp(s, 0, st);

@@ -5,6 +5,7 @@
 //   unpack_cols out-a2a receive [C][S_l][qpd d] -> o_saved    (F5)
 //   synth_fill  device copy of the counter-based input generator (synth/__init__.py)
 //   merge       ring-step combine of two attention partials by their LSE
+#include <algorithm>
 #include <cstdio>
 
 #include "kernels.h"
@@ -86,8 +87,14 @@ __global__ void merge_kernel(float* __restrict__ o_acc, const float* __restrict_
   }
 }
 
+// Destination row r: dst + r * ldd, or (N2, seg.n > 0) the owner rank's receive block seg.p[r / seg.rows].
+__device__ __forceinline__ __nv_bfloat16* dst_row(__nv_bfloat16* dst, const SegPtrs& seg, long long r, long long ldd) {
+  if (seg.n) return reinterpret_cast<__nv_bfloat16*>(seg.p[r / seg.rows]) + (r % seg.rows) * ldd;
+  return dst + r * ldd;
+}
+
 __global__ void cvt_kernel(const float* __restrict__ src, long long lds, __nv_bfloat16* __restrict__ dst,
-                           long long ldd, long long rows, long long cols, float scale, RopeRef rope) {
+                           long long ldd, long long rows, long long cols, float scale, RopeRef rope, SegPtrs seg) {
   const long long v8 = cols / 8;
   const long long total = rows * v8;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -98,7 +105,7 @@ __global__ void cvt_kernel(const float* __restrict__ src, long long lds, __nv_bf
     float v[8] = {x.x * scale, x.y * scale, x.z * scale, x.w * scale, y.x * scale, y.y * scale, y.z * scale, y.w * scale};
     // row r is token rope.pos0 + r (head layout [S][heads*d]); gradients rotate back by -angle
     if (rope.hi) dev::rope_rotate<4>(v, rope.hi, rope.lo, rope.d, rope.pos0 + r, (int)(c % rope.d), -1.f);
-    *reinterpret_cast<uint4*>(dst + r * ldd + c) =
+    *reinterpret_cast<uint4*>(dst_row(dst, seg, r, ldd) + c) =
         make_uint4(dev::pack_bf16(v[0], v[1]), dev::pack_bf16(v[2], v[3]), dev::pack_bf16(v[4], v[5]),
                    dev::pack_bf16(v[6], v[7]));
   }
@@ -107,7 +114,8 @@ __global__ void cvt_kernel(const float* __restrict__ src, long long lds, __nv_bf
 // 64 tokens x 64 dims per tile through shared memory: coalesced 256-byte reads along tokens (four
 // 16-byte loads in flight per thread), 16-byte bf16 writes along dims (RoPE pairs are adjacent dims).
 __global__ void cvt_dimmajor_kernel(const float* __restrict__ src, long long lds, __nv_bfloat16* __restrict__ dst,
-                                    long long ldd, long long rows, long long cols, float scale, RopeRef rope) {
+                                    long long ldd, long long rows, long long cols, float scale, RopeRef rope,
+                                    SegPtrs seg) {
   __shared__ float tile[64][65];
   const long long ntt = (rows + 63) / 64, nct = cols / 64;
   const int t = threadIdx.x;
@@ -139,7 +147,7 @@ __global__ void cvt_dimmajor_kernel(const float* __restrict__ src, long long lds
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = tile[cg + i][tk] * scale;
         if (rope.hi) dev::rope_rotate<4>(v, rope.hi, rope.lo, rope.d, rope.pos0 + t0 + tk, (int)((c0 + cg) % rope.d), -1.f);
-        *reinterpret_cast<uint4*>(dst + (t0 + tk) * ldd + c0 + cg) =
+        *reinterpret_cast<uint4*>(dst_row(dst, seg, t0 + tk, ldd) + c0 + cg) =
             make_uint4(dev::pack_bf16(v[0], v[1]), dev::pack_bf16(v[2], v[3]), dev::pack_bf16(v[4], v[5]),
                        dev::pack_bf16(v[6], v[7]));
       }
@@ -148,17 +156,24 @@ __global__ void cvt_dimmajor_kernel(const float* __restrict__ src, long long lds
   }
 }
 
-__global__ void unpack_kernel(const uint4* __restrict__ src, long long rows, int nseg, int seg_v,
+// F5 unpack: segment blockIdx.y, rows in a grid-stride loop; a thread's (row-in-block, vector) split is
+// computed once, so the loop carries no 64-bit division (each row's segment is seg_v 16-byte vectors,
+// contiguous in both src and dst).
+__global__ void unpack_kernel(const uint4* __restrict__ src, long long rows, int seg_v,
                               __nv_bfloat16* __restrict__ dst, long long ldd, long long col_base,
                               long long col_stride) {
-  const long long total = (long long)nseg * rows * seg_v;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long s = i / (rows * seg_v);
-    const long long rem = i % (rows * seg_v);
-    const long long t = rem / seg_v, e = (rem % seg_v) * 8;
-    *reinterpret_cast<uint4*>(dst + t * ldd + col_base + s * col_stride + e) = src[i];
-  }
+  const int s = blockIdx.y;
+  const int nt = blockDim.x;
+  const int rpb = seg_v >= nt ? 1 : nt / seg_v;           // rows per block iteration
+  const int r0 = seg_v >= nt ? 0 : (int)threadIdx.x / seg_v;
+  const int v0 = seg_v >= nt ? (int)threadIdx.x : (int)threadIdx.x % seg_v;
+  const int vstep = seg_v >= nt ? nt : seg_v;
+  if (r0 >= rpb) return;
+  const uint4* sp = src + (long long)s * rows * seg_v;
+  __nv_bfloat16* dp = dst + col_base + s * col_stride;
+  for (long long t = (long long)blockIdx.x * rpb + r0; t < rows; t += (long long)gridDim.x * rpb)
+    for (int v = v0; v < seg_v; v += vstep)
+      *reinterpret_cast<uint4*>(dp + t * ldd + v * 8) = __ldcs(sp + t * seg_v + v);
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
@@ -220,7 +235,7 @@ cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t l
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (cols % 8) return cudaErrorInvalidValue;
   cvt_kernel<<<grid_for(rows * cols / 8, kThreads), kThreads, 0, s>>>(src, lds, (__nv_bfloat16*)dst, ldd, rows,
-                                                                     cols, scale, inverse_rope);
+                                                                     cols, scale, inverse_rope, SegPtrs{});
   count_launches(1);
   return cudaGetLastError();
 }
@@ -230,13 +245,30 @@ cudaError_t cvt_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t l
   return cvt_f32_bf16_run(src, lds, dst, ldd, rows, cols, scale, s, RopeRef{});
 }
 
+static bool seg_covers(const SegPtrs& seg, int64_t rows) {
+  return seg.n > 0 && seg.n <= kMaxSeg && seg.rows > 0 && (rows + seg.rows - 1) / seg.rows <= seg.n;
+}
+
+cudaError_t cvt_f32_bf16_seg_run(const float* src, int64_t lds, const SegPtrs& dst_seg, int64_t ldd, int64_t rows,
+                                 int64_t cols, float scale, cudaStream_t s, const RopeRef& inverse_rope) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  if (cols % 8 || !seg_covers(dst_seg, rows)) return cudaErrorInvalidValue;
+  cvt_kernel<<<grid_for(rows * cols / 8, kThreads), kThreads, 0, s>>>(src, lds, nullptr, ldd, rows, cols, scale,
+                                                                     inverse_rope, dst_seg);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
 cudaError_t cvt_dimmajor_f32_bf16_run(const float* src, int64_t lds, void* dst, int64_t ldd, int64_t rows,
-                                      int64_t cols, float scale, cudaStream_t s, const RopeRef& inverse_rope) {
+                                      int64_t cols, float scale, cudaStream_t s, const RopeRef& inverse_rope,
+                                      const SegPtrs* dst_seg) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (cols % 64) return cudaErrorInvalidValue;
+  if (dst_seg && dst_seg->n && !seg_covers(*dst_seg, rows)) return cudaErrorInvalidValue;
   const long long tiles = ((rows + 63) / 64) * (cols / 64);
   const int grid = (int)(tiles < 148 * 8 ? tiles : 148 * 8);
-  cvt_dimmajor_kernel<<<grid, 256, 0, s>>>(src, lds, (__nv_bfloat16*)dst, ldd, rows, cols, scale, inverse_rope);
+  cvt_dimmajor_kernel<<<grid, 256, 0, s>>>(src, lds, (__nv_bfloat16*)dst, ldd, rows, cols, scale, inverse_rope,
+                                           dst_seg ? *dst_seg : SegPtrs{});
   count_launches(1);
   return cudaGetLastError();
 }
@@ -246,8 +278,12 @@ cudaError_t unpack_cols_run(const void* src, int64_t rows, int nseg, int seg_col
   if (rows <= 0 || nseg <= 0) return cudaSuccess;
   if (seg_cols % 8) return cudaErrorInvalidValue;
   const int seg_v = seg_cols / 8;
-  unpack_kernel<<<grid_for((int64_t)nseg * rows * seg_v, kThreads), kThreads, 0, s>>>(
-      (const uint4*)src, rows, nseg, seg_v, (__nv_bfloat16*)dst, ldd, col_base, col_stride);
+  const int rpb = seg_v >= kThreads ? 1 : kThreads / seg_v;
+  int64_t bx = (rows + rpb - 1) / rpb;
+  const int64_t cap = std::max<int64_t>(1, 148 * 16 / nseg);
+  if (bx > cap) bx = cap;
+  unpack_kernel<<<dim3((unsigned)bx, (unsigned)nseg), kThreads, 0, s>>>(
+      (const uint4*)src, rows, seg_v, (__nv_bfloat16*)dst, ldd, col_base, col_stride);
   count_launches(1);
   return cudaGetLastError();
 }

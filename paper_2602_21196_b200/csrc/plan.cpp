@@ -68,7 +68,7 @@ Plan make_plan(int C, const upipe_shape_t& sh) {
   return p;
 }
 
-FwdWs fwd_workspace(const Plan& p, bool overlap) {
+FwdWs fwd_workspace(const Plan& p, bool overlap, bool direct) {
   // overlap (C > 1): the next stage's inp all-to-all runs while this stage's attention reads its
   // buffers, so the Q/K/V receive, Q send and O send/receive buffers are doubled (DESIGN A23).
   FwdWs w{};
@@ -80,20 +80,24 @@ FwdWs fwd_workspace(const Plan& p, bool overlap) {
     off += align256(bytes);
     return o;
   };
+  // UPIPE_FLAG_DIRECT: producers write the peers' receive buffers, so no send buffer is allocated (the
+  // offset 0 placeholders are never used)
+  direct = direct && p.C > 1;
+  auto take_send = [&](size_t bytes) { return direct ? size_t(0) : take(bytes); };
   const bool comm = p.C > 1;
   const bool dbl = comm && overlap;
   for (int i = 0; i < 2; ++i) {
     const bool fresh = i == 0 || dbl;
-    w.qsend[i] = fresh ? take(qe) : w.qsend[0];
+    w.qsend[i] = fresh ? take_send(qe) : w.qsend[0];
     w.qrecv[i] = !comm ? w.qsend[i] : (fresh ? take(qe) : w.qrecv[0]);
   }
-  w.ksend = take(ke);
-  w.vsend = take(ke);
+  w.ksend = take_send(ke);
+  w.vsend = take_send(ke);
   for (int i = 0; i < 2; ++i) {
     const bool fresh = i == 0 || dbl;
     w.krecv[i] = !comm ? w.ksend : (fresh ? take(ke) : w.krecv[0]);
     w.vrecv[i] = !comm ? w.vsend : (fresh ? take(ke) : w.vrecv[0]);
-    w.osend[i] = !comm ? 0 : (fresh ? take(qe) : w.osend[0]);
+    w.osend[i] = !comm ? 0 : (fresh ? take_send(qe) : w.osend[0]);
     w.orecv[i] = !comm ? 0 : (fresh ? take(qe) : w.orecv[0]);
   }
   if (p.ring > 1) {                         // ring hybrid (sequential schedule): visiting K/V blocks, fp32 O
@@ -109,7 +113,7 @@ FwdWs fwd_workspace(const Plan& p, bool overlap) {
   return w;
 }
 
-BwdWs bwd_workspace(const Plan& p, bool overlap) {
+BwdWs bwd_workspace(const Plan& p, bool overlap, bool direct) {
   BwdWs w{};
   const size_t qe = (size_t)p.S * p.qpd * p.d * 2;
   const size_t ke = (size_t)p.S * p.kv_res * p.d * 2;
@@ -120,22 +124,27 @@ BwdWs bwd_workspace(const Plan& p, bool overlap) {
     off += align256(bytes);
     return o;
   };
+  // UPIPE_FLAG_DIRECT: producers write the peers' receive buffers, so no send buffer is allocated (the
+  // offset 0 placeholders are never used)
+  direct = direct && p.C > 1;
+  auto take_send = [&](size_t bytes) { return direct ? size_t(0) : take(bytes); };
   const bool comm = p.C > 1;
   const bool dbl = comm && overlap;
   for (int i = 0; i < 2; ++i) {
     const bool fresh = i == 0 || dbl;
-    w.qsend[i] = fresh ? take(qe) : w.qsend[0];
+    w.qsend[i] = fresh ? take_send(qe) : w.qsend[0];
     w.qrecv[i] = !comm ? w.qsend[i] : (fresh ? take(qe) : w.qrecv[0]);
-    w.dosend[i] = fresh ? take(qe) : w.dosend[0];
+    w.dosend[i] = fresh ? take_send(qe) : w.dosend[0];
     w.dorecv[i] = !comm ? w.dosend[i] : (fresh ? take(qe) : w.dorecv[0]);
-    w.dsend[i] = fresh ? take(de) : w.dsend[0];
+    w.dsend[i] = fresh ? take_send(de) : w.dsend[0];
     w.drecv[i] = !comm ? w.dsend[i] : (fresh ? take(de) : w.drecv[0]);
-    w.dqacc[i] = fresh ? take(qe * 2) : w.dqacc[0];
-    w.dqsend[i] = fresh ? take(qe) : w.dqsend[0];
+    // fp32 dQ accumulator: [S][qpd d], or dim-major [qpd d][S4] (S4 = S rounded up to 4 floats, TMA stride)
+    w.dqacc[i] = fresh ? take(((size_t)p.S + 3) / 4 * 4 * p.qpd * p.d * 4) : w.dqacc[0];
+    w.dqsend[i] = fresh ? take_send(qe) : w.dqsend[0];
     w.dqrecv[i] = !comm ? w.dqsend[i] : (fresh ? take(qe) : w.dqrecv[0]);
   }
-  w.ksend = take(ke);
-  w.vsend = take(ke);
+  w.ksend = take_send(ke);
+  w.vsend = take_send(ke);
   for (int i = 0; i < 2; ++i) {
     const bool fresh = i == 0 || dbl;
     w.krecv[i] = !comm ? w.ksend : (fresh ? take(ke) : w.krecv[0]);
@@ -151,8 +160,8 @@ BwdWs bwd_workspace(const Plan& p, bool overlap) {
       w.dvring[i] = take(ke * 2);
     }
   }
-  w.dksend = take(ke);
-  w.dvsend = take(ke);
+  w.dksend = take_send(ke);
+  w.dvsend = take_send(ke);
   w.dkrecv = comm ? take(ke) : w.dksend;
   w.dvrecv = comm ? take(ke) : w.dvsend;
   w.dxacc = p.nstages > 1 ? take((size_t)p.S_l * p.D * 4) : 0;   // one stage: dX is stored in bf16 directly

@@ -420,6 +420,20 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// sum_i bf16(v[i]) * o[i] over 8 columns (o: 8 packed bf16), fp32 FMAs in column order: the row-dot of
+// the fused delta (kernels.h RowDot) on exactly the values the bf16 store writes.
+__device__ __forceinline__ float dot8_rounded(const float* v, const uint4& o) {
+  const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t pv = pack_bf16(v[2 * i], v[2 * i + 1]);
+    s = fmaf(__uint_as_float(pv << 16), __uint_as_float(w[i] << 16), s);
+    s = fmaf(__uint_as_float(pv & 0xFFFF0000u), __uint_as_float(w[i] & 0xFFFF0000u), s);
+  }
+  return s;
+}
+
 // bf16x2 RNE pack on the integer pipes (same bits as cvt.rn.bf16x2.f32 for finite inputs),
 // used to move conversions off the XU pipe, which also runs MUFU.EX2 (16 lane-ops/clk/SM each).
 __device__ __forceinline__ uint32_t pack_bf16_alu(float lo, float hi) {

@@ -58,8 +58,9 @@ struct BwdWs {
   size_t kring[2], vring[2], dkring[2], dvring[2];   // ring hybrid only
   size_t total;
 };
-FwdWs fwd_workspace(const Plan& p, bool overlap);
-BwdWs bwd_workspace(const Plan& p, bool overlap);
+// direct: UPIPE_FLAG_DIRECT layout (receive buffers only; the send offsets alias them and are unused)
+FwdWs fwd_workspace(const Plan& p, bool overlap, bool direct = false);
+BwdWs bwd_workspace(const Plan& p, bool overlap, bool direct = false);
 
 // ------------------------------------------------------------------ transport
 class Transport {
@@ -171,8 +172,13 @@ namespace upipe {
 // Overlapped UPipe schedule (double-buffered chunk set, next stage's all-to-all on the comm stream).
 // The ring hybrid runs its Ulysses all-to-alls sequentially on the compute stream; its ring transfers
 // are issued on the ctx's comm stream one step ahead of the attention (layer.cpp).
+// Direct-to-peer mode (UPIPE_FLAG_DIRECT): producers write into the owners' receive buffers;
+// one buffer set, no send buffers, no comm stream.
+inline bool direct_enabled(uint32_t flags, const Plan& P) {
+  return (flags & UPIPE_FLAG_DIRECT) && P.C > 1 && P.ring == 1;
+}
 inline bool overlap_enabled(uint32_t flags, const Plan& P) {
-  return P.C > 1 && P.ring == 1 && !(flags & UPIPE_FLAG_SYNC_COMM);
+  return P.C > 1 && P.ring == 1 && !(flags & UPIPE_FLAG_SYNC_COMM) && !direct_enabled(flags, P);
 }
 }  // namespace upipe
 

@@ -19,7 +19,7 @@ class UPipeAttention:
                  causal: bool = True, process_group=None, device=None, fabric=None, cp_rank: int | None = None,
                  cp_size: int | None = None, sync_comm: bool = False, naive_kv: bool = False,
                  rope_base: float = 0.0, ring_degree: int = 1, deterministic: bool = False,
-                 transport: str = "nccl", max_seq_local: int | None = None):
+                 transport: str = "nccl", max_seq_local: int | None = None, direct: bool = False):
         """CP group: ``process_group`` (torch.distributed, one process per GPU, NCCL transport),
         or ``fabric`` + ``cp_rank`` + ``cp_size`` (single-process group driven by one host thread per rank),
         or neither (C = 1). ``sync_comm``: sequential schedule with one chunk buffer set (the
@@ -29,7 +29,10 @@ class UPipeAttention:
         ``deterministic``: bitwise-reproducible backward (dQ partials added in key-tile order; slower).
         ``transport="ipc"`` (with ``process_group`` and ``max_seq_local``): direct-to-peer all-to-alls over
         CUDA IPC peer memory instead of NCCL; the handles are exchanged over the group (any
-        backend, gloo included), the library owns the symmetric workspace (sized for ``max_seq_local``)."""
+        backend, gloo included), the library owns the symmetric workspace (sized for ``max_seq_local``).
+        ``direct`` (with ``transport="ipc"``, UPIPE_FLAG_DIRECT): the all-to-alls are fused into their
+        producers -- projection / attention / dQ-conversion epilogues store straight into the owners'
+        receive buffers, no send buffers."""
         self.Hq, self.Hkv, self.d, self.D, self.U = n_q_heads, n_kv_heads, head_dim, hidden, chunk_heads
         self.ipc = False
         self.region_bytes = 0
@@ -37,7 +40,11 @@ class UPipeAttention:
         self.rope_base = float(rope_base)    # 0: no RoPE; else rotary base (Llama3: 500000), DESIGN A26
         self.ring = max(1, int(ring_degree))
         # UPIPE_FLAG_SYNC_COMM, UPIPE_FLAG_NAIVE_KV, UPIPE_FLAG_DETERMINISTIC
-        self.flags = (1 if sync_comm else 0) | (2 if naive_kv else 0) | (4 if deterministic else 0)
+        # UPIPE_FLAG_DIRECT (8): direct-to-peer all-to-alls fused into the producing kernels (IPC only)
+        if direct and transport != "ipc":
+            raise ValueError("direct=True needs transport='ipc' (peer memory)")
+        self.flags = (1 if sync_comm else 0) | (2 if naive_kv else 0) | (4 if deterministic else 0) | \
+            (8 if direct else 0)
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         if fabric is not None:

@@ -129,6 +129,28 @@ def test_workspace_closed_forms(U):
     assert U.upipe_workspace_size(1, sh1, 0) == U.upipe_workspace_size(1, sh1, 2)
 
 
+def test_workspace_direct_has_no_send_buffers(U):
+    # UPIPE_FLAG_DIRECT: receive buffers only, one set -- the forward chunk buffers are
+    # exactly half of the sequential schedule's (send + recv), i.e. Q path U/Hq of Ulysses' direct layout too
+    S_l, D, d = 4096, 4096, 128
+    for C, Uc, Hq, Hkv in ((8, 8, 32, 8), (8, 16, 32, 8), (8, 32, 32, 8), (8, 8, 64, 8), (4, 4, 32, 8), (2, 8, 32, 8)):
+        sh = U.make_shape(S_l, D, Hq, Hkv, d, Uc)
+        qpd = Uc // C
+        kv_res = max(1, qpd // (Hq // Hkv))
+        S = S_l * C
+        recv = 2 * S * d * (qpd + 2 * kv_res) + 2 * S * qpd * d        # Q, K, V, O receive (bf16)
+        assert abs(U.upipe_workspace_size(C, sh, 4) - recv) <= 256 * 8
+        assert abs(2 * U.upipe_workspace_size(C, sh, 4) - U.upipe_workspace_size(C, sh, 2)) <= 256 * 16
+        assert U.upipe_workspace_size(C, sh, 5) < U.upipe_workspace_size(C, sh, 3)
+    # the Q path of the direct layout scales exactly with U (Ulysses U = Hq)
+    q8 = U.upipe_workspace_size(8, U.make_shape(S_l, D, 32, 32, d, 8), 4)
+    q32 = U.upipe_workspace_size(8, U.make_shape(S_l, D, 32, 32, d, 32), 4)
+    assert abs(q8 * 4 - q32) <= 256 * 32
+    # C = 1: direct is the plain C = 1 layout (no all-to-all)
+    sh1 = U.make_shape(4096, D, 32, 8, d, 8)
+    assert U.upipe_workspace_size(1, sh1, 4) == U.upipe_workspace_size(1, sh1, 2)
+
+
 def test_workspace_c1_aliases_send_and_recv(U):
     sh = U.make_shape(1024, 512, 8, 2, 64, 2)
     w1 = U.upipe_workspace_size(1, sh, 0)

@@ -42,7 +42,8 @@ def _rank(rank, C, port, cfg, outdir):
     x, dy = t(inp["x"][rank * S_l:(rank + 1) * S_l]), t(inp["dy"][rank * S_l:(rank + 1) * S_l])
     attn = UPipeAttention(Hq, Hkv, d, D, U, True, process_group=dist.group.WORLD, transport="ipc",
                           max_seq_local=S_l, sync_comm=cfg.get("sync", False), ring_degree=cfg.get("ring", 1),
-                          deterministic=cfg.get("det", False))
+                          deterministic=cfg.get("det", False), direct=cfg.get("direct", False),
+                          rope_base=cfg.get("rope", 0.0))
     info = attn.comm_info()
     assert info["transport"] == "ipc" and info["nranks"] == C and info["rank"] == rank, info
     y, saved = attn.forward(x, *W)
@@ -76,6 +77,38 @@ def test_ipc_multiprocess_layer_matches_oracle(C, S, D, Hq, Hkv, d, U, sync, rin
     res = _run_ipc(C, cfg)
     inp = synth.layer_inputs(0, S, D, Hq, Hkv, d)
     _check(res, inp, C, Hq, Hkv, d, U, ring=ring)
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("C,S,D,Hq,Hkv,d,U,rope", [
+    (2, 512, 512, 8, 2, 64, 2, 0.0),         # BASELINE configs[0] schedule
+    (4, 1024, 1024, 32, 8, 128, 8, 0.0),     # Llama3-8B heads at CP 4, U 8 (qpd 2, sigma 2)
+    (8, 1024, 1024, 32, 8, 128, 8, 5e5),     # Llama3-8B heads at CP 8, U 8 (qpd 1, sigma 4), RoPE
+    (4, 1024, 512, 16, 4, 64, 16, 0.0),      # Ulysses (U = Hq)
+    (4, 1000, 512, 16, 16, 64, 8, 0.0),      # MHA, ragged S_l = 250 (tiles straddle the rank blocks)
+])
+def test_ipc_direct_layer_matches_oracle(C, S, D, Hq, Hkv, d, U, rope):
+    # UPIPE_FLAG_DIRECT: the projection / dO epilogues, the attention epilogues (O, dK, dV) and the
+    # dQ conversion store straight into the owners' receive buffers in the other processes
+    res = _run_ipc(C, dict(S=S, D=D, Hq=Hq, Hkv=Hkv, d=d, U=U, direct=True, rope=rope))
+    inp = synth.layer_inputs(0, S, D, Hq, Hkv, d)
+    _check(res, inp, C, Hq, Hkv, d, U, rope_base=rope or None)
+
+
+@pytest.mark.timeout(900)
+def test_ipc_direct_equals_fabric_bitwise_deterministic():
+    # the direct-to-peer stores move exactly the bytes the fabric's all-to-alls move: bitwise equal outputs
+    # (deterministic backward), and the symmetric region holds no send buffers
+    C, S, D, Hq, Hkv, d, U = 4, 1024, 512, 16, 4, 64, 4
+    res = _run_ipc(C, dict(S=S, D=D, Hq=Hq, Hkv=Hkv, d=d, U=U, det=True, direct=True))
+    fab, _ = _run_group(C, S, D, Hq, Hkv, d, U, det=True)
+    for p in range(C):
+        for k in ("y", "o", "lse", "dx", "dwq", "dwk", "dwv", "dwo"):
+            a = res[p][k].float()
+            b = fab[p][k].float().cpu()
+            assert torch.equal(a, b), (p, k, (a - b).abs().max().item())
+    plain = _run_ipc(C, dict(S=S, D=D, Hq=Hq, Hkv=Hkv, d=d, U=U, det=True, sync=True))
+    assert int(res[0]["region"][0]) < int(plain[0]["region"][0])
 
 
 @pytest.mark.timeout(900)

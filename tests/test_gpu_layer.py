@@ -96,14 +96,36 @@ def _oracle(inp, Hq, Hkv, d, causal, rope_base, bwd):
     return hit
 
 
-def _check(results, inp, C, Hq, Hkv, d, U, causal=True, bwd=True, rope_base=None, ring=1):
+def _bf16(a):
+    return torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16).double().numpy()
+
+
+def _boundary_abs(inp, Hq, Hkv, d):
+    """(max|dO|, max|dy|) of an exact emulation of the method's mandated bf16 boundaries (Q/K/V after
+    projection, O after attention, y; A15/A16) against the fp64 oracle: the absolute error a bf16
+    implementation reaches on these inputs without any kernel error (DESIGN A28)."""
+    x = inp["x"]
+    S = x.shape[0]
+    q, k, v = (_bf16(oracle.project(x, inp[w])) for w in ("wq", "wk", "wv"))
+    o, _ = oracle.attn_fwd(q.reshape(S, Hq, d), k.reshape(S, Hkv, d), v.reshape(S, Hkv, d))
+    o_emu = _bf16(o.reshape(S, Hq * d))
+    y_emu = _bf16(oracle.project(o_emu, inp["wo"]))
+    Y, O, _ = oracle.layer_fwd(x, inp["wq"], inp["wk"], inp["wv"], inp["wo"], Hq, Hkv, d)
+
+    def ulp(v):   # half a bf16 ulp at magnitude v: the kernel's own P -> bf16 rounding (A16) on top
+        return 2.0 ** (np.floor(np.log2(v)) - 8)
+    return (float(np.abs(o_emu - O).max() + ulp(np.abs(O).max())),
+            float(np.abs(y_emu - Y).max() + ulp(np.abs(Y).max())))
+
+
+def _check(results, inp, C, Hq, Hkv, d, U, causal=True, bwd=True, rope_base=None, ring=1, abs_y=ABS, abs_o=ABS):
     x, wq, wk, wv, wo, dy = (inp[k] for k in ("x", "wq", "wk", "wv", "wo", "dy"))
     ref = _oracle(inp, Hq, Hkv, d, causal, rope_base, bwd)
     Y, O, L = ref["fwd"]
     y = np.concatenate([to_np(r["y"]) for r in results], 0)
     o = np.concatenate([to_np(r["o"]) for r in results], 0)
-    assert_close("y", y, Y, REL, ABS)
-    assert_close("o_saved", o, O, REL, ABS)
+    assert_close("y", y, Y, REL, abs_y)
+    assert_close("o_saved", o, O, REL, abs_o)
     # lse: rank p holds its heads in slot order s*qpd + j (upipe.h)
     from paper_2602_21196_b200 import upipe
     sh = upipe.make_shape(x.shape[0] // C, x.shape[1], Hq, Hkv, d, U, int(causal), ring_degree=ring)
@@ -320,8 +342,12 @@ def test_32b_class_layer(C):
 @pytest.mark.timeout(1200)
 def test_mha_control_cp8():
     # SURVEY §8d control: MHA 32/32 at CP 8, chunk 8 (R = 1: every stage sends its own K/V heads)
+    # max|y| = 6.3 here: the bf16 rounding of y alone costs up to 1.5e-2 and the exact boundary emulation
+    # reaches 2.056e-2 > 2e-2, so the absolute bars for y and O are max(2e-2, emulation + half a bf16 ulp at
+    # the largest magnitude) (DESIGN A28); the relative bar stays 5e-3
     r, inp = _run_group(8, 1024, 4096, 32, 32, 128, 8)
-    _check(r, inp, 8, 32, 32, 128, 8)
+    eo, ey = _boundary_abs(inp, 32, 32, 128)
+    _check(r, inp, 8, 32, 32, 128, 8, abs_y=max(ABS, ey), abs_o=max(ABS, eo))
 
 
 @pytest.mark.parametrize("C,Hq,Hkv,d,U,ring", [(2, 8, 2, 64, 2, 1), (4, 32, 8, 128, 8, 1), (1, 8, 2, 128, 4, 1),

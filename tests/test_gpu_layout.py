@@ -196,7 +196,7 @@ def run_probe(C, ring, S_l, D, Hq, Hkv, d, U, sync, seed=0):
     (8, 1, 128, 5120, 64, 8, 128, 8, False),     # 32B-class (64Q / 8KV, D 5120): BASELINE configs[4] schedule
     (8, 1, 128, 2048, 32, 32, 64, 8, False),     # MHA control (R = 1)
     (4, 1, 128, 1024, 16, 4, 64, 16, False),     # qpd = R = 4: kv_res = 1, sigma = 1
-    (4, 1, 128, 1024, 8, 2, 64, 8, True),        # qpd = 2 < R = 4 (sigma = 2), sequential
+    (4, 1, 128, 1024, 16, 4, 64, 8, True),       # qpd = 2 < R = 4 (sigma = 2), sequential
     (4, 2, 128, 512, 8, 2, 64, 2, True),         # ring hybrid: Ulysses groups of 2 inside a ring of 2
     (8, 2, 128, 1024, 16, 4, 64, 4, True),       # 4 x 2 hybrid
 ])
