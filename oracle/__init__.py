@@ -41,6 +41,11 @@ Functions and their pins (tests/test_oracle_*.py):
 * ``hybrid_forward/backward`` (UPipe x Ring) -- pinned: equal to the
                        un-sharded layer for every (a, r, U) of a grid; a = C, r = 1 is
                        bitwise ``upipe_forward``; a = 1 is pure ring attention.
+* ``rms_norm_heads``/``rms_norm_heads_bwd`` (Qwen3 per-head q/k RMSNorm)
+                    -- pinned: the textbook RMSNorm definition on hand values, unit-RMS
+                       output for gamma = 1, scale invariance (x -> c x leaves the output
+                       unchanged up to eps), torch fp64 autograd of the composed layer and
+                       central finite differences on dX, dW and d(gamma_q), d(gamma_k).
 * ``rope``          -- pinned: complex-exponential form (each pair times e^{i p theta_i}),
                        relative-position invariance of q.k, norm preservation, position 0 =
                        identity, inverse o forward = identity; the RoPE layer's gradients by
@@ -186,32 +191,58 @@ def rope(T, positions, base, inverse=False):
     return out
 
 
-def _qkv(X, Wq, Wk, Wv, Hq, Hkv, d, rope_base, pos0=0):
+def rms_norm_heads(T, gamma, eps):
+    """Per-head RMSNorm over the head dimension (Qwen3's q_norm / k_norm, applied to each head of
+    the projected Q and K before RoPE; the paper's second model family, whose attention
+    module the paper overrides as a whole):  y = T / sqrt(mean_e T_e^2 + eps) * gamma.
+    T: [S, H, d], gamma: [d].  Returns (y, rstd [S, H])."""
+    rstd = 1.0 / np.sqrt(np.mean(T * T, axis=-1) + eps)
+    return T * rstd[..., None] * gamma, rstd
+
+
+def rms_norm_heads_bwd(T, gamma, eps, G):
+    """Chain rule of ``rms_norm_heads`` for the cotangent G of its output:
+    T_hat = T * rstd,  dT_hat = G * gamma,  dT = rstd * (dT_hat - T_hat * mean_e(dT_hat * T_hat)),
+    dgamma = sum over tokens and heads of G * T_hat.  Returns (dT, dgamma)."""
+    rstd = 1.0 / np.sqrt(np.mean(T * T, axis=-1) + eps)
+    T_hat = T * rstd[..., None]
+    dT_hat = G * gamma
+    dT = rstd[..., None] * (dT_hat - T_hat * np.mean(dT_hat * T_hat, axis=-1, keepdims=True))
+    dgamma = np.sum(G * T_hat, axis=(0, 1))
+    return dT, dgamma
+
+
+def _qkv(X, Wq, Wk, Wv, Hq, Hkv, d, rope_base, pos0=0, qk_norm=None):
     S = X.shape[0]
     Q = project(X, Wq).reshape(S, Hq, d)
     K = project(X, Wk).reshape(S, Hkv, d)
     V = project(X, Wv).reshape(S, Hkv, d)
+    if qk_norm is not None:              # (gamma_q, gamma_k, eps): Qwen3 order, norm then RoPE
+        gq, gk, eps = qk_norm
+        Q, K = rms_norm_heads(Q, gq, eps)[0], rms_norm_heads(K, gk, eps)[0]
     if rope_base:
         pos = np.arange(pos0, pos0 + S)
         Q, K = rope(Q, pos, rope_base), rope(K, pos, rope_base)
     return Q, K, V
 
 
-def layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, causal=True, rope_base=None):
+def layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, causal=True, rope_base=None, qk_norm=None):
     """Y = O Wo^T with O = attn(X Wq^T, X Wk^T, X Wv^T) (Q and K rotated by ``rope`` at their
-    token positions when ``rope_base`` is given).  Returns (Y, O [S,Hq*d], lse [Hq,S])."""
+    token positions when ``rope_base`` is given; per-head RMSNorm of Q and K first when
+    ``qk_norm`` = (gamma_q, gamma_k, eps) is given).  Returns (Y, O [S,Hq*d], lse [Hq,S])."""
     S = X.shape[0]
-    Q, K, V = _qkv(X, Wq, Wk, Wv, Hq, Hkv, d, rope_base)
+    Q, K, V = _qkv(X, Wq, Wk, Wv, Hq, Hkv, d, rope_base, qk_norm=qk_norm)
     O, lse = attn_fwd(Q, K, V, causal)
     O2 = O.reshape(S, Hq * d)
     return project(O2, Wo), O2, lse
 
 
-def layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, causal=True, rope_base=None):
+def layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, causal=True, rope_base=None, qk_norm=None):
     """(dX, dWq, dWk, dWv, dWo) of the layer for cotangent dY; with RoPE the
-    gradients w.r.t. the rotated Q/K are rotated back (chain rule through an orthogonal map)."""
+    gradients w.r.t. the rotated Q/K are rotated back (chain rule through an orthogonal map); with
+    ``qk_norm`` they then pass through ``rms_norm_heads_bwd`` and (dgamma_q, dgamma_k) are appended."""
     S = X.shape[0]
-    Q, K, V = _qkv(X, Wq, Wk, Wv, Hq, Hkv, d, rope_base)
+    Q, K, V = _qkv(X, Wq, Wk, Wv, Hq, Hkv, d, rope_base, qk_norm=qk_norm)
     O, _ = attn_fwd(Q, K, V, causal)
     O2 = O.reshape(S, Hq * d)
     dWo = dY.T @ O2
@@ -220,12 +251,18 @@ def layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, causal=True, rope_base=None):
     if rope_base:
         pos = np.arange(S)
         dQ, dK = rope(dQ, pos, rope_base, inverse=True), rope(dK, pos, rope_base, inverse=True)
+    extra = ()
+    if qk_norm is not None:
+        gq, gk, eps = qk_norm
+        dQ, dgq = rms_norm_heads_bwd(project(X, Wq).reshape(S, Hq, d), gq, eps, dQ)
+        dK, dgk = rms_norm_heads_bwd(project(X, Wk).reshape(S, Hkv, d), gk, eps, dK)
+        extra = (dgq, dgk)
     dQ2, dK2, dV2 = dQ.reshape(S, -1), dK.reshape(S, -1), dV.reshape(S, -1)
     dWq = dQ2.T @ X
     dWk = dK2.T @ X
     dWv = dV2.T @ X
     dX = dQ2 @ Wq + dK2 @ Wk + dV2 @ Wv
-    return dX, dWq, dWk, dWv, dWo
+    return (dX, dWq, dWk, dWv, dWo) + extra
 
 
 def layer_fwd_rows(X_rows, rows, K, V, Wq, Wo, Hq, Hkv, d, causal=True, rope_base=None):

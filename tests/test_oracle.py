@@ -620,3 +620,82 @@ def test_hybrid_degenerate_compositions():
     ref = O.layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d)
     for x, y in zip(ring, ref):
         np.testing.assert_allclose(x, y, atol=1e-12)
+
+
+# ---------------------------------------------------------------- Qwen3 per-head q/k RMSNorm
+
+def test_rms_norm_heads_hand_values_and_invariants():
+    # textbook RMSNorm on a hand example: T = (3, 4): mean square 12.5, gamma = (1, 2)
+    y, rstd = O.rms_norm_heads(np.array([[[3.0, 4.0]]]), np.array([1.0, 2.0]), 0.0)
+    np.testing.assert_allclose(y[0, 0], [0.8485281374238570, 2.262741699796952], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(rstd, [[1 / math.sqrt(12.5)]], rtol=1e-15)
+    T = rand(5, 3, 8)
+    y1, _ = O.rms_norm_heads(T, np.ones(8), 0.0)
+    np.testing.assert_allclose(np.mean(y1 ** 2, axis=-1), 1.0, rtol=1e-13)        # unit RMS for gamma = 1
+    np.testing.assert_allclose(O.rms_norm_heads(7.5 * T, np.ones(8), 0.0)[0], y1, rtol=1e-13)   # scale invariant
+    g = rand(8)
+    np.testing.assert_allclose(O.rms_norm_heads(T, g, 0.0)[0], y1 * g, rtol=1e-13)  # gamma is a per-dim scale
+    # eps enters under the root: rstd = 1/sqrt(ms + eps)
+    _, r2 = O.rms_norm_heads(T, g, 0.25)
+    np.testing.assert_allclose(r2, 1 / np.sqrt(np.mean(T ** 2, -1) + 0.25), rtol=1e-15)
+
+
+def test_rms_norm_heads_bwd_matches_torch_rms_norm_autograd():
+    T, G, g = rand(6, 3, 8), rand(6, 3, 8), rand(8)
+    dT, dg = O.rms_norm_heads_bwd(T, g, 1e-6, G)
+    tT, tg = torch.from_numpy(T).requires_grad_(), torch.from_numpy(g).requires_grad_()
+    ty = F.rms_norm(tT, (8,), weight=tg, eps=1e-6)            # library routine, independent of the oracle
+    np.testing.assert_allclose(O.rms_norm_heads(T, g, 1e-6)[0], ty.detach().numpy(), atol=1e-13)
+    ty.backward(torch.from_numpy(G))
+    np.testing.assert_allclose(dT, tT.grad.numpy(), atol=1e-12)
+    np.testing.assert_allclose(dg, tg.grad.numpy(), atol=1e-12)
+
+
+def _torch_layer_qknorm(X, Wq, Wk, Wv, Wo, gq, gk, Hq, Hkv, d, eps):
+    S = X.shape[0]
+    q = F.rms_norm((X @ Wq.T).view(S, Hq, d), (d,), weight=gq, eps=eps).transpose(0, 1)[None]
+    k = F.rms_norm((X @ Wk.T).view(S, Hkv, d), (d,), weight=gk, eps=eps).transpose(0, 1)[None]
+    v = (X @ Wv.T).view(S, Hkv, d).transpose(0, 1)[None]
+    o = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+    return o[0].transpose(0, 1).reshape(S, Hq * d) @ Wo.T
+
+
+def test_qk_norm_layer_matches_torch_autograd():
+    S, D, Hq, Hkv, d, eps = 40, 24, 4, 2, 8, 1e-6
+    X, Wq, Wk, Wv = rand(S, D), rand(Hq * d, D, scale=.3), rand(Hkv * d, D, scale=.3), rand(Hkv * d, D, scale=.3)
+    Wo, dY, gq, gk = rand(D, Hq * d, scale=.3), rand(S, D), 1 + 0.3 * rand(d), 1 + 0.3 * rand(d)
+    Y, _, _ = O.layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, qk_norm=(gq, gk, eps))
+    grads = O.layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, qk_norm=(gq, gk, eps))
+    assert len(grads) == 7
+    ts = [torch.from_numpy(a).requires_grad_() for a in (X, Wq, Wk, Wv, Wo, gq, gk)]
+    ty = _torch_layer_qknorm(*ts, Hq, Hkv, d, eps)
+    np.testing.assert_allclose(Y, ty.detach().numpy(), atol=1e-11)
+    ty.backward(torch.from_numpy(dY))
+    for mine, t in zip(grads, ts):
+        np.testing.assert_allclose(mine, t.grad.numpy(), atol=1e-10)
+
+
+def test_qk_norm_rope_layer_finite_differences():
+    # norm, then RoPE (Qwen3 order): every gradient incl. d(gamma_q), d(gamma_k) by central differences
+    S, D, Hq, Hkv, d, base, eps = 5, 5, 2, 1, 4, 100.0, 1e-6
+    X, Wq, Wk, Wv, Wo, dY = (rand(S, D), rand(Hq * d, D), rand(Hkv * d, D), rand(Hkv * d, D),
+                             rand(D, Hq * d), rand(S, D))
+    gq, gk = 1 + 0.3 * rand(d), 1 + 0.3 * rand(d)
+    args = [X, Wq, Wk, Wv, Wo, gq, gk]
+    grads = O.layer_bwd(X, Wq, Wk, Wv, Wo, dY, Hq, Hkv, d, rope_base=base, qk_norm=(gq, gk, eps))
+    h = 1e-5
+
+    def loss(a):
+        return float(np.sum(O.layer_fwd(*a[:5], Hq, Hkv, d, rope_base=base, qk_norm=(a[5], a[6], eps))[0] * dY))
+    for idx, g in enumerate(grads):
+        num = np.zeros_like(args[idx])
+        for i in np.ndindex(num.shape):
+            ap = [a.copy() for a in args]
+            am = [a.copy() for a in args]
+            ap[idx][i] += h
+            am[idx][i] -= h
+            num[i] = (loss(ap) - loss(am)) / (2 * h)
+        assert np.linalg.norm(num - g) <= 1e-6 * np.linalg.norm(g), idx
+    # the norm changes the layer (not silently skipped)
+    assert not np.allclose(O.layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, rope_base=base)[0],
+                           O.layer_fwd(X, Wq, Wk, Wv, Wo, Hq, Hkv, d, rope_base=base, qk_norm=(gq, gk, eps))[0])
