@@ -93,6 +93,11 @@ typedef struct {
                           all-to-all inside the group; K/V blocks (and, in backward, their fp32
                           gradient accumulators) travel around the ring of the r ranks that share u,
                           and the partial outputs are merged by their log-sum-exp. */
+  float qk_norm_eps;   /* 0: off. > 0: Qwen3 per-head RMSNorm of Q and K (the paper's second model family,
+                          P:433, DESIGN A29): each head of the projection is divided by
+                          sqrt(mean of its squares + qk_norm_eps) and scaled by its weight vector
+                          (upipe_qk_norm_t), then rotated (RoPE) if rope_base > 0. Qwen3: 1e-6.
+                          Needs upipe_attn_fwd_ex / upipe_attn_bwd_ex and ring_degree <= 1. */
 } upipe_shape_t;
 
 #define UPIPE_UID_BYTES 128
@@ -227,6 +232,29 @@ UPIPE_API upipe_status_t upipe_attn_bwd(upipe_ctx_t ctx, const upipe_shape_t* sh
                               const upipe_bf16* dy, const upipe_bf16* o_saved, const float* lse_saved,
                               upipe_bf16* dx, float* dwq, float* dwk, float* dwv, float* dwo, int reduce_dw,
                               void* workspace, size_t ws_bytes, void* stream);
+
+/* Qwen3 q/k norm weights and their gradients (shape.qk_norm_eps > 0).
+ *  q_norm_w, k_norm_w   [d] bf16 in (replicated on every rank)
+ *  dq_norm_w, dk_norm_w [d] fp32 out of upipe_attn_bwd_ex: sum over this rank's heads and all S tokens,
+ *                       summed over the CP group too when reduce_dw != 0 (ignored by the forward). */
+typedef struct {
+  const upipe_bf16* q_norm_w;
+  const upipe_bf16* k_norm_w;
+  float* dq_norm_w;
+  float* dk_norm_w;
+} upipe_qk_norm_t;
+
+/* upipe_attn_fwd / upipe_attn_bwd with the Qwen3 q/k norm weights (qkn may be NULL when
+ * shape->qk_norm_eps == 0; the plain entry points are these with qkn = NULL). */
+UPIPE_API upipe_status_t upipe_attn_fwd_ex(upipe_ctx_t ctx, const upipe_shape_t* shape, const upipe_bf16* x,
+                              const upipe_bf16* wq, const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo,
+                              const upipe_qk_norm_t* qkn, upipe_bf16* y, upipe_bf16* o_saved, float* lse_saved,
+                              void* workspace, size_t ws_bytes, void* stream);
+UPIPE_API upipe_status_t upipe_attn_bwd_ex(upipe_ctx_t ctx, const upipe_shape_t* shape, const upipe_bf16* x,
+                              const upipe_bf16* wq, const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo,
+                              const upipe_qk_norm_t* qkn, const upipe_bf16* dy, const upipe_bf16* o_saved,
+                              const float* lse_saved, upipe_bf16* dx, float* dwq, float* dwk, float* dwv, float* dwo,
+                              int reduce_dw, void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- kernel-level entry points
  * The individual steps of the hot path, exposed for per-kernel parity tests and

@@ -58,17 +58,17 @@ struct BwdArgs {
   int head_inner;    // visiting order (head, query tile): 1 = heads inner, so every CTA of the launch is at
                      // the same query tile at the same step (needed by dq_sem, whose waits then chain in lockstep)
   long long* dbg;    // optional per-role cycle breakdown of CTA (0,0) (UPIPE_BWD_TIMELINE=1)
-  // N2 (nkvseg > 0): bf16 dK / dV row t -> {dk,dv}seg[t / kvseg_rows] + (t % kvseg_rows) * ld_kvb (a peer's
-  // receive block) instead of dk_bf16 / dv_bf16
+  // N2 (nkseg / nvseg > 0): bf16 dK / dV row t -> {dk,dv}seg[t / kvseg_rows] + (t % kvseg_rows) * ld_kvb (a
+  // peer's receive block) instead of dk_bf16 / dv_bf16
   __nv_bfloat16* dkseg[kMaxSeg];
   __nv_bfloat16* dvseg[kMaxSeg];
   long long kvseg_rows;
-  int nkvseg;
+  int nkseg, nvseg;
 };
 
 // Destination row of the bf16 dK / dV epilogue (plain or N2 segmented); key < S.
 __device__ __forceinline__ __nv_bfloat16* kv_out_row(const BwdArgs& a, int which, long long key) {
-  if (a.nkvseg) return (which ? a.dkseg : a.dvseg)[key / a.kvseg_rows] + (key % a.kvseg_rows) * a.ld_kvb;
+  if (which ? a.nkseg : a.nvseg) return (which ? a.dkseg : a.dvseg)[key / a.kvseg_rows] + (key % a.kvseg_rows) * a.ld_kvb;
   return (which ? a.dk_bf16 : a.dv_bf16) + key * a.ld_kvb;
 }
 
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tcol = which ? C::TM_DK : C::TM_DV;
     const float sc = which ? a.scale : 1.f;
     float* acc = (which ? a.dk_acc : a.dv_acc);
-    const bool ob = a.nkvseg ? true : (which ? a.dk_bf16 : a.dv_bf16) != nullptr;
+    const bool ob = which ? (a.nkseg || a.dk_bf16) : (a.nvseg || a.dv_bf16);
 #pragma unroll 1
     for (int c = cbeg; c < cbeg + D; c += 32) {
       uint32_t rr[32];
@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tcol = which ? C::TM_DK : C::TM_DV;
     const float sc = which ? a.scale : 1.f;
     float* acc = (which ? a.dk_acc : a.dv_acc);
-    const bool ob = a.nkvseg ? true : (which ? a.dk_bf16 : a.dv_bf16) != nullptr;
+    const bool ob = which ? (a.nkseg || a.dk_bf16) : (a.nvseg || a.dv_bf16);
 #pragma unroll 1
     for (int c = 0; c < D; c += 32) {
       uint32_t rr[32];
@@ -988,17 +988,19 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   a.dv_acc = p.dv_acc;
   a.dk_bf16 = reinterpret_cast<__nv_bfloat16*>(p.dk_bf16);
   a.dv_bf16 = reinterpret_cast<__nv_bfloat16*>(p.dv_bf16);
-  a.nkvseg = p.dk_seg.n;
-  a.kvseg_rows = p.dk_seg.rows > 0 ? p.dk_seg.rows : 1;
+  a.nkseg = p.dk_seg.n;
+  a.nvseg = p.dv_seg.n;
+  const int64_t seg_rows = p.dk_seg.n ? p.dk_seg.rows : p.dv_seg.rows;
+  a.kvseg_rows = seg_rows > 0 ? seg_rows : 1;
   for (int i = 0; i < kMaxSeg; ++i) {
     a.dkseg[i] = reinterpret_cast<__nv_bfloat16*>(p.dk_seg.p[i]);
     a.dvseg[i] = reinterpret_cast<__nv_bfloat16*>(p.dv_seg.p[i]);
   }
-  if (a.nkvseg && (p.dv_seg.n != p.dk_seg.n || p.dv_seg.rows != p.dk_seg.rows || p.dk_seg.rows <= 0 ||
-                   p.dk_seg.n > kMaxSeg || (p.S + p.dk_seg.rows - 1) / p.dk_seg.rows > p.dk_seg.n)) {
-    snprintf(err, errlen, "attn_bwd: segmented dK/dV need matching segments covering S");
-    return cudaErrorInvalidValue;
-  }
+  for (const SegPtrs* sp : {&p.dk_seg, &p.dv_seg})
+    if (sp->n && (sp->rows != seg_rows || sp->rows <= 0 || sp->n > kMaxSeg || (p.S + sp->rows - 1) / sp->rows > sp->n)) {
+      snprintf(err, errlen, "attn_bwd: segmented dK/dV need equal segment rows covering S");
+      return cudaErrorInvalidValue;
+    }
   a.S = p.S;
   a.ld_lse = p.ld_lse;
   a.ld_delta = p.ld_delta;

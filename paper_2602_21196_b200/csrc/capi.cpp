@@ -12,17 +12,17 @@
 #include "kernels.h"
 #include "upipe_internal.h"
 
-static_assert(sizeof(upipe_shape_t) == 40, "upipe_shape_t layout is part of the ABI (Python mirror in upipe.py)");
+static_assert(sizeof(upipe_shape_t) == 48, "upipe_shape_t layout is part of the ABI (Python mirror in upipe.py)");
 static_assert(sizeof(upipe_probe_t) == 104, "upipe_probe_t layout (Python mirror in upipe.py)");
 
 namespace upipe {
 upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, const upipe_bf16* x, const upipe_bf16* wq,
-                         const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo, upipe_bf16* y,
-                         upipe_bf16* o_saved, float* lse_saved, char* ws, cudaStream_t st);
+                         const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo, const upipe_qk_norm_t* qkn,
+                         upipe_bf16* y, upipe_bf16* o_saved, float* lse_saved, char* ws, cudaStream_t st);
 upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, const upipe_bf16* x, const upipe_bf16* wq,
-                         const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo, const upipe_bf16* dy,
-                         const upipe_bf16* o_saved, const float* lse_saved, upipe_bf16* dx, float* dwq, float* dwk,
-                         float* dwv, float* dwo, int reduce_dw, char* ws, cudaStream_t st);
+                         const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo, const upipe_qk_norm_t* qkn,
+                         const upipe_bf16* dy, const upipe_bf16* o_saved, const float* lse_saved, upipe_bf16* dx,
+                         float* dwq, float* dwk, float* dwv, float* dwo, int reduce_dw, char* ws, cudaStream_t st);
 }  // namespace upipe
 
 namespace upipe {
@@ -267,13 +267,33 @@ upipe_status_t upipe_plan_stage(int cp_size, const upipe_shape_t* shape, int sta
   return UPIPE_OK;
 }
 
+namespace {
+// the q/k norm weights a shape with qk_norm_eps > 0 needs (fwd: weights; bwd: weights and gradients)
+upipe_status_t check_qkn(upipe_ctx_t ctx, const upipe_shape_t* shape, const upipe_qk_norm_t* qkn, bool bwd) {
+  if (shape->qk_norm_eps <= 0.f) return UPIPE_OK;
+  if (!qkn || !qkn->q_norm_w || !qkn->k_norm_w || (bwd && (!qkn->dq_norm_w || !qkn->dk_norm_w)))
+    return set_err(ctx, UPIPE_ERR_INVALID_ARG, "qk_norm_eps > 0 needs upipe_qk_norm_t weights (and gradients in bwd)");
+  if (!all_aligned(qkn->q_norm_w, qkn->k_norm_w) || (bwd && !all_aligned(qkn->dq_norm_w, qkn->dk_norm_w)))
+    return set_err(ctx, UPIPE_ERR_INVALID_ARG, "q/k norm weights must be 16-byte aligned");
+  return UPIPE_OK;
+}
+}  // namespace
+
 upipe_status_t upipe_attn_fwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const upipe_bf16* x, const upipe_bf16* wq,
                               const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo, upipe_bf16* y,
                               upipe_bf16* o_saved, float* lse_saved, void* workspace, size_t ws_bytes,
                               void* stream) {
+  return upipe_attn_fwd_ex(ctx, shape, x, wq, wk, wv, wo, nullptr, y, o_saved, lse_saved, workspace, ws_bytes, stream);
+}
+
+upipe_status_t upipe_attn_fwd_ex(upipe_ctx_t ctx, const upipe_shape_t* shape, const upipe_bf16* x,
+                                 const upipe_bf16* wq, const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo,
+                                 const upipe_qk_norm_t* qkn, upipe_bf16* y, upipe_bf16* o_saved, float* lse_saved,
+                                 void* workspace, size_t ws_bytes, void* stream) {
   if (upipe_status_t st = check_ctx(ctx)) return st;
   std::string m;
   if (upipe_status_t st = validate_shape(ctx->C, shape, m)) return set_err(ctx, st, m);
+  if (upipe_status_t st = check_qkn(ctx, shape, qkn, false)) return st;
   if (!x || !wq || !wk || !wv || !wo || !y || !o_saved || !lse_saved || !resolve_ws(ctx, workspace, ws_bytes))
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "null tensor pointer");
   if (!all_aligned(x, wq, wk, wv, wo, y, o_saved, lse_saved) || (reinterpret_cast<uintptr_t>(workspace) & 255))
@@ -283,7 +303,7 @@ upipe_status_t upipe_attn_fwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
   if (ws_bytes < fwd_workspace(P, overlap_enabled(ctx->flags, P), direct_enabled(ctx->flags, P)).total)
     return set_err(ctx, UPIPE_ERR_WORKSPACE, "ws_bytes < upipe_workspace_size(pass=0, or 2 with UPIPE_FLAG_SYNC_COMM)");
   cudaSetDevice(ctx->device);
-  return layer_fwd(ctx, P, x, wq, wk, wv, wo, y, o_saved, lse_saved, static_cast<char*>(workspace),
+  return layer_fwd(ctx, P, x, wq, wk, wv, wo, qkn, y, o_saved, lse_saved, static_cast<char*>(workspace),
                    static_cast<cudaStream_t>(stream));
 }
 
@@ -292,9 +312,19 @@ upipe_status_t upipe_attn_bwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
                               const upipe_bf16* dy, const upipe_bf16* o_saved, const float* lse_saved,
                               upipe_bf16* dx, float* dwq, float* dwk, float* dwv, float* dwo, int reduce_dw,
                               void* workspace, size_t ws_bytes, void* stream) {
+  return upipe_attn_bwd_ex(ctx, shape, x, wq, wk, wv, wo, nullptr, dy, o_saved, lse_saved, dx, dwq, dwk, dwv, dwo,
+                           reduce_dw, workspace, ws_bytes, stream);
+}
+
+upipe_status_t upipe_attn_bwd_ex(upipe_ctx_t ctx, const upipe_shape_t* shape, const upipe_bf16* x,
+                                 const upipe_bf16* wq, const upipe_bf16* wk, const upipe_bf16* wv, const upipe_bf16* wo,
+                                 const upipe_qk_norm_t* qkn, const upipe_bf16* dy, const upipe_bf16* o_saved,
+                                 const float* lse_saved, upipe_bf16* dx, float* dwq, float* dwk, float* dwv, float* dwo,
+                                 int reduce_dw, void* workspace, size_t ws_bytes, void* stream) {
   if (upipe_status_t st = check_ctx(ctx)) return st;
   std::string m;
   if (upipe_status_t st = validate_shape(ctx->C, shape, m)) return set_err(ctx, st, m);
+  if (upipe_status_t st = check_qkn(ctx, shape, qkn, true)) return st;
   if (!x || !wq || !wk || !wv || !wo || !dy || !o_saved || !lse_saved || !dx || !dwq || !dwk || !dwv || !dwo ||
       !resolve_ws(ctx, workspace, ws_bytes))
     return set_err(ctx, UPIPE_ERR_INVALID_ARG, "null tensor pointer");
@@ -306,7 +336,7 @@ upipe_status_t upipe_attn_bwd(upipe_ctx_t ctx, const upipe_shape_t* shape, const
   if (ws_bytes < bwd_workspace(P, overlap_enabled(ctx->flags, P), direct_enabled(ctx->flags, P)).total)
     return set_err(ctx, UPIPE_ERR_WORKSPACE, "ws_bytes < upipe_workspace_size(pass=1, or 3 with UPIPE_FLAG_SYNC_COMM)");
   cudaSetDevice(ctx->device);
-  return layer_bwd(ctx, P, x, wq, wk, wv, wo, dy, o_saved, lse_saved, dx, dwq, dwk, dwv, dwo, reduce_dw,
+  return layer_bwd(ctx, P, x, wq, wk, wv, wo, qkn, dy, o_saved, lse_saved, dx, dwq, dwk, dwv, dwo, reduce_dw,
                    static_cast<char*>(workspace), static_cast<cudaStream_t>(stream));
 }
 

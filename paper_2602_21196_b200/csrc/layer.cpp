@@ -218,7 +218,8 @@ bool peer_blocks(Transport& T, int first, int C, int me, const char* local_recv,
 
 // ============================================================================ forward
 upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf16p wk, bf16p wv, bf16p wo,
-                         upipe_bf16* y, upipe_bf16* o_saved, float* lse_saved, char* ws, cudaStream_t st) {
+                         const upipe_qk_norm_t* qkn, upipe_bf16* y, upipe_bf16* o_saved, float* lse_saved, char* ws,
+                         cudaStream_t st) {
   const bool ov = overlap_enabled(ctx->flags, P);
   const bool dir = direct_enabled(ctx->flags, P);        // N2: producers write the peers' receive buffers
   if (upipe_status_t s = check_direct(ctx, P)) return s;
@@ -230,6 +231,12 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   const FwdWs W = fwd_workspace(P, ov, dir);
   RopeRef rope_seq;                        // projections: rows are this rank's tokens rank*S_l + t
   if (upipe_status_t s = ensure_rope(ctx, P, rope_seq)) return s;
+  // Qwen3 q/k norm (DESIGN A29): the projections send the pre-norm heads; each head owner normalises (and
+  // rotates: RoPE follows the norm) its received rows in place before the attention
+  const bool qknorm = P.sh.qk_norm_eps > 0.f;
+  RopeRef rope_head = rope_seq;            // head layout: rows are the global tokens 0..S-1 (no ring with q/k norm)
+  rope_head.pos0 = 0;
+  if (qknorm) rope_seq = RopeRef{};
   rope_seq.pos0 = (int64_t)ctx->rank * P.S_l;
   // Ulysses group of the ring hybrid (DESIGN A27): ranks [first, first + C); plain UPipe: first = 0, C = cp_size
   const int C = P.C, me = ctx->rank % P.C, d = P.d;
@@ -318,6 +325,17 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
         return probe_copy(ws + W.osend[b], pr.o_head, (size_t)P.S * qseg * 2, q);
       });
       return;
+    }
+    if (qknorm) {
+      R.run(UPIPE_TRACE_AUX, q, "q norm", [&](char*) {
+        return qk_prep_run(ws + W.qrecv[b], ws + W.qrecv[b], P.S, P.qpd, d, qseg, qkn->q_norm_w, P.sh.qk_norm_eps,
+                           rope_head, q);
+      });
+      if (P.kv_sent(s))                    // once per super-stage: the K heads stay resident for sigma stages
+        R.run(UPIPE_TRACE_AUX, q, "k norm", [&](char*) {
+          return qk_prep_run(ws + W.krecv[kvb(s)], ws + W.krecv[kvb(s)], P.S, P.kv_res, d, kseg, qkn->k_norm_w,
+                             P.sh.qk_norm_eps, rope_head, q);
+        });
     }
     AttnFwdProblem a{};
     a.q = ws + W.qrecv[b];
@@ -513,8 +531,8 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
 
 // ============================================================================ backward
 upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf16p wk, bf16p wv, bf16p wo,
-                         bf16p dy, bf16p o_saved, const float* lse_saved, upipe_bf16* dx, float* dwq, float* dwk,
-                         float* dwv, float* dwo, int reduce_dw, char* ws, cudaStream_t st) {
+                         const upipe_qk_norm_t* qkn, bf16p dy, bf16p o_saved, const float* lse_saved, upipe_bf16* dx,
+                         float* dwq, float* dwk, float* dwv, float* dwo, int reduce_dw, char* ws, cudaStream_t st) {
   const bool ov = overlap_enabled(ctx->flags, P);
   const bool dir = direct_enabled(ctx->flags, P);        // N2: producers write the peers' receive buffers
   if (upipe_status_t s = check_direct(ctx, P)) return s;
@@ -530,6 +548,8 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   if (upipe_status_t s = ensure_rope(ctx, P, rope_seq)) return s;
   rope_head = rope_seq;
   rope_head.pos0 = (int64_t)ring_i * P.S;
+  const bool qknorm = P.sh.qk_norm_eps > 0.f;   // DESIGN A29: projections send pre-norm heads (no RoPE there)
+  if (qknorm) rope_seq = RopeRef{};
   rope_seq.pos0 = (int64_t)ctx->rank * P.S_l;
   auto a2a = [&](const char* what, const void* snd, void* rcv, size_t bytes, cudaStream_t q) {
     R.comm(q, what, [&](std::string& m) { return T.alltoall_group(snd, rcv, bytes, first, C, q, m); });
@@ -556,6 +576,10 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     R.comm(q, what, [&](std::string& m) { return T.push_end(e, first, C, q, m); });
   };
 
+  if (qknorm)                                           // d(gamma_q), d(gamma_k) accumulate over the stages
+    R.run(UPIPE_TRACE_AUX, st, "memset d(gamma)", [&](char*) {
+      return cudaMemsetAsync(ws + W.dgam, 0, (size_t)2 * d * 4, st);
+    });
   // dWo = dY^T O over this rank's tokens (all stages at once: o_saved holds every head)
   {
     GemmProblem g;
@@ -729,9 +753,20 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     });
     const int r = P.kv_pos(s);
     const bool last = P.kv_last(s);
+    if (qknorm) {                                     // normalised (+ RoPE) copies; the receive buffers keep the
+      R.run(UPIPE_TRACE_AUX, q, "q norm", [&](char*) {   // pre-norm heads for the chain rule below
+        return qk_prep_run(ws + W.qrecv[b], ws + W.qn[b], P.S, P.qpd, d, qseg, qkn->q_norm_w, P.sh.qk_norm_eps,
+                           rope_head, q);
+      });
+      if (P.kv_sent(s))
+        R.run(UPIPE_TRACE_AUX, q, "k norm", [&](char*) {
+          return qk_prep_run(ws + W.krecv[kvb(s)], ws + W.kn[kvb(s)], P.S, P.kv_res, d, kseg, qkn->k_norm_w,
+                             P.sh.qk_norm_eps, rope_head, q);
+        });
+    }
     AttnBwdProblem bp{};
-    bp.q = ws + W.qrecv[b];
-    bp.k = ws + W.krecv[kvb(s)];
+    bp.q = qknorm ? ws + W.qn[b] : ws + W.qrecv[b];
+    bp.k = qknorm ? ws + W.kn[kvb(s)] : ws + W.krecv[kvb(s)];
     bp.v = ws + W.vrecv[kvb(s)];
     bp.dout = ws + W.dorecv[b];
     bp.lse = lse_saved + (int64_t)s * P.qpd * P.S;
@@ -741,12 +776,13 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     bp.dv_acc = P.sigma > 1 && !P.naive ? (float*)(ws + W.dvacc) : nullptr;
     bp.dk_bf16 = last ? ws + W.dksend : nullptr;
     bp.dv_bf16 = last ? ws + W.dvsend : nullptr;
-    SegPtrs dq_seg;                                   // N2: dQ / dK / dV rows of rank p's tokens -> peer p
+    SegPtrs dq_seg, dk_seg;                           // N2: dQ / dK / dV rows of rank p's tokens -> peer p
     if (dir) {
       bool ok = peer_blocks(T, first, C, me, ws + W.dqrecv[b], qbytes, P.S_l, dq_seg);
       if (last) {
-        ok = ok && peer_blocks(T, first, C, me, ws + W.dkrecv, kbytes, P.S_l, bp.dk_seg) &&
+        ok = ok && peer_blocks(T, first, C, me, ws + W.dkrecv, kbytes, P.S_l, dk_seg) &&
              peer_blocks(T, first, C, me, ws + W.dvrecv, kbytes, P.S_l, bp.dv_seg);
+        bp.dk_seg = dk_seg;
         bp.dk_bf16 = bp.dv_bf16 = nullptr;
       }
       if (!ok) {
@@ -769,6 +805,12 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     bp.kv_accumulate = r > 0;
     bp.kv_write_acc = !last;
     bp.rope = rope_head;
+    if (qknorm) {                                     // dK leaves in fp32 (pre-RoPE chain rule below)
+      bp.dk_acc = (float*)(ws + W.dkacc);
+      bp.kv_write_acc = 1;
+      bp.dk_bf16 = nullptr;
+      bp.dk_seg = SegPtrs{};
+    }
     bp.dq_dim_major = attn_bwd_dq_dim_major(bp) ? 1 : 0;   // [qpd*d][S] accumulator (64-query kernel)
     bp.ld_dqt = (P.S + 3) & ~int64_t(3);                  // 16-byte TMA row stride
     // UPIPE_FLAG_DETERMINISTIC: dQ partials added in key-tile order; fresh semaphores per launch
@@ -850,6 +892,22 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
           return cvt_f32_bf16_run((const float*)(ws + W.dvacc), kseg, ws + W.dvsend, kseg, P.S, kseg, 1.0f, q);
         });
       }
+    }
+    if (qknorm) {
+      // chain rule of the q/k norm fused into the gradients' fp32 -> bf16 conversion (A29): inverse RoPE, then
+      // d(pre-norm) from the pre-norm heads still in the receive buffers; d(gamma) accumulates in the workspace
+      R.run(UPIPE_TRACE_AUX, q, "dQ norm bwd", [&](char*) {
+        return norm_bwd_run((const float*)(ws + W.dqacc[b]), bp.dq_dim_major ? bp.ld_dqt : qseg, bp.dq_dim_major != 0,
+                            ws + W.qrecv[b], qseg, dir ? nullptr : ws + W.dqsend[b], qseg, dir ? &dq_seg : nullptr,
+                            P.S, P.qpd, d, 1.0f, qkn->q_norm_w, P.sh.qk_norm_eps, rope_head, (float*)(ws + W.dgam), q);
+      });
+      if (last)
+        R.run(UPIPE_TRACE_AUX, q, "dK norm bwd", [&](char*) {
+          return norm_bwd_run((const float*)(ws + W.dkacc), kseg, false, ws + W.krecv[kvb(s)], kseg,
+                              dir ? nullptr : ws + W.dksend, kseg, dir ? &dk_seg : nullptr, P.S, P.kv_res, d, 1.0f,
+                              qkn->k_norm_w, P.sh.qk_norm_eps, rope_head, (float*)(ws + W.dgam) + d, q);
+        });
+      return;
     }
     R.run(UPIPE_TRACE_AUX, q, "cvt dQ", [&](char*) {
       if (bp.dq_dim_major)
@@ -979,8 +1037,19 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     cudaStreamWaitEvent(st, e_out[(nu - 1) & 1], 0);
     post(nu - 1, (nu - 1) & 1, st);
   }
+  if (qknorm && R.status == UPIPE_OK)
+    R.run(UPIPE_TRACE_AUX, st, "d(gamma) out", [&](char*) {
+      cudaError_t e = cudaMemcpyAsync(qkn->dq_norm_w, ws + W.dgam, (size_t)d * 4, cudaMemcpyDeviceToDevice, st);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(qkn->dk_norm_w, ws + W.dgam + (size_t)d * 4, (size_t)d * 4, cudaMemcpyDeviceToDevice, st);
+      return e;
+    });
   // B7: dW summed over the CP group (the FSDP gradient reduction of P:437, A14)
   if (reduce_dw && T.size() > 1 && R.status == UPIPE_OK) {
+    if (qknorm) {
+      R.comm(st, "allreduce d(gamma_q)", [&](std::string& m) { return T.allreduce_sum_f32(qkn->dq_norm_w, d, st, m); });
+      R.comm(st, "allreduce d(gamma_k)", [&](std::string& m) { return T.allreduce_sum_f32(qkn->dk_norm_w, d, st, m); });
+    }
     R.comm(st, "allreduce dWq", [&](std::string& m) { return T.allreduce_sum_f32(dwq, (size_t)HqD * P.D, st, m); });
     R.comm(st, "allreduce dWk", [&](std::string& m) { return T.allreduce_sum_f32(dwk, (size_t)HkvD * P.D, st, m); });
     R.comm(st, "allreduce dWv", [&](std::string& m) { return T.allreduce_sum_f32(dwv, (size_t)HkvD * P.D, st, m); });

@@ -5,6 +5,8 @@
 //   unpack_cols out-a2a receive [C][S_l][qpd d] -> o_saved    (F5)
 //   synth_fill  device copy of the counter-based input generator (synth/__init__.py)
 //   merge       ring-step combine of two attention partials by their LSE
+//   qk_prep     Qwen3 per-head RMSNorm (+ RoPE) of the received Q / K rows
+//   norm_bwd    its chain rule fused into the fp32 -> bf16 conversion of dQ / dK (+ d(gamma))
 #include <algorithm>
 #include <cstdio>
 
@@ -176,6 +178,148 @@ __global__ void unpack_kernel(const uint4* __restrict__ src, long long rows, int
       *reinterpret_cast<uint4*>(dp + t * ldd + v * 8) = __ldcs(sp + t * seg_v + v);
 }
 
+// ---------------------------------------------------------------- Qwen3 q/k RMSNorm
+// One (row, head) of d dims is handled by a group of G = d / 8 consecutive lanes, 8 dims each (16-byte
+// bf16 vectors); the group reduces its sum of squares / dot products with xor-shuffles.
+template <int G>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// dst[t][h] = rope(src[t][h] * rstd * gamma), rstd = 1/sqrt(mean(src^2) + eps)   (dst may alias src)
+template <int G>
+__global__ void qk_prep_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst, long long rows, int heads, long long ld,
+                               const __nv_bfloat16* __restrict__ gamma, float eps, RopeRef rope) {
+  constexpr int d = G * 8;
+  const int sub = threadIdx.x % G;
+  float gm[8];
+  bf16x8_to_f32(*reinterpret_cast<const uint4*>(gamma + sub * 8), gm);
+  const long long groups = rows * heads;
+  const long long gstride = (long long)gridDim.x * blockDim.x / G;
+  // warp-uniform trip count (the group reductions shuffle across the whole warp); lanes past the end idle
+  const long long g0 = ((long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) / G;
+  for (long long gw = g0; gw < groups; gw += gstride) {
+    const long long gi = gw + (threadIdx.x & 31) / G;
+    const bool ok = gi < groups;
+    const long long t = ok ? gi / heads : 0;
+    const int h = ok ? (int)(gi % heads) : 0;
+    const long long off = t * ld + (long long)h * d + sub * 8;
+    float v[8];
+    if (ok) {
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(src + off), v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 0.f;
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss = fmaf(v[i], v[i], ss);
+    const float rstd = rsqrtf(group_sum<G>(ss) * (1.f / d) + eps);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = v[i] * rstd * gm[i];
+    if (!ok) continue;
+    if (rope.hi) dev::rope_rotate<4>(v, rope.hi, rope.lo, d, rope.pos0 + t, sub * 8, 1.f);
+    *reinterpret_cast<uint4*>(dst + off) =
+        make_uint4(dev::pack_bf16(v[0], v[1]), dev::pack_bf16(v[2], v[3]), dev::pack_bf16(v[4], v[5]),
+                   dev::pack_bf16(v[6], v[7]));
+  }
+}
+
+// Chain rule of qk_prep for one (row t, head h), fused into the fp32 -> bf16 conversion of the gradient:
+//   g = rope^-1(scale * src)  (gradient w.r.t. the normalised, pre-RoPE head),  x = the pre-norm head,
+//   x_hat = x rstd,  dx = rstd (g gamma - x_hat mean(g gamma x_hat)),  d(gamma) += g x_hat.
+// Tiles of 64 rows x one head through shared memory; src element (t, c) at src[t * st + c] (row-major,
+// DIM_MAJOR = false) or src[c * st + t] (dim-major dQ accumulator [heads d][S]).
+template <int G, bool DIM_MAJOR>
+__global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__ src, long long st,
+                                                       const __nv_bfloat16* __restrict__ x, long long ldx,
+                                                       __nv_bfloat16* __restrict__ dst, long long ldd, SegPtrs seg,
+                                                       long long rows, int heads, float scale,
+                                                       const __nv_bfloat16* __restrict__ gamma, float eps,
+                                                       RopeRef rope, float* __restrict__ dgamma) {
+  constexpr int d = G * 8;
+  __shared__ float tile[d][65];
+  __shared__ float red[d];
+  const int t = threadIdx.x;
+  const int sub = t % G;                            // fixed 8-dim chunk of this thread
+  for (int i = t; i < d; i += blockDim.x) red[i] = 0.f;
+  float gm[8], acc[8];
+  bf16x8_to_f32(*reinterpret_cast<const uint4*>(gamma + sub * 8), gm);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  const long long ntt = (rows + 63) / 64;
+  for (long long blk = blockIdx.x; blk < ntt * heads; blk += gridDim.x) {
+    const long long t0 = (blk / heads) * 64;
+    const int h = (int)(blk % heads);
+    __syncthreads();
+    if (DIM_MAJOR) {                                // dim c of the head: 64 consecutive tokens
+      for (int it = t; it < d * 16; it += blockDim.x) {
+        const int c = it >> 4, tk = (it & 15) * 4;
+        const float* sp = src + ((long long)h * d + c) * st + t0 + tk;
+        if ((st & 3) == 0 && t0 + tk + 4 <= rows) {
+          const float4 v4 = *reinterpret_cast<const float4*>(sp);
+          tile[c][tk] = v4.x; tile[c][tk + 1] = v4.y; tile[c][tk + 2] = v4.z; tile[c][tk + 3] = v4.w;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) tile[c][tk + k] = (t0 + tk + k < rows) ? sp[k] : 0.f;
+        }
+      }
+    } else {                                        // token tk: d consecutive dims
+      for (int it = t; it < 64 * (d / 4); it += blockDim.x) {
+        const int tk = it / (d / 4), c = (it % (d / 4)) * 4;
+        float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (t0 + tk < rows) v4 = *reinterpret_cast<const float4*>(src + (t0 + tk) * st + (long long)h * d + c);
+        tile[c][tk] = v4.x; tile[c + 1][tk] = v4.y; tile[c + 2][tk] = v4.z; tile[c + 3][tk] = v4.w;
+      }
+    }
+    __syncthreads();
+    for (int it = t; it < 64 * G; it += blockDim.x) {
+      const int tk = it / G;
+      const long long r = t0 + tk;
+      const bool ok = r < rows;                     // uniform within the G-lane group
+      float g[8], xv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) g[i] = tile[sub * 8 + i][tk] * scale;
+      if (rope.hi) dev::rope_rotate<4>(g, rope.hi, rope.lo, d, rope.pos0 + (ok ? r : 0), sub * 8, -1.f);
+      if (ok) {
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(x + r * ldx + (long long)h * d + sub * 8), xv);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xv[i] = 0.f;
+      }
+      float ss = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss = fmaf(xv[i], xv[i], ss);
+      const float rstd = rsqrtf(group_sum<G>(ss) * (1.f / d) + eps);
+      float dot = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        xv[i] *= rstd;                              // x_hat
+        dot = fmaf(g[i] * gm[i], xv[i], dot);
+        acc[i] = fmaf(g[i], xv[i], acc[i]);        // d(gamma): rows past the end contribute 0 (g = 0)
+      }
+      const float m = group_sum<G>(dot) * (1.f / d);
+      float o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = rstd * (g[i] * gm[i] - xv[i] * m);
+      if (ok) {
+        __nv_bfloat16* drow = seg.n ? reinterpret_cast<__nv_bfloat16*>(seg.p[r / seg.rows]) + (r % seg.rows) * ldd
+                                    : dst + r * ldd;
+        *reinterpret_cast<uint4*>(drow + (long long)h * d + sub * 8) =
+            make_uint4(dev::pack_bf16(o[0], o[1]), dev::pack_bf16(o[2], o[3]), dev::pack_bf16(o[4], o[5]),
+                       dev::pack_bf16(o[6], o[7]));
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) atomicAdd(&red[sub * 8 + i], acc[i]);
+  __syncthreads();
+  for (int i = t; i < d; i += blockDim.x) atomicAdd(dgamma + i, red[i]);
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
   z ^= z >> 30;
   z *= 0xBF58476D1CE4E5B9ull;
@@ -284,6 +428,41 @@ cudaError_t unpack_cols_run(const void* src, int64_t rows, int nseg, int seg_col
   if (bx > cap) bx = cap;
   unpack_kernel<<<dim3((unsigned)bx, (unsigned)nseg), kThreads, 0, s>>>(
       (const uint4*)src, rows, seg_v, (__nv_bfloat16*)dst, ldd, col_base, col_stride);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t qk_prep_run(const void* src, void* dst, int64_t rows, int heads, int d, int64_t ld, const void* gamma,
+                        float eps, const RopeRef& rope, cudaStream_t s) {
+  if (rows <= 0 || heads <= 0) return cudaSuccess;
+  const int64_t threads = rows * heads * (d / 8);
+  const auto* sp = static_cast<const __nv_bfloat16*>(src);
+  auto* dp = static_cast<__nv_bfloat16*>(dst);
+  const auto* gp = static_cast<const __nv_bfloat16*>(gamma);
+  if (d == 128) qk_prep_kernel<16><<<grid_for(threads, kThreads), kThreads, 0, s>>>(sp, dp, rows, heads, ld, gp, eps, rope);
+  else if (d == 64) qk_prep_kernel<8><<<grid_for(threads, kThreads), kThreads, 0, s>>>(sp, dp, rows, heads, ld, gp, eps, rope);
+  else return cudaErrorInvalidValue;
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t norm_bwd_run(const float* src, int64_t st, bool dim_major, const void* x, int64_t ldx, void* dst,
+                         int64_t ldd, const SegPtrs* dst_seg, int64_t rows, int heads, int d, float scale,
+                         const void* gamma, float eps, const RopeRef& inverse_rope, float* dgamma, cudaStream_t s) {
+  if (rows <= 0 || heads <= 0) return cudaSuccess;
+  if (dst_seg && dst_seg->n && !seg_covers(*dst_seg, rows)) return cudaErrorInvalidValue;
+  const SegPtrs seg = dst_seg ? *dst_seg : SegPtrs{};
+  const long long tiles = ((rows + 63) / 64) * heads;
+  const int grid = (int)(tiles < 148 * 6 ? tiles : 148 * 6);
+  const auto* xp = static_cast<const __nv_bfloat16*>(x);
+  auto* dp = static_cast<__nv_bfloat16*>(dst);
+  const auto* gp = static_cast<const __nv_bfloat16*>(gamma);
+#define UPIPE_NORM_BWD(G, DM) \
+  norm_bwd_kernel<G, DM><<<grid, 256, 0, s>>>(src, st, xp, ldx, dp, ldd, seg, rows, heads, scale, gp, eps, inverse_rope, dgamma)
+  if (d == 128) { if (dim_major) UPIPE_NORM_BWD(16, true); else UPIPE_NORM_BWD(16, false); }
+  else if (d == 64) { if (dim_major) UPIPE_NORM_BWD(8, true); else UPIPE_NORM_BWD(8, false); }
+  else return cudaErrorInvalidValue;
+#undef UPIPE_NORM_BWD
   count_launches(1);
   return cudaGetLastError();
 }

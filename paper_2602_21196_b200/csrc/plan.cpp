@@ -32,6 +32,10 @@ upipe_status_t validate_shape(int C, const upipe_shape_t* sh, std::string& msg) 
   if (sh->causal != 0 && sh->causal != 1) return bad(UPIPE_ERR_INVALID_ARG, "causal must be 0 or 1");
   if (!(sh->rope_base == 0.f || (sh->rope_base > 1.f && sh->rope_base < 1e30f)))
     return bad(UPIPE_ERR_INVALID_ARG, "rope_base must be 0 (off) or a finite base > 1 (DESIGN A26)");
+  if (!(sh->qk_norm_eps >= 0.f && sh->qk_norm_eps < 1.f))
+    return bad(UPIPE_ERR_INVALID_ARG, "qk_norm_eps must be 0 (off) or in (0, 1) (Qwen3: 1e-6; DESIGN A29)");
+  if (sh->qk_norm_eps > 0.f && ring > 1)
+    return bad(UPIPE_ERR_UNSUPPORTED, "qk_norm_eps > 0 with ring_degree > 1 (DESIGN A29)");
   if (sh->head_dim != 64 && sh->head_dim != 128) return bad(UPIPE_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
   if (sh->hidden < 64 || sh->hidden % 64) return bad(UPIPE_ERR_UNSUPPORTED, "hidden % 64 != 0 (TMA tile granule)");
   if (sh->n_kv_heads % C)
@@ -165,6 +169,15 @@ BwdWs bwd_workspace(const Plan& p, bool overlap, bool direct) {
   w.dkrecv = comm ? take(ke) : w.dksend;
   w.dvrecv = comm ? take(ke) : w.dvsend;
   w.dxacc = p.nstages > 1 ? take((size_t)p.S_l * p.D * 4) : 0;   // one stage: dX is stored in bf16 directly
+  if (p.sh.qk_norm_eps > 0.f) {             // Qwen3 q/k norm (DESIGN A29): normalised copies for the attention
+    for (int i = 0; i < 2; ++i) {           // (the receive buffers keep the pre-norm heads for the chain rule),
+      const bool fresh = i == 0 || dbl;     // fp32 dK for the fused norm backward, d(gamma) scratch
+      w.qn[i] = fresh ? take(qe) : w.qn[0];
+      w.kn[i] = fresh ? take(ke) : w.kn[0];
+    }
+    if (!w.dkacc) w.dkacc = take(ke * 2);
+    w.dgam = take((size_t)2 * p.d * 4);
+  }
   w.dqsem = take((size_t)attn_bwd_sem_count(p.S, p.qpd) * 4);     // deterministic mode (a few hundred KB)
   w.total = off;
   return w;

@@ -55,6 +55,7 @@ struct BwdWs {
   size_t qsend[2], qrecv[2], ksend, krecv[2], vsend, vrecv[2], dosend[2], dorecv[2], dsend[2], drecv[2], dqacc[2],
       dqsend[2], dqrecv[2], dkacc, dvacc, dksend, dvsend, dkrecv, dvrecv, dxacc;
   size_t dqsem;                                       // UPIPE_FLAG_DETERMINISTIC dQ-order semaphores (int32)
+  size_t qn[2], kn[2], dgam;                          // Qwen3 q/k norm (shape.qk_norm_eps > 0) only
   size_t kring[2], vring[2], dkring[2], dvring[2];   // ring hybrid only
   size_t total;
 };

@@ -19,7 +19,8 @@ class UPipeAttention:
                  causal: bool = True, process_group=None, device=None, fabric=None, cp_rank: int | None = None,
                  cp_size: int | None = None, sync_comm: bool = False, naive_kv: bool = False,
                  rope_base: float = 0.0, ring_degree: int = 1, deterministic: bool = False,
-                 transport: str = "nccl", max_seq_local: int | None = None, direct: bool = False):
+                 transport: str = "nccl", max_seq_local: int | None = None, direct: bool = False,
+                 qk_norm_eps: float = 0.0):
         """CP group: ``process_group`` (torch.distributed, one process per GPU, NCCL transport),
         or ``fabric`` + ``cp_rank`` + ``cp_size`` (single-process group driven by one host thread per rank),
         or neither (C = 1). ``sync_comm``: sequential schedule with one chunk buffer set (the
@@ -32,13 +33,16 @@ class UPipeAttention:
         backend, gloo included), the library owns the symmetric workspace (sized for ``max_seq_local``).
         ``direct`` (with ``transport="ipc"``, UPIPE_FLAG_DIRECT): the all-to-alls are fused into their
         producers -- projection / attention / dQ-conversion epilogues store straight into the owners'
-        receive buffers, no send buffers."""
+        receive buffers, no send buffers.
+        ``qk_norm_eps`` > 0: Qwen3 per-head RMSNorm of Q and K (DESIGN A29); ``forward`` then takes
+        ``q_norm_w``, ``k_norm_w`` (bf16 [head_dim]) and ``backward`` returns their fp32 gradients too."""
         self.Hq, self.Hkv, self.d, self.D, self.U = n_q_heads, n_kv_heads, head_dim, hidden, chunk_heads
         self.ipc = False
         self.region_bytes = 0
         self.causal = int(causal)
         self.rope_base = float(rope_base)    # 0: no RoPE; else rotary base (Llama3: 500000), DESIGN A26
         self.ring = max(1, int(ring_degree))
+        self.qk_norm_eps = float(qk_norm_eps)
         # UPIPE_FLAG_SYNC_COMM, UPIPE_FLAG_NAIVE_KV, UPIPE_FLAG_DETERMINISTIC
         # UPIPE_FLAG_DIRECT (8): direct-to-peer all-to-alls fused into the producing kernels (IPC only)
         if direct and transport != "ipc":
@@ -77,7 +81,7 @@ class UPipeAttention:
 
     def shape(self, seq_local: int) -> U.upipe_shape_t:
         return U.make_shape(seq_local, self.D, self.Hq, self.Hkv, self.d, self.U, self.causal, self.rope_base,
-                            self.ring)
+                            self.ring, self.qk_norm_eps)
 
     def workspace(self, seq_local: int, pass_: int) -> torch.Tensor:
         # One chunk-buffer workspace per sequence length, shared by the forward and the backward pass
@@ -92,7 +96,12 @@ class UPipeAttention:
     def release_workspace(self):
         self._ws.clear()
 
-    def forward(self, x, wq, wk, wv, wo, stream=None):
+    def _norm_w(self, q_norm_w, k_norm_w):
+        if self.qk_norm_eps > 0 and (q_norm_w is None or k_norm_w is None):
+            raise ValueError("qk_norm_eps > 0: pass q_norm_w and k_norm_w")
+        return (q_norm_w, k_norm_w) if self.qk_norm_eps > 0 else None
+
+    def forward(self, x, wq, wk, wv, wo, stream=None, q_norm_w=None, k_norm_w=None):
         S_l = x.shape[0]
         sh = self.shape(S_l)
         y = torch.empty((S_l, self.D), dtype=torch.bfloat16, device=x.device)
@@ -100,10 +109,12 @@ class UPipeAttention:
         a = self.C // self.ring                  # Ulysses degree; lse covers the rank's heads over its group's tokens
         lse = torch.empty((self.Hq // a, S_l * a), dtype=torch.float32, device=x.device)
         ws = None if self.ipc else self.workspace(S_l, 0)     # IPC: the library's symmetric region
-        U.upipe_attn_fwd(self.ctx, sh, x, wq, wk, wv, wo, y, o_saved, lse, ws, stream=stream)
+        U.upipe_attn_fwd(self.ctx, sh, x, wq, wk, wv, wo, y, o_saved, lse, ws, stream=stream,
+                         qk_norm=self._norm_w(q_norm_w, k_norm_w))
         return y, (o_saved, lse)
 
-    def backward(self, x, wq, wk, wv, wo, dy, saved, reduce_dw: bool = True, stream=None):
+    def backward(self, x, wq, wk, wv, wo, dy, saved, reduce_dw: bool = True, stream=None, q_norm_w=None,
+                 k_norm_w=None):
         o_saved, lse = saved
         S_l = x.shape[0]
         sh = self.shape(S_l)
@@ -113,9 +124,16 @@ class UPipeAttention:
         dwv = torch.empty(wv.shape, dtype=torch.float32, device=x.device)
         dwo = torch.empty(wo.shape, dtype=torch.float32, device=x.device)
         ws = None if self.ipc else self.workspace(S_l, 1)
+        nw = self._norm_w(q_norm_w, k_norm_w)
+        if nw is None:
+            U.upipe_attn_bwd(self.ctx, sh, x, wq, wk, wv, wo, dy, o_saved, lse, dx, dwq, dwk, dwv, dwo, reduce_dw, ws,
+                             stream=stream)
+            return dx, dwq, dwk, dwv, dwo
+        dgq = torch.empty(self.d, dtype=torch.float32, device=x.device)
+        dgk = torch.empty(self.d, dtype=torch.float32, device=x.device)
         U.upipe_attn_bwd(self.ctx, sh, x, wq, wk, wv, wo, dy, o_saved, lse, dx, dwq, dwk, dwv, dwo, reduce_dw, ws,
-                         stream=stream)
-        return dx, dwq, dwk, dwv, dwo
+                         stream=stream, qk_norm=(nw[0], nw[1], dgq, dgk))
+        return dx, dwq, dwk, dwv, dwo, dgq, dgk
 
     def wait(self, timeout_s: float = 0.0, stream=None):
         """Block until this rank's enqueued layer work is done, failing (UpipeError, communicator aborted)

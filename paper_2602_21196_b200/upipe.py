@@ -30,7 +30,11 @@ class UpipeError(RuntimeError):
 class upipe_shape_t(ctypes.Structure):
     _fields_ = [("seq_local", c_int64), ("hidden", c_int32), ("n_q_heads", c_int32), ("n_kv_heads", c_int32),
                 ("head_dim", c_int32), ("chunk_heads", c_int32), ("causal", c_int32), ("rope_base", ctypes.c_float),
-                ("ring_degree", c_int32)]
+                ("ring_degree", c_int32), ("qk_norm_eps", ctypes.c_float)]
+
+
+class upipe_qk_norm_t(ctypes.Structure):
+    _fields_ = [("q_norm_w", c_void_p), ("k_norm_w", c_void_p), ("dq_norm_w", c_void_p), ("dk_norm_w", c_void_p)]
 
 
 class upipe_stage_info_t(ctypes.Structure):
@@ -77,6 +81,10 @@ def lib() -> ctypes.CDLL:
             "upipe_validate": (st, [c_int, POINTER(upipe_shape_t), c_char_p, c_size_t]),
             "upipe_attn_fwd": (st, [P, POINTER(upipe_shape_t)] + [P] * 8 + [P, c_size_t, P]),
             "upipe_attn_bwd": (st, [P, POINTER(upipe_shape_t)] + [P] * 13 + [c_int, P, c_size_t, P]),
+            "upipe_attn_fwd_ex": (st, [P, POINTER(upipe_shape_t)] + [P] * 5 + [POINTER(upipe_qk_norm_t)] + [P] * 3 +
+                                  [P, c_size_t, P]),
+            "upipe_attn_bwd_ex": (st, [P, POINTER(upipe_shape_t)] + [P] * 5 + [POINTER(upipe_qk_norm_t)] + [P] * 8 +
+                                  [c_int, P, c_size_t, P]),
             "upipe_attn_core_fwd": (st, [P] * 5 + [c_int64, c_int, c_int, c_int, c_int] + [c_int64] * 4 + [P]),
             "upipe_attn_core_bwd": (st, [P] * 9 + [c_int64, c_int, c_int, c_int, c_int] + [c_int64] * 5 + [c_int, P, P]),
             "upipe_core_bwd_sem_count": (c_int64, [c_int64, c_int]),
@@ -107,7 +115,7 @@ EXPORTED = ("upipe_get_unique_id", "upipe_init", "upipe_fabric_create", "upipe_f
             "upipe_validate", "upipe_attn_fwd", "upipe_attn_bwd", "upipe_attn_core_fwd", "upipe_attn_core_bwd", "upipe_core_bwd_sem_count",
             "upipe_rowdot", "upipe_gemm_xwT", "upipe_synth_fill_bf16", "upipe_kernel_launches", "upipe_set_trace",
             "upipe_trace_read", "upipe_test_set_probe", "upipe_wait", "upipe_comm_info",
-            "upipe_ipc_region_size", "upipe_ipc_create", "upipe_ipc_connect")
+            "upipe_ipc_region_size", "upipe_ipc_create", "upipe_ipc_connect", "upipe_attn_fwd_ex", "upipe_attn_bwd_ex")
 
 TRACE_CATS = ("gemm", "attn_fwd", "attn_bwd", "comm", "aux")
 
@@ -137,9 +145,9 @@ def _stream(stream):
 
 
 def make_shape(seq_local, hidden, n_q_heads, n_kv_heads, head_dim, chunk_heads, causal=1,
-               rope_base=0.0, ring_degree=0) -> upipe_shape_t:
+               rope_base=0.0, ring_degree=0, qk_norm_eps=0.0) -> upipe_shape_t:
     return upipe_shape_t(seq_local, hidden, n_q_heads, n_kv_heads, head_dim, chunk_heads, int(causal),
-                         float(rope_base), int(ring_degree))
+                         float(rope_base), int(ring_degree), float(qk_norm_eps))
 
 
 # ------------------------------------------------------------------ lifecycle
@@ -248,18 +256,33 @@ def _ws_bytes(workspace, ws_bytes):
     return 0 if workspace is None else workspace.numel() * workspace.element_size()
 
 
-def upipe_attn_fwd(ctx, shape, x, wq, wk, wv, wo, y, o_saved, lse_saved, workspace, ws_bytes=None, stream=None):
+def _qkn(qk_norm):
+    """(q_norm_w, k_norm_w[, dq_norm_w, dk_norm_w]) -> upipe_qk_norm_t, or None."""
+    if qk_norm is None:
+        return None
+    t = list(qk_norm) + [None] * (4 - len(qk_norm))
+    return upipe_qk_norm_t(*[_ptr(a) for a in t])
+
+
+def upipe_attn_fwd(ctx, shape, x, wq, wk, wv, wo, y, o_saved, lse_saved, workspace, ws_bytes=None, stream=None,
+                   qk_norm=None):
+    """qk_norm: (q_norm_w, k_norm_w) bf16 [d] when shape.qk_norm_eps > 0 (upipe_attn_fwd_ex)."""
     wsb = _ws_bytes(workspace, ws_bytes)
-    _check(lib().upipe_attn_fwd(ctx, ctypes.byref(shape), _ptr(x), _ptr(wq), _ptr(wk), _ptr(wv), _ptr(wo), _ptr(y),
-                                _ptr(o_saved), _ptr(lse_saved), _ptr(workspace), wsb, _stream(stream)), ctx)
+    q = _qkn(qk_norm)
+    _check(lib().upipe_attn_fwd_ex(ctx, ctypes.byref(shape), _ptr(x), _ptr(wq), _ptr(wk), _ptr(wv), _ptr(wo),
+                                   ctypes.byref(q) if q is not None else None, _ptr(y), _ptr(o_saved),
+                                   _ptr(lse_saved), _ptr(workspace), wsb, _stream(stream)), ctx)
 
 
 def upipe_attn_bwd(ctx, shape, x, wq, wk, wv, wo, dy, o_saved, lse_saved, dx, dwq, dwk, dwv, dwo, reduce_dw,
-                   workspace, ws_bytes=None, stream=None):
+                   workspace, ws_bytes=None, stream=None, qk_norm=None):
+    """qk_norm: (q_norm_w, k_norm_w, dq_norm_w, dk_norm_w) (fp32 gradients out) when shape.qk_norm_eps > 0."""
     wsb = _ws_bytes(workspace, ws_bytes)
-    _check(lib().upipe_attn_bwd(ctx, ctypes.byref(shape), _ptr(x), _ptr(wq), _ptr(wk), _ptr(wv), _ptr(wo), _ptr(dy),
-                                _ptr(o_saved), _ptr(lse_saved), _ptr(dx), _ptr(dwq), _ptr(dwk), _ptr(dwv), _ptr(dwo),
-                                int(reduce_dw), _ptr(workspace), wsb, _stream(stream)), ctx)
+    q = _qkn(qk_norm)
+    _check(lib().upipe_attn_bwd_ex(ctx, ctypes.byref(shape), _ptr(x), _ptr(wq), _ptr(wk), _ptr(wv), _ptr(wo),
+                                   ctypes.byref(q) if q is not None else None, _ptr(dy), _ptr(o_saved),
+                                   _ptr(lse_saved), _ptr(dx), _ptr(dwq), _ptr(dwk), _ptr(dwv), _ptr(dwo),
+                                   int(reduce_dw), _ptr(workspace), wsb, _stream(stream)), ctx)
 
 
 # ------------------------------------------------------------------ kernel-level

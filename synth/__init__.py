@@ -31,7 +31,7 @@ import math
 import numpy as np
 
 TID = {"x": 1, "wq": 2, "wk": 3, "wv": 4, "wo": 5, "dy": 6,
-       "q": 11, "k": 12, "v": 13, "do": 14}
+       "q": 11, "k": 12, "v": 13, "do": 14, "q_norm_w": 7, "k_norm_w": 8}
 
 _M64 = (1 << 64) - 1
 _G1 = 0x9E3779B97F4A7C15
@@ -176,3 +176,11 @@ def payload_bits(seed: int, tensor_id: int, shape, start: int = 0) -> np.ndarray
     expo = (np.uint64(112) + ((z >> np.uint64(40)) & np.uint64(31))) << np.uint64(7)
     mant = (z >> np.uint64(20)) & np.uint64(0x7F)
     return (sign | expo | mant).astype(np.uint16).reshape(shape)
+
+
+def norm_weight(seed: int, name: str, d: int) -> np.ndarray:
+    """Qwen3 q/k RMSNorm weight vector [d]: 1 + k/128, k = m mod 33 - 16 in [-16, 16]
+    (values 0.875 .. 1.125 around the trained weights' typical 1; exact in bf16: spacing 2^-7 in [1, 2),
+    2^-8 in [0.5, 1))."""
+    m = draw_codes(seed, TID[name], 0, d)
+    return 1.0 + ((m % 33) - 16).astype(np.float64) / 128.0

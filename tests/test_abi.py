@@ -77,11 +77,12 @@ def test_rope_base_validation(U, base, ok):
 
 
 def test_shape_struct_layout_matches_header(U):
-    # the ctypes mirror of upipe_shape_t: 8 + 6*4 + 4 + 4 bytes, ring_degree last (include/upipe.h)
+    # the ctypes mirror of upipe_shape_t: 8 + 6*4 + 4 + 4 + 4 bytes (+ 4 padding), qk_norm_eps last (include/upipe.h)
     import ctypes
-    assert ctypes.sizeof(U.upipe_shape_t) == 40
+    assert ctypes.sizeof(U.upipe_shape_t) == 48
     assert U.upipe_shape_t.rope_base.offset == 32
     assert U.upipe_shape_t.ring_degree.offset == 36
+    assert U.upipe_shape_t.qk_norm_eps.offset == 40
 
 
 GRID = [(Hq, Hkv, C, Uc) for Hq, Hkv in ((8, 2), (16, 4), (32, 8), (64, 8), (8, 8), (32, 32))
@@ -149,6 +150,25 @@ def test_workspace_direct_has_no_send_buffers(U):
     # C = 1: direct is the plain C = 1 layout (no all-to-all)
     sh1 = U.make_shape(4096, D, 32, 8, d, 8)
     assert U.upipe_workspace_size(1, sh1, 4) == U.upipe_workspace_size(1, sh1, 2)
+
+
+def test_qk_norm_validation_and_workspace(U):
+    # Qwen3 q/k norm (DESIGN A29): eps in (0, 1); not with the ring hybrid; the backward workspace grows by the
+    # normalised Q/K copies, an fp32 dK and d(gamma); the forward normalises in place (no growth)
+    sh0 = U.make_shape(1024, 512, 8, 2, 64, 2)
+    sh1 = U.make_shape(1024, 512, 8, 2, 64, 2, qk_norm_eps=1e-6)
+    assert U.upipe_validate(2, sh1) == (0, "")
+    assert U.upipe_workspace_size(2, sh1, 2) == U.upipe_workspace_size(2, sh0, 2)
+    S, qe, ke = 2048, 2048 * 1 * 64 * 2, 2048 * 1 * 64 * 2
+    grow = U.upipe_workspace_size(2, sh1, 3) - U.upipe_workspace_size(2, sh0, 3)
+    assert abs(grow - (qe + ke + 2 * 64 * 4)) <= 256 * 4          # sigma = 4: the fp32 dK accumulator exists already
+    sh2 = U.make_shape(1024, 512, 8, 8, 64, 2, qk_norm_eps=1e-6)    # MHA, sigma = 1: the fp32 dK is new
+    grow2 = U.upipe_workspace_size(2, sh2, 3) - U.upipe_workspace_size(2, U.make_shape(1024, 512, 8, 8, 64, 2), 3)
+    assert abs(grow2 - (qe + ke + 2 * ke + 2 * 64 * 4)) <= 256 * 4
+    bad = U.make_shape(1024, 512, 8, 2, 64, 2, qk_norm_eps=-1.0)
+    assert U.upipe_validate(2, bad)[0] == 1
+    ring = U.make_shape(1024, 512, 8, 2, 64, 2, ring_degree=2, qk_norm_eps=1e-6)
+    assert U.upipe_validate(4, ring)[0] == 2
 
 
 def test_workspace_c1_aliases_send_and_recv(U):

@@ -14,7 +14,7 @@ import torch
 import torch.multiprocessing as mp
 
 import synth
-from test_gpu_layer import _check, _run_group
+from test_gpu_layer import ABS, _boundary_abs, _check, _run_group
 
 pytestmark = pytest.mark.gpu
 
@@ -43,13 +43,18 @@ def _rank(rank, C, port, cfg, outdir):
     attn = UPipeAttention(Hq, Hkv, d, D, U, True, process_group=dist.group.WORLD, transport="ipc",
                           max_seq_local=S_l, sync_comm=cfg.get("sync", False), ring_degree=cfg.get("ring", 1),
                           deterministic=cfg.get("det", False), direct=cfg.get("direct", False),
-                          rope_base=cfg.get("rope", 0.0))
+                          rope_base=cfg.get("rope", 0.0), qk_norm_eps=cfg.get("qkn", 0.0))
+    NW = {}
+    if cfg.get("qkn"):
+        NW = dict(q_norm_w=t(synth.norm_weight(0, "q_norm_w", d)), k_norm_w=t(synth.norm_weight(0, "k_norm_w", d)))
     info = attn.comm_info()
     assert info["transport"] == "ipc" and info["nranks"] == C and info["rank"] == rank, info
-    y, saved = attn.forward(x, *W)
-    dx, dwq, dwk, dwv, dwo = attn.backward(x, *W, dy, saved)
+    y, saved = attn.forward(x, *W, **NW)
+    g = attn.backward(x, *W, dy, saved, **NW)
     attn.wait(timeout_s=300)
-    out = {"y": y, "o": saved[0], "lse": saved[1], "dx": dx, "dwq": dwq, "dwk": dwk, "dwv": dwv, "dwo": dwo}
+    out = {"y": y, "o": saved[0], "lse": saved[1], "dx": g[0], "dwq": g[1], "dwk": g[2], "dwv": g[3], "dwo": g[4]}
+    if NW:
+        out.update(dgq=g[5], dgk=g[6])
     np.savez(os.path.join(outdir, f"r{rank}.npz"), **{k: v.float().cpu().numpy() for k, v in out.items()},
              region=np.array([attn.region_bytes]))
     attn.close()
@@ -93,6 +98,18 @@ def test_ipc_direct_layer_matches_oracle(C, S, D, Hq, Hkv, d, U, rope):
     res = _run_ipc(C, dict(S=S, D=D, Hq=Hq, Hkv=Hkv, d=d, U=U, direct=True, rope=rope))
     inp = synth.layer_inputs(0, S, D, Hq, Hkv, d)
     _check(res, inp, C, Hq, Hkv, d, U, rope_base=rope or None)
+
+
+@pytest.mark.timeout(900)
+def test_ipc_direct_qk_norm_matches_oracle():
+    # N2 direct stores with the Qwen3 q/k norm (N3): the fused norm backward writes dQ / dK into the peers
+    C, S, D, Hq, Hkv, d, U = 4, 1024, 1024, 64, 8, 128, 8
+    res = _run_ipc(C, dict(S=S, D=D, Hq=Hq, Hkv=Hkv, d=d, U=U, direct=True, rope=1e6, qkn=1e-6))
+    inp = synth.layer_inputs(0, S, D, Hq, Hkv, d)
+    inp.update(q_norm_w=synth.norm_weight(0, "q_norm_w", d), k_norm_w=synth.norm_weight(0, "k_norm_w", d),
+               qk_norm_eps=1e-6)
+    eo, ey = _boundary_abs(inp, Hq, Hkv, d, 1e6)
+    _check(res, inp, C, Hq, Hkv, d, U, rope_base=1e6, abs_y=max(ABS, ey), abs_o=max(ABS, eo))
 
 
 @pytest.mark.timeout(900)
