@@ -33,6 +33,25 @@ MODELS = {   # BASELINE configs: Llama3-8B attention (configs 1-4) and the 32B-c
 }
 
 
+def a2a_bytes(S_l, C, Hq, Hkv, d, U, naive=False):
+    """Bytes ONE rank sends to the other C - 1 ranks in one layer fwd+bwd, from the GQA schedule's buffer sizes
+    (Table 4): forward Q and O per stage, K and V per super-stage (every stage when
+    naive); backward Q, dO, dQ (bf16) and delta (fp32) per stage, K, V, dK, dV per super-stage. Each chunk
+    keeps 1/C of its blocks on the rank. Returns {"fwd_inp", "fwd_out", "bwd", "total"}."""
+    qpd, R = U // C, Hq // Hkv
+    kv_res = max(1, qpd // R)
+    sigma = 1 if naive else max(1, R // qpd)
+    stages = Hq // U
+    kv_events = stages // sigma
+    off = (C - 1) / C
+    qb = S_l * qpd * d * 2 * C                   # one Q-sized chunk (C blocks of [S_l][qpd d] bf16)
+    kb = S_l * kv_res * d * 2 * C
+    fwd_inp = (stages * qb + kv_events * 2 * kb) * off
+    fwd_out = stages * qb * off
+    bwd = (stages * (3 * qb + S_l * qpd * 4 * C) + kv_events * 4 * kb) * off
+    return {"fwd_inp": fwd_inp, "fwd_out": fwd_out, "bwd": bwd, "total": fwd_inp + fwd_out + bwd}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -53,6 +72,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="profiling runs: timed region only")
+    ap.add_argument("--qk-norm", type=float, default=0.0,
+                    help="Qwen3 per-head q/k RMSNorm with this eps (1e-6; SURVEY N3, DESIGN A29); 0 = off")
+    ap.add_argument("--transport", choices=["nccl", "ipc"], default="nccl",
+                    help="N > 1: NCCL collectives, or CUDA-IPC peer memory (the library's symmetric region)")
+    ap.add_argument("--direct", action="store_true",
+                    help="with --transport ipc: all-to-alls fused into their producers (UPIPE_FLAG_DIRECT, SURVEY N2)")
     return ap.parse_args()
 
 
@@ -236,7 +261,18 @@ def main():
     x = fill((S_l, D), "x", rank * S_l * D)
     dy = fill((S_l, D), "dy", rank * S_l * D)
     W = [fill((Hq * d, D), "wq"), fill((Hkv * d, D), "wk"), fill((Hkv * d, D), "wv"), fill((D, Hq * d), "wo")]
+    NW = {}                                        # Qwen3 q/k norm weights (DESIGN A29)
+    if args.qk_norm > 0:
+        NW = {k: torch.from_numpy(synth.norm_weight(0, k, d).astype("float32")).to(torch.bfloat16).to(dev)
+              for k in ("q_norm_w", "k_norm_w")}
     torch.cuda.synchronize()
+
+    def make_attn(chunk):
+        kw = {}
+        if pg is not None and args.transport == "ipc":
+            kw = dict(transport="ipc", max_seq_local=S_l, direct=args.direct)
+        return UPipeAttention(Hq, Hkv, d, D, chunk, True, process_group=pg, naive_kv=args.naive_kv,
+                              rope_base=args.rope_base, ring_degree=args.ring, qk_norm_eps=args.qk_norm, **kw)
 
     def barrier():
         if pg is not None:
@@ -252,13 +288,12 @@ def main():
     def run(chunk, steps, warmup, trace=False):
         torch.cuda.synchronize()
         base = torch.cuda.memory_allocated()       # inputs and weights only: workspace + outputs count as activation
-        attn = UPipeAttention(Hq, Hkv, d, D, chunk, True, process_group=pg, naive_kv=args.naive_kv,
-                              rope_base=args.rope_base, ring_degree=args.ring)
+        attn = make_attn(chunk)
         out = {}
 
         def step():
-            y, saved = attn.forward(x, *W)
-            g = attn.backward(x, *W, dy, saved)
+            y, saved = attn.forward(x, *W, **NW)
+            g = attn.backward(x, *W, dy, saved, **NW)
             return y, g
 
         for _ in range(warmup):
@@ -268,7 +303,7 @@ def main():
         step()
         torch.cuda.synchronize()
         out["peak_bytes"] = max_over_ranks(torch.cuda.max_memory_allocated() - base)   # max over ranks
-        out["ws_bytes"] = sum(t.numel() for t in attn._ws.values())
+        out["ws_bytes"] = attn.region_bytes if attn.ipc else sum(t.numel() for t in attn._ws.values())
         # chunk buffers = workspace minus the U-independent fp32 dX accumulator [S_l, D] (only allocated
         # when there is more than one stage): the "intermediate tensors" of P:332-343 (DESIGN A21)
         out["chunk_bytes"] = out["ws_bytes"] - (S_l * D * 4 if Hq // chunk > 1 else 0)
@@ -339,7 +374,8 @@ def main():
                    "parallelism": f"cp{C} (UPipe, U={U})" if args.ring == 1 else
                    f"cp{C} = ulysses{C // args.ring} x ring{args.ring} (UPipe x Ring, U={U})",
                    "kv_schedule": "naive (per-stage K/V resend)" if args.naive_kv else "GQA super-stage (P:362-380)",
-                   "rope_base": args.rope_base,
+                   "rope_base": args.rope_base, "qk_norm_eps": args.qk_norm,
+                   "transport": ("ipc-direct" if args.direct else args.transport) if C > 1 else "none (C = 1)",
                    "l2": f"inputs larger than L2 (x, dy: S_l x {D} bf16 per rank); no flush needed"},
         "tokens_per_s_total": tok_s_total,
         "value_definition": "S / (C * max-over-ranks device time of one fwd+bwd step): tokens/s/GPU as BASELINE's "
@@ -366,16 +402,7 @@ def main():
         # all-to-all volume of one fwd+bwd step on this rank (the plan's per-stage buffers; each rank keeps
         # 1/C of every block), its event-timed duration on the comm stream, the bus bandwidth against
         # NVLink 5's 900 GB/s per direction, and the share of that time hidden behind compute
-        qpd_, R_ = U // C, Hq // Hkv
-        kv_res = max(1, qpd_ // R_)
-        sigma = max(1, R_ // qpd_) if not args.naive_kv else 1
-        stages = Hq // U
-        qb = S_l * qpd_ * d * 2 * C                                  # one Q-sized chunk (all C blocks)
-        kb = S_l * kv_res * d * 2 * C
-        kv_events = stages // sigma
-        fwd_b = stages * 2 * qb + kv_events * 2 * kb                 # Q, O per stage; K, V per super-stage
-        bwd_b = stages * (3 * qb + S_l * qpd_ * 4 * C) + kv_events * 4 * kb   # Q, dO, dQ, delta; K, V, dK, dV
-        off_rank = (fwd_b + bwd_b) * (C - 1) / C
+        off_rank = a2a_bytes(S_l, C, Hq, Hkv, d, U, args.naive_kv)["total"]
         comm_ms = per_step_ms.get("comm", 0.0)
         compute_ms = sum(v for k, v in per_step_ms.items() if k != "comm")
         result["a2a"] = {"bytes_per_step_off_rank": off_rank, "ms_per_step": comm_ms,
@@ -415,8 +442,7 @@ def main():
         # the timed region. The copies run on two copy streams (H2D, D2H) with double-buffered device
         # inputs, so step i+1's upload overlaps step i's backward and step i's download overlaps step
         # i+1's forward (the usual input pipeline of a training loop); nothing is skipped or cached.
-        attn = UPipeAttention(Hq, Hkv, d, D, U, True, process_group=pg, naive_kv=args.naive_kv,
-                              rope_base=args.rope_base, ring_degree=args.ring)
+        attn = make_attn(U)
         xh = [x.cpu().pin_memory() for _ in range(2)]
         dyh = [dy.cpu().pin_memory() for _ in range(2)]
         dxh = [torch.empty_like(xh[0]).pin_memory() for _ in range(2)]
@@ -441,9 +467,9 @@ def main():
                 dy_ready = ev()
                 dy_ready.record(h2d)
             main_s.wait_event(x_ready)
-            y, saved = attn.forward(xd[b], *W)
+            y, saved = attn.forward(xd[b], *W, **NW)
             main_s.wait_event(dy_ready)
-            dx, *_ = attn.backward(xd[b], *W, dyd[b], saved)
+            dx, *_ = attn.backward(xd[b], *W, dyd[b], saved, **NW)
             bwd_done[b].record(main_s)
             with torch.cuda.stream(d2h):
                 d2h.wait_event(bwd_done[b])
