@@ -57,12 +57,21 @@ struct GemmArgs {
                              //    (bulk tensor store / reduce-add into L2) instead of per-thread global RMW
   int kcum[kMaxParts + 1];   // K-concat: first K index of each part (multiples of BK)
   int mcum[kMaxParts + 1];   // M-concat: first row of each part (multiples of BM)
+  int ncum[kMaxParts + 1];   // N-concat: first column of each part (multiples of BN)
   DevOpMap a[kMaxParts], b[kMaxParts];
   DevOut c[kMaxParts];
   DevDot dot;
   __nv_bfloat16* segp[kMaxSeg];   // N2: part 0's bf16 output segment bases (nsegp > 0), see OutMap::seg
   int nsegp;
+  int ksplit;                     // split-K: each output tile is computed by ksplit units over K / ksplit and
+                                  // ADDED (atomically) into the zero-initialised output (fp32 store epilogues)
 };
+
+// fp32 atomic add of 4 consecutive floats (split-K epilogue without a TMA map)
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
 
 constexpr int BM = 128;
 constexpr int BK = 64;
@@ -137,10 +146,16 @@ __global__ void __launch_bounds__(192, 1)
   const int ms = crank & 1, ns = CL == 4 ? crank >> 1 : 0;
   const int unit0 = blockIdx.x / CL, nunit_step = gridDim.x / CL;
   const int ntn_u = CL == 4 && !P4 ? ntn / 2 : ntn;              // n-units (CL = 4: pairs of n-blocks)
-  const int nunits = ntn_u * (P4 ? (ntm + 3) / 4 : (MC ? (ntm + 1) / 2 : ntm));
+  const int nunits0 = ntn_u * (P4 ? (ntm + 3) / 4 : (MC ? (ntm + 1) / 2 : ntm));
+  const int nunits = nunits0 * g.ksplit;          // split-K: unit u = split u / nunits0 of tile-unit u % nunits0
   const int nk = (g.K + BK - 1) / BK;
-  auto tile_m = [&](int u) { return P4 ? (u / ntn_u) * 4 + crank : (MC ? (u / ntn_u) * 2 + ms : u / ntn_u); };
-  auto tile_n = [&](int u) { return CL == 4 && !P4 ? (u % ntn_u) * 2 + ns : u % ntn_u; };
+  auto tile_m = [&](int u) {
+    u %= nunits0;
+    return P4 ? (u / ntn_u) * 4 + crank : (MC ? (u / ntn_u) * 2 + ms : u / ntn_u);
+  };
+  auto tile_n = [&](int u) { u %= nunits0; return CL == 4 && !P4 ? (u % ntn_u) * 2 + ns : u % ntn_u; };
+  auto kb_begin = [&](int u) { return (int)((long long)(u / nunits0) * nk / g.ksplit); };
+  auto kb_end = [&](int u) { return (int)((long long)(u / nunits0 + 1) * nk / g.ksplit); };
   const uint32_t leader = crank & ~1u;                            // PAIR: rank of this CTA's pair leader
   // multicast masks: A to the CTAs sharing this m-block (CL = 4), B to those sharing this n-block;
   // an MMA commit frees the stage in every CTA that writes into this CTA's ring
@@ -154,6 +169,12 @@ __global__ void __launch_bounds__(192, 1)
     int p = 0;
     if (g.kind == 1)
       while (p + 1 < g.nparts && m0 >= g.mcum[p + 1]) ++p;
+    return p;
+  };
+  auto npart = [&](int n0) {            // N-concat part of a tile
+    int p = 0;
+    if (g.kind == 2)
+      while (p + 1 < g.nparts && n0 >= g.ncum[p + 1]) ++p;
     return p;
   };
   if (warp == 0 && lane == 0) {
@@ -198,16 +219,18 @@ __global__ void __launch_bounds__(192, 1)
         const int mt = tile_m(u);
         const bool valid = mt < ntm;           // MC: the odd last m-block pairs with an empty tile
         const int m0 = mt * BM, n0 = tile_n(u) * BN;
-        const int pm = mpart(m0);
+        const int pm = mpart(m0), pn = npart(n0);
         const int ml0 = m0 - (g.kind == 1 ? g.mcum[pm] : 0);
+        const int nl0 = n0 - (g.kind == 2 ? g.ncum[pn] : 0);
         const int cb0 = P4 ? ms * (GB / 2) + ns * GB0 : (MC ? ms * GB0 : 0);   // first B granule (tile rows / 64)
         const int cbd = P4 ? ns * GB0 : (PAIR ? 0 : cb0);                        // its granule in this CTA's ring
         const int ca0 = CL == 4 && !P4 ? ns * GA0 : 0;
         int pk = -1, pa = 0, pb = 0;
-        int a_out[GA0], a_kb[GA0], b_out[GB0], b_kb[GB0];
+        int a_out[GA0], a_kb[GA0], b_out[GB0], b_kb[GB0], b_pt[GB0];
         int ka_len = 1, kb_len = 1, kqa_o = 0, kqa_k = 0, kqb_o = 0, kqb_k = 0;
         int kra = 0, krb = 0, kqa = 0, kqb = 0;
-        for (int kb = 0; kb < nk; ++kb) {
+        const int kb0 = kb_begin(u), kb1 = kb_end(u);
+        for (int kb = kb0; kb < kb1; ++kb) {
           const long long w0 = g.dbg ? clock64() : 0;
           mbar_wait(&empty[stage], phase ^ 1);
           if (g.dbg) tl_prod += clock64() - w0;
@@ -218,8 +241,8 @@ __global__ void __launch_bounds__(192, 1)
             while (npk + 1 < g.nparts && kb * BK >= g.kcum[npk + 1]) ++npk;
           if (npk != pk) {                     // new tile or new K part: per-(tile, part) constants
             pk = npk;
-            pa = g.kind == 1 ? pm : pk;
-            pb = g.kind == 1 ? 0 : pk;
+            pa = g.kind == 1 ? pm : (g.kind == 2 ? 0 : pk);
+            pb = g.kind == 1 ? 0 : (g.kind == 2 ? pn : pk);
             const DevOpMap& am = g.a[pa];
             const DevOpMap& bm = g.b[pb];
 #pragma unroll
@@ -231,17 +254,24 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
             for (int c = 0; c < GB0; ++c) {
               // WIDE: granule c of this CTA = half ms of MMA (c / 2)'s 256 B rows
-              const int ii = n0 + (WIDE ? (c >> 1) * (GB / NMMA) + ms * 2 + (c & 1) : cb0 + c) * 64;
-              b_out[c] = bm.o_base + (ii / bm.o_len) * bm.o_istride + ii % bm.o_len;
-              b_kb[c] = bm.k_base + (ii / bm.o_len) * bm.k_istride;
+              const int ig = (WIDE ? (c >> 1) * (GB / NMMA) + ms * 2 + (c & 1) : cb0 + c) * 64;
+              // N-concat: a tile may span parts; each 64-row granule takes its own part's B operand
+              const int pg = g.kind == 2 ? npart(n0 + ig) : pb;
+              const DevOpMap& bg = g.b[pg];
+              const int ii = (g.kind == 2 ? n0 + ig - g.ncum[pg] : nl0 + ig);
+              b_pt[c] = pg;
+              b_out[c] = bg.o_base + (ii / bg.o_len) * bg.o_istride + ii % bg.o_len;
+              b_kb[c] = bg.k_base + (ii / bg.o_len) * bg.k_istride;
             }
             ka_len = am.k_len; kqa_o = am.o_kstride; kqa_k = am.k_kstride;
             kb_len = bm.k_len; kqb_o = bm.o_kstride; kqb_k = bm.k_kstride;
-            kqa = kqb = 0;
-            kra = krb = 0;                     // parts start at k = 0 (K-concat offsets are multiples of BK)
+            // k within the part (K-concat offsets are multiples of BK; split-K units start mid-part)
+            const int kl = kb * BK - (g.kind == 1 ? 0 : g.kcum[pk]);
+            kqa = kl / ka_len; kra = kl % ka_len;
+            kqb = kl / kb_len; krb = kl % kb_len;
           }
           const CUtensorMap* tA = mapA(pa);
-          const CUtensorMap* tB = mapB(pb);
+          const CUtensorMap* tB = mapB(pb);   // N-concat: per granule (below)
           if (g.dbg_mode == 2) {                // timeline experiment: MMA-only
             mbar_arrive(&full[stage]);
             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -275,6 +305,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int c = 0; c < GB0; ++c) {
             if (c % g.b_box_g) continue;
+            if (g.kind == 2) tB = mapB(b_pt[c]);
             const int oc = b_out[c] + kqb * kqb_o, kc = b_kb[c] + kqb * kqb_k + krb;
             uint8_t* dst = sb + (cbd + c) * GRANULE_BYTES;
             if (P4) {                           // to both pairs; each copy completes on its pair leader's barrier
@@ -315,7 +346,8 @@ __global__ void __launch_bounds__(192, 1)
         if (g.dbg) tl_acc += clock64() - a0;
         tc_fence_after();
         const uint32_t acc = tmem + ab * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        const int kb0 = kb_begin(u), kb1 = kb_end(u);
+        for (int kb = kb0; kb < kb1; ++kb) {
           const long long w0 = g.dbg ? clock64() : 0;
           mbar_wait(&full[stage], phase);
           if (g.dbg) tl_full += clock64() - w0;
@@ -330,9 +362,9 @@ __global__ void __launch_bounds__(192, 1)
             if (PAIR) {
 #pragma unroll
               for (int j = 0; j < NMMA; ++j)             // MMA j: TMEM columns [256 j, 256 j + 256), B sub-tile j
-                mma_ss_pair_w(acc + j * MMA_N, da, db + ((j * (MMA_N / 2) * BK * 2) >> 4), idesc, (kb | kk) != 0);
+                mma_ss_pair_w(acc + j * MMA_N, da, db + ((j * (MMA_N / 2) * BK * 2) >> 4), idesc, (kb != kb0 || kk != 0));
             } else {
-              mma_ss_w(acc, da, db, idesc, (kb | kk) != 0);
+              mma_ss_w(acc, da, db, idesc, (kb != kb0 || kk != 0));
             }
           }
           if (PAIR) mma_commit_pair_w(&empty[stage], P4 ? 0xF : 0x3);  // frees the stage where this pair's data lives
@@ -358,15 +390,16 @@ __global__ void __launch_bounds__(192, 1)
     for (int u = unit0; u < nunits; u += nunit_step, ++i) {
       const int ab = i % NACC;
       const int m0 = tile_m(u) * BM, n0 = tile_n(u) * BN;
-      const int pc = mpart(m0);
+      const int pc = g.kind == 2 ? npart(n0) : mpart(m0);
       const DevOut& oc_ = g.c[pc];
+      const bool seg_out = pc == 0 || g.kind == 2;    // part 0's output map (N-concat: one segmented output)
       const int m = m0 + row;
       const int ml = m - (g.kind == 1 ? g.mcum[pc] : 0);
       mbar_wait(&acc_full[ab], (i / NACC) & 1);
       tc_fence_after();
       const bool mvalid = m < g.M;
       const long long mseg = mvalid ? ml / oc_.m_len : 0, min_ = mvalid ? ml % oc_.m_len : 0;
-      if (g.c_tma == 2 && pc == 0) {
+      if (g.c_tma == 2 && seg_out) {
         // bf16 store through shared memory: each warp stages its 32 rows x 64 columns (128B swizzle,
         // two 4 KB slots) and issues one TMA store per box into the output's 3-D view {col, row, segment}
         // (full-line writes instead of 32 rows x 16 bytes per store instruction). N2: one 2-D map per
@@ -384,9 +417,10 @@ __global__ void __launch_bounds__(192, 1)
           float v[64];
 #pragma unroll
           for (int q = 0; q < 64; ++q) v[q] = __uint_as_float(r[q]) * g.alpha;
-          if (oc_.rope.hi) {
-            rope_rotate<16>(v, oc_.rope.hi, oc_.rope.lo, oc_.rope.d, oc_.rope.pos0 + m, n % oc_.rope.d, 1.f);
-            rope_rotate<16>(v + 32, oc_.rope.hi, oc_.rope.lo, oc_.rope.d, oc_.rope.pos0 + m, (n + 32) % oc_.rope.d, 1.f);
+          const RopeRef& rp = g.kind == 2 ? g.c[npart(n)].rope : oc_.rope;   // N-concat: the box's own part
+          if (rp.hi) {
+            rope_rotate<16>(v, rp.hi, rp.lo, rp.d, rp.pos0 + m, n % rp.d, 1.f);
+            rope_rotate<16>(v + 32, rp.hi, rp.lo, rp.d, rp.pos0 + m, (n + 32) % rp.d, 1.f);
           }
           if (g.dot.o) {
             const long long seg = n / oc_.n_len, nin = n % oc_.n_len;
@@ -449,7 +483,7 @@ __global__ void __launch_bounds__(192, 1)
           fence_proxy_async_smem();
           named_bar_sync(1, 128);
           if (issuer) {
-            if (oc_.epi == (int)Epi::kAccF32) tma_reduce_add_2d(&tmC, slot, n, m0);
+            if (oc_.epi == (int)Epi::kAccF32 || g.ksplit > 1) tma_reduce_add_2d(&tmC, slot, n, m0);
             else tma_store_2d(&tmC, slot, n, m0);
             bulk_commit();
           }
@@ -464,7 +498,8 @@ __global__ void __launch_bounds__(192, 1)
         for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]) * g.alpha;
         if (oc_.epi == (int)Epi::kStoreBF16) {
           // RoPE on the projected Q/K (row m = token pos0 + m, columns n.. = head dims n % d..)
-          if (oc_.rope.hi) rope_rotate<16>(v, oc_.rope.hi, oc_.rope.lo, oc_.rope.d, oc_.rope.pos0 + m, n % oc_.rope.d, 1.f);
+          const RopeRef& rp = g.kind == 2 ? g.c[npart(n)].rope : oc_.rope;
+          if (rp.hi) rope_rotate<16>(v, rp.hi, rp.lo, rp.d, rp.pos0 + m, n % rp.d, 1.f);
           if (pc == 0 && g.dot.o) {                       // fused row-dot (see the TMA path)
             const uint4* orw = reinterpret_cast<const uint4*>(g.dot.o + (long long)ml * g.dot.ld_o + g.dot.col0 +
                                                               nseg * g.dot.col_stride + nin);
@@ -476,12 +511,16 @@ __global__ void __launch_bounds__(192, 1)
               dot_acc = 0.f;
             }
           }
-          uint4* dst = reinterpret_cast<uint4*>(pc == 0 && g.nsegp ? g.segp[nseg] + (long long)ml * oc_.ld_bf16 + nin
+          uint4* dst = reinterpret_cast<uint4*>(seg_out && g.nsegp ? g.segp[nseg] + (long long)ml * oc_.ld_bf16 + nin
                                                                      : oc_.bf16 + orow * oc_.ld_bf16 + ocol);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             dst[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
                                 pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+        } else if (g.ksplit > 1) {                     // split-K: atomic adds into the zeroed output
+          float* dst = oc_.f32 + orow * oc_.ld_f32 + ocol;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) red_add_v4(dst + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         } else {
           float4* dst = reinterpret_cast<float4*>(oc_.f32 + orow * oc_.ld_f32 + ocol);
           if (oc_.epi != (int)Epi::kStoreF32) {
@@ -574,9 +613,26 @@ cudaError_t launch(const CUtensorMap* ta, const CUtensorMap* tb, const CUtensorM
       mc_by_dev[dev] = max_clusters;
     }
   }
-  const int clusters = units < max_clusters ? units : max_clusters;
+  // split-K (args.ksplit == 0: allowed, the outputs are zeroed fp32): a long-K GEMM with fewer tile-units than
+  // co-resident clusters (the weight gradients: M x N = 1536 x 4096 over K = S_l) splits K so every cluster
+  // works; the first split count whose waves fill >= 90 % of the clusters, K-blocks per split >= 64
+  GemmArgs a = args;
+  if (a.ksplit == 0) {
+    const int nkb = (a.K + BK - 1) / BK;
+    int best = 1;
+    double best_util = 0.0;
+    for (int sk = 1; sk <= 16 && nkb / sk >= 64; ++sk) {
+      const long long u = (long long)units * sk;
+      const double util = (double)u / ((double)((u + max_clusters - 1) / max_clusters) * max_clusters);
+      if (util > best_util + 1e-9) { best_util = util; best = sk; }
+      if (util >= 0.9) break;
+    }
+    a.ksplit = best;
+  }
+  const int units_all = units * a.ksplit;
+  const int clusters = units_all < max_clusters ? units_all : max_clusters;
   cfg.gridDim = dim3(CL * clusters);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], *tc, sm, args);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], *tc, sm, a);
   count_launches(1);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -624,10 +680,47 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
     snprintf(err, errlen, "gemm: %d parts (1..%d)", n, kMaxParts);
     return cudaErrorInvalidValue;
   }
+  GemmProblem pp[kMaxParts];
+  for (int i = 0; i < n; ++i) pp[i] = parts[i];
+  int ncum[kMaxParts + 1] = {0, 0, 0, 0};
+  if (kind == GemmGroup::kNConcat) {
+    // [B_0; B_1; ...] against one A: part 0 carries the whole output, the parts' n_len-column segments in
+    // order (bf16 stores); the other parts contribute their B operand and their epilogue options (RoPE)
+    GemmProblem& q = pp[0];
+    q.c.seg = SegPtrs{};
+    int64_t ncols = 0;
+    for (int i = 0; i < n; ++i) {
+      const GemmProblem& pi = parts[i];
+      const int64_t nlen = pi.c.n_len < pi.N ? pi.c.n_len : pi.N;
+      if (pi.M != q.M || pi.K != q.K || pi.a.ptr != q.a.ptr || pi.b.mn_major != q.b.mn_major ||
+          pi.c.epi != Epi::kStoreBF16 || nlen != (q.c.n_len < parts[0].N ? q.c.n_len : parts[0].N) ||
+          pi.c.ld_bf16 != q.c.ld_bf16 || pi.N % nlen) {
+        snprintf(err, errlen, "gemm N-concat: parts need equal M, K, A, segment width and bf16 stores");
+        return cudaErrorInvalidValue;
+      }
+      for (int64_t j = 0; j < pi.N / nlen; ++j) {
+        if (q.c.seg.n >= kMaxSeg) {
+          snprintf(err, errlen, "gemm N-concat: more than %d output segments", kMaxSeg);
+          return cudaErrorInvalidValue;
+        }
+        q.c.seg.p[q.c.seg.n++] = pi.c.seg.n ? pi.c.seg.p[j]
+                                            : static_cast<char*>(pi.c.out_bf16) + (size_t)(j * pi.c.r_nstride * pi.c.ld_bf16) * 2;
+      }
+      ncols += pi.N;
+      ncum[i + 1] = (int)ncols;
+    }
+    for (int i = n + 1; i <= kMaxParts; ++i) ncum[i] = (int)ncols;
+    q.N = ncols;
+    q.c.out_bf16 = nullptr;
+    q.c.r_nstride = 0;
+    for (int i = 1; i < n; ++i) pp[i].N = ncols;      // the shared tile grid (B maps keep their own extents)
+  }
+  parts = pp;
   const GemmProblem& p0 = parts[0];
   int64_t M = p0.M, K = p0.K;
   for (int i = 1; i < n; ++i) {
     const GemmProblem& pi = parts[i];
+    if (kind == GemmGroup::kNConcat) continue;         // checked above
     if (pi.N != p0.N || pi.a.mn_major != p0.a.mn_major || pi.b.mn_major != p0.b.mn_major) {
       snprintf(err, errlen, "gemm group: parts differ in N or operand majorness");
       return cudaErrorInvalidValue;
@@ -655,6 +748,11 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
   int bn = 256;
   auto bn_ok = [&](int w) {
     if (p0.N % w) return false;
+    if (kind == GemmGroup::kNConcat) {       // tiles may span parts (per-granule B maps, segmented output)
+      for (int i = 0; i < n; ++i)
+        if (ncum[i] % 64 || parts[i].b.o_len % 64 || parts[i].c.n_len % 64) return false;
+      return true;
+    }
     for (int i = 0; i < n; ++i)
       if ((parts[i].b.o_len % w) || (parts[i].c.n_len % w)) return false;
     return true;
@@ -678,7 +776,16 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
     cudaMemsetAsync(dbg_dev, 0, 8 * sizeof(long long), stream);
     args.dbg = dbg_dev;
   }
-  args.kind = kind == GemmGroup::kMConcat ? 1 : 0;
+  args.kind = kind == GemmGroup::kMConcat ? 1 : (kind == GemmGroup::kNConcat ? 2 : 0);
+  for (int i = 0; i <= kMaxParts; ++i) args.ncum[i] = ncum[i];
+  // split-K allowed when every part stores fp32 into an output the caller zeroed (OutMap::zeroed)
+  bool splittable = true;
+  for (int i = 0; i < n; ++i) splittable = splittable && parts[i].c.epi == Epi::kStoreF32 && parts[i].c.zeroed;
+  static const int splitk_env = [] {
+    const char* e = getenv("UPIPE_GEMM_SPLITK");
+    return e ? atoi(e) : 1;
+  }();
+  args.ksplit = splittable && splitk_env ? 0 : 1;
   // Clusters with operand multicast (UPIPE_GEMM_MC caps the cluster size: 1, 2 or 4; default 4):
   // 2 CTAs share B (two m-blocks, same n-block); 4 CTAs (2 x 2) also share A. Needs BN >= 128 (B, A
   // split into 64-row halves), two or more m-blocks, and for 4 an even number of n-blocks.
@@ -717,6 +824,9 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
   // caps the inner box at 64 elements).
   auto box_g = [&](bool is_a, int rows) {
     int gr = rows / 64;
+    if (!is_a && kind == GemmGroup::kNConcat)   // a multi-granule B box must not cross a part boundary
+      for (int i = 0; i < n; ++i)
+        if (ncum[i] % rows) return 1;
     for (int i = 0; i < n; ++i) {
       const OperandMap& m = is_a ? parts[i].a : parts[i].b;
       if (m.mn_major || (m.o_len < (1 << 30) && m.o_len % rows)) return 1;
@@ -786,7 +896,7 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
     const int64_t nlen = c0.n_len < p0.N ? c0.n_len : p0.N;
     const int64_t nseg = (p0.N + nlen - 1) / nlen;
     const bool segd = c0.seg.n > 0;           // N2: per-segment destinations (peers' receive blocks)
-    if (tma_epi_env && tma_bf16_env && !args.c_tma && kind == GemmGroup::kKConcat && c0.epi == Epi::kStoreBF16 &&
+    if (tma_epi_env && tma_bf16_env && !args.c_tma && kind != GemmGroup::kMConcat && c0.epi == Epi::kStoreBF16 &&
         seg_rows_ok && (segd || (c0.out_bf16 && (reinterpret_cast<uintptr_t>(c0.out_bf16) & 15) == 0)) &&
         c0.ld_bf16 % 8 == 0 && nlen % 64 == 0 && (segd || nseg == 1 || c0.r_nstride >= M)) {
       if (!segd) {
@@ -808,7 +918,8 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
     const OutMap& c0 = p0.c;
     if (c0.seg.n > 0) {
       const int64_t nlen = c0.n_len < p0.N ? c0.n_len : p0.N;
-      if (n != 1 || c0.epi != Epi::kStoreBF16 || c0.seg.n > kMaxSeg || c0.seg.n * nlen < p0.N ||
+      if ((n != 1 && kind != GemmGroup::kNConcat) || c0.epi != Epi::kStoreBF16 || c0.seg.n > kMaxSeg ||
+          c0.seg.n * nlen < p0.N ||
           c0.r_mstride != 0 || c0.m_len < M || c0.r_base != 0 || c0.c_base != 0 || c0.c_nstride != 0 ||
           c0.c_mstride != 0 || c0.ld_bf16 % 8) {
         snprintf(err, errlen, "gemm: segmented (direct-to-peer) output needs a single bf16-store GEMM with "

@@ -53,7 +53,7 @@ struct RopeRef {
 // Direct-to-peer destinations: a producer kernel writes block `seg` of its output
 // straight into the receive buffer of the rank that owns it (a CUDA-IPC mapping of that rank's
 // symmetric workspace) instead of into a local send buffer. kMaxSeg bounds the group (one box: 8 GPUs).
-constexpr int kMaxSeg = 8;
+constexpr int kMaxSeg = 16;   // C <= 8 ranks x up to 2 N-concatenated outputs (K | V)
 struct SegPtrs {
   void* p[kMaxSeg] = {};        // base of segment 0..n-1 (n = 0: not segmented)
   int n = 0;
@@ -86,6 +86,9 @@ struct OutMap {
   // receive block; replaces out_bf16 / r_nstride). Part 0 of a single (non-grouped) GEMM only.
   SegPtrs seg;
   RowDot dot;                   // part 0 of a single GEMM, kStoreBF16: fused row-dot (dot.o non-null)
+  // kStoreF32: the caller zeroed the output, so the GEMM may split K across units that ADD their partial
+  // products (atomically) -- used for the weight gradients, whose M x N tile count is below the SM count
+  bool zeroed = false;
 };
 
 struct GemmProblem {
@@ -102,7 +105,10 @@ cudaError_t gemm_run(const GemmProblem& p, cudaStream_t stream, char* err, size_
 //            e.g. dX = dQ Wq + dK Wk + dV Wv with one fp32 read-modify-write of dX;
 //  kMConcat: rows of part i = A_i B^T (equal N and K; each M_i but the last a multiple of 128;
 //            B operand of part 0; own output map per part), e.g. [dWq; dWk; dWv] = [dQ; dK; dV]^T X.
-enum class GemmGroup : int { kKConcat = 0, kMConcat = 1 };
+//  kNConcat: columns of part i = A B_i^T (equal M and K, one A operand: part 0's; each N_i a multiple of the
+//            tile width; bf16 store outputs addressed as one segmented output: the parts' n_len-column
+//            segments in order, e.g. [K | V] = X [Wk; Wv]^T into the K and V send (or peer receive) buffers).
+enum class GemmGroup : int { kKConcat = 0, kMConcat = 1, kNConcat = 2 };
 cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cudaStream_t stream, char* err,
                            size_t errlen);
 

@@ -266,17 +266,16 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       if (dir) g = direct_to(g, ws + W.qrecv[b], qbytes, e);
       return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
     });
-    if (P.kv_sent(s)) {
+    if (P.kv_sent(s)) {                    // K | V in one N-concatenated GEMM (X read once for both)
       const int kb = kvb(s);
-      R.run(UPIPE_TRACE_GEMM, q, "proj K", [&](char* e) {
-        GemmProblem g = proj_to_send(P, x, wk, kvrows, kv0 * d, kseg, kseg, ws + W.ksend, rope_seq);
-        if (dir) g = direct_to(g, ws + W.krecv[kb], kbytes, e);
-        return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
-      });
-      R.run(UPIPE_TRACE_GEMM, q, "proj V", [&](char* e) {
-        GemmProblem g = proj_to_send(P, x, wv, kvrows, kv0 * d, kseg, kseg, ws + W.vsend);
-        if (dir) g = direct_to(g, ws + W.vrecv[kb], kbytes, e);
-        return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
+      R.run(UPIPE_TRACE_GEMM, q, "proj K|V", [&](char* e) {
+        GemmProblem g[2] = {proj_to_send(P, x, wk, kvrows, kv0 * d, kseg, kseg, ws + W.ksend, rope_seq),
+                            proj_to_send(P, x, wv, kvrows, kv0 * d, kseg, kseg, ws + W.vsend)};
+        if (dir) {
+          g[0] = direct_to(g[0], ws + W.krecv[kb], kbytes, e);
+          g[1] = direct_to(g[1], ws + W.vrecv[kb], kbytes, e);
+        }
+        return e[0] ? cudaErrorInvalidValue : gemm_run_group(g, 2, GemmGroup::kNConcat, q, e, 512);
       });
     }
   };
@@ -580,6 +579,15 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     R.run(UPIPE_TRACE_AUX, st, "memset d(gamma)", [&](char*) {
       return cudaMemsetAsync(ws + W.dgam, 0, (size_t)2 * d * 4, st);
     });
+  // The weight gradients are zeroed first so their long-K GEMMs (K = S_l, only M x N = 1536 x 4096 output tiles)
+  // may split K across all SMs and add their partials (gemm.cu split-K); every dW row is written by one GEMM.
+  R.run(UPIPE_TRACE_AUX, st, "zero dW", [&](char*) {
+    cudaError_t e = cudaMemsetAsync(dwq, 0, (size_t)HqD * P.D * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(dwk, 0, (size_t)HkvD * P.D * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(dwv, 0, (size_t)HkvD * P.D * 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(dwo, 0, (size_t)HqD * P.D * 4, st);
+    return e;
+  });
   // dWo = dY^T O over this rank's tokens (all stages at once: o_saved holds every head)
   {
     GemmProblem g;
@@ -591,6 +599,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     g.c.out_f32 = dwo;
     g.c.ld_f32 = HqD;
     g.c.epi = Epi::kStoreF32;
+    g.c.zeroed = true;
     R.run(UPIPE_TRACE_GEMM, st, "dWo", [&](char* e) { return gemm_run(g, st, e, 512); });
   }
   const int n_dx_terms = P.nstages;   // one K-concatenated dX GEMM per stage
@@ -637,6 +646,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     g.c.m_len = seg;
     g.c.r_mstride = row_step;
     g.c.epi = Epi::kStoreF32;
+    g.c.zeroed = true;                     // zeroed at the start of the backward: split-K allowed
     return g;
   };
 
@@ -648,17 +658,16 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       if (dir) g = direct_to(g, ws + W.qrecv[b], qbytes, e);
       return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
     });
-    if (P.kv_sent(s)) {
+    if (P.kv_sent(s)) {                    // K | V in one N-concatenated GEMM (X read once for both)
       const int kb = kvb(s);
-      R.run(UPIPE_TRACE_GEMM, q, "proj K", [&](char* e) {
-        GemmProblem g = proj_to_send(P, x, wk, HkvD, kv0 * d, kseg, kseg, ws + W.ksend, rope_seq);
-        if (dir) g = direct_to(g, ws + W.krecv[kb], kbytes, e);
-        return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
-      });
-      R.run(UPIPE_TRACE_GEMM, q, "proj V", [&](char* e) {
-        GemmProblem g = proj_to_send(P, x, wv, HkvD, kv0 * d, kseg, kseg, ws + W.vsend);
-        if (dir) g = direct_to(g, ws + W.vrecv[kb], kbytes, e);
-        return e[0] ? cudaErrorInvalidValue : gemm_run(g, q, e, 512);
+      R.run(UPIPE_TRACE_GEMM, q, "proj K|V", [&](char* e) {
+        GemmProblem g[2] = {proj_to_send(P, x, wk, HkvD, kv0 * d, kseg, kseg, ws + W.ksend, rope_seq),
+                            proj_to_send(P, x, wv, HkvD, kv0 * d, kseg, kseg, ws + W.vsend)};
+        if (dir) {
+          g[0] = direct_to(g[0], ws + W.krecv[kb], kbytes, e);
+          g[1] = direct_to(g[1], ws + W.vrecv[kb], kbytes, e);
+        }
+        return e[0] ? cudaErrorInvalidValue : gemm_run_group(g, 2, GemmGroup::kNConcat, q, e, 512);
       });
     }
     GemmProblem g;
@@ -675,6 +684,21 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     g.c.n_len = qseg;
     g.c.r_nstride = P.S_l;
     g.c.epi = Epi::kStoreBF16;
+    static const bool fuse_env = [] {                // UPIPE_FUSED_ROWDOT=0: separate row-dot kernel (A/B)
+      const char* e = getenv("UPIPE_FUSED_ROWDOT");
+      return !(e && e[0] == '0');
+    }();
+    if (!dir && !fuse_env) {
+      g.c.out_bf16 = ws + W.dosend[b];
+      R.run(UPIPE_TRACE_GEMM, q, "dO", [&](char* e) { return gemm_run(g, q, e, 512); });
+      for (int p = 0; p < C; ++p)
+        R.run(UPIPE_TRACE_AUX, q, "rowdot", [&](char*) {
+          return rowdot_run((const upipe_bf16*)(ws + W.dosend[b]) + (int64_t)p * P.S_l * qseg, qseg,
+                            o_saved + (int64_t)P.q0(s, p) * d, HqD, (float*)(ws + W.dsend[b]) + (int64_t)p * P.S_l * P.qpd,
+                            P.qpd, P.S_l, P.qpd, d, q);
+        });
+      return;
+    }
     // delta = rowsum(dO * O) fused into the epilogue (A13): dO column (p, nin) <-> o_saved column
     // q0(s, p) d + nin = q0 d + p qstep + nin; delta of (token t, head j) -> block p of the delta send
     // buffer [C][S_l][qpd] (N2: block `me` of peer p's delta receive buffer)
