@@ -304,9 +304,14 @@ def main():
         torch.cuda.synchronize()
         out["peak_bytes"] = max_over_ranks(torch.cuda.max_memory_allocated() - base)   # max over ranks
         out["ws_bytes"] = attn.region_bytes if attn.ipc else sum(t.numel() for t in attn._ws.values())
-        # chunk buffers = workspace minus the U-independent fp32 dX accumulator [S_l, D] (only allocated
-        # when there is more than one stage): the "intermediate tensors" of P:332-343 (DESIGN A21)
-        out["chunk_bytes"] = out["ws_bytes"] - (S_l * D * 4 if Hq // chunk > 1 else 0)
+        # chunk buffers = workspace minus the U-independent pre-allocated gradient buffer G [S_l, (Hq + 2 Hkv) d]
+        # bf16 (DESIGN A30; with --naive-kv the fp32 dX accumulator [S_l, D], only with more than one stage):
+        # the "intermediate tensors" of P:332-343 (DESIGN A21)
+        fixed = 0
+        if Hq // chunk > 1:
+            gb = (Hq + 2 * Hkv) * d * 2
+            fixed = S_l * (D * 4 if args.naive_kv or gb > D * 4 else gb)
+        out["chunk_bytes"] = out["ws_bytes"] - fixed
         stream = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if trace:

@@ -189,7 +189,8 @@ UPIPE_API upipe_status_t upipe_comm_info(upipe_ctx_t ctx, upipe_comm_info_t* inf
  * 3: backward for a ctx created with UPIPE_FLAG_SYNC_COMM (one buffer set, the paper's
  * memory-minimal schedule). At C = 1 all-to-alls are identities and 0 == 2, 1 == 3.
  * 4 / 5: forward / backward with UPIPE_FLAG_DIRECT (receive buffers only, one set; an IPC ctx holds
- * it in its symmetric region, see upipe_ipc_region_size). */
+ * it in its symmetric region, see upipe_ipc_region_size). Add 8 for a ctx with UPIPE_FLAG_NAIVE_KV (its
+ * backward keeps a fp32 dX accumulator instead of the pre-allocated gradient buffer, DESIGN A30). */
 UPIPE_API upipe_status_t upipe_workspace_size(int cp_size, const upipe_shape_t* shape, int pass, size_t* bytes);
 
 /* Stage plan of the GQA schedule (A8): for stage s and device p the

@@ -241,8 +241,11 @@ upipe_status_t upipe_workspace_size(int cp_size, const upipe_shape_t* shape, int
   std::string m;
   upipe_status_t st = validate_shape(cp_size, shape, m);
   if (st != UPIPE_OK) return set_err(nullptr, st, m);
-  if (!bytes || pass < 0 || pass > 5) return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "pass must be 0..5");
-  const Plan P = make_plan(cp_size, *shape);
+  if (!bytes || pass < 0 || (pass & 7) > 5 || pass > 15)
+    return set_err(nullptr, UPIPE_ERR_INVALID_ARG, "pass must be 0..5, plus 8 for UPIPE_FLAG_NAIVE_KV");
+  Plan P = make_plan(cp_size, *shape);
+  P.naive = (pass & 8) != 0;
+  pass &= 7;
   const bool ov = pass < 2 && P.C > 1 && P.ring == 1;   // 0/1: default (overlapped for C > 1); 2/3: sequential
   const bool dir = pass >= 4 && direct_enabled(UPIPE_FLAG_DIRECT, P);   // 4/5: UPIPE_FLAG_DIRECT
   *bytes = (pass & 1) == 0 ? fwd_workspace(P, ov, dir).total : bwd_workspace(P, ov, dir).total;

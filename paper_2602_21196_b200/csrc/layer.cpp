@@ -955,7 +955,67 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   // B6: dX and dW for the stage's heads (and the retired K/V heads). dX += dQ Wq + dK Wk + dV Wv is
   // one K-concatenated GEMM (one fp32 read-modify-write of the dX accumulator per stage) and
   // [dWq; dWk; dWv] = [dQ; dK; dV]^T X one M-concatenated GEMM (DESIGN A24).
+  // Pre-allocated gradient buffer G [S_l][(Hq + 2 Hkv) d] bf16 (DESIGN A30; the backward analogue of the
+  // pre-allocated output of P:329): each stage's received dQ (and the retired dK / dV) land in their head
+  // columns, and dX = G [Wq; Wk; Wv] and [dWq; dWk; dWv] = G^T X run once after the stage loop -- one
+  // long-K GEMM with a bf16 epilogue instead of a fp32 dX read-modify-write per stage. Not with the naive
+  // ablation, whose stages send partial dK / dV, nor with one stage (Ulysses), whose dX GEMM stores bf16 directly.
+  const bool gbuf = P.gbuf();
+  const int64_t Gc = HqD + 2 * HkvD;
+  auto post_g = [&](int s, int b, cudaStream_t q) {
+    const int64_t q0 = P.q0(s, 0), kv0 = P.kv0(s, 0);
+    upipe_bf16* G = reinterpret_cast<upipe_bf16*>(ws + W.gbuf);
+    R.run(UPIPE_TRACE_AUX, q, "unpack dQ", [&](char*) {
+      return unpack_cols_run(ws + W.dqrecv[b], P.S_l, C, (int)qseg, G, Gc, q0 * d, qstep, q);
+    });
+    if (P.kv_last(s)) {
+      R.run(UPIPE_TRACE_AUX, q, "unpack dK", [&](char*) {
+        return unpack_cols_run(ws + W.dkrecv, P.S_l, C, (int)kseg, G, Gc, HqD + kv0 * d, kseg, q);
+      });
+      R.run(UPIPE_TRACE_AUX, q, "unpack dV", [&](char*) {
+        return unpack_cols_run(ws + W.dvrecv, P.S_l, C, (int)kseg, G, Gc, HqD + HkvD + kv0 * d, kseg, q);
+      });
+    }
+  };
+  auto final_g = [&](cudaStream_t q) {
+    const upipe_bf16* G = reinterpret_cast<const upipe_bf16*>(ws + W.gbuf);
+    const void* Ws[3] = {wq, wk, wv};
+    float* dWs[3] = {dwq, dwk, dwv};
+    const int64_t rows[3] = {HqD, HkvD, HkvD}, c0[3] = {0, HqD, HqD + HkvD};
+    GemmProblem gx[3], gw[3];
+    for (int i = 0; i < 3; ++i) {
+      GemmProblem& x1 = gx[i];               // dX += G[:, c0 : c0 + rows] W_i   (B = W_i, N = D contiguous)
+      x1.M = P.S_l;
+      x1.N = P.D;
+      x1.K = rows[i];
+      x1.a = OperandMap{G, Gc, P.S_l, Gc, false};
+      x1.a.k_base = c0[i];
+      x1.b = OperandMap{Ws[i], P.D, rows[i], P.D, true};
+      x1.c.out_bf16 = dx;
+      x1.c.ld_bf16 = P.D;
+      x1.c.epi = Epi::kStoreBF16;
+      GemmProblem& w1 = gw[i];               // dW_i = G[:, c0 : c0 + rows]^T X   (A MN-major: rows along G)
+      w1.M = rows[i];
+      w1.N = P.D;
+      w1.K = P.S_l;
+      w1.a = OperandMap{G, Gc, P.S_l, Gc, true};
+      w1.a.o_base = c0[i];
+      w1.b = OperandMap{x, P.D, P.S_l, P.D, true};
+      w1.c.out_f32 = dWs[i];
+      w1.c.ld_f32 = P.D;
+      w1.c.epi = Epi::kStoreF32;
+      w1.c.zeroed = true;
+    }
+    R.run(UPIPE_TRACE_GEMM, q, "dX = G W", [&](char* e) { return gemm_run_group(gx, 3, GemmGroup::kKConcat, q, e, 512); });
+    R.run(UPIPE_TRACE_GEMM, q, "dW = G^T X", [&](char* e) {
+      return gemm_run_group(gw, 3, GemmGroup::kMConcat, q, e, 512);
+    });
+  };
   auto post = [&](int s, int b, cudaStream_t q) {
+    if (gbuf) {
+      post_g(s, b, q);
+      return;
+    }
     const int64_t q0 = P.q0(s, 0), kv0 = P.kv0(s, 0);
     GemmProblem gx[3], gw[3];
     int n = 1;
@@ -1061,6 +1121,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     cudaStreamWaitEvent(st, e_out[(nu - 1) & 1], 0);
     post(nu - 1, (nu - 1) & 1, st);
   }
+  if (gbuf && R.status == UPIPE_OK) final_g(st);
   if (qknorm && R.status == UPIPE_OK)
     R.run(UPIPE_TRACE_AUX, st, "d(gamma) out", [&](char*) {
       cudaError_t e = cudaMemcpyAsync(qkn->dq_norm_w, ws + W.dgam, (size_t)d * 4, cudaMemcpyDeviceToDevice, st);

@@ -168,7 +168,10 @@ BwdWs bwd_workspace(const Plan& p, bool overlap, bool direct) {
   w.dvsend = take_send(ke);
   w.dkrecv = comm ? take(ke) : w.dksend;
   w.dvrecv = comm ? take(ke) : w.dvsend;
-  w.dxacc = p.nstages > 1 ? take((size_t)p.S_l * p.D * 4) : 0;   // one stage: dX is stored in bf16 directly
+  // dX: the pre-allocated gradient buffer G [S_l][(Hq + 2 Hkv) d] bf16 (DESIGN A30), or with the naive
+  // ablation the fp32 accumulator [S_l][D] (one stage: dX is stored in bf16 directly)
+  w.gbuf = p.gbuf() ? take((size_t)p.S_l * (p.Hq + 2 * p.Hkv) * p.d * 2) : 0;
+  w.dxacc = !p.gbuf() && p.nstages > 1 ? take((size_t)p.S_l * p.D * 4) : 0;
   if (p.sh.qk_norm_eps > 0.f) {             // Qwen3 q/k norm (DESIGN A29): normalised copies for the attention
     for (int i = 0; i < 2; ++i) {           // (the receive buffers keep the pre-norm heads for the chain rule),
       const bool fresh = i == 0 || dbl;     // fp32 dK for the fused norm backward, d(gamma) scratch

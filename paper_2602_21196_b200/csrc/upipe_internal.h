@@ -34,6 +34,9 @@ struct Plan {
   bool kv_last(int s) const { return naive || (s % sigma) == sigma - 1; }
   int kv_group(int s) const { return naive ? s : s / sigma; }   // stages sharing one K/V receive buffer
   int kv_pos(int s) const { return naive ? 0 : s % sigma; }     // position within that group
+  // backward dX through the pre-allocated gradient buffer G [S_l][(Hq + 2 Hkv) d] bf16 (DESIGN A30) instead of
+  // a fp32 accumulator [S_l][D]: with more than one stage, not naive, and only where G is no larger
+  bool gbuf() const { return !naive && nstages > 1 && (int64_t)(Hq + 2 * Hkv) * d * 2 <= (int64_t)D * 4; }
   // per-device step of the first q head / kv head between consecutive devices (same for every s)
   int q_dev_stride() const { return kv_res * R; }
   int kv_dev_stride() const { return kv_res; }
@@ -54,6 +57,7 @@ struct FwdWs {
 struct BwdWs {
   size_t qsend[2], qrecv[2], ksend, krecv[2], vsend, vrecv[2], dosend[2], dorecv[2], dsend[2], drecv[2], dqacc[2],
       dqsend[2], dqrecv[2], dkacc, dvacc, dksend, dvsend, dkrecv, dvrecv, dxacc;
+  size_t gbuf;                                        // pre-allocated gradient buffer (not with naive KV)
   size_t dqsem;                                       // UPIPE_FLAG_DETERMINISTIC dQ-order semaphores (int32)
   size_t qn[2], kn[2], dgam;                          // Qwen3 q/k norm (shape.qk_norm_eps > 0) only
   size_t kring[2], vring[2], dkring[2], dvring[2];   // ring hybrid only

@@ -89,7 +89,8 @@ class UPipeAttention:
         key = seq_local
         if key not in self._ws:
             sync = 2 if self.flags & 1 else 0
-            n = max(U.upipe_workspace_size(self.C, self.shape(seq_local), p + sync) for p in (0, 1))
+            naive = 8 if self.flags & 2 else 0
+            n = max(U.upipe_workspace_size(self.C, self.shape(seq_local), p + sync + naive) for p in (0, 1))
             self._ws[key] = torch.empty(max(n, 256), dtype=torch.uint8, device=self.device)
         return self._ws[key]
 
