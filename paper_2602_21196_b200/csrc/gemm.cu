@@ -815,7 +815,13 @@ cudaError_t gemm_run_group(const GemmProblem* parts, int n, GemmGroup kind, cuda
     store_epi = store_epi && (parts[i].c.epi == Epi::kStoreBF16 || parts[i].c.epi == Epi::kStoreF32);
   // ... and only with K long enough to amortise the 128 x 512 tile's un-overlapped epilogue (~9K cycles
   // against 1K per k-block; measured 131072 x 4096 x 1024: 1044 TFLOP/s wide vs cuBLAS 1258)
-  if (pair && wide_env && pair_env == 1 && bn == 256 && store_epi && bn_ok(512) && K >= 2048) bn = 512;
+  // ... and (UPIPE_GEMM_WIDE_DOT=0) not with the fused row-dot, whose epilogue also reads O (A/B)
+  static const int wide_dot_env = [] {
+    const char* e = getenv("UPIPE_GEMM_WIDE_DOT");
+    return e ? atoi(e) : 1;
+  }();
+  const bool dot_ok = wide_dot_env || !parts[0].c.dot.o;
+  if (pair && wide_env && pair_env == 1 && bn == 256 && store_epi && bn_ok(512) && K >= 2048 && dot_ok) bn = 512;
   const bool pair4 = pair && pair_env >= 2 && bn == 256 && M > 3 * BM;
   if (pair) cl = pair4 ? 4 : 2;
   const bool mc = cl > 1;
