@@ -52,6 +52,37 @@ def a2a_bytes(S_l, C, Hq, Hkv, d, U, naive=False):
     return {"fwd_inp": fwd_inp, "fwd_out": fwd_out, "bwd": bwd, "total": fwd_inp + fwd_out + bwd}
 
 
+def memory_by_cp(upipe, S, Hq, Hkv, d, D, U, naive=False):
+    """Per-rank chunk buffers at the metric's CP degrees 1/2/4/8 for this S and U, from the library's workspace
+    planner (exact byte counts of the buffers the library would use; host-side, so the 2/4/8-GPU points are
+    PLANNED, not measured on this one-GPU run): the overlapped schedule (default for C > 1), the sequential one
+    and the direct-to-peer one (N2), UPipe against chunk = all-heads Ulysses. Chunk buffers = workspace minus
+    the U-independent gradient buffer (DESIGN A21, A30)."""
+    out = {}
+    gib = float(2 ** 30)
+    for C in (1, 2, 4, 8):
+        if S % C or U % C or Hkv % C:
+            continue
+        S_l = S // C
+        g = S_l * min((Hq + 2 * Hkv) * d * 2, D * 4) if not naive else S_l * D * 4
+        row = {}
+        for name, (pf, pb) in (("overlap", (0, 1)), ("sequential", (2, 3)), ("direct", (4, 5))):
+            if C == 1 and name != "sequential":
+                continue
+            nv = 8 if naive else 0
+            sh_u = upipe.make_shape(S_l, D, Hq, Hkv, d, U)
+            sh_h = upipe.make_shape(S_l, D, Hq, Hkv, d, Hq)
+            up = [upipe.upipe_workspace_size(C, sh_u, p + nv) for p in (pf, pb)]
+            ul = [upipe.upipe_workspace_size(C, sh_h, p + nv) for p in (pf, pb)]
+            up_chunk = max(up[0], up[1] - (g if Hq // U > 1 else 0))
+            ul_chunk = max(ul[0], ul[1])
+            row[name] = {"workspace_gib": max(up) / gib, "chunk_buffers_gib": up_chunk / gib,
+                         "ulysses_chunk_buffers_gib": ul_chunk / gib, "reduction": 1 - up_chunk / ul_chunk}
+        out[str(C)] = row
+    out["note"] = "per rank, from upipe_workspace_size (planned; only C = N is measured by this run)"
+    return out
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -402,6 +433,7 @@ def main():
         "workspace_gib": main_run["ws_bytes"] / 2**30,
         "chunk_buffers_gib": main_run["chunk_bytes"] / 2**30,
         "clocks": clocks,
+        "memory_by_cp": memory_by_cp(upipe, S, Hq, Hkv, d, D, U, args.naive_kv),
     }
     if C > 1 and args.ring == 1:
         # all-to-all volume of one fwd+bwd step on this rank (the plan's per-stage buffers; each rank keeps
