@@ -266,11 +266,22 @@ def main():
     import torch.distributed as dist
 
     rank, world, local = env_rank()
+    # UPIPE_BENCH_SAME_GPU=1 (tests only): every rank on cuda:0 with a gloo process group, so the N > 1 code
+    # path (IPC transport, max-over-ranks timing, all-to-all accounting) runs on a one-GPU box; its timings
+    # are of ranks sharing one GPU and mean nothing
+    same_gpu = os.environ.get("UPIPE_BENCH_SAME_GPU") == "1"
+    if same_gpu and world > 1 and args.transport != "ipc":
+        raise SystemExit("UPIPE_BENCH_SAME_GPU=1 needs --transport ipc (NCCL cannot run two ranks on one GPU)")
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         pg = dist.group.WORLD
     from paper_2602_21196_b200 import UPipeAttention, upipe
     import synth
@@ -312,7 +323,7 @@ def main():
     def max_over_ranks(v):
         if pg is None:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if same_gpu else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -366,7 +377,7 @@ def main():
         out["attn"] = attn
         return out
 
-    sampler = ClockSampler(local) if local == 0 else None
+    sampler = ClockSampler(local) if local == 0 and rank == 0 else None
     if sampler:
         sampler.start()
     main_run = run(U, args.steps, args.warmup, trace=True)
