@@ -97,7 +97,7 @@ typedef struct {
                           P:433, DESIGN A29): each head of the projection is divided by
                           sqrt(mean of its squares + qk_norm_eps) and scaled by its weight vector
                           (upipe_qk_norm_t), then rotated (RoPE) if rope_base > 0. Qwen3: 1e-6.
-                          Needs upipe_attn_fwd_ex / upipe_attn_bwd_ex and ring_degree <= 1. */
+                          Needs upipe_attn_fwd_ex / upipe_attn_bwd_ex. */
 } upipe_shape_t;
 
 #define UPIPE_UID_BYTES 128

@@ -234,8 +234,8 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
   // Qwen3 q/k norm (DESIGN A29): the projections send the pre-norm heads; each head owner normalises (and
   // rotates: RoPE follows the norm) its received rows in place before the attention
   const bool qknorm = P.sh.qk_norm_eps > 0.f;
-  RopeRef rope_head = rope_seq;            // head layout: rows are the global tokens 0..S-1 (no ring with q/k norm)
-  rope_head.pos0 = 0;
+  RopeRef rope_head = rope_seq;            // head layout: rows are the ring block's tokens (ring_i S ..)
+  rope_head.pos0 = (int64_t)(ctx->rank / P.C) * P.S;
   if (qknorm) rope_seq = RopeRef{};
   rope_seq.pos0 = (int64_t)ctx->rank * P.S_l;
   // Ulysses group of the ring hybrid (DESIGN A27): ranks [first, first + C); plain UPipe: first = 0, C = cp_size
@@ -909,9 +909,10 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       cudaStreamWaitEvent(q, rev[1 + (rr & 1)], 0);     // the home hop has landed
       if (last) {
         RopeRef rope_k = rope_head;                       // dK rows are the ring block's keys
-        R.run(UPIPE_TRACE_AUX, q, "cvt dK", [&](char*) {
-          return cvt_f32_bf16_run((const float*)(ws + W.dkacc), kseg, ws + W.dksend, kseg, P.S, kseg, 1.0f, q, rope_k);
-        });
+        if (!qknorm)                                      // (q/k norm: the chain rule below converts dK)
+          R.run(UPIPE_TRACE_AUX, q, "cvt dK", [&](char*) {
+            return cvt_f32_bf16_run((const float*)(ws + W.dkacc), kseg, ws + W.dksend, kseg, P.S, kseg, 1.0f, q, rope_k);
+          });
         R.run(UPIPE_TRACE_AUX, q, "cvt dV", [&](char*) {
           return cvt_f32_bf16_run((const float*)(ws + W.dvacc), kseg, ws + W.dvsend, kseg, P.S, kseg, 1.0f, q);
         });

@@ -34,8 +34,6 @@ upipe_status_t validate_shape(int C, const upipe_shape_t* sh, std::string& msg) 
     return bad(UPIPE_ERR_INVALID_ARG, "rope_base must be 0 (off) or a finite base > 1 (DESIGN A26)");
   if (!(sh->qk_norm_eps >= 0.f && sh->qk_norm_eps < 1.f))
     return bad(UPIPE_ERR_INVALID_ARG, "qk_norm_eps must be 0 (off) or in (0, 1) (Qwen3: 1e-6; DESIGN A29)");
-  if (sh->qk_norm_eps > 0.f && ring > 1)
-    return bad(UPIPE_ERR_UNSUPPORTED, "qk_norm_eps > 0 with ring_degree > 1 (DESIGN A29)");
   if (sh->head_dim != 64 && sh->head_dim != 128) return bad(UPIPE_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
   if (sh->hidden < 64 || sh->hidden % 64) return bad(UPIPE_ERR_UNSUPPORTED, "hidden % 64 != 0 (TMA tile granule)");
   if (sh->n_kv_heads % C)

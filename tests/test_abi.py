@@ -167,8 +167,8 @@ def test_qk_norm_validation_and_workspace(U):
     assert abs(grow2 - (qe + ke + 2 * ke + 2 * 64 * 4)) <= 256 * 4
     bad = U.make_shape(1024, 512, 8, 2, 64, 2, qk_norm_eps=-1.0)
     assert U.upipe_validate(2, bad)[0] == 1
-    ring = U.make_shape(1024, 512, 8, 2, 64, 2, ring_degree=2, qk_norm_eps=1e-6)
-    assert U.upipe_validate(4, ring)[0] == 2
+    ring = U.make_shape(1024, 512, 8, 2, 64, 2, ring_degree=2, qk_norm_eps=1e-6)   # with the ring hybrid too
+    assert U.upipe_validate(4, ring)[0] == 0
 
 
 def test_workspace_c1_aliases_send_and_recv(U):

@@ -421,17 +421,18 @@ def test_deterministic_backward_bitwise(C, Hq, Hkv, d, U, ring):
     _check(r1, inp, C, Hq, Hkv, d, U, ring=ring)
 
 
-@pytest.mark.parametrize("C,S,D,Hq,Hkv,d,U,rope,sync", [
-    (1, 512, 512, 8, 2, 64, 2, 0.0, False),           # one GPU, d = 64 (128-query backward, row-major dQ)
-    (1, 768, 1024, 8, 2, 128, 4, 1e6, False),         # d = 128: dim-major dQ, RoPE after the norm
-    (2, 1024, 512, 8, 2, 128, 4, 1e4, False),         # CP 2, overlapped schedule
-    (1, 1024, 512, 8, 2, 128, 4, 1e4, False),         # ... the same layer on one GPU
-    (4, 1024, 1024, 64, 8, 128, 8, 1e6, False),       # Qwen3-32B heads (64 Q / 8 KV), CP 4, sigma = 2
-    (2, 600, 512, 8, 8, 64, 4, 0.0, True),            # MHA, sequential, ragged S_l = 300
+@pytest.mark.parametrize("C,S,D,Hq,Hkv,d,U,rope,sync,ring", [
+    (1, 512, 512, 8, 2, 64, 2, 0.0, False, 1),        # one GPU, d = 64 (128-query backward, row-major dQ)
+    (1, 768, 1024, 8, 2, 128, 4, 1e6, False, 1),      # d = 128: dim-major dQ, RoPE after the norm
+    (2, 1024, 512, 8, 2, 128, 4, 1e4, False, 1),      # CP 2, overlapped schedule
+    (1, 1024, 512, 8, 2, 128, 4, 1e4, False, 1),      # ... the same layer on one GPU
+    (4, 1024, 1024, 64, 8, 128, 8, 1e6, False, 1),    # Qwen3-32B heads (64 Q / 8 KV), CP 4, sigma = 2
+    (2, 600, 512, 8, 8, 64, 4, 0.0, True, 1),         # MHA, sequential, ragged S_l = 300
+    (4, 1024, 512, 8, 2, 64, 2, 1e4, True, 2),        # UPipe x Ring (2 x 2): K blocks travel normalised
 ])
-def test_qk_norm_layer(C, S, D, Hq, Hkv, d, U, rope, sync):
+def test_qk_norm_layer(C, S, D, Hq, Hkv, d, U, rope, sync, ring):
     # Qwen3 per-head q/k RMSNorm (DESIGN A29): y, O, dx, every dW and d(gamma_q), d(gamma_k)
     # against the fp64 oracle at the north_star bar
-    r, inp = _run_group(C, S, D, Hq, Hkv, d, U, rope_base=rope, sync=sync, qk_norm_eps=1e-6)
+    r, inp = _run_group(C, S, D, Hq, Hkv, d, U, rope_base=rope, sync=sync, qk_norm_eps=1e-6, ring=ring)
     eo, ey = _boundary_abs(inp, Hq, Hkv, d, rope or None)     # absolute bars as in test_mha_control_cp8 (A28)
-    _check(r, inp, C, Hq, Hkv, d, U, rope_base=rope or None, abs_y=max(ABS, ey), abs_o=max(ABS, eo))
+    _check(r, inp, C, Hq, Hkv, d, U, rope_base=rope or None, abs_y=max(ABS, ey), abs_o=max(ABS, eo), ring=ring)
