@@ -116,7 +116,7 @@ typedef struct {
                                    projection and dO projection epilogues (TMA stores), the attention
                                    epilogue (O, dK, dV), the dQ conversion -- so no send buffers exist and no
                                    copy or NCCL kernel moves the chunk; ordering by GPU front-end flags.
-                                   Needs a ctx from upipe_ipc_create/connect, C <= 8, ring_degree 1; one
+                                   Needs a ctx from upipe_ipc_create/connect, Ulysses degree <= 8; one
                                    buffer set (the transfers overlap inside the kernels, not on a side
                                    stream). Ignored at C = 1. */
 

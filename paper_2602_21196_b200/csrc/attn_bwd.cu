@@ -55,8 +55,6 @@ struct BwdArgs {
   int dq_dim_major;  // q64 kernel: dq_acc is [nq*d][S] (TMA boxes of 32 dims x 32 tokens)
   int* dq_sem;       // deterministic dQ (UPIPE_FLAG_DETERMINISTIC): per (head, query tile, box group) the
                      // number of key tiles that have added their partial; key tile jb adds when it reads jb
-  int head_inner;    // visiting order (head, query tile): 1 = heads inner, so every CTA of the launch is at
-                     // the same query tile at the same step (needed by dq_sem, whose waits then chain in lockstep)
   long long* dbg;    // optional per-role cycle breakdown of CTA (0,0) (UPIPE_BWD_TIMELINE=1)
   // N2 (nkseg / nvseg > 0): bf16 dK / dV row t -> {dk,dv}seg[t / kvseg_rows] + (t % kvseg_rows) * ld_kvb (a
   // peer's receive block) instead of dk_bf16 / dv_bf16
@@ -146,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int N = G * n_qt;                         // (head, query tile) iterations
   constexpr int kSoftmax = kSoftmaxWarps * 32;
   // visiting order: heads outer, query tiles up from the diagonal (default), or heads inner and query
-  // tiles down to the diagonal (a.head_inner: all CTAs of the launch in lockstep, for dq_sem)
+  // tiles down to the diagonal (DET: all CTAs of the launch in lockstep, for dq_sem)
   auto tile_h = [&](int n) { return g * G + (DET ? n % G : n / n_qt); };
   auto tile_qt = [&](int n) { return DET ? nT - 1 - n / G : qt_begin + n % n_qt; };
 
@@ -587,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Query tiles are visited from the last one down to the diagonal: CTAs that run at the same time then
   // reduce their dQ partials into the same rows of dq_acc (L2 hits) instead of each starting at its own
   // diagonal and sweeping a different region (measured: the dQ reduce-adds dominated the energy).
-  // Heads of the KV group outer (default) or inner (a.head_inner).
+  // Heads of the KV group outer (default) or inner (DET, the deterministic lockstep order).
   auto tile_h = [&](int n) { return g * G + (DET ? n % G : n / n_qt); };
   auto tile_qt = [&](int n) { return nT64 - 1 - (DET ? n / G : n % n_qt); };
   constexpr int kWg = 128;
@@ -1015,7 +1013,6 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   a.rope = p.rope;
   a.dq_dim_major = 0;
   a.dq_sem = p.dq_sem;
-  a.head_inner = p.dq_sem ? 1 : 0;   // the deterministic variant's lockstep order (DET template)
   // UPIPE_BWD_TIMELINE=1: per-role cycle breakdown of CTA (0,0), printed to stderr after the launch
   static long long* dbg_dev = nullptr;
   const char* tlenv = getenv("UPIPE_BWD_TIMELINE");

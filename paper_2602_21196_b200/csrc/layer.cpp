@@ -373,6 +373,8 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     // each visible block's partial (fp32 O, lse) is merged by its LSE. Own block first (causal).
     void* const o_dst = a.o;
     const int64_t ld_dst = a.ldo;
+    const SegPtrs o_seg_dst = a.o_seg;                  // N2: the merged O goes to the owners (below)
+    a.o_seg = SegPtrs{};                                // the ring's attention writes fp32 partials
     float* const lse_acc = a.lse;
     a.o32 = (float*)(ws + W.oacc);
     a.ldo32 = qseg;
@@ -425,6 +427,9 @@ upipe_status_t layer_fwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       cudaStreamWaitEvent(q, rev[0], 0);
     }
     R.run(UPIPE_TRACE_AUX, q, "O fp32 -> bf16", [&](char*) {
+      if (o_seg_dst.n)
+        return cvt_f32_bf16_seg_run((const float*)(ws + W.oacc), qseg, o_seg_dst, ld_dst, P.S, qseg, 1.0f, q,
+                                    RopeRef{});
       return cvt_f32_bf16_run((const float*)(ws + W.oacc), qseg, o_dst, ld_dst, P.S, qseg, 1.0f, q);
     });
   };
@@ -859,6 +864,8 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       bp.dk_acc = (float*)(ws + W.dkacc);
       bp.dv_acc = (float*)(ws + W.dvacc);
       bp.dk_bf16 = bp.dv_bf16 = nullptr;
+      const SegPtrs dv_seg_dst = bp.dv_seg;             // N2: the home dK / dV go to the owners (below)
+      bp.dk_seg = bp.dv_seg = SegPtrs{};                // the ring's kernels accumulate fp32 only
       bp.kv_write_acc = 1;
       // Overlapped ring (all ring collectives on the ctx's comm stream, same order on every rank): the
       // accumulators of step t travel right after this rank's attention of step t-1 (that dependency is
@@ -911,9 +918,14 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
         RopeRef rope_k = rope_head;                       // dK rows are the ring block's keys
         if (!qknorm)                                      // (q/k norm: the chain rule below converts dK)
           R.run(UPIPE_TRACE_AUX, q, "cvt dK", [&](char*) {
+            if (dir)
+              return cvt_f32_bf16_seg_run((const float*)(ws + W.dkacc), kseg, dk_seg, kseg, P.S, kseg, 1.0f, q, rope_k);
             return cvt_f32_bf16_run((const float*)(ws + W.dkacc), kseg, ws + W.dksend, kseg, P.S, kseg, 1.0f, q, rope_k);
           });
         R.run(UPIPE_TRACE_AUX, q, "cvt dV", [&](char*) {
+          if (dir)
+            return cvt_f32_bf16_seg_run((const float*)(ws + W.dvacc), kseg, dv_seg_dst, kseg, P.S, kseg, 1.0f, q,
+                                        RopeRef{});
           return cvt_f32_bf16_run((const float*)(ws + W.dvacc), kseg, ws + W.dvsend, kseg, P.S, kseg, 1.0f, q);
         });
       }

@@ -180,7 +180,7 @@ namespace upipe {
 // Direct-to-peer mode (UPIPE_FLAG_DIRECT): producers write into the owners' receive buffers;
 // one buffer set, no send buffers, no comm stream.
 inline bool direct_enabled(uint32_t flags, const Plan& P) {
-  return (flags & UPIPE_FLAG_DIRECT) && P.C > 1 && P.ring == 1;
+  return (flags & UPIPE_FLAG_DIRECT) && P.C > 1;
 }
 inline bool overlap_enabled(uint32_t flags, const Plan& P) {
   return P.C > 1 && P.ring == 1 && !(flags & UPIPE_FLAG_SYNC_COMM) && !direct_enabled(flags, P);

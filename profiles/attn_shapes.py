@@ -77,7 +77,6 @@ for spec in args.shapes:
     pairs = S * (S + 1) // 2
     tf, tb = timed(fwd, args.reps), timed(bwd, args.reps)
     print(json.dumps({"S": S, "nq": nq, "nkv": nkv, "d": d, "det": args.det,
-                      "head_inner": os.environ.get("UPIPE_BWD_HEAD_INNER", "0"),
                       "fwd_ms": tf, "fwd_tflops": 4 * d * pairs * nq / tf / 1e9,
                       "bwd_ms": tb, "bwd_tflops": 10 * d * pairs * nq / tb / 1e9}), flush=True)
     del q, k, v, do, o, lse, delta, dq, dk, dv, sem

@@ -85,19 +85,20 @@ def test_ipc_multiprocess_layer_matches_oracle(C, S, D, Hq, Hkv, d, U, sync, rin
 
 
 @pytest.mark.timeout(900)
-@pytest.mark.parametrize("C,S,D,Hq,Hkv,d,U,rope", [
-    (2, 512, 512, 8, 2, 64, 2, 0.0),         # BASELINE configs[0] schedule
-    (4, 1024, 1024, 32, 8, 128, 8, 0.0),     # Llama3-8B heads at CP 4, U 8 (qpd 2, sigma 2)
-    (8, 1024, 1024, 32, 8, 128, 8, 5e5),     # Llama3-8B heads at CP 8, U 8 (qpd 1, sigma 4), RoPE
-    (4, 1024, 512, 16, 4, 64, 16, 0.0),      # Ulysses (U = Hq)
-    (4, 1000, 512, 16, 16, 64, 8, 0.0),      # MHA, ragged S_l = 250 (tiles straddle the rank blocks)
+@pytest.mark.parametrize("C,S,D,Hq,Hkv,d,U,rope,ring", [
+    (2, 512, 512, 8, 2, 64, 2, 0.0, 1),         # BASELINE configs[0] schedule
+    (4, 1024, 1024, 32, 8, 128, 8, 0.0, 1),     # Llama3-8B heads at CP 4, U 8 (qpd 2, sigma 2)
+    (8, 1024, 1024, 32, 8, 128, 8, 5e5, 1),     # Llama3-8B heads at CP 8, U 8 (qpd 1, sigma 4), RoPE
+    (4, 1024, 512, 16, 4, 64, 16, 0.0, 1),      # Ulysses (U = Hq)
+    (4, 1000, 512, 16, 16, 64, 8, 0.0, 1),      # MHA, ragged S_l = 250 (tiles straddle the rank blocks)
+    (4, 1024, 512, 8, 2, 64, 2, 1e4, 2),        # UPipe x Ring (2 x 2): direct Ulysses all-to-alls, IPC ring steps
 ])
-def test_ipc_direct_layer_matches_oracle(C, S, D, Hq, Hkv, d, U, rope):
+def test_ipc_direct_layer_matches_oracle(C, S, D, Hq, Hkv, d, U, rope, ring):
     # UPIPE_FLAG_DIRECT: the projection / dO epilogues, the attention epilogues (O, dK, dV) and the
     # dQ conversion store straight into the owners' receive buffers in the other processes
-    res = _run_ipc(C, dict(S=S, D=D, Hq=Hq, Hkv=Hkv, d=d, U=U, direct=True, rope=rope))
+    res = _run_ipc(C, dict(S=S, D=D, Hq=Hq, Hkv=Hkv, d=d, U=U, direct=True, rope=rope, ring=ring))
     inp = synth.layer_inputs(0, S, D, Hq, Hkv, d)
-    _check(res, inp, C, Hq, Hkv, d, U, rope_base=rope or None)
+    _check(res, inp, C, Hq, Hkv, d, U, rope_base=rope or None, ring=ring)
 
 
 @pytest.mark.timeout(900)
