@@ -229,3 +229,21 @@ def test_bench_a2a_bytes_match_oracle_comm_volume():
             # library's naive ablation re-sends the stage's distinct KV heads, not one duplicate per q head
             naive = a2a_bytes(S_l, C, Hq, Hkv, d, Uc, naive=True)["fwd_inp"] / slice_bytes
             assert naive == oracle.comm_volume(oracle.naive_schedule(Hq, Hkv, C, Uc), C), (Hq, Hkv, C, Uc)
+
+
+def test_bench_memory_by_cp_closed_forms():
+    # bench.memory_by_cp (the metric's "peak activation at 1/2/4/8", planned from the library): the MHA control
+    # meets 1 - U/H exactly at every CP degree and schedule; under GQA the Q-path floor keeps the total below it
+    # (DESIGN A22); the direct schedule needs the least memory
+    from bench import memory_by_cp
+    from paper_2602_21196_b200 import upipe
+    m = memory_by_cp(upipe, 1 << 20, 32, 32, 128, 4096, 8)
+    for C in ("1", "2", "4", "8"):
+        for sched, row in m[C].items():
+            assert abs(row["reduction"] - 0.75) < 1e-9, (C, sched)
+    g = memory_by_cp(upipe, 1 << 20, 32, 8, 128, 4096, 8)
+    assert abs(g["1"]["sequential"]["reduction"] - 0.75) < 1e-9
+    for C in ("2", "4", "8"):
+        r = g[C]
+        assert r["direct"]["chunk_buffers_gib"] < r["sequential"]["chunk_buffers_gib"] < r["overlap"]["chunk_buffers_gib"]
+    assert g["8"]["sequential"]["reduction"] < 0.75
