@@ -18,6 +18,8 @@
 #include <vector>
 #include <cstdlib>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing unless a profiler injects itself
+
 #include "kernels.h"
 #include "upipe_internal.h"
 
@@ -27,7 +29,8 @@ namespace {
 
 using bf16p = const upipe_bf16*;
 
-// Brackets one step with trace events on the stream it runs on (no-op when tracing is off).
+// Brackets one step with trace events on the stream it runs on (no-op when tracing is off) and an NVTX range
+// named after the step (host-side enqueue range; nsys / ncu correlate the step's launches with it).
 struct Step {
   upipe_ctx_s* ctx;
   cudaStream_t st;
@@ -35,12 +38,14 @@ struct Step {
   const char* label;
   cudaEvent_t a = nullptr;
   Step(upipe_ctx_s* c, cudaStream_t s, int k, const char* l = "") : ctx(c), st(s), cat(k), label(l) {
+    nvtxRangePushA(label && label[0] ? label : "upipe step");
     if (ctx->tracer.on) {
       a = ctx->tracer.get();
       cudaEventRecord(a, st);
     }
   }
   ~Step() {
+    nvtxRangePop();
     if (a) {
       cudaEvent_t b = ctx->tracer.get();
       cudaEventRecord(b, st);
