@@ -186,12 +186,14 @@ cudaError_t unpack_cols_run(const void* src, int64_t rows, int nseg, int seg_col
 // head h) of [rows][heads][d] bf16 (row stride ld; dst may alias src); rope.pos0 = position of row 0.
 cudaError_t qk_prep_run(const void* src, void* dst, int64_t rows, int heads, int d, int64_t ld, const void* gamma,
                         float eps, const RopeRef& rope, cudaStream_t s);
+constexpr int kNormBwdMaxBlocks = 148 * 6;
 // Its chain rule fused into the fp32 -> bf16 gradient conversion: g = rope^-1(scale * src) (src row-major
 // [rows][heads d] with row stride st, or dim_major [heads d][st]), x = the pre-norm rows (bf16, stride
 // ldx); writes bf16 dx to dst (row stride ldd) or dst_seg (N2) and ADDS sum_t g * x_hat into dgamma[d] (fp32).
 cudaError_t norm_bwd_run(const float* src, int64_t st, bool dim_major, const void* x, int64_t ldx, void* dst,
                          int64_t ldd, const SegPtrs* dst_seg, int64_t rows, int heads, int d, float scale,
-                         const void* gamma, float eps, const RopeRef& inverse_rope, float* dgamma, cudaStream_t s);
+                         const void* gamma, float eps, const RopeRef& inverse_rope, float* dgamma, cudaStream_t s,
+                         float* det_partials = nullptr);   // non-null: [kNormBwdMaxBlocks][d] scratch, fixed order
 cudaError_t synth_fill_bf16_run(void* dst, int64_t n, uint64_t seed, int tensor_id, int exponent, int64_t start,
                                 cudaStream_t s);
 

@@ -589,6 +589,8 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     R.run(UPIPE_TRACE_AUX, st, "memset d(gamma)", [&](char*) {
       return cudaMemsetAsync(ws + W.dgam, 0, (size_t)2 * d * 4, st);
     });
+  // UPIPE_FLAG_DETERMINISTIC: no split-K either (its partial products are added in arrival order)
+  const bool det_order = (ctx->flags & UPIPE_FLAG_DETERMINISTIC) != 0;
   // The weight gradients are zeroed first so their long-K GEMMs (K = S_l, only M x N = 1536 x 4096 output tiles)
   // may split K across all SMs and add their partials (gemm.cu split-K); every dW row is written by one GEMM.
   R.run(UPIPE_TRACE_AUX, st, "zero dW", [&](char*) {
@@ -609,7 +611,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     g.c.out_f32 = dwo;
     g.c.ld_f32 = HqD;
     g.c.epi = Epi::kStoreF32;
-    g.c.zeroed = true;
+    g.c.zeroed = !det_order;
     R.run(UPIPE_TRACE_GEMM, st, "dWo", [&](char* e) { return gemm_run(g, st, e, 512); });
   }
   const int n_dx_terms = P.nstages;   // one K-concatenated dX GEMM per stage
@@ -656,7 +658,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
     g.c.m_len = seg;
     g.c.r_mstride = row_step;
     g.c.epi = Epi::kStoreF32;
-    g.c.zeroed = true;                     // zeroed at the start of the backward: split-K allowed
+    g.c.zeroed = !det_order;                     // zeroed at the start of the backward: split-K allowed
     return g;
   };
 
@@ -941,13 +943,15 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       R.run(UPIPE_TRACE_AUX, q, "dQ norm bwd", [&](char*) {
         return norm_bwd_run((const float*)(ws + W.dqacc[b]), bp.dq_dim_major ? bp.ld_dqt : qseg, bp.dq_dim_major != 0,
                             ws + W.qrecv[b], qseg, dir ? nullptr : ws + W.dqsend[b], qseg, dir ? &dq_seg : nullptr,
-                            P.S, P.qpd, d, 1.0f, qkn->q_norm_w, P.sh.qk_norm_eps, rope_head, (float*)(ws + W.dgam), q);
+                            P.S, P.qpd, d, 1.0f, qkn->q_norm_w, P.sh.qk_norm_eps, rope_head, (float*)(ws + W.dgam), q,
+                            det ? (float*)(ws + W.dgam) + 2 * d : nullptr);
       });
       if (last)
         R.run(UPIPE_TRACE_AUX, q, "dK norm bwd", [&](char*) {
           return norm_bwd_run((const float*)(ws + W.dkacc), kseg, false, ws + W.krecv[kvb(s)], kseg,
                               dir ? nullptr : ws + W.dksend, kseg, dir ? &dk_seg : nullptr, P.S, P.kv_res, d, 1.0f,
-                              qkn->k_norm_w, P.sh.qk_norm_eps, rope_head, (float*)(ws + W.dgam) + d, q);
+                              qkn->k_norm_w, P.sh.qk_norm_eps, rope_head, (float*)(ws + W.dgam) + d, q,
+                              det ? (float*)(ws + W.dgam) + 2 * d : nullptr);
         });
       return;
     }
@@ -1022,7 +1026,7 @@ upipe_status_t layer_bwd(upipe_ctx_s* ctx, const Plan& P, bf16p x, bf16p wq, bf1
       w1.c.out_f32 = dWs[i];
       w1.c.ld_f32 = P.D;
       w1.c.epi = Epi::kStoreF32;
-      w1.c.zeroed = true;
+      w1.c.zeroed = !det_order;              // split-K adds in arrival order: not in deterministic mode
     }
     R.run(UPIPE_TRACE_GEMM, q, "dX = G W", [&](char* e) { return gemm_run_group(gx, 3, GemmGroup::kKConcat, q, e, 512); });
     R.run(UPIPE_TRACE_GEMM, q, "dW = G^T X", [&](char* e) {

@@ -238,7 +238,8 @@ __global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__
                                                        __nv_bfloat16* __restrict__ dst, long long ldd, SegPtrs seg,
                                                        long long rows, int heads, float scale,
                                                        const __nv_bfloat16* __restrict__ gamma, float eps,
-                                                       RopeRef rope, float* __restrict__ dgamma) {
+                                                       RopeRef rope, float* __restrict__ dgamma,
+                                                       float* __restrict__ partials) {
   constexpr int d = G * 8;
   __shared__ float tile[d][65];
   __shared__ float red[d];
@@ -314,10 +315,29 @@ __global__ void __launch_bounds__(256) norm_bwd_kernel(const float* __restrict__
     }
   }
   __syncthreads();
+  if (partials) {   // deterministic: this block's d(gamma) partial in thread order, reduced in block order below
+    for (int w = 0; w < (int)blockDim.x / G; ++w) {
+      if (t / G == w)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) red[sub * 8 + i] += acc[i];
+      __syncthreads();
+    }
+    for (int i = t; i < d; i += blockDim.x) partials[(long long)blockIdx.x * d + i] = red[i];
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 8; ++i) atomicAdd(&red[sub * 8 + i], acc[i]);
   __syncthreads();
   for (int i = t; i < d; i += blockDim.x) atomicAdd(dgamma + i, red[i]);
+}
+
+// dgamma[i] += sum over blocks b (in order) of partials[b][i]
+__global__ void sum_partials_kernel(const float* __restrict__ partials, int nblocks, int d, float* __restrict__ dgamma) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < nblocks; ++b) s += partials[(long long)b * d + i];
+    dgamma[i] += s;
+  }
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
@@ -448,22 +468,28 @@ cudaError_t qk_prep_run(const void* src, void* dst, int64_t rows, int heads, int
 
 cudaError_t norm_bwd_run(const float* src, int64_t st, bool dim_major, const void* x, int64_t ldx, void* dst,
                          int64_t ldd, const SegPtrs* dst_seg, int64_t rows, int heads, int d, float scale,
-                         const void* gamma, float eps, const RopeRef& inverse_rope, float* dgamma, cudaStream_t s) {
+                         const void* gamma, float eps, const RopeRef& inverse_rope, float* dgamma, cudaStream_t s,
+                         float* det_partials) {
   if (rows <= 0 || heads <= 0) return cudaSuccess;
   if (dst_seg && dst_seg->n && !seg_covers(*dst_seg, rows)) return cudaErrorInvalidValue;
   const SegPtrs seg = dst_seg ? *dst_seg : SegPtrs{};
   const long long tiles = ((rows + 63) / 64) * heads;
-  const int grid = (int)(tiles < 148 * 6 ? tiles : 148 * 6);
+  const int grid = (int)(tiles < kNormBwdMaxBlocks ? tiles : kNormBwdMaxBlocks);
   const auto* xp = static_cast<const __nv_bfloat16*>(x);
   auto* dp = static_cast<__nv_bfloat16*>(dst);
   const auto* gp = static_cast<const __nv_bfloat16*>(gamma);
 #define UPIPE_NORM_BWD(G, DM) \
-  norm_bwd_kernel<G, DM><<<grid, 256, 0, s>>>(src, st, xp, ldx, dp, ldd, seg, rows, heads, scale, gp, eps, inverse_rope, dgamma)
+  norm_bwd_kernel<G, DM><<<grid, 256, 0, s>>>(src, st, xp, ldx, dp, ldd, seg, rows, heads, scale, gp, eps, inverse_rope, \
+                                               dgamma, det_partials)
   if (d == 128) { if (dim_major) UPIPE_NORM_BWD(16, true); else UPIPE_NORM_BWD(16, false); }
   else if (d == 64) { if (dim_major) UPIPE_NORM_BWD(8, true); else UPIPE_NORM_BWD(8, false); }
   else return cudaErrorInvalidValue;
 #undef UPIPE_NORM_BWD
   count_launches(1);
+  if (det_partials) {
+    sum_partials_kernel<<<1, 128, 0, s>>>(det_partials, grid, d, dgamma);
+    count_launches(1);
+  }
   return cudaGetLastError();
 }
 

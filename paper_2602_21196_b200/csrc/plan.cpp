@@ -177,7 +177,7 @@ BwdWs bwd_workspace(const Plan& p, bool overlap, bool direct) {
       w.kn[i] = fresh ? take(ke) : w.kn[0];
     }
     if (!w.dkacc) w.dkacc = take(ke * 2);
-    w.dgam = take((size_t)2 * p.d * 4);
+    w.dgam = take((size_t)(2 + kNormBwdMaxBlocks) * p.d * 4);   // d(gamma_q), d(gamma_k), det partials
   }
   w.dqsem = take((size_t)attn_bwd_sem_count(p.S, p.qpd) * 4);     // deterministic mode (a few hundred KB)
   w.total = off;

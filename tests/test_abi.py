@@ -161,10 +161,11 @@ def test_qk_norm_validation_and_workspace(U):
     assert U.upipe_workspace_size(2, sh1, 2) == U.upipe_workspace_size(2, sh0, 2)
     S, qe, ke = 2048, 2048 * 1 * 64 * 2, 2048 * 1 * 64 * 2
     grow = U.upipe_workspace_size(2, sh1, 3) - U.upipe_workspace_size(2, sh0, 3)
-    assert abs(grow - (qe + ke + 2 * 64 * 4)) <= 256 * 4          # sigma = 4: the fp32 dK accumulator exists already
+    dgam = (2 + 148 * 6) * 64 * 4                                   # d(gamma) + deterministic per-block partials
+    assert abs(grow - (qe + ke + dgam)) <= 256 * 4                  # sigma = 4: the fp32 dK accumulator exists already
     sh2 = U.make_shape(1024, 512, 8, 8, 64, 2, qk_norm_eps=1e-6)    # MHA, sigma = 1: the fp32 dK is new
     grow2 = U.upipe_workspace_size(2, sh2, 3) - U.upipe_workspace_size(2, U.make_shape(1024, 512, 8, 8, 64, 2), 3)
-    assert abs(grow2 - (qe + ke + 2 * ke + 2 * 64 * 4)) <= 256 * 4
+    assert abs(grow2 - (qe + ke + 2 * ke + dgam)) <= 256 * 4
     bad = U.make_shape(1024, 512, 8, 2, 64, 2, qk_norm_eps=-1.0)
     assert U.upipe_validate(2, bad)[0] == 1
     ring = U.make_shape(1024, 512, 8, 2, 64, 2, ring_degree=2, qk_norm_eps=1e-6)   # with the ring hybrid too

@@ -436,3 +436,25 @@ def test_qk_norm_layer(C, S, D, Hq, Hkv, d, U, rope, sync, ring):
     r, inp = _run_group(C, S, D, Hq, Hkv, d, U, rope_base=rope, sync=sync, qk_norm_eps=1e-6, ring=ring)
     eo, ey = _boundary_abs(inp, Hq, Hkv, d, rope or None)     # absolute bars as in test_mha_control_cp8 (A28)
     _check(r, inp, C, Hq, Hkv, d, U, rope_base=rope or None, abs_y=max(ABS, ey), abs_o=max(ABS, eo), ring=ring)
+
+
+def test_qk_norm_deterministic_bitwise():
+    # UPIPE_FLAG_DETERMINISTIC with the q/k norm: d(gamma) is reduced over fixed per-block partials in block order
+    # (no float atomics) and the weight gradients skip split-K, so the whole backward is bitwise reproducible
+    r1, inp = _run_group(2, 1024, 512, 8, 2, 128, 4, rope_base=1e4, qk_norm_eps=1e-6, det=True)
+    r2, _ = _run_group(2, 1024, 512, 8, 2, 128, 4, rope_base=1e4, qk_norm_eps=1e-6, det=True)
+    for p in range(2):
+        for k in r1[p]:
+            assert torch.equal(r1[p][k], r2[p][k]), (p, k)
+    eo, ey = _boundary_abs(inp, 8, 2, 128, 1e4)
+    _check(r1, inp, 2, 8, 2, 128, 4, rope_base=1e4, abs_y=max(ABS, ey), abs_o=max(ABS, eo))
+
+
+def test_deterministic_backward_bitwise_with_long_k():
+    # at S_l = 16384 the weight-gradient GEMMs would split K across CTA pairs (atomic adds); the deterministic
+    # mode keeps them unsplit, so dW stays bitwise reproducible at sizes where split-K is active by default
+    S, D, Hq, Hkv, d, U = 16384, 512, 8, 2, 64, 2
+    r1, inp = _run_group(1, S, D, Hq, Hkv, d, U, det=True)
+    r2, _ = _run_group(1, S, D, Hq, Hkv, d, U, det=True)
+    for k in r1[0]:
+        assert torch.equal(r1[0][k], r2[0][k]), k
