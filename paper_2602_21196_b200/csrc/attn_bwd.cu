@@ -551,7 +551,10 @@ struct Q64Cfg {
   static constexpr uint32_t TM_S0 = 0, TM_DP0 = 64, TM_S1 = 128, TM_DP1 = 192, TM_DV = 256, TM_DK = 384;
 };
 
-template <bool TL, bool DET = false>
+// PAIR (UPIPE_BWD_PAIR): clusters of two CTAs on adjacent key tiles (2i, 2i+1) of one KV head visit the same
+// query tiles in the same order (the even tile's range; the odd CTA's extra tiles are fully masked for it), so
+// each CTA loads one half of every Q / dO tile and multicasts it to both: half the L2 -> SM operand traffic.
+template <bool TL, bool DET = false, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_q64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -579,7 +582,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int g = blockIdx.y;
   const int G = a.nq / a.nkv;
   const int nT64 = (int)((a.S + 63) / 64);
-  const int qt_begin = a.causal ? 2 * jb : 0;
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0;
+  const int qt_begin = a.causal ? 2 * (PAIR ? (jb & ~1) : jb) : 0;   // PAIR: the pair's common (even) range
   const int n_qt = nT64 - qt_begin;
   const int N = G * n_qt;
   // Query tiles are visited from the last one down to the diagonal: CTAs that run at the same time then
@@ -592,13 +596,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == kTmaWarp && lane == 0) {
     tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
-    for (int i = 0; i < 22; ++i) mbar_init(&bars[i], (i == 15 || i == 16 || i == 19 || i == 20) ? kWg : 1);
+    for (int i = 0; i < 22; ++i) {
+      const bool slot_empty = (i >= 4 && i < 7) || (i >= 10 && i < 13);   // q_empty, do_empty: both CTAs release
+      mbar_init(&bars[i], (i == 15 || i == 16 || i == 19 || i == 20) ? kWg : (PAIR && slot_empty ? 2 : 1));
+    }
     fence_barrier_init();
     tmem_slot[1] = smem_u32(smem);
   }
   if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();                // the peer's barriers exist before any multicast lands in them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -616,15 +624,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int qt = tile_qt(n);
         const int st = n % C::NQ;
         const uint32_t ph = ((n / C::NQ) & 1) ^ 1;
-        mbar_wait(&q_empty[st], ph);
+        mbar_wait(&q_empty[st], ph);              // PAIR: this slot is free in both CTAs
         mbar_arrive_expect_tx(&q_full[st], C::QT);
+        if (PAIR) {                               // this CTA's half (one 64-dim chunk) to both CTAs
+          tma_load_3d_mc(smem + C::OFF_Q + st * C::QT + crank * 8192, &tmQ, &q_full[st], crank * 64, h, qt * 64, 0x3);
+        } else {
 #pragma unroll
-        for (int c = 0; c < 2; ++c) tma_load_3d(smem + C::OFF_Q + st * C::QT + c * 8192, &tmQ, &q_full[st], c * 64, h, qt * 64);
+          for (int c = 0; c < 2; ++c) tma_load_3d(smem + C::OFF_Q + st * C::QT + c * 8192, &tmQ, &q_full[st], c * 64, h, qt * 64);
+        }
         mbar_wait(&do_empty[st], ph);
         mbar_arrive_expect_tx(&do_full[st], C::QT);
+        if (PAIR) {
+          tma_load_3d_mc(smem + C::OFF_DO + st * C::QT + crank * 8192, &tmdO, &do_full[st], crank * 64, h, qt * 64,
+                         0x3);
+        } else {
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d(smem + C::OFF_DO + st * C::QT + c * 8192, &tmdO, &do_full[st], c * 64, h, qt * 64);
+          for (int c = 0; c < 2; ++c)
+            tma_load_3d(smem + C::OFF_DO + st * C::QT + c * 8192, &tmdO, &do_full[st], c * 64, h, qt * 64);
+        }
       }
     }
   } else if (warp == kMmaWarp) {
@@ -682,11 +699,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       load_base();
       const uint32_t sds = base + C::OFF_DS + x * 16384;
       mma_dv(tmem + slot_s(x), base + C::OFF_DO + st * C::QT, n > 0);
-      mma_commit_w(&do_empty[st]);
+      if (PAIR) mma_commit_mc_w(&do_empty[st], 0x3);   // released in both CTAs (each loads into both)
+      else mma_commit_w(&do_empty[st]);
       mma_dq(base + C::OFF_K, sds, tmem + slot_dp(x));
       mma_commit_w(&dq_full[x]);
       mma_dk(sds, base + C::OFF_Q + st * C::QT, n > 0);
-      mma_commit_w(&q_empty[st]);
+      if (PAIR) mma_commit_mc_w(&q_empty[st], 0x3);
+      else mma_commit_w(&q_empty[st]);
       if (n + 2 < N) {
         const int st2 = (n + 2) % C::NQ;
         const uint32_t ph2 = ((n + 2) / C::NQ) & 1;
@@ -744,7 +763,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long e1 = tick<TL>();
       te[0] += e1 - e0;
       tc_fence_after();
-      const bool need_mask = (a.causal && (qt >> 1) == jb) || q0 + 64 > a.S || (long long)jb * 128 + 128 > a.S;
+      // the diagonal tile pair, and (PAIR, odd CTA) the pair's common tiles that lie entirely below its keys
+      const bool need_mask = (a.causal && (qt >> 1) <= jb) || q0 + 64 > a.S || (long long)jb * 128 + 128 > a.S;
       const long long qmin = key >= a.S ? a.S : (a.causal ? key : 0);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -937,6 +957,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+  if (PAIR) cluster_sync();                // no CTA leaves while its peer may still multicast into it or signal it
 }
 
 // d = 128: the 64-query ping-pong kernel. Under the 1000 W power cap it runs at lower SM clocks than
@@ -944,6 +965,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 // query order it is ahead at every length measured: attn bwd per step 375 -> 340 ms at 128K, 5940 ->
 // 5618 ms at 512K, 24184 -> 24066 ms at 1M (profiles/r01_ab_bwd_q64_dimmajor_512k_1m.txt). Before those
 // two changes it lost at 512K (6005 vs 6091 ms). UPIPE_BWD_Q64=0 selects the 128-query kernel.
+// The CTA-pair variant of the 64-query kernel (Q / dO multicast within the pair), default: half the L2 -> SM
+// operand traffic lowers the energy per tile, so the power-capped clock rises (A/B at 128K on one box: attn
+// bwd 350.3 -> 342.7 ms per step at 1477-1485 -> 1507 MHz). UPIPE_BWD_PAIR=0 selects the single-CTA launch.
+bool bwd_pair() {
+  static const bool on = [] {
+    const char* v = getenv("UPIPE_BWD_PAIR");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 bool use_q64(const AttnBwdProblem& p) {
   static const int q64_env = [] {
     const char* v = getenv("UPIPE_BWD_Q64");
@@ -1042,7 +1074,9 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
                                  errlen)) {
       return cudaErrorInvalidValue;
     }
-    const cudaError_t attr = set_smem_attr((const void*)attn_bwd_q64_kernel<false>, Q64Cfg::SMEM) == cudaSuccess
+    const cudaError_t attr = set_smem_attr((const void*)attn_bwd_q64_kernel<false>, Q64Cfg::SMEM) == cudaSuccess &&
+                                     set_smem_attr((const void*)attn_bwd_q64_kernel<false, false, true>, Q64Cfg::SMEM) ==
+                                         cudaSuccess
                                  ? set_smem_attr((const void*)attn_bwd_q64_kernel<false, true>, Q64Cfg::SMEM)
                                  : cudaErrorInvalidValue;
     if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd_q64 attr: %s", cudaGetErrorString(attr)); return attr; }
@@ -1050,7 +1084,23 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
     if (attr2 != cudaSuccess) { snprintf(err, errlen, "attn_bwd_q64 attr: %s", cudaGetErrorString(attr2)); return attr2; }
     if (a.dbg) attn_bwd_q64_kernel<true><<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
     else if (a.dq_sem) attn_bwd_q64_kernel<false, true><<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
-    else attn_bwd_q64_kernel<false><<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
+    else if (bwd_pair()) {
+      // CTA pairs (clusters of 2 along the key tiles; an odd tile count gets one key tile past the end, fully
+      // masked and written nowhere)
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      cfg.gridDim = dim3((unsigned)((nT + 1) & ~1), (unsigned)p.nkv);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = Q64Cfg::SMEM;
+      cfg.stream = stream;
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, attn_bwd_q64_kernel<false, false, true>, tq64, tk, tv, tdo64, tdq64, a);
+    } else attn_bwd_q64_kernel<false><<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
     count_launches(1);
     e = cudaGetLastError();
     if (e != cudaSuccess) snprintf(err, errlen, "attn_bwd_q64 launch: %s", cudaGetErrorString(e));

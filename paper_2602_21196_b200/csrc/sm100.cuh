@@ -107,6 +107,15 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* s
 }
 // TMA 2D load multicast to the CTAs of ctaMask in the cluster (same smem offset and mbarrier
 // offset in every destination CTA; each destination's barrier receives the complete_tx bytes).
+// 3-D box multicast to the CTAs of `mask` (same shared-memory offset and barrier offset in each)
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
                                                uint16_t mask) {
   asm volatile(
