@@ -82,7 +82,10 @@ struct FwdCfg {
   static_assert(SMEM <= 232448, "shared memory");
 };
 
-template <int D, bool TL>
+// PAIR (UPIPE_FWD_PAIR): clusters of two CTAs on adjacent query-tile pairs of one head stream the same KV
+// tiles (the longer pair's range; the shorter one's extra tiles are fully masked for its tile B), each CTA
+// loading one 64-dimension half of every K / V tile with a TMA multicast to both: half the L2 -> SM K/V traffic.
+template <int D, bool TL, bool PAIR = false>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
@@ -103,20 +106,22 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = warp_id(), lane = lane_id();
-  const int pair = a.n_pairs - 1 - blockIdx.x;    // longest (causal) work first
+  const int pair = a.n_pairs - 1 - blockIdx.x;    // longest (causal) work first (PAIR: -1 = padding CTA)
   const int head = blockIdx.y;
   const int kvh = head / (a.nq / a.nkv);
   const int qt0 = 2 * pair;                       // query tile index of A (B = qt0 + 1)
   const int ntiles_kv = (int)((a.S + 127) / 128);
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0;
+  const int qt_long = PAIR ? 2 * (a.n_pairs - 1 - (int)(blockIdx.x & ~1u)) : qt0;   // the cluster's longer pair
   const int nA = a.causal ? min(qt0 + 1, ntiles_kv) : ntiles_kv;
-  const int nB = a.causal ? min(qt0 + 2, ntiles_kv) : ntiles_kv;
+  const int nB = a.causal ? min(qt_long + 2, ntiles_kv) : ntiles_kv;   // PAIR: the KV stream both CTAs share
 
   if (warp == 8 && lane == 0) {
     tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);
     mbar_init(q_full, 1);
-    mbar_init(k_full, 1); mbar_init(k_empty, 1);
+    mbar_init(k_full, 1); mbar_init(k_empty, PAIR ? 2 : 1);   // PAIR: released by both CTAs
     for (int s = 0; s < C::V_STAGES; ++s) {
-      mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1);
+      mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], PAIR ? 2 : 1);
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1); mbar_init(&s_free[t], 128); mbar_init(&p_full[t], 128); mbar_init(&o_full[t], 1);
@@ -127,6 +132,7 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();                      // the peer's barriers exist before any multicast lands in them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -143,15 +149,24 @@ __global__ void __launch_bounds__(384, 1)
       for (int it = 0; it < nB; ++it) {
         mbar_wait(k_empty, (it & 1) ^ 1);
         mbar_arrive_expect_tx(k_full, C::QBYTES);
+        if (PAIR) {                                 // this CTA's 64-dimension half to both CTAs
+          tma_load_3d_mc(smem + C::OFF_K + crank * 16384, &tmK, k_full, crank * 64, kvh, it * 128, 0x3);
+        } else {
 #pragma unroll
-        for (int c = 0; c < NCH; ++c)
-          tma_load_3d(smem + C::OFF_K + c * 16384, &tmK, k_full, c * 64, kvh, it * 128);
+          for (int c = 0; c < NCH; ++c)
+            tma_load_3d(smem + C::OFF_K + c * 16384, &tmK, k_full, c * 64, kvh, it * 128);
+        }
         const int sv = it % C::V_STAGES;
         mbar_wait(&v_empty[sv], ((it / C::V_STAGES) & 1) ^ 1);
         mbar_arrive_expect_tx(&v_full[sv], C::QBYTES);
+        if (PAIR) {
+          tma_load_3d_mc(smem + C::OFF_V + sv * C::QBYTES + crank * 16384, &tmV, &v_full[sv], crank * 64, kvh, it * 128,
+                         0x3);
+        } else {
 #pragma unroll
-        for (int c = 0; c < NCH; ++c)
-          tma_load_3d(smem + C::OFF_V + sv * C::QBYTES + c * 16384, &tmV, &v_full[sv], c * 64, kvh, it * 128);
+          for (int c = 0; c < NCH; ++c)
+            tma_load_3d(smem + C::OFF_V + sv * C::QBYTES + c * 16384, &tmV, &v_full[sv], c * 64, kvh, it * 128);
+        }
       }
     }
   } else if (warp == 9) {
@@ -187,7 +202,8 @@ __global__ void __launch_bounds__(384, 1)
       mma_commit_w(&s_full[0]);
       issue_S(base + C::OFF_QB, base + C::OFF_K, tmem + C::TM_SB);
       mma_commit_w(&s_full[1]);
-      mma_commit_w(k_empty);                      // K(0) consumed once both S MMAs complete
+      if (PAIR) mma_commit_mc_w(k_empty, 0x3);   // K(0) consumed once both S MMAs complete (both CTAs)
+      else mma_commit_w(k_empty);
       // Per KV tile: S(it+1) of each tile is issued as soon as its softmax has read S(it) (P lives in
       // smem, so the S columns are free), then PV(it) once P(it) is written. The softmax of a tile
       // therefore never waits for its own PV + S round trip, only for the tensor core's queue.
@@ -209,7 +225,8 @@ __global__ void __launch_bounds__(384, 1)
           tc_fence_after();
           issue_S(base + C::OFF_QB, base + C::OFF_K, tmem + C::TM_SB);
           mma_commit_w(&s_full[1]);
-          mma_commit_w(k_empty);
+          if (PAIR) mma_commit_mc_w(k_empty, 0x3);
+          else mma_commit_w(k_empty);
         }
         tw[0] += tick<TL>() - w0;
         w0 = tick<TL>();
@@ -230,7 +247,8 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         issue_PV(base + C::OFF_PB, base + C::OFF_V + sv * C::QBYTES, tmem + C::TM_OB, it > 0);
         mma_commit_w(&o_full[1]);
-        mma_commit_w(&v_empty[sv]);
+        if (PAIR) mma_commit_mc_w(&v_empty[sv], 0x3);
+        else mma_commit_w(&v_empty[sv]);
       }
       if (TL && a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) {
         for (int i = 0; i < 4; ++i) a.dbg[i] = tw[i];
@@ -270,7 +288,7 @@ __global__ void __launch_bounds__(384, 1)
       const long long e2 = tick<TL>();
       ts[1] += e2 - e1;
       const long long key0 = (long long)it * 128;
-      const bool edge = a.causal ? (it == qt) : (key0 + 128 > a.S);
+      const bool edge = a.causal ? (it >= qt) : (key0 + 128 > a.S);   // PAIR: it > qt is fully masked
       if (edge) {
 #pragma unroll
         for (int i = 0; i < 128; ++i) {
@@ -359,34 +377,36 @@ __global__ void __launch_bounds__(384, 1)
     if (TL && a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && quad == 0)
       for (int i = 0; i < 5; ++i) a.dbg[6 + wg * 5 + i] = ts[i];
     // ---- epilogue: O / l -> bf16, lse
-    mbar_wait(&o_full[wg], (n - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l_run;
-    const bool valid = q < a.S;
-    __nv_bfloat16* orow = (a.noseg ? a.oseg[valid ? q / a.oseg_rows : 0] + (q % a.oseg_rows) * a.ldo : a.o + q * a.ldo) +
-                          (long long)head * D;   // N2: straight into the owner rank's O receive block
+    if (n > 0) {                                    // PAIR padding CTA: tile A has no key tiles
+      mbar_wait(&o_full[wg], (n - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l_run;
+      const bool valid = q >= 0 && q < a.S;
+      __nv_bfloat16* orow = (a.noseg ? a.oseg[valid ? q / a.oseg_rows : 0] + (q % a.oseg_rows) * a.ldo : a.o + q * a.ldo) +
+                            (long long)head * D;   // N2: straight into the owner rank's O receive block
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t r[32];
-      tmem_ld32(tO + c * 32, r);
-      tmem_wait_ld();
-      if (valid && a.o32) {
-        float4* dst = reinterpret_cast<float4*>(a.o32 + q * a.ldo32 + (long long)head * D + c * 32);
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tO + c * 32, r);
+        tmem_wait_ld();
+        if (valid && a.o32) {
+          float4* dst = reinterpret_cast<float4*>(a.o32 + q * a.ldo32 + (long long)head * D + c * 32);
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          dst[i] = make_float4(__uint_as_float(r[4 * i + 0]) * inv, __uint_as_float(r[4 * i + 1]) * inv,
-                               __uint_as_float(r[4 * i + 2]) * inv, __uint_as_float(r[4 * i + 3]) * inv);
-      } else if (valid) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(__uint_as_float(r[4 * i + 0]) * inv, __uint_as_float(r[4 * i + 1]) * inv,
+                                 __uint_as_float(r[4 * i + 2]) * inv, __uint_as_float(r[4 * i + 3]) * inv);
+        } else if (valid) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_uint4(pack_bf16(__uint_as_float(r[8 * i + 0]) * inv, __uint_as_float(r[8 * i + 1]) * inv),
-                              pack_bf16(__uint_as_float(r[8 * i + 2]) * inv, __uint_as_float(r[8 * i + 3]) * inv),
-                              pack_bf16(__uint_as_float(r[8 * i + 4]) * inv, __uint_as_float(r[8 * i + 5]) * inv),
-                              pack_bf16(__uint_as_float(r[8 * i + 6]) * inv, __uint_as_float(r[8 * i + 7]) * inv));
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(pack_bf16(__uint_as_float(r[8 * i + 0]) * inv, __uint_as_float(r[8 * i + 1]) * inv),
+                                pack_bf16(__uint_as_float(r[8 * i + 2]) * inv, __uint_as_float(r[8 * i + 3]) * inv),
+                                pack_bf16(__uint_as_float(r[8 * i + 4]) * inv, __uint_as_float(r[8 * i + 5]) * inv),
+                                pack_bf16(__uint_as_float(r[8 * i + 6]) * inv, __uint_as_float(r[8 * i + 7]) * inv));
+        }
       }
+      if (valid) a.lse[(long long)head * a.ld_lse + q] = (m_ref + __log2f(l_run)) * 0.69314718055994531f;
     }
-    if (valid) a.lse[(long long)head * a.ld_lse + q] = (m_ref + __log2f(l_run)) * 0.69314718055994531f;
   }
   tc_fence_before();
   __syncthreads();
@@ -394,6 +414,7 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+  if (PAIR) cluster_sync();                      // no CTA leaves while its peer may still multicast into it
 }
 
 }  // namespace
@@ -448,7 +469,32 @@ cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err
     count_launches(1);
     return cudaSuccess;
   };
-  if (p.d == 128) e = a.dbg ? go(attn_fwd_kernel<128, true>, FwdCfg<128>::SMEM) : go(attn_fwd_kernel<128, false>, FwdCfg<128>::SMEM);
+  // PAIR: clusters of two CTAs (an odd pair count gets one padding CTA, fully masked, storing nothing)
+  auto go_pair = [&](auto kern, int smem) -> cudaError_t {
+    cudaError_t at = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (at != cudaSuccess) { snprintf(err, errlen, "attn_fwd attr: %s", cudaGetErrorString(at)); return at; }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute la[1];
+    cfg.gridDim = dim3((unsigned)((a.n_pairs + 1) & ~1), (unsigned)p.nq);
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = 2;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, a);
+    count_launches(1);
+    return le;
+  };
+  static const bool pair_env = [] {
+    const char* v = getenv("UPIPE_FWD_PAIR");
+    return v && v[0] == '1';
+  }();
+  if (p.d == 128 && !a.dbg && pair_env) e = go_pair(attn_fwd_kernel<128, false, true>, FwdCfg<128>::SMEM);
+  else if (p.d == 128) e = a.dbg ? go(attn_fwd_kernel<128, true>, FwdCfg<128>::SMEM) : go(attn_fwd_kernel<128, false>, FwdCfg<128>::SMEM);
   else e = go(attn_fwd_kernel<64, false>, FwdCfg<64>::SMEM);
   if (e != cudaSuccess) return e;
   e = cudaGetLastError();
