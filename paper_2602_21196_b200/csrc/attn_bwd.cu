@@ -536,6 +536,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   dV(n) += P^T dO, dQ^T(n) = K^T dS (into dP_x), dK(n) += dS^T Q, S(n+2), dP(n+2)
 // where S / dP / dQ^T are N = 64 MMAs. dQ^T leaves TMEM with one dimension per lane and is staged
 // transposed (one 64 x 32 fp32 box per drain warp) for the TMA reduce-add into dq_acc.
+// kDkTs (UPIPE_BWD_DK_TS=1 at build time): the q64 kernel's dK MMA takes dS^T from TMEM (TS form; the softmax
+// warps store it next to P^T in the slot's S columns, which the S^T read has freed) instead of from shared
+// memory: 16 KB less shared-memory operand traffic per 64-query tile. Measured neutral (same-box A/B at 128K,
+// profiles/r02_ab_bwd_dkts.txt: attn bwd 82.5 vs 82.7 ms per launch, 339.9 vs 338.7 ms per bench step), so the
+// tensor pipe's operand reads do not compete with the other shared-memory traffic here; off by default.
+#ifndef UPIPE_BWD_DK_TS
+#define UPIPE_BWD_DK_TS 0
+#endif
+constexpr bool kDkTs = UPIPE_BWD_DK_TS != 0;
+
 struct Q64Cfg {
   static constexpr int D = 128;
   static constexpr int KT = 128 * D * 2;            // K or V tile: 128 keys x 128 d bf16 (two 16 KB chunks)
@@ -658,17 +668,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_ss_w(tm, da + (((i >> 2) * 16384 + (i & 3) * 32) >> 4), db + (((i >> 2) * 8192 + (i & 3) * 32) >> 4),
                  id_sp, i != 0);
     };
+    // TMEM column of the 16-query A chunk ks (P^T, or dS^T at +16) in a slot's S columns: see kDkTs
+    auto a_col = [](int ks) -> uint32_t { return kDkTs ? (ks >> 1) * 32 + (ks & 1) * 8 : ks * 8; };
     auto mma_dv = [&](uint32_t tp, uint32_t sdo, bool acc) {       // dV += P^T dO: A = P^T (TMEM, 64 q)
       const uint64_t db = desc_sw128(sdo, 8192, 1024);
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks)
-        mma_ts_w(tmem + C::TM_DV, tp + ks * 8, db + ks * (2048 >> 4), id_kmn, (acc || ks) ? 1u : 0u);
+        mma_ts_w(tmem + C::TM_DV, tp + a_col(ks), db + ks * (2048 >> 4), id_kmn, (acc || ks) ? 1u : 0u);
     };
-    auto mma_dk = [&](uint32_t sds, uint32_t sq, bool acc) {       // dK += dS^T Q: A = dS^T (K-major, 64 q)
+    auto mma_dk = [&](uint32_t sds, uint32_t tp, uint32_t sq, bool acc) {   // dK += dS^T Q (64 q)
       const uint64_t da = desc_sw128(sds, 16, 1024), db = desc_sw128(sq, 8192, 1024);
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks)
-        mma_ss_w(tmem + C::TM_DK, da + ((ks * 32) >> 4), db + ks * (2048 >> 4), id_kmn, (acc || ks) ? 1u : 0u);
+      for (int ks = 0; ks < 4; ++ks) {
+        if constexpr (kDkTs)   // A = dS^T from TMEM (the slot's S columns next to P^T)
+          mma_ts_w(tmem + C::TM_DK, tp + a_col(ks) + 16, db + ks * (2048 >> 4), id_kmn, (acc || ks) ? 1u : 0u);
+        else                   // A = dS^T from shared memory (K-major)
+          mma_ss_w(tmem + C::TM_DK, da + ((ks * 32) >> 4), db + ks * (2048 >> 4), id_kmn, (acc || ks) ? 1u : 0u);
+      }
     };
     auto mma_dq = [&](uint32_t sk, uint32_t sds, uint32_t tm) {    // dQ^T = K^T dS over the 128 keys
       const uint64_t da = desc_sw128(sk, 16384, 1024), db = desc_sw128(sds, 8192, 1024);
@@ -703,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       else mma_commit_w(&do_empty[st]);
       mma_dq(base + C::OFF_K, sds, tmem + slot_dp(x));
       mma_commit_w(&dq_full[x]);
-      mma_dk(sds, base + C::OFF_Q + st * C::QT, n > 0);
+      mma_dk(sds, tmem + slot_s(x), base + C::OFF_Q + st * C::QT, n > 0);
       if (PAIR) mma_commit_mc_w(&q_empty[st], 0x3);
       else mma_commit_w(&q_empty[st]);
       if (n + 2 < N) {
@@ -813,8 +829,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           rp[j] = pack_bf16(d0, d1);
           rs[j] = pack_bf16(p0, p1);
         }
-        // P^T (bf16 pairs) into the S^T columns already read: queries [col0, col0+32) -> cols 16 c
-        tmem_st16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(rs));
+        // P^T (bf16 pairs) into the S^T columns already read: queries [col0, col0+32) -> cols 16 c, or (kDkTs)
+        // cols 32 c with dS^T (the dK MMA's A operand) next to it in cols 32 c + 16
+        if constexpr (kDkTs) {
+          tmem_st16(tS + c * 32, *reinterpret_cast<uint32_t(*)[16]>(rs));
+          tmem_st16(tS + c * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(rp));
+          if (c == 0) tmem_wait_st();   // the stores' source registers stay reserved until the wait (else: spills)
+        } else {
+          tmem_st16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(rs));
+        }
 #pragma unroll
         for (int v8 = 0; v8 < 4; ++v8)
           st_shared_v4(dsbase + sw128_offset(r, col0 + v8 * 8), rp[4 * v8], rp[4 * v8 + 1], rp[4 * v8 + 2], rp[4 * v8 + 3]);

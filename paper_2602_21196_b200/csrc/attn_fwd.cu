@@ -489,11 +489,15 @@ cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err
     count_launches(1);
     return le;
   };
-  static const bool pair_env = [] {
+  // UPIPE_FWD_PAIR=1 / 0 forces the CTA-pair launch on / off. Default: pairs when the KV stream is shared by
+  // >= 4 query heads of the launch (A/B at 128K on one box, profiles/r02_ab_fwd_pair.txt: nq/nkv 8/2 1235 -> 1248
+  // TFLOP/s, attn fwd 117.1 -> 116.4 ms per bench step; nq/nkv 1/1 1328 -> 1113 TFLOP/s, so not there)
+  static const int pair_env = [] {
     const char* v = getenv("UPIPE_FWD_PAIR");
-    return v && v[0] == '1';
+    return v ? (v[0] == '1' ? 1 : 0) : -1;
   }();
-  if (p.d == 128 && !a.dbg && pair_env) e = go_pair(attn_fwd_kernel<128, false, true>, FwdCfg<128>::SMEM);
+  const bool use_pair = pair_env < 0 ? p.nq >= 4 : pair_env == 1;
+  if (p.d == 128 && !a.dbg && use_pair) e = go_pair(attn_fwd_kernel<128, false, true>, FwdCfg<128>::SMEM);
   else if (p.d == 128) e = a.dbg ? go(attn_fwd_kernel<128, true>, FwdCfg<128>::SMEM) : go(attn_fwd_kernel<128, false>, FwdCfg<128>::SMEM);
   else e = go(attn_fwd_kernel<64, false>, FwdCfg<64>::SMEM);
   if (e != cudaSuccess) return e;

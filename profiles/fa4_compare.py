@@ -1,0 +1,65 @@
+"""Library comparison (context only, not part of the product path): FlashAttention-4 (the CuTe-DSL sm_100 kernels
+vendored in vllm's `vllm_flash_attn.cute`) forward and backward at the attention shapes of the bench, timed with
+CUDA events like `profiles/attn_shapes.py` times ours. FLOP convention as in DESIGN §7: causal fwd 4·d·S(S+1)/2
+per head, bwd 10·d·S(S+1)/2 per head. The FA4 backward time includes its preprocess (row-dot) and postprocess
+(dQ conversion) kernels; ours (attn_shapes.py) is the main kernel alone (the row-dot is fused in our dO GEMM, the
+conversion is a separate ~0.2 ms launch).
+
+usage: python profiles/fa4_compare.py [--two-cta both|on|off] S:nq:nkv ...
+"""
+import argparse
+import json
+import sys
+
+import torch
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("shapes", nargs="*", default=["131072:8:2"])
+    ap.add_argument("--two-cta", default="both")
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    from vllm.vllm_flash_attn.cute import interface as fa, utils as fau
+
+    modes = {"both": [False, True], "on": [True], "off": [False]}[args.two_cta]
+    for shp in args.shapes:
+        S, nq, nkv = (int(v) for v in shp.split(":"))
+        d = 128
+        g = torch.Generator(device="cuda").manual_seed(0)
+        q = torch.randn(1, S, nq, d, device="cuda", dtype=torch.bfloat16, generator=g)
+        k = torch.randn(1, S, nkv, d, device="cuda", dtype=torch.bfloat16, generator=g)
+        v = torch.randn(1, S, nkv, d, device="cuda", dtype=torch.bfloat16, generator=g)
+        do = torch.randn(1, S, nq, d, device="cuda", dtype=torch.bfloat16, generator=g)
+        fl = d * S * (S + 1) / 2 * nq
+        for two in modes:
+            fau._fa_disable_2cta_cuda12 = not two
+            fau._fa_disable_2cta_enabled = not two
+            try:
+                qq, kk, vv = (t.detach().clone().requires_grad_(True) for t in (q, k, v))
+                out = fa.flash_attn_func(qq, kk, vv, causal=True)
+                out.backward(do)                      # compile both directions
+                torch.cuda.synchronize()
+                fwd, bwd = [], []
+                for _ in range(args.reps):
+                    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                    qq.grad = kk.grad = vv.grad = None
+                    e0.record()
+                    out = fa.flash_attn_func(qq, kk, vv, causal=True)
+                    e1.record()
+                    out.backward(do)
+                    e2.record()
+                    torch.cuda.synchronize()
+                    fwd.append(e0.elapsed_time(e1))
+                    bwd.append(e1.elapsed_time(e2))
+                f, b = min(fwd), min(bwd)
+                print(json.dumps({"impl": "fa4", "two_cta": two, "S": S, "nq": nq, "nkv": nkv, "d": d,
+                                  "fwd_ms": f, "fwd_tflops": 4 * fl / f / 1e9, "bwd_ms": b,
+                                  "bwd_tflops": 10 * fl / b / 1e9}), flush=True)
+            except Exception as ex:  # noqa: BLE001 - a library failure is reported, not fatal
+                print(json.dumps({"impl": "fa4", "two_cta": two, "S": S, "error": repr(ex)[:400]}), flush=True)
+            torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    sys.exit(main())
