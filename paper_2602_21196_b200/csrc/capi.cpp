@@ -375,7 +375,7 @@ upipe_status_t upipe_attn_core_bwd(const upipe_bf16* q, const upipe_bf16* k, con
   if (flags & UPIPE_CORE_DQ_DIM_MAJOR) {
     p.dq_dim_major = 1;
     p.ld_dqt = (S + 3) & ~int64_t(3);   // TMA: 16-byte row stride
-    if (!attn_bwd_dq_dim_major(p))
+    if (!attn_bwd_dq_dim_major_supported(p))
       return set_err(nullptr, UPIPE_ERR_UNSUPPORTED, "attn_core_bwd: dim-major dQ needs the 64-query kernel (d = 128)");
   }
   if (flags & UPIPE_CORE_DETERMINISTIC) {

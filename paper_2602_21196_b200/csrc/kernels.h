@@ -156,6 +156,8 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
 // Whether attn_bwd_run can accumulate dQ dim-major for this problem (the 64-query kernel, whose dQ^T
 // tile has one head dimension per TMEM lane, then stages 16-byte vectors instead of transposing).
 bool attn_bwd_dq_dim_major(const AttnBwdProblem& p);
+// Whether a dim-major dq_acc can be requested at all (the 64-query kernel serves it)
+bool attn_bwd_dq_dim_major_supported(const AttnBwdProblem& p);
 
 // ---------------------------------------------------------------- HBM-bound helpers
 // delta[t][j] = sum_e dO[t][j*d+e] * O[t][j*d+e] over bf16 inputs, fp32 result.

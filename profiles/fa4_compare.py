@@ -38,6 +38,7 @@ def main():
             try:
                 qq, kk, vv = (t.detach().clone().requires_grad_(True) for t in (q, k, v))
                 out = fa.flash_attn_func(qq, kk, vv, causal=True)
+                out = out[0] if isinstance(out, tuple) else out
                 out.backward(do)                      # compile both directions
                 torch.cuda.synchronize()
                 fwd, bwd = [], []
@@ -46,6 +47,7 @@ def main():
                     qq.grad = kk.grad = vv.grad = None
                     e0.record()
                     out = fa.flash_attn_func(qq, kk, vv, causal=True)
+                    out = out[0] if isinstance(out, tuple) else out
                     e1.record()
                     out.backward(do)
                     e2.record()
