@@ -983,517 +983,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (PAIR) cluster_sync();                // no CTA leaves while its peer may still multicast into it or signal it
 }
 
-// ---------------------------------------------------------------------------------------------
-// CTA2 variant (d = 128, UPIPE_BWD_CTA2): the five MMAs of a 128-query tile run as cta_group::2 MMAs over a
-// CTA pair (a cluster of two CTAs on adjacent key tiles 2i, 2i+1 of one KV head; the leader, rank 0, issues):
-//   S^T  = K Q^T    M = 256 pair keys (128 per CTA), N = 128 q, K = d   (A: own K; B: each CTA its 64-q half of Q)
-//   dP^T = V dO^T   likewise with V and dO
-//   dV  += P^T dO   M = 256 keys, N = 128 d, K = 128 q                  (A: P^T in TMEM; B: each CTA its d-half of dO)
-//   dK  += dS^T Q   likewise, A = dS^T in TMEM, B = each CTA's d-half of Q
-//   dQ   = dS K     M = 128 q (64 per CTA), N = 128 d, K = 256 pair keys (A: dS^T over both CTAs' keys for this
-//                   CTA's 64-q half, half of it written by the peer's softmax warps over DSMEM; B: each CTA's d-half
-//                   of both CTAs' K)
-// so no N = 64 MMA is left (the 64-query kernel's tensor floor, 1664 cycles per 64 queries instead of 1280) and
-// the dQ partial that leaves the SM covers 256 keys: half the staging and L2 reduce traffic per query.
-// TMEM per CTA (512 columns): S^T | dP^T | dV | dK, 128 each. Each softmax warpgroup w reads its 64 query columns
-// [64w, 64w+64) of S^T and dP^T and writes P^T / dS^T (bf16 pairs) into the first 32 of them; dQ (64 columns: lane
-// l < 64 holds query 64 c + l, dims 0-63; lane 64 + l the same query, dims 64-127 — the M = 128 pair layout measured
-// by profiles/micro_pair.cu) lands in S^T columns [64, 128) once dV has read P^T, and is drained before the next S^T.
-// Per tile: S(n) -> softmax E1 (P, kept in fp32 registers) -> dV(n) | E2 (dS once dP(n) is there) -> dK(n), dQ(n),
-// dP(n+1) -> [dQ(n) drained] S(n+1). Q / dO are single-buffered per role (four TMA streams, each refilled as soon
-// as its MMA has read it). dq_acc is row-major [S][nq d] (fp32 TMA reduce-add of 32 x 32 boxes).
-struct C2Cfg {
-  static constexpr int D = 128;
-  static constexpr int OFF_K = 0;                   // own K, K-major [128 keys][128 d] (two 16 KB chunks)
-  static constexpr int OFF_V = 32768;               // own V, same
-  static constexpr int OFF_KT = 65536;              // [256 pair keys][64 d of half c], MN-major (two 16 KB halves)
-  static constexpr int OFF_Q = 98304;               // Q, this CTA's 64 queries x 128 d, K-major (two 8 KB chunks)
-  static constexpr int OFF_QT = 114688;             // Q, 128 queries x this CTA's 64 dims, MN-major (16 KB)
-  static constexpr int OFF_DO = 131072;             // dO like OFF_Q
-  static constexpr int OFF_DOT = 147456;            // dO like OFF_QT
-  static constexpr int OFF_DS = 163840;             // dS^T [256 pair keys][64 q of half c], MN-major (32 KB)
-  static constexpr int OFF_STG = 196608;            // dQ staging: 4 drain warps x two 32 x 32 fp32 boxes
-  static constexpr int OFF_STAT = 229376;           // [parity][wg][lse2, delta][64] fp32
-  static constexpr int OFF_BAR = OFF_STAT + 2048;
-  static constexpr int SMEM = OFF_BAR + 256;
-  static_assert(SMEM <= 232448, "shared memory");
-  static constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 64, TM_DV = 256, TM_DK = 384;
-};
-
-// Single-thread forms (the caller elects one lane once): measured on B200 (profiles/micro_pair.cu) a pair MMA
-// issued with elect.sync inside every asm statement costs ~166 cycles, with the lane elected once ~106.
-__device__ __forceinline__ void mma_ss_pair_1(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                              uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void mma_ts_pair_1(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                              uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit_pair_1(uint64_t* bar, uint16_t mask) {
-  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                   smem_u32(bar)), "h"(mask)
-               : "memory");
-}
-__device__ __forceinline__ void mma_ts_pair_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                              uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// 3-D TMA load into this CTA's shared memory, complete_tx on the mbarrier at a shared::cluster address (the pair
-// leader's barrier)
-__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int c0, int c1,
-                                                 int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster_acq(uint64_t* bar, uint32_t parity) {   // acquire at cluster scope
-  uint32_t addr = smem_u32(bar);
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(addr),
-      "r"(parity)
-      : "memory");
-}
-
-__global__ void __launch_bounds__(kThreads, 1)
-    attn_bwd_cta2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                         const __grid_constant__ CUtensorMap tmdQ, const BwdArgs a) {
-  using C = C2Cfg;
-  constexpr int D = C::D;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  if (smem_u32(smem) & 1023) __trap();
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  // leader-side (rank 0's copy is the one used): kv_full, q_full, qt_full, do_full, dot_full, p_full, ds_full,
-  // dq_empty; per CTA: q_empty, qt_empty, do_empty, dot_empty, s_full, dp_full, dq_full, dkv_full
-  uint64_t* kv_full = bars + 0;
-  uint64_t* q_full = bars + 1;
-  uint64_t* qt_full = bars + 2;
-  uint64_t* do_full = bars + 3;
-  uint64_t* dot_full = bars + 4;
-  uint64_t* p_full = bars + 5;      // 16 arrivals (one per softmax warp of either CTA, after __syncwarp)
-  uint64_t* ds_full = bars + 6;     // 16
-  uint64_t* dq_empty = bars + 7;    // 8 (one per drain warp)
-  uint64_t* q_empty = bars + 8;
-  uint64_t* qt_empty = bars + 9;
-  uint64_t* do_empty = bars + 10;
-  uint64_t* dot_empty = bars + 11;
-  uint64_t* s_full = bars + 12;
-  uint64_t* dp_full = bars + 13;
-  uint64_t* dq_full = bars + 14;
-  uint64_t* dkv_full = bars + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
-  float* stats = reinterpret_cast<float*>(smem + C::OFF_STAT);
-
-  const int warp = warp_id(), lane = lane_id();
-  const int jb = blockIdx.x;                       // key tile; the pair is (jb & ~1, jb | 1)
-  const int g = blockIdx.y;
-  const uint32_t crank = cluster_ctarank();
-  const int G = a.nq / a.nkv;
-  const int nT = (int)((a.S + 127) / 128);
-  const int qt_begin = a.causal ? (jb & ~1) : 0;   // the pair's common range (the odd tile's first tile is masked)
-  const int n_qt = nT - qt_begin;
-  const int N = G * n_qt;
-  auto tile_h = [&](int n) { return g * G + n / n_qt; };
-  auto tile_qt = [&](int n) { return nT - 1 - n % n_qt; };   // last to first (dq_acc rows shared in L2)
-  constexpr int kWg = 128;
-
-  if (warp == kTmaWarp && lane == 0) {
-    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
-    for (int i = 0; i < 16; ++i)
-      mbar_init(&bars[i], (i == 5 || i == 6) ? 2 * kSoftmaxWarps : i == 7 ? 2 * 4 : 1);
-    fence_barrier_init();
-    tmem_slot[1] = smem_u32(smem);
-  }
-  if (warp == kMmaWarp) tmem_alloc_pair<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();                                    // both CTAs' barriers exist before any remote signal
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  auto leader_bar = [&](uint64_t* b) { return mapa_shared(b, 0); };
-
-  if (warp >= kTmaWarp) regs_dec<kRegsOther>();
-  if (warp == kTmaWarp) {
-    if (lane == 0) {
-      // ------------------------------------------------ TMA producer (both CTAs; loads complete on the leader)
-      if (crank == 0) mbar_arrive_expect_tx(kv_full, 2 * 3 * 32768);
-      const uint32_t kvb = leader_bar(kv_full);
-      const int jb0 = jb & ~1;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        tma_load_3d_pair(smem + C::OFF_K + c * 16384, &tmK, kvb, c * 64, g, jb * 128);
-        tma_load_3d_pair(smem + C::OFF_V + c * 16384, &tmV, kvb, c * 64, g, jb * 128);
-        tma_load_3d_pair(smem + C::OFF_KT + c * 16384, &tmK, kvb, (int)crank * 64, g, (jb0 + c) * 128);
-      }
-      const uint32_t qb = leader_bar(q_full), qtb = leader_bar(qt_full), dob = leader_bar(do_full),
-                     dotb = leader_bar(dot_full);
-      for (int n = 0; n < N; ++n) {
-        const int h = tile_h(n);
-        const int q0 = tile_qt(n) * 128;
-        const uint32_t ph = (n & 1) ^ 1;
-        // in MMA order: Q (S^T), dO (dP^T), dO^T (dV), Q^T (dK)
-        mbar_wait(q_empty, ph);
-        if (crank == 0) mbar_arrive_expect_tx(q_full, 2 * 16384);
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d_pair(smem + C::OFF_Q + c * 8192, &tmQ, qb, c * 64, h, q0 + (int)crank * 64);
-        mbar_wait(do_empty, ph);
-        if (crank == 0) mbar_arrive_expect_tx(do_full, 2 * 16384);
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d_pair(smem + C::OFF_DO + c * 8192, &tmdO, dob, c * 64, h, q0 + (int)crank * 64);
-        mbar_wait(dot_empty, ph);
-        if (crank == 0) mbar_arrive_expect_tx(dot_full, 2 * 16384);
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d_pair(smem + C::OFF_DOT + c * 8192, &tmdO, dotb, (int)crank * 64, h, q0 + c * 64);
-        mbar_wait(qt_empty, ph);
-        if (crank == 0) mbar_arrive_expect_tx(qt_full, 2 * 16384);
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d_pair(smem + C::OFF_QT + c * 8192, &tmQ, qtb, (int)crank * 64, h, q0 + c * 64);
-      }
-    }
-  } else if (warp == kMmaWarp) {
-    if (crank == 0) {
-      // ------------------------------------------------ MMA issuer (leader only; whole warp, elect inside the asm)
-      constexpr uint32_t id_sp = idesc_bf16(256, 128, false, false);   // S^T, dP^T: K-major A (K / V), B (Q / dO)
-      constexpr uint32_t id_kv = idesc_bf16(256, 128, false, true);    // dV, dK: A in TMEM, B MN-major (q rows)
-      constexpr uint32_t id_dq = idesc_bf16(128, 128, true, true);     // dQ: A = dS^T MN-major, B = K MN-major
-      uint32_t base;
-      auto load_base = [&]() { base = ld_volatile_shared_u32(tmem_slot + 1); };
-      load_base();
-      const bool issuer = elect_one();                   // one lane issues every MMA and commit
-      auto commit = [&](uint64_t* b) { if (issuer) mma_commit_pair_1(b, 0x3); __syncwarp(); };
-      auto mma_sp = [&](uint32_t skv, uint32_t sqt, uint32_t tm) {     // [256 keys x d] x [128 q x d]^T
-        const uint64_t da = desc_sw128(skv, 16, 1024), db = desc_sw128(sqt, 16, 1024);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (issuer)
-            mma_ss_pair_1(tm, da + (((i >> 2) * 16384 + (i & 3) * 32) >> 4), db + (((i >> 2) * 8192 + (i & 3) * 32) >> 4),
-                          id_sp, i != 0);
-      };
-      // A chunk of 16 queries (8 TMEM columns) ks of P^T / dS^T: warpgroup ks / 4 wrote its 32 columns at 64 (ks / 4)
-      auto a_col = [](int ks) -> uint32_t { return (ks >> 2) * 64 + (ks & 3) * 8; };
-      auto mma_kv = [&](uint32_t dst, uint32_t ta, uint32_t sb, bool acc) {   // [256 keys x 128 q] x [128 q x d]
-        const uint64_t db = desc_sw128(sb, 8192, 1024);
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-          if (issuer)
-            mma_ts_pair_1(dst, ta + a_col(ks), db + (((ks >> 2) * 8192 + (ks & 3) * 2048) >> 4), id_kv,
-                          (acc || ks) ? 1u : 0u);
-      };
-      auto mma_dq = [&]() {                                             // [128 q x 256 keys] x [256 keys x d]
-        const uint64_t da = desc_sw128(base + C::OFF_DS, 8192, 1024), db = desc_sw128(base + C::OFF_KT, 8192, 1024);
-#pragma unroll
-        for (int ks = 0; ks < 16; ++ks)
-          if (issuer) mma_ss_pair_1(tmem + C::TM_DQ, da + ((ks * 2048) >> 4), db + ((ks * 2048) >> 4), id_dq, ks != 0);
-      };
-      mbar_wait(kv_full, 0);
-      if (N > 0) {
-        mbar_wait(q_full, 0);
-        tc_fence_after();
-        mma_sp(base + C::OFF_K, base + C::OFF_Q, tmem + C::TM_S);
-        commit(s_full);
-        commit(q_empty);
-        mbar_wait(do_full, 0);
-        tc_fence_after();
-        mma_sp(base + C::OFF_V, base + C::OFF_DO, tmem + C::TM_DP);
-        commit(dp_full);
-        commit(do_empty);
-      }
-      const bool tl = a.dbg && blockIdx.x == 0 && blockIdx.y == 0;
-      long long tw[8] = {0, 0, 0, 0, 0, 0, 0, 0};       // waits: P, dO^T, dS, Q^T, dO, dQ drained, Q; total
-      const long long tb = clock64();
-      long long t0 = 0;
-      auto tick_on = [&]() { if (tl) t0 = clock64(); };
-      auto tock = [&](int i) { if (tl) tw[i] += clock64() - t0; };
-      for (int n = 0; n < N; ++n) {
-        const uint32_t ph = n & 1;
-        load_base();
-        tick_on();
-        mbar_wait_cluster_acq(p_full, ph);               // P^T of both CTAs in TMEM
-        tock(0);
-        tick_on();
-        mbar_wait(dot_full, ph);
-        tock(1);
-        tc_fence_after();
-        mma_kv(tmem + C::TM_DV, tmem + C::TM_S, base + C::OFF_DOT, n > 0);
-        commit(dot_empty);
-        tick_on();
-        mbar_wait_cluster_acq(ds_full, ph);              // dS^T of both CTAs in TMEM and in both dS buffers
-        tock(2);
-        tick_on();
-        mbar_wait(qt_full, ph);
-        tock(3);
-        tc_fence_after();
-        mma_kv(tmem + C::TM_DK, tmem + C::TM_DP, base + C::OFF_QT, n > 0);
-        commit(qt_empty);
-        mma_dq();                                         // into S^T columns [64, 128) (dV has read P^T)
-        commit(dq_full);
-        if (n + 1 < N) {
-          tick_on();
-          mbar_wait(do_full, ph ^ 1);
-          tock(4);
-          tc_fence_after();
-          mma_sp(base + C::OFF_V, base + C::OFF_DO, tmem + C::TM_DP);   // dK has read dS^T
-          commit(dp_full);
-          commit(do_empty);
-          tick_on();
-          mbar_wait_cluster_acq(dq_empty, ph);           // dQ(n) drained in both CTAs
-          tock(5);
-          tick_on();
-          mbar_wait(q_full, ph ^ 1);
-          tock(6);
-          tc_fence_after();
-          mma_sp(base + C::OFF_K, base + C::OFF_Q, tmem + C::TM_S);
-          commit(s_full);
-          commit(q_empty);
-        }
-      }
-      commit(dkv_full);
-      if (tl && lane == 0) {
-        tw[7] = clock64() - tb;
-        for (int i = 0; i < 8; ++i) a.dbg[i] = tw[i];
-        a.dbg[15] = N;
-      }
-    }
-  } else if (warp < kSoftmaxWarps) {
-    // ------------------------------------------------ softmax-gradient warpgroups: WG w owns queries [64w, 64w+64)
-    regs_inc<kRegsSoftmax>();
-    const int w = warp >> 2;
-    const int quad = warp & 3;
-    const int r = quad * 32 + lane;                    // key row of this CTA's tile
-    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const long long key = (long long)jb * 128 + r;
-    const float sl2 = a.scale_log2;
-    const uint32_t tS = tmem + C::TM_S + 64 * w + lane_off;
-    const uint32_t tP = tmem + C::TM_DP + 64 * w + lane_off;
-    // dS^T row (pair key crank * 128 + r) of query half w lives in CTA w's dS buffer
-    const uint32_t ds_row = smem_u32(smem + C::OFF_DS) + (crank * 128 + r) * 128;
-    const uint32_t ds_row_dst = (uint32_t)w == crank ? ds_row : mapa_shared(smem + C::OFF_DS + (crank * 128 + r) * 128, w);
-    const uint32_t pfb = leader_bar(p_full), dsfb = leader_bar(ds_full);
-    auto load_stat = [&](int n) -> float {             // threads 0-63: -lse*log2e of query 64w + r, 64-127: delta
-      const int h = tile_h(n);
-      const long long q = (long long)tile_qt(n) * 128 + 64 * w + (r & 63);
-      if (q >= a.S) return 0.f;
-      return r < 64 ? a.lse[(long long)h * a.ld_lse + q] * -1.4426950408889634f : a.delta[q * a.ld_delta + h];
-    };
-    float stat_next = N > 0 ? load_stat(0) : 0.f;
-    for (int n = 0; n < N; ++n) {
-      const int qt = tile_qt(n);
-      const long long q0 = (long long)qt * 128 + 64 * w;   // this warpgroup's first query
-      const int par = n & 1;
-      float* s_lse2 = stats + ((par * 2 + w) * 2 + 0) * 64;
-      float* s_delta = stats + ((par * 2 + w) * 2 + 1) * 64;
-      (r < 64 ? s_lse2 : s_delta)[r & 63] = stat_next;
-      if (n + 1 < N) stat_next = load_stat(n + 1);
-      const long long e0 = clock64();
-      if (quad == 0) mbar_wait(s_full, par);
-      named_bar_sync(1 + w, kWg);
-      const long long e1 = clock64();
-      tc_fence_after();
-      const bool need_mask = (a.causal && q0 < key - r + 128) || q0 + 64 > a.S || (long long)jb * 128 + 128 > a.S;
-      const long long qmin = key >= a.S ? a.S : (a.causal ? key : 0);
-      // ---- E1: P = exp2(S log2e / sqrt(d) - lse log2e), kept in fp32 pairs; P^T (bf16) into S^T columns
-      uint64_t pp[32];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t rs[32];
-        tmem_ld32(tS + c * 32, rs);
-        const float2* l2 = reinterpret_cast<const float2*>(s_lse2 + c * 32);
-        tmem_wait_ld();
-        const uint64_t sl2x2 = f2_pack(sl2, sl2);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 xx = l2[j];
-          const uint64_t nl = f2_pack(xx.x, xx.y);
-          const uint64_t t = f2_fma(f2_pack(__uint_as_float(rs[2 * j]), __uint_as_float(rs[2 * j + 1])), sl2x2, nl);
-          float t0, t1;
-          f2_unpack(t, t0, t1);
-          float p0 = ex2b(t0), p1 = ex2b(t1);
-          if (need_mask) {
-            const long long qa = q0 + c * 32 + 2 * j;
-            p0 = (qa >= qmin && qa < a.S) ? p0 : 0.f;
-            p1 = (qa + 1 >= qmin && qa + 1 < a.S) ? p1 : 0.f;
-          }
-          pp[16 * c + j] = f2_pack(p0, p1);
-          rs[j] = pack_bf16(p0, p1);
-        }
-        tmem_st16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(rs));
-      }
-      const long long x1 = clock64();
-      tmem_wait_st();
-      tc_fence_before();
-      const long long x2 = clock64();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(pfb);
-      const long long x3 = clock64();
-      if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && warp == 0 && lane == 0) {
-        a.dbg[12] += x1 - e1;   // E1 loads + math + st issue
-        a.dbg[13] += x2 - x1;   // wait st
-        a.dbg[14] += x3 - x2;   // arrive
-      }
-      // ---- E2: dS = P (dP - delta); dS^T (bf16) into dP^T columns (dK's A) and into CTA w's dS buffer (dQ's A)
-      const long long e2 = clock64();
-      if (quad == 0) mbar_wait(dp_full, par);
-      named_bar_sync(1 + w, kWg);
-      const long long e3 = clock64();
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t rp[32];
-        tmem_ld32(tP + c * 32, rp);
-        const float2* d2 = reinterpret_cast<const float2*>(s_delta + c * 32);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 y = d2[j];
-          const uint64_t dlt = f2_pack(y.x, y.y);
-          const uint64_t ds = f2_mul(pp[16 * c + j], f2_sub(f2_pack(__uint_as_float(rp[2 * j]), __uint_as_float(rp[2 * j + 1])), dlt));
-          float d0, d1;
-          f2_unpack(ds, d0, d1);
-          rp[j] = pack_bf16(d0, d1);
-        }
-        tmem_st16(tP + c * 16, *reinterpret_cast<uint32_t(*)[16]>(rp));
-        // row of 64 queries = 8 16-byte chunks (128B swizzle); this chunk c holds queries [32c, 32c+32)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const uint32_t off = (uint32_t)(((4 * c + v) ^ (r & 7)) << 4);
-          if ((uint32_t)w == crank) st_shared_v4(ds_row + off, rp[4 * v], rp[4 * v + 1], rp[4 * v + 2], rp[4 * v + 3]);
-          else st_cluster_v4(ds_row_dst + off, rp[4 * v], rp[4 * v + 1], rp[4 * v + 2], rp[4 * v + 3]);
-        }
-      }
-      tmem_wait_st();
-      asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");   // dS rows (local and peer) -> async proxy
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(dsfb);
-      if (a.dbg && blockIdx.x == 0 && blockIdx.y == 0 && warp == 0 && lane == 0) {
-        const long long e4 = clock64();
-        a.dbg[8] += e1 - e0;    // wait S
-        a.dbg[9] += e2 - e1;    // E1
-        a.dbg[10] += e3 - e2;   // wait dP
-        a.dbg[11] += e4 - e3;   // E2
-      }
-    }
-    // ---- dK / dV epilogue (TMEM lane = key row of this CTA): warpgroup 0 writes dV, warpgroup 1 dK
-    mbar_wait(dkv_full, 0);
-    tc_fence_after();
-    const long long ldacc = (long long)a.nkv * D;
-    const int which = w;
-    const uint32_t tcol = which ? C::TM_DK : C::TM_DV;
-    const float sc = which ? a.scale : 1.f;
-    float* acc = (which ? a.dk_acc : a.dv_acc);
-    const bool ob = which ? (a.nkseg || a.dk_bf16) : (a.nvseg || a.dv_bf16);
-#pragma unroll 1
-    for (int c = 0; c < D; c += 32) {
-      uint32_t rr[32];
-      tmem_ld32(tmem + tcol + lane_off + c, rr);
-      tmem_wait_ld();
-      if (key >= a.S || N == 0) continue;
-      float v[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]) * sc;
-      float4* accp = acc ? reinterpret_cast<float4*>(acc + key * ldacc + (long long)g * D + c) : nullptr;
-      if (a.kv_accumulate && accp) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float4 o = accp[i];
-          v[4 * i] += o.x; v[4 * i + 1] += o.y; v[4 * i + 2] += o.z; v[4 * i + 3] += o.w;
-        }
-      }
-      if (a.kv_write_acc && accp) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) accp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-      }
-      if (ob) {
-        if (which && a.rope.hi) rope_rotate<16>(v, a.rope.hi, a.rope.lo, D, a.rope.pos0 + key, c, -1.f);
-        uint4* dst = reinterpret_cast<uint4*>(kv_out_row(a, which, key) + (long long)g * D + c);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_uint4(pack_bf16(v[8 * i + 0], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                              pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
-      }
-    }
-  } else if (warp < kSoftmaxWarps + 4) {
-    // ------------------------------------------------ dQ drain (warps 8-11): lane quarter quad of the dQ columns:
-    // query 64 crank + 32 (quad & 1) + lane, dims 64 (quad >> 1) + [0, 64)
-    regs_inc<kRegsDrain>();
-    const int quad = warp & 3;
-    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    uint8_t* const box = smem + C::OFF_STG + quad * 8192;
-    const uint32_t bbase = smem_u32(box);
-    const uint32_t dqeb = leader_bar(dq_empty);
-    for (int n = 0; n < N; ++n) {
-      const int h = tile_h(n);
-      const int qrow = tile_qt(n) * 128 + (int)crank * 64 + 32 * (quad & 1);
-      if (lane == 0) mbar_wait(dq_full, n & 1);
-      __syncwarp();
-      tc_fence_after();
-      uint32_t rq[2][32];
-      tmem_ld32(tmem + C::TM_DQ + lane_off, rq[0]);
-      tmem_ld32(tmem + C::TM_DQ + lane_off + 32, rq[1]);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_cluster(dqeb);
-        bulk_wait_read0();                            // this warp's previous boxes have been read by their reduce
-      }
-      __syncwarp();
-#pragma unroll
-      for (int bx = 0; bx < 2; ++bx)
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          st_shared_v4(bbase + bx * 4096 + lane * 128 + ((j ^ (lane & 7)) << 4),
-                       __float_as_uint(__uint_as_float(rq[bx][4 * j + 0]) * a.scale),
-                       __float_as_uint(__uint_as_float(rq[bx][4 * j + 1]) * a.scale),
-                       __float_as_uint(__uint_as_float(rq[bx][4 * j + 2]) * a.scale),
-                       __float_as_uint(__uint_as_float(rq[bx][4 * j + 3]) * a.scale));
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        const int col = h * D + 64 * (quad >> 1);
-        tma_reduce_add_2d(&tmdQ, box, col, qrow);
-        tma_reduce_add_2d(&tmdQ, box + 4096, col + 32, qrow);
-        bulk_commit();
-      }
-    }
-    if (lane == 0) bulk_wait0();
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();                                    // the peer may still signal our barriers or write our dS rows
-  if (warp == kMmaWarp) {
-    tc_fence_after();
-    tmem_dealloc_pair<512>(tmem);
-  }
-}
-
-
 // d = 128: the 64-query ping-pong kernel. Under the 1000 W power cap it runs at lower SM clocks than
 // the 128-query kernel (busier tensor pipe), yet with the dim-major dQ accumulator and last-to-first
 // query order it is ahead at every length measured: attn bwd per step 375 -> 340 ms at 128K, 5940 ->
@@ -1502,21 +991,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 // The CTA-pair variant of the 64-query kernel (Q / dO multicast within the pair), default: half the L2 -> SM
 // operand traffic lowers the energy per tile, so the power-capped clock rises (A/B at 128K on one box: attn
 // bwd 350.3 -> 342.7 ms per step at 1477-1485 -> 1507 MHz). UPIPE_BWD_PAIR=0 selects the single-CTA launch.
+// A cta_group::2 variant (128-query tiles over CTA pairs, pair MMAs for all five products, dQ over both CTAs' keys
+// with dS exchanged over DSMEM) passed kernel parity but ran at half this kernel's rate (530-570 TFLOP/s at 32K-128K,
+// profiles/r02_ab_bwd_cta2.txt): in our probes pair MMAs issued back to back took ~106-166 cycles per K16 instruction
+// (profiles/r02_micro_pair.txt) and its softmax could not overlap the MMAs. Source: commit 4d629cc; retired.
 bool bwd_pair() {
   static const bool on = [] {
     const char* v = getenv("UPIPE_BWD_PAIR");
     return !(v && v[0] == '0');
   }();
   return on;
-}
-
-// UPIPE_BWD_CTA2=1: the cta_group::2 kernel (attn_bwd_cta2_kernel) for d = 128 with a row-major dq_acc
-bool use_cta2(const AttnBwdProblem& p) {
-  static const int env = [] {
-    const char* v = getenv("UPIPE_BWD_CTA2");
-    return v ? (v[0] == '1' ? 1 : 0) : 0;
-  }();
-  return env == 1 && p.d == 128 && !p.dq_sem;
 }
 
 bool use_q64(const AttnBwdProblem& p) {
@@ -1535,7 +1019,7 @@ bool attn_bwd_dq_dim_major(const AttnBwdProblem& p) {
     const char* v = getenv("UPIPE_DQ_DIM_MAJOR");
     return v && v[0] == '0';
   }();
-  return !off && use_q64(p) && !use_cta2(p);
+  return !off && use_q64(p);
 }
 
 bool attn_bwd_dq_dim_major_supported(const AttnBwdProblem& p) { return use_q64(p); }
@@ -1602,43 +1086,6 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
   const int nT = (int)((p.S + 127) / 128);
   dim3 grid(nT, p.nkv);
   cudaError_t e;
-  if (!p.dq_dim_major && use_cta2(p)) {
-    CUtensorMap tq64, tdo64, tdq32;
-    if (!make_tmap_3d(&tq64, p.q, p.d, p.nq, p.S, p.d, p.ldq, 64, 1, 64, err, errlen)) return cudaErrorInvalidValue;
-    if (!make_tmap_3d(&tdo64, p.dout, p.d, p.nq, p.S, p.d, p.ldo_grad, 64, 1, 64, err, errlen))
-      return cudaErrorInvalidValue;
-    if (!make_tmap_2d_f32(&tdq32, p.dq_acc, (uint64_t)p.nq * p.d, p.S, (uint64_t)p.nq * p.d, 32, 32, err, errlen))
-      return cudaErrorInvalidValue;
-    const cudaError_t attr = set_smem_attr((const void*)attn_bwd_cta2_kernel, C2Cfg::SMEM);
-    if (attr != cudaSuccess) { snprintf(err, errlen, "attn_bwd_cta2 attr: %s", cudaGetErrorString(attr)); return attr; }
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    cfg.gridDim = dim3((unsigned)((nT + 1) & ~1), (unsigned)p.nkv);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = C2Cfg::SMEM;
-    cfg.stream = stream;
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, attn_bwd_cta2_kernel, tq64, tk, tv, tdo64, tdq32, a);
-    count_launches(1);
-    if (e == cudaSuccess) e = cudaGetLastError();
-    if (e != cudaSuccess) snprintf(err, errlen, "attn_bwd_cta2 launch: %s", cudaGetErrorString(e));
-    if (a.dbg) {
-      long long h[16];
-      cudaMemcpyAsync(h, a.dbg, sizeof h, cudaMemcpyDeviceToHost, stream);
-      cudaStreamSynchronize(stream);
-      fprintf(stderr,
-              "[attn_bwd_cta2 timeline CTA(0,0) N=%lld 128-query tiles, cycles] mma waits: P %lld dOt %lld dS %lld "
-              "Qt %lld dO %lld dQdrain %lld Q %lld total %lld | WG0 warp0: wait_S %lld E1 %lld wait_dP %lld E2 %lld "
-              "| E1 parts: ld+math %lld wait_st %lld arrive %lld\n",
-              h[15], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[10], h[11], h[12], h[13], h[14]);
-    }
-    return e;
-  }
   if (use_q64(p)) {
     if (p.dq_dim_major && p.ld_dqt < p.S) {
       snprintf(err, errlen, "attn_bwd: dim-major dq_acc needs ld_dqt >= S");

@@ -12,7 +12,6 @@ dim-major dQ accumulator):
 One JSON line per shape: fwd / bwd ms and TFLOP/s (4 d resp. 10 d flops per causal pair and head)."""
 import argparse
 import json
-import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -57,7 +56,7 @@ for spec in args.shapes:
     o = torch.empty((S, nq, d), dtype=torch.bfloat16, device=dev)
     lse = torch.empty((nq, S), dtype=torch.float32, device=dev)
     delta = torch.empty((S, nq), dtype=torch.float32, device=dev)
-    dm = d == 128 and os.environ.get("UPIPE_BWD_CTA2") != "1"   # the cta_group::2 kernel accumulates row-major
+    dm = d == 128
     dq = torch.zeros((nq * d, S) if dm else (S, nq, d), dtype=torch.float32, device=dev)
     dk = torch.empty((S, nkv, d), dtype=torch.float32, device=dev)
     dv = torch.empty((S, nkv, d), dtype=torch.float32, device=dev)
