@@ -27,7 +27,25 @@ __global__ void __launch_bounds__(384, 1) mma_rate(long long* out, int iters, in
   tc_fence_after();
   const uint32_t tm = slot;
   const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 65536);
-  if (warp == 0 && (mode == 8 || mode == 9)) {
+  if (warp == 0 && (mode == 10 || mode == 11)) {
+    // mode 10: TS N128 warp-issued, unrolled (A from TMEM columns 256+, D at column 0; the dV / dK form);
+    // mode 11: TS N128 with B MN-major (exactly the backward's dV: B = dO MN-major)
+    const uint32_t id = idesc_bf16(128, 128, false, mode == 11);
+    const uint64_t db = mode == 11 ? desc_sw128(sb, 8192, 1024) : desc_sw128(sb, 16, 1024);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t off = mode == 11 ? (k * 2048) >> 4 : ((k >> 2) * 16384 + (k & 3) * 32) >> 4;
+        mma_ts_w(tm, tm + 256 + k * 8, db + off, id, (it | k) != 0);
+      }
+    }
+    if (elect_one()) mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (lane_id() == 0) out[blockIdx.x] = t1 - t0;
+    if (lane_id() == 0) stop = 1;
+  } else if (warp == 0 && (mode == 8 || mode == 9)) {
     const uint32_t id = idesc_bf16(128, mode == 9 ? 64 : 128, false, false);
     const uint64_t da = desc_sw128(sa, 16, 1024), db = desc_sw128(sb, 16, 1024);
     long long t0 = clock64();
@@ -106,10 +124,10 @@ int main() {
   cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* names[] = {"SS N128 K-major", "SS N256 K-major", "TS N128", "SS N128 B MN-major",
                          "SS N128 2 accums", "TS N128 2 accums", "SS N64 2 accums", "SS N128 unrolled",
-                         "SS N128 warp-issued", "SS N64 warp-issued"};
+                         "SS N128 warp-issued", "SS N64 warp-issued", "TS N128 warp-issued", "TS N128 B-MN warp-issued"};
   const int iters = 4096;
   for (int sts : {0, 8}) {
-    for (int mode = 0; mode < 10; ++mode) {
+    for (int mode = 0; mode < 12; ++mode) {
       mma_rate<<<148, 384, smem>>>(d, iters, mode, sts);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
