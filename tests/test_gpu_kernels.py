@@ -61,8 +61,11 @@ def _run_fwd(U, c, S, Hq, Hkv, d, causal):
     return q, k, v, o, lse
 
 
+# (640, 4, 1) and (1300, 8, 2): odd query-tile-pair counts under the forward's default CTA-pair launch (nq >= 4,
+# one fully masked padding CTA), causal and not
 FWD_CASES = [(128, 1, 1, 64, 1), (200, 2, 1, 64, 1), (512, 4, 1, 128, 1), (1000, 8, 2, 128, 1),
-             (384, 2, 2, 64, 0), (333, 4, 2, 128, 0), (2048, 2, 1, 128, 1)]
+             (384, 2, 2, 64, 0), (333, 4, 2, 128, 0), (2048, 2, 1, 128, 1), (640, 4, 1, 128, 1),
+             (1300, 8, 2, 128, 0)]
 
 
 @pytest.mark.parametrize("score_std", [1.0, 4.0])
