@@ -12,6 +12,7 @@ dim-major dQ accumulator):
 One JSON line per shape: fwd / bwd ms and TFLOP/s (4 d resp. 10 d flops per causal pair and head)."""
 import argparse
 import json
+import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -1,14 +1,16 @@
 """Library comparison (context only, not part of the product path): FlashAttention-4 (the CuTe-DSL sm_100 kernels
-vendored in vllm's `vllm_flash_attn.cute`) forward and backward at the attention shapes of the bench, timed with
-CUDA events like `profiles/attn_shapes.py` times ours. FLOP convention as in DESIGN §7: causal fwd 4·d·S(S+1)/2
-per head, bwd 10·d·S(S+1)/2 per head. The FA4 backward time includes its preprocess (row-dot) and postprocess
-(dQ conversion) kernels; ours (attn_shapes.py) is the main kernel alone (the row-dot is fused in our dO GEMM, the
-conversion is a separate ~0.2 ms launch).
+vendored in vllm's `vllm_flash_attn.cute`) forward and backward at the attention shapes of the bench, and ours
+through the C ABI on the same inputs in the same process, both timed the same way (CUDA events, median of `reps`
+launches after a warm-up; `--ours` adds our lines). FLOP convention as in DESIGN §7: causal fwd 4·d·S(S+1)/2 per
+head, bwd 10·d·S(S+1)/2 per head. The FA4 backward time includes its preprocess (row-dot) and postprocess (dQ
+conversion) kernels; ours is the main kernel alone (the row-dot is fused in our dO GEMM, the conversion is a separate
+~0.2 ms launch).
 
-usage: python profiles/fa4_compare.py [--two-cta both|on|off] S:nq:nkv ...
+usage: python profiles/fa4_compare.py [--two-cta both|on|off] [--ours] S:nq:nkv ...
 """
 import argparse
 import json
+import os
 import sys
 
 import torch
@@ -18,7 +20,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("shapes", nargs="*", default=["131072:8:2"])
     ap.add_argument("--two-cta", default="both")
-    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--ours", action="store_true")
     args = ap.parse_args()
     from vllm.vllm_flash_attn.cute import interface as fa, utils as fau
 
@@ -54,12 +57,48 @@ def main():
                     torch.cuda.synchronize()
                     fwd.append(e0.elapsed_time(e1))
                     bwd.append(e1.elapsed_time(e2))
-                f, b = min(fwd), min(bwd)
+                f, b = sorted(fwd)[len(fwd) // 2], sorted(bwd)[len(bwd) // 2]
                 print(json.dumps({"impl": "fa4", "two_cta": two, "S": S, "nq": nq, "nkv": nkv, "d": d,
                                   "fwd_ms": f, "fwd_tflops": 4 * fl / f / 1e9, "bwd_ms": b,
                                   "bwd_tflops": 10 * fl / b / 1e9}), flush=True)
             except Exception as ex:  # noqa: BLE001 - a library failure is reported, not fatal
                 print(json.dumps({"impl": "fa4", "two_cta": two, "S": S, "error": repr(ex)[:400]}), flush=True)
+            torch.cuda.empty_cache()
+        if args.ours:
+            sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+            from paper_2602_21196_b200 import upipe
+            # our layout: [S][heads][d] rows (the same memory as FA4's [1][S][heads][d])
+            qq, kk, vv, dd = (t[0].contiguous() for t in (q, k, v, do))
+            o = torch.empty((S, nq, d), dtype=torch.bfloat16, device="cuda")
+            lse = torch.empty((nq, S), dtype=torch.float32, device="cuda")
+            delta = torch.empty((S, nq), dtype=torch.float32, device="cuda")
+            dq = torch.zeros((nq * d, S), dtype=torch.float32, device="cuda")   # dim-major, as the layer uses it
+            dk = torch.empty((S, nkv, d), dtype=torch.float32, device="cuda")
+            dv = torch.empty((S, nkv, d), dtype=torch.float32, device="cuda")
+
+            def fwd_o():
+                upipe.upipe_attn_core_fwd(qq, kk, vv, o, lse, S, nq, nkv, d, 1, nq * d, nkv * d, nq * d, S)
+
+            def bwd_o():
+                upipe.upipe_attn_core_bwd(qq, kk, vv, dd, lse, delta, dq, dk, dv, S, nq, nkv, d, 1, nq * d, nkv * d,
+                                          nq * d, S, nq, dq_dim_major=True)
+
+            fwd_o()
+            upipe.upipe_rowdot(dd, nq * d, o, nq * d, delta, nq, S, nq, d)
+            fwd, bwd = [], []
+            for f_, acc in ((fwd_o, fwd), (bwd_o, bwd)):
+                f_()
+                for _ in range(args.reps):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    f_()
+                    e1.record()
+                    torch.cuda.synchronize()
+                    acc.append(e0.elapsed_time(e1))
+            f, b = sorted(fwd)[len(fwd) // 2], sorted(bwd)[len(bwd) // 2]
+            print(json.dumps({"impl": "ours", "S": S, "nq": nq, "nkv": nkv, "d": d, "fwd_ms": f,
+                              "fwd_tflops": 4 * fl / f / 1e9, "bwd_ms": b, "bwd_tflops": 10 * fl / b / 1e9}), flush=True)
+            del qq, kk, vv, dd, o, lse, delta, dq, dk, dv
             torch.cuda.empty_cache()
 
 
