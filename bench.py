@@ -488,8 +488,9 @@ def main():
         # end to end through the public API: pinned host inputs -> HBM, fwd+bwd, dx -> pinned host
         # Every step copies its own x and dY from pinned host memory and reads its dx back, all inside
         # the timed region. The copies run on two copy streams (H2D, D2H) with double-buffered device
-        # inputs, so step i+1's upload overlaps step i's backward and step i's download overlaps step
-        # i+1's forward (the usual input pipeline of a training loop); nothing is skipped or cached.
+        # inputs, so step i+1's upload overlaps step i's backward, step i's y download overlaps its own backward
+        # and its dx download step i+1's forward (the usual input pipeline of a training loop); nothing is
+        # skipped or cached.
         attn = make_attn(U)
         xh = [x.cpu().pin_memory() for _ in range(2)]
         dyh = [dy.cpu().pin_memory() for _ in range(2)]
@@ -516,15 +517,19 @@ def main():
                 dy_ready.record(h2d)
             main_s.wait_event(x_ready)
             y, saved = attn.forward(xd[b], *W, **NW)
+            fwd_done = ev()
+            fwd_done.record(main_s)
+            with torch.cuda.stream(d2h):                    # y goes down while the backward runs
+                d2h.wait_event(fwd_done)
+                y.record_stream(d2h)
+                yh[b].copy_(y, non_blocking=True)
             main_s.wait_event(dy_ready)
             dx, *_ = attn.backward(xd[b], *W, dyd[b], saved, **NW)
             bwd_done[b].record(main_s)
             with torch.cuda.stream(d2h):
                 d2h.wait_event(bwd_done[b])
                 dx.record_stream(d2h)
-                y.record_stream(d2h)
                 dxh[b].copy_(dx, non_blocking=True)
-                yh[b].copy_(y, non_blocking=True)
 
         e2e_step(0)
         e2e_step(1)
