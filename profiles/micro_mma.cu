@@ -27,7 +27,36 @@ __global__ void __launch_bounds__(384, 1) mma_rate(long long* out, int iters, in
   tc_fence_after();
   const uint32_t tm = slot;
   const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 65536);
-  if (warp == 0 && (mode == 10 || mode == 11)) {
+  if (warp == 0 && mode == 12) {
+    // mode 12: the 64-query backward's per-tile MMA sequence, back to back (no waits): dV += P^T dO (4 x TS N128,
+    // B MN-major), dQ^T = K^T dS (8 x SS N64, both MN-major), dK += dS^T Q (4 x SS N128, B MN-major), S (8 x SS N64),
+    // dP (8 x SS N64); TMEM as in the kernel (S 0 | dP 64 | dV 256 | dK 384); "cycles/MMA" = cycles per tile / 32
+    const uint32_t id_sp = idesc_bf16(128, 64, false, false), id_kmn = idesc_bf16(128, 128, false, true),
+                   id_dq = idesc_bf16(128, 64, true, true);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const uint64_t db_do = desc_sw128(sb, 8192, 1024), da_k = desc_sw128(sa, 16384, 1024), db_ds = desc_sw128(sb, 8192, 1024);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) mma_ts_w(tm + 256, tm + ks * 8, db_do + ks * (2048 >> 4), id_kmn, 1);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mma_ss_w(tm + 64, da_k + i * (2048 >> 4), db_ds + i * (2048 >> 4), id_dq, i != 0);
+      const uint64_t da_ds = desc_sw128(sa, 16, 1024), db_q = desc_sw128(sb, 8192, 1024);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) mma_ss_w(tm + 384, da_ds + ((ks * 32) >> 4), db_q + ks * (2048 >> 4), id_kmn, 1);
+      const uint64_t da = desc_sw128(sa, 16, 1024), db = desc_sw128(sb, 16, 1024);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        mma_ss_w(tm, da + (((i >> 2) * 16384 + (i & 3) * 32) >> 4), db + (((i >> 2) * 8192 + (i & 3) * 32) >> 4), id_sp, i != 0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        mma_ss_w(tm + 64, da + (((i >> 2) * 16384 + (i & 3) * 32) >> 4), db + (((i >> 2) * 8192 + (i & 3) * 32) >> 4), id_sp, i != 0);
+    }
+    if (elect_one()) mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (lane_id() == 0) out[blockIdx.x] = (t1 - t0) / 4;   // report per 8 MMAs: the harness divides by iters * 8
+    if (lane_id() == 0) stop = 1;
+  } else if (warp == 0 && (mode == 10 || mode == 11)) {
     // mode 10: TS N128 warp-issued, unrolled (A from TMEM columns 256+, D at column 0; the dV / dK form);
     // mode 11: TS N128 with B MN-major (exactly the backward's dV: B = dO MN-major)
     const uint32_t id = idesc_bf16(128, 128, false, mode == 11);
@@ -103,7 +132,20 @@ __global__ void __launch_bounds__(384, 1) mma_rate(long long* out, int iters, in
       out[blockIdx.x] = t1 - t0;
       stop = 1;
     }
-  } else if (warp <= sts_warps) {
+  } else if (mode == 12 && warp >= 1 && warp <= 8 && sts_warps > 8) {
+    // mode 12 with sts_warps = 16: warps 1..8 stream tcgen05.ld 32x32b.x32 from TMEM (the softmax / drain loads of
+    // the backward: ~96 KB per tile there) instead of STS
+    volatile int* st = &stop;
+    const uint32_t ta = tm + ((uint32_t)((warp & 3) * 32) << 16) + 448;   // a warp reads its sub-partition's lanes
+    uint32_t acc = 0;
+    while (!*st) {
+      uint32_t r[32];
+      tmem_ld32(ta, r);
+      tmem_wait_ld();
+      acc += r[0] ^ r[31];
+    }
+    if (acc == 0x12345678) stop = 2;
+  } else if (warp <= sts_warps && sts_warps <= 8) {
     const uint32_t base = smem_u32(smem + 131072) + ((warp - 1) & 3) * 8192 + lane_id() * 16;
     volatile int* st = &stop;
     uint32_t v = threadIdx.x;
@@ -124,10 +166,11 @@ int main() {
   cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* names[] = {"SS N128 K-major", "SS N256 K-major", "TS N128", "SS N128 B MN-major",
                          "SS N128 2 accums", "TS N128 2 accums", "SS N64 2 accums", "SS N128 unrolled",
-                         "SS N128 warp-issued", "SS N64 warp-issued", "TS N128 warp-issued", "TS N128 B-MN warp-issued"};
+                         "SS N128 warp-issued", "SS N64 warp-issued", "TS N128 warp-issued", "TS N128 B-MN warp-issued",
+                         "bwd tile sequence (x4 = cycles per 64-query tile; floor 1664)"};
   const int iters = 4096;
-  for (int sts : {0, 8}) {
-    for (int mode = 0; mode < 12; ++mode) {
+  for (int sts : {0, 8, 16}) {
+    for (int mode = 0; mode < 13; ++mode) {
       mma_rate<<<148, 384, smem>>>(d, iters, mode, sts);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
