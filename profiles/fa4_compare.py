@@ -16,6 +16,45 @@ import sys
 import torch
 
 
+class ClockSampler:
+    """nvidia-smi-equivalent SM clock / power samples (NVML) taken every 5 ms while a timed region runs."""
+
+    def __init__(self):
+        import threading
+        import pynvml
+        pynvml.nvmlInit()
+        self.nv = pynvml
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        self.on = False
+        self.samples = []
+        self.threading = threading
+
+    def __enter__(self):
+        self.samples = []
+        self.on = True
+
+        def loop():
+            import time
+            while self.on:
+                self.samples.append((self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM),
+                                     self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0))
+                time.sleep(0.005)
+        self.t = self.threading.Thread(target=loop, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self.on = False
+        self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return None
+        cl = sorted(c for c, _ in self.samples)
+        pw = sorted(p for _, p in self.samples)
+        return {"sm_mhz_median": cl[len(cl) // 2], "power_w_median": round(pw[len(pw) // 2], 1), "n": len(cl)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("shapes", nargs="*", default=["131072:8:2"])
@@ -45,6 +84,8 @@ def main():
                 out.backward(do)                      # compile both directions
                 torch.cuda.synchronize()
                 fwd, bwd = [], []
+                cs = ClockSampler()
+                cs.__enter__()
                 for _ in range(args.reps):
                     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                     qq.grad = kk.grad = vv.grad = None
@@ -57,10 +98,17 @@ def main():
                     torch.cuda.synchronize()
                     fwd.append(e0.elapsed_time(e1))
                     bwd.append(e1.elapsed_time(e2))
+                cs.__exit__()
+                cf = ClockSampler()                       # forward alone (no autograd), for its clock
+                with torch.no_grad(), cf:
+                    for _ in range(args.reps):
+                        fa.flash_attn_func(q, k, v, causal=True)
+                    torch.cuda.synchronize()
                 f, b = sorted(fwd)[len(fwd) // 2], sorted(bwd)[len(bwd) // 2]
                 print(json.dumps({"impl": "fa4", "two_cta": two, "S": S, "nq": nq, "nkv": nkv, "d": d,
                                   "fwd_ms": f, "fwd_tflops": 4 * fl / f / 1e9, "bwd_ms": b,
-                                  "bwd_tflops": 10 * fl / b / 1e9}), flush=True)
+                                  "bwd_tflops": 10 * fl / b / 1e9,
+                                  "clocks": {"fwd": cf.summary(), "fwd_bwd": cs.summary()}}), flush=True)
             except Exception as ex:  # noqa: BLE001 - a library failure is reported, not fatal
                 print(json.dumps({"impl": "fa4", "two_cta": two, "S": S, "error": repr(ex)[:400]}), flush=True)
             torch.cuda.empty_cache()
@@ -86,8 +134,11 @@ def main():
             fwd_o()
             upipe.upipe_rowdot(dd, nq * d, o, nq * d, delta, nq, S, nq, d)
             fwd, bwd = [], []
-            for f_, acc in ((fwd_o, fwd), (bwd_o, bwd)):
+            clk = {}
+            for f_, acc, nm in ((fwd_o, fwd, "fwd"), (bwd_o, bwd, "bwd")):
                 f_()
+                cs = ClockSampler()
+                cs.__enter__()
                 for _ in range(args.reps):
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record()
@@ -95,9 +146,12 @@ def main():
                     e1.record()
                     torch.cuda.synchronize()
                     acc.append(e0.elapsed_time(e1))
+                cs.__exit__()
+                clk[nm] = cs.summary()
             f, b = sorted(fwd)[len(fwd) // 2], sorted(bwd)[len(bwd) // 2]
             print(json.dumps({"impl": "ours", "S": S, "nq": nq, "nkv": nkv, "d": d, "fwd_ms": f,
-                              "fwd_tflops": 4 * fl / f / 1e9, "bwd_ms": b, "bwd_tflops": 10 * fl / b / 1e9}), flush=True)
+                              "fwd_tflops": 4 * fl / f / 1e9, "bwd_ms": b, "bwd_tflops": 10 * fl / b / 1e9,
+                              "clocks": clk}), flush=True)
             del qq, kk, vv, dd, o, lse, delta, dq, dk, dv
             torch.cuda.empty_cache()
 
