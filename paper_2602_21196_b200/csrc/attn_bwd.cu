@@ -564,6 +564,14 @@ struct Q64Cfg {
 // PAIR (UPIPE_BWD_PAIR): clusters of two CTAs on adjacent key tiles (2i, 2i+1) of one KV head visit the same
 // query tiles in the same order (the even tile's range; the odd CTA's extra tiles are fully masked for it), so
 // each CTA loads one half of every Q / dO tile and multicasts it to both: half the L2 -> SM operand traffic.
+// UPIPE_BWD_CLUSTER (build time, 2 or 4): CTAs per cluster of the PAIR launch. With 4, each CTA loads one quarter of
+// every Q / dO tile (one 64-dimension chunk, 32 query rows) and multicasts it to all four.
+#ifndef UPIPE_BWD_CLUSTER
+#define UPIPE_BWD_CLUSTER 2
+#endif
+constexpr int kBwdCluster = UPIPE_BWD_CLUSTER;
+static_assert(kBwdCluster == 2 || kBwdCluster == 4, "UPIPE_BWD_CLUSTER: 2 or 4");
+
 template <bool TL, bool DET = false, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_q64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -592,8 +600,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int g = blockIdx.y;
   const int G = a.nq / a.nkv;
   const int nT64 = (int)((a.S + 63) / 64);
+  constexpr int CLN = PAIR ? kBwdCluster : 1;
+  constexpr uint16_t kMask = (uint16_t)((1u << CLN) - 1);
   const uint32_t crank = PAIR ? cluster_ctarank() : 0;
-  const int qt_begin = a.causal ? 2 * (PAIR ? (jb & ~1) : jb) : 0;   // PAIR: the pair's common (even) range
+  const int qt_begin = a.causal ? 2 * (jb & ~(CLN - 1)) : 0;   // PAIR: the cluster's common range (its first tile's)
   const int n_qt = nT64 - qt_begin;
   const int N = G * n_qt;
   // Query tiles are visited from the last one down to the diagonal: CTAs that run at the same time then
@@ -608,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
     for (int i = 0; i < 22; ++i) {
       const bool slot_empty = (i >= 4 && i < 7) || (i >= 10 && i < 13);   // q_empty, do_empty: both CTAs release
-      mbar_init(&bars[i], (i == 15 || i == 16 || i == 19 || i == 20) ? kWg : (PAIR && slot_empty ? 2 : 1));
+      mbar_init(&bars[i], (i == 15 || i == 16 || i == 19 || i == 20) ? kWg : (slot_empty ? CLN : 1));
     }
     fence_barrier_init();
     tmem_slot[1] = smem_u32(smem);
@@ -636,7 +646,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ph = ((n / C::NQ) & 1) ^ 1;
         mbar_wait(&q_empty[st], ph);              // PAIR: this slot is free in both CTAs
         mbar_arrive_expect_tx(&q_full[st], C::QT);
-        if (PAIR) {                               // this CTA's half (one 64-dim chunk) to both CTAs
+        if (PAIR && CLN == 4) {                   // this CTA's quarter (chunk crank & 1, rows 32 (crank >> 1)) to all
+          tma_load_3d_mc(smem + C::OFF_Q + st * C::QT + (crank & 1) * 8192 + (crank >> 1) * 4096, &tmQ, &q_full[st],
+                         (crank & 1) * 64, h, qt * 64 + (crank >> 1) * 32, kMask);
+        } else if (PAIR) {                        // this CTA's half (one 64-dim chunk) to both CTAs
           tma_load_3d_mc(smem + C::OFF_Q + st * C::QT + crank * 8192, &tmQ, &q_full[st], crank * 64, h, qt * 64, 0x3);
         } else {
 #pragma unroll
@@ -644,7 +657,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(&do_empty[st], ph);
         mbar_arrive_expect_tx(&do_full[st], C::QT);
-        if (PAIR) {
+        if (PAIR && CLN == 4) {
+          tma_load_3d_mc(smem + C::OFF_DO + st * C::QT + (crank & 1) * 8192 + (crank >> 1) * 4096, &tmdO, &do_full[st],
+                         (crank & 1) * 64, h, qt * 64 + (crank >> 1) * 32, kMask);
+        } else if (PAIR) {
           tma_load_3d_mc(smem + C::OFF_DO + st * C::QT + crank * 8192, &tmdO, &do_full[st], crank * 64, h, qt * 64,
                          0x3);
         } else {
@@ -715,12 +731,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       load_base();
       const uint32_t sds = base + C::OFF_DS + x * 16384;
       mma_dv(tmem + slot_s(x), base + C::OFF_DO + st * C::QT, n > 0);
-      if (PAIR) mma_commit_mc_w(&do_empty[st], 0x3);   // released in both CTAs (each loads into both)
+      if (PAIR) mma_commit_mc_w(&do_empty[st], kMask);   // released in every CTA of the cluster (each loads into all)
       else mma_commit_w(&do_empty[st]);
       mma_dq(base + C::OFF_K, sds, tmem + slot_dp(x));
       mma_commit_w(&dq_full[x]);
       mma_dk(sds, tmem + slot_s(x), base + C::OFF_Q + st * C::QT, n > 0);
-      if (PAIR) mma_commit_mc_w(&q_empty[st], 0x3);
+      if (PAIR) mma_commit_mc_w(&q_empty[st], kMask);
       else mma_commit_w(&q_empty[st]);
       if (n + 2 < N) {
         const int st2 = (n + 2) % C::NQ;
@@ -1118,17 +1134,23 @@ cudaError_t attn_bwd_run(const AttnBwdProblem& p, cudaStream_t stream, char* err
       // masked and written nowhere)
       cudaLaunchConfig_t cfg = {};
       cudaLaunchAttribute at[1];
-      cfg.gridDim = dim3((unsigned)((nT + 1) & ~1), (unsigned)p.nkv);
+      cfg.gridDim = dim3((unsigned)((nT + kBwdCluster - 1) / kBwdCluster * kBwdCluster), (unsigned)p.nkv);
       cfg.blockDim = dim3(kThreads);
       cfg.dynamicSmemBytes = Q64Cfg::SMEM;
       cfg.stream = stream;
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.x = kBwdCluster;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, attn_bwd_q64_kernel<false, false, true>, tq64, tk, tv, tdo64, tdq64, a);
+      CUtensorMap tq32, tdo32;                 // quads: one quarter (32 query rows of one 64-dim chunk) per CTA
+      if (kBwdCluster == 4 &&
+          (!make_tmap_3d(&tq32, p.q, p.d, p.nq, p.S, p.d, p.ldq, 64, 1, 32, err, errlen) ||
+           !make_tmap_3d(&tdo32, p.dout, p.d, p.nq, p.S, p.d, p.ldo_grad, 64, 1, 32, err, errlen)))
+        return cudaErrorInvalidValue;
+      cudaLaunchKernelEx(&cfg, attn_bwd_q64_kernel<false, false, true>, kBwdCluster == 4 ? tq32 : tq64, tk, tv,
+                         kBwdCluster == 4 ? tdo32 : tdo64, tdq64, a);
     } else attn_bwd_q64_kernel<false><<<grid, kThreads, Q64Cfg::SMEM, stream>>>(tq64, tk, tv, tdo64, tdq64, a);
     count_launches(1);
     e = cudaGetLastError();
