@@ -35,6 +35,8 @@ struct FwdArgs {
   float* lse;
   long long S, ldo, ldo32, ld_lse;
   int nq, nkv, causal, n_pairs;
+  int pair_heads;    // PAIR launch with clusters of two query heads of one KV group (same query tiles) instead of
+                     // two adjacent query-tile pairs of one head
   float scale_log2;  // log2(e) / sqrt(d)
   long long* dbg;    // UPIPE_FWD_TIMELINE=1: per-role cycle totals of CTA (0, 0)
   __nv_bfloat16* oseg[kMaxSeg];   // N2 (noseg > 0): row q of O -> oseg[q / oseg_rows] + (q % oseg_rows) * ldo
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(384, 1)
   const int qt0 = 2 * pair;                       // query tile index of A (B = qt0 + 1)
   const int ntiles_kv = (int)((a.S + 127) / 128);
   const uint32_t crank = PAIR ? cluster_ctarank() : 0;
-  const int qt_long = PAIR ? 2 * (a.n_pairs - 1 - (int)(blockIdx.x & ~1u)) : qt0;   // the cluster's longer pair
+  const int qt_long = PAIR && !a.pair_heads ? 2 * (a.n_pairs - 1 - (int)(blockIdx.x & ~1u)) : qt0;   // the cluster's longer pair
   const int nA = a.causal ? min(qt0 + 1, ntiles_kv) : ntiles_kv;
   const int nB = a.causal ? min(qt_long + 2, ntiles_kv) : ntiles_kv;   // PAIR: the KV stream both CTAs share
 
@@ -475,13 +477,13 @@ cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err
     if (at != cudaSuccess) { snprintf(err, errlen, "attn_fwd attr: %s", cudaGetErrorString(at)); return at; }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute la[1];
-    cfg.gridDim = dim3((unsigned)((a.n_pairs + 1) & ~1), (unsigned)p.nq);
+    cfg.gridDim = a.pair_heads ? dim3((unsigned)a.n_pairs, (unsigned)p.nq) : dim3((unsigned)((a.n_pairs + 1) & ~1), (unsigned)p.nq);
     cfg.blockDim = dim3(384);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     la[0].id = cudaLaunchAttributeClusterDimension;
-    la[0].val.clusterDim.x = 2;
-    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.x = a.pair_heads ? 1 : 2;
+    la[0].val.clusterDim.y = a.pair_heads ? 2 : 1;
     la[0].val.clusterDim.z = 1;
     cfg.attrs = la;
     cfg.numAttrs = 1;
@@ -494,9 +496,12 @@ cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err
   // TFLOP/s, attn fwd 117.1 -> 116.4 ms per bench step; nq/nkv 1/1 1328 -> 1113 TFLOP/s, so not there)
   static const int pair_env = [] {
     const char* v = getenv("UPIPE_FWD_PAIR");
-    return v ? (v[0] == '1' ? 1 : 0) : -1;
+    return v ? (v[0] == '1' ? 1 : v[0] == '2' ? 2 : 0) : -1;
   }();
-  const bool use_pair = pair_env < 0 ? p.nq >= 4 : pair_env == 1;
+  const int G = p.nq / p.nkv;
+  // UPIPE_FWD_PAIR=2: clusters of two query heads of one KV group (needs an even group size)
+  a.pair_heads = pair_env == 2 && G % 2 == 0 ? 1 : 0;
+  const bool use_pair = pair_env < 0 ? p.nq >= 4 : (pair_env == 1 || a.pair_heads);
   if (p.d == 128 && !a.dbg && use_pair) e = go_pair(attn_fwd_kernel<128, false, true>, FwdCfg<128>::SMEM);
   else if (p.d == 128) e = a.dbg ? go(attn_fwd_kernel<128, true>, FwdCfg<128>::SMEM) : go(attn_fwd_kernel<128, false>, FwdCfg<128>::SMEM);
   else e = go(attn_fwd_kernel<64, false>, FwdCfg<64>::SMEM);
