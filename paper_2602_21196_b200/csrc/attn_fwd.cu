@@ -491,8 +491,8 @@ cudaError_t attn_fwd_run(const AttnFwdProblem& p, cudaStream_t stream, char* err
     count_launches(1);
     return le;
   };
-  // UPIPE_FWD_PAIR=1 / 0 forces the CTA-pair launch on / off. Default: pairs when the KV stream is shared by
-  // >= 4 query heads of the launch (A/B at 128K on one box, profiles/r02_ab_fwd_pair.txt: nq/nkv 8/2 1235 -> 1248
+  // UPIPE_FWD_PAIR=1 / 0 forces the CTA-pair launch on / off. Default: pairs when the launch has >= 4 query heads
+  // (grids of >= 4 x 512 CTAs at 128K) (A/B at 128K on one box, profiles/r02_ab_fwd_pair.txt: nq/nkv 8/2 1235 -> 1248
   // TFLOP/s, attn fwd 117.1 -> 116.4 ms per bench step; nq/nkv 1/1 1328 -> 1113 TFLOP/s, so not there)
   static const int pair_env = [] {
     const char* v = getenv("UPIPE_FWD_PAIR");
