@@ -55,7 +55,10 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 #ifndef UPIPE_FWD_POLY_EVERY
-#define UPIPE_FWD_POLY_EVERY 4   // exp pairs j with j % N == N - 1 use the FMA-pipe polynomial (0: none)
+// exp pairs j with j % N == N - 1 use the FMA-pipe polynomial (0: none). Under the power cap at 128K
+// (profiles/r02_ab_fwd_poly*.txt): N = 8 114.5 ms of attn fwd per bench step, 4: 117.0, all MUFU 120.8, 3: 121.5,
+// 2: 134.5 (round 1 chose 4 from short 32K runs)
+#define UPIPE_FWD_POLY_EVERY 8
 #endif
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
